@@ -1,0 +1,200 @@
+/*
+ * tgs.h — C ABI of the B200 rasterizer library (libtgs.so).
+ *
+ * This is the drop-in boundary for the reference's rasterizer hot path
+ * (slimsplat, /root/reference/pkg/src/slimsplat).  The reference's own
+ * "kernel ABI" is three numba functions that take caller-allocated positional
+ * arrays and write them in place (_kernels.py:12-36, 92-115, 184-202), with the
+ * Python layer owning the contract (_kernels.py:4-5).  This header generalises
+ * that ABI to the whole path the reference runs per training step:
+ *
+ *   tgs_preprocess_forward   replaces rasterizer._prepare minus binning
+ *                            (rasterizer.py:167-197: masking.py:21-43,84-86,
+ *                            geometry.py:19-41,74-77,138-195, sh.py:135-161)
+ *   tgs_count_tiles          the per-Gaussian rect/count half of bin_tiles
+ *                            (rasterizer.py:112-128)
+ *   tgs_bin_gaussians +      the sort half of bin_tiles
+ *   tgs_bin_instances        (rasterizer.py:130-148: repeat, lexsort, CSR)
+ *   tgs_blend_forward        _kernels.forward_kernel (_kernels.py:12-89)
+ *   tgs_blend_backward       _kernels.backward_kernel (_kernels.py:92-181)
+ *   tgs_preprocess_backward  render_backward after the kernel
+ *                            (rasterizer.py:375-419, sh.py:164-215,
+ *                            geometry.py:44-71,80-89,198-251, masking.py:28-31)
+ *   tgs_loss_l1_ssim         training.total_loss image terms (training.py:61-89,
+ *                            metrics.py:138-188)
+ *   tgs_adam_step            optim.Adam.update (optim.py:37-49)
+ *   tgs_compact_rows         cloud.take / Adam.compact row compaction
+ *                            (cloud.py:86-89, optim.py:51-55)
+ *
+ * Conventions (all entry points):
+ *   - every pointer is DEVICE memory owned by the caller, row-major, float32
+ *     unless stated; the library never allocates persistent memory and never
+ *     frees caller memory; scratch comes from caller-provided workspaces;
+ *   - every call is asynchronous on the given stream (cudaStream_t; NULL = the
+ *     legacy default stream) and returns a TGS_* status code; no exception or
+ *     C++ type crosses the ABI;
+ *   - no global mutable state: calls are re-entrant per stream.
+ */
+#ifndef TGS_H_
+#define TGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *tgs_stream_t; /* == cudaStream_t */
+
+enum {
+  TGS_OK = 0,
+  TGS_ERR_INVALID = 1,             /* -> ContractViolationError */
+  TGS_ERR_DEGENERATE_ROTATION = 2, /* -> DegenerateRotationError (geometry.py:23-24) */
+  TGS_ERR_CUDA = 3,                /* a CUDA launch/API call failed */
+  TGS_ERR_UNSUPPORTED = 4,         /* e.g. tile_size > 32 */
+  TGS_ERR_CAPACITY = 5             /* caller buffer smaller than required */
+};
+
+/* Per-Gaussian projected record written by tgs_preprocess_forward, 12 floats:
+ *   [0..1] means2d (pixels)      [2..4] conic (a, b, c) = inverse cov2d packed
+ *   [5]    alpha (sigmoid(o)*M)  [6..8] rgb (SH colour, clamped >= 0)
+ *   [9]    depth (camera z)      [10]   radius (3 sigma, pixels)
+ *   [11]   screen area 9*pi*sqrt(det), 0 when not visible
+ * 48 B = one 16 B-aligned record, so the blend kernels stage a Gaussian with
+ * three 16 B loads.  Rows of non-visible Gaussians are zero. */
+#define TGS_SPLAT_FLOATS 12
+/* Per-Gaussian screen-space partials written by tgs_blend_backward, 9 floats:
+ *   [0..1] dL/dmeans2d  [2..4] dL/dcov2d packed (g00, g01 both slots, g11)
+ *   [5] dL/dalpha       [6..8] dL/drgb          (_kernels.py:111-115) */
+#define TGS_DSPLAT_FLOATS 9
+
+typedef struct {
+  float fx, fy, cx, cy;
+  float R[9];      /* world -> camera, row-major (cameras.py:25) */
+  float t[3];      /* x_cam = R x + t */
+  float center[3]; /* -R^T t, computed by the caller (cameras.py:42-45) */
+  int32_t width, height;
+} tgs_camera;
+
+typedef struct {
+  float lowpass_s;         /* added to both cov2d diagonals (geometry.py:170-172) */
+  float near_plane;        /* cull t_z <= near (geometry.py:154) */
+  /* Hard masks are evaluated in logit space: sigmoid(m) > eps  <=>  m > logit(eps).
+   * The caller passes logit(eps) in float64 rounded DOWN to float32, which makes
+   * the float32 comparison identical to the reference's float64 one
+   * (masking.py:21-25).  Same for the alpha-skip gate sigmoid(o) >= 1/255
+   * (rasterizer.py:178) with logit(1/255) rounded UP. */
+  float mask_logit_min;    /* keep Gaussian iff mask_logit > mask_logit_min */
+  float sh_mask_logit_min; /* keep SH band iff sh_mask_logit > sh_mask_logit_min */
+  float opacity_logit_min; /* alpha-skip survivor iff opacity_logit >= opacity_logit_min */
+  float background[3];
+  int32_t active_sh_degree; /* 0..3 */
+  int32_t tile_size;        /* 1..32 */
+  int32_t compute_sh_rest_grads;
+  int32_t reserved;
+} tgs_settings;
+
+typedef struct {
+  const float *positions;      /* (n, 3) */
+  const float *log_scales;     /* (n, 3) */
+  const float *rotations;      /* (n, 4) w, x, y, z */
+  const float *opacity_logits; /* (n,) */
+  const float *sh_dc;          /* (n, 3) */
+  const float *sh_rest;        /* (n, 15, 3) band-major */
+  const float *mask_logits;    /* (n,) */
+  const float *sh_mask_logits; /* (n, 3) */
+  int64_t n;
+} tgs_cloud;
+
+typedef struct { /* CloudGrads (cloud.py:110-126) */
+  float *positions, *log_scales, *rotations, *opacity_logits;
+  float *sh_dc, *sh_rest, *mask_logits, *sh_mask_logits;
+  float *mean2d_screen; /* (n, 2); may be NULL */
+} tgs_grads;
+
+int tgs_version(void);
+const char *tgs_last_error_string(int status);
+
+/* ---- (1) preprocess -----------------------------------------------------
+ * splats (n, 12), visible (n,) 0/1, tiles_touched (n,) = number of tiles the
+ * Gaussian's 3-sigma box covers (0 when not visible / off screen).
+ * error_flag: device int32, OR-ed with 1 when a quaternion has norm < 1e-12;
+ * the caller reads it back and raises DegenerateRotationError. */
+int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
+                           float *splats, uint8_t *visible, int32_t *tiles_touched,
+                           int32_t *error_flag, tgs_stream_t stream);
+
+/* tiles_touched for arbitrary projected records (the bin_tiles(...) entry,
+ * rasterizer.py:95-128): only splat fields means2d and radius are read. */
+int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
+                    int32_t *tiles_touched, tgs_stream_t stream);
+
+/* ---- (2) binning ----------------------------------------------------------
+ * Sort order is the reference's np.lexsort((gid, depth, tile)) (rasterizer.py:143):
+ * ascending tile, then depth, then Gaussian index — realised as a stable LSD radix
+ * sort of the 64-bit key (tile << 32 | orderable(depth)) whose 32 depth-digit
+ * passes run over Gaussians (n items) before duplication and whose tile-digit
+ * passes run over instances.  Tiles are restricted to tile rows
+ * [row_begin, row_end) (tile-row sharding); tile_offsets has
+ * (row_end-row_begin)*tiles_x + 1 entries, relative to the band.
+ *
+ * Step A: tgs_bin_gaussians() needs a workspace of tgs_bin_gaussians_workspace()
+ * bytes, which must stay alive until step B returns.  It writes the instance count
+ * to *d_num_instances (device int64).
+ * Step B: tgs_bin_instances() with num_instances read back by the caller. */
+int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes);
+int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
+                      int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
+                      void *workspace, int64_t *d_num_instances, tgs_stream_t stream);
+int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes);
+int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
+                      int32_t row_begin, int32_t row_end, void *gauss_workspace, int64_t num_instances,
+                      void *workspace, int32_t *tile_offsets, int32_t *sorted_ids, tgs_stream_t stream);
+
+/* ---- (3) forward blend ------------------------------------------------------
+ * image (H, W, 3), transmit / weight_sum (H, W) float32, n_contrib / last_pos
+ * (H, W) int32 (_kernels.py:83-89); hits (n,) int32 or NULL (record_hits).
+ * Only pixels of tile rows [row_begin, row_end) are written. */
+int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                      const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
+                      float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
+                      int32_t *last_pos, int32_t *hits, tgs_stream_t stream);
+
+/* ---- (4) backward blend -----------------------------------------------------
+ * dsplats (n, 9) is ACCUMULATED into (caller zeroes it). dimage (H, W, 3). */
+int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                       const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
+                       const float *transmit, const int32_t *last_pos, const float *dimage,
+                       float *dsplats, tgs_stream_t stream);
+
+/* ---- (5) preprocess backward ------------------------------------------------
+ * accumulate != 0 adds into grads (multi-view batches), else overwrites. */
+int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
+                            const uint8_t *visible, const float *dsplats, tgs_grads *grads,
+                            int32_t accumulate, tgs_stream_t stream);
+
+/* ---- (6) loss: (1-lambda)*L1 + lambda*(1-SSIM)/2, 11x11 sigma 1.5 window,
+ * symmetric padding (training.py:76-89, metrics.py:138-188).  image/target
+ * (H, W, 3); dimage (H, W, 3) written; terms (device float64[2]) receives
+ * {mean |image-target|, mean SSIM}.  Workspace: tgs_loss_workspace() bytes. */
+int tgs_loss_workspace(int32_t width, int32_t height, size_t *bytes);
+int tgs_loss_l1_ssim(const float *image, const float *target, int32_t width, int32_t height,
+                     float lambda_ssim, float *dimage, double *terms, void *workspace,
+                     tgs_stream_t stream);
+
+/* ---- (7) Adam (optim.py:37-49) over one parameter group of n floats.
+ * bias corrections are passed in (1 - beta^step) so the step counter stays host-side. */
+int tgs_adam_step(float *param, const float *grad, float *m, float *v, int64_t n, float lr,
+                  float beta1, float beta2, float eps, float bias_c1, float bias_c2,
+                  tgs_stream_t stream);
+
+/* ---- (8) row compaction (cloud.take / Adam.compact): out[k] = in[keep[k]] for
+ * rows of `row_floats` floats. */
+int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,
+                    int32_t row_floats, tgs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGS_H_ */
