@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the Trick-GS rasterizer training step on B200 (BASELINE.json config 3).
+
+Workload (`c3`): 1,000,000 Gaussians, SH degree 3, 8 cameras at 1920x1080 on a
+radius U(4,6) sphere, Gaussian-mask threshold 0.01, SH-band masks 0.1.  One
+step = for each view: render_forward -> (0.8 L1 + 0.2 D-SSIM) loss ->
+render_backward, gradients summed over the 8 views, NCCL all-reduce (N > 1),
+Adam over all 8 parameter groups.  Views are sharded over ranks (weak scaling
+of per-GPU render work is NOT used: the 8-view batch is fixed, so "scaling":
+"strong").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (see the repo's bench contract).  The reference
+arm (`--impl reference`) times the CPU oracle port (oracle/, float64 C++
+restatement of the reference's algorithm; the Python reference cannot travel to
+the GPU box) on the host's cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train step/s & render FPS at 1M Gaussians 1080p, 1/2/4/8 B200; HBM % of peak"
+VIEWS = 8
+LAMBDA_SSIM = 0.2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=1_000_000, help="Gaussians (default: config 3)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0, help="reference arm threads (0 = all cores)")
+    a = p.parse_args()
+    a.warmup = max(a.warmup, 3)
+    return a
+
+
+def settings_kwargs():
+    return dict(near=0.2, tile_size=16, lowpass_s=0.3, active_sh_degree=3, mask_threshold=0.01,
+                sh_mask_threshold=0.1, compute_sh_rest_grads=True, background=(0.0, 0.0, 0.0))
+
+
+def config_dict(n, world):
+    return {"workload": "c3: BASELINE.json configs[2] training step", "gaussians": n, "sh_degree": 3,
+            "views_per_step": VIEWS, "resolution": "1920x1080", "tile": 16, "loss": "0.8*L1 + 0.2*D-SSIM (11x11)",
+            "mask_threshold": 0.01, "sh_mask_threshold": 0.1, "optimizer": "Adam, 8 groups",
+            "parallelism": f"dp{world} (views sharded, NCCL all-reduce of the flat gradient buffer)",
+            "l2": "inputs larger than L2: params+grads+Adam moments = 1.0 GB touched per step"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 7:
+                    rows.append(f)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        busy = [v for v in sm if v > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ roofline
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def stage_bytes(n, vis_n, inst, pixels, views):
+    """Algorithmic bytes per stage instance (one libtgs entry point).
+
+    n Gaussians, inst instances and pixels are per view."""
+    return {
+        # read 252 B of parameters, write 48 B record + 1 visible + 4 tiles + 8 depth key
+        "preprocess_fwd": n * (252 + 48 + 1 + 4 + 8),
+        # select (16 B record fields + 4 tiles + 8 written) + compaction (24 B) + 8 stable passes moving
+        # (u64 key, u32 id) in and out (24 B) + counts gather/scan (16 B), per on-screen Gaussian
+        "bin_gaussians": n * 28 + vis_n * (24 + 8 * 24 + 16),
+        # duplicate writes (key, id) 8 B + 2 tile-digit passes x 16 B + ranges read 4 B, per instance
+        "bin_instances": inst * (8 + 2 * 16 + 4),
+        # per instance: 4 B id + 48 B record staged; per pixel 28 B out (rgb, T, w, n, last)
+        "blend_fwd": inst * 52 + pixels * 28,
+        # per instance 52 B; per pixel 20 B in (dimage, T, last); 36 B partials RMW per Gaussian
+        "blend_bwd": inst * 52 + pixels * 20 + vis_n * 72,
+        # read params 252 + partials 36 + visible 1, write grads 260 (RMW when accumulating: +260)
+        "preprocess_bwd": n * (252 + 36 + 1 + 2 * 260),
+        # read image + target 24 B, write dimage 12 B per pixel
+        "loss": pixels * 36,
+        # 63 floats x (read p, g, m, v; write p, m, v) once per step (one stage = 8 group launches)
+        "adam": n * 63 * 28,
+    }
+
+
+def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: str) -> tuple[dict, dict]:
+    stages = {}
+    for k, ms in prof_ms.items():
+        c = counts.get(k, 0)
+        if not c or k not in sbytes:
+            stages[k] = {"ms_total": round(ms, 4), "launches": c}
+            continue
+        per = ms / c
+        gbs = sbytes[k] / (per * 1e-3) / 1e9
+        stages[k] = {"ms_per_launch": round(per, 4), "launches": c, "ms_total": round(ms, 4),
+                     "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    dom = max((k for k in stages if "achieved_gbs" in stages[k]), key=lambda k: stages[k]["ms_total"])
+    d = stages[dom]
+    return {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": d["frac"], "traffic": None, "peak_source": peak_kind}, stages
+
+
+# ------------------------------------------------------- CPU reference
+def cpu_view_step(fields, cam, target, st, threads_note=""):
+    """One view: oracle fp64 render fwd -> loss -> render bwd (the reference algorithm)."""
+    from oracle import loss_ref, oracle
+    f = oracle.render_forward(fields, cam, st, "f64")
+    _, _, dimg = loss_ref.total_loss_image(f["image"], target, LAMBDA_SSIM)
+    g = oracle.render_backward(fields, cam, st, dimg, f, "f64")
+    return g
+
+
+def cpu_adam_seconds(n_floats):
+    rng = np.random.default_rng(0)
+    p, g = rng.standard_normal(n_floats), rng.standard_normal(n_floats)
+    m, v = np.zeros(n_floats), np.zeros(n_floats)
+    t = time.perf_counter()
+    m = 0.9 * m + 0.1 * g  # optim.py:45-49
+    v = 0.999 * v + 0.001 * g * g
+    p -= 1e-3 * (m / 0.1) / (np.sqrt(v / 0.001) + 1e-15)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(sc, st, views_to_time=1):
+    """Bounded sample: `views_to_time` view-steps on 1 core, scaled to the 8-view step."""
+    t0 = time.perf_counter()
+    for v in range(views_to_time):
+        cpu_view_step(sc.fields, sc.cameras[v], sc.targets[v], st)
+    t_view = (time.perf_counter() - t0) / views_to_time
+    t_adam = cpu_adam_seconds(sc.n * 63)
+    t_step = VIEWS * t_view + t_adam
+    return {"value": round(1.0 / t_step, 6), "unit": "train step/s", "cores": 1, "kind": "port",
+            "sample": f"{views_to_time} of 8 views (fwd+loss+bwd, float64 oracle/oracle.cpp) timed "
+                      f"({t_view:.1f} s/view) + numpy Adam over {sc.n * 63} floats ({t_adam:.1f} s); "
+                      f"step = 8 x view + Adam = {t_step:.1f} s"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+    from types import SimpleNamespace
+
+    from paper_2501_14534_b200 import scenes
+    sc = scenes.config3(n=args.n)
+    st = SimpleNamespace(record_hits=False, **settings_kwargs())
+    threads = args.cpu_threads or os.cpu_count() or 1
+    workers = max(1, min(threads, VIEWS))
+    steps = max(1, min(args.steps, 2))  # bounded: each step is ~10-30 s of CPU work per view
+
+    def step():
+        with ThreadPoolExecutor(workers) as ex:  # ctypes releases the GIL: views run in parallel
+            list(ex.map(lambda v: cpu_view_step(sc.fields, sc.cameras[v], sc.targets[v], st), range(VIEWS)))
+        cpu_adam_seconds(sc.n * 63)
+
+    step()  # warm-up (page-in, oracle build)
+    t = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t) / steps
+    v = 1.0 / dt
+    line = {"metric": METRIC, "value": round(v, 6), "unit": "train step/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": round(dt * 1e3, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE.json config 3 generator)", "config": config_dict(args.n, 1),
+            "cpu_baseline": {"value": round(v, 6), "unit": "train step/s", "cores": workers, "kind": "port",
+                             "sample": f"full 8-view step: views in {workers} threads of the float64 oracle "
+                                       f"(oracle/oracle.cpp + oracle/loss_ref.py), numpy Adam; "
+                                       f"{steps} timed step(s) after 1 warm-up"},
+            "e2e": {"value": round(v, 6), "unit": "train step/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_14534_b200 import GaussianCloud, RenderSettings, _lib, profiler, scenes
+    from paper_2501_14534_b200.train import Trainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    _lib.load()
+
+    sc = scenes.config3(n=args.n)
+    views = list(range(rank, VIEWS, world))
+    st = RenderSettings(**settings_kwargs())
+    cloud = GaussianCloud.from_fields(sc.fields, device=dev)
+    h, w = sc.cameras[0].height, sc.cameras[0].width
+    host_targets = {v: torch.from_numpy(sc.targets[v]).pin_memory() for v in views}
+    targets = [None] * VIEWS
+    for v in views:
+        targets[v] = host_targets[v].to(dev)
+    trainer = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, process_group=pg, views=views)
+
+    def barrier():
+        if pg is not None:
+            dist.barrier()
+
+    def timed(k, body):
+        torch.cuda.synchronize()
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(k):
+            body()
+        e.record()
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([s.elapsed_time(e) / 1e3], device=dev)
+        if pg is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    for _ in range(args.warmup):
+        trainer.step()
+    # ---- device-resident timed region (inputs already in HBM)
+    with ClockSampler(local) as clk, profiler.StageTimer() as prof:
+        t_dev = timed(args.steps, trainer.step)
+    clocks = clk.summary()
+    value = args.steps / t_dev
+    # ---- end-to-end through the public API: targets H2D from pinned host memory, loss D2H
+    terms_host = torch.empty((VIEWS, 2), dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        for v in views:
+            trainer.targets[v].copy_(host_targets[v], non_blocking=True)
+        trainer.step()
+        terms_host.copy_(trainer.terms, non_blocking=True)
+
+    e2e_step()
+    t_e2e = timed(args.steps, e2e_step)
+    h2d = sum(host_targets[v].numel() * 4 for v in views)
+    d2h = terms_host.numel() * 8
+
+    # ---- workload statistics for the roofline (one extra untimed forward per view)
+    from paper_2501_14534_b200.rasterizer import render_forward
+    inst = []
+    vis_n = 0
+    for v in views:
+        out = render_forward(cloud, sc.cameras[v], st)
+        inst.append(int(out._tiles.indices.numel()))
+        vis_n = int((out._state.tiles_touched[: len(cloud)] > 0).sum())
+    inst_mean = sum(inst) / len(inst)
+    pk, pk_kind = peaks()
+    sb = stage_bytes(len(cloud), vis_n, inst_mean, h * w, VIEWS)
+    rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
+    launches = trainer_launches(prof.counts(), args.steps)
+
+    # ---- render FPS (forward only, same scene) as a secondary number
+    fps_t = timed(args.steps, lambda: [render_forward(cloud, sc.cameras[v], st) for v in views])
+    render_fps = args.steps * len(views) * world / fps_t
+
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "train step/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_dev / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE.json config 3 generator; random-init Gaussians, U[0,1] targets)",
+            "config": config_dict(len(cloud), world),
+            "e2e": {"value": round(args.steps / t_e2e, 4), "unit": "train step/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
+            "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean)}
+    if world == 1 and not args.no_cpu_baseline:
+        from types import SimpleNamespace
+        line["cpu_baseline"] = cpu_baseline(sc, SimpleNamespace(record_hits=False, **settings_kwargs()))
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        dist.destroy_process_group()
+
+
+def trainer_launches(counts: dict, steps: int) -> int:
+    """Kernels of libtgs.so launched in the timed region (the per-entry-point counts are fixed by the
+    host code in csrc/: see DESIGN.md "Kernel inventory")."""
+    per_call = {"preprocess_fwd": 1, "bin_gaussians": 1 + 3 + 1 + 8 * 5 + 1 + 3, "bin_instances": 1 + 2 * 5 + 1,
+                "blend_fwd": 1, "loss": 5, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 8}
+    return int(sum(per_call[k] * c for k, c in counts.items() if k in per_call))
+
+
+if __name__ == "__main__":
+    main()

@@ -23,7 +23,7 @@
  *   tgs_loss_l1_ssim         training.total_loss image terms (training.py:61-89,
  *                            metrics.py:138-188)
  *   tgs_adam_step            optim.Adam.update (optim.py:37-49)
- *   tgs_compact_rows         cloud.take / Adam.compact row compaction
+ *   tgs_gather_rows          cloud.take / Adam.compact row compaction
  *                            (cloud.py:86-89, optim.py:51-55)
  *
  * Conventions (all entry points):
@@ -46,6 +46,12 @@ extern "C" {
 #endif
 
 typedef struct CUstream_st *tgs_stream_t; /* == cudaStream_t */
+
+#if defined(__GNUC__)
+#define TGS_API __attribute__((visibility("default")))
+#else
+#define TGS_API
+#endif
 
 enum {
   TGS_OK = 0,
@@ -75,6 +81,10 @@ typedef struct {
   float t[3];      /* x_cam = R x + t */
   float center[3]; /* -R^T t, computed by the caller (cameras.py:42-45) */
   int32_t width, height;
+  /* float64 third row of [R | t]: the depth SORT KEY is computed in float64 so the
+   * tile lists order exactly like the reference's float64 np.lexsort (float32
+   * depths collide ~2k times at 200k Gaussians and would reorder blends). */
+  double depth_row[4];
 } tgs_camera;
 
 typedef struct {
@@ -113,21 +123,23 @@ typedef struct { /* CloudGrads (cloud.py:110-126) */
   float *mean2d_screen; /* (n, 2); may be NULL */
 } tgs_grads;
 
-int tgs_version(void);
-const char *tgs_last_error_string(int status);
+TGS_API int tgs_version(void);
+TGS_API const char *tgs_last_error_string(int status);
 
 /* ---- (1) preprocess -----------------------------------------------------
  * splats (n, 12), visible (n,) 0/1, tiles_touched (n,) = number of tiles the
  * Gaussian's 3-sigma box covers (0 when not visible / off screen).
+ * depth_keys (n,) uint64 or NULL: order-preserving bits of the float64 depth
+ * (cam->depth_row . [x, 1]), the sort key consumed by tgs_bin_gaussians.
  * error_flag: device int32, OR-ed with 1 when a quaternion has norm < 1e-12;
  * the caller reads it back and raises DegenerateRotationError. */
-int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
-                           float *splats, uint8_t *visible, int32_t *tiles_touched,
+TGS_API int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
+                           float *splats, uint8_t *visible, int32_t *tiles_touched, uint64_t *depth_keys,
                            int32_t *error_flag, tgs_stream_t stream);
 
 /* tiles_touched for arbitrary projected records (the bin_tiles(...) entry,
  * rasterizer.py:95-128): only splat fields means2d and radius are read. */
-int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
+TGS_API int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
                     int32_t *tiles_touched, tgs_stream_t stream);
 
 /* ---- (2) binning ----------------------------------------------------------
@@ -139,16 +151,20 @@ int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32_t heigh
  * [row_begin, row_end) (tile-row sharding); tile_offsets has
  * (row_end-row_begin)*tiles_x + 1 entries, relative to the band.
  *
+ * depth_keys: per-Gaussian uint64 keys from tgs_preprocess_forward, or NULL to
+ * key on the float32 splat depth (the raw-array bin_tiles entry).
+ *
  * Step A: tgs_bin_gaussians() needs a workspace of tgs_bin_gaussians_workspace()
  * bytes, which must stay alive until step B returns.  It writes the instance count
  * to *d_num_instances (device int64).
  * Step B: tgs_bin_instances() with num_instances read back by the caller. */
-int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes);
-int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
+TGS_API int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes);
+TGS_API int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, const uint64_t *depth_keys,
+                      int64_t n, int32_t width,
                       int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
                       void *workspace, int64_t *d_num_instances, tgs_stream_t stream);
-int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes);
-int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
+TGS_API int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes);
+TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
                       int32_t row_begin, int32_t row_end, void *gauss_workspace, int64_t num_instances,
                       void *workspace, int32_t *tile_offsets, int32_t *sorted_ids, tgs_stream_t stream);
 
@@ -156,21 +172,29 @@ int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t hei
  * image (H, W, 3), transmit / weight_sum (H, W) float32, n_contrib / last_pos
  * (H, W) int32 (_kernels.py:83-89); hits (n,) int32 or NULL (record_hits).
  * Only pixels of tile rows [row_begin, row_end) are written. */
-int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+TGS_API int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                       const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                       float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
                       int32_t *last_pos, int32_t *hits, tgs_stream_t stream);
 
+/* Per-pixel ordered (Gaussian, blend weight) records — the reference's
+ * records_kernel (_kernels.py:184-241), a test/debug payload.  pixel_offsets
+ * (H*W,) int64 is the exclusive cumsum of n_contrib; rec_gauss (int32) and
+ * rec_weight (float32) have sum(n_contrib) entries.  Full image only. */
+TGS_API int tgs_blend_records(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                      const tgs_camera *cam, const tgs_settings *s, const int64_t *pixel_offsets,
+                      int32_t *rec_gauss, float *rec_weight, tgs_stream_t stream);
+
 /* ---- (4) backward blend -----------------------------------------------------
  * dsplats (n, 9) is ACCUMULATED into (caller zeroes it). dimage (H, W, 3). */
-int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+TGS_API int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                        const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                        const float *transmit, const int32_t *last_pos, const float *dimage,
                        float *dsplats, tgs_stream_t stream);
 
 /* ---- (5) preprocess backward ------------------------------------------------
  * accumulate != 0 adds into grads (multi-view batches), else overwrites. */
-int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
+TGS_API int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                             const uint8_t *visible, const float *dsplats, tgs_grads *grads,
                             int32_t accumulate, tgs_stream_t stream);
 
@@ -178,20 +202,20 @@ int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const
  * symmetric padding (training.py:76-89, metrics.py:138-188).  image/target
  * (H, W, 3); dimage (H, W, 3) written; terms (device float64[2]) receives
  * {mean |image-target|, mean SSIM}.  Workspace: tgs_loss_workspace() bytes. */
-int tgs_loss_workspace(int32_t width, int32_t height, size_t *bytes);
-int tgs_loss_l1_ssim(const float *image, const float *target, int32_t width, int32_t height,
+TGS_API int tgs_loss_workspace(int32_t width, int32_t height, size_t *bytes);
+TGS_API int tgs_loss_l1_ssim(const float *image, const float *target, int32_t width, int32_t height,
                      float lambda_ssim, float *dimage, double *terms, void *workspace,
                      tgs_stream_t stream);
 
 /* ---- (7) Adam (optim.py:37-49) over one parameter group of n floats.
  * bias corrections are passed in (1 - beta^step) so the step counter stays host-side. */
-int tgs_adam_step(float *param, const float *grad, float *m, float *v, int64_t n, float lr,
+TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, int64_t n, float lr,
                   float beta1, float beta2, float eps, float bias_c1, float bias_c2,
                   tgs_stream_t stream);
 
 /* ---- (8) row compaction (cloud.take / Adam.compact): out[k] = in[keep[k]] for
  * rows of `row_floats` floats. */
-int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,
+TGS_API int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,
                     int32_t row_floats, tgs_stream_t stream);
 
 #ifdef __cplusplus

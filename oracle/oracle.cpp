@@ -323,7 +323,11 @@ static Fwd<R> forward_one(const oracle_cloud &cl, int64_t i, const Cam<R> &cam, 
 template <typename R>
 static int64_t tile_rect(R mx, R my, R r, int W, int H, int ts, int *x0, int *y0, int *x1, int *y1) {
   const int tx = (W + ts - 1) / ts, ty = (H + ts - 1) / ts;
-  auto cl = [](R v, int hi) { return (int)std::min(std::max(v, R(0)), R(hi)); };
+  auto cl = [](R v, int hi) {
+    if (!(v >= R(0))) v = R(0);
+    if (v > R(hi)) v = R(hi);
+    return (int)v;
+  };
   *x0 = cl(M<R>::floor((mx - r) / R(ts)), tx - 1);
   *x1 = cl(M<R>::floor((mx + r) / R(ts)), tx - 1);
   *y0 = cl(M<R>::floor((my - r) / R(ts)), ty - 1);
@@ -332,9 +336,16 @@ static int64_t tile_rect(R mx, R my, R r, int W, int H, int ts, int *x0, int *y0
   return on ? int64_t(*x1 - *x0 + 1) * int64_t(*y1 - *y0 + 1) : 0;
 }
 
+// float64 camera-space depth from the float32-valued inputs and the float64 camera:
+// the sort key of BOTH instantiations (float32 depths
+// collide ~2k times at c2 and would reorder blends relative to the reference).
+static double depth64(const oracle_cloud &cl, int64_t i, const oracle_camera &oc) {
+  return cl.positions[3 * i] * oc.R[6] + cl.positions[3 * i + 1] * oc.R[7] + cl.positions[3 * i + 2] * oc.R[8] + oc.t[2];
+}
+
 template <typename R>
 static int preprocess(const oracle_cloud *cl, const oracle_camera *oc, const oracle_settings *s, R *splats,
-                      uint8_t *visible, int32_t *tiles) {
+                      uint8_t *visible, int32_t *tiles, double *depth_key) {
   const Cam<R> cam(*oc);
   int degenerate = 0;
   for (int64_t i = 0; i < cl->n; ++i) {
@@ -344,6 +355,7 @@ static int preprocess(const oracle_cloud *cl, const oracle_camera *oc, const ora
     std::fill(o, o + 12, R(0));
     visible[i] = f.visible;
     tiles[i] = 0;
+    if (depth_key) depth_key[i] = f.visible ? depth64(*cl, i, *oc) : 0.0;
     if (!f.visible) continue;
     o[0] = f.mean[0]; o[1] = f.mean[1];
     o[2] = f.conic[0]; o[3] = f.conic[1]; o[4] = f.conic[2];
@@ -358,8 +370,8 @@ static int preprocess(const oracle_cloud *cl, const oracle_camera *oc, const ora
 
 // bin_tiles: emit row-major instances, stable sort by (tile, depth, index)
 template <typename R>
-static int64_t bin(const R *splats, const int32_t *tiles, int64_t n, int W, int H, int ts, int64_t *offsets,
-                   int64_t *ids, int64_t capacity) {
+static int64_t bin(const R *splats, const int32_t *tiles, const double *depth_key, int64_t n, int W, int H, int ts,
+                   int64_t *offsets, int64_t *ids, int64_t capacity) {
   const int tx = (W + ts - 1) / ts, ty = (H + ts - 1) / ts;
   const int64_t T = int64_t(tx) * ty;
   std::vector<std::pair<int64_t, int64_t>> inst;  // (tile, gid)
@@ -373,7 +385,8 @@ static int64_t bin(const R *splats, const int32_t *tiles, int64_t n, int W, int 
   }
   std::stable_sort(inst.begin(), inst.end(), [&](const auto &a, const auto &b) {
     if (a.first != b.first) return a.first < b.first;
-    const R da = splats[12 * a.second + 9], db = splats[12 * b.second + 9];
+    const double da = depth_key ? depth_key[a.second] : double(splats[12 * a.second + 9]);
+    const double db = depth_key ? depth_key[b.second] : double(splats[12 * b.second + 9]);
     if (da != db) return da < db;
     return a.second < b.second;
   });
@@ -610,12 +623,12 @@ extern "C" {
 float oracle_sem_expf(float x) { return sem_expf(x); }
 
 int oracle_preprocess_f64(const oracle_cloud *c, const oracle_camera *cam, const oracle_settings *s,
-                          double *splats, uint8_t *vis, int32_t *tiles) {
-  return preprocess<double>(c, cam, s, splats, vis, tiles);
+                          double *splats, uint8_t *vis, int32_t *tiles, double *depth_key) {
+  return preprocess<double>(c, cam, s, splats, vis, tiles, depth_key);
 }
 int oracle_preprocess_f32(const oracle_cloud *c, const oracle_camera *cam, const oracle_settings *s,
-                          float *splats, uint8_t *vis, int32_t *tiles) {
-  return preprocess<float>(c, cam, s, splats, vis, tiles);
+                          float *splats, uint8_t *vis, int32_t *tiles, double *depth_key) {
+  return preprocess<float>(c, cam, s, splats, vis, tiles, depth_key);
 }
 int oracle_count_tiles_f64(const double *splats, int64_t n, int W, int H, int ts, int32_t *tiles) {
   for (int64_t g = 0; g < n; ++g) {
@@ -631,13 +644,13 @@ int oracle_count_tiles_f32(const float *splats, int64_t n, int W, int H, int ts,
   }
   return 0;
 }
-int64_t oracle_bin_f64(const double *sp, const int32_t *tiles, int64_t n, int W, int H, int ts, int64_t *offsets,
-                       int64_t *ids, int64_t cap) {
-  return bin<double>(sp, tiles, n, W, H, ts, offsets, ids, cap);
+int64_t oracle_bin_f64(const double *sp, const int32_t *tiles, const double *dk, int64_t n, int W, int H, int ts,
+                       int64_t *offsets, int64_t *ids, int64_t cap) {
+  return bin<double>(sp, tiles, dk, n, W, H, ts, offsets, ids, cap);
 }
-int64_t oracle_bin_f32(const float *sp, const int32_t *tiles, int64_t n, int W, int H, int ts, int64_t *offsets,
-                       int64_t *ids, int64_t cap) {
-  return bin<float>(sp, tiles, n, W, H, ts, offsets, ids, cap);
+int64_t oracle_bin_f32(const float *sp, const int32_t *tiles, const double *dk, int64_t n, int W, int H, int ts,
+                       int64_t *offsets, int64_t *ids, int64_t cap) {
+  return bin<float>(sp, tiles, dk, n, W, H, ts, offsets, ids, cap);
 }
 void oracle_blend_fwd_f64(const double *sp, const int64_t *off, const int64_t *ids, int W, int H, int ts,
                           const double *bg, double *img, double *T, double *ws, int32_t *nc, int32_t *lp, int64_t *hits) {

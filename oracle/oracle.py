@@ -147,10 +147,12 @@ def preprocess(cloud, cam, settings, dtype="f64"):
     splats = np.zeros((n, 12), dtype=npt)
     visible = np.zeros(n, dtype=np.uint8)
     tiles = np.zeros(n, dtype=np.int32)
+    depth_key = np.zeros(n, dtype=np.float64)
     cc, ss = _camera(cam), _settings(settings)
     rc = getattr(lib(), f"oracle_preprocess_{sfx}")(ctypes.byref(hold.c), ctypes.byref(cc), ctypes.byref(ss),
-                                                    _ptr(splats), _ptr(visible), _ptr(tiles))
-    return dict(splats=splats, visible=visible.astype(bool), tiles_touched=tiles, status=int(rc))
+                                                    _ptr(splats), _ptr(visible), _ptr(tiles), _ptr(depth_key))
+    return dict(splats=splats, visible=visible.astype(bool), tiles_touched=tiles, depth_key=depth_key,
+                status=int(rc))
 
 
 def count_tiles(splats, width, height, tile_size, dtype="f64"):
@@ -162,7 +164,7 @@ def count_tiles(splats, width, height, tile_size, dtype="f64"):
     return tiles
 
 
-def bin_tiles(splats, tiles_touched, width, height, tile_size, dtype="f64"):
+def bin_tiles(splats, tiles_touched, width, height, tile_size, dtype="f64", depth_key=None):
     npt, sfx = _rt(dtype)
     splats = np.ascontiguousarray(splats, dtype=npt)
     tiles_touched = np.ascontiguousarray(tiles_touched, dtype=np.int32)
@@ -172,8 +174,9 @@ def bin_tiles(splats, tiles_touched, width, height, tile_size, dtype="f64"):
     fn = getattr(lib(), f"oracle_bin_{sfx}")
     total = int(tiles_touched.astype(np.int64).sum())
     ids = np.zeros(max(total, 1), dtype=np.int64)
-    got = fn(_ptr(splats), _ptr(tiles_touched), n, int(width), int(height), int(tile_size), _ptr(offsets),
-             _ptr(ids), ctypes.c_int64(ids.size))
+    dk = None if depth_key is None else np.ascontiguousarray(depth_key, dtype=np.float64)
+    got = fn(_ptr(splats), _ptr(tiles_touched), _ptr(dk), n, int(width), int(height), int(tile_size),
+             _ptr(offsets), _ptr(ids), ctypes.c_int64(ids.size))
     assert got == total, (got, total)
     return offsets, ids[:total], tx, ty
 
@@ -233,7 +236,7 @@ def render_forward(cloud, cam, settings, dtype="f64"):
     if pre["status"] == 2:
         raise ValueError("degenerate rotation")
     W, H, ts = int(cam.width), int(cam.height), int(settings.tile_size)
-    offsets, ids, tx, ty = bin_tiles(pre["splats"], pre["tiles_touched"], W, H, ts, dtype)
+    offsets, ids, tx, ty = bin_tiles(pre["splats"], pre["tiles_touched"], W, H, ts, dtype, pre["depth_key"])
     out = blend_forward(pre["splats"], offsets, ids, W, H, ts, settings.background,
                         getattr(settings, "record_hits", False), dtype)
     out.update(pre)

@@ -1,0 +1,157 @@
+"""ctypes binding of libtgs.so (include/tgs.h).
+
+The product path has exactly one implementation: the CUDA library.  If the
+shared object is missing or fails to load, every entry point raises
+NativeLibraryError — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import ContractViolationError, NativeLibraryError, raise_for_status
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtgs.so")
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_F = ctypes.c_float
+_D = ctypes.c_double
+
+
+class TgsCamera(ctypes.Structure):
+    _fields_ = [("fx", _F), ("fy", _F), ("cx", _F), ("cy", _F), ("R", _F * 9), ("t", _F * 3), ("center", _F * 3),
+                ("width", _I32), ("height", _I32), ("depth_row", _D * 4)]
+
+
+class TgsSettings(ctypes.Structure):
+    _fields_ = [("lowpass_s", _F), ("near_plane", _F), ("mask_logit_min", _F), ("sh_mask_logit_min", _F),
+                ("opacity_logit_min", _F), ("background", _F * 3), ("active_sh_degree", _I32),
+                ("tile_size", _I32), ("compute_sh_rest_grads", _I32), ("reserved", _I32)]
+
+
+CLOUD_FIELDS = ("positions", "log_scales", "rotations", "opacity_logits", "sh_dc", "sh_rest", "mask_logits",
+                "sh_mask_logits")
+GRAD_FIELDS = CLOUD_FIELDS + ("mean2d_screen",)
+
+
+class TgsCloud(ctypes.Structure):
+    _fields_ = [(f, _P) for f in CLOUD_FIELDS] + [("n", _I64)]
+
+
+class TgsGrads(ctypes.Structure):
+    _fields_ = [(f, _P) for f in GRAD_FIELDS]
+
+
+_SIGS = {
+    "tgs_version": ([], _I32),
+    "tgs_preprocess_forward": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
+    "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
+    "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P], _I32),
+    "tgs_bin_instances_workspace": ([_I64, _I64, _P], _I32),
+    "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),
+    "tgs_blend_forward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_records": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_backward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P], _I32),
+    "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
+    "tgs_loss_workspace": ([_I32, _I32, _P], _I32),
+    "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
+    "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),
+    "tgs_gather_rows": ([_P, _P, _P, _I64, _I32, _P], _I32),
+}
+
+_lib = None
+
+
+def load():
+    """Load libtgs.so once; raises NativeLibraryError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryError(
+            f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    import torch  # noqa: F401  (loads libcudart first so the library binds to the same runtime)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover
+        raise NativeLibraryError(f"failed to load {LIB_PATH}: {e}") from e
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    raise_for_status(int(getattr(load(), name)(*args)), name)
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(device=None):
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _logit(p: float) -> float:
+    return float(np.log(p / (1.0 - p)))
+
+
+def logit_floor_f32(eps: float) -> float:
+    """Largest float32 <= logit(eps): sigmoid(m) > eps <=> m > this (masking.py:21-25)."""
+    L = _logit(eps)
+    f = np.float32(L)
+    if float(f) > L:
+        f = np.nextafter(f, np.float32(-np.inf))
+    return float(f)
+
+
+def logit_ceil_f32(p: float) -> float:
+    """Smallest float32 >= logit(p): sigmoid(o) >= p <=> o >= this (rasterizer.py:178)."""
+    L = _logit(p)
+    f = np.float32(L)
+    if float(f) < L:
+        f = np.nextafter(f, np.float32(np.inf))
+    return float(f)
+
+
+def make_camera(cam) -> TgsCamera:
+    v = cam.native_fields() if hasattr(cam, "native_fields") else _native_fields(cam)
+    return TgsCamera(v["fx"], v["fy"], v["cx"], v["cy"], (_F * 9)(*v["R"]), (_F * 3)(*v["t"]),
+                     (_F * 3)(*v["center"]), v["width"], v["height"], (_D * 4)(*v["depth_row"]))
+
+
+def _native_fields(cam) -> dict:
+    R = np.asarray(cam.R, dtype=np.float64).reshape(3, 3)
+    t = np.asarray(cam.t, dtype=np.float64).reshape(3)
+    f32 = lambda x: float(np.float32(x))  # noqa: E731
+    return dict(fx=f32(cam.fx), fy=f32(cam.fy), cx=f32(cam.cx), cy=f32(cam.cy), R=[f32(x) for x in R.reshape(-1)],
+                t=[f32(x) for x in t], center=[f32(x) for x in (-R.T @ t)], width=int(cam.width),
+                height=int(cam.height), depth_row=[float(R[2, 0]), float(R[2, 1]), float(R[2, 2]), float(t[2])])
+
+
+def make_settings(s) -> TgsSettings:
+    if not 0.0 < s.mask_threshold < 1.0 or not 0.0 < s.sh_mask_threshold < 1.0:
+        raise ContractViolationError("mask threshold must lie in (0, 1)")  # masking.py:23-24
+    if s.lowpass_s < 0:
+        raise ContractViolationError("lowpass_s must be >= 0")  # geometry.py:150-151
+    if not 0 <= int(s.active_sh_degree) <= 3:
+        raise ContractViolationError("active_degree must be in 0..3")  # sh.py:147-148
+    if int(s.tile_size) < 1:
+        raise ContractViolationError("tile_size must be >= 1")  # rasterizer.py:103-104
+    bg = [float(v) for v in s.background]
+    return TgsSettings(float(s.lowpass_s), float(s.near), logit_floor_f32(s.mask_threshold),
+                       logit_floor_f32(s.sh_mask_threshold), logit_ceil_f32(1.0 / 255.0), (_F * 3)(*bg),
+                       int(s.active_sh_degree), int(s.tile_size), int(bool(s.compute_sh_rest_grads)), 0)

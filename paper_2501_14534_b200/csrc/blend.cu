@@ -1,0 +1,330 @@
+// blend.cu — per-tile alpha blending forward (R6) and backward (R7).
+//
+// Reference semantics (must match exactly):
+//   forward  _kernels.py:38-89  — per pixel over the tile's depth-sorted list:
+//            break when T < 1e-4 (checked BEFORE each entry, so the entry that
+//            drives T below the threshold is still blended); e = -1/2(a dx^2 +
+//            c dy^2) - b dx dy, skip e < -4.5 or e > 0; a = alpha * exp(e), skip
+//            a < 1/255, clamp 0.99; C += c a T; T *= 1 - a; image = C + bg T;
+//            last_pos = list position after the last blended entry.
+//   backward _kernels.py:125-181 — per pixel back to front from last_pos,
+//            T_before = T_after / (1 - a), suffix colour S seeded with bg*T_final;
+//            the alpha/mean/cov partials only when a_raw <= 0.99.
+//
+// B200 mapping: one CTA per 16x16 tile (one thread per pixel), Gaussians staged
+// through shared memory in batches of up to 256 records (48 B each, three
+// 16 B loads).  The forward CTA leaves as soon as every pixel has terminated
+// (__syncthreads_count).  The backward keeps the reference's per-pixel
+// recurrence but accumulates per SPLAT: each staged Gaussian's 9 partials are
+// reduced across the warp with shuffles (skipped when no lane of the warp
+// touched it), combined across the CTA's warps in shared memory, and written
+// with ONE global atomic per (tile, Gaussian, field) — no per-pixel global
+// atomics.
+//
+// The exponent and alpha are evaluated by blend_alpha() with explicit
+// round-to-nearest intrinsics in BOTH kernels, so the backward re-derives the
+// forward's blend decisions bit for bit (a mismatch would corrupt the
+// T_before = T_after / (1 - a) recovery).
+#include "tgs_common.cuh"
+
+namespace tgs {
+
+constexpr int kBatch = 256;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// e = -0.5 (a dx^2 + c dy^2) - b dx dy with a fixed operation sequence.
+__device__ __forceinline__ float blend_exponent(float ca, float cb, float cc, float dx, float dy) {
+  const float q = __fmaf_rn(__fmul_rn(cc, dy), dy, __fmul_rn(__fmul_rn(ca, dx), dx));
+  return __fmaf_rn(-__fmul_rn(cb, dx), dy, __fmul_rn(-0.5f, q));
+}
+
+__device__ __forceinline__ float blend_gauss(float e) { return ex2_approx(__fmul_rn(e, 1.44269504088896341f)); }
+
+__global__ void k_blend_fwd(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
+                            const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x, int row_begin,
+                            float bg0, float bg1, float bg2, float *__restrict__ image, float *__restrict__ transmit,
+                            float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
+                            int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
+  __shared__ float4 sm[kBatch * 3];
+  __shared__ int32_t sid[kBatch];
+  const int B = blockDim.x;
+  const int batch = B < kBatch ? B : kBatch;
+  const int tile = blockIdx.x;
+  const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
+  const int t = threadIdx.x;
+  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  const bool inside = t < ts * ts && px < W && py < H;
+  const int start = offsets[tile], stop = offsets[tile + 1];
+  const float fpx = (float)px, fpy = (float)py;
+  float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, ws = 0.0f;
+  int contrib = 0, lastp = 0;
+  bool done = !inside;
+  for (int base = start; base < stop; base += batch) {
+    if (__syncthreads_count(done) == B) break;
+    if (t < batch && base + t < stop) {
+      const int g = ids[base + t];
+      sm[3 * t] = splats[3 * g];
+      sm[3 * t + 1] = splats[3 * g + 1];
+      sm[3 * t + 2] = splats[3 * g + 2];
+      sid[t] = g;
+    }
+    __syncthreads();
+    const int cnt = min(batch, stop - base);
+    if (!done) {
+      for (int k = 0; k < cnt; ++k) {
+        if (T < kTTerm) {
+          done = true;
+          break;
+        }
+        const float4 a = sm[3 * k];
+        const float4 b = sm[3 * k + 1];
+        const float e = blend_exponent(a.z, a.w, b.x, fpx - a.x, fpy - a.y);
+        if (e < kEMin || e > 0.0f) continue;
+        float al = __fmul_rn(b.y, blend_gauss(e));
+        if (al < kAlphaSkip) continue;
+        al = fminf(al, kAlphaMax);
+        const float c2v = sm[3 * k + 2].x;
+        const float w = al * T;
+        c0 += b.z * w;
+        c1 += b.w * w;
+        c2 += c2v * w;
+        ws += w;
+        T = __fmul_rn(T, __fsub_rn(1.0f, al));
+        ++contrib;
+        lastp = base - start + k + 1;
+        if (hits) atomicAdd(hits + sid[k], 1);
+      }
+      if (T < kTTerm) done = true;
+    }
+  }
+  if (inside) {
+    const int p = py * W + px;
+    image[3 * p] = c0 + bg0 * T;
+    image[3 * p + 1] = c1 + bg1 * T;
+    image[3 * p + 2] = c2 + bg2 * T;
+    transmit[p] = T;
+    wsum_out[p] = ws;
+    n_contrib[p] = contrib;
+    last_pos[p] = lastp;
+  }
+}
+
+__global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
+                            const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x, int row_begin,
+                            float bg0, float bg1, float bg2, const float *__restrict__ transmit,
+                            const int32_t *__restrict__ last_pos, const float *__restrict__ dimage,
+                            float *__restrict__ dsplats) {
+  __shared__ float4 sm[kBatch * 3];
+  __shared__ int32_t sid[kBatch];
+  __shared__ float acc[9][kBatch];
+  __shared__ int wmax[32];
+  const int B = blockDim.x;
+  const int batch = B < kBatch ? B : kBatch;
+  const int tile = blockIdx.x;
+  const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  const bool inside = t < ts * ts && px < W && py < H;
+  const int start = offsets[tile];
+  const float fpx = (float)px, fpy = (float)py;
+  int lastp = 0;
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f, T_after = 0.f;
+  if (inside) {
+    const int p = py * W + px;
+    lastp = last_pos[p];
+    g0 = dimage[3 * p];
+    g1 = dimage[3 * p + 1];
+    g2 = dimage[3 * p + 2];
+    if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) lastp = 0;  // _kernels.py:133-134
+    T_after = transmit[p];
+  }
+  float s0 = bg0 * T_after, s1 = bg1 * T_after, s2 = bg2 * T_after;
+  // longest list prefix any pixel of the tile needs
+  int m = __reduce_max_sync(0xffffffffu, lastp);
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < (B + 31) / 32 ? wmax[lane] : 0;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) wmax[0] = m;
+  }
+  __syncthreads();
+  const int max_last = wmax[0];
+  for (int hi = max_last; hi > 0; hi -= batch) {
+    const int lo = hi > batch ? hi - batch : 0;
+    const int cnt = hi - lo;
+    __syncthreads();
+    if (t < cnt) {
+      const int g = ids[start + lo + t];
+      sm[3 * t] = splats[3 * g];
+      sm[3 * t + 1] = splats[3 * g + 1];
+      sm[3 * t + 2] = splats[3 * g + 2];
+      sid[t] = g;
+#pragma unroll
+      for (int f = 0; f < 9; ++f) acc[f][t] = 0.0f;
+    }
+    __syncthreads();
+    for (int q = cnt - 1; q >= 0; --q) {
+      float v[9];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+      bool hit = false;
+      if (lo + q < lastp) {
+        const float4 a = sm[3 * q];
+        const float4 b = sm[3 * q + 1];
+        const float dx = fpx - a.x, dy = fpy - a.y;
+        const float e = blend_exponent(a.z, a.w, b.x, dx, dy);
+        if (!(e < kEMin || e > 0.0f)) {
+          const float gauss = blend_gauss(e);
+          const float a_raw = __fmul_rn(b.y, gauss);
+          const float al = fminf(a_raw, kAlphaMax);
+          if (al >= kAlphaSkip) {
+            hit = true;
+            const float cz = sm[3 * q + 2].x;
+            const float inv_om = 1.0f / (1.0f - al);
+            const float t_before = T_after * inv_om;
+            const float ga = g0 * (b.z * t_before - s0 * inv_om) + g1 * (b.w * t_before - s1 * inv_om) +
+                             g2 * (cz * t_before - s2 * inv_om);
+            const float w = al * t_before;
+            v[6] = g0 * w;
+            v[7] = g1 * w;
+            v[8] = g2 * w;
+            if (a_raw <= kAlphaMax) {
+              v[5] = ga * gauss;
+              const float gG = ga * b.y * gauss;
+              const float v0 = a.z * dx + a.w * dy, v1 = a.w * dx + b.x * dy;
+              v[0] = gG * v0;
+              v[1] = gG * v1;
+              v[2] = gG * 0.5f * v0 * v0;
+              v[3] = gG * v0 * v1;
+              v[4] = gG * 0.5f * v1 * v1;
+            }
+            s0 += b.z * w;
+            s1 += b.w * w;
+            s2 += cz * w;
+            T_after = t_before;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+        for (int f = 0; f < 9; ++f) {
+          float x = v[f];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          v[f] = x;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int f = 0; f < 9; ++f)
+            if (v[f] != 0.0f) atomicAdd(&acc[f][q], v[f]);
+        }
+      }
+    }
+    __syncthreads();
+    if (t < cnt) {
+      float *d = dsplats + 9 * (int64_t)sid[t];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) {
+        const float x = acc[f][t];
+        if (x != 0.0f) atomicAdd(d + f, x);
+      }
+    }
+  }
+}
+
+// _kernels.py:184-241: same walk as the forward, writing (gid, a*T) per blended entry
+__global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
+                                const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x,
+                                const int64_t *__restrict__ pix_off, int32_t *__restrict__ rec_g,
+                                float *__restrict__ rec_w) {
+  const int tile = blockIdx.x;
+  const int ty = tile / tiles_x, tx = tile % tiles_x;
+  const int t = threadIdx.x;
+  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  if (t >= ts * ts || px >= W || py >= H) return;
+  const int start = offsets[tile], stop = offsets[tile + 1];
+  int64_t pos = pix_off[py * W + px];
+  float T = 1.0f;
+  for (int k = start; k < stop; ++k) {
+    if (T < kTTerm) break;
+    const int g = ids[k];
+    const float4 a = splats[3 * g], b = splats[3 * g + 1];
+    const float e = blend_exponent(a.z, a.w, b.x, (float)px - a.x, (float)py - a.y);
+    if (e < kEMin || e > 0.0f) continue;
+    float al = __fmul_rn(b.y, blend_gauss(e));
+    if (al < kAlphaSkip) continue;
+    al = fminf(al, kAlphaMax);
+    rec_g[pos] = g;
+    rec_w[pos] = al * T;
+    ++pos;
+    T = __fmul_rn(T, __fsub_rn(1.0f, al));
+  }
+}
+
+inline bool blend_args(const tgs_camera *cam, const tgs_settings *s, int rb, int re, int &tiles_x, int &ntiles) {
+  if (!cam || !s || s->tile_size < 1 || s->tile_size > 32) return false;
+  tiles_x = (cam->width + s->tile_size - 1) / s->tile_size;
+  const int tiles_y = (cam->height + s->tile_size - 1) / s->tile_size;
+  if (rb < 0 || re > tiles_y || rb > re) return false;
+  ntiles = (re - rb) * tiles_x;
+  return true;
+}
+
+inline int tile_size_guard(int ts) { return ts < 1 ? 1 : ts; }
+
+}  // namespace tgs
+
+using namespace tgs;
+
+extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                                 const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
+                                 float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
+                                 int32_t *last_pos, int32_t *hits, tgs_stream_t stream) {
+  int tiles_x, ntiles;
+  if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if (ntiles == 0) return TGS_OK;
+  const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
+  k_blend_fwd<<<ntiles, B, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      tiles_x, row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum,
+      n_contrib, last_pos, hits);
+  return launch_status();
+}
+
+extern "C" int tgs_blend_records(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                                 const tgs_camera *cam, const tgs_settings *s, const int64_t *pixel_offsets,
+                                 int32_t *rec_gauss, float *rec_weight, tgs_stream_t stream) {
+  int tiles_x, ntiles;
+  if (!cam || !s) return TGS_ERR_INVALID;
+  const int tiles_y = (cam->height + s->tile_size - 1) / tile_size_guard(s->tile_size);
+  if (!blend_args(cam, s, 0, tiles_y, tiles_x, ntiles)) return TGS_ERR_INVALID;
+  if (ntiles == 0) return TGS_OK;
+  const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
+  k_blend_records<<<ntiles, B, 0, as_stream(stream)>>>(reinterpret_cast<const float4 *>(splats), tile_offsets,
+                                                       sorted_ids, cam->width, cam->height, s->tile_size, tiles_x,
+                                                       pixel_offsets, rec_gauss, rec_weight);
+  return launch_status();
+}
+
+extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+                                  const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
+                                  const float *transmit, const int32_t *last_pos, const float *dimage,
+                                  float *dsplats, tgs_stream_t stream) {
+  int tiles_x, ntiles;
+  if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if (ntiles == 0) return TGS_OK;
+  const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
+  k_blend_bwd<<<ntiles, B, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage,
+      dsplats);
+  return launch_status();
+}

@@ -1,0 +1,298 @@
+"""Drop-in rasterizer API over libtgs.so.
+
+Mirrors `slimsplat.rasterizer` (rasterizer.py:44-419): same function names,
+argument lists, settings fields, output field names and exceptions, with
+float32 CUDA tensors in place of float64 numpy arrays:
+
+    render_forward(cloud, cam, settings) -> RenderOutput      (rasterizer.py:215)
+    render_backward(cloud, cam, settings, dimage, output)     (rasterizer.py:326)
+        -> CloudGrads
+    bin_tiles(means2d, radii, depths, width, height, tile_size) -> TileBins
+                                                              (rasterizer.py:95)
+    sh_rest_update_step(iteration, cadence) -> bool           (rasterizer.py:88)
+
+Deliberate differences:
+  * RenderOutput.visible / screen_areas / hit_counts are full-length (N,) as in the
+    reference; TileBins.indices are CLOUD ROWS (the reference indexes its
+    compacted visible subset — same order, different numbering).
+  * render_backward reuses the forward's projected records and tile lists instead
+    of re-running _prepare (rasterizer.py:342); results are identical by
+    construction because both passes see the same cloud, camera and settings.
+    If `output` carries no device state (e.g. built by hand), it recomputes them.
+  * extension keywords: `grads=` / `accumulate=` on render_backward let a
+    multi-view step accumulate into one CloudGrads buffer; `row_band=` renders
+    a band of tile rows (tile-row sharding, parallel.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cameras import Camera
+from .cloud import CloudGrads, GaussianCloud
+from .errors import ContractViolationError, DegenerateRotationError
+from .profiler import stage
+
+NEAR_PLANE = 0.01  # geometry.py:16
+ALPHA_SKIP = 1.0 / 255.0
+ALPHA_MAX = 0.99
+E_MIN = -4.5
+T_TERMINATE = 1e-4
+
+
+@dataclass
+class RenderSettings:
+    """rasterizer.py:44-55."""
+
+    lowpass_s: float = 0.3
+    active_sh_degree: int = 3
+    background: tuple = (0.0, 0.0, 0.0)
+    tile_size: int = 16
+    near: float = NEAR_PLANE
+    record_hits: bool = False
+    record_full: bool = False
+    mask_threshold: float = 0.05
+    sh_mask_threshold: float = 0.1
+    compute_sh_rest_grads: bool = True
+
+
+@dataclass
+class TileBins:
+    """Per-tile depth-sorted Gaussian lists in CSR layout (rasterizer.py:78-85)."""
+
+    offsets: torch.Tensor  # (tiles_y*tiles_x + 1,) int32
+    indices: torch.Tensor  # (I,) int32 cloud rows
+    tiles_x: int
+    tiles_y: int
+    row_begin: int = 0
+    row_end: int | None = None
+
+
+@dataclass
+class _DeviceState:
+    """Forward products reused by the backward."""
+
+    cloud_ptr: int
+    n: int
+    splats: torch.Tensor        # (N, 12)
+    visible_u8: torch.Tensor    # (N,)
+    tiles_touched: torch.Tensor
+    depth_keys: torch.Tensor | None
+    bins: TileBins
+
+
+@dataclass
+class RenderOutput:
+    """rasterizer.py:58-75."""
+
+    image: torch.Tensor          # (H, W, 3)
+    transmittance: torch.Tensor  # (H, W)
+    weight_sum: torch.Tensor     # (H, W)
+    n_contrib: torch.Tensor      # (H, W) int32
+    last_pos: torch.Tensor       # (H, W) int32
+    visible: torch.Tensor        # (N,) bool
+    screen_areas: torch.Tensor   # (N,)
+    hit_counts: torch.Tensor | None = None
+    hit_records: list | None = None
+    _tiles: TileBins | None = field(default=None, repr=False)
+    _state: _DeviceState | None = field(default=None, repr=False)
+
+
+def sh_rest_update_step(iteration: int, cadence: int) -> bool:
+    """Whether higher-band SH gradients are computed at this iteration (rasterizer.py:88-92)."""
+    if cadence < 1:
+        raise ContractViolationError("SH update cadence must be >= 1")
+    return iteration % cadence == 0
+
+
+def _tiles_y(cam, ts):
+    return (cam.height + ts - 1) // ts
+
+
+def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
+         row_begin: int, row_end: int, err: torch.Tensor | None = None,
+         depth_keys: torch.Tensor | None = None) -> TileBins:
+    """tgs_bin_gaussians + one host read of the instance count + tgs_bin_instances."""
+    dev = splats.device
+    st = _lib.stream_handle(dev)
+    tiles_x = (width + ts - 1) // ts
+    tiles_y = (height + ts - 1) // ts
+    nb = ctypes_size("tgs_bin_gaussians_workspace", n)
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
+    d_count = torch.empty(2, dtype=torch.int64, device=dev)
+    with stage("bin_gaussians"):
+        _lib.call("tgs_bin_gaussians", _lib.ptr(splats), _lib.ptr(tiles_touched), _lib.ptr(depth_keys), n, width,
+                  height, ts, row_begin, row_end, _lib.ptr(ws), _lib.ptr(d_count), st)
+    if err is not None:
+        d_count[1:2].copy_(err.to(torch.int64))
+        count, flag = (int(v) for v in d_count.cpu().tolist())
+        if flag:
+            raise DegenerateRotationError("quaternion with (near-)zero norm")
+    else:
+        count = int(d_count[0].item())
+    ntiles = (row_end - row_begin) * tiles_x
+    offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
+    ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+    ib = ctypes_size("tgs_bin_instances_workspace", n, count)
+    ws2 = torch.empty(max(ib, 16), dtype=torch.uint8, device=dev)
+    with stage("bin_instances"):
+        _lib.call("tgs_bin_instances", _lib.ptr(splats), n, width, height, ts, row_begin, row_end, _lib.ptr(ws),
+                  count, _lib.ptr(ws2), _lib.ptr(offsets), _lib.ptr(ids), st)
+    return TileBins(offsets, ids[:count], tiles_x, tiles_y, row_begin, row_end)
+
+
+def ctypes_size(fn: str, *args) -> int:
+    import ctypes
+    out = ctypes.c_size_t(0)
+    _lib.call(fn, *args, ctypes.byref(out))
+    return int(out.value)
+
+
+def bin_tiles(means2d, radii, depths, width: int, height: int, tile_size: int) -> TileBins:
+    """GPU bin_tiles on raw arrays (rasterizer.py:95-148); indices are input rows."""
+    if tile_size < 1:
+        raise ContractViolationError("tile_size must be >= 1")
+    dev = torch.device("cuda")
+    m = torch.as_tensor(np.asarray(means2d) if not torch.is_tensor(means2d) else means2d).to(dev, torch.float32)
+    n = int(m.shape[0])
+    sp = torch.zeros((max(n, 1), 12), dtype=torch.float32, device=dev)
+    if n:
+        sp[:n, 0:2] = m.reshape(n, 2)
+        sp[:n, 9] = torch.as_tensor(np.asarray(depths) if not torch.is_tensor(depths) else depths).to(dev, torch.float32)
+        sp[:n, 10] = torch.as_tensor(np.asarray(radii) if not torch.is_tensor(radii) else radii).to(dev, torch.float32)
+    tiles = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+    st = _lib.stream_handle(dev)
+    if n:
+        _lib.call("tgs_count_tiles", _lib.ptr(sp), n, width, height, tile_size, _lib.ptr(tiles), st)
+    ty = (height + tile_size - 1) // tile_size
+    return _bin(sp, tiles, n, width, height, tile_size, 0, ty)
+
+
+def _as_cloud(cloud) -> GaussianCloud:
+    if isinstance(cloud, GaussianCloud):
+        return cloud
+    return GaussianCloud.from_fields(cloud)
+
+
+def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
+    """tgs_preprocess_forward: (splats (N,12), visible u8, tiles_touched i32, float64 depth keys, error flag)."""
+    n = len(cloud)
+    dev = cloud.device
+    splats = torch.empty((max(n, 1), 12), dtype=torch.float32, device=dev)
+    vis = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+    tiles = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    if n:
+        c_cloud, c_cam, c_set = cloud.native(), _lib.make_camera(cam), _lib.make_settings(settings)
+        import ctypes
+        with stage("preprocess_fwd"):
+            _lib.call("tgs_preprocess_forward", ctypes.byref(c_cloud), ctypes.byref(c_cam), ctypes.byref(c_set),
+                      _lib.ptr(splats), _lib.ptr(vis), _lib.ptr(tiles), _lib.ptr(keys), _lib.ptr(err),
+                      _lib.stream_handle(dev))
+    return splats, vis, tiles, keys, err
+
+
+def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple | None = None) -> RenderOutput:
+    """Render a cloud into an (H, W, 3) image plus blending auxiliaries (rasterizer.py:215-284)."""
+    import ctypes
+    cloud = _as_cloud(cloud)
+    c_set = _lib.make_settings(settings)  # validates settings even for empty clouds
+    if settings.tile_size > 32:
+        raise ContractViolationError("tile_size > 32 is not supported by the CUDA kernels")
+    h, w, ts = int(cam.height), int(cam.width), int(settings.tile_size)
+    n = len(cloud)
+    dev = cloud.device
+    rb, re = row_band if row_band is not None else (0, _tiles_y(cam, ts))
+    splats, vis, tiles, keys, err = preprocess(cloud, cam, settings)
+    bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys)
+    image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+    transmit = torch.empty((h, w), dtype=torch.float32, device=dev)
+    wsum = torch.empty((h, w), dtype=torch.float32, device=dev)
+    n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
+    last_pos = torch.empty((h, w), dtype=torch.int32, device=dev)
+    if row_band is not None:  # pixels outside the band are not rendered here
+        for t_, v in ((image, 0.0), (transmit, 1.0), (wsum, 0.0), (n_contrib, 0), (last_pos, 0)):
+            t_.fill_(v)
+    hits = torch.zeros(max(n, 1), dtype=torch.int32, device=dev) if settings.record_hits else None
+    c_cam = _lib.make_camera(cam)
+    with stage("blend_fwd"):
+        _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+                  ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
+                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.stream_handle(dev))
+    visible = vis[:n].bool()
+    out = RenderOutput(image=image, transmittance=transmit, weight_sum=wsum, n_contrib=n_contrib,
+                       last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11],
+                       hit_counts=hits[:n].to(torch.int64) if hits is not None else None,
+                       _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins))
+    if settings.record_full:
+        out.hit_records = _records(out, splats, bins, cam, c_cam, c_set, dev)
+    return out
+
+
+def _records(out, splats, bins, cam, c_cam, c_set, dev):
+    """Per-pixel [(cloud row, weight), ...] lists (rasterizer.py:287-323); debug payload."""
+    import ctypes
+    flat = out.n_contrib.reshape(-1).to(torch.int64)
+    total = int(flat.sum().item())
+    offsets = torch.zeros_like(flat)
+    if flat.numel() > 1:
+        offsets[1:] = torch.cumsum(flat[:-1], 0)
+    g = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    wt = torch.empty(max(total, 1), dtype=torch.float32, device=dev)
+    if total:
+        _lib.call("tgs_blend_records", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+                  ctypes.byref(c_cam), ctypes.byref(c_set), _lib.ptr(offsets), _lib.ptr(g), _lib.ptr(wt),
+                  _lib.stream_handle(dev))
+    g, wt, cnt, off = g.cpu().numpy(), wt.cpu().numpy(), flat.cpu().numpy(), offsets.cpu().numpy()
+    return [[(int(g[o + k]), float(wt[o + k])) for k in range(c)] for o, c in zip(off, cnt)]
+
+
+def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
+                    grads: CloudGrads | None = None, accumulate: bool = False) -> CloudGrads:
+    """Analytic gradients of sum(dimage * image) w.r.t. every cloud field (rasterizer.py:326-419)."""
+    import ctypes
+    if output is None or output.transmittance is None or output.last_pos is None:
+        raise ContractViolationError("render_backward needs the forward pass auxiliaries")
+    h, w = int(cam.height), int(cam.width)
+    if tuple(dimage.shape) != (h, w, 3):
+        raise ContractViolationError("upstream gradient shape does not match the camera")
+    cloud = _as_cloud(cloud)
+    n = len(cloud)
+    dev = cloud.device
+    c_set = _lib.make_settings(settings)
+    if grads is None:
+        grads = CloudGrads(n, dev, zero=not accumulate and n == 0)
+        accumulate = False
+    if n == 0:
+        return grads
+    st = output._state
+    if st is None or st.n != n or st.cloud_ptr != cloud.flat.data_ptr():
+        # no reusable device state: recompute the forward products (rasterizer.py:342)
+        splats, vis, tiles, keys, err = preprocess(cloud, cam, settings)
+        rb, re = (0, _tiles_y(cam, settings.tile_size))
+        bins = _bin(splats, tiles, n, w, h, int(settings.tile_size), rb, re, err, keys)
+        st = _DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins)
+    bins = st.bins
+    rb = bins.row_begin
+    re = bins.row_end if bins.row_end is not None else _tiles_y(cam, settings.tile_size)
+    d = dimage if torch.is_tensor(dimage) else torch.from_numpy(np.ascontiguousarray(dimage, dtype=np.float32))
+    d = d.to(dev, torch.float32).contiguous()
+    transmit = output.transmittance.to(dev, torch.float32).contiguous()
+    last_pos = output.last_pos.to(dev, torch.int32).contiguous()
+    dsplats = torch.zeros((n, 9), dtype=torch.float32, device=dev)
+    c_cam = _lib.make_camera(cam)
+    s = _lib.stream_handle(dev)
+    with stage("blend_bwd"):
+        _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+                  ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
+                  _lib.ptr(d), _lib.ptr(dsplats), s)
+    c_cloud, c_grads = cloud.native(), grads.native()
+    with stage("preprocess_bwd"):
+        _lib.call("tgs_preprocess_backward", ctypes.byref(c_cloud), ctypes.byref(c_cam), ctypes.byref(c_set),
+                  _lib.ptr(st.visible_u8), _lib.ptr(dsplats), ctypes.byref(c_grads), int(bool(accumulate)), s)
+    return grads

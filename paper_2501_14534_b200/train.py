@@ -1,0 +1,83 @@
+"""Multi-view training step over the CUDA rasterizer (the hot path's caller).
+
+Restates the per-step body of the reference's `train_step` (training.py:248-366)
+for a BATCH of views, which is how BASELINE.json config 3 defines the step:
+
+    for each view of this rank:  render_forward -> L1 + D-SSIM loss -> render_backward
+                                 (gradients accumulated into one flat buffer)
+    mask-penalty gradients       (masking.py:60-67, training.py:310-311)
+    NCCL all-reduce(sum) of the flat gradient buffer       (data parallel, N > 1)
+    Adam over the 8 parameter groups                        (training.py:314-331)
+
+The batch gradient is the sum of per-view reference gradients (SURVEY.md
+§8(d): "define batch gradient = sum of per-view reference gradients"), so the
+all-reduced result is independent of how views are sharded over ranks.
+Densification/pruning events are not part of the timed step (they are
+scheduled events).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import loss as loss_mod
+from .cloud import CloudGrads, GaussianCloud
+from .optim import Adam
+from .profiler import stage
+from .rasterizer import RenderSettings, render_backward, render_forward
+
+# reference defaults (config.py:76-92 OptimConfig; config.py:67-73 MaskConfig)
+DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opacity_logits": 0.05,
+               "sh_dc": 2.5e-3, "sh_rest": 2.5e-3 / 20.0, "mask_logits": 0.5, "sh_mask_logits": 0.05}
+
+
+class Trainer:
+    def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
+                 lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
+                 views=None):
+        self.cloud = cloud
+        self.cameras = cameras
+        self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
+        self.views = list(range(len(cameras))) if views is None else list(views)
+        self.settings = settings
+        self.lambda_ssim = lambda_ssim
+        self.lambda_m, self.lambda_sh = lambda_m, lambda_sh
+        self.pg = process_group
+        self.rank = 0
+        if process_group is not None:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(process_group)
+        self.grads = CloudGrads(len(cloud), cloud.device)
+        self.opt = Adam(cloud, lrs or DEFAULT_LRS)
+        dev = cloud.device
+        self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
+        self.dimage = {}
+        self.launches_per_step = 0
+
+    def step(self) -> torch.Tensor:
+        """One optimisation step over this rank's views; returns the device loss terms."""
+        g = self.grads
+        g.flat.zero_()
+        for v in self.views:
+            cam, target = self.cameras[v], self.targets[v]
+            out = render_forward(self.cloud, cam, self.settings)
+            d = self.dimage.get((cam.height, cam.width))
+            if d is None:
+                d = self.dimage[(cam.height, cam.width)] = torch.empty_like(out.image)
+            with stage("loss"):
+                loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
+            render_backward(self.cloud, cam, self.settings, d, out, grads=g, accumulate=True)
+        if self.pg is None or self.rank == 0:
+            with stage("mask_loss"):
+                # mask penalties of total_loss (masking.py:60-67), once per optimisation
+                # step (rank 0 only, so the all-reduce does not multiply them)
+                _, _, dm, dsh = loss_mod.mask_terms(self.cloud.mask_logits, self.cloud.sh_mask_logits)
+                g.mask_logits.add_(dm, alpha=self.lambda_m)
+                g.sh_mask_logits.add_(dsh, alpha=self.lambda_sh)
+        if self.pg is not None:
+            import torch.distributed as dist
+            with stage("allreduce"):
+                dist.all_reduce(g.flat, group=self.pg)
+        with stage("adam"):
+            self.opt.step(self.cloud, g)
+        return self.terms

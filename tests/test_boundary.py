@@ -1,0 +1,101 @@
+"""The C-ABI boundary and host-side logic (CPU only, no GPU calls)."""
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tgs.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^TGS_API [^;]*?\b(tgs_\w+)\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2501_14534_b200 import _lib
+    assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build() first"
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    # every declared entry point has a ctypes signature in the binding and vice versa
+    assert set(names) - {"tgs_last_error_string"} == set(_lib._SIGS)
+    lib.tgs_version.restype = ctypes.c_int
+    assert lib.tgs_version() == 1
+    lib.tgs_last_error_string.restype = ctypes.c_char_p
+    assert lib.tgs_last_error_string(2) == b"quaternion with (near-)zero norm"
+
+
+def test_workspace_queries_need_no_gpu():
+    from paper_2501_14534_b200 import _lib
+    lib = _lib.load()
+    nb = ctypes.c_size_t(0)
+    assert lib.tgs_bin_gaussians_workspace(1_000_000, ctypes.byref(nb)) == 0 and nb.value > 28_000_000
+    assert lib.tgs_bin_instances_workspace(1_000_000, 27_000_000, ctypes.byref(nb)) == 0 and nb.value > 3 * 4 * 27e6
+    assert lib.tgs_loss_workspace(1920, 1080, ctypes.byref(nb)) == 0 and nb.value == 1920 * 1080 * 33 * 4
+    assert lib.tgs_bin_gaussians_workspace(-1, ctypes.byref(nb)) == 1
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2501_14534_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", text, flags=re.M), f
+                assert "liboracle" not in text, f
+
+
+def test_logit_thresholds_match_sigmoid_comparison():
+    """m > logit_floor_f32(eps) <=> sigmoid(m) > eps for float32 m (masking.py:21-25)."""
+    from paper_2501_14534_b200._lib import logit_ceil_f32, logit_floor_f32
+    rng = np.random.default_rng(0)
+    for eps in (0.01, 0.05, 0.1, 0.3, 0.85, 1.0 / 255.0):
+        L = math.log(eps / (1 - eps))
+        m = np.concatenate([rng.normal(L, 1.0, 20000), np.float32(L) + np.arange(-50, 50) * np.spacing(np.float32(L))])
+        m = m.astype(np.float32)
+        s = 1.0 / (1.0 + np.exp(-m.astype(np.float64)))
+        assert np.array_equal(m > np.float32(logit_floor_f32(eps)), s > eps)
+        assert np.array_equal(m >= np.float32(logit_ceil_f32(eps)), s >= eps)
+
+
+def test_settings_validation_raises_reference_errors():
+    from paper_2501_14534_b200 import ContractViolationError, RenderSettings, sh_rest_update_step
+    from paper_2501_14534_b200._lib import make_settings
+    make_settings(RenderSettings())
+    for bad in (dict(mask_threshold=0.0), dict(sh_mask_threshold=1.0), dict(lowpass_s=-0.1),
+                dict(active_sh_degree=4), dict(tile_size=0)):
+        with pytest.raises(ContractViolationError):
+            make_settings(RenderSettings(**bad))
+    assert sh_rest_update_step(16, 16) and not sh_rest_update_step(17, 16) and sh_rest_update_step(0, 16)
+    with pytest.raises(ContractViolationError):
+        sh_rest_update_step(3, 0)
+
+
+def test_camera_contract():
+    from paper_2501_14534_b200 import Camera, ContractViolationError, look_at
+    R, t = look_at(np.array([0.0, -3.5, 1.0]), np.zeros(3))
+    cam = Camera(40.0, 42.0, 15.5, 15.5, R, t, 32, 32)
+    np.testing.assert_allclose(cam.center, [0.0, -3.5, 1.0], atol=1e-12)
+    half = cam.resized(16, 16)
+    assert half.fx == 20.0 and half.cx == (15.5 + 0.5) * 0.5 - 0.5
+    with pytest.raises(ContractViolationError):
+        Camera(1, 1, 0, 0, 2 * np.eye(3), np.zeros(3), 4, 4)
+    nf = cam.native_fields()
+    assert nf["center"] == [float(np.float32(v)) for v in cam.center]
+
+
+def test_scene_generators_are_deterministic():
+    from paper_2501_14534_b200 import scenes
+    a, b = scenes.config1(), scenes.config1()
+    for f in scenes.PARAM_FIELDS:
+        assert a.fields[f].dtype == np.float32 and np.array_equal(a.fields[f], b.fields[f])
+    assert np.allclose(np.linalg.norm(a.fields["rotations"], axis=1), 1.0, atol=1e-6)
+    assert np.linalg.norm(a.fields["positions"], axis=1).max() <= 2.0 + 1e-5

@@ -114,3 +114,11 @@ def test_bin_tiles_on_raw_arrays_matches_reference():
         off, ids, _, _ = oracle.bin_tiles(sp, tiles, w, h, 16, "f64")
         assert np.array_equal(off, z[f"{pre}offsets"])
         assert np.array_equal(ids, z[f"{pre}indices"])
+
+
+def test_loss_restatement_matches_reference():
+    from oracle import loss_ref
+    z = dict(np.load(f"{golden_io.GOLDEN}/loss.npz"))
+    l1, dssim, d = loss_ref.total_loss_image(z["image"], z["target"], float(z["lambda_ssim"]))
+    assert abs(l1 - float(z["l1"])) < 1e-12 and abs(dssim - float(z["d_ssim"])) < 1e-12
+    np.testing.assert_allclose(d, z["dimage"], rtol=1e-9, atol=1e-15)
