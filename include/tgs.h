@@ -163,6 +163,10 @@ TGS_API int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched,
                       int64_t n, int32_t width,
                       int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
                       void *workspace, int64_t *d_num_instances, tgs_stream_t stream);
+/* Instances per tile row (row_counts: tiles_y int64, accumulated): the replicated
+ * histogram from which every rank derives the same balanced tile-row bands. */
+TGS_API int tgs_row_histogram(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
+                              int32_t height, int32_t tile_size, int64_t *row_counts, tgs_stream_t stream);
 TGS_API int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes);
 TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
                       int32_t row_begin, int32_t row_end, void *gauss_workspace, int64_t num_instances,

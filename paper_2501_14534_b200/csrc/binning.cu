@@ -387,6 +387,25 @@ __global__ void k_ranges(const uint32_t *__restrict__ keys, int64_t count, uint3
     for (int64_t t = (int64_t)k + 1; t <= (int64_t)ntiles; ++t) offsets[t] = (int32_t)count;
 }
 
+__global__ void k_row_hist(const float *__restrict__ splats, const int32_t *__restrict__ tiles_touched, int64_t n,
+                           Band b, unsigned long long *__restrict__ rows) {
+  extern __shared__ unsigned long long sh[];
+  const bool use_sh = b.tiles_y <= 2048;
+  if (use_sh)
+    for (int r = threadIdx.x; r < b.tiles_y; r += blockDim.x) sh[r] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && tiles_touched[i] > 0) {
+    int x0, y0, x1, y1;
+    if (band_rect(splats + 12 * i, b, x0, y0, x1, y1) > 0)
+      for (int y = y0; y <= y1; ++y) atomicAdd(use_sh ? &sh[y] : &rows[y], (unsigned long long)(x1 - x0 + 1));
+  }
+  __syncthreads();
+  if (use_sh)
+    for (int r = threadIdx.x; r < b.tiles_y; r += blockDim.x)
+      if (sh[r]) atomicAdd(&rows[r], sh[r]);
+}
+
 __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) p[j] = v;
@@ -537,5 +556,17 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   }
   k_ranges<<<(unsigned)ceil_div<int64_t>(num_instances, 256), 256, 0, st>>>(kin, num_instances, ntiles,
                                                                            tile_offsets);
+  return launch_status();
+}
+
+extern "C" int tgs_row_histogram(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
+                                 int32_t height, int32_t tile_size, int64_t *row_counts, tgs_stream_t stream) {
+  Band b;
+  if (n < 0 || !row_counts) return TGS_ERR_INVALID;
+  if (!band_ok(width, height, tile_size, 0, (height + tile_size - 1) / tile_size, b)) return TGS_ERR_INVALID;
+  if (n == 0) return TGS_OK;
+  const size_t sh = b.tiles_y <= 2048 ? (size_t)b.tiles_y * 8 : 0;
+  k_row_hist<<<(unsigned)ceil_div<int64_t>(n, 256), 256, sh, as_stream(stream)>>>(
+      splats, tiles_touched, n, b, reinterpret_cast<unsigned long long *>(row_counts));
   return launch_status();
 }

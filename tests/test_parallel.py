@@ -1,0 +1,100 @@
+"""Multi-process host logic of parallel.py under gloo (world_size 2, CPU only).
+
+The CUDA kernels cannot run here, so the per-rank compute is the oracle; what
+is under test is the partitioning: the balanced tile-row split, the row-band
+all-gather, the view sharding and the gradient all-reduce.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2501_14534_b200 import parallel
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_row_split_is_balanced_and_covering():
+    rng = np.random.default_rng(0)
+    for rows in (1, 2, 7, 68, 135):
+        counts = rng.integers(0, 5000, rows)
+        for world in (1, 2, 3, 4, 8):
+            bands = parallel.row_split(counts, world)
+            assert bands[0][0] == 0 and bands[-1][1] == rows
+            assert all(b[1] == c[0] for b, c in zip(bands, bands[1:]))
+            assert all(e > b for b, e in bands)
+            assert len(bands) == min(world, rows)
+            loads = [counts[b:e].sum() for b, e in bands]
+            assert max(loads) <= counts.sum() / len(bands) + counts.max() + 1
+    assert parallel.shard_views(8, 1, 3) == [1, 4, 7]
+
+
+def _scene():
+    from paper_2501_14534_b200 import scenes
+    sc = scenes.small_scene(seed=9, n=600, width=80, height=64, dist=3.0)
+    cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * d, 80, 64) for d in
+                              (np.array([1.0, 0.2, 0.3]), np.array([-0.4, 1.0, 0.2]), np.array([0.1, -0.3, 1.0]))]
+    return sc.fields, cams
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        fields, cams = _scene()
+        st = oracle.default_settings(near=0.2)
+        # --- render: tile-row sharding, assembled with gather_rows
+        ref = oracle.render_forward(fields, cams[0], st, "f32")
+        ty, tx = ref["tiles_y"], ref["tiles_x"]
+        row_counts = np.diff(ref["offsets"]).reshape(ty, tx).sum(axis=1)
+        bands = parallel.row_split(row_counts, world)
+        b, e = bands[rank]
+        mine = torch.zeros((64, 80, 3))
+        mine[b * 16:min(e * 16, 64)] = torch.from_numpy(ref["image"][b * 16:min(e * 16, 64)])
+        full = parallel.gather_rows(mine, bands, rank, 16, 64)
+        ok_render = torch.equal(full, torch.from_numpy(ref["image"]))
+        # --- training: view sharding + flat-buffer all-reduce == sum over all views
+        rng = np.random.default_rng(1)
+        dimgs = [rng.standard_normal((64, 80, 3)) for _ in cams]
+
+        def view_grad(v):
+            f = oracle.render_forward(fields, cams[v], st, "f64")
+            g = oracle.render_backward(fields, cams[v], st, dimgs[v], f, "f64")
+            return np.concatenate([g[k].ravel() for k in oracle.FIELDS])
+
+        local = sum(view_grad(v) for v in parallel.shard_views(len(cams), rank, world))
+        flat = torch.from_numpy(np.asarray(local, dtype=np.float64))
+        parallel.allreduce_grads(flat)
+        want = sum(view_grad(v) for v in range(len(cams)))
+        ok_grads = np.allclose(flat.numpy(), want, rtol=1e-12, atol=1e-12)
+        q.put((rank, bool(ok_render), bool(ok_grads)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_gloo_world2_sharded_render_and_dp_grads():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1]
+    assert all(r[1] for r in res), res
+    assert all(r[2] for r in res), res
