@@ -45,20 +45,69 @@ __device__ __forceinline__ float blend_exponent(float ca, float cb, float cc, fl
 
 __device__ __forceinline__ float blend_gauss(float e) { return ex2_approx(__fmul_rn(e, 1.44269504088896341f)); }
 
-__global__ void k_blend_fwd(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
-                            const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x, int row_begin,
-                            float bg0, float bg1, float bg2, float *__restrict__ image, float *__restrict__ transmit,
-                            float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
-                            int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
-  __shared__ float4 sm[kBatch * 3];
+// Pixel owned by thread t of a tile.  For 16x16 tiles each warp owns an 8x4
+// pixel block (compact footprints: a splat touches fewer warps than with 16x2
+// rows); other tile sizes use row-major order.
+__device__ __forceinline__ void pixel_of(int t, int ts, int &lx, int &ly) {
+  if (ts == 16) {
+    const int w = t >> 5, l = t & 31;
+    lx = ((w & 1) << 3) | (l & 7);
+    ly = ((w >> 1) << 2) | (l >> 3);
+  } else {
+    lx = t % ts;
+    ly = t / ts;
+  }
+}
+
+// Axis-aligned box of the pixels a staged splat can blend into: e >= -emax with
+// emax = min(4.5, ln(255 alpha)) (a = alpha exp(e) >= 1/255 and e >= -4.5), i.e.
+// Q = d^T conic d <= 2 emax, whose extent is sqrt(2 emax (conic^-1)_xx), ...  The
+// margins make it conservative under float32 rounding, so culling a warp whose
+// pixel block misses the box never changes a result.
+__device__ __forceinline__ float4 splat_box(float4 a, float4 b) {
+  const float ca = a.z, cb = a.w, cc = b.x;
+  const float det = ca * cc - cb * cb;
+  const float emax = fminf(4.5f, __logf(255.0f * b.y)) + 0.05f;
+  if (!(det > 0.0f)) return make_float4(-1e30f, 1e30f, -1e30f, 1e30f);
+  if (emax < 0.0f) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);
+  const float q = 2.0f * emax / det;
+  const float hx = sqrtf(q * cc) * 1.001f + 0.01f, hy = sqrtf(q * ca) * 1.001f + 0.01f;
+  return make_float4(a.x - hx, a.x + hx, a.y - hy, a.y + hy);
+}
+
+// Bounds of the pixels this warp owns (empty when none is inside the image).
+__device__ __forceinline__ float4 warp_bounds(bool inside, int px, int py) {
+  const int x0 = __reduce_min_sync(0xffffffffu, inside ? px : 0x7fffffff);
+  const int x1 = __reduce_max_sync(0xffffffffu, inside ? px : -0x7fffffff);
+  const int y0 = __reduce_min_sync(0xffffffffu, inside ? py : 0x7fffffff);
+  const int y1 = __reduce_max_sync(0xffffffffu, inside ? py : -0x7fffffff);
+  return make_float4((float)x0, (float)x1, (float)y0, (float)y1);
+}
+
+__device__ __forceinline__ bool box_misses(float4 bx, float4 wb) {
+  return bx.y < wb.x || bx.x > wb.y || bx.w < wb.z || bx.z > wb.w;
+}
+
+__global__ void __launch_bounds__(256) k_blend_fwd(const float4 *__restrict__ splats,
+                                                   const int32_t *__restrict__ offsets,
+                                                   const int32_t *__restrict__ ids, int W, int H, int ts,
+                                                   int tiles_x, int row_begin, float bg0, float bg1, float bg2,
+                                                   float *__restrict__ image, float *__restrict__ transmit,
+                                                   float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
+                                                   int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
+  __shared__ float4 sA[kBatch], sB[kBatch], sBox[kBatch];
+  __shared__ float sC[kBatch];
   __shared__ int32_t sid[kBatch];
   const int B = blockDim.x;
   const int batch = B < kBatch ? B : kBatch;
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x;
-  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  int lx, ly;
+  pixel_of(t, ts, lx, ly);
+  const int px = tx * ts + lx, py = ty * ts + ly;
   const bool inside = t < ts * ts && px < W && py < H;
+  const float4 wb = warp_bounds(inside, px, py);
   const int start = offsets[tile], stop = offsets[tile + 1];
   const float fpx = (float)px, fpy = (float)py;
   float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, ws = 0.0f;
@@ -68,31 +117,33 @@ __global__ void k_blend_fwd(const float4 *__restrict__ splats, const int32_t *__
     if (__syncthreads_count(done) == B) break;
     if (t < batch && base + t < stop) {
       const int g = ids[base + t];
-      sm[3 * t] = splats[3 * g];
-      sm[3 * t + 1] = splats[3 * g + 1];
-      sm[3 * t + 2] = splats[3 * g + 2];
+      const float4 a = splats[3 * g], b = splats[3 * g + 1];
+      sA[t] = a;
+      sB[t] = b;
+      sC[t] = splats[3 * g + 2].x;
+      sBox[t] = splat_box(a, b);
       sid[t] = g;
     }
     __syncthreads();
     const int cnt = min(batch, stop - base);
     if (!done) {
       for (int k = 0; k < cnt; ++k) {
+        if (box_misses(sBox[k], wb)) continue;  // warp-uniform
         if (T < kTTerm) {
           done = true;
           break;
         }
-        const float4 a = sm[3 * k];
-        const float4 b = sm[3 * k + 1];
+        const float4 a = sA[k];
+        const float4 b = sB[k];
         const float e = blend_exponent(a.z, a.w, b.x, fpx - a.x, fpy - a.y);
         if (e < kEMin || e > 0.0f) continue;
         float al = __fmul_rn(b.y, blend_gauss(e));
         if (al < kAlphaSkip) continue;
         al = fminf(al, kAlphaMax);
-        const float c2v = sm[3 * k + 2].x;
         const float w = al * T;
         c0 += b.z * w;
         c1 += b.w * w;
-        c2 += c2v * w;
+        c2 += sC[k] * w;
         ws += w;
         T = __fmul_rn(T, __fsub_rn(1.0f, al));
         ++contrib;
@@ -114,12 +165,39 @@ __global__ void k_blend_fwd(const float4 *__restrict__ splats, const int32_t *__
   }
 }
 
-__global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
-                            const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x, int row_begin,
-                            float bg0, float bg1, float bg2, const float *__restrict__ transmit,
-                            const int32_t *__restrict__ last_pos, const float *__restrict__ dimage,
-                            float *__restrict__ dsplats) {
-  __shared__ float4 sm[kBatch * 3];
+// Sum v[0..7] over the warp with a transposing butterfly (9 shuffles): on return
+// lane l holds the warp total of value (l >> 2) & 7.
+__device__ __forceinline__ float warp_reduce8_transpose(const float v[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float k4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? v[i] : v[4 + i];
+    const float keep = b4 ? v[4 + i] : v[i];
+    k4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float k2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b3 ? k4[i] : k4[2 + i];
+    const float keep = b3 ? k4[2 + i] : k4[i];
+    k2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float k1 = (b2 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? k2[0] : k2[1], 4);
+  k1 += __shfl_xor_sync(0xffffffffu, k1, 2);
+  k1 += __shfl_xor_sync(0xffffffffu, k1, 1);
+  return k1;
+}
+
+__global__ void __launch_bounds__(256) k_blend_bwd(const float4 *__restrict__ splats,
+                                                   const int32_t *__restrict__ offsets,
+                                                   const int32_t *__restrict__ ids, int W, int H, int ts,
+                                                   int tiles_x, int row_begin, float bg0, float bg1, float bg2,
+                                                   const float *__restrict__ transmit,
+                                                   const int32_t *__restrict__ last_pos,
+                                                   const float *__restrict__ dimage, float *__restrict__ dsplats) {
+  __shared__ float4 sA[kBatch], sB[kBatch], sBox[kBatch];
+  __shared__ float sC[kBatch];
   __shared__ int32_t sid[kBatch];
   __shared__ float acc[9][kBatch];
   __shared__ int wmax[32];
@@ -128,7 +206,9 @@ __global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  int lx, ly;
+  pixel_of(t, ts, lx, ly);
+  const int px = tx * ts + lx, py = ty * ts + ly;
   const bool inside = t < ts * ts && px < W && py < H;
   const int start = offsets[tile];
   const float fpx = (float)px, fpy = (float)py;
@@ -143,6 +223,8 @@ __global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__
     if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) lastp = 0;  // _kernels.py:133-134
     T_after = transmit[p];
   }
+  // warps whose pixels all skip (lastp == 0) cull every splat
+  const float4 wb = warp_bounds(lastp > 0, px, py);
   float s0 = bg0 * T_after, s1 = bg1 * T_after, s2 = bg2 * T_after;
   // longest list prefix any pixel of the tile needs
   int m = __reduce_max_sync(0xffffffffu, lastp);
@@ -161,22 +243,25 @@ __global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__
     __syncthreads();
     if (t < cnt) {
       const int g = ids[start + lo + t];
-      sm[3 * t] = splats[3 * g];
-      sm[3 * t + 1] = splats[3 * g + 1];
-      sm[3 * t + 2] = splats[3 * g + 2];
+      const float4 a = splats[3 * g], b = splats[3 * g + 1];
+      sA[t] = a;
+      sB[t] = b;
+      sC[t] = splats[3 * g + 2].x;
+      sBox[t] = splat_box(a, b);
       sid[t] = g;
 #pragma unroll
       for (int f = 0; f < 9; ++f) acc[f][t] = 0.0f;
     }
     __syncthreads();
     for (int q = cnt - 1; q >= 0; --q) {
+      if (box_misses(sBox[q], wb)) continue;  // warp-uniform
       float v[9];
 #pragma unroll
       for (int f = 0; f < 9; ++f) v[f] = 0.0f;
       bool hit = false;
       if (lo + q < lastp) {
-        const float4 a = sm[3 * q];
-        const float4 b = sm[3 * q + 1];
+        const float4 a = sA[q];
+        const float4 b = sB[q];
         const float dx = fpx - a.x, dy = fpy - a.y;
         const float e = blend_exponent(a.z, a.w, b.x, dx, dy);
         if (!(e < kEMin || e > 0.0f)) {
@@ -185,7 +270,7 @@ __global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__
           const float al = fminf(a_raw, kAlphaMax);
           if (al >= kAlphaSkip) {
             hit = true;
-            const float cz = sm[3 * q + 2].x;
+            const float cz = sC[q];
             const float inv_om = 1.0f / (1.0f - al);
             const float t_before = T_after * inv_om;
             const float ga = g0 * (b.z * t_before - s0 * inv_om) + g1 * (b.w * t_before - s1 * inv_om) +
@@ -212,18 +297,12 @@ __global__ void k_blend_bwd(const float4 *__restrict__ splats, const int32_t *__
         }
       }
       if (__any_sync(0xffffffffu, hit)) {
+        const float r8 = warp_reduce8_transpose(v, lane);
+        float r9 = v[8];
 #pragma unroll
-        for (int f = 0; f < 9; ++f) {
-          float x = v[f];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          v[f] = x;
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int f = 0; f < 9; ++f)
-            if (v[f] != 0.0f) atomicAdd(&acc[f][q], v[f]);
-        }
+        for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+        if ((lane & 3) == 0 && r8 != 0.0f) atomicAdd(&acc[lane >> 2][q], r8);
+        if (lane == 0 && r9 != 0.0f) atomicAdd(&acc[8][q], r9);
       }
     }
     __syncthreads();

@@ -52,6 +52,7 @@ __device__ __forceinline__ void stage_rest(const float *__restrict__ rest, int64
 
 // Forward quantities of Gaussian i in the documented float32 order.  `rest`
 // points at this Gaussian's 45 staged coefficients (may be null when degree 0).
+template <int DEG>
 __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
                                               const tgs_settings &s, const float *rest, GaussFwd &f) {
   // hard masks in logit space (masking.py:21-25; see tgs.h)
@@ -139,21 +140,22 @@ __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, co
   f.dir[1] = d1 / f.dnorm;
   f.dir[2] = d2 / f.dnorm;
   // SH colour (sh.py:135-161): C0*dc + 0.5 + sum_k Y_{k+1} * rest_k * bandmask_k, clamped at 0
-  const int deg = s.active_sh_degree;
-  const int K = (deg + 1) * (deg + 1) - 1;
+  constexpr int K = (DEG + 1) * (DEG + 1) - 1;
   float b[15];
   sh_basis_rest(f.dir[0], f.dir[1], f.dir[2], b);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     float acc = 0.0f;
+#pragma unroll
     for (int k = 0; k < K; ++k) acc = acc + b[k] * (rest[3 * k + c] * f.band[band_of(k)]);
     float col = SH_C0 * cl.sh_dc[3 * i + c] + 0.5f;
-    if (deg > 0) col = col + acc;
+    if (DEG > 0) col = col + acc;
     f.pre[c] = col;
     f.col[c] = max0(col);
   }
 }
 
+template <int DEG>
 __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd(tgs_cloud cl, tgs_camera cam, tgs_settings s,
                                                               float *__restrict__ splats,
                                                               uint8_t *__restrict__ visible,
@@ -163,12 +165,12 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd(tgs_cloud cl, tgs_
   __shared__ __align__(16) float rest_s[kPreBlock * 45];
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
-  if (s.active_sh_degree > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
   __syncthreads();
   if ((int)threadIdx.x >= count) return;
   const int64_t i = base + threadIdx.x;
   GaussFwd f;
-  gauss_forward(cl, i, cam, s, rest_s + 45 * threadIdx.x, f);
+  gauss_forward<DEG>(cl, i, cam, s, rest_s + 45 * threadIdx.x, f);
   if (f.degenerate) atomicOr(err, 1);
   float4 *o = reinterpret_cast<float4 *>(splats + 12 * i);
   int nt = 0;
@@ -212,14 +214,14 @@ __device__ __forceinline__ void put(float *p, float v) {
   if (kAcc) *p += v; else *p = v;
 }
 
-template <bool kAcc>
+template <int DEG, bool kAcc>
 __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_camera cam, tgs_settings s,
                                                               const uint8_t *__restrict__ visible,
                                                               const float *__restrict__ dsplats, tgs_grads g) {
   __shared__ __align__(16) float rest_s[kPreBlock * 45];
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
-  const int deg = s.active_sh_degree;
+  constexpr int deg = DEG;
   const bool rest_grads = deg > 0 && s.compute_sh_rest_grads;
   if (deg > 0) stage_rest(cl.sh_rest, base, count, rest_s);
   __syncthreads();
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
   float *my_rest = rest_s + 45 * threadIdx.x;
   if (live) {
     GaussFwd f;
-    gauss_forward(cl, i, cam, s, my_rest, f);
+    gauss_forward<DEG>(cl, i, cam, s, my_rest, f);
     const bool vis = visible[i] != 0;
     float dm0 = 0.f, dm1 = 0.f, g00 = 0.f, g01 = 0.f, g11 = 0.f, da = 0.f, dcol[3] = {0.f, 0.f, 0.f};
     if (vis) {
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
       dcol[0] = d[6]; dcol[1] = d[7]; dcol[2] = d[8];
     }
     // ---- colour path (sh.py:164-215) ----
-    const int K = (deg + 1) * (deg + 1) - 1;
+    constexpr int K = (DEG + 1) * (DEG + 1) - 1;
     float dcolor[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) dcolor[c] = f.pre[c] > 0.0f ? dcol[c] : 0.0f;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
       float b[15], bg[15][3];
       sh_basis_rest(f.dir[0], f.dir[1], f.dir[2], b);
       sh_basis_rest_grad(f.dir[0], f.dir[1], f.dir[2], bg);
+#pragma unroll
       for (int k = 0; k < K; ++k) {
         const float mb = f.band[band_of(k)];
         float mr[3];
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
           for (int c = 0; c < 3; ++c) d_dirs[dd] += bg[k][dd] * mr[c] * dcolor[c];
       }
       if (rest_grads) {
+#pragma unroll
         for (int k = 0; k < K; ++k) {
           const float mb = f.band[band_of(k)];
           float pc = 0.0f;
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
           }
           d_band[band_of(k)] += pc;
         }
+#pragma unroll
         for (int k = 3 * K; k < 45; ++k) my_rest[k] = 0.0f;
       }
     }
@@ -396,8 +401,13 @@ extern "C" int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *
   if (cloud->n == 0) return TGS_OK;
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
-  k_preprocess_fwd<<<grid, kPreBlock, 0, as_stream(stream)>>>(*cloud, *cam, *s, splats, visible, tiles_touched,
-                                                              depth_keys, error_flag);
+  cudaStream_t st = as_stream(stream);
+  switch (s->active_sh_degree) {
+#define TGS_FWD(D) \
+  case D: k_preprocess_fwd<D><<<grid, kPreBlock, 0, st>>>(*cloud, *cam, *s, splats, visible, tiles_touched, depth_keys, error_flag); break;
+    TGS_FWD(0) TGS_FWD(1) TGS_FWD(2) TGS_FWD(3)
+#undef TGS_FWD
+  }
   return launch_status();
 }
 
@@ -418,9 +428,12 @@ extern "C" int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera 
   if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
   if (cloud->n == 0) return TGS_OK;
   const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
-  if (accumulate)
-    k_preprocess_bwd<true><<<grid, kPreBlock, 0, as_stream(stream)>>>(*cloud, *cam, *s, visible, dsplats, *grads);
-  else
-    k_preprocess_bwd<false><<<grid, kPreBlock, 0, as_stream(stream)>>>(*cloud, *cam, *s, visible, dsplats, *grads);
+  cudaStream_t st = as_stream(stream);
+  switch (s->active_sh_degree * 2 + (accumulate ? 1 : 0)) {
+#define TGS_BWD(D, A) \
+  case D * 2 + A: k_preprocess_bwd<D, A><<<grid, kPreBlock, 0, st>>>(*cloud, *cam, *s, visible, dsplats, *grads); break;
+    TGS_BWD(0, 0) TGS_BWD(0, 1) TGS_BWD(1, 0) TGS_BWD(1, 1) TGS_BWD(2, 0) TGS_BWD(2, 1) TGS_BWD(3, 0) TGS_BWD(3, 1)
+#undef TGS_BWD
+  }
   return launch_status();
 }
