@@ -21,9 +21,9 @@
 // with ONE global atomic per (tile, Gaussian, field) — no per-pixel global
 // atomics.
 //
-// The exponent and alpha are evaluated by blend_alpha() with explicit
-// round-to-nearest intrinsics in BOTH kernels, so the backward re-derives the
-// forward's blend decisions bit for bit (a mismatch would corrupt the
+// The exponent is evaluated by exponent2() (log2 units, pre-scaled conic) with
+// explicit round-to-nearest intrinsics in every kernel, so the backward re-derives
+// the forward's blend decisions bit for bit (a mismatch would corrupt the
 // T_before = T_after / (1 - a) recovery).
 #include "tgs_common.cuh"
 
@@ -37,13 +37,22 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// e = -0.5 (a dx^2 + c dy^2) - b dx dy with a fixed operation sequence.
-__device__ __forceinline__ float blend_exponent(float ca, float cb, float cc, float dx, float dy) {
-  const float q = __fmaf_rn(__fmul_rn(cc, dy), dy, __fmul_rn(__fmul_rn(ca, dx), dx));
-  return __fmaf_rn(-__fmul_rn(cb, dx), dy, __fmul_rn(-0.5f, q));
+constexpr float kLog2e = 1.44269504088896341f;
+constexpr float kE2Min = (float)(-4.5 * 1.44269504088896341);  // the e >= -4.5 cut in log2 units
+
+// Pre-scaled conic (A, B, C, alpha) with A = -a log2(e) / 2, B = -b log2(e),
+// C = -c log2(e) / 2, so e2 = A dx^2 + B dx dy + C dy^2 = e log2(e) and
+// exp(e) = ex2(e2).  Every blend kernel evaluates the exponent with exactly this
+// sequence, so the backward and the records kernel re-derive the forward's
+// blend decisions bit for bit.
+__device__ __forceinline__ float4 prescaled_conic(float4 a, float4 b) {
+  return make_float4(__fmul_rn(a.z, -0.5f * kLog2e), __fmul_rn(a.w, -kLog2e), __fmul_rn(b.x, -0.5f * kLog2e), b.y);
 }
 
-__device__ __forceinline__ float blend_gauss(float e) { return ex2_approx(__fmul_rn(e, 1.44269504088896341f)); }
+__device__ __forceinline__ float exponent2(float4 q, float dx, float dy) {
+  const float s = __fmaf_rn(__fmul_rn(q.z, dy), dy, __fmul_rn(__fmul_rn(q.x, dx), dx));
+  return __fmaf_rn(__fmul_rn(q.y, dx), dy, s);
+}
 
 // Pixel owned by thread t of a tile.  For 16x16 tiles each warp owns an 8x4
 // pixel block (compact footprints: a splat touches fewer warps than with 16x2
@@ -75,12 +84,12 @@ __device__ __forceinline__ float4 splat_box(float4 a, float4 b) {
   return make_float4(a.x - hx, a.x + hx, a.y - hy, a.y + hy);
 }
 
-// Bounds of the pixels this warp owns (empty when none is inside the image).
-__device__ __forceinline__ float4 warp_bounds(bool inside, int px, int py) {
-  const int x0 = __reduce_min_sync(0xffffffffu, inside ? px : 0x7fffffff);
-  const int x1 = __reduce_max_sync(0xffffffffu, inside ? px : -0x7fffffff);
-  const int y0 = __reduce_min_sync(0xffffffffu, inside ? py : 0x7fffffff);
-  const int y1 = __reduce_max_sync(0xffffffffu, inside ? py : -0x7fffffff);
+// Bounds of the pixels this warp owns (empty when `live` is false on every lane).
+__device__ __forceinline__ float4 warp_bounds(bool live, int px, int py) {
+  const int x0 = __reduce_min_sync(0xffffffffu, live ? px : 0x7fffffff);
+  const int x1 = __reduce_max_sync(0xffffffffu, live ? px : -0x7fffffff);
+  const int y0 = __reduce_min_sync(0xffffffffu, live ? py : 0x7fffffff);
+  const int y1 = __reduce_max_sync(0xffffffffu, live ? py : -0x7fffffff);
   return make_float4((float)x0, (float)x1, (float)y0, (float)y1);
 }
 
@@ -88,21 +97,41 @@ __device__ __forceinline__ bool box_misses(float4 bx, float4 wb) {
   return bx.y < wb.x || bx.x > wb.y || bx.w < wb.z || bx.z > wb.w;
 }
 
-__global__ void __launch_bounds__(256) k_blend_fwd(const float4 *__restrict__ splats,
-                                                   const int32_t *__restrict__ offsets,
-                                                   const int32_t *__restrict__ ids, int W, int H, int ts,
-                                                   int tiles_x, int row_begin, float bg0, float bg1, float bg2,
-                                                   float *__restrict__ image, float *__restrict__ transmit,
-                                                   float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
-                                                   int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
-  __shared__ float4 sA[kBatch], sB[kBatch], sBox[kBatch];
-  __shared__ float sC[kBatch];
-  __shared__ int32_t sid[kBatch];
+// Staged splat (structure of arrays in shared memory).
+struct Stage {
+  float2 xy[kBatch];
+  float4 q[kBatch];    // prescaled conic + alpha
+  float4 col[kBatch];  // r, g, b, -
+  float4 box[kBatch];
+  int32_t id[kBatch];
+};
+
+__device__ __forceinline__ void stage_splat(Stage &S, int slot, const float4 *__restrict__ splats, int g) {
+  const float4 a = splats[3 * g], b = splats[3 * g + 1];
+  const float c = splats[3 * g + 2].x;
+  S.xy[slot] = make_float2(a.x, a.y);
+  S.q[slot] = prescaled_conic(a, b);
+  S.col[slot] = make_float4(b.z, b.w, c, 0.0f);
+  S.box[slot] = splat_box(a, b);
+  S.id[slot] = g;
+}
+
+template <int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads) k_blend_fwd(const float4 *__restrict__ splats,
+                                                           const int32_t *__restrict__ offsets,
+                                                           const int32_t *__restrict__ ids, int W, int H, int ts,
+                                                           int tiles_x, int row_begin, float bg0, float bg1,
+                                                           float bg2, float *__restrict__ image,
+                                                           float *__restrict__ transmit, float *__restrict__ wsum_out,
+                                                           int32_t *__restrict__ n_contrib,
+                                                           int32_t *__restrict__ last_pos,
+                                                           int32_t *__restrict__ hits) {
+  __shared__ Stage S;
   const int B = blockDim.x;
   const int batch = B < kBatch ? B : kBatch;
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
   int lx, ly;
   pixel_of(t, ts, lx, ly);
   const int px = tx * ts + lx, py = ty * ts + ly;
@@ -115,43 +144,42 @@ __global__ void __launch_bounds__(256) k_blend_fwd(const float4 *__restrict__ sp
   bool done = !inside;
   for (int base = start; base < stop; base += batch) {
     if (__syncthreads_count(done) == B) break;
-    if (t < batch && base + t < stop) {
-      const int g = ids[base + t];
-      const float4 a = splats[3 * g], b = splats[3 * g + 1];
-      sA[t] = a;
-      sB[t] = b;
-      sC[t] = splats[3 * g + 2].x;
-      sBox[t] = splat_box(a, b);
-      sid[t] = g;
-    }
+    if (t < batch && base + t < stop) stage_splat(S, t, splats, ids[base + t]);
     __syncthreads();
     const int cnt = min(batch, stop - base);
-    if (!done) {
-      for (int k = 0; k < cnt; ++k) {
-        if (box_misses(sBox[k], wb)) continue;  // warp-uniform
-        if (T < kTTerm) {
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      if (__all_sync(0xffffffffu, done)) break;
+      // one splat per lane: the warp-level cull, then iterate the survivors in order
+      const int j = j0 + lane;
+      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && !box_misses(S.box[j], wb));
+      while (mask) {
+        const int k = j0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        if (done) continue;
+        if (T < kTTerm) {  // checked before each entry (_kernels.py:57-58)
           done = true;
-          break;
+          continue;
         }
-        const float4 a = sA[k];
-        const float4 b = sB[k];
-        const float e = blend_exponent(a.z, a.w, b.x, fpx - a.x, fpy - a.y);
-        if (e < kEMin || e > 0.0f) continue;
-        float al = __fmul_rn(b.y, blend_gauss(e));
+        const float2 m = S.xy[k];
+        const float4 q = S.q[k];
+        const float e2 = exponent2(q, fpx - m.x, fpy - m.y);
+        if (e2 < kE2Min || e2 > 0.0f) continue;
+        float al = __fmul_rn(q.w, ex2_approx(e2));
         if (al < kAlphaSkip) continue;
         al = fminf(al, kAlphaMax);
+        const float4 col = S.col[k];
         const float w = al * T;
-        c0 += b.z * w;
-        c1 += b.w * w;
-        c2 += sC[k] * w;
+        c0 += col.x * w;
+        c1 += col.y * w;
+        c2 += col.z * w;
         ws += w;
         T = __fmul_rn(T, __fsub_rn(1.0f, al));
         ++contrib;
         lastp = base - start + k + 1;
-        if (hits) atomicAdd(hits + sid[k], 1);
+        if (hits) atomicAdd(hits + S.id[k], 1);
       }
-      if (T < kTTerm) done = true;
     }
+    if (T < kTTerm) done = true;
   }
   if (inside) {
     const int p = py * W + px;
@@ -189,20 +217,37 @@ __device__ __forceinline__ float warp_reduce8_transpose(const float v[8], int la
   return k1;
 }
 
-__global__ void __launch_bounds__(256) k_blend_bwd(const float4 *__restrict__ splats,
-                                                   const int32_t *__restrict__ offsets,
-                                                   const int32_t *__restrict__ ids, int W, int H, int ts,
-                                                   int tiles_x, int row_begin, float bg0, float bg1, float bg2,
-                                                   const float *__restrict__ transmit,
-                                                   const int32_t *__restrict__ last_pos,
-                                                   const float *__restrict__ dimage, float *__restrict__ dsplats) {
-  __shared__ float4 sA[kBatch], sB[kBatch], sBox[kBatch];
-  __shared__ float sC[kBatch];
-  __shared__ int32_t sid[kBatch];
-  __shared__ float acc[9][kBatch];
+// Backward batch: 128 splats at 16x16 tiles; each warp owns a private slice of
+// the per-splat accumulators (plain stores, no shared-memory float atomics,
+// which sm_100 emulates with a CAS loop), summed over warps at the flush.
+template <int kMaxThreads>
+struct BwdShared {
+  static constexpr int kWarpsMax = kMaxThreads / 32;
+  static constexpr int kBB = kMaxThreads <= 256 ? 128 : 32;
+  float2 xy[kBB];
+  float4 q[kBB];
+  float4 conic[kBB];  // a, b, c, alpha (raw, for the partials)
+  float4 col[kBB];
+  float4 box[kBB];
+  int32_t id[kBB];
+  float acc[kWarpsMax][9][kBB];
+};
+
+template <int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restrict__ splats,
+                                                           const int32_t *__restrict__ offsets,
+                                                           const int32_t *__restrict__ ids, int W, int H, int ts,
+                                                           int tiles_x, int row_begin, float bg0, float bg1,
+                                                           float bg2, const float *__restrict__ transmit,
+                                                           const int32_t *__restrict__ last_pos,
+                                                           const float *__restrict__ dimage,
+                                                           float *__restrict__ dsplats) {
+  using SM = BwdShared<kMaxThreads>;
+  constexpr int kBB = SM::kBB;
+  __shared__ SM S;
   __shared__ int wmax[32];
   const int B = blockDim.x;
-  const int batch = B < kBatch ? B : kBatch;
+  const int nwarps = B >> 5;
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -223,94 +268,101 @@ __global__ void __launch_bounds__(256) k_blend_bwd(const float4 *__restrict__ sp
     if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) lastp = 0;  // _kernels.py:133-134
     T_after = transmit[p];
   }
-  // warps whose pixels all skip (lastp == 0) cull every splat
+  // pixels with lastp == 0 never contribute: they neither widen the warp box nor its list prefix
   const float4 wb = warp_bounds(lastp > 0, px, py);
+  const int wlast = __reduce_max_sync(0xffffffffu, lastp);
   float s0 = bg0 * T_after, s1 = bg1 * T_after, s2 = bg2 * T_after;
-  // longest list prefix any pixel of the tile needs
-  int m = __reduce_max_sync(0xffffffffu, lastp);
-  if (lane == 0) wmax[warp] = m;
+  if (lane == 0) wmax[warp] = wlast;
   __syncthreads();
   if (warp == 0) {
-    m = lane < (B + 31) / 32 ? wmax[lane] : 0;
+    int m = lane < nwarps ? wmax[lane] : 0;
     m = __reduce_max_sync(0xffffffffu, m);
     if (lane == 0) wmax[0] = m;
   }
   __syncthreads();
   const int max_last = wmax[0];
-  for (int hi = max_last; hi > 0; hi -= batch) {
-    const int lo = hi > batch ? hi - batch : 0;
+  for (int hi = max_last; hi > 0; hi -= kBB) {
+    const int lo = hi > kBB ? hi - kBB : 0;
     const int cnt = hi - lo;
     __syncthreads();
     if (t < cnt) {
       const int g = ids[start + lo + t];
       const float4 a = splats[3 * g], b = splats[3 * g + 1];
-      sA[t] = a;
-      sB[t] = b;
-      sC[t] = splats[3 * g + 2].x;
-      sBox[t] = splat_box(a, b);
-      sid[t] = g;
-#pragma unroll
-      for (int f = 0; f < 9; ++f) acc[f][t] = 0.0f;
+      S.xy[t] = make_float2(a.x, a.y);
+      S.q[t] = prescaled_conic(a, b);
+      S.conic[t] = make_float4(a.z, a.w, b.x, b.y);
+      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, 0.0f);
+      S.box[t] = splat_box(a, b);
+      S.id[t] = g;
     }
+    for (int e = t; e < nwarps * 9 * kBB; e += B) (&S.acc[0][0][0])[e] = 0.0f;
     __syncthreads();
-    for (int q = cnt - 1; q >= 0; --q) {
-      if (box_misses(sBox[q], wb)) continue;  // warp-uniform
-      float v[9];
+    // back to front over 32-splat chunks; inside a chunk the survivors high to low
+    for (int j0 = (cnt - 1) & ~31; j0 >= 0; j0 -= 32) {
+      const int j = j0 + lane;
+      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && lo + j < wlast && !box_misses(S.box[j], wb));
+      while (mask) {
+        const int bit = 31 - __clz(mask);
+        mask &= ~(1u << bit);
+        const int q = j0 + bit;
+        float v[9];
 #pragma unroll
-      for (int f = 0; f < 9; ++f) v[f] = 0.0f;
-      bool hit = false;
-      if (lo + q < lastp) {
-        const float4 a = sA[q];
-        const float4 b = sB[q];
-        const float dx = fpx - a.x, dy = fpy - a.y;
-        const float e = blend_exponent(a.z, a.w, b.x, dx, dy);
-        if (!(e < kEMin || e > 0.0f)) {
-          const float gauss = blend_gauss(e);
-          const float a_raw = __fmul_rn(b.y, gauss);
-          const float al = fminf(a_raw, kAlphaMax);
-          if (al >= kAlphaSkip) {
-            hit = true;
-            const float cz = sC[q];
-            const float inv_om = 1.0f / (1.0f - al);
-            const float t_before = T_after * inv_om;
-            const float ga = g0 * (b.z * t_before - s0 * inv_om) + g1 * (b.w * t_before - s1 * inv_om) +
-                             g2 * (cz * t_before - s2 * inv_om);
-            const float w = al * t_before;
-            v[6] = g0 * w;
-            v[7] = g1 * w;
-            v[8] = g2 * w;
-            if (a_raw <= kAlphaMax) {
-              v[5] = ga * gauss;
-              const float gG = ga * b.y * gauss;
-              const float v0 = a.z * dx + a.w * dy, v1 = a.w * dx + b.x * dy;
-              v[0] = gG * v0;
-              v[1] = gG * v1;
-              v[2] = gG * 0.5f * v0 * v0;
-              v[3] = gG * v0 * v1;
-              v[4] = gG * 0.5f * v1 * v1;
+        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+        bool hit = false;
+        if (lo + q < lastp) {
+          const float2 m = S.xy[q];
+          const float dx = fpx - m.x, dy = fpy - m.y;
+          const float e2 = exponent2(S.q[q], dx, dy);
+          if (!(e2 < kE2Min || e2 > 0.0f)) {
+            const float4 cn = S.conic[q];
+            const float gauss = ex2_approx(e2);
+            const float a_raw = __fmul_rn(cn.w, gauss);
+            const float al = fminf(a_raw, kAlphaMax);
+            if (al >= kAlphaSkip) {
+              hit = true;
+              const float4 col = S.col[q];
+              const float inv_om = 1.0f / (1.0f - al);
+              const float t_before = T_after * inv_om;
+              const float ga = g0 * (col.x * t_before - s0 * inv_om) + g1 * (col.y * t_before - s1 * inv_om) +
+                               g2 * (col.z * t_before - s2 * inv_om);
+              const float w = al * t_before;
+              v[6] = g0 * w;
+              v[7] = g1 * w;
+              v[8] = g2 * w;
+              if (a_raw <= kAlphaMax) {
+                v[5] = ga * gauss;
+                const float gG = ga * cn.w * gauss;
+                const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
+                v[0] = gG * v0;
+                v[1] = gG * v1;
+                v[2] = gG * 0.5f * v0 * v0;
+                v[3] = gG * v0 * v1;
+                v[4] = gG * 0.5f * v1 * v1;
+              }
+              s0 += col.x * w;
+              s1 += col.y * w;
+              s2 += col.z * w;
+              T_after = t_before;
             }
-            s0 += b.z * w;
-            s1 += b.w * w;
-            s2 += cz * w;
-            T_after = t_before;
           }
         }
-      }
-      if (__any_sync(0xffffffffu, hit)) {
-        const float r8 = warp_reduce8_transpose(v, lane);
-        float r9 = v[8];
+        if (__any_sync(0xffffffffu, hit)) {
+          const float r8 = warp_reduce8_transpose(v, lane);
+          float r9 = v[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
-        if ((lane & 3) == 0 && r8 != 0.0f) atomicAdd(&acc[lane >> 2][q], r8);
-        if (lane == 0 && r9 != 0.0f) atomicAdd(&acc[8][q], r9);
+          for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+          if ((lane & 3) == 0) S.acc[warp][lane >> 2][q] = r8;
+          if (lane == 0) S.acc[warp][8][q] = r9;
+        }
       }
     }
     __syncthreads();
     if (t < cnt) {
-      float *d = dsplats + 9 * (int64_t)sid[t];
+      float *d = dsplats + 9 * (int64_t)S.id[t];
 #pragma unroll
       for (int f = 0; f < 9; ++f) {
-        const float x = acc[f][t];
+        float x = 0.0f;
+        for (int w = 0; w < nwarps; ++w) x += S.acc[w][f][t];
         if (x != 0.0f) atomicAdd(d + f, x);
       }
     }
@@ -325,7 +377,9 @@ __global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t
   const int tile = blockIdx.x;
   const int ty = tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x;
-  const int px = tx * ts + t % ts, py = ty * ts + t / ts;
+  int lx, ly;
+  pixel_of(t, ts, lx, ly);
+  const int px = tx * ts + lx, py = ty * ts + ly;
   if (t >= ts * ts || px >= W || py >= H) return;
   const int start = offsets[tile], stop = offsets[tile + 1];
   int64_t pos = pix_off[py * W + px];
@@ -334,9 +388,9 @@ __global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t
     if (T < kTTerm) break;
     const int g = ids[k];
     const float4 a = splats[3 * g], b = splats[3 * g + 1];
-    const float e = blend_exponent(a.z, a.w, b.x, (float)px - a.x, (float)py - a.y);
-    if (e < kEMin || e > 0.0f) continue;
-    float al = __fmul_rn(b.y, blend_gauss(e));
+    const float e2 = exponent2(prescaled_conic(a, b), (float)px - a.x, (float)py - a.y);
+    if (e2 < kE2Min || e2 > 0.0f) continue;
+    float al = __fmul_rn(b.y, ex2_approx(e2));
     if (al < kAlphaSkip) continue;
     al = fminf(al, kAlphaMax);
     rec_g[pos] = g;
@@ -370,7 +424,7 @@ extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offset
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
-  k_blend_fwd<<<ntiles, B, 0, as_stream(stream)>>>(
+  (B <= 256 ? k_blend_fwd<256> : k_blend_fwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum,
       n_contrib, last_pos, hits);
@@ -401,7 +455,7 @@ extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offse
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
-  k_blend_bwd<<<ntiles, B, 0, as_stream(stream)>>>(
+  (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage,
       dsplats);

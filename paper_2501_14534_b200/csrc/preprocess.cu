@@ -276,14 +276,15 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
         for (int k = 3 * K; k < 45; ++k) my_rest[k] = 0.0f;
       }
     }
+    // all outputs are gathered in registers and written once at the end (one batch of
+    // independent loads for the accumulate read-modify-write)
+    float o_dc[3], o_shm[3], o_pos[3], o_ls[3], o_rot[4], o_op, o_mask, o_m2d[2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) put<kAcc>(g.sh_dc + 3 * i + c, SH_C0 * dcolor[c]);
-    if (rest_grads || !kAcc) {
+    for (int c = 0; c < 3; ++c) o_dc[c] = SH_C0 * dcolor[c];
 #pragma unroll
-      for (int l = 0; l < 3; ++l) {
-        const float sg = sem_sigmoidf(cl.sh_mask_logits[3 * i + l]);
-        put<kAcc>(g.sh_mask_logits + 3 * i + l, d_band[l] * (sg * (1.0f - sg)));
-      }
+    for (int l = 0; l < 3; ++l) {
+      const float sg = sem_sigmoidf(cl.sh_mask_logits[3 * i + l]);
+      o_shm[l] = d_band[l] * (sg * (1.0f - sg));
     }
     const float inner = d_dirs[0] * f.dir[0] + d_dirs[1] * f.dir[1] + d_dirs[2] * f.dir[2];
     float gp[3];
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
     for (int k = 0; k < 3; ++k) gp[k] = (d_dirs[k] - f.dir[k] * inner) / f.dnorm;
     // ---- opacity path (rasterizer.py:397-400) ----
     const float s_op = sem_sigmoidf(cl.opacity_logits[i]);
-    put<kAcc>(g.opacity_logits + i, vis ? da * f.Mg * s_op * (1.0f - s_op) : 0.0f);
+    o_op = vis ? da * f.Mg * s_op * (1.0f - s_op) : 0.0f;
     float dmask = vis ? da * s_op : 0.0f;
     // ---- project_backward (geometry.py:198-251) ----
     float dS[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
       for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) put<kAcc>(g.positions + 3 * i + k, gp[k]);
+    for (int k = 0; k < 3; ++k) o_pos[k] = gp[k];
     // ---- covariance_backward + quat_backward (geometry.py:44-89) ----
     float L[9], dL[9], dsc[3], dR[9];
 #pragma unroll
@@ -365,15 +366,59 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
     dqu[3] = 2.0f * (x * (dR[2] + dR[6]) + y * (dR[5] + dR[7])) + 2.0f * w * (dR[3] - dR[1]) - 4.0f * z * (dR[0] + dR[4]);
     const float qin = dqu[0] * w + dqu[1] * x + dqu[2] * y + dqu[3] * z;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) put<kAcc>(g.rotations + 4 * i + k, (dqu[k] - f.qn[k] * qin) / f.qnorm);
+    for (int k = 0; k < 4; ++k) o_rot[k] = (dqu[k] - f.qn[k] * qin) / f.qnorm;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) put<kAcc>(g.log_scales + 3 * i + k, dsc[k] * f.s_raw[k] * f.Mg);
+    for (int k = 0; k < 3; ++k) o_ls[k] = dsc[k] * f.s_raw[k] * f.Mg;
     dmask += dsc[0] * f.s_raw[0] + dsc[1] * f.s_raw[1] + dsc[2] * f.s_raw[2];
     const float sm = sem_sigmoidf(cl.mask_logits[i]);
-    put<kAcc>(g.mask_logits + i, dmask * (sm * (1.0f - sm)));
+    o_mask = dmask * (sm * (1.0f - sm));
+    o_m2d[0] = vis ? dm0 : 0.0f;
+    o_m2d[1] = vis ? dm1 : 0.0f;
+    const bool w_shm = rest_grads || !kAcc;
+    if (kAcc) {  // independent loads first, then the adds
+      float p_dc[3], p_shm[3] = {0.f, 0.f, 0.f}, p_pos[3], p_ls[3], p_rot[4], p_m2d[2] = {0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        p_dc[k] = g.sh_dc[3 * i + k];
+        p_pos[k] = g.positions[3 * i + k];
+        p_ls[k] = g.log_scales[3 * i + k];
+        if (w_shm) p_shm[k] = g.sh_mask_logits[3 * i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) p_rot[k] = g.rotations[4 * i + k];
+      const float p_op = g.opacity_logits[i], p_mask = g.mask_logits[i];
+      if (g.mean2d_screen) {
+        p_m2d[0] = g.mean2d_screen[2 * i];
+        p_m2d[1] = g.mean2d_screen[2 * i + 1];
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o_dc[k] += p_dc[k];
+        o_pos[k] += p_pos[k];
+        o_ls[k] += p_ls[k];
+        o_shm[k] += p_shm[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o_rot[k] += p_rot[k];
+      o_op += p_op;
+      o_mask += p_mask;
+      o_m2d[0] += p_m2d[0];
+      o_m2d[1] += p_m2d[1];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      g.sh_dc[3 * i + k] = o_dc[k];
+      g.positions[3 * i + k] = o_pos[k];
+      g.log_scales[3 * i + k] = o_ls[k];
+      if (w_shm) g.sh_mask_logits[3 * i + k] = o_shm[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g.rotations[4 * i + k] = o_rot[k];
+    g.opacity_logits[i] = o_op;
+    g.mask_logits[i] = o_mask;
     if (g.mean2d_screen) {
-      put<kAcc>(g.mean2d_screen + 2 * i, vis ? dm0 : 0.0f);
-      put<kAcc>(g.mean2d_screen + 2 * i + 1, vis ? dm1 : 0.0f);
+      g.mean2d_screen[2 * i] = o_m2d[0];
+      g.mean2d_screen[2 * i + 1] = o_m2d[1];
     }
   }
   // ---- sh_rest gradients: coalesced write-out of the smem block ----
