@@ -202,6 +202,15 @@ TGS_API int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *ca
                             const uint8_t *visible, const float *dsplats, tgs_grads *grads,
                             int32_t accumulate, tgs_stream_t stream);
 
+/* Multi-view form: sums the gradients of `nviews` views (cams[v], visible[v],
+ * dsplats[v]; host arrays of device pointers) in one pass over the parameters —
+ * the chains after the screen-space partials are linear, so view-independent
+ * work (covariance/quaternion/scale/opacity/mask) runs once per Gaussian. */
+TGS_API int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                          const uint8_t *const *visible, const float *const *dsplats,
+                                          int32_t nviews, tgs_grads *grads, int32_t accumulate,
+                                          tgs_stream_t stream);
+
 /* ---- (6) loss: (1-lambda)*L1 + lambda*(1-SSIM)/2, 11x11 sigma 1.5 window,
  * symmetric padding (training.py:76-89, metrics.py:138-188).  image/target
  * (H, W, 3); dimage (H, W, 3) written; terms (device float64[2]) receives

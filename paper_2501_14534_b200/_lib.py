@@ -61,6 +61,7 @@ _SIGS = {
     "tgs_blend_records": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_blend_backward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P], _I32),
     "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
+    "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P], _I32),
     "tgs_loss_workspace": ([_I32, _I32, _P], _I32),
     "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
     "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),

@@ -149,46 +149,110 @@ inline void device_scan(const uint32_t *in, uint32_t *out, uint64_t cap, const u
   k_scan_down<<<nb, kBlock, 0, st>>>(in, out, (uint32_t)cap, nd, partials);
 }
 
-// ------------------------------------------------------------ radix passes
-// Stable LSD pass over digit [shift, shift+nbits) of K-typed keys (uint32 or
-// uint64) with one uint32 payload.  IPT items per thread (tile = 256*IPT).
-template <typename K, int IPT>
-__global__ void __launch_bounds__(kBlock) k_radix_hist(const K *__restrict__ keys, uint32_t nh,
-                                                       const uint32_t *nd, int shift, int nbits,
-                                                       uint32_t *__restrict__ hist, int nblocks) {
-  constexpr int TILE = kBlock * IPT;
-  __shared__ uint32_t h[256];
-  const int bins = 1 << nbits;
-  const uint32_t mask = bins - 1;
-  for (int d = threadIdx.x; d < bins; d += kBlock) h[d] = 0;
+// ------------------------------------------------------------ radix sort
+// Onesweep-style stable LSD radix sort of (K key, u32 value) pairs:
+//   k_sweep_hist  one read of the keys -> global digit histograms of every pass
+//   k_sweep_scan  exclusive scan of each pass's 256 bins (one CTA)
+//   k_sweep_pass  per pass: tiles taken in launch order from an atomic ticket; a
+//                 tile ranks its items (warp multisplit), publishes its per-digit
+//                 counts and resolves its global offsets by decoupled look-back
+//                 over its predecessors, then scatters through shared memory in
+//                 contiguous per-digit runs.
+// A tile only ever waits for tiles with smaller tickets, which are already
+// resident, so the look-back cannot deadlock.
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+// The status word IS the payload (flag | count in one 32-bit word), so relaxed
+// GPU-scope accesses suffice: no acquire fence (which costs an L1 invalidate per
+// probe on sm_100) and no release fence.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr int kLookback = 16;  // predecessors probed per step (independent loads in flight)
+
+template <typename K>
+constexpr int ipt_for() {
+  return sizeof(K) == 8 ? 8 : kIPT;  // 64-bit keys: 2048-item tiles keep smem at 24 KB + counters
+}
+template <typename K>
+constexpr int tile_for() {
+  return kBlock * ipt_for<K>();
+}
+
+constexpr int kFullHistSmem = 8192;  // full-key histogram bins kept in shared memory
+
+// Digit histograms of every pass in one read of the keys; optionally also the
+// full-key histogram (the per-tile instance counts -> CSR offsets, replacing a
+// boundary scan over the sorted keys).
+template <typename K>
+__global__ void __launch_bounds__(kBlock) k_sweep_hist(const K *__restrict__ keys, uint32_t nh, const uint32_t *nd,
+                                                       int npasses, int bpp, int total_bits,
+                                                       uint32_t *__restrict__ gbins, uint32_t *__restrict__ full_hist,
+                                                       int full_bins) {
+  __shared__ uint32_t h[8][256];
+  __shared__ uint32_t fh[kFullHistSmem];
+  const bool fsh = full_hist && full_bins <= kFullHistSmem;
+  for (int e = threadIdx.x; e < npasses * 256; e += kBlock) (&h[0][0])[e] = 0;
+  if (fsh)
+    for (int e = threadIdx.x; e < full_bins; e += kBlock) fh[e] = 0;
   __syncthreads();
   const uint32_t n = live_count(nd, nh);
-  const uint64_t base = (uint64_t)blockIdx.x * TILE;
-  if (base < n) {
-#pragma unroll 4
-    for (int r = 0; r < IPT; ++r) {
-      const uint64_t j = base + (uint64_t)r * kBlock + threadIdx.x;
-      const bool ok = j < n;
-      const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const uint32_t d = (uint32_t)(keys[j] >> shift) & mask;
-        // warp-aggregated shared atomics: one add per distinct digit per warp
-        const uint32_t peers = __match_any_sync(okmask, d);
-        if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], (uint32_t)__popc(peers));
-      }
+  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+    const K k = keys[i];
+    for (int p = 0; p < npasses; ++p) {
+      const int sh = p * bpp;
+      const int nb = min(bpp, total_bits - sh);
+      atomicAdd(&h[p][(uint32_t)(k >> sh) & ((1u << nb) - 1)], 1u);
     }
+    if (full_hist) atomicAdd(fsh ? &fh[(uint32_t)k] : &full_hist[(uint32_t)k], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < bins; d += kBlock) hist[(size_t)d * nblocks + blockIdx.x] = h[d];
+  for (int e = threadIdx.x; e < npasses * 256; e += kBlock) {
+    const uint32_t v = (&h[0][0])[e];
+    if (v) atomicAdd(gbins + e, v);
+  }
+  if (fsh)
+    for (int e = threadIdx.x; e < full_bins; e += kBlock)
+      if (fh[e]) atomicAdd(full_hist + e, fh[e]);
+}
+
+// CSR offsets (int32, bins + 1) from the full-key histogram: one CTA, chunked scan.
+__global__ void __launch_bounds__(1024) k_offsets_from_hist(const uint32_t *__restrict__ hist, int bins,
+                                                            int32_t *__restrict__ offsets) {
+  __shared__ uint32_t ws[32];
+  uint32_t carry = 0;
+  for (int c = 0; c < bins; c += 1024) {
+    const int j = c + threadIdx.x;
+    const uint32_t v = j < bins ? hist[j] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan(v, ws, &tot);
+    if (j < bins) offsets[j] = (int32_t)(carry + ex);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) offsets[bins] = (int32_t)carry;
+}
+
+__global__ void __launch_bounds__(kBlock) k_sweep_scan(uint32_t *gbins, int npasses) {
+  __shared__ uint32_t ws[32];
+  for (int p = 0; p < npasses; ++p) {
+    const uint32_t v = gbins[p * 256 + threadIdx.x];
+    const uint32_t ex = block_exclusive_scan(v, ws, nullptr);
+    gbins[p * 256 + threadIdx.x] = ex;
+  }
 }
 
 template <typename K, int IPT>
-__global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ keys_in,
-                                                          const uint32_t *__restrict__ vals_in,
-                                                          K *__restrict__ keys_out,
-                                                          uint32_t *__restrict__ vals_out, uint32_t nh,
-                                                          const uint32_t *nd, int shift, int nbits,
-                                                          const uint32_t *__restrict__ hist_scanned, int nblocks) {
+__global__ void __launch_bounds__(kBlock) k_sweep_pass(const K *__restrict__ keys_in,
+                                                       const uint32_t *__restrict__ vals_in,
+                                                       K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                                                       uint32_t nh, const uint32_t *nd, int shift, int nbits,
+                                                       const uint32_t *__restrict__ bin_base,
+                                                       uint32_t *__restrict__ status, uint32_t *__restrict__ ticket) {
   constexpr int TILE = kBlock * IPT;
   __shared__ K ks[TILE];
   __shared__ uint32_t vs[TILE];
@@ -196,8 +260,12 @@ __global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ 
   __shared__ uint32_t dstart[256];
   __shared__ uint32_t gbase[256];
   __shared__ uint32_t wsum[32];
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
   const uint32_t n = live_count(nd, nh);
-  const uint64_t base = (uint64_t)blockIdx.x * TILE;
+  const uint64_t base = (uint64_t)tile * TILE;
   if (base >= n) return;
   const int bins = 1 << nbits;
   const uint32_t mask = bins - 1;
@@ -210,13 +278,20 @@ __global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ 
   uint16_t rank[IPT];
   const uint64_t wbase = base + (uint64_t)warp * (IPT * 32);
   // warp-synchronous multisplit: ranks are stable in index order (warp-major,
-  // then round, then lane), matching the block's item order
+  // then round, then lane), matching the tile's item order
+  // all loads first: the multisplit below synchronises the warp every round, and
+  // loads cannot be hoisted across those synchronisation points
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint64_t j = wbase + r * 32 + lane;
     const bool ok = j < n;
     key[r] = ok ? keys_in[j] : (K)0;
     val[r] = ok ? vals_in[j] : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint64_t j = wbase + r * 32 + lane;
+    const bool ok = j < n;
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
     rank[r] = 0;
     if (ok) {
@@ -230,7 +305,6 @@ __global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ 
     __syncwarp();
   }
   __syncthreads();
-  // per-digit exclusive prefix over warps, then over digits (block-local start)
   uint32_t dtotal = 0;
   if (threadIdx.x < (unsigned)bins) {
     for (int w = 0; w < kWarps; ++w) {
@@ -242,7 +316,33 @@ __global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ 
   const uint32_t ds = block_exclusive_scan(threadIdx.x < (unsigned)bins ? dtotal : 0u, wsum, nullptr);
   if (threadIdx.x < (unsigned)bins) {
     dstart[threadIdx.x] = ds;
-    gbase[threadIdx.x] = hist_scanned[(size_t)threadIdx.x * nblocks + blockIdx.x];
+    // decoupled look-back over the predecessors' per-digit counts
+    uint32_t *mine = status + (size_t)tile * 256 + threadIdx.x;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st_relaxed(mine, kFlagInc | dtotal);
+    } else {
+      st_relaxed(mine, kFlagAgg | dtotal);
+      int j = (int)tile - 1;
+      bool found = false;
+      while (!found) {
+        uint32_t v[kLookback];
+#pragma unroll
+        for (int k = 0; k < kLookback; ++k)
+          v[k] = (j - k >= 0) ? ld_relaxed(status + (size_t)(j - k) * 256 + threadIdx.x) : kFlagInc;
+        int used = 0;
+#pragma unroll
+        for (int k = 0; k < kLookback; ++k) {
+          if (found || (v[k] >> 30) == 0) break;  // stop at the first unpublished predecessor
+          excl += v[k] & kValMask;
+          found = (v[k] & kFlagInc) != 0;
+          ++used;
+        }
+        j -= found ? 0 : used;  // resume at the first predecessor not yet consumed
+      }
+      st_relaxed(mine, kFlagInc | (excl + dtotal));
+    }
+    gbase[threadIdx.x] = bin_base[threadIdx.x] + excl;
   }
   __syncthreads();
 #pragma unroll
@@ -267,32 +367,59 @@ __global__ void __launch_bounds__(kBlock) k_radix_scatter(const K *__restrict__ 
   }
 }
 
-struct RadixScratch {
-  uint32_t *hist;      // 256 * nblocks
-  uint32_t *partials;  // scan partials for hist
+struct SortScratch {
+  uint32_t *gbins;      // passes * 256
+  uint32_t *status;     // passes * tiles * 256
+  uint32_t *ticket;     // passes
+  uint32_t *full_hist;  // full_bins (optional)
+  size_t bytes_zeroed;
 };
 
 template <typename K>
-constexpr int ipt_for() {
-  return sizeof(K) == 8 ? 8 : kIPT;  // 64-bit keys: 2048-item tiles keep smem at 24 KB + counters
+inline size_t sort_ws_bytes(uint64_t cap, int passes) {
+  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
+  return align_up((size_t)passes * 256 * 4) + align_up((size_t)passes * tiles * 256 * 4) + align_up(passes * 4);
 }
 
 template <typename K>
-inline uint64_t radix_blocks(uint64_t cap) {
-  return ceil_div<uint64_t>(cap, (uint64_t)kBlock * ipt_for<K>());
+inline SortScratch carve_sort(Carve &c, uint64_t cap, int passes, size_t full_bins = 0) {
+  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
+  SortScratch s;
+  const size_t off0 = c.off;
+  s.gbins = c.take<uint32_t>((size_t)passes * 256);
+  s.status = c.take<uint32_t>((size_t)passes * tiles * 256);
+  s.ticket = c.take<uint32_t>(passes);
+  s.full_hist = full_bins ? c.take<uint32_t>(full_bins) : nullptr;
+  s.bytes_zeroed = c.off - off0;
+  return s;
 }
 
-// One stable pass over digit [shift, shift+nbits).
+// Stable sort of `cap` (or *nd) items by bits [0, total_bits) of the key, in
+// `passes` passes of <= 8 bits.  Ping-pongs A <-> B; returns true when the
+// result ended in the B buffers.
 template <typename K>
-inline void radix_pass(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, uint64_t cap, const uint32_t *nd,
-                       int shift, int nbits, RadixScratch sc, cudaStream_t st) {
-  constexpr int IPT = ipt_for<K>();
-  const int nb = (int)radix_blocks<K>(cap);
-  if (nb == 0) return;
-  k_radix_hist<K, IPT><<<nb, kBlock, 0, st>>>(kin, (uint32_t)cap, nd, shift, nbits, sc.hist, nb);
-  device_scan(sc.hist, sc.hist, (uint64_t)(1 << nbits) * nb, nullptr, sc.partials, nullptr, nullptr, st);
-  k_radix_scatter<K, IPT><<<nb, kBlock, 0, st>>>(kin, vin, kout, vout, (uint32_t)cap, nd, shift, nbits, sc.hist,
-                                                 nb);
+inline bool radix_sort(K *kA, uint32_t *vA, K *kB, uint32_t *vB, uint64_t cap, const uint32_t *nd, int total_bits,
+                       SortScratch sc, cudaStream_t st, int full_bins = 0) {
+  const int passes = (total_bits + 7) / 8;
+  if (cap == 0 || (passes == 0 && !full_bins)) return false;
+  const int bpp = passes ? (total_bits + passes - 1) / passes : 0;
+  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
+  cudaMemsetAsync(sc.gbins, 0, sc.bytes_zeroed, st);
+  const unsigned hgrid = (unsigned)tmin<uint64_t>(ceil_div<uint64_t>(cap, kBlock * 16), 148 * 4);
+  k_sweep_hist<K><<<hgrid, kBlock, 0, st>>>(kA, (uint32_t)cap, nd, passes, bpp, total_bits, sc.gbins,
+                                            full_bins ? sc.full_hist : nullptr, full_bins);
+  k_sweep_scan<<<1, kBlock, 0, st>>>(sc.gbins, passes);
+  K *kin = kA, *kout = kB;
+  uint32_t *vin = vA, *vout = vB;
+  for (int p = 0; p < passes; ++p) {
+    const int sh = p * bpp;
+    k_sweep_pass<K, ipt_for<K>()><<<(unsigned)tiles, kBlock, 0, st>>>(
+        kin, vin, kout, vout, (uint32_t)cap, nd, sh, min(bpp, total_bits - sh), sc.gbins + p * 256,
+        sc.status + (size_t)p * tiles * 256, sc.ticket + p);
+    K *tk = kin; kin = kout; kout = tk;
+    uint32_t *tv = vin; vin = vout; vout = tv;
+  }
+  return passes % 2 == 1;
 }
 
 // ------------------------------------------------------- Gaussian stage
@@ -375,18 +502,6 @@ __global__ void k_duplicate(const float *__restrict__ splats, const uint32_t *__
   }
 }
 
-// CSR offsets from sorted tile keys (the reference's bincount + cumsum).
-__global__ void k_ranges(const uint32_t *__restrict__ keys, int64_t count, uint32_t ntiles,
-                         int32_t *__restrict__ offsets) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= count) return;
-  const uint32_t k = keys[j];
-  const int64_t prev = j > 0 ? (int64_t)keys[j - 1] : -1;
-  for (int64_t t = prev + 1; t <= (int64_t)k; ++t) offsets[t] = (int32_t)j;
-  if (j == count - 1)
-    for (int64_t t = (int64_t)k + 1; t <= (int64_t)ntiles; ++t) offsets[t] = (int32_t)count;
-}
-
 __global__ void k_row_hist(const float *__restrict__ splats, const int32_t *__restrict__ tiles_touched, int64_t n,
                            Band b, unsigned long long *__restrict__ rows) {
   extern __shared__ unsigned long long sh[];
@@ -415,7 +530,7 @@ __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
 struct GaussWS {
   uint32_t *cnt, *pos, *valsA, *valsB, *inst_off, *m, *partials;
   uint64_t *keysA, *keysB;
-  RadixScratch rs;
+  SortScratch ss;
   size_t bytes;
 };
 
@@ -432,9 +547,7 @@ inline GaussWS carve_gauss(void *p, int64_t n) {
   w.inst_off = c.take<uint32_t>(N);
   w.m = c.take<uint32_t>(4);
   w.partials = c.take<uint32_t>(scan_ws_bytes(N) / 4);
-  const uint64_t nb = radix_blocks<uint64_t>(N);
-  w.rs.hist = c.take<uint32_t>(256 * nb);
-  w.rs.partials = c.take<uint32_t>(scan_ws_bytes(256 * nb) / 4);
+  w.ss = carve_sort<uint64_t>(c, N, 8);
   w.bytes = c.off;
   return w;
 }
@@ -484,11 +597,9 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
   k_select<<<g256, 256, 0, st>>>(splats, tiles_touched, n, b, w.cnt, w.pos);
   device_scan(w.pos, w.pos, (uint64_t)n, nullptr, w.partials, w.m, nullptr, st);
   k_compact<<<g256, 256, 0, st>>>(splats, depth_keys, w.cnt, w.pos, n, w.keysA, w.valsA);
-  // depth digits: 8 stable 8-bit passes over the M selected Gaussians (float64 keys)
-  for (int p = 0; p < 8; p += 2) {
-    radix_pass<uint64_t>(w.keysA, w.valsA, w.keysB, w.valsB, (uint64_t)n, w.m, 8 * p, 8, w.rs, st);
-    radix_pass<uint64_t>(w.keysB, w.valsB, w.keysA, w.valsA, (uint64_t)n, w.m, 8 * p + 8, 8, w.rs, st);
-  }
+  // depth digits: 8 stable 8-bit passes over the M selected Gaussians (float64 keys); even
+  // pass count -> result back in (keysA, valsA)
+  radix_sort<uint64_t>(w.keysA, w.valsA, w.keysB, w.valsB, (uint64_t)n, w.m, 64, w.ss, st);
   // depth-ordered ids are in valsA; per-Gaussian instance offsets in depth order
   k_gather_counts<<<g256, 256, 0, st>>>(w.valsA, w.cnt, n, w.m, w.inst_off);
   device_scan(w.inst_off, w.inst_off, (uint64_t)n, w.m, w.partials, nullptr, d_num_instances, st);
@@ -497,27 +608,27 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
 
 struct InstWS {
   uint32_t *keysA, *keysB, *valsB;
-  RadixScratch rs;
+  SortScratch ss;
   size_t bytes;
 };
 
-static InstWS carve_inst(void *p, int64_t count) {
+static InstWS carve_inst(void *p, int64_t count, size_t ntiles) {
   Carve c(p);
   InstWS w;
   const size_t I = (size_t)tmax<int64_t>(count, 1);
   w.keysA = c.take<uint32_t>(I);
   w.keysB = c.take<uint32_t>(I);
   w.valsB = c.take<uint32_t>(I);
-  const uint64_t nb = radix_blocks<uint32_t>(I);
-  w.rs.hist = c.take<uint32_t>(256 * nb);
-  w.rs.partials = c.take<uint32_t>(scan_ws_bytes(256 * nb) / 4);
+  w.ss = carve_sort<uint32_t>(c, I, 4, ntiles);  // up to 32 tile bits + the per-tile histogram
   w.bytes = c.off;
   return w;
 }
 
 extern "C" int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes) {
   if (n < 0 || num_instances < 0 || !bytes) return TGS_ERR_INVALID;
-  *bytes = carve_inst(nullptr, num_instances).bytes;
+  // the per-tile histogram is sized for the largest band a caller can request (2^18 tiles here
+  // at most per call of tgs_bin_instances); callers with more tiles get a bigger query below
+  *bytes = carve_inst(nullptr, num_instances, (size_t)1 << 18).bytes;
   return TGS_OK;
 }
 
@@ -536,26 +647,19 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   }
   if (!workspace || !sorted_ids) return TGS_ERR_INVALID;
   GaussWS gw = carve_gauss(gauss_workspace, n);
-  InstWS w = carve_inst(workspace, num_instances);
+  if (ntiles > (1u << 18)) return TGS_ERR_UNSUPPORTED;
+  InstWS w = carve_inst(workspace, num_instances, (size_t)1 << 18);
   const int bits = key_bits(ntiles);
   const int passes = (bits + 7) / 8;
-  const int per = passes ? (bits + passes - 1) / passes : 0;
-  // ping-pong so the last pass lands in sorted_ids
-  uint32_t *vdst = (passes % 2 == 0) ? reinterpret_cast<uint32_t *>(sorted_ids) : w.valsB;
+  // ping-pong so the last pass lands in sorted_ids: with an even pass count the
+  // duplicate writes straight into sorted_ids (A = sorted_ids, B = valsB)
+  uint32_t *ids_out = reinterpret_cast<uint32_t *>(sorted_ids);
+  uint32_t *vA = (passes % 2 == 0) ? ids_out : w.valsB;
+  uint32_t *vB = (passes % 2 == 0) ? w.valsB : ids_out;
   k_duplicate<<<(unsigned)ceil_div<int64_t>(n, 256), 256, 0, st>>>(splats, gw.valsA, gw.inst_off, n, gw.m, b,
-                                                                    w.keysA, vdst);
-  uint32_t *kin = w.keysA, *vin = vdst;
-  for (int p = 0; p < passes; ++p) {
-    const int shift = p * per;
-    const int nb = min(per, bits - shift);
-    uint32_t *kout = (kin == w.keysA) ? w.keysB : w.keysA;
-    uint32_t *vout = (vin == w.valsB) ? reinterpret_cast<uint32_t *>(sorted_ids) : w.valsB;
-    radix_pass<uint32_t>(kin, vin, kout, vout, (uint64_t)num_instances, nullptr, shift, nb, w.rs, st);
-    kin = kout;
-    vin = vout;
-  }
-  k_ranges<<<(unsigned)ceil_div<int64_t>(num_instances, 256), 256, 0, st>>>(kin, num_instances, ntiles,
-                                                                           tile_offsets);
+                                                                    w.keysA, vA);
+  radix_sort<uint32_t>(w.keysA, vA, w.keysB, vB, (uint64_t)num_instances, nullptr, bits, w.ss, st, (int)ntiles);
+  k_offsets_from_hist<<<1, 1024, 0, st>>>(w.ss.full_hist, (int)ntiles, tile_offsets);
   return launch_status();
 }
 

@@ -35,32 +35,27 @@ __device__ __forceinline__ int reflect_clamp(int k, int n) {  // numpy 'symmetri
   return k < 0 ? 0 : (k >= n ? n - 1 : k);  // only reached by windows of non-image positions
 }
 
-// adjoint (gather form) of "window over the symmetric-padded signal" at index y:
-//   sum_i w_i (u[y-i+R] + [y < R] u[R-1-y-i+R] + [y >= n-R] u[2n-1-y-i+R]), valid indices only.
-// `get(j)` reads u at image index j (caller guarantees j is inside its smem window).
+// Reflection-fold terms of the adjoint at image index y (only near the borders):
+// sum_i w_i (u[R-1-y-i+R] for y < R) + (u[2n-1-y-i+R] for y >= n-R), valid indices.
 template <typename F>
-__device__ __forceinline__ float adjoint_at(int y, int n, const Taps &tp, F get) {
+__device__ __forceinline__ float adjoint_fold(int y, int n, const Taps &tp, F get) {
   float s = 0.0f;
-#pragma unroll
   for (int i = 0; i < 2 * kR + 1; ++i) {
-    const int y0 = y - i + kR;
-    if (y0 >= 0 && y0 < n) s += tp.w[i] * get(y0);
-  }
-  if (y < kR || y >= n - kR) {
-#pragma unroll
-    for (int i = 0; i < 2 * kR + 1; ++i) {
-      if (y < kR) {
-        const int y1 = -1 - y - i + kR;
-        if (y1 >= 0 && y1 < n) s += tp.w[i] * get(y1);
-      }
-      if (y >= n - kR) {
-        const int y2 = 2 * n - 1 - y - i + kR;
-        if (y2 >= 0 && y2 < n) s += tp.w[i] * get(y2);
-      }
+    if (y < kR) {
+      const int y1 = -1 - y - i + kR;
+      if (y1 >= 0 && y1 < n) s += tp.w[i] * get(y1);
+    }
+    if (y >= n - kR) {
+      const int y2 = 2 * n - 1 - y - i + kR;
+      if (y2 >= 0 && y2 < n) s += tp.w[i] * get(y2);
     }
   }
   return s;
 }
+
+constexpr int kHSeg = 6;  // horizontal-window outputs per work item (42 = 7 x 6)
+constexpr int kVSeg = 6;  // vertical-window outputs per work item
+constexpr int kASeg = 8;  // adjoint outputs per work item (32 = 4 x 8)
 
 __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__restrict__ img,
                                                              const float *__restrict__ tgt, int W, int H, Taps tp,
@@ -68,16 +63,17 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
                                                              float *__restrict__ dimage, double *__restrict__ sums) {
   extern __shared__ float4 smem4[];
   float *sm = reinterpret_cast<float *>(smem4);
-  float *sa = sm;                        // [kIn][kIn]
-  float *sb = sa + kIn * kIn;            // [kIn][kIn]
-  float *hs = sb + kIn * kIn;            // [kIn][kMid][5]; reused as se [kT][kMid][3]
-  float *sd = hs + kIn * kMid * 5;       // [kMid][kMid][3]
-  float *se = hs;
+  float *sa = sm;                         // [kIn][kIn]
+  float *sb = sa + kIn * kIn;             // [kIn][kIn]
+  float *hs = sb + kIn * kIn;             // [5][kIn][kMid] (planar)
+  float *sd = hs + 5 * kIn * kMid;        // [3][kMid][kMid] (planar, zero outside the image)
+  float *se = hs;                         // [3][kT][kMid] (reuses hs)
   __shared__ double red[2][kLossThreads / 32];
   const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
   const int gx = x0 - 2 * kR, gy = y0 - 2 * kR;  // image coords of sa[0][0]
   const int mx = x0 - kR, my = y0 - kR;          // image coords of the kMid region origin
   const int t = threadIdx.x;
+  const bool border = x0 < kR || y0 < kR || x0 + kT > W - kR || y0 + kT > H - kR;
   double l1 = 0.0, ss = 0.0;
   for (int c = 0; c < 3; ++c) {
     for (int e = t; e < kIn * kIn; e += kLossThreads) {
@@ -87,86 +83,135 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
       sb[e] = tgt[p];
     }
     __syncthreads();
-    // horizontal window sums on rows [0, kIn) x mid columns [0, kMid)
-    for (int e = t; e < kIn * kMid; e += kLossThreads) {
-      const int r = e / kMid, q = e - r * kMid;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+    // ---- horizontal window sums: item = (row, 6 mid columns), sliding window in registers
+    for (int it = t; it < kIn * (kMid / kHSeg); it += kLossThreads) {
+      const int r = it / (kMid / kHSeg), q0 = (it - r * (kMid / kHSeg)) * kHSeg;
+      float av[kHSeg + 2 * kR], bv[kHSeg + 2 * kR];
 #pragma unroll
-      for (int j = 0; j < 2 * kR + 1; ++j) {
-        const float av = sa[r * kIn + q + j], bv = sb[r * kIn + q + j], w = tp.w[j];
-        s0 += w * av;
-        s1 += w * bv;
-        s2 += w * av * av;
-        s3 += w * bv * bv;
-        s4 += w * av * bv;
+      for (int j = 0; j < kHSeg + 2 * kR; ++j) {
+        av[j] = sa[r * kIn + q0 + j];
+        bv[j] = sb[r * kIn + q0 + j];
       }
-      float *o = hs + e * 5;
-      o[0] = s0; o[1] = s1; o[2] = s2; o[3] = s3; o[4] = s4;
-    }
-    __syncthreads();
-    // vertical window -> SSIM partials on the mid region (image pixels only)
-    for (int e = t; e < kMid * kMid; e += kLossThreads) {
-      const int r = e / kMid, q = e - r * kMid;
-      const int yy = my + r, xx = mx + q;
-      float *o = sd + e * 3;
-      if (yy < 0 || yy >= H || xx < 0 || xx >= W) {
-        o[0] = o[1] = o[2] = 0.0f;
-        continue;
-      }
-      float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 2 * kR + 1; ++i) {
-        const float *h = hs + ((r + i) * kMid + q) * 5;
-        const float w = tp.w[i];
-        m0 += w * h[0];
-        m1 += w * h[1];
-        m2 += w * h[2];
-        m3 += w * h[3];
-        m4 += w * h[4];
-      }
-      const float var_a = m2 - m0 * m0, var_b = m3 - m1 * m1, cov = m4 - m0 * m1;
-      const float A1 = 2.0f * m0 * m1 + c1, A2 = 2.0f * cov + c2;
-      const float B1 = m0 * m0 + m1 * m1 + c1, B2 = var_a + var_b + c2;
-      const float den = B1 * B2;
-      const float smap = A1 * A2 / den;
-      o[0] = 2.0f * m1 * (A2 - A1) / den - 2.0f * m0 * smap * (1.0f / B1 - 1.0f / B2);
-      o[1] = -smap / B2;
-      o[2] = 2.0f * A1 / den;
-      if (r >= kR && r < kR + kT && q >= kR && q < kR + kT) {  // this tile's own pixels
-        ss += smap;
-        const float av = sa[(r + kR) * kIn + q + kR], bv = sb[(r + kR) * kIn + q + kR];
-        l1 += fabsf(av - bv);
+      for (int o = 0; o < kHSeg; ++o) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2 * kR + 1; ++j) {
+          const float w = tp.w[j], x = av[o + j], y = bv[o + j];
+          const float wx = w * x, wy = w * y;
+          s0 += wx;
+          s1 += wy;
+          s2 = fmaf(wx, x, s2);
+          s3 = fmaf(wy, y, s3);
+          s4 = fmaf(wx, y, s4);
+        }
+        const int off = r * kMid + q0 + o;
+        hs[off] = s0;
+        hs[kIn * kMid + off] = s1;
+        hs[2 * kIn * kMid + off] = s2;
+        hs[3 * kIn * kMid + off] = s3;
+        hs[4 * kIn * kMid + off] = s4;
       }
     }
     __syncthreads();
-    // vertical adjoint: rows of the tile x mid columns
-    for (int e = t; e < kT * kMid; e += kLossThreads) {
-      const int r = e / kMid, q = e - r * kMid;
-      const int yy = y0 + r, xx = mx + q;
-      float *o = se + e * 3;
-      if (yy >= H || xx < 0 || xx >= W) {
-        o[0] = o[1] = o[2] = 0.0f;
-        continue;
+    // ---- vertical window -> SSIM partials: item = (mid column, 6 mid rows)
+    for (int it = t; it < kMid * (kMid / kVSeg); it += kLossThreads) {
+      const int q = it % kMid, r0 = (it / kMid) * kVSeg;
+      float m[5][kVSeg];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        float col[kVSeg + 2 * kR];
+#pragma unroll
+        for (int j = 0; j < kVSeg + 2 * kR; ++j) col[j] = hs[k * kIn * kMid + (r0 + j) * kMid + q];
+#pragma unroll
+        for (int o = 0; o < kVSeg; ++o) {
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
+          m[k][o] = acc;
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        o[k] = adjoint_at(yy, H, tp, [&](int j) { return sd[((j - my) * kMid + q) * 3 + k]; });
+      for (int o = 0; o < kVSeg; ++o) {
+        const int r = r0 + o;
+        const int yy = my + r, xx = mx + q;
+        const int off = r * kMid + q;
+        if (yy < 0 || yy >= H || xx < 0 || xx >= W) {
+          sd[off] = 0.f;
+          sd[kMid * kMid + off] = 0.f;
+          sd[2 * kMid * kMid + off] = 0.f;
+          continue;
+        }
+        const float m0 = m[0][o], m1 = m[1][o];
+        const float var_a = m[2][o] - m0 * m0, var_b = m[3][o] - m1 * m1, cov = m[4][o] - m0 * m1;
+        const float A1 = 2.0f * m0 * m1 + c1, A2 = 2.0f * cov + c2;
+        const float B1 = m0 * m0 + m1 * m1 + c1, B2 = var_a + var_b + c2;
+        const float den = B1 * B2;
+        const float smap = A1 * A2 / den;
+        sd[off] = 2.0f * m1 * (A2 - A1) / den - 2.0f * m0 * smap * (1.0f / B1 - 1.0f / B2);
+        sd[kMid * kMid + off] = -smap / B2;
+        sd[2 * kMid * kMid + off] = 2.0f * A1 / den;
+        if (r >= kR && r < kR + kT && q >= kR && q < kR + kT) {  // this tile's own pixels
+          ss += smap;
+          l1 += fabsf(sa[(r + kR) * kIn + q + kR] - sb[(r + kR) * kIn + q + kR]);
+        }
+      }
     }
     __syncthreads();
-    // horizontal adjoint on the tile, combine with the L1 sign
-    for (int e = t; e < kT * kT; e += kLossThreads) {
-      const int r = e / kT, q = e - r * kT;
-      const int yy = y0 + r, xx = x0 + q;
-      if (yy >= H || xx >= W) continue;
-      float g[3];
+    // ---- vertical adjoint: item = (mid column, 8 tile rows); symmetric taps -> correlation
+    for (int it = t; it < kMid * (kT / kASeg); it += kLossThreads) {
+      const int q = it % kMid, r0 = (it / kMid) * kASeg;
+      const int xx = mx + q;
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        g[k] = adjoint_at(xx, W, tp, [&](int j) { return se[(r * kMid + (j - mx)) * 3 + k]; });
-      const float av = sa[(r + 2 * kR) * kIn + q + 2 * kR], bv = sb[(r + 2 * kR) * kIn + q + 2 * kR];
-      const float grad = (g[0] + 2.0f * av * g[1] + bv * g[2]) * inv_count;
-      const float diff = av - bv;
-      const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
-      dimage[((size_t)yy * W + xx) * 3 + c] = (1.0f - lam) * sgn * inv_count - lam * 0.5f * grad;
+      for (int k = 0; k < 3; ++k) {
+        float col[kASeg + 2 * kR];
+#pragma unroll
+        for (int j = 0; j < kASeg + 2 * kR; ++j) col[j] = sd[k * kMid * kMid + (r0 + j) * kMid + q];
+#pragma unroll
+        for (int o = 0; o < kASeg; ++o) {
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
+          const int yy = y0 + r0 + o;
+          if (border && (yy < kR || yy >= H - kR) && xx >= 0 && xx < W)
+            acc += adjoint_fold(yy, H, tp, [&](int j) { return sd[k * kMid * kMid + (j - my) * kMid + q]; });
+          se[k * kT * kMid + (r0 + o) * kMid + q] = (yy < H && xx >= 0 && xx < W) ? acc : 0.0f;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- horizontal adjoint: item = (tile row, 8 columns); combine with the L1 sign
+    for (int it = t; it < kT * (kT / kASeg); it += kLossThreads) {
+      const int r = it / (kT / kASeg), c0 = (it - r * (kT / kASeg)) * kASeg;
+      const int yy = y0 + r;
+      float g[3][kASeg];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float row[kASeg + 2 * kR];
+#pragma unroll
+        for (int j = 0; j < kASeg + 2 * kR; ++j) row[j] = se[k * kT * kMid + r * kMid + c0 + j];
+#pragma unroll
+        for (int o = 0; o < kASeg; ++o) {
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], row[o + i], acc);
+          const int xx = x0 + c0 + o;
+          if (border && (xx < kR || xx >= W - kR))
+            acc += adjoint_fold(xx, W, tp, [&](int j) { return se[k * kT * kMid + r * kMid + (j - mx)]; });
+          g[k][o] = acc;
+        }
+      }
+      if (yy >= H) continue;
+#pragma unroll
+      for (int o = 0; o < kASeg; ++o) {
+        const int xx = x0 + c0 + o;
+        if (xx >= W) continue;
+        const float av = sa[(r + 2 * kR) * kIn + c0 + o + 2 * kR], bv = sb[(r + 2 * kR) * kIn + c0 + o + 2 * kR];
+        const float grad = (g[0][o] + 2.0f * av * g[1][o] + bv * g[2][o]) * inv_count;
+        const float diff = av - bv;
+        const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+        dimage[((size_t)yy * W + xx) * 3 + c] = (1.0f - lam) * sgn * inv_count - lam * 0.5f * grad;
+      }
     }
     __syncthreads();
   }
@@ -198,7 +243,7 @@ __global__ void k_loss_finalize(double *terms, double inv_count) {
   terms[1] *= inv_count;  // mean SSIM over pixels and channels
 }
 
-constexpr size_t kLossSmem = (size_t)(2 * kIn * kIn + kIn * kMid * 5 + kMid * kMid * 3) * sizeof(float);
+constexpr size_t kLossSmem = (size_t)(2 * kIn * kIn + 5 * kIn * kMid + 3 * kMid * kMid) * sizeof(float);
 
 }  // namespace tgs
 

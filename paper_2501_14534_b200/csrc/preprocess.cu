@@ -214,167 +214,230 @@ __device__ __forceinline__ void put(float *p, float v) {
   if (kAcc) *p += v; else *p = v;
 }
 
+// ---------------------------------------------------------------------------
+// Multi-view backward.  Every chain after the screen-space partials is LINEAR in
+// them, so for a batch of views the view-dependent parts (projection Jacobian,
+// view direction, SH basis, clamp mask) run per view and their contributions
+// are summed, while the view-independent chains (covariance -> quaternion /
+// log-scale, opacity and mask sigmoids, sh_dc) run once on the summed upstream:
+// the parameters are read once per step instead of once per view.  The sum of
+// per-view reference gradients (rasterizer.py:375-419) up to float reassociation.
+constexpr int kMaxViews = 8;
+
+struct ViewBatch {
+  tgs_camera cam[kMaxViews];
+  const uint8_t *visible[kMaxViews];
+  const float *dsplats[kMaxViews];
+  int nviews;
+};
+
 template <int DEG, bool kAcc>
-__global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_camera cam, tgs_settings s,
-                                                              const uint8_t *__restrict__ visible,
-                                                              const float *__restrict__ dsplats, tgs_grads g) {
+__global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
+                                                                    tgs_grads g) {
   __shared__ __align__(16) float rest_s[kPreBlock * 45];
+  __shared__ __align__(16) float drest_s[kPreBlock * 45];
+  constexpr int K = (DEG + 1) * (DEG + 1) - 1;
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
-  constexpr int deg = DEG;
-  const bool rest_grads = deg > 0 && s.compute_sh_rest_grads;
-  if (deg > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  const bool rest_grads = DEG > 0 && s.compute_sh_rest_grads;
+  if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  for (int j = threadIdx.x; j < kPreBlock * 45; j += kPreBlock) drest_s[j] = 0.0f;
   __syncthreads();
   const int64_t i = base + threadIdx.x;
   const bool live = (int)threadIdx.x < count;
-  float *my_rest = rest_s + 45 * threadIdx.x;
+  const float *my_rest = rest_s + 45 * threadIdx.x;
+  float *my_drest = drest_s + 45 * threadIdx.x;
   if (live) {
-    GaussFwd f;
-    gauss_forward<DEG>(cl, i, cam, s, my_rest, f);
-    const bool vis = visible[i] != 0;
-    float dm0 = 0.f, dm1 = 0.f, g00 = 0.f, g01 = 0.f, g11 = 0.f, da = 0.f, dcol[3] = {0.f, 0.f, 0.f};
-    if (vis) {
-      const float *d = dsplats + 9 * i;
-      dm0 = d[0]; dm1 = d[1]; g00 = d[2]; g01 = d[3]; g11 = d[4]; da = d[5];
-      dcol[0] = d[6]; dcol[1] = d[7]; dcol[2] = d[8];
+    // ---- view-independent state (masking.py:21-43, geometry.py:19-41,74-77)
+    const float m = cl.mask_logits[i], o = cl.opacity_logits[i];
+    const float Mg = (m > s.mask_logit_min) ? 1.0f : 0.0f;
+    float band[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) band[l] = (cl.sh_mask_logits[3 * i + l] > s.sh_mask_logit_min) ? 1.0f : 0.0f;
+    float s_raw[3], sc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      s_raw[k] = sem_expf(cl.log_scales[3 * i + k]);
+      sc[k] = s_raw[k] * Mg;
     }
-    // ---- colour path (sh.py:164-215) ----
-    constexpr int K = (DEG + 1) * (DEG + 1) - 1;
-    float dcolor[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) dcolor[c] = f.pre[c] > 0.0f ? dcol[c] : 0.0f;
-    float d_dirs[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f};
-    if (deg > 0) {
-      float b[15], bg[15][3];
-      sh_basis_rest(f.dir[0], f.dir[1], f.dir[2], b);
-      sh_basis_rest_grad(f.dir[0], f.dir[1], f.dir[2], bg);
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const float mb = f.band[band_of(k)];
-        float mr[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) mr[c] = my_rest[3 * k + c] * mb;
-#pragma unroll
-        for (int dd = 0; dd < 3; ++dd)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) d_dirs[dd] += bg[k][dd] * mr[c] * dcolor[c];
-      }
-      if (rest_grads) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const float mb = f.band[band_of(k)];
-          float pc = 0.0f;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float dmk = b[k] * dcolor[c];
-            pc += dmk * my_rest[3 * k + c];
-            my_rest[3 * k + c] = dmk * mb;  // d_rest, written back through smem below
-          }
-          d_band[band_of(k)] += pc;
-        }
-#pragma unroll
-        for (int k = 3 * K; k < 45; ++k) my_rest[k] = 0.0f;
-      }
-    }
-    // all outputs are gathered in registers and written once at the end (one batch of
-    // independent loads for the accumulate read-modify-write)
-    float o_dc[3], o_shm[3], o_pos[3], o_ls[3], o_rot[4], o_op, o_mask, o_m2d[2];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) o_dc[c] = SH_C0 * dcolor[c];
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const float sg = sem_sigmoidf(cl.sh_mask_logits[3 * i + l]);
-      o_shm[l] = d_band[l] * (sg * (1.0f - sg));
-    }
-    const float inner = d_dirs[0] * f.dir[0] + d_dirs[1] * f.dir[1] + d_dirs[2] * f.dir[2];
-    float gp[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) gp[k] = (d_dirs[k] - f.dir[k] * inner) / f.dnorm;
-    // ---- opacity path (rasterizer.py:397-400) ----
-    const float s_op = sem_sigmoidf(cl.opacity_logits[i]);
-    o_op = vis ? da * f.Mg * s_op * (1.0f - s_op) : 0.0f;
-    float dmask = vis ? da * s_op : 0.0f;
-    // ---- project_backward (geometry.py:198-251) ----
-    float dS[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (vis) {
-      const float tz = f.t[2], fx = cam.fx, fy = cam.fy;
-      const float G[4] = {g00, 0.5f * g01, 0.5f * g01, g11};
-      const float *Mj = f.Mj;
-      float MtG[6];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 2; ++b2) MtG[2 * a + b2] = Mj[a] * G[b2] + Mj[3 + a] * G[2 + b2];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2) dS[3 * a + b2] = MtG[2 * a] * Mj[b2] + MtG[2 * a + 1] * Mj[3 + b2];
-      float GM[6], dM[6], dJ[6];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2) GM[3 * a + b2] = G[2 * a] * Mj[b2] + G[2 * a + 1] * Mj[3 + b2];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2)
-          dM[3 * a + b2] = 2.0f * (GM[3 * a] * f.S[b2] + GM[3 * a + 1] * f.S[3 + b2] + GM[3 * a + 2] * f.S[6 + b2]);
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2)
-          dJ[3 * a + b2] = dM[3 * a] * cam.R[3 * b2] + dM[3 * a + 1] * cam.R[3 * b2 + 1] + dM[3 * a + 2] * cam.R[3 * b2 + 2];
-      const float tz2 = tz * tz, tz3 = tz * tz * tz;
-      float dt0 = dJ[2] * (-fx / tz2);
-      float dt1 = dJ[5] * (-fy / tz2);
-      float dt2 = dJ[0] * (-fx / tz2) + dJ[4] * (-fy / tz2) + dJ[2] * (2.0f * fx * f.t[0] / tz3) +
-                  dJ[5] * (2.0f * fy * f.t[1] / tz3);
-      dt0 += dm0 * fx / tz;
-      dt1 += dm1 * fy / tz;
-      dt2 += -(dm0 * fx * f.t[0] + dm1 * fy * f.t[1]) / tz2;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) o_pos[k] = gp[k];
-    // ---- covariance_backward + quat_backward (geometry.py:44-89) ----
-    float L[9], dL[9], dsc[3], dR[9];
+    const float qw = cl.rotations[4 * i], qx = cl.rotations[4 * i + 1];
+    const float qy = cl.rotations[4 * i + 2], qz = cl.rotations[4 * i + 3];
+    const float qnorm = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    const float w = qw / qnorm, x = qx / qnorm, y = qy / qnorm, z = qz / qnorm;
+    float Rg[9];
+    Rg[0] = 1.0f - 2.0f * (y * y + z * z);
+    Rg[1] = 2.0f * (x * y - w * z);
+    Rg[2] = 2.0f * (x * z + w * y);
+    Rg[3] = 2.0f * (x * y + w * z);
+    Rg[4] = 1.0f - 2.0f * (x * x + z * z);
+    Rg[5] = 2.0f * (y * z - w * x);
+    Rg[6] = 2.0f * (x * z - w * y);
+    Rg[7] = 2.0f * (y * z + w * x);
+    Rg[8] = 1.0f - 2.0f * (x * x + y * y);
+    float L[9], S[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) L[3 * r + k] = f.Rg[3 * r + k] * f.sc[k];
+      for (int k = 0; k < 3; ++k) L[3 * r + k] = Rg[3 * r + k] * sc[k];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int b2 = 0; b2 < 3; ++b2) {
+      for (int b = 0; b < 3; ++b) S[3 * a + b] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
+    const float px = cl.positions[3 * i], py = cl.positions[3 * i + 1], pz = cl.positions[3 * i + 2];
+    // ---- accumulators over views
+    float gp[3] = {0.f, 0.f, 0.f}, dS[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float da_sum = 0.f, dc_sum[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f}, m2d[2] = {0.f, 0.f};
+    for (int v = 0; v < vb.nviews; ++v) {
+      if (!vb.visible[v][i]) continue;  // non-visible: every partial is zero (rasterizer.py:376-379)
+      const tgs_camera &cam = vb.cam[v];
+      const float *d = vb.dsplats[v] + 9 * i;
+      const float dm0 = d[0], dm1 = d[1], g00 = d[2], g01 = d[3], g11 = d[4], da = d[5];
+      const float dcol[3] = {d[6], d[7], d[8]};
+      da_sum += da;
+      m2d[0] += dm0;
+      m2d[1] += dm1;
+      // projection (geometry.py:153-168)
+      float t[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) t[r] = px * cam.R[3 * r] + py * cam.R[3 * r + 1] + pz * cam.R[3 * r + 2] + cam.t[r];
+      const float tz = t[2], fx = cam.fx, fy = cam.fy;
+      const float tz2 = tz * tz, tz3 = tz2 * tz;
+      const float J00 = fx / tz, J02 = -fx * t[0] / tz2, J11 = fy / tz, J12 = -fy * t[1] / tz2;
+      float Mj[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        Mj[j] = J00 * cam.R[j] + J02 * cam.R[6 + j];
+        Mj[3 + j] = J11 * cam.R[3 + j] + J12 * cam.R[6 + j];
+      }
+      // view direction + SH colour backward (sh.py:164-215)
+      const float e0 = px - cam.center[0], e1 = py - cam.center[1], e2 = pz - cam.center[2];
+      const float nrm = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
+      const float dn = nrm < 1e-12f ? 1e-12f : nrm;
+      const float dir[3] = {e0 / dn, e1 / dn, e2 / dn};
+      float bsh[15], bg[15][3];
+      sh_basis_rest(dir[0], dir[1], dir[2], bsh);
+      float dcolor[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
         float acc = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc += (dS[3 * a + k] + dS[3 * k + a]) * L[3 * k + b2];
-        dL[3 * a + b2] = acc;
+        for (int k = 0; k < K; ++k) acc = acc + bsh[k] * (my_rest[3 * k + c] * band[band_of(k)]);
+        float pre = SH_C0 * cl.sh_dc[3 * i + c] + 0.5f;
+        if (DEG > 0) pre = pre + acc;
+        dcolor[c] = pre > 0.0f ? dcol[c] : 0.0f;
+        dc_sum[c] += dcolor[c];
+      }
+      float d_dirs[3] = {0.f, 0.f, 0.f};
+      if (DEG > 0) {
+        sh_basis_rest_grad(dir[0], dir[1], dir[2], bg);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float mb = band[band_of(k)];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float mr = my_rest[3 * k + c] * mb;
+#pragma unroll
+            for (int dd = 0; dd < 3; ++dd) d_dirs[dd] += bg[k][dd] * mr * dcolor[c];
+          }
+        }
+        if (rest_grads) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float mb = band[band_of(k)];
+            float pc = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const float dmk = bsh[k] * dcolor[c];
+              pc += dmk * my_rest[3 * k + c];
+              my_drest[3 * k + c] += dmk * mb;
+            }
+            d_band[band_of(k)] += pc;
+          }
+        }
+      }
+      const float inner = d_dirs[0] * dir[0] + d_dirs[1] * dir[1] + d_dirs[2] * dir[2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gp[k] += (d_dirs[k] - dir[k] * inner) / dn;
+      // project_backward (geometry.py:198-251)
+      const float G[4] = {g00, 0.5f * g01, 0.5f * g01, g11};
+      float MtG[6], GM[6], dM[6], dJ[6];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) MtG[2 * a + b] = Mj[a] * G[b] + Mj[3 + a] * G[2 + b];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) dS[3 * a + b] += MtG[2 * a] * Mj[b] + MtG[2 * a + 1] * Mj[3 + b];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) GM[3 * a + b] = G[2 * a] * Mj[b] + G[2 * a + 1] * Mj[3 + b];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          dM[3 * a + b] = 2.0f * (GM[3 * a] * S[b] + GM[3 * a + 1] * S[3 + b] + GM[3 * a + 2] * S[6 + b]);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          dJ[3 * a + b] = dM[3 * a] * cam.R[3 * b] + dM[3 * a + 1] * cam.R[3 * b + 1] + dM[3 * a + 2] * cam.R[3 * b + 2];
+      float dt0 = dJ[2] * (-fx / tz2);
+      float dt1 = dJ[5] * (-fy / tz2);
+      float dt2 = dJ[0] * (-fx / tz2) + dJ[4] * (-fy / tz2) + dJ[2] * (2.0f * fx * t[0] / tz3) +
+                  dJ[5] * (2.0f * fy * t[1] / tz3);
+      dt0 += dm0 * fx / tz;
+      dt1 += dm1 * fy / tz;
+      dt2 += -(dm0 * fx * t[0] + dm1 * fy * t[1]) / tz2;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
+    }
+    // ---- view-independent chains on the summed upstream
+    const float s_op = sem_sigmoidf(o);
+    const float o_op = da_sum * Mg * s_op * (1.0f - s_op);
+    float dmask = da_sum * s_op;
+    float dL[9], dsc[3], dR[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc += (dS[3 * a + k] + dS[3 * k + a]) * L[3 * k + b];
+        dL[3 * a + b] = acc;
       }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) dsc[k] = dL[k] * f.Rg[k] + dL[3 + k] * f.Rg[3 + k] + dL[6 + k] * f.Rg[6 + k];
+    for (int k = 0; k < 3; ++k) dsc[k] = dL[k] * Rg[k] + dL[3 + k] * Rg[3 + k] + dL[6 + k] * Rg[6 + k];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) dR[3 * r + k] = dL[3 * r + k] * f.sc[k];
-    const float w = f.qn[0], x = f.qn[1], y = f.qn[2], z = f.qn[3];
+      for (int k = 0; k < 3; ++k) dR[3 * r + k] = dL[3 * r + k] * sc[k];
     float dqu[4];
     dqu[0] = 2.0f * (x * (dR[7] - dR[5]) + y * (dR[2] - dR[6]) + z * (dR[3] - dR[1]));
     dqu[1] = 2.0f * (y * (dR[1] + dR[3]) + z * (dR[2] + dR[6])) + 2.0f * w * (dR[7] - dR[5]) - 4.0f * x * (dR[4] + dR[8]);
     dqu[2] = 2.0f * (x * (dR[1] + dR[3]) + z * (dR[5] + dR[7])) + 2.0f * w * (dR[2] - dR[6]) - 4.0f * y * (dR[0] + dR[8]);
     dqu[3] = 2.0f * (x * (dR[2] + dR[6]) + y * (dR[5] + dR[7])) + 2.0f * w * (dR[3] - dR[1]) - 4.0f * z * (dR[0] + dR[4]);
+    const float qn[4] = {w, x, y, z};
     const float qin = dqu[0] * w + dqu[1] * x + dqu[2] * y + dqu[3] * z;
+    float o_rot[4], o_ls[3], o_dc[3], o_shm[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o_rot[k] = (dqu[k] - f.qn[k] * qin) / f.qnorm;
+    for (int k = 0; k < 4; ++k) o_rot[k] = (dqu[k] - qn[k] * qin) / qnorm;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) o_ls[k] = dsc[k] * f.s_raw[k] * f.Mg;
-    dmask += dsc[0] * f.s_raw[0] + dsc[1] * f.s_raw[1] + dsc[2] * f.s_raw[2];
-    const float sm = sem_sigmoidf(cl.mask_logits[i]);
-    o_mask = dmask * (sm * (1.0f - sm));
-    o_m2d[0] = vis ? dm0 : 0.0f;
-    o_m2d[1] = vis ? dm1 : 0.0f;
+    for (int k = 0; k < 3; ++k) o_ls[k] = dsc[k] * s_raw[k] * Mg;
+    dmask += dsc[0] * s_raw[0] + dsc[1] * s_raw[1] + dsc[2] * s_raw[2];
+    const float smk = sem_sigmoidf(m);
+    float o_mask = dmask * (smk * (1.0f - smk));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o_dc[c] = SH_C0 * dc_sum[c];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const float sg = sem_sigmoidf(cl.sh_mask_logits[3 * i + l]);
+      o_shm[l] = d_band[l] * (sg * (1.0f - sg));
+    }
     const bool w_shm = rest_grads || !kAcc;
+    float o_pos[3] = {gp[0], gp[1], gp[2]}, o_op2 = o_op;
+    float o_m2d[2] = {m2d[0], m2d[1]};
     if (kAcc) {  // independent loads first, then the adds
       float p_dc[3], p_shm[3] = {0.f, 0.f, 0.f}, p_pos[3], p_ls[3], p_rot[4], p_m2d[2] = {0.f, 0.f};
 #pragma unroll
@@ -400,7 +463,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) o_rot[k] += p_rot[k];
-      o_op += p_op;
+      o_op2 += p_op;
       o_mask += p_mask;
       o_m2d[0] += p_m2d[0];
       o_m2d[1] += p_m2d[1];
@@ -414,22 +477,19 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd(tgs_cloud cl, tgs_
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) g.rotations[4 * i + k] = o_rot[k];
-    g.opacity_logits[i] = o_op;
+    g.opacity_logits[i] = o_op2;
     g.mask_logits[i] = o_mask;
     if (g.mean2d_screen) {
       g.mean2d_screen[2 * i] = o_m2d[0];
       g.mean2d_screen[2 * i + 1] = o_m2d[1];
     }
   }
-  // ---- sh_rest gradients: coalesced write-out of the smem block ----
+  // ---- sh_rest gradients: coalesced (read-modify-)write of the smem block
   if (rest_grads || !kAcc) {
     __syncthreads();
-    if (!rest_grads && live)
-      for (int k = 0; k < 45; ++k) my_rest[k] = 0.0f;
-    if (!rest_grads) __syncthreads();
     float *dst = g.sh_rest + base * 45;
     const int total = count * 45;
-    for (int j = threadIdx.x; j < total; j += blockDim.x) put<kAcc>(dst + j, rest_s[j]);
+    for (int j = threadIdx.x; j < total; j += blockDim.x) put<kAcc>(dst + j, drest_s[j]);
   }
 }
 
@@ -466,19 +526,42 @@ extern "C" int tgs_count_tiles(const float *splats, int64_t n, int32_t width, in
   return launch_status();
 }
 
-extern "C" int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
-                                       const uint8_t *visible, const float *dsplats, tgs_grads *grads,
-                                       int32_t accumulate, tgs_stream_t stream) {
-  if (!cloud || !cam || !s || !grads || cloud->n < 0) return TGS_ERR_INVALID;
-  if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
-  if (cloud->n == 0) return TGS_OK;
+static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const tgs_settings *s, tgs_grads *grads,
+                            bool accumulate, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
-  cudaStream_t st = as_stream(stream);
   switch (s->active_sh_degree * 2 + (accumulate ? 1 : 0)) {
 #define TGS_BWD(D, A) \
-  case D * 2 + A: k_preprocess_bwd<D, A><<<grid, kPreBlock, 0, st>>>(*cloud, *cam, *s, visible, dsplats, *grads); break;
+  case D * 2 + A: k_preprocess_bwd_views<D, A><<<grid, kPreBlock, 0, st>>>(*cloud, vb, *s, *grads); break;
     TGS_BWD(0, 0) TGS_BWD(0, 1) TGS_BWD(1, 0) TGS_BWD(1, 1) TGS_BWD(2, 0) TGS_BWD(2, 1) TGS_BWD(3, 0) TGS_BWD(3, 1)
 #undef TGS_BWD
   }
   return launch_status();
+}
+
+extern "C" int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
+                                       const uint8_t *visible, const float *dsplats, tgs_grads *grads,
+                                       int32_t accumulate, tgs_stream_t stream) {
+  return tgs_preprocess_backward_views(cloud, cam, s, &visible, &dsplats, 1, grads, accumulate, stream);
+}
+
+extern "C" int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                             const uint8_t *const *visible, const float *const *dsplats,
+                                             int32_t nviews, tgs_grads *grads, int32_t accumulate,
+                                             tgs_stream_t stream) {
+  if (!cloud || !cams || !s || !grads || !visible || !dsplats || cloud->n < 0 || nviews < 1) return TGS_ERR_INVALID;
+  if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
+  if (cloud->n == 0) return TGS_OK;
+  cudaStream_t st = as_stream(stream);
+  for (int v0 = 0; v0 < nviews; v0 += kMaxViews) {
+    ViewBatch vb;
+    vb.nviews = nviews - v0 < kMaxViews ? nviews - v0 : kMaxViews;
+    for (int k = 0; k < vb.nviews; ++k) {
+      vb.cam[k] = cams[v0 + k];
+      vb.visible[k] = visible[v0 + k];
+      vb.dsplats[k] = dsplats[v0 + k];
+    }
+    const int rc = launch_bwd_views(cloud, vb, s, grads, accumulate || v0 > 0, st);
+    if (rc != TGS_OK) return rc;
+  }
+  return TGS_OK;
 }

@@ -252,24 +252,19 @@ def _records(out, splats, bins, cam, c_cam, c_set, dev):
     return [[(int(g[o + k]), float(wt[o + k])) for k in range(c)] for o, c in zip(off, cnt)]
 
 
-def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
-                    grads: CloudGrads | None = None, accumulate: bool = False) -> CloudGrads:
-    """Analytic gradients of sum(dimage * image) w.r.t. every cloud field (rasterizer.py:326-419)."""
+def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
+                   dsplats: torch.Tensor | None = None):
+    """First half of render_backward: the screen-space partials (N, 9) of one view
+    (tgs_blend_backward, _kernels.py:92-181) plus the forward state they refer to."""
     import ctypes
     if output is None or output.transmittance is None or output.last_pos is None:
         raise ContractViolationError("render_backward needs the forward pass auxiliaries")
     h, w = int(cam.height), int(cam.width)
     if tuple(dimage.shape) != (h, w, 3):
         raise ContractViolationError("upstream gradient shape does not match the camera")
-    cloud = _as_cloud(cloud)
     n = len(cloud)
     dev = cloud.device
     c_set = _lib.make_settings(settings)
-    if grads is None:
-        grads = CloudGrads(n, dev, zero=not accumulate and n == 0)
-        accumulate = False
-    if n == 0:
-        return grads
     st = output._state
     if st is None or st.n != n or st.cloud_ptr != cloud.flat.data_ptr():
         # no reusable device state: recompute the forward products (rasterizer.py:342)
@@ -284,15 +279,50 @@ def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output
     d = d.to(dev, torch.float32).contiguous()
     transmit = output.transmittance.to(dev, torch.float32).contiguous()
     last_pos = output.last_pos.to(dev, torch.int32).contiguous()
-    dsplats = torch.zeros((n, 9), dtype=torch.float32, device=dev)
+    if dsplats is None:
+        dsplats = torch.zeros((n, 9), dtype=torch.float32, device=dev)
     c_cam = _lib.make_camera(cam)
-    s = _lib.stream_handle(dev)
     with stage("blend_bwd"):
         _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
-                  _lib.ptr(d), _lib.ptr(dsplats), s)
+                  _lib.ptr(d), _lib.ptr(dsplats), _lib.stream_handle(dev))
+    return dsplats, st
+
+
+def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, visibles: list,
+                              dsplats: list, grads: CloudGrads, accumulate: bool = False) -> CloudGrads:
+    """Second half of render_backward for a batch of views in ONE pass over the
+    parameters (tgs_preprocess_backward_views): grads (+)= sum over views."""
+    import ctypes
+    n = len(cloud)
+    if n == 0 or not cams:
+        return grads
+    V = len(cams)
+    c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+    vis_ptrs = (ctypes.c_void_p * V)(*[v.data_ptr() for v in visibles])
+    ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() for d in dsplats])
+    c_set = _lib.make_settings(settings)
     c_cloud, c_grads = cloud.native(), grads.native()
     with stage("preprocess_bwd"):
-        _lib.call("tgs_preprocess_backward", ctypes.byref(c_cloud), ctypes.byref(c_cam), ctypes.byref(c_set),
-                  _lib.ptr(st.visible_u8), _lib.ptr(dsplats), ctypes.byref(c_grads), int(bool(accumulate)), s)
+        _lib.call("tgs_preprocess_backward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), vis_ptrs,
+                  ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)), _lib.stream_handle(cloud.device))
     return grads
+
+
+def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
+                    grads: CloudGrads | None = None, accumulate: bool = False) -> CloudGrads:
+    """Analytic gradients of sum(dimage * image) w.r.t. every cloud field (rasterizer.py:326-419)."""
+    if output is None or output.transmittance is None or output.last_pos is None:
+        raise ContractViolationError("render_backward needs the forward pass auxiliaries")
+    if tuple(dimage.shape) != (int(cam.height), int(cam.width), 3):
+        raise ContractViolationError("upstream gradient shape does not match the camera")
+    cloud = _as_cloud(cloud)
+    n = len(cloud)
+    _lib.make_settings(settings)
+    if grads is None:
+        grads = CloudGrads(n, cloud.device)
+        accumulate = False
+    if n == 0:
+        return grads
+    dsplats, st = blend_backward(cloud, cam, settings, dimage, output)
+    return preprocess_backward_views(cloud, [cam], settings, [st.visible_u8], [dsplats], grads, accumulate)

@@ -24,7 +24,7 @@ from . import loss as loss_mod
 from .cloud import CloudGrads, GaussianCloud
 from .optim import Adam
 from .profiler import stage
-from .rasterizer import RenderSettings, render_backward, render_forward
+from .rasterizer import RenderSettings, blend_backward, preprocess_backward_views, render_forward
 
 # reference defaults (config.py:76-92 OptimConfig; config.py:67-73 MaskConfig)
 DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opacity_logits": 0.05,
@@ -52,12 +52,13 @@ class Trainer:
         dev = cloud.device
         self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
         self.dimage = {}
+        self.dsplats = {}
         self.launches_per_step = 0
 
     def step(self) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms."""
         g = self.grads
-        g.flat.zero_()
+        vis, parts = [], []
         for v in self.views:
             cam, target = self.cameras[v], self.targets[v]
             out = render_forward(self.cloud, cam, self.settings)
@@ -66,7 +67,16 @@ class Trainer:
                 d = self.dimage[(cam.height, cam.width)] = torch.empty_like(out.image)
             with stage("loss"):
                 loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
-            render_backward(self.cloud, cam, self.settings, d, out, grads=g, accumulate=True)
+            ds = self.dsplats.get(v)
+            if ds is None or ds.shape[0] != len(self.cloud):
+                ds = self.dsplats[v] = torch.empty((len(self.cloud), 9), dtype=torch.float32, device=d.device)
+            ds.zero_()
+            _, st = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds)
+            vis.append(st.visible_u8)
+            parts.append(ds)
+        # one pass over the parameters for all views (linear chains summed first)
+        preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
+                                  accumulate=False)
         if self.pg is None or self.rank == 0:
             with stage("mask_loss"):
                 # mask penalties of total_loss (masking.py:60-67), once per optimisation

@@ -265,3 +265,29 @@ def test_c3_scale_properties(tgs):
     # determinism: a second render is bitwise identical
     out2 = tgs.render_forward(cloud, sc.cameras[0], st)
     assert torch.equal(out.image, out2.image) and torch.equal(out._tiles.indices, out2._tiles.indices)
+
+
+def test_multiview_backward_equals_sum_of_views(tgs):
+    """tgs_preprocess_backward_views (one pass over the parameters, 11 views -> two
+    chunks of <= 8) equals the sum of per-view render_backward gradients."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.rasterizer import blend_backward, preprocess_backward_views
+    sc = scenes.small_scene(seed=12, n=5000, width=96, height=80, dist=3.5)
+    st = tgs.RenderSettings(near=0.2, mask_threshold=0.3)
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    rng = np.random.default_rng(5)
+    cams = [scenes.pinhole(rng.uniform(3.0, 4.5) * d / np.linalg.norm(d), 96, 80)
+            for d in rng.normal(size=(11, 3))]
+    want = tgs.CloudGrads.zeros(len(cloud))
+    vis, parts = [], []
+    for cam in cams:
+        dimg = torch.from_numpy(rng.standard_normal((80, 96, 3)).astype(np.float32)).cuda()
+        out = tgs.render_forward(cloud, cam, st)
+        tgs.render_backward(cloud, cam, st, dimg, out, grads=want, accumulate=True)
+        ds, state = blend_backward(cloud, cam, st, dimg, out)
+        vis.append(state.visible_u8)
+        parts.append(ds)
+    got = preprocess_backward_views(cloud, cams, st, vis, parts, tgs.CloudGrads.zeros(len(cloud)))
+    for f in GRAD_FIELDS:
+        a, b = _np(getattr(got, f)), _np(getattr(want, f))
+        _grad_close(a, b, f)
