@@ -68,20 +68,31 @@ __device__ __forceinline__ void pixel_of(int t, int ts, int &lx, int &ly) {
   }
 }
 
-// Axis-aligned box of the pixels a staged splat can blend into: e >= -emax with
-// emax = min(4.5, ln(255 alpha)) (a = alpha exp(e) >= 1/255 and e >= -4.5), i.e.
-// Q = d^T conic d <= 2 emax, whose extent is sqrt(2 emax (conic^-1)_xx), ...  The
-// margins make it conservative under float32 rounding, so culling a warp whose
-// pixel block misses the box never changes a result.
-__device__ __forceinline__ float4 splat_box(float4 a, float4 b) {
-  const float ca = a.z, cb = a.w, cc = b.x;
-  const float det = ca * cc - cb * cb;
-  const float emax = fminf(4.5f, __logf(255.0f * b.y)) + 0.05f;
-  if (!(det > 0.0f)) return make_float4(-1e30f, 1e30f, -1e30f, 1e30f);
-  if (emax < 0.0f) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);
-  const float q = 2.0f * emax / det;
-  const float hx = sqrtf(q * cc) * 1.001f + 0.01f, hy = sqrtf(q * ca) * 1.001f + 0.01f;
-  return make_float4(a.x - hx, a.x + hx, a.y - hy, a.y + hy);
+// Exact per-warp cull.  The staged splat can blend into a pixel only if
+// e2(d) = A dx^2 + B dx dy + C dy^2 >= thr2 = -min(4.5, ln(255 alpha)) log2(e)
+// (e >= -4.5 and alpha exp(e) >= 1/255).  e2 is a concave quadratic, so its maximum
+// over the warp's pixel rectangle is 0 if the mean lies inside, else the best of
+// the four edge maxima (1-D concave quadratics, vertex clamped to the edge).  A
+// 0.02 (log2 units) margin keeps the test conservative under float32 rounding, so
+// culling never changes a result.
+__device__ __forceinline__ float splat_thr2(float alpha) {
+  return fmaxf(kE2Min, -__log2f(255.0f * alpha)) - 0.02f;
+}
+
+__device__ __forceinline__ bool quad_misses(float2 m, float4 q, float thr2, float4 wb) {
+  const float X0 = wb.x - m.x, X1 = wb.y - m.x, Y0 = wb.z - m.y, Y1 = wb.w - m.y;
+  if (X0 <= 0.0f && X1 >= 0.0f && Y0 <= 0.0f && Y1 >= 0.0f) return false;
+  const float ky = __fdividef(-q.y, 2.0f * q.z), kx = __fdividef(-q.y, 2.0f * q.x);
+  auto edge_x = [&](float X) {  // max over y in [Y0, Y1] at dx = X
+    const float y = fminf(fmaxf(ky * X, Y0), Y1);
+    return q.x * X * X + (q.y * X + q.z * y) * y;
+  };
+  auto edge_y = [&](float Y) {  // max over x in [X0, X1] at dy = Y
+    const float x = fminf(fmaxf(kx * Y, X0), X1);
+    return (q.x * x + q.y * Y) * x + q.z * Y * Y;
+  };
+  const float best = fmaxf(fmaxf(edge_x(X0), edge_x(X1)), fmaxf(edge_y(Y0), edge_y(Y1)));
+  return !(best >= thr2);
 }
 
 // Bounds of the pixels this warp owns (empty when `live` is false on every lane).
@@ -93,16 +104,12 @@ __device__ __forceinline__ float4 warp_bounds(bool live, int px, int py) {
   return make_float4((float)x0, (float)x1, (float)y0, (float)y1);
 }
 
-__device__ __forceinline__ bool box_misses(float4 bx, float4 wb) {
-  return bx.y < wb.x || bx.x > wb.y || bx.w < wb.z || bx.z > wb.w;
-}
 
 // Staged splat (structure of arrays in shared memory).
 struct Stage {
   float2 xy[kBatch];
   float4 q[kBatch];    // prescaled conic + alpha
-  float4 col[kBatch];  // r, g, b, -
-  float4 box[kBatch];
+  float4 col[kBatch];  // r, g, b, cull threshold (log2 units)
   int32_t id[kBatch];
 };
 
@@ -111,8 +118,7 @@ __device__ __forceinline__ void stage_splat(Stage &S, int slot, const float4 *__
   const float c = splats[3 * g + 2].x;
   S.xy[slot] = make_float2(a.x, a.y);
   S.q[slot] = prescaled_conic(a, b);
-  S.col[slot] = make_float4(b.z, b.w, c, 0.0f);
-  S.box[slot] = splat_box(a, b);
+  S.col[slot] = make_float4(b.z, b.w, c, splat_thr2(b.y));
   S.id[slot] = g;
 }
 
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_fwd(const float4 *__restr
       if (__all_sync(0xffffffffu, done)) break;
       // one splat per lane: the warp-level cull, then iterate the survivors in order
       const int j = j0 + lane;
-      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && !box_misses(S.box[j], wb));
+      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
       while (mask) {
         const int k = j0 + __ffs(mask) - 1;
         mask &= mask - 1;
@@ -227,8 +233,7 @@ struct BwdShared {
   float2 xy[kBB];
   float4 q[kBB];
   float4 conic[kBB];  // a, b, c, alpha (raw, for the partials)
-  float4 col[kBB];
-  float4 box[kBB];
+  float4 col[kBB];    // r, g, b, cull threshold
   int32_t id[kBB];
   float acc[kWarpsMax][9][kBB];
 };
@@ -291,8 +296,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
       S.xy[t] = make_float2(a.x, a.y);
       S.q[t] = prescaled_conic(a, b);
       S.conic[t] = make_float4(a.z, a.w, b.x, b.y);
-      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, 0.0f);
-      S.box[t] = splat_box(a, b);
+      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, splat_thr2(b.y));
       S.id[t] = g;
     }
     for (int e = t; e < nwarps * 9 * kBB; e += B) (&S.acc[0][0][0])[e] = 0.0f;
@@ -300,7 +304,8 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
     // back to front over 32-splat chunks; inside a chunk the survivors high to low
     for (int j0 = (cnt - 1) & ~31; j0 >= 0; j0 -= 32) {
       const int j = j0 + lane;
-      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && lo + j < wlast && !box_misses(S.box[j], wb));
+      uint32_t mask =
+          __ballot_sync(0xffffffffu, j < cnt && lo + j < wlast && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
       while (mask) {
         const int bit = 31 - __clz(mask);
         mask &= ~(1u << bit);
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
             if (al >= kAlphaSkip) {
               hit = true;
               const float4 col = S.col[q];
-              const float inv_om = 1.0f / (1.0f - al);
+              const float inv_om = __fdividef(1.0f, 1.0f - al);
               const float t_before = T_after * inv_om;
               const float ga = g0 * (col.x * t_before - s0 * inv_om) + g1 * (col.y * t_before - s1 * inv_om) +
                                g2 * (col.z * t_before - s2 * inv_om);

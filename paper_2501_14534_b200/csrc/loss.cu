@@ -53,9 +53,15 @@ __device__ __forceinline__ float adjoint_fold(int y, int n, const Taps &tp, F ge
   return s;
 }
 
-constexpr int kHSeg = 6;  // horizontal-window outputs per work item (42 = 7 x 6)
-constexpr int kVSeg = 6;  // vertical-window outputs per work item
-constexpr int kASeg = 8;  // adjoint outputs per work item (32 = 4 x 8)
+// Work items per phase are sized so each phase fills the 256 threads between
+// barriers: H 52x14 = 728 items (3 outputs), V 42x6 = 252 (7 outputs),
+// vertical adjoint 42x6 = 252 (6 row segments of 5-6 outputs), horizontal
+// adjoint 32x8 = 256 (4 outputs).
+constexpr int kHSeg = 3;
+constexpr int kVSeg = 7;
+constexpr int kAVSeg = 6;   // max rows per vertical-adjoint item
+constexpr int kAVItems = 6; // row segments per column: 32 = 6+5+5+5+5+6
+constexpr int kAHSeg = 4;
 
 __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__restrict__ img,
                                                              const float *__restrict__ tgt, int W, int H, Taps tp,
@@ -158,17 +164,20 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
       }
     }
     __syncthreads();
-    // ---- vertical adjoint: item = (mid column, 8 tile rows); symmetric taps -> correlation
-    for (int it = t; it < kMid * (kT / kASeg); it += kLossThreads) {
-      const int q = it % kMid, r0 = (it / kMid) * kASeg;
+    // ---- vertical adjoint: item = (mid column, row segment of 5-6); symmetric taps -> correlation
+    for (int it = t; it < kMid * kAVItems; it += kLossThreads) {
+      const int q = it % kMid, sgi = it / kMid;
+      const int r0 = sgi == 0 ? 0 : 1 + 5 * sgi;       // 0, 6, 11, 16, 21, 26
+      const int len = (sgi == 0 || sgi == kAVItems - 1) ? 6 : 5;
       const int xx = mx + q;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float col[kASeg + 2 * kR];
+        float col[kAVSeg + 2 * kR];
 #pragma unroll
-        for (int j = 0; j < kASeg + 2 * kR; ++j) col[j] = sd[k * kMid * kMid + (r0 + j) * kMid + q];
+        for (int j = 0; j < kAVSeg + 2 * kR; ++j) col[j] = (j < len + 2 * kR) ? sd[k * kMid * kMid + (r0 + j) * kMid + q] : 0.0f;
 #pragma unroll
-        for (int o = 0; o < kASeg; ++o) {
+        for (int o = 0; o < kAVSeg; ++o) {
+          if (o >= len) break;
           float acc = 0.f;
 #pragma unroll
           for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
@@ -180,18 +189,18 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
       }
     }
     __syncthreads();
-    // ---- horizontal adjoint: item = (tile row, 8 columns); combine with the L1 sign
-    for (int it = t; it < kT * (kT / kASeg); it += kLossThreads) {
-      const int r = it / (kT / kASeg), c0 = (it - r * (kT / kASeg)) * kASeg;
+    // ---- horizontal adjoint: item = (tile row, 4 columns); combine with the L1 sign
+    for (int it = t; it < kT * (kT / kAHSeg); it += kLossThreads) {
+      const int r = it / (kT / kAHSeg), c0 = (it - r * (kT / kAHSeg)) * kAHSeg;
       const int yy = y0 + r;
-      float g[3][kASeg];
+      float g[3][kAHSeg];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float row[kASeg + 2 * kR];
+        float row[kAHSeg + 2 * kR];
 #pragma unroll
-        for (int j = 0; j < kASeg + 2 * kR; ++j) row[j] = se[k * kT * kMid + r * kMid + c0 + j];
+        for (int j = 0; j < kAHSeg + 2 * kR; ++j) row[j] = se[k * kT * kMid + r * kMid + c0 + j];
 #pragma unroll
-        for (int o = 0; o < kASeg; ++o) {
+        for (int o = 0; o < kAHSeg; ++o) {
           float acc = 0.f;
 #pragma unroll
           for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], row[o + i], acc);
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
       }
       if (yy >= H) continue;
 #pragma unroll
-      for (int o = 0; o < kASeg; ++o) {
+      for (int o = 0; o < kAHSeg; ++o) {
         const int xx = x0 + c0 + o;
         if (xx >= W) continue;
         const float av = sa[(r + 2 * kR) * kIn + c0 + o + 2 * kR], bv = sb[(r + 2 * kR) * kIn + c0 + o + 2 * kR];
