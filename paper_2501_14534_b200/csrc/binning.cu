@@ -173,7 +173,10 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 __device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-constexpr int kLookback = 16;  // predecessors probed per step (independent loads in flight)
+template <typename K>
+constexpr int lookback_for() {  // predecessors probed per step (independent loads in flight)
+  return sizeof(K) == 8 ? 32 : 16;
+}
 
 template <typename K>
 constexpr int ipt_for() {
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep_scan(uint32_t *gbins, int npas
 }
 
 template <typename K, int IPT>
-__global__ void __launch_bounds__(kBlock) k_sweep_pass(const K *__restrict__ keys_in,
+__global__ void __launch_bounds__(kBlock, 3) k_sweep_pass(const K *__restrict__ keys_in,
                                                        const uint32_t *__restrict__ vals_in,
                                                        K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
                                                        uint32_t nh, const uint32_t *nd, int shift, int nbits,
@@ -326,6 +329,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep_pass(const K *__restrict__ key
       int j = (int)tile - 1;
       bool found = false;
       while (!found) {
+        constexpr int kLookback = lookback_for<K>();
         uint32_t v[kLookback];
 #pragma unroll
         for (int k = 0; k < kLookback; ++k)
@@ -397,24 +401,29 @@ inline SortScratch carve_sort(Carve &c, uint64_t cap, int passes, size_t full_bi
 // Stable sort of `cap` (or *nd) items by bits [0, total_bits) of the key, in
 // `passes` passes of <= 8 bits.  Ping-pongs A <-> B; returns true when the
 // result ended in the B buffers.
+// hist_ready: the caller already wrote the exclusive-scanned digit histograms of
+// every pass to sc.gbins (and zeroed the look-back state); last_keys: write the
+// keys on the final pass (not needed when the CSR offsets come from a histogram).
 template <typename K>
 inline bool radix_sort(K *kA, uint32_t *vA, K *kB, uint32_t *vB, uint64_t cap, const uint32_t *nd, int total_bits,
-                       SortScratch sc, cudaStream_t st, int full_bins = 0) {
+                       SortScratch sc, cudaStream_t st, bool hist_ready = false, bool last_keys = true) {
   const int passes = (total_bits + 7) / 8;
-  if (cap == 0 || (passes == 0 && !full_bins)) return false;
-  const int bpp = passes ? (total_bits + passes - 1) / passes : 0;
+  if (cap == 0 || passes == 0) return false;
+  const int bpp = (total_bits + passes - 1) / passes;
   const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
-  cudaMemsetAsync(sc.gbins, 0, sc.bytes_zeroed, st);
-  const unsigned hgrid = (unsigned)tmin<uint64_t>(ceil_div<uint64_t>(cap, kBlock * 16), 148 * 4);
-  k_sweep_hist<K><<<hgrid, kBlock, 0, st>>>(kA, (uint32_t)cap, nd, passes, bpp, total_bits, sc.gbins,
-                                            full_bins ? sc.full_hist : nullptr, full_bins);
-  k_sweep_scan<<<1, kBlock, 0, st>>>(sc.gbins, passes);
+  if (!hist_ready) {
+    cudaMemsetAsync(sc.gbins, 0, sc.bytes_zeroed, st);
+    const unsigned hgrid = (unsigned)tmin<uint64_t>(ceil_div<uint64_t>(cap, kBlock * 16), 148 * 4);
+    k_sweep_hist<K><<<hgrid, kBlock, 0, st>>>(kA, (uint32_t)cap, nd, passes, bpp, total_bits, sc.gbins, nullptr, 0);
+    k_sweep_scan<<<1, kBlock, 0, st>>>(sc.gbins, passes);
+  }
   K *kin = kA, *kout = kB;
   uint32_t *vin = vA, *vout = vB;
   for (int p = 0; p < passes; ++p) {
     const int sh = p * bpp;
     k_sweep_pass<K, ipt_for<K>()><<<(unsigned)tiles, kBlock, 0, st>>>(
-        kin, vin, kout, vout, (uint32_t)cap, nd, sh, min(bpp, total_bits - sh), sc.gbins + p * 256,
+        kin, vin, (p == passes - 1 && !last_keys) ? nullptr : kout, vout, (uint32_t)cap, nd, sh,
+        min(bpp, total_bits - sh), sc.gbins + p * 256,
         sc.status + (size_t)p * tiles * 256, sc.ticket + p);
     K *tk = kin; kin = kout; kout = tk;
     uint32_t *tv = vin; vin = vout; vout = tv;
@@ -499,6 +508,107 @@ __global__ void k_duplicate(const float *__restrict__ splats, const uint32_t *__
       keys[so + e] = (uint32_t)(sy0 + row) * b.tiles_x + (uint32_t)(sx0 + col) - base_tile;
       vals[so + e] = sg;
     }
+  }
+}
+
+// Per-tile instance counts from the Gaussians' rectangles: a 2D difference array
+// (+1/-1 at the four corners of each band-clipped rect, 4 atomics per Gaussian)
+// integrated by k_tile_hist_finalize.  Grid (rows + 1) x (tiles_x + 1), int32.
+constexpr int kDiffSmem = 12288;
+
+__global__ void __launch_bounds__(256) k_tile_hist2d(const float *__restrict__ splats, const uint32_t *__restrict__ ids,
+                                                     int64_t cap, const uint32_t *nd, Band b,
+                                                     int32_t *__restrict__ diff) {
+  extern __shared__ int32_t dsm[];
+  const int gw = b.tiles_x + 1, gh = b.row_end - b.row_begin + 1;
+  const int cells = gw * gh;
+  const bool priv = cells <= kDiffSmem;
+  if (priv)
+    for (int e = threadIdx.x; e < cells; e += blockDim.x) dsm[e] = 0;
+  __syncthreads();
+  int32_t *d = priv ? dsm : diff;
+  const int64_t m = tmin<int64_t>(*nd, cap);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    int x0, y0, x1, y1;
+    if (band_rect(splats + 12 * (int64_t)ids[j], b, x0, y0, x1, y1) == 0) continue;
+    y0 -= b.row_begin;
+    y1 -= b.row_begin;
+    atomicAdd(&d[y0 * gw + x0], 1);
+    atomicAdd(&d[y0 * gw + x1 + 1], -1);
+    atomicAdd(&d[(y1 + 1) * gw + x0], -1);
+    atomicAdd(&d[(y1 + 1) * gw + x1 + 1], 1);
+  }
+  __syncthreads();
+  if (priv)
+    for (int e = threadIdx.x; e < cells; e += blockDim.x)
+      if (dsm[e]) atomicAdd(diff + e, dsm[e]);
+}
+
+// One CTA: integrate the difference grid into per-tile counts, write the CSR
+// offsets, and derive the exclusive digit histograms of every radix pass of the
+// tile key (so the instance sort needs no histogram pass over its keys).
+__global__ void __launch_bounds__(1024) k_tile_hist_finalize(int32_t *__restrict__ diff, int tiles_x, int rows,
+                                                             int passes, int bpp, int total_bits,
+                                                             int32_t *__restrict__ offsets,
+                                                             uint32_t *__restrict__ gbins) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t gb[4][256];
+  const int gw = tiles_x + 1;
+  for (int e = threadIdx.x; e < 4 * 256; e += 1024) (&gb[0][0])[e] = 0;
+  // prefix along x then along y, one warp per row / column (warp scans with carry)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < rows; r += 32) {
+    int32_t carry_r = 0;
+    for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+      const int x = x0 + lane;
+      int32_t v = x < tiles_x ? diff[r * gw + x] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (x < tiles_x) diff[r * gw + x] = v + carry_r;
+      carry_r += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int x = warp; x < tiles_x; x += 32) {
+    int32_t carry_c = 0;
+    for (int r0 = 0; r0 < rows; r0 += 32) {
+      const int r = r0 + lane;
+      int32_t v = r < rows ? diff[r * gw + x] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (r < rows) diff[r * gw + x] = v + carry_c;
+      carry_c += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const int ntiles = rows * tiles_x;
+  uint32_t carry = 0;
+  for (int c = 0; c < ntiles; c += 1024) {
+    const int t = c + threadIdx.x;
+    const uint32_t v = t < ntiles ? (uint32_t)diff[(t / tiles_x) * gw + (t % tiles_x)] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan(v, ws, &tot);
+    if (t < ntiles) {
+      offsets[t] = (int32_t)(carry + ex);
+      for (int p = 0; p < passes; ++p) {
+        const int sh = p * bpp, nb = min(bpp, total_bits - sh);
+        if (v) atomicAdd(&gb[p][((uint32_t)t >> sh) & ((1u << nb) - 1)], v);
+      }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) offsets[ntiles] = (int32_t)carry;
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t v = threadIdx.x < 256 ? gb[p][threadIdx.x] : 0u;
+    const uint32_t ex = block_exclusive_scan(v, ws, nullptr);
+    if (threadIdx.x < 256) gbins[p * 256 + threadIdx.x] = ex;
   }
 }
 
@@ -608,6 +718,7 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
 
 struct InstWS {
   uint32_t *keysA, *keysB, *valsB;
+  int32_t *diff;
   SortScratch ss;
   size_t bytes;
 };
@@ -619,7 +730,8 @@ static InstWS carve_inst(void *p, int64_t count, size_t ntiles) {
   w.keysA = c.take<uint32_t>(I);
   w.keysB = c.take<uint32_t>(I);
   w.valsB = c.take<uint32_t>(I);
-  w.ss = carve_sort<uint32_t>(c, I, 4, ntiles);  // up to 32 tile bits + the per-tile histogram
+  w.ss = carve_sort<uint32_t>(c, I, 4);  // up to 32 tile bits
+  w.diff = c.take<int32_t>(ntiles);       // (rows + 1) x (tiles_x + 1) difference grid bound
   w.bytes = c.off;
   return w;
 }
@@ -656,10 +768,25 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   uint32_t *ids_out = reinterpret_cast<uint32_t *>(sorted_ids);
   uint32_t *vA = (passes % 2 == 0) ? ids_out : w.valsB;
   uint32_t *vB = (passes % 2 == 0) ? w.valsB : ids_out;
+  // per-tile counts (-> CSR offsets) and the digit histograms from the rects
+  const int rows = b.row_end - b.row_begin;
+  const int cells = (rows + 1) * (b.tiles_x + 1);
+  static bool attr_done = false;  // idempotent function attribute, set once per process
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_tile_hist2d, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiffSmem * 4);
+    attr_done = true;
+  }
+  cudaMemsetAsync(w.ss.gbins, 0, w.ss.bytes_zeroed, st);
+  cudaMemsetAsync(w.diff, 0, (size_t)cells * 4, st);
+  const unsigned dgrid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n, 256), 148 * 2);
+  k_tile_hist2d<<<dgrid, 256, cells <= kDiffSmem ? (size_t)cells * 4 : 0, st>>>(splats, gw.valsA, n, gw.m, b,
+                                                                                w.diff);
+  const int bpp = passes ? (bits + passes - 1) / passes : 0;
+  k_tile_hist_finalize<<<1, 1024, 0, st>>>(w.diff, b.tiles_x, rows, passes, bpp, bits, tile_offsets, w.ss.gbins);
   k_duplicate<<<(unsigned)ceil_div<int64_t>(n, 256), 256, 0, st>>>(splats, gw.valsA, gw.inst_off, n, gw.m, b,
                                                                     w.keysA, vA);
-  radix_sort<uint32_t>(w.keysA, vA, w.keysB, vB, (uint64_t)num_instances, nullptr, bits, w.ss, st, (int)ntiles);
-  k_offsets_from_hist<<<1, 1024, 0, st>>>(w.ss.full_hist, (int)ntiles, tile_offsets);
+  radix_sort<uint32_t>(w.keysA, vA, w.keysB, vB, (uint64_t)num_instances, nullptr, bits, w.ss, st,
+                       /*hist_ready=*/true, /*last_keys=*/false);
   return launch_status();
 }
 
