@@ -132,8 +132,10 @@ def stage_bytes(n, vis_n, inst, pixels, views):
         # select (16 B record fields + 4 tiles + 8 written) + compaction (24 B) + 8 stable passes moving
         # (u64 key, u32 id) in and out (24 B) + counts gather/scan (16 B), per on-screen Gaussian
         "bin_gaussians": n * 28 + vis_n * (24 + 8 * 24 + 16),
-        # duplicate writes (key, id) 8 B + 2 tile-digit passes x 16 B + ranges read 4 B, per instance
-        "bin_instances": inst * (8 + 2 * 16 + 4),
+        # per on-screen Gaussian: rect fields for the tile-count grid + ids/offsets for the
+        # duplicate (24 B); per instance: duplicate writes (key, id) 8 B, pass 1 moves (key, id)
+        # 16 B, the last pass reads (key, id) and writes the id 12 B
+        "bin_instances": vis_n * 24 + inst * (8 + 16 + 12),
         # per instance: 4 B id + 48 B record staged; per pixel 28 B out (rgb, T, w, n, last)
         "blend_fwd": inst * 52 + pixels * 28,
         # per instance 52 B; per pixel 20 B in (dimage, T, last); 36 B partials RMW per Gaussian
@@ -288,10 +290,23 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
+    # Every timed region starts from the same initial parameters and Adam state: training
+    # changes the scene (e.g. the reference's mask lr 0.5 prunes Gaussians within a few
+    # steps), so regions timed after other steps would measure a lighter workload.
+    init = (cloud.flat.clone(), trainer.opt.m.clone(), trainer.opt.v.clone(), dict(trainer.opt.steps))
+
+    def reset(tr):
+        cloud.flat.copy_(init[0])
+        tr.opt.m.copy_(init[1])
+        tr.opt.v.copy_(init[2])
+        tr.opt.steps = dict(init[3])
+        torch.cuda.synchronize()
+
     for _ in range(args.warmup):
         trainer.step()
-    # ---- device-resident timed region (inputs already in HBM)
-    with ClockSampler(local) as clk, profiler.StageTimer() as prof:
+    reset(trainer)
+    # ---- device-resident timed region (inputs already in HBM), views pipelined on 2 streams
+    with ClockSampler(local) as clk:
         t_dev = timed(args.steps, trainer.step)
     clocks = clk.summary()
     value = args.steps / t_dev
@@ -305,11 +320,20 @@ def main():
         terms_host.copy_(trainer.terms, non_blocking=True)
 
     e2e_step()
+    reset(trainer)
     t_e2e = timed(args.steps, e2e_step)
     h2d = sum(host_targets[v].numel() * 4 for v in views)
     d2h = terms_host.numel() * 8
 
-    # ---- workload statistics for the roofline (one extra untimed forward per view)
+    # ---- per-kernel roofline: the same step with views serialised on one stream, so the
+    # CUDA-event duration of each stage is its own (no overlap with the other view)
+    serial = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, process_group=pg, views=views, streams=1)
+    serial.opt = trainer.opt
+    serial.step()
+    reset(serial)
+    with profiler.StageTimer() as prof:
+        t_serial = timed(args.steps, serial.step)
+    reset(serial)
     from paper_2501_14534_b200.rasterizer import render_forward
     inst = []
     vis_n = 0
@@ -323,7 +347,7 @@ def main():
     rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
     launches = trainer_launches(prof.counts(), args.steps)
 
-    # ---- render FPS (forward only, same scene) as a secondary number
+    # ---- render FPS (forward only, initial scene) as a secondary number
     fps_t = timed(args.steps, lambda: [render_forward(cloud, sc.cameras[v], st) for v in views])
     render_fps = args.steps * len(views) * world / fps_t
 
@@ -337,6 +361,7 @@ def main():
             "e2e": {"value": round(args.steps / t_e2e, 4), "unit": "train step/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
+            "ms_per_step_serial_views": round(t_serial / args.steps * 1e3, 3),
             "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean)}
     if world == 1 and not args.no_cpu_baseline:
         from types import SimpleNamespace
@@ -349,8 +374,12 @@ def main():
 def trainer_launches(counts: dict, steps: int) -> int:
     """Kernels of libtgs.so launched in the timed region (the per-entry-point counts are fixed by the
     host code in csrc/: see DESIGN.md "Kernel inventory")."""
-    per_call = {"preprocess_fwd": 1, "bin_gaussians": 1 + 3 + 1 + 8 * 5 + 1 + 3, "bin_instances": 1 + 2 * 5 + 1,
-                "blend_fwd": 1, "loss": 5, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 8}
+    per_call = {"preprocess_fwd": 1,
+                # select, scan(3), compact, depth-sort hist + scan + 8 passes, count gather, scan(3)
+                "bin_gaussians": 1 + 3 + 1 + 2 + 8 + 1 + 3,
+                # tile difference grid, finalize (CSR + digit histograms), duplicate, 2 passes
+                "bin_instances": 1 + 1 + 1 + 2,
+                "blend_fwd": 1, "loss": 2, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 8}
     return int(sum(per_call[k] * c for k, c in counts.items() if k in per_call))
 
 

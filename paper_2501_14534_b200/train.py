@@ -34,7 +34,7 @@ DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opac
 class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
-                 views=None):
+                 views=None, streams: int = 2):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -53,27 +53,39 @@ class Trainer:
         self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
         self.dimage = {}
         self.dsplats = {}
+        # >= 2 streams pipeline consecutive views; 1 stream serialises them (per-kernel timing)
+        self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
         self.launches_per_step = 0
 
     def step(self) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms."""
         g = self.grads
         vis, parts = [], []
-        for v in self.views:
-            cam, target = self.cameras[v], self.targets[v]
-            out = render_forward(self.cloud, cam, self.settings)
-            d = self.dimage.get((cam.height, cam.width))
-            if d is None:
-                d = self.dimage[(cam.height, cam.width)] = torch.empty_like(out.image)
-            with stage("loss"):
-                loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
-            ds = self.dsplats.get(v)
-            if ds is None or ds.shape[0] != len(self.cloud):
-                ds = self.dsplats[v] = torch.empty((len(self.cloud), 9), dtype=torch.float32, device=d.device)
-            ds.zero_()
-            _, st = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds)
-            vis.append(st.visible_u8)
-            parts.append(ds)
+        main = torch.cuda.current_stream(self.cloud.device)
+        for s_ in self.streams:
+            s_.wait_stream(main)  # parameters updated by the previous step's Adam
+        for i, v in enumerate(self.views):
+            # consecutive views alternate between two streams: the latency-bound binning of
+            # view v overlaps the blend/loss kernels of view v-1 (and the host round trip
+            # for the instance count blocks only this view's stream)
+            st = self.streams[i % len(self.streams)]
+            with torch.cuda.stream(st):
+                cam, target = self.cameras[v], self.targets[v]
+                out = render_forward(self.cloud, cam, self.settings)
+                d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
+                if d is None:
+                    d = self.dimage[(i % len(self.streams), cam.height, cam.width)] = torch.empty_like(out.image)
+                with stage("loss"):
+                    loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
+                ds = self.dsplats.get(v)
+                if ds is None or ds.shape[0] != len(self.cloud):
+                    ds = self.dsplats[v] = torch.empty((len(self.cloud), 9), dtype=torch.float32, device=d.device)
+                ds.zero_()
+                _, st_state = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds)
+                vis.append(st_state.visible_u8)
+                parts.append(ds)
+        for s_ in self.streams:
+            main.wait_stream(s_)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
                                   accumulate=False)
