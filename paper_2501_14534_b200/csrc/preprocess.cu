@@ -222,6 +222,27 @@ __device__ __forceinline__ void put(float *p, float v) {
 // log-scale, opacity and mask sigmoids, sh_dc) run once on the summed upstream:
 // the parameters are read once per step instead of once per view.  The sum of
 // per-view reference gradients (rasterizer.py:375-419) up to float reassociation.
+// unit quaternion -> rotation (geometry.py:19-41); returns the raw norm
+__device__ __forceinline__ float quat_rot(const tgs_cloud &cl, int64_t i, float Rg[9], float qn[4] = nullptr) {
+  const float qw = cl.rotations[4 * i], qx = cl.rotations[4 * i + 1];
+  const float qy = cl.rotations[4 * i + 2], qz = cl.rotations[4 * i + 3];
+  const float qnorm = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+  const float w = qw / qnorm, x = qx / qnorm, y = qy / qnorm, z = qz / qnorm;
+  if (qn) {
+    qn[0] = w; qn[1] = x; qn[2] = y; qn[3] = z;
+  }
+  Rg[0] = 1.0f - 2.0f * (y * y + z * z);
+  Rg[1] = 2.0f * (x * y - w * z);
+  Rg[2] = 2.0f * (x * z + w * y);
+  Rg[3] = 2.0f * (x * y + w * z);
+  Rg[4] = 1.0f - 2.0f * (x * x + z * z);
+  Rg[5] = 2.0f * (y * z - w * x);
+  Rg[6] = 2.0f * (x * z - w * y);
+  Rg[7] = 2.0f * (y * z + w * x);
+  Rg[8] = 1.0f - 2.0f * (x * x + y * y);
+  return qnorm;
+}
+
 constexpr int kMaxViews = 8;
 
 struct ViewBatch {
@@ -232,7 +253,7 @@ struct ViewBatch {
 };
 
 template <int DEG, bool kAcc>
-__global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
+__global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
                                                                     tgs_grads g) {
   __shared__ __align__(16) float rest_s[kPreBlock * 45];
   __shared__ __align__(16) float drest_s[kPreBlock * 45];
@@ -248,44 +269,32 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd_views(tgs_cloud cl
   const float *my_rest = rest_s + 45 * threadIdx.x;
   float *my_drest = drest_s + 45 * threadIdx.x;
   if (live) {
-    // ---- view-independent state (masking.py:21-43, geometry.py:19-41,74-77)
+    // ---- view-independent state needed inside the view loop: masks and Sigma (6 unique)
     const float m = cl.mask_logits[i], o = cl.opacity_logits[i];
     const float Mg = (m > s.mask_logit_min) ? 1.0f : 0.0f;
     float band[3];
 #pragma unroll
     for (int l = 0; l < 3; ++l) band[l] = (cl.sh_mask_logits[3 * i + l] > s.sh_mask_logit_min) ? 1.0f : 0.0f;
-    float s_raw[3], sc[3];
+    float S6[6];  // S00 S01 S02 S11 S12 S22
+    {
+      float Rg[9], sc[3];
+      quat_rot(cl, i, Rg);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      s_raw[k] = sem_expf(cl.log_scales[3 * i + k]);
-      sc[k] = s_raw[k] * Mg;
+      for (int k = 0; k < 3; ++k) sc[k] = sem_expf(cl.log_scales[3 * i + k]) * Mg;
+      float L[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) L[3 * r + k] = Rg[3 * r + k] * sc[k];
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) S6[e++] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
     }
-    const float qw = cl.rotations[4 * i], qx = cl.rotations[4 * i + 1];
-    const float qy = cl.rotations[4 * i + 2], qz = cl.rotations[4 * i + 3];
-    const float qnorm = sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
-    const float w = qw / qnorm, x = qx / qnorm, y = qy / qnorm, z = qz / qnorm;
-    float Rg[9];
-    Rg[0] = 1.0f - 2.0f * (y * y + z * z);
-    Rg[1] = 2.0f * (x * y - w * z);
-    Rg[2] = 2.0f * (x * z + w * y);
-    Rg[3] = 2.0f * (x * y + w * z);
-    Rg[4] = 1.0f - 2.0f * (x * x + z * z);
-    Rg[5] = 2.0f * (y * z - w * x);
-    Rg[6] = 2.0f * (x * z - w * y);
-    Rg[7] = 2.0f * (y * z + w * x);
-    Rg[8] = 1.0f - 2.0f * (x * x + y * y);
-    float L[9], S[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) L[3 * r + k] = Rg[3 * r + k] * sc[k];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) S[3 * a + b] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
     const float px = cl.positions[3 * i], py = cl.positions[3 * i + 1], pz = cl.positions[3 * i + 2];
-    // ---- accumulators over views
-    float gp[3] = {0.f, 0.f, 0.f}, dS[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // ---- accumulators over views (dS symmetric: 6 unique entries)
+    float gp[3] = {0.f, 0.f, 0.f}, dS6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float da_sum = 0.f, dc_sum[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f}, m2d[2] = {0.f, 0.f};
     for (int v = 0; v < vb.nviews; ++v) {
       if (!vb.visible[v][i]) continue;  // non-visible: every partial is zero (rasterizer.py:376-379)
@@ -296,102 +305,136 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd_views(tgs_cloud cl
       da_sum += da;
       m2d[0] += dm0;
       m2d[1] += dm1;
-      // projection (geometry.py:153-168)
-      float t[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) t[r] = px * cam.R[3 * r] + py * cam.R[3 * r + 1] + pz * cam.R[3 * r + 2] + cam.t[r];
-      const float tz = t[2], fx = cam.fx, fy = cam.fy;
-      const float tz2 = tz * tz, tz3 = tz2 * tz;
-      const float J00 = fx / tz, J02 = -fx * t[0] / tz2, J11 = fy / tz, J12 = -fy * t[1] / tz2;
-      float Mj[6];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        Mj[j] = J00 * cam.R[j] + J02 * cam.R[6 + j];
-        Mj[3 + j] = J11 * cam.R[3 + j] + J12 * cam.R[6 + j];
-      }
       // view direction + SH colour backward (sh.py:164-215)
-      const float e0 = px - cam.center[0], e1 = py - cam.center[1], e2 = pz - cam.center[2];
-      const float nrm = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
-      const float dn = nrm < 1e-12f ? 1e-12f : nrm;
-      const float dir[3] = {e0 / dn, e1 / dn, e2 / dn};
-      float bsh[15], bg[15][3];
-      sh_basis_rest(dir[0], dir[1], dir[2], bsh);
-      float dcolor[3];
+      {
+        const float e0 = px - cam.center[0], e1 = py - cam.center[1], e2 = pz - cam.center[2];
+        const float nrm = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
+        const float dn = nrm < 1e-12f ? 1e-12f : nrm;
+        const float dir[3] = {e0 / dn, e1 / dn, e2 / dn};
+        float bsh[15];
+        sh_basis_rest(dir[0], dir[1], dir[2], bsh);
+        float dcolor[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float acc = 0.0f;
+        for (int c = 0; c < 3; ++c) {
+          float acc = 0.0f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) acc = acc + bsh[k] * (my_rest[3 * k + c] * band[band_of(k)]);
-        float pre = SH_C0 * cl.sh_dc[3 * i + c] + 0.5f;
-        if (DEG > 0) pre = pre + acc;
-        dcolor[c] = pre > 0.0f ? dcol[c] : 0.0f;
-        dc_sum[c] += dcolor[c];
-      }
-      float d_dirs[3] = {0.f, 0.f, 0.f};
-      if (DEG > 0) {
-        sh_basis_rest_grad(dir[0], dir[1], dir[2], bg);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const float mb = band[band_of(k)];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float mr = my_rest[3 * k + c] * mb;
-#pragma unroll
-            for (int dd = 0; dd < 3; ++dd) d_dirs[dd] += bg[k][dd] * mr * dcolor[c];
-          }
+          for (int k = 0; k < K; ++k) acc = acc + bsh[k] * (my_rest[3 * k + c] * band[band_of(k)]);
+          float pre = SH_C0 * cl.sh_dc[3 * i + c] + 0.5f;
+          if (DEG > 0) pre = pre + acc;
+          dcolor[c] = pre > 0.0f ? dcol[c] : 0.0f;
+          dc_sum[c] += dcolor[c];
         }
-        if (rest_grads) {
+        if (DEG > 0) {
+          float wk[15];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const float mb = band[band_of(k)];
-            float pc = 0.0f;
+          for (int k = 0; k < 15; ++k) {
+            wk[k] = 0.0f;
+            if (k < K) {
+              const float mb = band[band_of(k)];
+              float pc = 0.0f;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const float dmk = bsh[k] * dcolor[c];
-              pc += dmk * my_rest[3 * k + c];
-              my_drest[3 * k + c] += dmk * mb;
+              for (int c = 0; c < 3; ++c) {
+                wk[k] += my_rest[3 * k + c] * mb * dcolor[c];
+                if (rest_grads) {
+                  const float dmk = bsh[k] * dcolor[c];
+                  pc += dmk * my_rest[3 * k + c];
+                  my_drest[3 * k + c] += dmk * mb;
+                }
+              }
+              if (rest_grads) d_band[band_of(k)] += pc;
             }
-            d_band[band_of(k)] += pc;
           }
+          float d_dirs[3];
+          sh_dir_grad<K>(dir[0], dir[1], dir[2], wk, d_dirs);
+          const float inner = d_dirs[0] * dir[0] + d_dirs[1] * dir[1] + d_dirs[2] * dir[2];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) gp[k] += (d_dirs[k] - dir[k] * inner) / dn;
         }
       }
-      const float inner = d_dirs[0] * dir[0] + d_dirs[1] * dir[1] + d_dirs[2] * dir[2];
+      // projection + project_backward (geometry.py:153-168, 198-251)
+      {
+        float t[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gp[k] += (d_dirs[k] - dir[k] * inner) / dn;
-      // project_backward (geometry.py:198-251)
-      const float G[4] = {g00, 0.5f * g01, 0.5f * g01, g11};
-      float MtG[6], GM[6], dM[6], dJ[6];
+        for (int r = 0; r < 3; ++r) t[r] = px * cam.R[3 * r] + py * cam.R[3 * r + 1] + pz * cam.R[3 * r + 2] + cam.t[r];
+        const float tz = t[2], fx = cam.fx, fy = cam.fy;
+        const float tz2 = tz * tz, tz3 = tz2 * tz;
+        const float J00 = fx / tz, J02 = -fx * t[0] / tz2, J11 = fy / tz, J12 = -fy * t[1] / tz2;
+        float Mj[6];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          Mj[j] = J00 * cam.R[j] + J02 * cam.R[6 + j];
+          Mj[3 + j] = J11 * cam.R[3 + j] + J12 * cam.R[6 + j];
+        }
+        const float G0 = g00, G1 = 0.5f * g01, G3 = g11;
+        // dS += M^T G M (symmetric)
+        float MtG0[3], MtG1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          MtG0[a] = Mj[a] * G0 + Mj[3 + a] * G1;
+          MtG1[a] = Mj[a] * G1 + Mj[3 + a] * G3;
+        }
+        {
+          int e = 0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = a; b < 3; ++b) dS6[e++] += MtG0[a] * Mj[b] + MtG1[a] * Mj[3 + b];
+        }
+        // dM = 2 (G M) Sigma, dJ = dM Rc^T
+        auto Sg = [&](int a, int b) -> float {
+          const int lo = a < b ? a : b, hi = a < b ? b : a;
+          return S6[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
+        };
+        float dM[6], dJ[6];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const float ga = a == 0 ? G0 : G1, gb = a == 0 ? G1 : G3;
+          float GM[3];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) GM[b] = ga * Mj[b] + gb * Mj[3 + b];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) dM[3 * a + b] = 2.0f * (GM[0] * Sg(0, b) + GM[1] * Sg(1, b) + GM[2] * Sg(2, b));
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            dJ[3 * a + b] = dM[3 * a] * cam.R[3 * b] + dM[3 * a + 1] * cam.R[3 * b + 1] + dM[3 * a + 2] * cam.R[3 * b + 2];
+        float dt0 = dJ[2] * (-fx / tz2);
+        float dt1 = dJ[5] * (-fy / tz2);
+        float dt2 = dJ[0] * (-fx / tz2) + dJ[4] * (-fy / tz2) + dJ[2] * (2.0f * fx * t[0] / tz3) +
+                    dJ[5] * (2.0f * fy * t[1] / tz3);
+        dt0 += dm0 * fx / tz;
+        dt1 += dm1 * fy / tz;
+        dt2 += -(dm0 * fx * t[0] + dm1 * fy * t[1]) / tz2;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
+      }
+    }
+    // ---- view-independent state again (recomputed rather than kept live across the loop)
+    float s_raw[3], sc[3], Rg[9], L[9], qn[4], qnorm;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      s_raw[k] = sem_expf(cl.log_scales[3 * i + k]);
+      sc[k] = s_raw[k] * Mg;
+    }
+    qnorm = quat_rot(cl, i, Rg, qn);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) L[3 * r + k] = Rg[3 * r + k] * sc[k];
+    const float w = qn[0], x = qn[1], y = qn[2], z = qn[3];
+    float dS[9];
+    {
+      int e = 0;
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 2; ++b) MtG[2 * a + b] = Mj[a] * G[b] + Mj[3 + a] * G[2 + b];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) dS[3 * a + b] += MtG[2 * a] * Mj[b] + MtG[2 * a + 1] * Mj[3 + b];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) GM[3 * a + b] = G[2 * a] * Mj[b] + G[2 * a + 1] * Mj[3 + b];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-          dM[3 * a + b] = 2.0f * (GM[3 * a] * S[b] + GM[3 * a + 1] * S[3 + b] + GM[3 * a + 2] * S[6 + b]);
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-          dJ[3 * a + b] = dM[3 * a] * cam.R[3 * b] + dM[3 * a + 1] * cam.R[3 * b + 1] + dM[3 * a + 2] * cam.R[3 * b + 2];
-      float dt0 = dJ[2] * (-fx / tz2);
-      float dt1 = dJ[5] * (-fy / tz2);
-      float dt2 = dJ[0] * (-fx / tz2) + dJ[4] * (-fy / tz2) + dJ[2] * (2.0f * fx * t[0] / tz3) +
-                  dJ[5] * (2.0f * fy * t[1] / tz3);
-      dt0 += dm0 * fx / tz;
-      dt1 += dm1 * fy / tz;
-      dt2 += -(dm0 * fx * t[0] + dm1 * fy * t[1]) / tz2;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
+        for (int b = a; b < 3; ++b) {
+          dS[3 * a + b] = dS6[e];
+          dS[3 * b + a] = dS6[e];
+          ++e;
+        }
     }
     // ---- view-independent chains on the summed upstream
     const float s_op = sem_sigmoidf(o);
@@ -418,7 +461,6 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_bwd_views(tgs_cloud cl
     dqu[1] = 2.0f * (y * (dR[1] + dR[3]) + z * (dR[2] + dR[6])) + 2.0f * w * (dR[7] - dR[5]) - 4.0f * x * (dR[4] + dR[8]);
     dqu[2] = 2.0f * (x * (dR[1] + dR[3]) + z * (dR[5] + dR[7])) + 2.0f * w * (dR[2] - dR[6]) - 4.0f * y * (dR[0] + dR[8]);
     dqu[3] = 2.0f * (x * (dR[2] + dR[6]) + y * (dR[5] + dR[7])) + 2.0f * w * (dR[3] - dR[1]) - 4.0f * z * (dR[0] + dR[4]);
-    const float qn[4] = {w, x, y, z};
     const float qin = dqu[0] * w + dqu[1] * x + dqu[2] * y + dqu[3] * z;
     float o_rot[4], o_ls[3], o_dc[3], o_shm[3];
 #pragma unroll

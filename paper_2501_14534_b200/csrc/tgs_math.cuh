@@ -112,6 +112,38 @@ __device__ __forceinline__ void sh_basis_rest_grad(float x, float y, float z, fl
   g[14][1] = SH_C3_6 * (-6.0f * x * y);
 }
 
+// sum_k w[k] * d b[k] / d dir (k < K) without materialising the 15x3 gradient table
+// (sh.py:77-120); used by the backward where registers are the occupancy limit.
+template <int K>
+__device__ __forceinline__ void sh_dir_grad(float x, float y, float z, const float w[15], float g[3]) {
+  float gx = 0.0f, gy = 0.0f, gz = 0.0f;
+  if (K > 0) {
+    gy += w[0] * -SH_C1;
+    gz += w[1] * SH_C1;
+    gx += w[2] * -SH_C1;
+  }
+  if (K > 3) {
+    gx += w[3] * (SH_C2_0 * y) + w[5] * (SH_C2_2 * (-2.0f * x)) + w[6] * (SH_C2_3 * z) + w[7] * (SH_C2_4 * (2.0f * x));
+    gy += w[3] * (SH_C2_0 * x) + w[4] * (SH_C2_1 * z) + w[5] * (SH_C2_2 * (-2.0f * y)) + w[7] * (SH_C2_4 * (-2.0f * y));
+    gz += w[4] * (SH_C2_1 * y) + w[5] * (SH_C2_2 * (4.0f * z)) + w[6] * (SH_C2_3 * x);
+  }
+  if (K > 8) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    gx += w[8] * (SH_C3_0 * 6.0f * x * y) + w[9] * (SH_C3_1 * y * z) + w[10] * (SH_C3_2 * (-2.0f * x * y)) +
+          w[11] * (SH_C3_3 * (-6.0f * x * z)) + w[12] * (SH_C3_4 * (4.0f * zz - 3.0f * xx - yy)) +
+          w[13] * (SH_C3_5 * (2.0f * x * z)) + w[14] * (SH_C3_6 * (3.0f * xx - 3.0f * yy));
+    gy += w[8] * (SH_C3_0 * (3.0f * xx - 3.0f * yy)) + w[9] * (SH_C3_1 * x * z) +
+          w[10] * (SH_C3_2 * (4.0f * zz - xx - 3.0f * yy)) + w[11] * (SH_C3_3 * (-6.0f * y * z)) +
+          w[12] * (SH_C3_4 * (-2.0f * x * y)) + w[13] * (SH_C3_5 * (-2.0f * y * z)) + w[14] * (SH_C3_6 * (-6.0f * x * y));
+    gz += w[9] * (SH_C3_1 * x * y) + w[10] * (SH_C3_2 * (8.0f * y * z)) +
+          w[11] * (SH_C3_3 * (6.0f * zz - 3.0f * xx - 3.0f * yy)) + w[12] * (SH_C3_4 * (8.0f * x * z)) +
+          w[13] * (SH_C3_5 * (xx - yy));
+  }
+  g[0] = gx;
+  g[1] = gy;
+  g[2] = gz;
+}
+
 // bin_tiles rect + on-screen gate (rasterizer.py:112-128).  Returns the tile
 // count (0 when the box misses the pixel grid or r <= 0).
 __device__ __forceinline__ int tile_rect(float mx, float my, float r, int W, int H, int ts, int tiles_x,
