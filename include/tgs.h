@@ -226,6 +226,15 @@ TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, i
                   float beta1, float beta2, float eps, float bias_c1, float bias_c2,
                   tgs_stream_t stream);
 
+/* ---- target-side progressive ops (images.py:58-102), (H, W, 3) float32.
+ * area_resize: exact fractional box filter (downsampling only); workspace
+ * out_h * in_w * 3 floats.  gaussian_blur: odd size <= 31, reflect edges;
+ * workspace h * w * 3 floats. */
+TGS_API int tgs_area_resize(const float *in, int32_t in_h, int32_t in_w, float *out, int32_t out_h, int32_t out_w,
+                            float *workspace, tgs_stream_t stream);
+TGS_API int tgs_gaussian_blur(const float *in, int32_t h, int32_t w, int32_t size, float sigma, float *out,
+                              float *workspace, tgs_stream_t stream);
+
 /* ---- (8) row compaction (cloud.take / Adam.compact): out[k] = in[keep[k]] for
  * rows of `row_floats` floats. */
 TGS_API int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,

@@ -73,7 +73,8 @@ class CloudGradsNP:
 
 
 def _settings(s) -> _r.RenderSettings:
-    return _r.RenderSettings(**{k: getattr(s, k) for k in _r.RenderSettings.__dataclass_fields__})
+    d = _r.RenderSettings()
+    return _r.RenderSettings(**{k: getattr(s, k, getattr(d, k)) for k in _r.RenderSettings.__dataclass_fields__})
 
 
 def _np64(t):

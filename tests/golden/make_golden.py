@@ -244,5 +244,43 @@ def main():
     print(f"loss: lambda={cfg.lambda_ssim} l1={terms.l1:.6f} d_ssim={terms.d_ssim:.6f}")
 
 
+
+
+def schedule_and_images():
+    """Progressive hooks (schedule.py:107-170,218-247) and target ops (images.py:58-102)."""
+    from slimsplat.schedule import BlurSpec, Timeline, blur_at, default_blur_decay, lowpass_s_at, phase_at, resolution_at
+    from slimsplat.images import area_resize, gaussian_blur
+    rows = []
+    for mode in ("linear", "logarithmic"):
+        for i in (0, 1, 7, 100, 977, 5000, 9999, 19499, 19500, 25000):
+            for rs, re_ in ((135, 1080), (240, 1920), (6, 48), (48, 48)):
+                rows.append((0 if mode == "linear" else 1, i, rs, re_, 19500, resolution_at(i, rs, re_, 19500, mode)))
+    res = np.array(rows, dtype=np.int64)
+    lp = np.array([(n, h, w, lowpass_s_at(n, h, w)) for n in (1, 10, 1000, 100000, 1000000)
+                   for h, w in ((1080, 1920), (135, 240), (48, 48))], dtype=np.float64)
+    blur = []
+    spec0 = BlurSpec(9, 2.4)
+    decay = default_blur_decay(2.4, 100, 19500, 0.3)
+    for i in (0, 50, 100, 1000, 5000, 10000, 19000, 19499, 19500):
+        for down in (1.0, 2.0, 8.0, 3.5):
+            b = blur_at(i, spec0, 100, decay, 19500, down)
+            blur.append((i, down, b.size, b.sigma))
+    blur = np.array(blur, dtype=np.float64)
+    tl = Timeline()
+    names = ["standard_densify", "late_densify", "mask_prune", "significance_prune", "sh_full_update",
+             "progressive_scale_active"]
+    its = np.array([0, 16, 500, 600, 9999, 10000, 15500, 16000, 20000, 20100, 20500, 21000, 29999])
+    phases = np.array([[n in phase_at(int(i), tl) for n in names] for i in its], dtype=np.uint8)
+    rng = np.random.default_rng(77)
+    img = rng.uniform(0, 1, (61, 83, 3))
+    np.savez_compressed(os.path.join(HERE, "schedule.npz"), res=res, lowpass=lp, blur=blur, decay=decay,
+                        phase_its=its, phases=phases, phase_names=np.array(names), img=img,
+                        area_17x29=area_resize(img, 17, 29), area_61x40=area_resize(img, 61, 40),
+                        blur_7_1p3=gaussian_blur(img, 7, 1.3), blur_9_2p4=gaussian_blur(img, 9, 2.4))
+    print("schedule: ok")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) == 1:
+        main()
+    schedule_and_images()

@@ -291,3 +291,110 @@ def test_multiview_backward_equals_sum_of_views(tgs):
     for f in GRAD_FIELDS:
         a, b = _np(getattr(got, f)), _np(getattr(want, f))
         _grad_close(a, b, f)
+
+
+def test_target_ops_vs_reference(tgs):
+    from paper_2501_14534_b200 import images
+    z = dict(np.load(f"{golden_io.GOLDEN}/schedule.npz"))
+    img = torch.from_numpy(z["img"].astype(np.float32)).cuda()
+    np.testing.assert_allclose(_np(images.area_resize(img, 17, 29)), z["area_17x29"], atol=2e-6)
+    np.testing.assert_allclose(_np(images.area_resize(img, 61, 40)), z["area_61x40"], atol=2e-6)
+    np.testing.assert_allclose(_np(images.gaussian_blur(img, 7, 1.3)), z["blur_7_1p3"], atol=2e-6)
+    np.testing.assert_allclose(_np(images.gaussian_blur(img, 9, 2.4)), z["blur_9_2p4"], atol=2e-6)
+    assert torch.equal(images.area_resize(img, 61, 83), img)
+
+
+def test_prune_compaction_and_adam(tgs):
+    """masking.prune_by_mask (masking.py:70-81) + Adam row compaction (optim.py:51-55)."""
+    from paper_2501_14534_b200 import optim, pruning
+    case = golden_io.load("masked72x40")
+    cloud = tgs.GaussianCloud.from_fields(case.fields)
+    opt = optim.Adam(cloud, {f: 1e-2 for f in golden_io.FIELDS})
+    g = tgs.CloudGrads.zeros(len(cloud))
+    g.flat.normal_()
+    opt.step(cloud, g)
+    old = cloud
+    new, keep = pruning.prune_by_mask(cloud, 0.85)
+    s = 1.0 / (1.0 + np.exp(-_np(old.mask_logits).astype(np.float64)))  # logits after the Adam step
+    want = np.flatnonzero(s > 0.85)                       # reference: hard_mask(m, eps) > 0
+    assert np.array_equal(_np(keep), want)
+    for f in golden_io.FIELDS:
+        assert np.array_equal(_np(getattr(new, f)), _np(getattr(old, f))[want])
+    mo = {f: _np(opt.m[old.field_range(f)[0]:][: old.field_range(f)[1]]) for f in golden_io.FIELDS}
+    pruning.compact_adam(opt, old, new, keep)
+    for f in golden_io.FIELDS:
+        o, size = new.field_range(f)
+        got = _np(opt.m[o:o + size]).reshape((len(new),) + tuple(getattr(new, f).shape[1:]))
+        assert np.array_equal(got, mo[f].reshape((len(old),) + tuple(getattr(old, f).shape[1:]))[want])
+    with pytest.raises(tgs.EmptySceneError):
+        pruning.prune_by_mask(new, 0.9999)
+
+
+def test_adam_matches_reference_formula(tgs):
+    """optim.Adam.update (optim.py:37-49) in float64 vs the kernel."""
+    from paper_2501_14534_b200 import optim
+    rng = np.random.default_rng(0)
+    sc = golden_io.load("fd16")
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    opt = optim.Adam(cloud, {f: 1e-2 for f in golden_io.FIELDS}, eps=1e-15)
+    p = _np(cloud.positions).astype(np.float64)
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    for step in range(1, 4):
+        grad = rng.standard_normal(p.shape).astype(np.float32)
+        g = tgs.CloudGrads.zeros(len(cloud))
+        g.positions.copy_(torch.from_numpy(grad))
+        opt.update(cloud, g, "positions")
+        m = 0.9 * m + 0.1 * grad
+        v = 0.999 * v + 0.001 * grad * grad
+        p -= 1e-2 * (m / (1 - 0.9 ** step)) / (np.sqrt(v / (1 - 0.999 ** step)) + 1e-15)
+    np.testing.assert_allclose(_np(cloud.positions), p, rtol=1e-5, atol=1e-6)
+
+
+def test_compat_adaptor_reference_conventions(tgs):
+    """numpy in/out with V'-space tile ids, as the reference's RenderOutput (rasterizer.py:177-200)."""
+    from paper_2501_14534_b200 import compat
+    case = golden_io.load("masked72x40")
+    from types import SimpleNamespace
+    cloud = SimpleNamespace(**{f: case.fields[f].astype(np.float64) for f in golden_io.FIELDS})
+    out = compat.render_forward(cloud, case.cam, case.settings)
+    z = case.z
+    assert out.image.dtype == np.float64 and out.image.shape == z["image"].shape
+    np.testing.assert_allclose(out.image, z["image"], atol=1e-4)
+    assert np.array_equal(out._tiles.offsets, z["tile_offsets"])
+    assert np.array_equal(out._tiles.indices, z["tile_ids"])
+    g = compat.render_backward(cloud, case.cam, case.settings, z["dimage"], out)
+    for f in golden_io.FIELDS:
+        _grad_close(getattr(g, f), z[f"grad_{f}"], f)
+    b = compat.bin_tiles(z["image"][:0, 0, :2].reshape(0, 2), np.zeros(0), np.zeros(0), 16, 16, 16)
+    assert b.indices.size == 0 and np.all(b.offsets == 0)
+
+
+def test_render_sharded_single_rank_nccl(tgs):
+    """parallel.render_sharded through a real NCCL group (world size 1 on this box)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2501_14534_b200 import parallel, scenes
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        sc = scenes.small_scene(seed=8, n=20_000, width=300, height=170)
+        st = tgs.RenderSettings(near=0.2)
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        img = parallel.render_sharded(cloud, sc.cameras[0], st)
+        ref = tgs.render_forward(cloud, sc.cameras[0], st).image
+        assert torch.equal(img, ref)
+        from paper_2501_14534_b200 import rasterizer
+        splats, _, tiles, _, _ = rasterizer.preprocess(cloud, sc.cameras[0], st)
+        counts = parallel.row_histogram(splats, tiles, len(cloud), sc.cameras[0], 16)
+        out = tgs.render_forward(cloud, sc.cameras[0], st)
+        per_tile = np.diff(_np(out._tiles.offsets)).reshape(-1, out._tiles.tiles_x).sum(axis=1)
+        assert np.array_equal(_np(counts), per_tile)
+    finally:
+        dist.destroy_process_group()
