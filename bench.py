@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--n", type=int, default=1_000_000, help="Gaussians (default: config 3)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0, help="reference arm threads (0 = all cores)")
+    p.add_argument("--config", choices=["c3", "c4"], default="c3",
+                   help="c3: training step (default, the metric's config); c4: 3M-Gaussian 4K render orbit")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -241,6 +243,8 @@ def reference_arm(args):
 # ----------------------------------------------------------------- ours
 def main():
     args = parse()
+    if args.config == "c4":
+        return render_c4(args)
     if args.impl == "reference":
         return reference_arm(args)
     import torch
@@ -368,6 +372,68 @@ def main():
         line["cpu_baseline"] = cpu_baseline(sc, SimpleNamespace(record_hits=False, **settings_kwargs()))
     print(json.dumps(line), flush=True)
     if pg is not None:
+        dist.destroy_process_group()
+
+
+def render_c4(args):
+    """BASELINE.json configs[3]: 3M Gaussians in 64 anisotropic clusters (radius 10), 3840x2160,
+    render-only over the 200-frame orbit; tile rows sharded across ranks (parallel.render_sharded:
+    replicated preprocess, balanced bands from the replicated row histogram, one all-gather)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_14534_b200 import GaussianCloud, RenderSettings, _lib, parallel, scenes
+    from paper_2501_14534_b200.rasterizer import render_forward
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    n = 3_000_000 if args.n == 1_000_000 else args.n
+    sc = scenes.config4(n=n)
+    cloud = GaussianCloud.from_fields(sc.fields, device=dev)
+    st = RenderSettings(near=0.2, tile_size=16)
+    frames = sc.cameras
+
+    def frame(k):
+        cam = frames[k % len(frames)]
+        if world > 1:
+            return parallel.render_sharded(cloud, cam, st)
+        return render_forward(cloud, cam, st).image
+
+    for k in range(args.warmup):
+        frame(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        s.record()
+        for k in range(args.steps):
+            frame(args.warmup + k)
+        e.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([s.elapsed_time(e) / 1e3], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    fps = args.steps / float(t)
+    if rank == 0:
+        print(json.dumps({"metric": "render FPS at 3M Gaussians 3840x2160 (c4 orbit)", "value": round(fps, 3),
+                          "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(float(t) / args.steps * 1e3, 3), "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                          "data": "synthetic (seeded BASELINE.json config 4 generator)",
+                          "config": {"workload": "c4: BASELINE.json configs[3] render-only", "gaussians": n,
+                                     "resolution": "3840x2160", "frames": len(frames),
+                                     "parallelism": f"tile-row sharding x{world}" if world > 1 else "single GPU"},
+                          "clocks": clk.summary()}), flush=True)
+    if world > 1:
         dist.destroy_process_group()
 
 
