@@ -374,6 +374,261 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// 16x16 tiles, two pixels per thread: 128 threads, warp w owns the 8x8 block at
+// ((w & 1) * 8, (w >> 1) * 8), lane -> (x = lane & 7, y = lane >> 3) and the
+// pixels (x, y) and (x, y + 4).  Per surviving splat a warp evaluates 64 pixels
+// and (backward) performs ONE reduction, halving the per-visit overhead.
+constexpr int kT16Threads = 128;
+
+__device__ __forceinline__ void pixel_pair16(int t, int tx, int ty, int &px, int &pyA, int &pyB) {
+  const int w = t >> 5, l = t & 31;
+  px = tx * 16 + ((w & 1) << 3) + (l & 7);
+  pyA = ty * 16 + ((w >> 1) << 3) + (l >> 3);
+  pyB = pyA + 4;
+}
+
+__device__ __forceinline__ float4 warp_bounds2(bool liveA, bool liveB, int px, int pyA, int pyB) {
+  const bool live = liveA || liveB;
+  const int x0 = __reduce_min_sync(0xffffffffu, live ? px : 0x7fffffff);
+  const int x1 = __reduce_max_sync(0xffffffffu, live ? px : -0x7fffffff);
+  const int y0 = __reduce_min_sync(0xffffffffu, liveA ? pyA : (liveB ? pyB : 0x7fffffff));
+  const int y1 = __reduce_max_sync(0xffffffffu, liveB ? pyB : (liveA ? pyA : -0x7fffffff));
+  return make_float4((float)x0, (float)x1, (float)y0, (float)y1);
+}
+
+struct Fwd16Pixel {
+  float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, ws = 0.0f;
+  int contrib = 0, lastp = 0;
+  bool done;
+};
+
+// one list entry for one pixel (_kernels.py:57-81)
+__device__ __forceinline__ void fwd_entry(Fwd16Pixel &P, float fpx, float fpy, float2 m, float4 q, float4 col, int pos,
+                                          int32_t *hits, int32_t gid) {
+  if (P.done) return;
+  if (P.T < kTTerm) {  // checked before each entry (_kernels.py:57-58)
+    P.done = true;
+    return;
+  }
+  const float e2 = exponent2(q, fpx - m.x, fpy - m.y);
+  if (e2 < kE2Min || e2 > 0.0f) return;
+  float al = __fmul_rn(q.w, ex2_approx(e2));
+  if (al < kAlphaSkip) return;
+  al = fminf(al, kAlphaMax);
+  const float w = al * P.T;
+  P.c0 += col.x * w;
+  P.c1 += col.y * w;
+  P.c2 += col.z * w;
+  P.ws += w;
+  P.T = __fmul_rn(P.T, __fsub_rn(1.0f, al));
+  ++P.contrib;
+  P.lastp = pos;
+  if (hits) atomicAdd(hits + gid, 1);
+}
+
+__global__ void __launch_bounds__(kT16Threads) k_blend_fwd16(
+    const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
+    int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
+    float *__restrict__ transmit, float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
+    int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
+  __shared__ Stage S;
+  const int tile = blockIdx.x;
+  const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
+  const int t = threadIdx.x, lane = t & 31;
+  int px, pyA, pyB;
+  pixel_pair16(t, tx, ty, px, pyA, pyB);
+  const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
+  const float4 wb = warp_bounds2(inA, inB, px, pyA, pyB);
+  const int start = offsets[tile], stop = offsets[tile + 1];
+  const float fpx = (float)px, fyA = (float)pyA, fyB = (float)pyB;
+  Fwd16Pixel A, B;
+  A.done = !inA;
+  B.done = !inB;
+  for (int base = start; base < stop; base += kBatch) {
+    if (__syncthreads_count(A.done && B.done) == kT16Threads) break;
+    for (int k = t; k < kBatch && base + k < stop; k += kT16Threads) stage_splat(S, k, splats, ids[base + k]);
+    __syncthreads();
+    const int cnt = min(kBatch, stop - base);
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      if (__all_sync(0xffffffffu, A.done && B.done)) break;
+      const int j = j0 + lane;
+      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
+      while (mask) {
+        const int k = j0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float2 m = S.xy[k];
+        const float4 q = S.q[k], col = S.col[k];
+        const int pos = base - start + k + 1;
+        fwd_entry(A, fpx, fyA, m, q, col, pos, hits, S.id[k]);
+        fwd_entry(B, fpx, fyB, m, q, col, pos, hits, S.id[k]);
+      }
+    }
+    if (A.T < kTTerm) A.done = true;
+    if (B.T < kTTerm) B.done = true;
+  }
+  if (inA) {
+    const int p = pyA * W + px;
+    image[3 * p] = A.c0 + bg0 * A.T;
+    image[3 * p + 1] = A.c1 + bg1 * A.T;
+    image[3 * p + 2] = A.c2 + bg2 * A.T;
+    transmit[p] = A.T;
+    wsum_out[p] = A.ws;
+    n_contrib[p] = A.contrib;
+    last_pos[p] = A.lastp;
+  }
+  if (inB) {
+    const int p = pyB * W + px;
+    image[3 * p] = B.c0 + bg0 * B.T;
+    image[3 * p + 1] = B.c1 + bg1 * B.T;
+    image[3 * p + 2] = B.c2 + bg2 * B.T;
+    transmit[p] = B.T;
+    wsum_out[p] = B.ws;
+    n_contrib[p] = B.contrib;
+    last_pos[p] = B.lastp;
+  }
+}
+
+struct Bwd16Pixel {
+  int lastp = 0;
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 0.f;
+  float GS = 0.f;  // sum_c g_c * S_c, S = suffix colour seeded with bg * T_final
+};
+
+// one list entry of the back-to-front walk for one pixel (_kernels.py:136-181),
+// with dL/dalpha_hat = (g . c) T_before - (g . S) / (1 - a)
+__device__ __forceinline__ bool bwd_entry(Bwd16Pixel &P, int pos, float fpx, float fpy, float2 m, float4 q,
+                                          float4 cn, float4 col, float v[9]) {
+  if (pos >= P.lastp) return false;
+  const float dx = fpx - m.x, dy = fpy - m.y;
+  const float e2 = exponent2(q, dx, dy);
+  if (e2 < kE2Min || e2 > 0.0f) return false;
+  const float gauss = ex2_approx(e2);
+  const float a_raw = __fmul_rn(cn.w, gauss);
+  const float al = fminf(a_raw, kAlphaMax);
+  if (al < kAlphaSkip) return false;
+  const float inv_om = __fdividef(1.0f, 1.0f - al);
+  const float t_before = P.T * inv_om;
+  const float gc = P.g0 * col.x + P.g1 * col.y + P.g2 * col.z;
+  const float ga = gc * t_before - P.GS * inv_om;
+  const float w = al * t_before;
+  v[6] += P.g0 * w;
+  v[7] += P.g1 * w;
+  v[8] += P.g2 * w;
+  if (a_raw <= kAlphaMax) {
+    v[5] += ga * gauss;
+    const float gG = ga * cn.w * gauss;
+    const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
+    v[0] += gG * v0;
+    v[1] += gG * v1;
+    v[2] += gG * 0.5f * v0 * v0;
+    v[3] += gG * v0 * v1;
+    v[4] += gG * 0.5f * v1 * v1;
+  }
+  P.GS += gc * w;
+  P.T = t_before;
+  return true;
+}
+
+struct Bwd16Shared {
+  float2 xy[kT16Threads];
+  float4 q[kT16Threads];
+  float4 conic[kT16Threads];
+  float4 col[kT16Threads];
+  int32_t id[kT16Threads];
+  float acc[kT16Threads / 32][9][kT16Threads];
+};
+
+__global__ void __launch_bounds__(kT16Threads) k_blend_bwd16(
+    const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
+    int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, const float *__restrict__ transmit,
+    const int32_t *__restrict__ last_pos, const float *__restrict__ dimage, float *__restrict__ dsplats) {
+  constexpr int kBB = kT16Threads;
+  constexpr int kW = kT16Threads / 32;
+  __shared__ Bwd16Shared S;
+  __shared__ int wmax[kW];
+  const int tile = blockIdx.x;
+  const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int px, pyA, pyB;
+  pixel_pair16(t, tx, ty, px, pyA, pyB);
+  const int start = offsets[tile];
+  const float fpx = (float)px, fyA = (float)pyA, fyB = (float)pyB;
+  Bwd16Pixel A, B;
+  auto load_pixel = [&](Bwd16Pixel &P, int py) {
+    if (px >= W || py >= H) return;
+    const int p = py * W + px;
+    P.lastp = last_pos[p];
+    P.g0 = dimage[3 * p];
+    P.g1 = dimage[3 * p + 1];
+    P.g2 = dimage[3 * p + 2];
+    if (P.g0 == 0.0f && P.g1 == 0.0f && P.g2 == 0.0f) P.lastp = 0;  // _kernels.py:133-134
+    P.T = transmit[p];
+    P.GS = (P.g0 * bg0 + P.g1 * bg1 + P.g2 * bg2) * P.T;
+  };
+  load_pixel(A, pyA);
+  load_pixel(B, pyB);
+  const float4 wb = warp_bounds2(A.lastp > 0, B.lastp > 0, px, pyA, pyB);
+  const int wlast = __reduce_max_sync(0xffffffffu, max(A.lastp, B.lastp));
+  if (lane == 0) wmax[warp] = wlast;
+  __syncthreads();
+  int max_last = 0;
+#pragma unroll
+  for (int w = 0; w < kW; ++w) max_last = max(max_last, wmax[w]);
+  for (int hi = max_last; hi > 0; hi -= kBB) {
+    const int lo = hi > kBB ? hi - kBB : 0;
+    const int cnt = hi - lo;
+    __syncthreads();
+    if (t < cnt) {
+      const int g = ids[start + lo + t];
+      const float4 a = splats[3 * g], b = splats[3 * g + 1];
+      S.xy[t] = make_float2(a.x, a.y);
+      S.q[t] = prescaled_conic(a, b);
+      S.conic[t] = make_float4(a.z, a.w, b.x, b.y);
+      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, splat_thr2(b.y));
+      S.id[t] = g;
+    }
+    for (int e = t; e < kW * 9 * kBB; e += kT16Threads) (&S.acc[0][0][0])[e] = 0.0f;
+    __syncthreads();
+    for (int j0 = (cnt - 1) & ~31; j0 >= 0; j0 -= 32) {
+      const int j = j0 + lane;
+      uint32_t mask =
+          __ballot_sync(0xffffffffu, j < cnt && lo + j < wlast && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
+      while (mask) {
+        const int bit = 31 - __clz(mask);
+        mask &= ~(1u << bit);
+        const int qi = j0 + bit;
+        const float2 m = S.xy[qi];
+        const float4 q = S.q[qi], cn = S.conic[qi], col = S.col[qi];
+        float v[9];
+#pragma unroll
+        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+        const bool hA = bwd_entry(A, lo + qi, fpx, fyA, m, q, cn, col, v);
+        const bool hB = bwd_entry(B, lo + qi, fpx, fyB, m, q, cn, col, v);
+        if (__any_sync(0xffffffffu, hA || hB)) {
+          const float r8 = warp_reduce8_transpose(v, lane);
+          float r9 = v[8];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+          if ((lane & 3) == 0) S.acc[warp][lane >> 2][qi] = r8;
+          if (lane == 0) S.acc[warp][8][qi] = r9;
+        }
+      }
+    }
+    __syncthreads();
+    if (t < cnt) {
+      float *d = dsplats + 9 * (int64_t)S.id[t];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) {
+        float x = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) x += S.acc[w][f][t];
+        if (x != 0.0f) atomicAdd(d + f, x);
+      }
+    }
+  }
+}
+
 // _kernels.py:184-241: same walk as the forward, writing (gid, a*T) per blended entry
 __global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
                                 const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x,
@@ -428,6 +683,13 @@ extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offset
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
+  if (s->tile_size == 16) {
+    k_blend_fwd16<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
+        row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
+        last_pos, hits);
+    return launch_status();
+  }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
   (B <= 256 ? k_blend_fwd<256> : k_blend_fwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
@@ -459,6 +721,12 @@ extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offse
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
+  if (s->tile_size == 16) {
+    k_blend_bwd16<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
+        row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats);
+    return launch_status();
+  }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
   (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
