@@ -144,12 +144,13 @@ TGS_API int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32
 
 /* ---- (2) binning ----------------------------------------------------------
  * Sort order is the reference's np.lexsort((gid, depth, tile)) (rasterizer.py:143):
- * ascending tile, then depth, then Gaussian index — realised as a stable LSD radix
- * sort of the 64-bit key (tile << 32 | orderable(depth)) whose 32 depth-digit
- * passes run over Gaussians (n items) before duplication and whose tile-digit
- * passes run over instances.  Tiles are restricted to tile rows
- * [row_begin, row_end) (tile-row sharding); tile_offsets has
- * (row_end-row_begin)*tiles_x + 1 entries, relative to the band.
+ * ascending tile, then depth, then Gaussian index.  Because all instances of a
+ * Gaussian share its depth, the order is produced in two steps: a stable sort of
+ * the on-screen GAUSSIANS by their 64-bit depth key (step A, one launch), then a
+ * stable counting placement of the instances into their tile lists in that
+ * depth order (step B) — no per-instance key is materialised.  Tiles are
+ * restricted to tile rows [row_begin, row_end) (tile-row sharding); tile_offsets
+ * has (row_end-row_begin)*tiles_x + 1 entries, relative to the band.
  *
  * depth_keys: per-Gaussian uint64 keys from tgs_preprocess_forward, or NULL to
  * key on the float32 splat depth (the raw-array bin_tiles entry).
@@ -157,7 +158,8 @@ TGS_API int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32
  * Step A: tgs_bin_gaussians() needs a workspace of tgs_bin_gaussians_workspace()
  * bytes, which must stay alive until step B returns.  It writes the instance count
  * to *d_num_instances (device int64).
- * Step B: tgs_bin_instances() with num_instances read back by the caller. */
+ * Step B: tgs_bin_instances() with num_instances read back by the caller and a
+ * workspace of tgs_bin_instances_workspace() bytes (same band arguments). */
 TGS_API int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes);
 TGS_API int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, const uint64_t *depth_keys,
                       int64_t n, int32_t width,
@@ -167,7 +169,8 @@ TGS_API int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched,
  * histogram from which every rank derives the same balanced tile-row bands. */
 TGS_API int tgs_row_histogram(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
                               int32_t height, int32_t tile_size, int64_t *row_counts, tgs_stream_t stream);
-TGS_API int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes);
+TGS_API int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, int32_t width, int32_t height,
+                                        int32_t tile_size, int32_t row_begin, int32_t row_end, size_t *bytes);
 TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int32_t height, int32_t tile_size,
                       int32_t row_begin, int32_t row_end, void *gauss_workspace, int64_t num_instances,
                       void *workspace, int32_t *tile_offsets, int32_t *sorted_ids, tgs_stream_t stream);

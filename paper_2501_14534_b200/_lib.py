@@ -54,7 +54,7 @@ _SIGS = {
     "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
     "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P], _I32),
-    "tgs_bin_instances_workspace": ([_I64, _I64, _P], _I32),
+    "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),
     "tgs_blend_forward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),

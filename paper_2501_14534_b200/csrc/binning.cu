@@ -1,39 +1,29 @@
-// binning.cu — tile binning and the (tile | depth | index) sort (R5).
+// binning.cu — tile binning and the (tile | depth | index) order (R5).
 //
 // Reference: bin_tiles (rasterizer.py:95-148) emits one instance per covered
 // tile (row-major within the Gaussian's rect), then np.lexsort((gid, depth,
 // tile)) and a bincount/cumsum for the CSR offsets.
 //
-// B200 design: a stable LSD radix sort of the key
-//     tile << 64 | orderable(float64 depth)
-// whose value is the Gaussian index (the north star's 64-bit tile|depth key with
-// the depth widened to float64 so ties break exactly like the reference's float64
-// lexsort).  Because every instance of a Gaussian carries the same depth, the
-// eight 8-bit depth passes commute with duplication: they run over the M
-// on-screen GAUSSIANS (M <= n items) instead of the I instances (I = 27*n at c3),
-// and only the ceil(log2 tiles) tile bits are sorted at instance granularity
-// (2 passes at 1080p).  Stability of every pass plus
-// index-ordered emission gives exactly lexsort's (tile, depth, index) order,
-// bit-identical to the oracle.
-//
-// Pass kernels are reduce-then-scan (histogram, device scan of the digit x block
-// matrix, rank + scatter).  Ranking inside a block is warp-synchronous multisplit
-// with __match_any_sync, then a shared-memory reorder so the scatter writes
-// contiguous runs per digit.  Item counts may live on the device (grids are
-// sized for the capacity; blocks past the live count do nothing) so nothing
-// here needs a host round trip except the one instance count the caller reads
-// between tgs_bin_gaussians and tgs_bin_instances.
+// B200 design.  Every instance of a Gaussian carries the Gaussian's depth, so the
+// lexsort factors into
+//   (A) a stable sort of the M on-screen GAUSSIANS by their float64 depth key
+//       (ties by index) — tgs_bin_gaussians, ONE launch: a ticketed chain of
+//       selection tiles and eight 8-bit onesweep passes (decoupled look-back
+//       inside a pass, a completion counter between passes), and
+//   (B) a stable counting sort of the INSTANCES by tile in which no instance key
+//       is ever materialised — tgs_bin_instances: the depth-ordered Gaussians are
+//       cut into chunks of C; a chunk x tile count matrix (u16) gives every chunk
+//       its base offset in every tile list; one warp per chunk then writes each
+//       instance straight to its final slot.  Inside a warp the 32 Gaussians of a
+//       group are ranked per tile by two coverage bitmasks (Gaussians whose
+//       column range / row range contains the tile), so the rank of Gaussian k
+//       in tile (x, y) is popc(col[x] & row[y] & lanes_below(k)).
+// Stability of (A) plus the depth-ordered chunk walk of (B) gives exactly
+// lexsort's (tile, depth, index) order, bit-identical to the oracle.
 #include "tgs_common.cuh"
 #include "tgs_math.cuh"
 
 namespace tgs {
-
-constexpr int kBlock = 256;
-constexpr int kIPT = 16;
-constexpr int kTile = kBlock * kIPT;  // 4096 items per block
-constexpr int kWarps = kBlock / 32;
-
-__device__ __forceinline__ uint32_t live_count(const uint32_t *nd, uint32_t nh) { return nd ? *nd : nh; }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -69,102 +59,10 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
   return res;
 }
 
-// ---------------------------------------------------------------- scan (u32)
-__global__ void __launch_bounds__(kBlock) k_scan_reduce(const uint32_t *__restrict__ in, uint32_t nh,
-                                                        const uint32_t *nd, uint32_t *__restrict__ partials) {
-  __shared__ uint32_t ws[32];
-  const uint32_t n = live_count(nd, nh);
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
-  uint32_t s = 0;
-  if (base < n) {
-    const uint32_t end = (uint32_t)tmin<uint64_t>(base + kTile, n);
-    for (uint32_t j = (uint32_t)base + threadIdx.x; j < end; j += kBlock) s += in[j];
-  }
-  uint32_t tot;
-  block_exclusive_scan(s, ws, &tot);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *partials, int nb, uint32_t *total_u32,
-                                                        int64_t *total_i64) {
-  __shared__ uint32_t ws[32];
-  uint32_t carry = 0;
-  for (int c = 0; c < nb; c += 1024) {
-    const int j = c + threadIdx.x;
-    const uint32_t v = j < nb ? partials[j] : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan(v, ws, &tot);
-    if (j < nb) partials[j] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) {
-    if (total_u32) *total_u32 = carry;
-    if (total_i64) *total_i64 = (int64_t)carry;
-  }
-}
-
-__global__ void __launch_bounds__(kBlock) k_scan_down(const uint32_t *in, uint32_t *out, uint32_t nh,
-                                                      const uint32_t *nd, const uint32_t *__restrict__ partials) {
-  __shared__ uint32_t tile[kTile];
-  __shared__ uint32_t ws[32];
-  const uint32_t n = live_count(nd, nh);
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
-  if (base >= n) return;
-  const uint32_t cnt = (uint32_t)tmin<uint64_t>(kTile, n - base);
-  for (uint32_t j = threadIdx.x; j < kTile; j += kBlock) tile[j] = j < cnt ? in[base + j] : 0u;
-  __syncthreads();
-  uint32_t local[kIPT], s = 0;
-#pragma unroll
-  for (int k = 0; k < kIPT; ++k) {
-    local[k] = tile[threadIdx.x * kIPT + k];
-    s += local[k];
-  }
-  uint32_t run = block_exclusive_scan(s, ws, nullptr) + partials[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < kIPT; ++k) {
-    tile[threadIdx.x * kIPT + k] = run;
-    run += local[k];
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < cnt; j += kBlock) out[base + j] = tile[j];
-}
-
-struct ScanPlan {
-  int nb;
-  uint32_t *partials;
-};
-
-inline size_t scan_ws_bytes(uint64_t cap) { return align_up((ceil_div<uint64_t>(cap, kTile) + 1) * 4); }
-
-// In-place capable exclusive scan of `cap` (host) or *nd (device, <= cap) items.
-inline void device_scan(const uint32_t *in, uint32_t *out, uint64_t cap, const uint32_t *nd, uint32_t *partials,
-                        uint32_t *total_u32, int64_t *total_i64, cudaStream_t st) {
-  const int nb = (int)ceil_div<uint64_t>(cap, kTile);
-  if (nb == 0) {
-    k_scan_partials<<<1, 1024, 0, st>>>(partials, 0, total_u32, total_i64);
-    return;
-  }
-  k_scan_reduce<<<nb, kBlock, 0, st>>>(in, (uint32_t)cap, nd, partials);
-  k_scan_partials<<<1, 1024, 0, st>>>(partials, nb, total_u32, total_i64);
-  k_scan_down<<<nb, kBlock, 0, st>>>(in, out, (uint32_t)cap, nd, partials);
-}
-
-// ------------------------------------------------------------ radix sort
-// Onesweep-style stable LSD radix sort of (K key, u32 value) pairs:
-//   k_sweep_hist  one read of the keys -> global digit histograms of every pass
-//   k_sweep_scan  exclusive scan of each pass's 256 bins (one CTA)
-//   k_sweep_pass  per pass: tiles taken in launch order from an atomic ticket; a
-//                 tile ranks its items (warp multisplit), publishes its per-digit
-//                 counts and resolves its global offsets by decoupled look-back
-//                 over its predecessors, then scatters through shared memory in
-//                 contiguous per-digit runs.
-// A tile only ever waits for tiles with smaller tickets, which are already
-// resident, so the look-back cannot deadlock.
+// Look-back status words: flag | count in one 32-bit word, so relaxed GPU-scope
+// accesses suffice (no acquire fence, which costs an L1 invalidate per probe).
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
-// The status word IS the payload (flag | count in one 32-bit word), so relaxed
-// GPU-scope accesses suffice: no acquire fence (which costs an L1 invalidate per
-// probe on sm_100) and no release fence.
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -173,443 +71,868 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
 __device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-template <typename K>
-constexpr int lookback_for() {  // predecessors probed per step (independent loads in flight)
-  return sizeof(K) == 8 ? 32 : 16;
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-template <typename K>
-constexpr int ipt_for() {
-  return sizeof(K) == 8 ? 8 : kIPT;  // 64-bit keys: 2048-item tiles keep smem at 24 KB + counters
-}
-template <typename K>
-constexpr int tile_for() {
-  return kBlock * ipt_for<K>();
-}
-
-constexpr int kFullHistSmem = 8192;  // full-key histogram bins kept in shared memory
-
-// Digit histograms of every pass in one read of the keys; optionally also the
-// full-key histogram (the per-tile instance counts -> CSR offsets, replacing a
-// boundary scan over the sorted keys).
-template <typename K>
-__global__ void __launch_bounds__(kBlock) k_sweep_hist(const K *__restrict__ keys, uint32_t nh, const uint32_t *nd,
-                                                       int npasses, int bpp, int total_bits,
-                                                       uint32_t *__restrict__ gbins, uint32_t *__restrict__ full_hist,
-                                                       int full_bins) {
-  __shared__ uint32_t h[8][256];
-  __shared__ uint32_t fh[kFullHistSmem];
-  const bool fsh = full_hist && full_bins <= kFullHistSmem;
-  for (int e = threadIdx.x; e < npasses * 256; e += kBlock) (&h[0][0])[e] = 0;
-  if (fsh)
-    for (int e = threadIdx.x; e < full_bins; e += kBlock) fh[e] = 0;
-  __syncthreads();
-  const uint32_t n = live_count(nd, nh);
-  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
-    const K k = keys[i];
-    for (int p = 0; p < npasses; ++p) {
-      const int sh = p * bpp;
-      const int nb = min(bpp, total_bits - sh);
-      atomicAdd(&h[p][(uint32_t)(k >> sh) & ((1u << nb) - 1)], 1u);
-    }
-    if (full_hist) atomicAdd(fsh ? &fh[(uint32_t)k] : &full_hist[(uint32_t)k], 1u);
+// Decoupled look-back for one counter: publish `agg` for `tile`, return the
+// exclusive prefix of all earlier tiles (which hold earlier tickets, so they are
+// resident or finished — the wait cannot deadlock).
+template <int W>
+__device__ __forceinline__ uint32_t lookback(uint32_t *status, size_t stride, uint32_t tile, uint32_t agg) {
+  uint32_t *mine = status + (size_t)tile * stride;
+  if (tile == 0) {
+    st_relaxed(mine, kFlagInc | agg);
+    return 0;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < npasses * 256; e += kBlock) {
-    const uint32_t v = (&h[0][0])[e];
-    if (v) atomicAdd(gbins + e, v);
-  }
-  if (fsh)
-    for (int e = threadIdx.x; e < full_bins; e += kBlock)
-      if (fh[e]) atomicAdd(full_hist + e, fh[e]);
-}
-
-// CSR offsets (int32, bins + 1) from the full-key histogram: one CTA, chunked scan.
-__global__ void __launch_bounds__(1024) k_offsets_from_hist(const uint32_t *__restrict__ hist, int bins,
-                                                            int32_t *__restrict__ offsets) {
-  __shared__ uint32_t ws[32];
-  uint32_t carry = 0;
-  for (int c = 0; c < bins; c += 1024) {
-    const int j = c + threadIdx.x;
-    const uint32_t v = j < bins ? hist[j] : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan(v, ws, &tot);
-    if (j < bins) offsets[j] = (int32_t)(carry + ex);
-    carry += tot;
-  }
-  if (threadIdx.x == 0) offsets[bins] = (int32_t)carry;
-}
-
-__global__ void __launch_bounds__(kBlock) k_sweep_scan(uint32_t *gbins, int npasses) {
-  __shared__ uint32_t ws[32];
-  for (int p = 0; p < npasses; ++p) {
-    const uint32_t v = gbins[p * 256 + threadIdx.x];
-    const uint32_t ex = block_exclusive_scan(v, ws, nullptr);
-    gbins[p * 256 + threadIdx.x] = ex;
-  }
-}
-
-template <typename K, int IPT>
-__global__ void __launch_bounds__(kBlock, 3) k_sweep_pass(const K *__restrict__ keys_in,
-                                                       const uint32_t *__restrict__ vals_in,
-                                                       K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-                                                       uint32_t nh, const uint32_t *nd, int shift, int nbits,
-                                                       const uint32_t *__restrict__ bin_base,
-                                                       uint32_t *__restrict__ status, uint32_t *__restrict__ ticket) {
-  constexpr int TILE = kBlock * IPT;
-  __shared__ K ks[TILE];
-  __shared__ uint32_t vs[TILE];
-  __shared__ uint32_t wcnt[kWarps][256];
-  __shared__ uint32_t dstart[256];
-  __shared__ uint32_t gbase[256];
-  __shared__ uint32_t wsum[32];
-  __shared__ uint32_t s_tile;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint32_t n = live_count(nd, nh);
-  const uint64_t base = (uint64_t)tile * TILE;
-  if (base >= n) return;
-  const int bins = 1 << nbits;
-  const uint32_t mask = bins - 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = threadIdx.x; j < kWarps * 256; j += kBlock) (&wcnt[0][0])[j] = 0;
-  __syncthreads();
-  const uint32_t lt = lanemask_lt();
-  K key[IPT];
-  uint32_t val[IPT];
-  uint16_t rank[IPT];
-  const uint64_t wbase = base + (uint64_t)warp * (IPT * 32);
-  // warp-synchronous multisplit: ranks are stable in index order (warp-major,
-  // then round, then lane), matching the tile's item order
-  // all loads first: the multisplit below synchronises the warp every round, and
-  // loads cannot be hoisted across those synchronisation points
+  st_relaxed(mine, kFlagAgg | agg);
+  uint32_t excl = 0;
+  int j = (int)tile - 1;
+  bool found = false;
+  while (!found) {
+    uint32_t v[W];
 #pragma unroll
-  for (int r = 0; r < IPT; ++r) {
-    const uint64_t j = wbase + r * 32 + lane;
-    const bool ok = j < n;
-    key[r] = ok ? keys_in[j] : (K)0;
-    val[r] = ok ? vals_in[j] : 0u;
-  }
+    for (int k = 0; k < W; ++k) v[k] = (j - k >= 0) ? ld_relaxed(status + (size_t)(j - k) * stride) : kFlagInc;
+    int used = 0;
 #pragma unroll
-  for (int r = 0; r < IPT; ++r) {
-    const uint64_t j = wbase + r * 32 + lane;
-    const bool ok = j < n;
-    const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
-    rank[r] = 0;
-    if (ok) {
-      const uint32_t d = (uint32_t)(key[r] >> shift) & mask;
-      const uint32_t peers = __match_any_sync(okmask, d);
-      const uint32_t prev = wcnt[warp][d];
-      rank[r] = (uint16_t)(prev + __popc(peers & lt));
-      __syncwarp(okmask);
-      if (lane == __ffs(peers) - 1) wcnt[warp][d] = prev + __popc(peers);
+    for (int k = 0; k < W; ++k) {
+      if (found || (v[k] >> 30) == 0) break;  // stop at the first unpublished predecessor
+      excl += v[k] & kValMask;
+      found = (v[k] & kFlagInc) != 0;
+      ++used;
     }
-    __syncwarp();
+    j -= found ? 0 : used;
   }
-  __syncthreads();
-  uint32_t dtotal = 0;
-  if (threadIdx.x < (unsigned)bins) {
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = wcnt[w][threadIdx.x];
-      wcnt[w][threadIdx.x] = dtotal;
-      dtotal += c;
-    }
-  }
-  const uint32_t ds = block_exclusive_scan(threadIdx.x < (unsigned)bins ? dtotal : 0u, wsum, nullptr);
-  if (threadIdx.x < (unsigned)bins) {
-    dstart[threadIdx.x] = ds;
-    // decoupled look-back over the predecessors' per-digit counts
-    uint32_t *mine = status + (size_t)tile * 256 + threadIdx.x;
-    uint32_t excl = 0;
-    if (tile == 0) {
-      st_relaxed(mine, kFlagInc | dtotal);
-    } else {
-      st_relaxed(mine, kFlagAgg | dtotal);
-      int j = (int)tile - 1;
-      bool found = false;
-      while (!found) {
-        constexpr int kLookback = lookback_for<K>();
-        uint32_t v[kLookback];
-#pragma unroll
-        for (int k = 0; k < kLookback; ++k)
-          v[k] = (j - k >= 0) ? ld_relaxed(status + (size_t)(j - k) * 256 + threadIdx.x) : kFlagInc;
-        int used = 0;
-#pragma unroll
-        for (int k = 0; k < kLookback; ++k) {
-          if (found || (v[k] >> 30) == 0) break;  // stop at the first unpublished predecessor
-          excl += v[k] & kValMask;
-          found = (v[k] & kFlagInc) != 0;
-          ++used;
-        }
-        j -= found ? 0 : used;  // resume at the first predecessor not yet consumed
-      }
-      st_relaxed(mine, kFlagInc | (excl + dtotal));
-    }
-    gbase[threadIdx.x] = bin_base[threadIdx.x] + excl;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < IPT; ++r) {
-    const uint64_t j = wbase + r * 32 + lane;
-    if (j < n) {
-      const uint32_t d = (uint32_t)(key[r] >> shift) & mask;
-      const uint32_t p = dstart[d] + wcnt[warp][d] + rank[r];
-      ks[p] = key[r];
-      vs[p] = val[r];
-    }
-  }
-  __syncthreads();
-  // contiguous runs per digit -> coalesced scatter
-  const uint32_t cnt = (uint32_t)tmin<uint64_t>(TILE, n - base);
-  for (uint32_t j = threadIdx.x; j < cnt; j += kBlock) {
-    const K k = ks[j];
-    const uint32_t d = (uint32_t)(k >> shift) & mask;
-    const uint32_t o = gbase[d] + (j - dstart[d]);
-    if (keys_out) keys_out[o] = k;
-    vals_out[o] = vs[j];
-  }
+  st_relaxed(mine, kFlagInc | (excl + agg));
+  return excl;
 }
 
-struct SortScratch {
-  uint32_t *gbins;      // passes * 256
-  uint32_t *status;     // passes * tiles * 256
-  uint32_t *ticket;     // passes
-  uint32_t *full_hist;  // full_bins (optional)
-  size_t bytes_zeroed;
-};
-
-template <typename K>
-inline size_t sort_ws_bytes(uint64_t cap, int passes) {
-  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
-  return align_up((size_t)passes * 256 * 4) + align_up((size_t)passes * tiles * 256 * 4) + align_up(passes * 4);
-}
-
-template <typename K>
-inline SortScratch carve_sort(Carve &c, uint64_t cap, int passes, size_t full_bins = 0) {
-  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
-  SortScratch s;
-  const size_t off0 = c.off;
-  s.gbins = c.take<uint32_t>((size_t)passes * 256);
-  s.status = c.take<uint32_t>((size_t)passes * tiles * 256);
-  s.ticket = c.take<uint32_t>(passes);
-  s.full_hist = full_bins ? c.take<uint32_t>(full_bins) : nullptr;
-  s.bytes_zeroed = c.off - off0;
-  return s;
-}
-
-// Stable sort of `cap` (or *nd) items by bits [0, total_bits) of the key, in
-// `passes` passes of <= 8 bits.  Ping-pongs A <-> B; returns true when the
-// result ended in the B buffers.
-// hist_ready: the caller already wrote the exclusive-scanned digit histograms of
-// every pass to sc.gbins (and zeroed the look-back state); last_keys: write the
-// keys on the final pass (not needed when the CSR offsets come from a histogram).
-template <typename K>
-inline bool radix_sort(K *kA, uint32_t *vA, K *kB, uint32_t *vB, uint64_t cap, const uint32_t *nd, int total_bits,
-                       SortScratch sc, cudaStream_t st, bool hist_ready = false, bool last_keys = true) {
-  const int passes = (total_bits + 7) / 8;
-  if (cap == 0 || passes == 0) return false;
-  const int bpp = (total_bits + passes - 1) / passes;
-  const uint64_t tiles = ceil_div<uint64_t>(cap, tile_for<K>());
-  if (!hist_ready) {
-    cudaMemsetAsync(sc.gbins, 0, sc.bytes_zeroed, st);
-    const unsigned hgrid = (unsigned)tmin<uint64_t>(ceil_div<uint64_t>(cap, kBlock * 16), 148 * 4);
-    k_sweep_hist<K><<<hgrid, kBlock, 0, st>>>(kA, (uint32_t)cap, nd, passes, bpp, total_bits, sc.gbins, nullptr, 0);
-    k_sweep_scan<<<1, kBlock, 0, st>>>(sc.gbins, passes);
-  }
-  K *kin = kA, *kout = kB;
-  uint32_t *vin = vA, *vout = vB;
-  for (int p = 0; p < passes; ++p) {
-    const int sh = p * bpp;
-    k_sweep_pass<K, ipt_for<K>()><<<(unsigned)tiles, kBlock, 0, st>>>(
-        kin, vin, (p == passes - 1 && !last_keys) ? nullptr : kout, vout, (uint32_t)cap, nd, sh,
-        min(bpp, total_bits - sh), sc.gbins + p * 256,
-        sc.status + (size_t)p * tiles * 256, sc.ticket + p);
-    K *tk = kin; kin = kout; kout = tk;
-    uint32_t *tv = vin; vin = vout; vout = tv;
-  }
-  return passes % 2 == 1;
-}
-
-// ------------------------------------------------------- Gaussian stage
+// ------------------------------------------------------------------ bands
 struct Band {
   int W, H, ts, tiles_x, tiles_y, row_begin, row_end;
 };
 
-// Band-restricted tile count of Gaussian i (0 when off-screen / not visible).
+// Band-restricted tile rect of a projected record (0 when off-screen / outside the band).
 __device__ __forceinline__ int band_rect(const float *sp, const Band &b, int &x0, int &y0, int &x1, int &y1) {
-  const float4 a = reinterpret_cast<const float4 *>(sp)[0];
-  const float4 c = reinterpret_cast<const float4 *>(sp)[2];
-  const int n = tile_rect(a.x, a.y, c.z, b.W, b.H, b.ts, b.tiles_x, b.tiles_y, x0, y0, x1, y1);
+  const float4 a = __ldg(reinterpret_cast<const float4 *>(sp));
+  const float r = __ldg(sp + 10);
+  const int n = tile_rect(a.x, a.y, r, b.W, b.H, b.ts, b.tiles_x, b.tiles_y, x0, y0, x1, y1);
   if (n == 0) return 0;
   y0 = max(y0, b.row_begin);
   y1 = min(y1, b.row_end - 1);
   return y1 >= y0 ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0;
 }
 
-__global__ void k_select(const float *__restrict__ splats, const int32_t *__restrict__ tiles_touched, int64_t n,
-                         Band b, uint32_t *__restrict__ cnt, uint32_t *__restrict__ flag) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t c = 0;
-  if (tiles_touched[i] > 0) {
-    int x0, y0, x1, y1;
-    c = (uint32_t)band_rect(splats + 12 * i, b, x0, y0, x1, y1);
+// Band rect packed as (x0 | x1 << 16, y0 | y1 << 16), rows relative to the band.
+__device__ __forceinline__ uint2 pack_rect(int x0, int y0, int x1, int y1) {
+  return make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+}
+
+// ======================================================= (A) depth sort
+// One launch.  Tickets [0, T0) are selection tiles over the n Gaussians (in-band
+// test, index-order compaction by look-back, digit histograms of all passes, the
+// instance total); tickets T0 + p*TP + j are tile j of radix pass p.  A pass tile
+// first waits for the completion counter of the stage feeding it; every stage it
+// waits on holds strictly earlier tickets, so the chain is deadlock-free without
+// any co-residency assumption.
+constexpr int kDsThreads = 512;
+constexpr int kDsIPT = 8;
+constexpr int kDsTile = kDsThreads * kDsIPT;  // 4096 items per tile
+constexpr int kDsWarps = kDsThreads / 32;
+constexpr int kDsPasses = 8;                  // 64-bit keys, 8-bit digits
+constexpr int kDsLookback = 16;
+
+struct DsCtl {                       // zeroed before every launch
+  uint32_t ticket;
+  uint32_t m;                        // selected Gaussians
+  uint32_t done[kDsPasses + 1];      // done[0]: selection tiles; done[p]: tiles of pass p-1
+  uint32_t pad[5];
+  uint32_t hist[kDsPasses][256];     // global digit histograms
+};
+
+struct DsArgs {
+  const float *splats;
+  const int32_t *tiles_touched;
+  const uint64_t *depth_keys;        // may be null: key on the float32 splat depth
+  uint32_t n;
+  Band b;
+  uint64_t *keysA, *keysB;
+  uint32_t *valsA, *valsB;
+  DsCtl *ctl;
+  uint2 *rect_by_gid;                // n: band rect of each selected Gaussian (packed u16 pairs)
+  uint2 *rects_sorted;               // M: the same, in depth order (written by the last pass)
+  uint32_t *sel_status;              // T0
+  uint32_t *status;                  // kDsPasses * TP * 256
+  uint32_t T0, TP;
+  unsigned long long *num_instances;
+};
+
+__device__ __forceinline__ void wait_count(const uint32_t *p, uint32_t need) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(p) < need) __nanosleep(128);
+  __syncthreads();
+}
+__device__ __forceinline__ void signal_done(uint32_t *p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p, 1u);
   }
-  cnt[i] = c;
-  flag[i] = c > 0;
 }
 
-__global__ void k_compact(const float *__restrict__ splats, const uint64_t *__restrict__ depth_keys,
-                          const uint32_t *__restrict__ cnt, const uint32_t *__restrict__ pos, int64_t n,
-                          uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || cnt[i] == 0) return;
-  const uint32_t p = pos[i];
-  keys[p] = depth_keys ? depth_keys[i] : orderable_key64((double)splats[12 * i + 9]);
-  vals[p] = (uint32_t)i;
-}
+struct DsSmem {
+  union {
+    struct {
+      uint64_t ks[kDsTile];
+      uint32_t vs[kDsTile];
+      uint32_t wcnt[kDsWarps][256];
+    } pass;
+    struct {
+      uint32_t hist[kDsPasses][256];
+    } sel;
+  };
+  uint32_t dstart[256];
+  uint32_t gbase[256];
+  uint32_t wsum[32];
+  uint32_t ticket, m, excl;
+  unsigned long long inst;
+};
 
-__global__ void k_gather_counts(const uint32_t *__restrict__ ids, const uint32_t *__restrict__ cnt, int64_t cap,
-                                const uint32_t *nd, uint32_t *__restrict__ out) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= cap || j >= (int64_t)*nd) return;
-  out[j] = cnt[ids[j]];
-}
-
-// Warp-cooperative expansion: each warp owns 32 depth-ordered Gaussians and
-// emits their band tiles row-major with lane-strided, coalesced stores.
-__global__ void k_duplicate(const float *__restrict__ splats, const uint32_t *__restrict__ ids,
-                            const uint32_t *__restrict__ inst_off, int64_t cap, const uint32_t *nd, Band b,
-                            uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t m = *nd;
-  const int lane = threadIdx.x & 31;
-  int x0 = 0, y0 = 0, x1 = -1, y1 = -1, cnt = 0;
-  uint32_t g = 0, off = 0;
-  if (j < m && j < cap) {
-    g = ids[j];
-    off = inst_off[j];
-    cnt = band_rect(splats + 12 * (int64_t)g, b, x0, y0, x1, y1);
-  }
-  const uint32_t base_tile = (uint32_t)b.row_begin * b.tiles_x;
-  uint32_t todo = __ballot_sync(0xffffffffu, cnt > 0);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const int sc = __shfl_sync(0xffffffffu, cnt, src);
-    const int sx0 = __shfl_sync(0xffffffffu, x0, src);
-    const int sy0 = __shfl_sync(0xffffffffu, y0, src);
-    const int snx = __shfl_sync(0xffffffffu, x1 - x0 + 1, src);
-    const uint32_t sg = __shfl_sync(0xffffffffu, g, src);
-    const uint32_t so = __shfl_sync(0xffffffffu, off, src);
-    for (int e = lane; e < sc; e += 32) {
-      const int row = e / snx, col = e - row * snx;
-      keys[so + e] = (uint32_t)(sy0 + row) * b.tiles_x + (uint32_t)(sx0 + col) - base_tile;
-      vals[so + e] = sg;
+__device__ void ds_select_tile(const DsArgs &a, DsSmem &sm, uint32_t t) {
+  for (int e = threadIdx.x; e < kDsPasses * 256; e += kDsThreads) (&sm.sel.hist[0][0])[e] = 0;
+  if (threadIdx.x == 0) sm.inst = 0;
+  __syncthreads();
+  // blocked layout: thread owns 8 consecutive Gaussians -> compaction in index order
+  const uint32_t i0 = t * kDsTile + threadIdx.x * kDsIPT;
+  uint64_t key[kDsIPT];
+  uint32_t flags = 0, cnt_sum = 0, nsel = 0;
+#pragma unroll
+  for (int r = 0; r < kDsIPT; ++r) {
+    const uint32_t i = i0 + r;
+    key[r] = 0;
+    if (i < a.n && a.tiles_touched[i] > 0) {
+      int x0, y0, x1, y1;
+      const int c = band_rect(a.splats + 12 * (size_t)i, a.b, x0, y0, x1, y1);
+      if (c > 0) {
+        a.rect_by_gid[i] = pack_rect(x0, y0 - a.b.row_begin, x1, y1 - a.b.row_begin);
+        flags |= 1u << r;
+        cnt_sum += (uint32_t)c;
+        ++nsel;
+        key[r] = a.depth_keys ? a.depth_keys[i] : orderable_key64((double)a.splats[12 * (size_t)i + 9]);
+      }
     }
   }
-}
-
-// Per-tile instance counts from the Gaussians' rectangles: a 2D difference array
-// (+1/-1 at the four corners of each band-clipped rect, 4 atomics per Gaussian)
-// integrated by k_tile_hist_finalize.  Grid (rows + 1) x (tiles_x + 1), int32.
-constexpr int kDiffSmem = 12288;
-
-__global__ void __launch_bounds__(256) k_tile_hist2d(const float *__restrict__ splats, const uint32_t *__restrict__ ids,
-                                                     int64_t cap, const uint32_t *nd, Band b,
-                                                     int32_t *__restrict__ diff) {
-  extern __shared__ int32_t dsm[];
-  const int gw = b.tiles_x + 1, gh = b.row_end - b.row_begin + 1;
-  const int cells = gw * gh;
-  const bool priv = cells <= kDiffSmem;
-  if (priv)
-    for (int e = threadIdx.x; e < cells; e += blockDim.x) dsm[e] = 0;
+  uint32_t total;
+  const uint32_t off = block_exclusive_scan(nsel, sm.wsum, &total);
+  if (threadIdx.x == 0) {
+    sm.excl = lookback<kDsLookback>(a.sel_status, 1, t, total);
+    atomicAdd(&a.ctl->m, total);
+  }
+  atomicAdd(&sm.inst, (unsigned long long)cnt_sum);
   __syncthreads();
-  int32_t *d = priv ? dsm : diff;
-  const int64_t m = tmin<int64_t>(*nd, cap);
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-    int x0, y0, x1, y1;
-    if (band_rect(splats + 12 * (int64_t)ids[j], b, x0, y0, x1, y1) == 0) continue;
-    y0 -= b.row_begin;
-    y1 -= b.row_begin;
-    atomicAdd(&d[y0 * gw + x0], 1);
-    atomicAdd(&d[y0 * gw + x1 + 1], -1);
-    atomicAdd(&d[(y1 + 1) * gw + x0], -1);
-    atomicAdd(&d[(y1 + 1) * gw + x1 + 1], 1);
+  uint32_t pos = sm.excl + off;
+#pragma unroll
+  for (int r = 0; r < kDsIPT; ++r) {
+    if (flags >> r & 1u) {
+      a.keysA[pos] = key[r];
+      a.valsA[pos] = i0 + r;
+      ++pos;
+#pragma unroll
+      for (int p = 0; p < kDsPasses; ++p) atomicAdd(&sm.sel.hist[p][(uint32_t)(key[r] >> (8 * p)) & 255u], 1u);
+    }
   }
   __syncthreads();
-  if (priv)
-    for (int e = threadIdx.x; e < cells; e += blockDim.x)
-      if (dsm[e]) atomicAdd(diff + e, dsm[e]);
+  for (int e = threadIdx.x; e < kDsPasses * 256; e += kDsThreads) {
+    const uint32_t v = (&sm.sel.hist[0][0])[e];
+    if (v) atomicAdd(&a.ctl->hist[0][0] + e, v);
+  }
+  if (threadIdx.x == 0 && sm.inst) atomicAdd(a.num_instances, sm.inst);
+  signal_done(&a.ctl->done[0]);
 }
 
-// One CTA: integrate the difference grid into per-tile counts, write the CSR
-// offsets, and derive the exclusive digit histograms of every radix pass of the
-// tile key (so the instance sort needs no histogram pass over its keys).
-__global__ void __launch_bounds__(1024) k_tile_hist_finalize(int32_t *__restrict__ diff, int tiles_x, int rows,
-                                                             int passes, int bpp, int total_bits,
-                                                             int32_t *__restrict__ offsets,
-                                                             uint32_t *__restrict__ gbins) {
-  __shared__ uint32_t ws[32];
-  __shared__ uint32_t gb[4][256];
-  const int gw = tiles_x + 1;
-  for (int e = threadIdx.x; e < 4 * 256; e += 1024) (&gb[0][0])[e] = 0;
-  // prefix along x then along y, one warp per row / column (warp scans with carry)
+__device__ void ds_pass_tile(const DsArgs &a, DsSmem &sm, int p, uint32_t j, uint32_t m) {
+  const uint64_t *keys_in = (p & 1) ? a.keysB : a.keysA;
+  const uint32_t *vals_in = (p & 1) ? a.valsB : a.valsA;
+  uint64_t *keys_out = (p & 1) ? a.keysA : a.keysB;
+  uint32_t *vals_out = (p & 1) ? a.valsA : a.valsB;
+  const bool last = p == kDsPasses - 1;
+  const int shift = 8 * p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < rows; r += 32) {
-    int32_t carry_r = 0;
-    for (int x0 = 0; x0 < tiles_x; x0 += 32) {
-      const int x = x0 + lane;
-      int32_t v = x < tiles_x ? diff[r * gw + x] : 0;
+  for (int e = threadIdx.x; e < kDsWarps * 256; e += kDsThreads) (&sm.pass.wcnt[0][0])[e] = 0;
+  const uint64_t base = (uint64_t)j * kDsTile;
+  const uint64_t wbase = base + (uint64_t)warp * (kDsIPT * 32);
+  uint64_t key[kDsIPT];
+  uint32_t val[kDsIPT];
+  uint16_t rank[kDsIPT];
+  // all loads first (L2 only: the buffers were written by other CTAs of this launch)
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      if (x < tiles_x) diff[r * gw + x] = v + carry_r;
-      carry_r += __shfl_sync(0xffffffffu, v, 31);
-    }
+  for (int r = 0; r < kDsIPT; ++r) {
+    const uint64_t q = wbase + r * 32 + lane;
+    const bool ok = q < m;
+    key[r] = ok ? (uint64_t)__ldcg(reinterpret_cast<const unsigned long long *>(keys_in) + q) : 0ull;
+    val[r] = ok ? __ldcg(vals_in + q) : 0u;
   }
   __syncthreads();
-  for (int x = warp; x < tiles_x; x += 32) {
-    int32_t carry_c = 0;
-    for (int r0 = 0; r0 < rows; r0 += 32) {
-      const int r = r0 + lane;
-      int32_t v = r < rows ? diff[r * gw + x] : 0;
+  const uint32_t lt = lanemask_lt();
+  // warp-synchronous multisplit: ranks stable in item order (warp-major, round, lane)
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      if (r < rows) diff[r * gw + x] = v + carry_c;
-      carry_c += __shfl_sync(0xffffffffu, v, 31);
+  for (int r = 0; r < kDsIPT; ++r) {
+    const uint64_t q = wbase + r * 32 + lane;
+    const bool ok = q < m;
+    const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
+    rank[r] = 0;
+    if (ok) {
+      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+      const uint32_t peers = __match_any_sync(okmask, d);
+      const uint32_t prev = sm.pass.wcnt[warp][d];
+      rank[r] = (uint16_t)(prev + __popc(peers & lt));
+      __syncwarp(okmask);
+      if (lane == __ffs(peers) - 1) sm.pass.wcnt[warp][d] = prev + __popc(peers);
     }
+    __syncwarp();
   }
   __syncthreads();
-  const int ntiles = rows * tiles_x;
+  uint32_t dtotal = 0;
+  if (threadIdx.x < 256) {
+    for (int w = 0; w < kDsWarps; ++w) {
+      const uint32_t c = sm.pass.wcnt[w][threadIdx.x];
+      sm.pass.wcnt[w][threadIdx.x] = dtotal;
+      dtotal += c;
+    }
+  }
+  const uint32_t ds = block_exclusive_scan(threadIdx.x < 256 ? dtotal : 0u, sm.wsum, nullptr);
+  if (threadIdx.x < 256) sm.dstart[threadIdx.x] = ds;
+  __syncthreads();
+  // local reorder first (frees the key registers), then the look-back
+#pragma unroll
+  for (int r = 0; r < kDsIPT; ++r) {
+    const uint64_t q = wbase + r * 32 + lane;
+    if (q < m) {
+      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+      const uint32_t s = sm.dstart[d] + sm.pass.wcnt[warp][d] + rank[r];
+      sm.pass.ks[s] = key[r];
+      sm.pass.vs[s] = val[r];
+    }
+  }
+  if (threadIdx.x < 256) {
+    const uint32_t excl = lookback<kDsLookback>(a.status + (size_t)p * a.TP * 256 + threadIdx.x, 256, j, dtotal);
+    sm.gbase[threadIdx.x] += excl;  // gbase holds this pass's exclusive digit base
+  }
+  __syncthreads();
+  const uint32_t cnt = (uint32_t)tmin<uint64_t>(kDsTile, m - base);
+  for (uint32_t e = threadIdx.x; e < cnt; e += kDsThreads) {
+    const uint64_t k = sm.pass.ks[e];
+    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const uint32_t o = sm.gbase[d] + (e - sm.dstart[d]);
+    if (!last) __stcg(reinterpret_cast<unsigned long long *>(keys_out) + o, (unsigned long long)k);
+    const uint32_t v = sm.pass.vs[e];
+    __stcg(vals_out + o, v);
+    if (last) {
+      const uint2 rc = __ldcg(a.rect_by_gid + v);
+      __stcg(a.rects_sorted + o, rc);
+    }
+  }
+  signal_done(&a.ctl->done[p + 1]);
+}
+
+__global__ void __launch_bounds__(kDsThreads, 2) k_depth_sort(DsArgs a) {
+  extern __shared__ __align__(16) unsigned char ds_raw[];
+  DsSmem &sm = *reinterpret_cast<DsSmem *>(ds_raw);
+  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.ctl->ticket, 1u);
+  __syncthreads();
+  const uint32_t t = sm.ticket;
+  if (t < a.T0) {
+    ds_select_tile(a, sm, t);
+    return;
+  }
+  const int p = (int)((t - a.T0) / a.TP);
+  const uint32_t j = (t - a.T0) % a.TP;
+  wait_count(&a.ctl->done[0], a.T0);
+  if (threadIdx.x == 0) sm.m = __ldcg(&a.ctl->m);
+  __syncthreads();
+  const uint32_t m = sm.m;
+  const uint32_t live = (m + kDsTile - 1) / kDsTile;
+  if (j >= live) return;
+  // this pass's exclusive digit base (from the selection histograms)
+  const uint32_t h = threadIdx.x < 256 ? __ldcg(&a.ctl->hist[p][threadIdx.x]) : 0u;
+  const uint32_t hb = block_exclusive_scan(h, sm.wsum, nullptr);
+  if (threadIdx.x < 256) sm.gbase[threadIdx.x] = hb;
+  if (p > 0) wait_count(&a.ctl->done[p], live);
+  __syncthreads();
+  ds_pass_tile(a, sm, p, j, m);
+}
+
+struct GaussWS {
+  uint64_t *keysA, *keysB;
+  uint32_t *valsA, *valsB;  // valsA: depth-ordered Gaussian ids after the sort
+  uint2 *rect_by_gid, *rects_sorted;
+  DsCtl *ctl;
+  uint32_t *sel_status, *status;
+  uint32_t T0, TP;
+  size_t zero_off, zero_bytes, bytes;
+};
+
+inline GaussWS carve_gauss(void *p, int64_t n) {
+  Carve c(p);
+  GaussWS w;
+  const size_t N = (size_t)tmax<int64_t>(n, 1);
+  w.T0 = (uint32_t)ceil_div<size_t>(N, kDsTile);
+  w.TP = w.T0;
+  w.keysA = c.take<uint64_t>(N);
+  w.keysB = c.take<uint64_t>(N);
+  w.valsA = c.take<uint32_t>(N);
+  w.valsB = c.take<uint32_t>(N);
+  w.rect_by_gid = c.take<uint2>(N);
+  w.rects_sorted = c.take<uint2>(N);
+  w.zero_off = c.off;
+  w.ctl = c.take<DsCtl>(1);
+  w.sel_status = c.take<uint32_t>(w.T0);
+  w.status = c.take<uint32_t>((size_t)kDsPasses * w.TP * 256);
+  w.zero_bytes = c.off - w.zero_off;
+  w.bytes = c.off;
+  return w;
+}
+
+// ================================================= (B) instance placement
+// Two levels.  Super-tiles are 8x8 tiles.
+//  L1 places ENTRIES (Gaussian, super-tile it overlaps) — ~1.5 per Gaussian
+//     instead of ~30 instances — into per-super-tile lists, stably in depth order:
+//     the depth-ordered Gaussians are cut into chunks of C = 512 and the chunks
+//     into segments of kSeg; rel[c][S] (u16) counts the Gaussians of earlier
+//     chunks of c's segment overlapping super-tile S, segbase[s][S] (u32) those of
+//     earlier segments, and inside a chunk an entry's rank comes from 64-bit
+//     coverage masks (Gaussians whose super-tile column / row range contains S).
+//  L2 places the INSTANCES of one super-tile: its entries are split over 16
+//     warps; per round of 32 entries a warp builds 8 column and 8 row ballots,
+//     lane L owns tiles L and L + 32 of the super-tile, and writes the ids of the
+//     entries covering them in order (bit iteration over col & row masks).
+//  The per-tile CSR offsets come from the L2 per-unit counts.
+constexpr int kST = 8;                  // super-tile edge in tiles
+constexpr int kSTShift = 3;
+constexpr int kChunk = 512;             // Gaussians per chunk = 8 warps x 64
+constexpr int kChunkWarps = kChunk / 64;
+constexpr int kSeg = 4;                 // chunks per segment (counted by one CTA, in order)
+constexpr int kDiffCells = 12288;       // 2D difference cells per count CTA
+constexpr int kUnit = 8192;             // entries per L1 scatter CTA
+constexpr int kScanCols = 128;          // bins per segment-scan CTA
+constexpr int kScanGroups = 8;          // segment ranges per segment-scan CTA
+constexpr int kPlaceWarps = 16;
+constexpr int kPUnit = 2048;            // entries per L2 unit
+
+struct InstGeom {
+  uint32_t nchunks, nseg, NS, T;        // NS super-tiles, T tiles (band)
+  int sx, sy;                           // super-tile grid
+  int slab_rows, slabs;                 // super-tile-row slabs of the count kernel
+  uint64_t ecap;                        // entry capacity
+  uint32_t punits;                      // L2 unit capacity
+};
+
+inline InstGeom inst_geom(int64_t n, int64_t num_instances, const Band &b) {
+  InstGeom g;
+  const uint64_t N = (uint64_t)tmax<int64_t>(n, 1);
+  const int rows = b.row_end - b.row_begin;
+  g.T = (uint32_t)tmax(rows * b.tiles_x, 1);
+  g.sx = (b.tiles_x + kST - 1) / kST;
+  g.sy = (rows + kST - 1) / kST;
+  g.NS = (uint32_t)tmax(g.sx * g.sy, 1);
+  g.nchunks = (uint32_t)ceil_div<uint64_t>(N, kChunk);
+  g.nseg = ceil_div<uint32_t>(g.nchunks, kSeg);
+  g.slab_rows = tmax(1, tmin(g.sy, kDiffCells / (g.sx + 1) - 1));
+  g.slabs = ceil_div(g.sy, g.slab_rows);
+  // super-tiles spanned by an nx x ny rect <= min(nx ny, nx ny / 4 + 4)
+  const uint64_t I = (uint64_t)tmax<int64_t>(num_instances, 1);
+  g.ecap = tmin<uint64_t>(I, I / 4 + 4 * N);
+  g.punits = (uint32_t)(g.NS + g.ecap / kPUnit + 1);
+  return g;
+}
+
+__device__ __forceinline__ void unpack_rect(uint2 r, int &x0, int &y0, int &x1, int &y1) {
+  x0 = (int)(r.x & 0xffffu); x1 = (int)(r.x >> 16);
+  y0 = (int)(r.y & 0xffffu); y1 = (int)(r.y >> 16);
+}
+
+// L1 counts.  One CTA per (segment, super-tile-row slab): for each of the
+// segment's chunks in order, +-1 at the four corners of every super-tile rect in
+// a shared difference grid, a 2D prefix, then rel = the running per-bin count
+// before this chunk, running += counts.  Also the per-chunk entry totals.
+__global__ void __launch_bounds__(256) k_seg_count(const uint2 *__restrict__ rects, const uint32_t *__restrict__ d_m,
+                                                   int sx, int slab_rows, int sy,
+                                                   uint16_t *__restrict__ rel, uint32_t *__restrict__ segsum,
+                                                   uint32_t *__restrict__ chunk_ent) {
+  extern __shared__ int32_t smc[];
+  __shared__ uint32_t red[8];
+  const uint32_t m = *d_m;
+  const uint32_t s = blockIdx.x;
+  const uint32_t live = ceil_div<uint32_t>(m, (uint32_t)kChunk);
+  if (s * kSeg >= live) return;
+  const uint32_t NS = (uint32_t)(sx * sy);
+  const int r0 = blockIdx.y * slab_rows;
+  const int nr = min(slab_rows, sy - r0);
+  const int gw = sx + 1;
+  const int cells = gw * (nr + 1);
+  int32_t *dg = smc;
+  uint32_t *run = reinterpret_cast<uint32_t *>(smc + cells);  // nr * sx running counts
+  for (int e = threadIdx.x; e < nr * sx; e += blockDim.x) run[e] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t c1 = tmin<uint32_t>((s + 1) * kSeg, live);
+  for (uint32_t c = s * kSeg; c < c1; ++c) {
+    for (int e = threadIdx.x; e < cells; e += blockDim.x) dg[e] = 0;
+    __syncthreads();
+    const uint32_t end = tmin<uint32_t>((c + 1) * (uint32_t)kChunk, m);
+    uint32_t ent = 0;
+    for (uint32_t j = c * kChunk + threadIdx.x; j < end; j += blockDim.x) {
+      int x0, y0, x1, y1;
+      unpack_rect(__ldg(rects + j), x0, y0, x1, y1);
+      x0 >>= kSTShift; x1 >>= kSTShift;
+      y0 = max((y0 >> kSTShift) - r0, 0);
+      y1 = min((y1 >> kSTShift) - r0, nr - 1);
+      if (y1 < y0) continue;
+      ent += (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+      atomicAdd(&dg[y0 * gw + x0], 1);
+      atomicAdd(&dg[y0 * gw + x1 + 1], -1);
+      atomicAdd(&dg[(y1 + 1) * gw + x0], -1);
+      atomicAdd(&dg[(y1 + 1) * gw + x1 + 1], 1);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ent += __shfl_xor_sync(0xffffffffu, ent, o);
+    if (lane == 0) red[warp] = ent;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < nw; ++w) tot += red[w];
+      if (tot) atomicAdd(chunk_ent + c, tot);
+    }
+    for (int r = warp; r < nr; r += nw) {  // prefix along x, one warp per row
+      int32_t carry = 0;
+      for (int xb = 0; xb < sx; xb += 32) {
+        const int x = xb + lane;
+        int32_t v = x < sx ? dg[r * gw + x] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        if (x < sx) dg[r * gw + x] = v + carry;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    __syncthreads();
+    // prefix along y, one thread per column; emit the running count, then add
+    uint16_t *out = rel + (size_t)c * NS + (size_t)r0 * sx;
+    for (int x = threadIdx.x; x < sx; x += blockDim.x) {
+      int32_t col = 0;
+      for (int r = 0; r < nr; ++r) {
+        col += dg[r * gw + x];
+        const uint32_t cur = run[r * sx + x];
+        out[r * sx + x] = (uint16_t)cur;
+        run[r * sx + x] = cur + (uint32_t)col;
+      }
+    }
+    __syncthreads();
+  }
+  uint32_t *sout = segsum + (size_t)s * NS + (size_t)r0 * sx;
+  for (int e = threadIdx.x; e < nr * sx; e += blockDim.x) sout[e] = run[e];
+}
+
+// Exclusive scan over segments down each bin column (in place) + the CSR
+// offsets over bins.  A CTA owns kScanCols bins; its kScanGroups thread rows scan
+// contiguous ranges of segments, combined through shared memory; CTAs take
+// tickets and chain their bin totals by decoupled look-back.
+__global__ void __launch_bounds__(kScanCols * kScanGroups) k_seg_base(uint32_t *__restrict__ segsum,
+                                                                     const uint32_t *__restrict__ d_m, uint32_t NB,
+                                                                     uint32_t *__restrict__ status,
+                                                                     uint32_t *__restrict__ ticket,
+                                                                     uint32_t *__restrict__ offsets) {
+  __shared__ uint32_t part[kScanGroups][kScanCols];
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t s_blk, s_excl;
+  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const int col = threadIdx.x % kScanCols, grp = threadIdx.x / kScanCols;
+  const uint32_t t = blk * kScanCols + col;
+  const uint32_t nseg = ceil_div<uint32_t>(ceil_div<uint32_t>(*d_m, (uint32_t)kChunk), kSeg);
+  const uint32_t per = ceil_div<uint32_t>(nseg, kScanGroups);
+  const uint32_t s0 = tmin<uint32_t>(grp * per, nseg), s1 = tmin<uint32_t>(s0 + per, nseg);
+  uint32_t sum = 0;
+  if (t < NB)
+    for (uint32_t s = s0; s < s1; ++s) sum += segsum[(size_t)s * NB + t];
+  part[grp][col] = sum;
+  __syncthreads();
+  if (grp == 0) {  // exclusive over the groups of this column
+    uint32_t r = 0;
+#pragma unroll
+    for (int g = 0; g < kScanGroups; ++g) {
+      const uint32_t v = part[g][col];
+      part[g][col] = r;
+      r += v;
+    }
+    sum = r;  // column total
+  }
+  __syncthreads();
+  uint32_t runv = part[grp][col];
+  if (t < NB)
+    for (uint32_t s = s0; s < s1; ++s) {
+      const uint32_t v = segsum[(size_t)s * NB + t];
+      segsum[(size_t)s * NB + t] = runv;
+      runv += v;
+    }
+  __syncthreads();
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan(grp == 0 && t < NB ? sum : 0u, ws, &tot);
+  if (threadIdx.x == 0) s_excl = lookback<16>(status, 1, blk, tot);
+  __syncthreads();
+  if (grp == 0 && t < NB) {
+    offsets[t] = s_excl + ex;
+    if (t == NB - 1) offsets[NB] = s_excl + ex + sum;
+  }
+}
+
+// L1 scatter.  CTAs take balanced units of <= kUnit entries of one chunk; a CTA
+// builds the 64-bit super-tile coverage masks of all 8 groups (64 Gaussians
+// each) of its chunk, then entry (Gaussian k of group w, super-tile S = (x, y))
+// goes to  soff[S] + segbase[s][S] + rel[c][S]
+//          + sum_{w' < w} popc(col_w'[x] & row_w'[y]) + popc(col_w[x] & row_w[y] & below(k)),
+// and stores the Gaussian's depth-order index.
+__global__ void __launch_bounds__(kChunkWarps * 32) k_scatter(const uint2 *__restrict__ rects,
+                                                              const uint32_t *__restrict__ d_m, int sx, int sy,
+                                                              const uint32_t *__restrict__ chunk_ent,
+                                                              const uint16_t *__restrict__ rel,
+                                                              const uint32_t *__restrict__ segbase,
+                                                              const uint32_t *__restrict__ soff,
+                                                              uint32_t *__restrict__ entries) {
+  extern __shared__ unsigned long long mk[];
+  __shared__ uint32_t s_pre[kChunk];    // exclusive entry prefix over the chunk's Gaussians
+  __shared__ uint32_t s_rect[kChunk];   // x0 | y0 << 16 (super-tiles)
+  __shared__ uint32_t s_nx[kChunk];
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t s_c, s_part;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t m = *d_m;
+  const uint32_t live = ceil_div<uint32_t>(m, (uint32_t)kChunk);
+  const uint32_t NS = (uint32_t)(sx * sy);
+  if (threadIdx.x == 0) s_c = 0xffffffffu;
+  __syncthreads();
   uint32_t carry = 0;
-  for (int c = 0; c < ntiles; c += 1024) {
-    const int t = c + threadIdx.x;
-    const uint32_t v = t < ntiles ? (uint32_t)diff[(t / tiles_x) * gw + (t % tiles_x)] : 0u;
+  for (uint32_t b0 = 0; b0 < live; b0 += blockDim.x) {
+    const uint32_t c = b0 + threadIdx.x;
+    const uint32_t u = c < live ? ceil_div<uint32_t>(__ldg(chunk_ent + c), kUnit) : 0u;
     uint32_t tot;
-    const uint32_t ex = block_exclusive_scan(v, ws, &tot);
-    if (t < ntiles) {
-      offsets[t] = (int32_t)(carry + ex);
-      for (int p = 0; p < passes; ++p) {
-        const int sh = p * bpp, nb = min(bpp, total_bits - sh);
-        if (v) atomicAdd(&gb[p][((uint32_t)t >> sh) & ((1u << nb) - 1)], v);
-      }
+    const uint32_t ex = carry + block_exclusive_scan(u, ws, &tot);
+    if (u && blockIdx.x >= ex && blockIdx.x < ex + u) {
+      s_c = c;
+      s_part = blockIdx.x - ex;
     }
     carry += tot;
   }
-  if (threadIdx.x == 0) offsets[ntiles] = (int32_t)carry;
   __syncthreads();
-  for (int p = 0; p < passes; ++p) {
-    const uint32_t v = threadIdx.x < 256 ? gb[p][threadIdx.x] : 0u;
-    const uint32_t ex = block_exclusive_scan(v, ws, nullptr);
-    if (threadIdx.x < 256) gbins[p * 256 + threadIdx.x] = ex;
+  const uint32_t c = s_c;
+  if (c == 0xffffffffu) return;
+  const int mw = sx + sy + 2;           // column masks [0, sx], row masks after
+  for (int e = threadIdx.x; e < kChunkWarps * mw; e += blockDim.x) mk[e] = 0ull;
+  const uint32_t j0 = c * kChunk;
+  uint32_t cnt[2];
+  int x0[2], y0[2], x1[2], y1[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t k = threadIdx.x * 2 + h;
+    const uint32_t j = j0 + k;
+    cnt[h] = 0;
+    x0[h] = 0; y0[h] = 0; x1[h] = -1; y1[h] = -1;
+    if (j < m) {
+      unpack_rect(__ldg(rects + j), x0[h], y0[h], x1[h], y1[h]);
+      x0[h] >>= kSTShift; x1[h] >>= kSTShift; y0[h] >>= kSTShift; y1[h] >>= kSTShift;
+      cnt[h] = (uint32_t)((x1[h] - x0[h] + 1) * (y1[h] - y0[h] + 1));
+    }
+    s_rect[k] = (uint32_t)x0[h] | ((uint32_t)y0[h] << 16);
+    s_nx[k] = (uint32_t)(x1[h] - x0[h] + 1);
   }
+  const uint32_t ex = block_exclusive_scan(cnt[0] + cnt[1], ws, nullptr);  // also a barrier (mk zeroed)
+  s_pre[threadIdx.x * 2] = ex;
+  s_pre[threadIdx.x * 2 + 1] = ex + cnt[0];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (cnt[h] == 0) continue;
+    const uint32_t k = threadIdx.x * 2 + h;
+    unsigned long long *cm = mk + (k >> 6) * mw;
+    unsigned long long *rm = cm + sx + 1;
+    const unsigned long long bit = 1ull << (k & 63);
+    atomicXor(&cm[x0[h]], bit);
+    atomicXor(&cm[x1[h] + 1], bit);
+    atomicXor(&rm[y0[h]], bit);
+    atomicXor(&rm[y1[h] + 1], bit);
+  }
+  __syncthreads();
+  {  // XOR prefix over warp w's own group arrays
+    unsigned long long *cm = mk + warp * mw;
+    unsigned long long *rm = cm + sx + 1;
+    const int cper = (sx + 31) / 32, rper = (sy + 31) / 32;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      unsigned long long *arr = pass ? rm : cm;
+      const int len = pass ? sy : sx, per = pass ? rper : cper;
+      const int a0 = lane * per, a1 = min(a0 + per, len);
+      unsigned long long acc = 0;
+      for (int x = a0; x < a1; ++x) acc ^= arr[x];
+      unsigned long long pre = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre ^= y;
+      }
+      unsigned long long r = pre ^ acc;  // exclusive
+      for (int x = a0; x < a1; ++x) {
+        r ^= arr[x];
+        arr[x] = r;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t total = __ldg(chunk_ent + c);
+  const uint32_t e_begin = s_part * kUnit, e_end = tmin<uint32_t>(e_begin + kUnit, total);
+  const uint16_t *crel = rel + (size_t)c * NS;
+  const uint32_t *sb = segbase + (size_t)(c / kSeg) * NS;
+  for (uint32_t e = e_begin + threadIdx.x; e < e_end; e += blockDim.x) {
+    int k = 0;  // owner: last Gaussian whose exclusive prefix is <= e
+#pragma unroll
+    for (int step = kChunk / 2; step >= 1; step >>= 1)
+      if (s_pre[k + step] <= e) k += step;
+    const int local = (int)(e - s_pre[k]);
+    const uint32_t rc = s_rect[k];
+    const int knx = (int)s_nx[k];
+    const int row = local / knx;
+    const int tx = (int)(rc & 0xffffu) + local - row * knx, ty = (int)(rc >> 16) + row;
+    const uint32_t t = (uint32_t)ty * sx + (uint32_t)tx;
+    const int g = k >> 6;
+    const unsigned long long *cg = mk + g * mw;
+    uint32_t pos = __ldg(soff + t) + __ldg(sb + t) + (uint32_t)__ldg(crel + t) +
+                   (uint32_t)__popcll(cg[tx] & cg[sx + 1 + ty] & ((1ull << (k & 63)) - 1ull));
+    for (int w = 0; w < g; ++w) {
+      const unsigned long long *cw = mk + w * mw;
+      pos += (uint32_t)__popcll(cw[tx] & cw[sx + 1 + ty]);
+    }
+    entries[pos] = j0 + (uint32_t)k;
+  }
+}
+
+// L2.  A super-tile's entry list (depth order) is cut into units of <= kPUnit
+// entries; CTAs map to (super-tile, unit) through a prefix over the super-tiles.
+// Rounds of 512 entries: warp w builds 8 column and 8 row ballots over its 32
+// entries, lane L owns tiles L and L + 32 of the super-tile (mask of entries
+// covering it).
+constexpr int kPRound = kPlaceWarps * 32;
+
+__device__ __forceinline__ void place_masks(uint2 rc, bool ok, int stx0, int sty0, int lane, uint32_t &m0,
+                                            uint32_t &m1) {
+  int x0, y0, x1, y1;
+  unpack_rect(rc, x0, y0, x1, y1);
+  x0 -= stx0; x1 -= stx0; y0 -= sty0; y1 -= sty0;
+  const int cx = lane & 7, cy = lane >> 3;
+  uint32_t col = 0, r0 = 0, r1 = 0;
+#pragma unroll
+  for (int q = 0; q < kST; ++q) {
+    const uint32_t bc = __ballot_sync(0xffffffffu, ok && x0 <= q && q <= x1);
+    const uint32_t br = __ballot_sync(0xffffffffu, ok && y0 <= q && q <= y1);
+    if (cx == q) col = bc;
+    if (cy == q) r0 = br;
+    if (cy + 4 == q) r1 = br;
+  }
+  m0 = col & r0;
+  m1 = col & r1;
+}
+
+// (super-tile, unit-in-super-tile, first entry, end entry) of unit u; false past the last unit
+__device__ __forceinline__ bool place_unit(const uint32_t *__restrict__ soff, uint32_t NS, uint32_t u, uint32_t *ws,
+                                           uint32_t &S, uint32_t &k, uint32_t &ea, uint32_t &eb, uint32_t &u0) {
+  __shared__ uint32_t s_S, s_k, s_u0;
+  if (threadIdx.x == 0) s_S = 0xffffffffu;
+  __syncthreads();
+  uint32_t carry = 0;
+  for (uint32_t b0 = 0; b0 < NS; b0 += blockDim.x) {
+    const uint32_t s = b0 + threadIdx.x;
+    const uint32_t n = s < NS ? ceil_div<uint32_t>(__ldg(soff + s + 1) - __ldg(soff + s), kPUnit) : 0u;
+    uint32_t tot;
+    const uint32_t ex = carry + block_exclusive_scan(n, ws, &tot);
+    if (n && u >= ex && u < ex + n) {
+      s_S = s;
+      s_k = u - ex;
+      s_u0 = ex;
+    }
+    carry += tot;
+  }
+  __syncthreads();
+  S = s_S;
+  if (S == 0xffffffffu) return false;
+  k = s_k;
+  u0 = s_u0;
+  ea = __ldg(soff + S) + k * kPUnit;
+  eb = tmin<uint32_t>(ea + kPUnit, __ldg(soff + S + 1));
+  return true;
+}
+
+// Pass 1: per (unit, tile-of-super-tile) instance counts.
+__global__ void __launch_bounds__(kPlaceWarps * 32) k_place_count(const uint32_t *__restrict__ entries,
+                                                                   const uint32_t *__restrict__ soff,
+                                                                   const uint2 *__restrict__ rects, int sx,
+                                                                   uint32_t NS, uint32_t *__restrict__ ucnt) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t wc[kPlaceWarps][64];
+  uint32_t S, k, ea, eb, u0;
+  if (!place_unit(soff, NS, blockIdx.x, ws, S, k, ea, eb, u0)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int stx0 = (int)(S % sx) * kST, sty0 = (int)(S / sx) * kST;
+  uint32_t n0 = 0, n1 = 0;
+  for (uint32_t b = ea + warp * 32; b < eb; b += kPRound) {
+    const bool ok = b + lane < eb;
+    const uint2 rc = ok ? __ldg(rects + __ldg(entries + b + lane)) : make_uint2(0, 0);
+    uint32_t m0, m1;
+    place_masks(rc, ok, stx0, sty0, lane, m0, m1);
+    n0 += __popc(m0);
+    n1 += __popc(m1);
+  }
+  wc[warp][lane] = n0;
+  wc[warp][lane + 32] = n1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int w = 0; w < kPlaceWarps; ++w) r += wc[w][threadIdx.x];
+    ucnt[(size_t)blockIdx.x * 64 + threadIdx.x] = r;
+  }
+}
+
+// Per tile: exclusive scan of its super-tile's unit counts (in place), the tile
+// total, and the CSR offsets (blocks of 256 tiles chained by look-back).
+__global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ soff, uint32_t NS, int sx,
+                                                   int tiles_x, int rows, uint32_t *__restrict__ ucnt,
+                                                   uint32_t *__restrict__ status, uint32_t *__restrict__ ticket,
+                                                   int32_t *__restrict__ offsets) {
+  extern __shared__ uint32_t ubase[];  // NS + 1 unit prefix
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t s_blk, s_excl;
+  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+  uint32_t carry = 0;
+  for (uint32_t b0 = 0; b0 < NS; b0 += blockDim.x) {
+    const uint32_t s = b0 + threadIdx.x;
+    const uint32_t n = s < NS ? ceil_div<uint32_t>(__ldg(soff + s + 1) - __ldg(soff + s), kPUnit) : 0u;
+    uint32_t tot;
+    const uint32_t ex = carry + block_exclusive_scan(n, ws, &tot);
+    if (s < NS) ubase[s] = ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) ubase[NS] = carry;
+  __syncthreads();
+  const uint32_t T = (uint32_t)(rows * tiles_x);
+  const uint32_t t = s_blk * blockDim.x + threadIdx.x;
+  uint32_t run = 0;
+  if (t < T) {
+    const int ty = (int)(t / tiles_x), tx = (int)(t % tiles_x);
+    const uint32_t S = (uint32_t)((ty >> kSTShift) * sx + (tx >> kSTShift));
+    const uint32_t q = (uint32_t)(((ty & (kST - 1)) << kSTShift) | (tx & (kST - 1)));
+    for (uint32_t u = ubase[S]; u < ubase[S + 1]; ++u) {
+      const uint32_t v = ucnt[(size_t)u * 64 + q];
+      ucnt[(size_t)u * 64 + q] = run;
+      run += v;
+    }
+  }
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan(run, ws, &tot);
+  if (threadIdx.x == 0) s_excl = lookback<16>(status, 1, s_blk, tot);
+  __syncthreads();
+  if (t < T) {
+    offsets[t] = (int32_t)(s_excl + ex);
+    if (t == T - 1) offsets[T] = (int32_t)(s_excl + ex + run);
+  }
+}
+
+// Pass 2: rounds of 512 entries; each tile's run of the round (entries of all
+// warps covering it, in order) is written by consecutive lanes (coalesced).
+__global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t *__restrict__ entries,
+                                                                   const uint32_t *__restrict__ soff,
+                                                                   const uint2 *__restrict__ rects,
+                                                                   const uint32_t *__restrict__ ids, int sx,
+                                                                   uint32_t NS, int tiles_x, int rows,
+                                                                   const uint32_t *__restrict__ ucnt,
+                                                                   const int32_t *__restrict__ offsets,
+                                                                   int32_t *__restrict__ sorted_ids) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t mk[kPlaceWarps][64];     // entries of warp w covering tile q
+  __shared__ uint32_t pre[kPlaceWarps + 1][64];  // exclusive over warps; row kPlaceWarps = run length
+  __shared__ uint32_t sg[kPlaceWarps][32];
+  __shared__ uint32_t cur[64];
+  uint32_t S, k, ea, eb, u0;
+  if (!place_unit(soff, NS, blockIdx.x, ws, S, k, ea, eb, u0)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int stx0 = (int)(S % sx) * kST, sty0 = (int)(S / sx) * kST;
+  if (threadIdx.x < 64) {
+    const int q = threadIdx.x, tx = stx0 + (q & 7), ty = sty0 + (q >> 3);
+    cur[q] = (tx < tiles_x && ty < rows) ? (uint32_t)__ldg(offsets + ty * tiles_x + tx) +
+                                               __ldg(ucnt + (size_t)blockIdx.x * 64 + q)
+                                         : 0u;
+  }
+  for (uint32_t a = ea; a < eb; a += kPRound) {
+    const uint32_t b = a + warp * 32 + lane;
+    const bool ok = b < eb;
+    const uint32_t j = ok ? __ldg(entries + b) : 0u;
+    const uint2 rc = ok ? __ldg(rects + j) : make_uint2(0, 0);
+    sg[warp][lane] = ok ? __ldg(ids + j) : 0u;
+    uint32_t m0, m1;
+    place_masks(rc, ok, stx0, sty0, lane, m0, m1);
+    mk[warp][lane] = m0;
+    mk[warp][lane + 32] = m1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int w = 0; w < kPlaceWarps; ++w) {
+        pre[w][threadIdx.x] = r;
+        r += __popc(mk[w][threadIdx.x]);
+      }
+      pre[kPlaceWarps][threadIdx.x] = r;
+    }
+    __syncthreads();
+    for (int q = warp; q < 64; q += kPlaceWarps) {
+      const uint32_t len = pre[kPlaceWarps][q];
+      const uint32_t base = cur[q];
+      for (uint32_t i = lane; i < len; i += 32) {
+        int w = 0;  // last warp whose prefix is <= i
+#pragma unroll
+        for (int step = kPlaceWarps / 2; step >= 1; step >>= 1)
+          if (pre[w + step][q] <= i) w += step;
+        const uint32_t bit = __fns(mk[w][q], 0, (int)(i - pre[w][q]) + 1);
+        sorted_ids[base + i] = (int32_t)sg[w][bit];
+      }
+      if (lane == 0) cur[q] = base + len;
+    }
+    __syncthreads();
+  }
+}
+
+struct InstWS {
+  uint16_t *rel;
+  uint32_t *segsum, *soff, *entries, *ucnt, *status, *ticket, *chunk_ent, *tstatus, *tticket;
+  size_t zero_off, zero_bytes, bytes;
+};
+
+static InstWS carve_inst(void *p, const InstGeom &g) {
+  Carve c(p);
+  InstWS w;
+  w.rel = c.take<uint16_t>((size_t)g.nchunks * g.NS);
+  w.segsum = c.take<uint32_t>((size_t)g.nseg * g.NS);
+  w.soff = c.take<uint32_t>(g.NS + 1);
+  w.entries = c.take<uint32_t>(g.ecap);
+  w.ucnt = c.take<uint32_t>((size_t)g.punits * 64);
+  w.zero_off = c.off;
+  w.ticket = c.take<uint32_t>(1);
+  w.status = c.take<uint32_t>(ceil_div<uint32_t>(g.NS, kScanCols));
+  w.chunk_ent = c.take<uint32_t>(g.nchunks);
+  w.tticket = c.take<uint32_t>(1);
+  w.tstatus = c.take<uint32_t>(ceil_div<uint32_t>(g.T, 256));
+  w.zero_bytes = c.off - w.zero_off;
+  w.bytes = c.off;
+  return w;
 }
 
 __global__ void k_row_hist(const float *__restrict__ splats, const int32_t *__restrict__ tiles_touched, int64_t n,
@@ -634,38 +957,6 @@ __global__ void k_row_hist(const float *__restrict__ splats, const int32_t *__re
 __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) p[j] = v;
-}
-
-// Gaussian-stage workspace (persists into the instance stage)
-struct GaussWS {
-  uint32_t *cnt, *pos, *valsA, *valsB, *inst_off, *m, *partials;
-  uint64_t *keysA, *keysB;
-  SortScratch ss;
-  size_t bytes;
-};
-
-inline GaussWS carve_gauss(void *p, int64_t n) {
-  Carve c(p);
-  GaussWS w;
-  const size_t N = (size_t)tmax<int64_t>(n, 1);
-  w.cnt = c.take<uint32_t>(N);
-  w.pos = c.take<uint32_t>(N);
-  w.keysA = c.take<uint64_t>(N);
-  w.valsA = c.take<uint32_t>(N);
-  w.keysB = c.take<uint64_t>(N);
-  w.valsB = c.take<uint32_t>(N);
-  w.inst_off = c.take<uint32_t>(N);
-  w.m = c.take<uint32_t>(4);
-  w.partials = c.take<uint32_t>(scan_ws_bytes(N) / 4);
-  w.ss = carve_sort<uint64_t>(c, N, 8);
-  w.bytes = c.off;
-  return w;
-}
-
-inline int key_bits(uint32_t ntiles) {
-  int bits = 0;
-  while (bits < 32 && (1ull << bits) < ntiles) ++bits;
-  return bits;
 }
 
 inline bool band_ok(int W, int H, int ts, int rb, int re, Band &b) {
@@ -693,54 +984,45 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
                                  int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
                                  void *workspace, int64_t *d_num_instances, tgs_stream_t stream) {
   Band b;
-  if (n < 0 || n >= (int64_t)1 << 31 || !workspace || !d_num_instances ||
+  if (n < 0 || n >= (int64_t)1 << 30 || !workspace || !d_num_instances ||
       !band_ok(width, height, tile_size, row_begin, row_end, b))
     return TGS_ERR_INVALID;
   cudaStream_t st = as_stream(stream);
   GaussWS w = carve_gauss(workspace, n);
-  if (n == 0) {
-    cudaMemsetAsync(w.m, 0, 4, st);
-    cudaMemsetAsync(d_num_instances, 0, 8, st);
-    return launch_status();
+  cudaMemsetAsync(static_cast<char *>(workspace) + w.zero_off, 0, w.zero_bytes, st);
+  cudaMemsetAsync(d_num_instances, 0, 8, st);
+  if (n == 0) return launch_status();
+  DsArgs a;
+  a.splats = splats;
+  a.tiles_touched = tiles_touched;
+  a.depth_keys = depth_keys;
+  a.n = (uint32_t)n;
+  a.b = b;
+  a.keysA = w.keysA; a.keysB = w.keysB;
+  a.valsA = w.valsA; a.valsB = w.valsB;
+  a.ctl = w.ctl;
+  a.rect_by_gid = w.rect_by_gid;
+  a.rects_sorted = w.rects_sorted;
+  a.sel_status = w.sel_status;
+  a.status = w.status;
+  a.T0 = w.T0;
+  a.TP = w.TP;
+  a.num_instances = reinterpret_cast<unsigned long long *>(d_num_instances);
+  static bool attr_done = false;  // idempotent function attribute, set once per process
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsSmem));
+    attr_done = true;
   }
-  const unsigned g256 = (unsigned)ceil_div<int64_t>(n, 256);
-  k_select<<<g256, 256, 0, st>>>(splats, tiles_touched, n, b, w.cnt, w.pos);
-  device_scan(w.pos, w.pos, (uint64_t)n, nullptr, w.partials, w.m, nullptr, st);
-  k_compact<<<g256, 256, 0, st>>>(splats, depth_keys, w.cnt, w.pos, n, w.keysA, w.valsA);
-  // depth digits: 8 stable 8-bit passes over the M selected Gaussians (float64 keys); even
-  // pass count -> result back in (keysA, valsA)
-  radix_sort<uint64_t>(w.keysA, w.valsA, w.keysB, w.valsB, (uint64_t)n, w.m, 64, w.ss, st);
-  // depth-ordered ids are in valsA; per-Gaussian instance offsets in depth order
-  k_gather_counts<<<g256, 256, 0, st>>>(w.valsA, w.cnt, n, w.m, w.inst_off);
-  device_scan(w.inst_off, w.inst_off, (uint64_t)n, w.m, w.partials, nullptr, d_num_instances, st);
+  k_depth_sort<<<w.T0 + kDsPasses * w.TP, kDsThreads, sizeof(DsSmem), st>>>(a);
   return launch_status();
 }
 
-struct InstWS {
-  uint32_t *keysA, *keysB, *valsB;
-  int32_t *diff;
-  SortScratch ss;
-  size_t bytes;
-};
-
-static InstWS carve_inst(void *p, int64_t count, size_t ntiles) {
-  Carve c(p);
-  InstWS w;
-  const size_t I = (size_t)tmax<int64_t>(count, 1);
-  w.keysA = c.take<uint32_t>(I);
-  w.keysB = c.take<uint32_t>(I);
-  w.valsB = c.take<uint32_t>(I);
-  w.ss = carve_sort<uint32_t>(c, I, 4);  // up to 32 tile bits
-  w.diff = c.take<int32_t>(ntiles);       // (rows + 1) x (tiles_x + 1) difference grid bound
-  w.bytes = c.off;
-  return w;
-}
-
-extern "C" int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, size_t *bytes) {
-  if (n < 0 || num_instances < 0 || !bytes) return TGS_ERR_INVALID;
-  // the per-tile histogram is sized for the largest band a caller can request (2^18 tiles here
-  // at most per call of tgs_bin_instances); callers with more tiles get a bigger query below
-  *bytes = carve_inst(nullptr, num_instances, (size_t)1 << 18).bytes;
+extern "C" int tgs_bin_instances_workspace(int64_t n, int64_t num_instances, int32_t width, int32_t height,
+                                           int32_t tile_size, int32_t row_begin, int32_t row_end, size_t *bytes) {
+  Band b;
+  if (n < 0 || num_instances < 0 || !bytes || !band_ok(width, height, tile_size, row_begin, row_end, b))
+    return TGS_ERR_INVALID;
+  *bytes = carve_inst(nullptr, inst_geom(n, num_instances, b)).bytes;
   return TGS_OK;
 }
 
@@ -751,42 +1033,41 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   if (n < 0 || num_instances < 0 || num_instances >= (int64_t)1 << 31 || !gauss_workspace || !tile_offsets ||
       !band_ok(width, height, tile_size, row_begin, row_end, b))
     return TGS_ERR_INVALID;
+  if (num_instances >= (int64_t)1 << 30) return TGS_ERR_UNSUPPORTED;  // 30-bit look-back payloads
   cudaStream_t st = as_stream(stream);
-  const uint32_t ntiles = (uint32_t)(b.row_end - b.row_begin) * b.tiles_x;
+  const InstGeom g = inst_geom(n, num_instances, b);
+  const int rows = b.row_end - b.row_begin;
   if (num_instances == 0) {
-    k_fill_i32<<<(unsigned)ceil_div<int64_t>(ntiles + 1, 256), 256, 0, st>>>(tile_offsets, ntiles + 1, 0);
+    k_fill_i32<<<(unsigned)ceil_div<int64_t>(g.T + 1, 256), 256, 0, st>>>(tile_offsets, g.T + 1, 0);
     return launch_status();
   }
   if (!workspace || !sorted_ids) return TGS_ERR_INVALID;
+  const size_t sc_smem = (size_t)kChunkWarps * (g.sx + g.sy + 2) * 8;
+  const size_t cnt_smem = ((size_t)(g.sx + 1) * (g.slab_rows + 1) + (size_t)g.slab_rows * g.sx) * 4;
+  if (sc_smem > 160 * 1024 || (g.NS + 1) * 4 > 160 * 1024) return TGS_ERR_UNSUPPORTED;
   GaussWS gw = carve_gauss(gauss_workspace, n);
-  if (ntiles > (1u << 18)) return TGS_ERR_UNSUPPORTED;
-  InstWS w = carve_inst(workspace, num_instances, (size_t)1 << 18);
-  const int bits = key_bits(ntiles);
-  const int passes = (bits + 7) / 8;
-  // ping-pong so the last pass lands in sorted_ids: with an even pass count the
-  // duplicate writes straight into sorted_ids (A = sorted_ids, B = valsB)
-  uint32_t *ids_out = reinterpret_cast<uint32_t *>(sorted_ids);
-  uint32_t *vA = (passes % 2 == 0) ? ids_out : w.valsB;
-  uint32_t *vB = (passes % 2 == 0) ? w.valsB : ids_out;
-  // per-tile counts (-> CSR offsets) and the digit histograms from the rects
-  const int rows = b.row_end - b.row_begin;
-  const int cells = (rows + 1) * (b.tiles_x + 1);
-  static bool attr_done = false;  // idempotent function attribute, set once per process
+  InstWS w = carve_inst(workspace, g);
+  const uint32_t *d_m = &gw.ctl->m;
+  static bool attr_done = false;  // idempotent function attributes, set once per process
   if (!attr_done) {
-    cudaFuncSetAttribute(k_tile_hist2d, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiffSmem * 4);
+    cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_seg_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDiffCells * 4);
+    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr_done = true;
   }
-  cudaMemsetAsync(w.ss.gbins, 0, w.ss.bytes_zeroed, st);
-  cudaMemsetAsync(w.diff, 0, (size_t)cells * 4, st);
-  const unsigned dgrid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n, 256), 148 * 2);
-  k_tile_hist2d<<<dgrid, 256, cells <= kDiffSmem ? (size_t)cells * 4 : 0, st>>>(splats, gw.valsA, n, gw.m, b,
-                                                                                w.diff);
-  const int bpp = passes ? (bits + passes - 1) / passes : 0;
-  k_tile_hist_finalize<<<1, 1024, 0, st>>>(w.diff, b.tiles_x, rows, passes, bpp, bits, tile_offsets, w.ss.gbins);
-  k_duplicate<<<(unsigned)ceil_div<int64_t>(n, 256), 256, 0, st>>>(splats, gw.valsA, gw.inst_off, n, gw.m, b,
-                                                                    w.keysA, vA);
-  radix_sort<uint32_t>(w.keysA, vA, w.keysB, vB, (uint64_t)num_instances, nullptr, bits, w.ss, st,
-                       /*hist_ready=*/true, /*last_keys=*/false);
+  cudaMemsetAsync(static_cast<char *>(workspace) + w.zero_off, 0, w.zero_bytes, st);
+  k_seg_count<<<dim3(g.nseg, g.slabs), 256, cnt_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.slab_rows, g.sy, w.rel,
+                                                           w.segsum, w.chunk_ent);
+  k_seg_base<<<ceil_div<uint32_t>(g.NS, kScanCols), kScanCols * kScanGroups, 0, st>>>(w.segsum, d_m, g.NS, w.status,
+                                                                                    w.ticket, w.soff);
+  const uint32_t units = g.nchunks + (uint32_t)(g.ecap / kUnit) + 1;
+  k_scatter<<<units, kChunkWarps * 32, sc_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.sy, w.chunk_ent, w.rel,
+                                                      w.segsum, w.soff, w.entries);
+  k_place_count<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, g.sx, g.NS, w.ucnt);
+  k_tile_scan<<<ceil_div<uint32_t>(g.T, 256), 256, (g.NS + 1) * 4, st>>>(w.soff, g.NS, g.sx, b.tiles_x, rows, w.ucnt,
+                                                                        w.tstatus, w.tticket, tile_offsets);
+  k_place_write<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, gw.valsA, g.sx, g.NS,
+                                                       b.tiles_x, rows, w.ucnt, tile_offsets, sorted_ids);
   return launch_status();
 }
 

@@ -137,7 +137,7 @@ def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, 
     ntiles = (row_end - row_begin) * tiles_x
     offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
     ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
-    ib = ctypes_size("tgs_bin_instances_workspace", n, count)
+    ib = ctypes_size("tgs_bin_instances_workspace", n, count, width, height, ts, row_begin, row_end)
     ws2 = torch.empty(max(ib, 16), dtype=torch.uint8, device=dev)
     with stage("bin_instances"):
         _lib.call("tgs_bin_instances", _lib.ptr(splats), n, width, height, ts, row_begin, row_end, _lib.ptr(ws),

@@ -77,7 +77,7 @@ def test_forward_backward_vs_reference_golden(tgs, name):
         _grad_close(_np(getattr(g, f))[rows], z[f"grad_{f}"], f)
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "masked", "deg1", "tile8", "tile32"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "masked", "deg1", "tile8", "tile32", "uhd", "uhd_c4"])
 def test_preprocess_and_sort_bit_exact_vs_fp32_oracle(tgs, cfg):
     from paper_2501_14534_b200 import scenes
     kw = {}
@@ -85,6 +85,11 @@ def test_preprocess_and_sort_bit_exact_vs_fp32_oracle(tgs, cfg):
         sc = scenes.config1()
     elif cfg == "c2":
         sc = scenes.config2()
+    elif cfg == "uhd":  # 3840x2160: 32,400 tiles -> two count slabs, C > 512 is not needed
+        sc = scenes.small_scene(seed=22, n=150_000, width=3840, height=2160, dist=3.0)
+    elif cfg == "uhd_c4":  # c4 cluster scene, fewer Gaussians, 4K, frame 37 of the orbit
+        sc = scenes.config4(n=300_000, frames=200)
+        sc.cameras[0] = sc.cameras[37]
     else:
         sc = scenes.small_scene(seed=21, n=30_000, width=333, height=207, dist=3.0)
         kw = {"masked": dict(mask_threshold=0.85, sh_mask_threshold=0.85, lowpass_s=0.5),
@@ -182,6 +187,15 @@ def test_row_bands_compose_to_full_render(tgs):
         rows = slice(rb * 16, min(re * 16, cam.height))
         img[rows] = part.image[rows]
     assert torch.equal(img, full.image)
+    # the band's tile lists are exactly the full lists of its tiles
+    fo, fi = _np(full._tiles.offsets), _np(full._tiles.indices)
+    tx = (cam.width + 15) // 16
+    for rb, re in ((0, 3), (3, 4), (4, ty), (1, ty - 1)):
+        part = tgs.render_forward(cloud, cam, st, row_band=(rb, re))
+        po, pi = _np(part._tiles.offsets), _np(part._tiles.indices)
+        want_o = fo[rb * tx: re * tx + 1] - fo[rb * tx]
+        assert np.array_equal(po, want_o)
+        assert np.array_equal(pi, fi[fo[rb * tx]: fo[re * tx]])
 
 
 def test_errors_and_edges(tgs):
@@ -262,6 +276,18 @@ def test_c3_scale_properties(tgs):
     tile_of = np.repeat(np.arange(off.size - 1), np.diff(off))
     same = tile_of[1:] == tile_of[:-1]
     assert ((k[1:] > k[:-1]) | ((k[1:] == k[:-1]) & (ids[1:] > ids[:-1])))[same].all()
+    # completeness: every Gaussian sits in exactly the tiles of its rect, once each
+    sp = _np(out._state.splats)[: len(cloud)]
+    tt = _np(out._state.tiles_touched)[: len(cloud)]
+    assert np.array_equal(np.bincount(ids, minlength=len(cloud)), np.maximum(tt, 0))
+    mx, my, r = sp[ids, 0], sp[ids, 1], sp[ids, 10]
+    f16 = np.float32(16)
+    tx_, ty_ = tile_of % 120, tile_of // 120
+    x0 = np.clip(np.floor((mx - r) / f16), 0, 119)
+    x1 = np.clip(np.floor((mx + r) / f16), 0, 119)
+    y0 = np.clip(np.floor((my - r) / f16), 0, 67)
+    y1 = np.clip(np.floor((my + r) / f16), 0, 67)
+    assert ((tx_ >= x0) & (tx_ <= x1) & (ty_ >= y0) & (ty_ <= y1)).all()
     # determinism: a second render is bitwise identical
     out2 = tgs.render_forward(cloud, sc.cameras[0], st)
     assert torch.equal(out.image, out2.image) and torch.equal(out._tiles.indices, out2._tiles.indices)
