@@ -131,23 +131,27 @@ __device__ __forceinline__ uint2 pack_rect(int x0, int y0, int x1, int y1) {
 }
 
 // ======================================================= (A) depth sort
-// One launch.  Tickets [0, T0) are selection tiles over the n Gaussians (in-band
-// test, index-order compaction by look-back, digit histograms of all passes, the
-// instance total); tickets T0 + p*TP + j are tile j of radix pass p.  A pass tile
-// first waits for the completion counter of the stage feeding it; every stage it
-// waits on holds strictly earlier tickets, so the chain is deadlock-free without
-// any co-residency assumption.
-constexpr int kDsThreads = 512;
-constexpr int kDsIPT = 8;
+// One launch.  Tickets [0, T0) are histogram tiles over the n Gaussians (in-band
+// test, packed band rect per Gaussian, digit histograms of all passes, the
+// selected and instance totals); tickets T0 + p*TP + j are tile j of radix pass
+// p.  Pass 0 reads the Gaussians in index order straight from the inputs and
+// compacts the selected ones as it scatters; later passes ping-pong between two
+// buffers.  A pass tile first waits for the completion counter of the stage
+// feeding it; every stage it waits on holds strictly earlier tickets, so the
+// chain is deadlock-free without any co-residency assumption.  Passes whose
+// digit is the same for all keys are skipped.
+constexpr int kDsThreads = 256;
+constexpr int kDsIPT = 16;
 constexpr int kDsTile = kDsThreads * kDsIPT;  // 4096 items per tile
 constexpr int kDsWarps = kDsThreads / 32;
 constexpr int kDsPasses = 8;                  // 64-bit keys, 8-bit digits
 constexpr int kDsLookback = 16;
+constexpr uint32_t kNoRect = 0xffffffffu;     // rect_by_gid of an unselected Gaussian
 
 struct DsCtl {                       // zeroed before every launch
   uint32_t ticket;
   uint32_t m;                        // selected Gaussians
-  uint32_t done[kDsPasses + 1];      // done[0]: selection tiles; done[p]: tiles of pass p-1
+  uint32_t done[kDsPasses + 1];      // done[0]: histogram tiles; done[p + 1]: tiles of pass p
   uint32_t pad[5];
   uint32_t hist[kDsPasses][256];     // global digit histograms
 };
@@ -161,17 +165,27 @@ struct DsArgs {
   uint64_t *keysA, *keysB;
   uint32_t *valsA, *valsB;
   DsCtl *ctl;
-  uint2 *rect_by_gid;                // n: band rect of each selected Gaussian (packed u16 pairs)
-  uint2 *rects_sorted;               // M: the same, in depth order (written by the last pass)
-  uint32_t *sel_status;              // T0
-  uint32_t *status;                  // kDsPasses * TP * 256
+  uint2 *rect_by_gid;                // n: band rect of each Gaussian (packed u16 pairs) or kNoRect
+  uint2 *rects_sorted;               // M: the selected rects in depth order (written by the last pass)
+  uint32_t *ids;                     // M: Gaussian ids in depth order (written by the last pass)
+  uint32_t *status;                  // kDsPasses * TP * 256 look-back words
   uint32_t T0, TP;
   unsigned long long *num_instances;
 };
 
+// Optional per-ticket phase timestamps (tgs_debug_trace_depth_sort; null = off).
+__device__ unsigned long long *g_ds_trace = nullptr;
+__device__ __forceinline__ void ds_mark(uint32_t ticket, int k) {
+  if (threadIdx.x == 0 && g_ds_trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_ds_trace[(size_t)ticket * 8 + k] = t;
+  }
+}
+
 __device__ __forceinline__ void wait_count(const uint32_t *p, uint32_t need) {
   if (threadIdx.x == 0)
-    while (ld_acquire(p) < need) __nanosleep(128);
+    while (ld_acquire(p) < need) __nanosleep(32);
   __syncthreads();
 }
 __device__ __forceinline__ void signal_done(uint32_t *p) {
@@ -187,6 +201,7 @@ struct DsSmem {
     struct {
       uint64_t ks[kDsTile];
       uint32_t vs[kDsTile];
+      uint32_t vin[kDsTile];        // values in item order (kept out of registers while ranking)
       uint32_t wcnt[kDsWarps][256];
     } pass;
     struct {
@@ -196,132 +211,181 @@ struct DsSmem {
   uint32_t dstart[256];
   uint32_t gbase[256];
   uint32_t wsum[32];
-  uint32_t ticket, m, excl;
+  uint32_t ticket, m, cnt;
   unsigned long long inst;
+  uint32_t nsel;
 };
 
-__device__ void ds_select_tile(const DsArgs &a, DsSmem &sm, uint32_t t) {
+__device__ __forceinline__ uint64_t ds_key(const DsArgs &a, uint32_t i) {
+  return a.depth_keys ? __ldg(a.depth_keys + i) : orderable_key64((double)__ldg(a.splats + 12 * (size_t)i + 9));
+}
+
+__device__ void ds_hist_tile(const DsArgs &a, DsSmem &sm, uint32_t t) {
   for (int e = threadIdx.x; e < kDsPasses * 256; e += kDsThreads) (&sm.sel.hist[0][0])[e] = 0;
-  if (threadIdx.x == 0) sm.inst = 0;
+  if (threadIdx.x == 0) {
+    sm.inst = 0;
+    sm.nsel = 0;
+  }
   __syncthreads();
-  // blocked layout: thread owns 8 consecutive Gaussians -> compaction in index order
-  const uint32_t i0 = t * kDsTile + threadIdx.x * kDsIPT;
-  uint64_t key[kDsIPT];
-  uint32_t flags = 0, cnt_sum = 0, nsel = 0;
+  const int lane = threadIdx.x & 31;
+  uint32_t nsel = 0;
+  unsigned long long inst = 0;
+  // striped, four batches of 4 items: all loads of a batch are issued before use
 #pragma unroll
-  for (int r = 0; r < kDsIPT; ++r) {
-    const uint32_t i = i0 + r;
-    key[r] = 0;
-    if (i < a.n && a.tiles_touched[i] > 0) {
-      int x0, y0, x1, y1;
-      const int c = band_rect(a.splats + 12 * (size_t)i, a.b, x0, y0, x1, y1);
-      if (c > 0) {
-        a.rect_by_gid[i] = pack_rect(x0, y0 - a.b.row_begin, x1, y1 - a.b.row_begin);
-        flags |= 1u << r;
-        cnt_sum += (uint32_t)c;
-        ++nsel;
-        key[r] = a.depth_keys ? a.depth_keys[i] : orderable_key64((double)a.splats[12 * (size_t)i + 9]);
+  for (int hh = 0; hh < 4; ++hh) {
+    int32_t tt[4];
+    float4 sp[4];
+    float rad[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t i = t * kDsTile + (hh * 4 + r) * kDsThreads + threadIdx.x;
+      const bool in = i < a.n;
+      tt[r] = in ? __ldg(a.tiles_touched + i) : 0;
+      sp[r] = in ? __ldg(reinterpret_cast<const float4 *>(a.splats + 12 * (size_t)i)) : make_float4(0, 0, 0, 0);
+      rad[r] = in ? __ldg(a.splats + 12 * (size_t)i + 10) : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t i = t * kDsTile + (hh * 4 + r) * kDsThreads + threadIdx.x;
+      int x0 = 0, y0 = 0, x1 = -1, y1 = -1, c = 0;
+      if (tt[r] > 0) {
+        c = tile_rect(sp[r].x, sp[r].y, rad[r], a.b.W, a.b.H, a.b.ts, a.b.tiles_x, a.b.tiles_y, x0, y0, x1, y1);
+        if (c > 0) {
+          y0 = max(y0, a.b.row_begin);
+          y1 = min(y1, a.b.row_end - 1);
+          c = y1 >= y0 ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0;
+        }
+      }
+      const bool ok = c > 0;
+      if (i < a.n)
+        a.rect_by_gid[i] = ok ? pack_rect(x0, y0 - a.b.row_begin, x1, y1 - a.b.row_begin) : make_uint2(kNoRect, kNoRect);
+      const uint64_t key = ok ? ds_key(a, i) : 0ull;
+      nsel += ok;
+      inst += (uint32_t)c;
+      // digit histograms; the high key bytes are nearly constant, so a warp whose
+      // valid lanes share a digit adds once instead of contending on one bin
+      const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+      if (okm == 0) continue;
+      const int src = __ffs(okm) - 1;
+#pragma unroll
+      for (int p = 0; p < kDsPasses; ++p) {
+        const uint32_t d = (uint32_t)(key >> (8 * p)) & 255u;
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, src);
+        if (__all_sync(0xffffffffu, !ok || d == d0)) {
+          if (lane == src) atomicAdd(&sm.sel.hist[p][d], (uint32_t)__popc(okm));
+        } else if (ok) {
+          atomicAdd(&sm.sel.hist[p][d], 1u);
+        }
       }
     }
   }
-  uint32_t total;
-  const uint32_t off = block_exclusive_scan(nsel, sm.wsum, &total);
-  if (threadIdx.x == 0) {
-    sm.excl = lookback<kDsLookback>(a.sel_status, 1, t, total);
-    atomicAdd(&a.ctl->m, total);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+    inst += __shfl_xor_sync(0xffffffffu, inst, o);
   }
-  atomicAdd(&sm.inst, (unsigned long long)cnt_sum);
-  __syncthreads();
-  uint32_t pos = sm.excl + off;
-#pragma unroll
-  for (int r = 0; r < kDsIPT; ++r) {
-    if (flags >> r & 1u) {
-      a.keysA[pos] = key[r];
-      a.valsA[pos] = i0 + r;
-      ++pos;
-#pragma unroll
-      for (int p = 0; p < kDsPasses; ++p) atomicAdd(&sm.sel.hist[p][(uint32_t)(key[r] >> (8 * p)) & 255u], 1u);
-    }
+  if (lane == 0) {
+    atomicAdd(&sm.nsel, nsel);
+    atomicAdd(&sm.inst, inst);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kDsPasses * 256; e += kDsThreads) {
     const uint32_t v = (&sm.sel.hist[0][0])[e];
     if (v) atomicAdd(&a.ctl->hist[0][0] + e, v);
   }
-  if (threadIdx.x == 0 && sm.inst) atomicAdd(a.num_instances, sm.inst);
+  if (threadIdx.x == 0 && sm.nsel) atomicAdd(&a.ctl->m, sm.nsel);
   signal_done(&a.ctl->done[0]);
 }
 
-__device__ void ds_pass_tile(const DsArgs &a, DsSmem &sm, int p, uint32_t j, uint32_t m) {
-  const uint64_t *keys_in = (p & 1) ? a.keysB : a.keysA;
-  const uint32_t *vals_in = (p & 1) ? a.valsB : a.valsA;
-  uint64_t *keys_out = (p & 1) ? a.keysA : a.keysB;
-  uint32_t *vals_out = (p & 1) ? a.valsA : a.valsB;
-  const bool last = p == kDsPasses - 1;
+__device__ void ds_pass_tile(const DsArgs &a, DsSmem &sm, int p, uint32_t j, uint32_t m, uint32_t ticket,
+                             bool odd, bool last) {
+  const uint64_t *keys_in = odd ? a.keysB : a.keysA;
+  const uint32_t *vals_in = odd ? a.valsB : a.valsA;
+  uint64_t *keys_out = odd ? a.keysA : a.keysB;
+  uint32_t *vals_out = last ? a.ids : (odd ? a.valsA : a.valsB);
   const int shift = 8 * p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < kDsWarps * 256; e += kDsThreads) (&sm.pass.wcnt[0][0])[e] = 0;
   const uint64_t base = (uint64_t)j * kDsTile;
   const uint64_t wbase = base + (uint64_t)warp * (kDsIPT * 32);
   uint64_t key[kDsIPT];
-  uint32_t val[kDsIPT];
-  uint16_t rank[kDsIPT];
-  // all loads first (L2 only: the buffers were written by other CTAs of this launch)
+  uint32_t okbits = 0;
+  const uint32_t ibase = warp * (kDsIPT * 32) + lane;  // item index in the tile = ibase + 32 r
+  if (p == 0) {
+    // pass 0: Gaussians in index order from the inputs; unselected ones drop out
+    uint32_t rx[kDsIPT];
 #pragma unroll
-  for (int r = 0; r < kDsIPT; ++r) {
-    const uint64_t q = wbase + r * 32 + lane;
-    const bool ok = q < m;
-    key[r] = ok ? (uint64_t)__ldcg(reinterpret_cast<const unsigned long long *>(keys_in) + q) : 0ull;
-    val[r] = ok ? __ldcg(vals_in + q) : 0u;
+    for (int r = 0; r < kDsIPT; ++r) {
+      const uint64_t q = wbase + r * 32 + lane;
+      rx[r] = q < a.n ? __ldcg(&a.rect_by_gid[q].x) : kNoRect;
+    }
+#pragma unroll
+    for (int r = 0; r < kDsIPT; ++r) {
+      const uint32_t q = (uint32_t)(wbase + r * 32 + lane);
+      const bool ok = rx[r] != kNoRect;
+      okbits |= (uint32_t)ok << r;
+      key[r] = ok ? ds_key(a, q) : 0ull;
+      sm.pass.vin[ibase + 32 * r] = q;
+    }
+  } else {
+    // all loads first (L2 only: the buffers were written by other CTAs of this launch)
+#pragma unroll
+    for (int r = 0; r < kDsIPT; ++r) {
+      const uint64_t q = wbase + r * 32 + lane;
+      const bool ok = q < m;
+      okbits |= (uint32_t)ok << r;
+      key[r] = ok ? (uint64_t)__ldcg(reinterpret_cast<const unsigned long long *>(keys_in) + q) : 0ull;
+      sm.pass.vin[ibase + 32 * r] = ok ? __ldcg(vals_in + q) : 0u;
+    }
   }
   __syncthreads();
+  ds_mark(ticket, 2);
   const uint32_t lt = lanemask_lt();
+  uint32_t rank2[kDsIPT / 2];  // two 16-bit ranks per register
   // warp-synchronous multisplit: ranks stable in item order (warp-major, round, lane)
 #pragma unroll
   for (int r = 0; r < kDsIPT; ++r) {
-    const uint64_t q = wbase + r * 32 + lane;
-    const bool ok = q < m;
-    const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
-    rank[r] = 0;
-    if (ok) {
-      const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
-      const uint32_t peers = __match_any_sync(okmask, d);
-      const uint32_t prev = sm.pass.wcnt[warp][d];
-      rank[r] = (uint16_t)(prev + __popc(peers & lt));
-      __syncwarp(okmask);
-      if (lane == __ffs(peers) - 1) sm.pass.wcnt[warp][d] = prev + __popc(peers);
+    const bool ok = okbits >> r & 1u;
+    const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
+    uint32_t peers = __ballot_sync(0xffffffffu, ok);  // lanes with the same digit: 8 ballots
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bb : ~bb;
     }
+    const uint32_t prev = ok ? sm.pass.wcnt[warp][d] : 0u;
+    const uint32_t rk = prev + __popc(peers & lt);
+    rank2[r >> 1] = (r & 1) ? (rank2[r >> 1] | (rk << 16)) : rk;
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) sm.pass.wcnt[warp][d] = prev + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
+  ds_mark(ticket, 3);
   uint32_t dtotal = 0;
-  if (threadIdx.x < 256) {
-    for (int w = 0; w < kDsWarps; ++w) {
-      const uint32_t c = sm.pass.wcnt[w][threadIdx.x];
-      sm.pass.wcnt[w][threadIdx.x] = dtotal;
-      dtotal += c;
-    }
+  for (int w = 0; w < kDsWarps; ++w) {  // kDsThreads == 256: one digit per thread
+    const uint32_t c = sm.pass.wcnt[w][threadIdx.x];
+    sm.pass.wcnt[w][threadIdx.x] = dtotal;
+    dtotal += c;
   }
-  const uint32_t ds = block_exclusive_scan(threadIdx.x < 256 ? dtotal : 0u, sm.wsum, nullptr);
-  if (threadIdx.x < 256) sm.dstart[threadIdx.x] = ds;
+  uint32_t cnt;
+  const uint32_t ds = block_exclusive_scan(dtotal, sm.wsum, &cnt);
+  sm.dstart[threadIdx.x] = ds;
   __syncthreads();
   // local reorder first (frees the key registers), then the look-back
 #pragma unroll
   for (int r = 0; r < kDsIPT; ++r) {
-    const uint64_t q = wbase + r * 32 + lane;
-    if (q < m) {
+    if (okbits >> r & 1u) {
       const uint32_t d = (uint32_t)(key[r] >> shift) & 255u;
-      const uint32_t s = sm.dstart[d] + sm.pass.wcnt[warp][d] + rank[r];
+      const uint32_t s = sm.dstart[d] + sm.pass.wcnt[warp][d] + ((rank2[r >> 1] >> (16 * (r & 1))) & 0xffffu);
       sm.pass.ks[s] = key[r];
-      sm.pass.vs[s] = val[r];
+      sm.pass.vs[s] = sm.pass.vin[ibase + 32 * r];
     }
   }
-  if (threadIdx.x < 256) {
-    const uint32_t excl = lookback<kDsLookback>(a.status + (size_t)p * a.TP * 256 + threadIdx.x, 256, j, dtotal);
-    sm.gbase[threadIdx.x] += excl;  // gbase holds this pass's exclusive digit base
-  }
+  const uint32_t excl = lookback<kDsLookback>(a.status + (size_t)p * a.TP * 256 + threadIdx.x, 256, j, dtotal);
+  sm.gbase[threadIdx.x] += excl;  // gbase holds this pass's exclusive digit base
   __syncthreads();
-  const uint32_t cnt = (uint32_t)tmin<uint64_t>(kDsTile, m - base);
+  ds_mark(ticket, 4);
   for (uint32_t e = threadIdx.x; e < cnt; e += kDsThreads) {
     const uint64_t k = sm.pass.ks[e];
     const uint32_t d = (uint32_t)(k >> shift) & 255u;
@@ -329,22 +393,19 @@ __device__ void ds_pass_tile(const DsArgs &a, DsSmem &sm, int p, uint32_t j, uin
     if (!last) __stcg(reinterpret_cast<unsigned long long *>(keys_out) + o, (unsigned long long)k);
     const uint32_t v = sm.pass.vs[e];
     __stcg(vals_out + o, v);
-    if (last) {
-      const uint2 rc = __ldcg(a.rect_by_gid + v);
-      __stcg(a.rects_sorted + o, rc);
-    }
+    if (last) __stcg(a.rects_sorted + o, __ldcg(a.rect_by_gid + v));
   }
   signal_done(&a.ctl->done[p + 1]);
+  ds_mark(ticket, 5);
 }
 
-__global__ void __launch_bounds__(kDsThreads, 2) k_depth_sort(DsArgs a) {
-  extern __shared__ __align__(16) unsigned char ds_raw[];
-  DsSmem &sm = *reinterpret_cast<DsSmem *>(ds_raw);
-  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.ctl->ticket, 1u);
-  __syncthreads();
-  const uint32_t t = sm.ticket;
+// One ticket of the chain (see above).
+__device__ void ds_ticket(const DsArgs &a, DsSmem &sm, uint32_t t) {
+  ds_mark(t, 0);
   if (t < a.T0) {
-    ds_select_tile(a, sm, t);
+    ds_mark(t, 1);
+    ds_hist_tile(a, sm, t);
+    ds_mark(t, 5);
     return;
   }
   const int p = (int)((t - a.T0) / a.TP);
@@ -354,24 +415,246 @@ __global__ void __launch_bounds__(kDsThreads, 2) k_depth_sort(DsArgs a) {
   __syncthreads();
   const uint32_t m = sm.m;
   const uint32_t live = (m + kDsTile - 1) / kDsTile;
-  if (j >= live) return;
-  // this pass's exclusive digit base (from the selection histograms)
-  const uint32_t h = threadIdx.x < 256 ? __ldcg(&a.ctl->hist[p][threadIdx.x]) : 0u;
-  const uint32_t hb = block_exclusive_scan(h, sm.wsum, nullptr);
-  if (threadIdx.x < 256) sm.gbase[threadIdx.x] = hb;
-  if (p > 0) wait_count(&a.ctl->done[p], live);
+  if (m == 0 || (p > 0 && j >= live)) return;  // pass 0 tiles cover all n Gaussians
+  // passes whose digit is the same for every key are the identity: skip them
+  // (pass 0 always runs: it compacts and, if it is the only pass, writes the outputs)
+  uint32_t active = 1u;
+#pragma unroll
+  for (int q = 1; q < kDsPasses; ++q) {
+    const uint32_t hq = __ldcg(&a.ctl->hist[q][threadIdx.x]);
+    if (__syncthreads_count(hq != 0u) > 1) active |= 1u << q;
+  }
+  if (!(active >> p & 1u)) return;
+  const bool odd = __popc(active & ((1u << p) - 1u)) & 1;
+  const bool last = (active >> (p + 1)) == 0u;
+  const int prev = p > 0 ? 31 - __clz(active & ((1u << p) - 1u)) : -1;
+  // this pass's exclusive digit base (from the histograms)
+  const uint32_t h = __ldcg(&a.ctl->hist[p][threadIdx.x]);
+  sm.gbase[threadIdx.x] = block_exclusive_scan(h, sm.wsum, nullptr);
+  if (prev >= 0) wait_count(&a.ctl->done[prev + 1], prev == 0 ? a.T0 : live);
   __syncthreads();
-  ds_pass_tile(a, sm, p, j, m);
+  ds_mark(t, 1);
+  ds_pass_tile(a, sm, p, j, m, t, odd, last);
+}
+
+// The fallback sort: a small persistent grid; each CTA takes tickets until the
+// chain is exhausted.  A CTA only ever waits for stages whose tickets were
+// already taken by running CTAs, so any grid size is deadlock-free.  Exits at
+// once unless the bucket fast path overflowed.
+__global__ void __launch_bounds__(kDsThreads, 3) k_depth_sort(DsArgs a, const uint32_t *overflow) {
+  if (*overflow == 0u) return;
+  extern __shared__ __align__(16) unsigned char ds_raw[];
+  DsSmem &sm = *reinterpret_cast<DsSmem *>(ds_raw);
+  const uint32_t total = a.T0 + kDsPasses * a.TP;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.ctl->ticket, 1u);
+    __syncthreads();
+    const uint32_t t = sm.ticket;
+    if (t >= total) return;
+    ds_ticket(a, sm, t);
+  }
+}
+
+// ----------------------------------------------- (A) fast path: value buckets
+// Every selected key falls in one of 2^kBBits buckets by (key - kmin) >> shift,
+// which is monotone in the key, so bucket order is key order.  K0 selects and
+// finds [kmin, kmax]; K1 counts per bucket; K2 scans; K3 scatters (unstable, by
+// atomic slot claims); K4 ranks every item inside its bucket by (key, index) —
+// buckets hold a handful of items — and writes the outputs.  A bucket larger
+// than kBMax (an adversarial depth distribution) raises `overflow`, and the
+// ticketed LSD sort below (k_depth_sort, launched on a small persistent grid
+// that exits at once otherwise) recomputes the order from scratch.
+constexpr int kBBits = 17;
+constexpr uint32_t kBuckets = 1u << kBBits;
+constexpr uint32_t kBMax = 256;
+constexpr int kBScanIPT = 16;
+constexpr int kBScanTile = 256 * kBScanIPT;  // buckets per scan CTA
+
+struct BsCtl {                 // zeroed before every call
+  unsigned long long kmin_inv; // atomicMax of ~key
+  unsigned long long kmax;
+  uint32_t m, overflow, ticket, pad;
+};
+
+struct BsArgs {
+  const float *splats;
+  const int32_t *tiles_touched;
+  const uint64_t *depth_keys;
+  uint32_t n;
+  Band b;
+  BsCtl *ctl;
+  uint2 *rect_by_gid;
+  uint32_t *bcount, *boff, *bstatus;
+  uint64_t *keys;
+  uint32_t *vals, *ids;
+  uint2 *rects_sorted;
+  unsigned long long *num_instances;
+  uint32_t *zero;              // fallback state zeroed here (zero_words)
+  size_t zero_words;
+};
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t key, uint64_t kmin, int shift) {
+  return (uint32_t)((key - kmin) >> shift);
+}
+__device__ __forceinline__ int bucket_shift(uint64_t kmin, uint64_t kmax) {
+  const uint64_t range = kmax - kmin;
+  return range == 0 ? 0 : max(0, 64 - __clzll((long long)range) - kBBits);
+}
+
+__device__ __forceinline__ uint64_t bs_key(const BsArgs &a, uint32_t i) {
+  return a.depth_keys ? __ldg(a.depth_keys + i) : orderable_key64((double)__ldg(a.splats + 12 * (size_t)i + 9));
+}
+
+// K0: per Gaussian band rect (kNoRect if not selected), key range, counts.
+// Grid-stride over a few CTAs per SM with one block reduction per CTA, so the
+// four global counters see a few hundred atomics instead of one per warp.
+__global__ void __launch_bounds__(256) k_bs_select(BsArgs a) {
+  __shared__ unsigned long long r_min[8], r_max[8], r_inst[8];
+  __shared__ uint32_t r_sel[8];
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  for (size_t e = gtid; e < kBuckets; e += gstride) a.bcount[e] = 0;
+  for (size_t e = gtid; e < a.zero_words; e += gstride) a.zero[e] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long kmin_inv = 0ull, kmax = 0ull, inst = 0ull;
+  uint32_t nsel = 0;
+  for (size_t ii = gtid; ii < a.n; ii += gstride) {
+    const uint32_t i = (uint32_t)ii;
+    int x0 = 0, y0 = 0, x1 = -1, y1 = -1, c = 0;
+    if (__ldg(a.tiles_touched + i) > 0) {
+      const float4 sp = __ldg(reinterpret_cast<const float4 *>(a.splats + 12 * (size_t)i));
+      c = tile_rect(sp.x, sp.y, __ldg(a.splats + 12 * (size_t)i + 10), a.b.W, a.b.H, a.b.ts, a.b.tiles_x,
+                    a.b.tiles_y, x0, y0, x1, y1);
+      if (c > 0) {
+        y0 = max(y0, a.b.row_begin);
+        y1 = min(y1, a.b.row_end - 1);
+        c = y1 >= y0 ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0;
+      }
+    }
+    const bool ok = c > 0;
+    a.rect_by_gid[i] = ok ? pack_rect(x0, y0 - a.b.row_begin, x1, y1 - a.b.row_begin) : make_uint2(kNoRect, kNoRect);
+    if (ok) {
+      const uint64_t key = bs_key(a, i);
+      kmin_inv = max(kmin_inv, (unsigned long long)~key);
+      kmax = max(kmax, (unsigned long long)key);
+      ++nsel;
+      inst += (uint32_t)c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    kmin_inv = max(kmin_inv, __shfl_xor_sync(0xffffffffu, kmin_inv, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+    inst += __shfl_xor_sync(0xffffffffu, inst, o);
+  }
+  if (lane == 0) {
+    r_min[warp] = kmin_inv; r_max[warp] = kmax; r_inst[warp] = inst; r_sel[warp] = nsel;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      kmin_inv = max(kmin_inv, r_min[w]); kmax = max(kmax, r_max[w]);
+      inst += r_inst[w]; nsel += r_sel[w];
+    }
+    if (nsel) {
+      atomicMax(&a.ctl->kmin_inv, kmin_inv);
+      atomicMax(&a.ctl->kmax, kmax);
+      atomicAdd(&a.ctl->m, nsel);
+      atomicAdd(a.num_instances, inst);
+    }
+  }
+}
+
+// K1: bucket counts.
+__global__ void __launch_bounds__(256) k_bs_hist(BsArgs a) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n || __ldg(&a.rect_by_gid[i].x) == kNoRect) return;
+  const uint64_t kmin = ~a.ctl->kmin_inv;
+  const int shift = bucket_shift(kmin, a.ctl->kmax);
+  atomicAdd(a.bcount + bucket_of(bs_key(a, i), kmin, shift), 1u);
+}
+
+// K2: exclusive scan of the bucket counts -> boff (kBuckets + 1) and the scatter
+// cursors (bcount, in place); CTAs chained by decoupled look-back.
+__global__ void __launch_bounds__(256) k_bs_scan(BsArgs a) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t s_blk, s_excl;
+  if (threadIdx.x == 0) s_blk = atomicAdd(&a.ctl->ticket, 1u);
+  __syncthreads();
+  const uint32_t base = s_blk * kBScanTile + threadIdx.x * kBScanIPT;
+  uint4 v[kBScanIPT / 4];
+#pragma unroll
+  for (int k = 0; k < kBScanIPT / 4; ++k) v[k] = reinterpret_cast<const uint4 *>(a.bcount + base)[k];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kBScanIPT / 4; ++k) s += v[k].x + v[k].y + v[k].z + v[k].w;
+  uint32_t tot;
+  uint32_t run = block_exclusive_scan(s, ws, &tot);
+  if (threadIdx.x == 0) s_excl = lookback<16>(a.bstatus, 1, s_blk, tot);
+  __syncthreads();
+  run += s_excl;
+#pragma unroll
+  for (int k = 0; k < kBScanIPT / 4; ++k) {
+    uint4 o;
+    o.x = run; run += v[k].x;
+    o.y = run; run += v[k].y;
+    o.z = run; run += v[k].z;
+    o.w = run; run += v[k].w;
+    reinterpret_cast<uint4 *>(a.boff + base)[k] = o;
+    reinterpret_cast<uint4 *>(a.bcount + base)[k] = o;
+  }
+  if (base + kBScanIPT == kBuckets) a.boff[kBuckets] = run;
+}
+
+// K3: scatter into buckets (slot order inside a bucket is arbitrary).
+__global__ void __launch_bounds__(256) k_bs_scatter(BsArgs a) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n || __ldg(&a.rect_by_gid[i].x) == kNoRect) return;
+  const uint64_t kmin = ~a.ctl->kmin_inv;
+  const int shift = bucket_shift(kmin, a.ctl->kmax);
+  const uint64_t key = bs_key(a, i);
+  const uint32_t pos = atomicAdd(a.bcount + bucket_of(key, kmin, shift), 1u);
+  a.keys[pos] = key;
+  a.vals[pos] = i;
+}
+
+// K4: exact rank inside the bucket by (key, index); outputs in depth order.
+__global__ void __launch_bounds__(256) k_bs_rank(BsArgs a) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.ctl->m) return;
+  const uint64_t kmin = ~a.ctl->kmin_inv;
+  const int shift = bucket_shift(kmin, a.ctl->kmax);
+  const uint64_t key = a.keys[p];
+  const uint32_t val = a.vals[p];
+  const uint32_t b = bucket_of(key, kmin, shift);
+  const uint32_t s = __ldg(a.boff + b), e = __ldg(a.boff + b + 1);
+  if (e - s > kBMax) {
+    a.ctl->overflow = 1u;
+    return;
+  }
+  uint32_t rank = 0;
+  for (uint32_t q = s; q < e; ++q) {
+    const uint64_t kq = a.keys[q];
+    const uint32_t vq = a.vals[q];
+    rank += (kq < key) || (kq == key && vq < val);
+  }
+  a.ids[s + rank] = val;
+  a.rects_sorted[s + rank] = __ldg(a.rect_by_gid + val);
 }
 
 struct GaussWS {
   uint64_t *keysA, *keysB;
-  uint32_t *valsA, *valsB;  // valsA: depth-ordered Gaussian ids after the sort
+  uint32_t *valsA, *valsB;
+  uint32_t *ids;            // depth-ordered Gaussian ids after the sort
   uint2 *rect_by_gid, *rects_sorted;
   DsCtl *ctl;
-  uint32_t *sel_status, *status;
+  uint32_t *status;
   uint32_t T0, TP;
-  size_t zero_off, zero_bytes, bytes;
+  BsCtl *bctl;
+  uint32_t *bcount, *boff, *bstatus;
+  size_t zero_off, zero_bytes, bytes;   // [zero_off, +zero_bytes): fallback state + bstatus, zeroed by K0
 };
 
 inline GaussWS carve_gauss(void *p, int64_t n) {
@@ -384,13 +667,17 @@ inline GaussWS carve_gauss(void *p, int64_t n) {
   w.keysB = c.take<uint64_t>(N);
   w.valsA = c.take<uint32_t>(N);
   w.valsB = c.take<uint32_t>(N);
+  w.ids = c.take<uint32_t>(N);
   w.rect_by_gid = c.take<uint2>(N);
   w.rects_sorted = c.take<uint2>(N);
   w.zero_off = c.off;
   w.ctl = c.take<DsCtl>(1);
-  w.sel_status = c.take<uint32_t>(w.T0);
   w.status = c.take<uint32_t>((size_t)kDsPasses * w.TP * 256);
+  w.bstatus = c.take<uint32_t>(kBuckets / kBScanTile);
   w.zero_bytes = c.off - w.zero_off;
+  w.bctl = c.take<BsCtl>(1);
+  w.bcount = c.take<uint32_t>(kBuckets);
+  w.boff = c.take<uint32_t>(kBuckets + 1);
   w.bytes = c.off;
   return w;
 }
@@ -415,9 +702,8 @@ constexpr int kChunk = 512;             // Gaussians per chunk = 8 warps x 64
 constexpr int kChunkWarps = kChunk / 64;
 constexpr int kSeg = 4;                 // chunks per segment (counted by one CTA, in order)
 constexpr int kDiffCells = 12288;       // 2D difference cells per count CTA
-constexpr int kUnit = 8192;             // entries per L1 scatter CTA
-constexpr int kScanCols = 128;          // bins per segment-scan CTA
-constexpr int kScanGroups = 8;          // segment ranges per segment-scan CTA
+constexpr int kScanCols = 32;           // bins per segment-scan CTA
+constexpr int kScanGroups = 32;         // segment ranges per segment-scan CTA
 constexpr int kPlaceWarps = 16;
 constexpr int kPUnit = 2048;            // entries per L2 unit
 
@@ -590,7 +876,7 @@ __global__ void __launch_bounds__(kScanCols * kScanGroups) k_seg_base(uint32_t *
   }
 }
 
-// L1 scatter.  CTAs take balanced units of <= kUnit entries of one chunk; a CTA
+// L1 scatter.  One CTA per chunk (a chunk has ~1.5 entries per Gaussian); it
 // builds the 64-bit super-tile coverage masks of all 8 groups (64 Gaussians
 // each) of its chunk, then entry (Gaussian k of group w, super-tile S = (x, y))
 // goes to  soff[S] + segbase[s][S] + rel[c][S]
@@ -608,28 +894,12 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_scatter(const uint2 *__res
   __shared__ uint32_t s_rect[kChunk];   // x0 | y0 << 16 (super-tiles)
   __shared__ uint32_t s_nx[kChunk];
   __shared__ uint32_t ws[32];
-  __shared__ uint32_t s_c, s_part;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t m = *d_m;
   const uint32_t live = ceil_div<uint32_t>(m, (uint32_t)kChunk);
   const uint32_t NS = (uint32_t)(sx * sy);
-  if (threadIdx.x == 0) s_c = 0xffffffffu;
-  __syncthreads();
-  uint32_t carry = 0;
-  for (uint32_t b0 = 0; b0 < live; b0 += blockDim.x) {
-    const uint32_t c = b0 + threadIdx.x;
-    const uint32_t u = c < live ? ceil_div<uint32_t>(__ldg(chunk_ent + c), kUnit) : 0u;
-    uint32_t tot;
-    const uint32_t ex = carry + block_exclusive_scan(u, ws, &tot);
-    if (u && blockIdx.x >= ex && blockIdx.x < ex + u) {
-      s_c = c;
-      s_part = blockIdx.x - ex;
-    }
-    carry += tot;
-  }
-  __syncthreads();
-  const uint32_t c = s_c;
-  if (c == 0xffffffffu) return;
+  const uint32_t c = blockIdx.x;
+  if (c >= live) return;
   const int mw = sx + sy + 2;           // column masks [0, sx], row masks after
   for (int e = threadIdx.x; e < kChunkWarps * mw; e += blockDim.x) mk[e] = 0ull;
   const uint32_t j0 = c * kChunk;
@@ -690,8 +960,7 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_scatter(const uint2 *__res
     }
   }
   __syncthreads();
-  const uint32_t total = __ldg(chunk_ent + c);
-  const uint32_t e_begin = s_part * kUnit, e_end = tmin<uint32_t>(e_begin + kUnit, total);
+  const uint32_t e_begin = 0, e_end = __ldg(chunk_ent + c);
   const uint16_t *crel = rel + (size_t)c * NS;
   const uint32_t *sb = segbase + (size_t)(c / kSeg) * NS;
   for (uint32_t e = e_begin + threadIdx.x; e < e_end; e += blockDim.x) {
@@ -973,6 +1242,12 @@ inline bool band_ok(int W, int H, int ts, int rb, int re, Band &b) {
 
 using namespace tgs;
 
+// Debug: record per-ticket phase timestamps of the depth sort into `buf`
+// (8 u64 per ticket; null disables).  Not part of the product API.
+extern "C" __attribute__((visibility("default"))) int tgs_debug_trace_depth_sort(unsigned long long *buf) {
+  return cuda_status(cudaMemcpyToSymbol(g_ds_trace, &buf, sizeof(buf)));
+}
+
 extern "C" int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes) {
   if (n < 0 || !bytes) return TGS_ERR_INVALID;
   *bytes = carve_gauss(nullptr, n).bytes;
@@ -989,9 +1264,34 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
     return TGS_ERR_INVALID;
   cudaStream_t st = as_stream(stream);
   GaussWS w = carve_gauss(workspace, n);
-  cudaMemsetAsync(static_cast<char *>(workspace) + w.zero_off, 0, w.zero_bytes, st);
+  cudaMemsetAsync(w.bctl, 0, sizeof(BsCtl), st);
   cudaMemsetAsync(d_num_instances, 0, 8, st);
   if (n == 0) return launch_status();
+  BsArgs ba;
+  ba.splats = splats;
+  ba.tiles_touched = tiles_touched;
+  ba.depth_keys = depth_keys;
+  ba.n = (uint32_t)n;
+  ba.b = b;
+  ba.ctl = w.bctl;
+  ba.rect_by_gid = w.rect_by_gid;
+  ba.bcount = w.bcount;
+  ba.boff = w.boff;
+  ba.bstatus = w.bstatus;
+  ba.keys = w.keysA;
+  ba.vals = w.valsA;
+  ba.ids = w.ids;
+  ba.rects_sorted = w.rects_sorted;
+  ba.num_instances = reinterpret_cast<unsigned long long *>(d_num_instances);
+  ba.zero = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + w.zero_off);
+  ba.zero_words = w.zero_bytes / 4;  // fallback state + scan look-back words
+  const unsigned g = (unsigned)ceil_div<int64_t>(n, 256);
+  k_bs_select<<<(unsigned)tmin<int64_t>(g, 148 * 8), 256, 0, st>>>(ba);
+  k_bs_hist<<<g, 256, 0, st>>>(ba);
+  k_bs_scan<<<kBuckets / kBScanTile, 256, 0, st>>>(ba);
+  k_bs_scatter<<<g, 256, 0, st>>>(ba);
+  k_bs_rank<<<g, 256, 0, st>>>(ba);
+  // fallback: the ticketed LSD chain, only if a bucket overflowed
   DsArgs a;
   a.splats = splats;
   a.tiles_touched = tiles_touched;
@@ -1003,17 +1303,18 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
   a.ctl = w.ctl;
   a.rect_by_gid = w.rect_by_gid;
   a.rects_sorted = w.rects_sorted;
-  a.sel_status = w.sel_status;
+  a.ids = w.ids;
   a.status = w.status;
   a.T0 = w.T0;
   a.TP = w.TP;
-  a.num_instances = reinterpret_cast<unsigned long long *>(d_num_instances);
+  a.num_instances = nullptr;
   static bool attr_done = false;  // idempotent function attribute, set once per process
   if (!attr_done) {
     cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsSmem));
     attr_done = true;
   }
-  k_depth_sort<<<w.T0 + kDsPasses * w.TP, kDsThreads, sizeof(DsSmem), st>>>(a);
+  const unsigned fg = (unsigned)tmin<uint64_t>((uint64_t)w.T0 + kDsPasses * w.TP, 148 * 3);
+  k_depth_sort<<<fg, kDsThreads, sizeof(DsSmem), st>>>(a, &w.bctl->overflow);
   return launch_status();
 }
 
@@ -1047,7 +1348,7 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   if (sc_smem > 160 * 1024 || (g.NS + 1) * 4 > 160 * 1024) return TGS_ERR_UNSUPPORTED;
   GaussWS gw = carve_gauss(gauss_workspace, n);
   InstWS w = carve_inst(workspace, g);
-  const uint32_t *d_m = &gw.ctl->m;
+  const uint32_t *d_m = &gw.bctl->m;
   static bool attr_done = false;  // idempotent function attributes, set once per process
   if (!attr_done) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -1060,13 +1361,12 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
                                                            w.segsum, w.chunk_ent);
   k_seg_base<<<ceil_div<uint32_t>(g.NS, kScanCols), kScanCols * kScanGroups, 0, st>>>(w.segsum, d_m, g.NS, w.status,
                                                                                     w.ticket, w.soff);
-  const uint32_t units = g.nchunks + (uint32_t)(g.ecap / kUnit) + 1;
-  k_scatter<<<units, kChunkWarps * 32, sc_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.sy, w.chunk_ent, w.rel,
+  k_scatter<<<g.nchunks, kChunkWarps * 32, sc_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.sy, w.chunk_ent, w.rel,
                                                       w.segsum, w.soff, w.entries);
   k_place_count<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, g.sx, g.NS, w.ucnt);
   k_tile_scan<<<ceil_div<uint32_t>(g.T, 256), 256, (g.NS + 1) * 4, st>>>(w.soff, g.NS, g.sx, b.tiles_x, rows, w.ucnt,
                                                                         w.tstatus, w.tticket, tile_offsets);
-  k_place_write<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, gw.valsA, g.sx, g.NS,
+  k_place_write<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, gw.ids, g.sx, g.NS,
                                                        b.tiles_x, rows, w.ucnt, tile_offsets, sorted_ids);
   return launch_status();
 }

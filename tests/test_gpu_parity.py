@@ -77,7 +77,7 @@ def test_forward_backward_vs_reference_golden(tgs, name):
         _grad_close(_np(getattr(g, f))[rows], z[f"grad_{f}"], f)
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2", "masked", "deg1", "tile8", "tile32", "uhd", "uhd_c4"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "masked", "deg1", "tile8", "tile32", "uhd", "uhd_c4", "plane"])
 def test_preprocess_and_sort_bit_exact_vs_fp32_oracle(tgs, cfg):
     from paper_2501_14534_b200 import scenes
     kw = {}
@@ -90,6 +90,10 @@ def test_preprocess_and_sort_bit_exact_vs_fp32_oracle(tgs, cfg):
     elif cfg == "uhd_c4":  # c4 cluster scene, fewer Gaussians, 4K, frame 37 of the orbit
         sc = scenes.config4(n=300_000, frames=200)
         sc.cameras[0] = sc.cameras[37]
+    elif cfg == "plane":  # 12k Gaussians at exactly one depth: overflows a value bucket -> LSD fallback
+        sc = scenes.small_scene(seed=23, n=24_000, width=320, height=240, dist=4.0)
+        sc.fields["positions"][:12_000, 0] = 0.0
+        sc.cameras[0] = scenes.pinhole((4.0, 0.0, 0.0), 320, 240)
     else:
         sc = scenes.small_scene(seed=21, n=30_000, width=333, height=207, dist=3.0)
         kw = {"masked": dict(mask_threshold=0.85, sh_mask_threshold=0.85, lowpass_s=0.5),
@@ -424,3 +428,35 @@ def test_render_sharded_single_rank_nccl(tgs):
         assert np.array_equal(_np(counts), per_tile)
     finally:
         dist.destroy_process_group()
+
+
+def test_depth_sort_fallback_path_runs_only_on_bucket_overflow(tgs):
+    """The value-bucket depth sort hands over to the ticketed LSD chain exactly when a
+    bucket overflows; the chain's per-ticket trace shows which path ran."""
+    import ctypes
+    from paper_2501_14534_b200 import _lib, scenes
+    lib = _lib.load()
+    st = tgs.RenderSettings(near=0.2)
+    buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+    ran = {}
+    for name in ("random", "plane"):
+        sc = scenes.small_scene(seed=23, n=24_000, width=320, height=240, dist=4.0)
+        cam = sc.cameras[0]
+        if name == "plane":
+            sc.fields["positions"][:12_000, 0] = 0.0
+            cam = scenes.pinhole((4.0, 0.0, 0.0), 320, 240)
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        buf.zero_()
+        lib.tgs_debug_trace_depth_sort(ctypes.c_void_p(buf.data_ptr()))
+        try:
+            out = tgs.render_forward(cloud, cam, st)
+            torch.cuda.synchronize()
+        finally:
+            lib.tgs_debug_trace_depth_sort(ctypes.c_void_p(0))
+        ran[name] = bool((buf != 0).any())
+        ref = oracle.preprocess(sc.fields, cam, st, "f32")
+        off, ids, _, _ = oracle.bin_tiles(ref["splats"], ref["tiles_touched"], cam.width, cam.height, st.tile_size,
+                                          "f32", ref["depth_key"])
+        assert np.array_equal(_np(out._tiles.offsets).astype(np.int64), off)
+        assert np.array_equal(_np(out._tiles.indices).astype(np.int64), ids)
+    assert ran == {"random": False, "plane": True}
