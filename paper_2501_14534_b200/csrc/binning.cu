@@ -1012,31 +1012,32 @@ __device__ __forceinline__ void place_masks(uint2 rc, bool ok, int stx0, int sty
   m1 = col & r1;
 }
 
-// (super-tile, unit-in-super-tile, first entry, end entry) of unit u; false past the last unit
-__device__ __forceinline__ bool place_unit(const uint32_t *__restrict__ soff, uint32_t NS, uint32_t u, uint32_t *ws,
-                                           uint32_t &S, uint32_t &k, uint32_t &ea, uint32_t &eb, uint32_t &u0) {
-  __shared__ uint32_t s_S, s_k, s_u0;
-  if (threadIdx.x == 0) s_S = 0xffffffffu;
-  __syncthreads();
+// Unit table: ubase[S] = units before super-tile S (ubase[NS] = total), utab[u] = S.
+__global__ void __launch_bounds__(1024) k_unit_table(const uint32_t *__restrict__ soff, uint32_t NS,
+                                                     uint32_t *__restrict__ ubase, uint32_t *__restrict__ utab) {
+  __shared__ uint32_t ws[32];
   uint32_t carry = 0;
   for (uint32_t b0 = 0; b0 < NS; b0 += blockDim.x) {
     const uint32_t s = b0 + threadIdx.x;
-    const uint32_t n = s < NS ? ceil_div<uint32_t>(__ldg(soff + s + 1) - __ldg(soff + s), kPUnit) : 0u;
+    const uint32_t n = s < NS ? ceil_div<uint32_t>(soff[s + 1] - soff[s], kPUnit) : 0u;
     uint32_t tot;
     const uint32_t ex = carry + block_exclusive_scan(n, ws, &tot);
-    if (n && u >= ex && u < ex + n) {
-      s_S = s;
-      s_k = u - ex;
-      s_u0 = ex;
+    if (s < NS) {
+      ubase[s] = ex;
+      for (uint32_t k = 0; k < n; ++k) utab[ex + k] = s;
     }
     carry += tot;
   }
-  __syncthreads();
-  S = s_S;
-  if (S == 0xffffffffu) return false;
-  k = s_k;
-  u0 = s_u0;
-  ea = __ldg(soff + S) + k * kPUnit;
+  if (threadIdx.x == 0) ubase[NS] = carry;
+}
+
+// (super-tile, first entry, end entry) of unit u; false past the last unit
+__device__ __forceinline__ bool place_unit(const uint32_t *__restrict__ soff, const uint32_t *__restrict__ ubase,
+                                           const uint32_t *__restrict__ utab, uint32_t NS, uint32_t u, uint32_t &S,
+                                           uint32_t &ea, uint32_t &eb) {
+  if (u >= __ldg(ubase + NS)) return false;
+  S = __ldg(utab + u);
+  ea = __ldg(soff + S) + (u - __ldg(ubase + S)) * kPUnit;
   eb = tmin<uint32_t>(ea + kPUnit, __ldg(soff + S + 1));
   return true;
 }
@@ -1044,12 +1045,13 @@ __device__ __forceinline__ bool place_unit(const uint32_t *__restrict__ soff, ui
 // Pass 1: per (unit, tile-of-super-tile) instance counts.
 __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_count(const uint32_t *__restrict__ entries,
                                                                    const uint32_t *__restrict__ soff,
+                                                                   const uint32_t *__restrict__ ubase,
+                                                                   const uint32_t *__restrict__ utab,
                                                                    const uint2 *__restrict__ rects, int sx,
                                                                    uint32_t NS, uint32_t *__restrict__ ucnt) {
-  __shared__ uint32_t ws[32];
   __shared__ uint32_t wc[kPlaceWarps][64];
-  uint32_t S, k, ea, eb, u0;
-  if (!place_unit(soff, NS, blockIdx.x, ws, S, k, ea, eb, u0)) return;
+  uint32_t S, ea, eb;
+  if (!place_unit(soff, ubase, utab, NS, blockIdx.x, S, ea, eb)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int stx0 = (int)(S % sx) * kST, sty0 = (int)(S / sx) * kST;
   uint32_t n0 = 0, n1 = 0;
@@ -1074,24 +1076,13 @@ __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_count(const uint32_t
 
 // Per tile: exclusive scan of its super-tile's unit counts (in place), the tile
 // total, and the CSR offsets (blocks of 256 tiles chained by look-back).
-__global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ soff, uint32_t NS, int sx,
-                                                   int tiles_x, int rows, uint32_t *__restrict__ ucnt,
+__global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ ubase, int sx, int tiles_x,
+                                                   int rows, uint32_t *__restrict__ ucnt,
                                                    uint32_t *__restrict__ status, uint32_t *__restrict__ ticket,
                                                    int32_t *__restrict__ offsets) {
-  extern __shared__ uint32_t ubase[];  // NS + 1 unit prefix
   __shared__ uint32_t ws[32];
   __shared__ uint32_t s_blk, s_excl;
   if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
-  uint32_t carry = 0;
-  for (uint32_t b0 = 0; b0 < NS; b0 += blockDim.x) {
-    const uint32_t s = b0 + threadIdx.x;
-    const uint32_t n = s < NS ? ceil_div<uint32_t>(__ldg(soff + s + 1) - __ldg(soff + s), kPUnit) : 0u;
-    uint32_t tot;
-    const uint32_t ex = carry + block_exclusive_scan(n, ws, &tot);
-    if (s < NS) ubase[s] = ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) ubase[NS] = carry;
   __syncthreads();
   const uint32_t T = (uint32_t)(rows * tiles_x);
   const uint32_t t = s_blk * blockDim.x + threadIdx.x;
@@ -1100,7 +1091,7 @@ __global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ 
     const int ty = (int)(t / tiles_x), tx = (int)(t % tiles_x);
     const uint32_t S = (uint32_t)((ty >> kSTShift) * sx + (tx >> kSTShift));
     const uint32_t q = (uint32_t)(((ty & (kST - 1)) << kSTShift) | (tx & (kST - 1)));
-    for (uint32_t u = ubase[S]; u < ubase[S + 1]; ++u) {
+    for (uint32_t u = __ldg(ubase + S); u < __ldg(ubase + S + 1); ++u) {
       const uint32_t v = ucnt[(size_t)u * 64 + q];
       ucnt[(size_t)u * 64 + q] = run;
       run += v;
@@ -1116,24 +1107,32 @@ __global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ 
   }
 }
 
-// Pass 2: rounds of 512 entries; each tile's run of the round (entries of all
-// warps covering it, in order) is written by consecutive lanes (coalesced).
+// Pass 2: rounds of 512 entries.  Per round and tile, the run of ids (entries of
+// all warps covering the tile, in entry order) is assembled in shared memory —
+// each entry's lane writes its id to stage[tile start + warp prefix + rank among
+// the warp's entries covering the tile] for every tile of its clipped rect — and
+// then copied out by consecutive lanes (coalesced).
+constexpr int kStage = 8192;
+
 __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t *__restrict__ entries,
                                                                    const uint32_t *__restrict__ soff,
+                                                                   const uint32_t *__restrict__ ubase,
+                                                                   const uint32_t *__restrict__ utab,
                                                                    const uint2 *__restrict__ rects,
                                                                    const uint32_t *__restrict__ ids, int sx,
                                                                    uint32_t NS, int tiles_x, int rows,
                                                                    const uint32_t *__restrict__ ucnt,
                                                                    const int32_t *__restrict__ offsets,
                                                                    int32_t *__restrict__ sorted_ids) {
-  __shared__ uint32_t ws[32];
   __shared__ uint32_t mk[kPlaceWarps][64];     // entries of warp w covering tile q
-  __shared__ uint32_t pre[kPlaceWarps + 1][64];  // exclusive over warps; row kPlaceWarps = run length
-  __shared__ uint32_t sg[kPlaceWarps][32];
-  __shared__ uint32_t cur[64];
-  uint32_t S, k, ea, eb, u0;
-  if (!place_unit(soff, NS, blockIdx.x, ws, S, k, ea, eb, u0)) return;
+  __shared__ uint32_t pre[kPlaceWarps][64];    // exclusive over warps
+  __shared__ uint32_t len[64], sst[64], cur[64];
+  __shared__ uint32_t s_total;
+  __shared__ uint32_t stage[kStage];
+  uint32_t S, ea, eb;
+  if (!place_unit(soff, ubase, utab, NS, blockIdx.x, S, ea, eb)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
   const int stx0 = (int)(S % sx) * kST, sty0 = (int)(S / sx) * kST;
   if (threadIdx.x < 64) {
     const int q = threadIdx.x, tx = stx0 + (q & 7), ty = sty0 + (q >> 3);
@@ -1146,7 +1145,7 @@ __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t
     const bool ok = b < eb;
     const uint32_t j = ok ? __ldg(entries + b) : 0u;
     const uint2 rc = ok ? __ldg(rects + j) : make_uint2(0, 0);
-    sg[warp][lane] = ok ? __ldg(ids + j) : 0u;
+    const uint32_t gid = ok ? __ldg(ids + j) : 0u;
     uint32_t m0, m1;
     place_masks(rc, ok, stx0, sty0, lane, m0, m1);
     mk[warp][lane] = m0;
@@ -1159,29 +1158,63 @@ __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t
         pre[w][threadIdx.x] = r;
         r += __popc(mk[w][threadIdx.x]);
       }
-      pre[kPlaceWarps][threadIdx.x] = r;
+      len[threadIdx.x] = r;
     }
     __syncthreads();
-    for (int q = warp; q < 64; q += kPlaceWarps) {
-      const uint32_t len = pre[kPlaceWarps][q];
-      const uint32_t base = cur[q];
-      for (uint32_t i = lane; i < len; i += 32) {
-        int w = 0;  // last warp whose prefix is <= i
+    if (warp == 0) {  // run starts in the stage: exclusive scan over the 64 tiles
+      const uint32_t l0 = len[2 * lane], l1 = len[2 * lane + 1];
+      uint32_t v = l0 + l1;
 #pragma unroll
-        for (int step = kPlaceWarps / 2; step >= 1; step >>= 1)
-          if (pre[w + step][q] <= i) w += step;
-        const uint32_t bit = __fns(mk[w][q], 0, (int)(i - pre[w][q]) + 1);
-        sorted_ids[base + i] = (int32_t)sg[w][bit];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
       }
-      if (lane == 0) cur[q] = base + len;
+      const uint32_t ex = v - l0 - l1;
+      sst[2 * lane] = ex;
+      sst[2 * lane + 1] = ex + l0;
+      if (lane == 31) s_total = v;
     }
+    __syncthreads();
+    const uint32_t total = s_total;
+    if (total <= (uint32_t)kStage) {
+      if (ok) {  // this entry's tiles inside the super-tile
+        int x0, y0, x1, y1;
+        unpack_rect(rc, x0, y0, x1, y1);
+        x0 = max(x0 - stx0, 0); x1 = min(x1 - stx0, kST - 1);
+        y0 = max(y0 - sty0, 0); y1 = min(y1 - sty0, kST - 1);
+        for (int y = y0; y <= y1; ++y)
+          for (int x = x0; x <= x1; ++x) {
+            const int q = y * kST + x;
+            stage[sst[q] + pre[warp][q] + __popc(mk[warp][q] & lt)] = gid;
+          }
+      }
+      __syncthreads();
+      for (int q = warp; q < 64; q += kPlaceWarps) {
+        const uint32_t l = len[q], so = sst[q], base = cur[q];
+        for (uint32_t i = lane; i < l; i += 32) sorted_ids[base + i] = (int32_t)stage[so + i];
+      }
+    } else {  // oversized round (huge rects): each entry writes its ids directly
+      if (ok) {
+        int x0, y0, x1, y1;
+        unpack_rect(rc, x0, y0, x1, y1);
+        x0 = max(x0 - stx0, 0); x1 = min(x1 - stx0, kST - 1);
+        y0 = max(y0 - sty0, 0); y1 = min(y1 - sty0, kST - 1);
+        for (int y = y0; y <= y1; ++y)
+          for (int x = x0; x <= x1; ++x) {
+            const int q = y * kST + x;
+            sorted_ids[cur[q] + pre[warp][q] + __popc(mk[warp][q] & lt)] = (int32_t)gid;
+          }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) cur[threadIdx.x] += len[threadIdx.x];
     __syncthreads();
   }
 }
 
 struct InstWS {
   uint16_t *rel;
-  uint32_t *segsum, *soff, *entries, *ucnt, *status, *ticket, *chunk_ent, *tstatus, *tticket;
+  uint32_t *segsum, *soff, *entries, *ucnt, *status, *ticket, *chunk_ent, *tstatus, *tticket, *ubase, *utab;
   size_t zero_off, zero_bytes, bytes;
 };
 
@@ -1193,6 +1226,8 @@ static InstWS carve_inst(void *p, const InstGeom &g) {
   w.soff = c.take<uint32_t>(g.NS + 1);
   w.entries = c.take<uint32_t>(g.ecap);
   w.ucnt = c.take<uint32_t>((size_t)g.punits * 64);
+  w.ubase = c.take<uint32_t>(g.NS + 1);
+  w.utab = c.take<uint32_t>(g.punits);
   w.zero_off = c.off;
   w.ticket = c.take<uint32_t>(1);
   w.status = c.take<uint32_t>(ceil_div<uint32_t>(g.NS, kScanCols));
@@ -1345,7 +1380,7 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   if (!workspace || !sorted_ids) return TGS_ERR_INVALID;
   const size_t sc_smem = (size_t)kChunkWarps * (g.sx + g.sy + 2) * 8;
   const size_t cnt_smem = ((size_t)(g.sx + 1) * (g.slab_rows + 1) + (size_t)g.slab_rows * g.sx) * 4;
-  if (sc_smem > 160 * 1024 || (g.NS + 1) * 4 > 160 * 1024) return TGS_ERR_UNSUPPORTED;
+  if (sc_smem > 160 * 1024) return TGS_ERR_UNSUPPORTED;
   GaussWS gw = carve_gauss(gauss_workspace, n);
   InstWS w = carve_inst(workspace, g);
   const uint32_t *d_m = &gw.bctl->m;
@@ -1353,7 +1388,6 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   if (!attr_done) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(k_seg_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDiffCells * 4);
-    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr_done = true;
   }
   cudaMemsetAsync(static_cast<char *>(workspace) + w.zero_off, 0, w.zero_bytes, st);
@@ -1363,10 +1397,13 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
                                                                                     w.ticket, w.soff);
   k_scatter<<<g.nchunks, kChunkWarps * 32, sc_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.sy, w.chunk_ent, w.rel,
                                                       w.segsum, w.soff, w.entries);
-  k_place_count<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, g.sx, g.NS, w.ucnt);
-  k_tile_scan<<<ceil_div<uint32_t>(g.T, 256), 256, (g.NS + 1) * 4, st>>>(w.soff, g.NS, g.sx, b.tiles_x, rows, w.ucnt,
-                                                                        w.tstatus, w.tticket, tile_offsets);
-  k_place_write<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, gw.rects_sorted, gw.ids, g.sx, g.NS,
+  k_unit_table<<<1, 1024, 0, st>>>(w.soff, g.NS, w.ubase, w.utab);
+  k_place_count<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, w.ubase, w.utab, gw.rects_sorted, g.sx,
+                                                       g.NS, w.ucnt);
+  k_tile_scan<<<ceil_div<uint32_t>(g.T, 256), 256, 0, st>>>(w.ubase, g.sx, b.tiles_x, rows, w.ucnt, w.tstatus,
+                                                           w.tticket, tile_offsets);
+  k_place_write<<<g.punits, kPlaceWarps * 32, 0, st>>>(w.entries, w.soff, w.ubase, w.utab, gw.rects_sorted, gw.ids,
+                                                       g.sx, g.NS,
                                                        b.tiles_x, rows, w.ucnt, tile_offsets, sorted_ids);
   return launch_status();
 }
