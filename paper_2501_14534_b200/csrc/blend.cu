@@ -37,6 +37,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 constexpr float kLog2e = 1.44269504088896341f;
 constexpr float kE2Min = (float)(-4.5 * 1.44269504088896341);  // the e >= -4.5 cut in log2 units
 
@@ -379,6 +385,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
 // ((w & 1) * 8, (w >> 1) * 8), lane -> (x = lane & 7, y = lane >> 3) and the
 // pixels (x, y) and (x, y + 4).  Per surviving splat a warp evaluates 64 pixels
 // and (backward) performs ONE reduction, halving the per-visit overhead.
+// (The kernels follow below: k_blend_fwd16w / k_blend_bwd16w.)
 constexpr int kT16Threads = 128;
 
 __device__ __forceinline__ void pixel_pair16(int t, int tx, int ty, int &px, int &pyA, int &pyB) {
@@ -427,45 +434,129 @@ __device__ __forceinline__ void fwd_entry(Fwd16Pixel &P, float fpx, float fpy, f
   if (hits) atomicAdd(hits + gid, 1);
 }
 
-__global__ void __launch_bounds__(kT16Threads) k_blend_fwd16(
+struct Bwd16Pixel {
+  int lastp = 0;
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 0.f;
+  float GS = 0.f;  // sum_c g_c * S_c, S = suffix colour seeded with bg * T_final
+};
+
+// one list entry of the back-to-front walk for one pixel (_kernels.py:136-181),
+// with dL/dalpha_hat = (g . c) T_before - (g . S) / (1 - a)
+__device__ __forceinline__ bool bwd_entry(Bwd16Pixel &P, int pos, float fpx, float fpy, float2 m, float4 q,
+                                          float4 cn, float4 col, float v[9]) {
+  if (pos >= P.lastp) return false;
+  const float dx = fpx - m.x, dy = fpy - m.y;
+  const float e2 = exponent2(q, dx, dy);
+  if (e2 < kE2Min || e2 > 0.0f) return false;
+  const float gauss = ex2_approx(e2);
+  const float a_raw = __fmul_rn(cn.w, gauss);
+  const float al = fminf(a_raw, kAlphaMax);
+  if (al < kAlphaSkip) return false;
+  const float inv_om = rcp_approx(1.0f - al);  // 1 - al >= 0.01: no denormal path needed
+  const float t_before = P.T * inv_om;
+  const float gc = P.g0 * col.x + P.g1 * col.y + P.g2 * col.z;
+  const float ga = gc * t_before - P.GS * inv_om;
+  const float w = al * t_before;
+  v[6] += P.g0 * w;
+  v[7] += P.g1 * w;
+  v[8] += P.g2 * w;
+  if (a_raw <= kAlphaMax) {
+    v[5] += ga * gauss;
+    const float gG = ga * cn.w * gauss;
+    const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
+    v[0] += gG * v0;
+    v[1] += gG * v1;
+    v[2] += gG * 0.5f * v0 * v0;
+    v[3] += gG * v0 * v1;
+    v[4] += gG * 0.5f * v1 * v1;
+  }
+  P.GS += gc * w;
+  P.T = t_before;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-independent 16x16 kernels: each warp of a tile's CTA walks the tile list
+// on its own, staging 32 splats at a time in a private shared-memory slot (the
+// next chunk's records are prefetched into registers while the current one is
+// processed), culls them against its own 8x8 pixel block and leaves as soon as
+// its pixels are done.  No CTA barrier anywhere: the 4 warps of a tile never wait
+// for one another.  The backward flushes each visit's warp-reduced partials with
+// global reductions straight away.
+struct WStage {
+  float2 xy[32];
+  float4 q[32];      // prescaled conic + alpha
+  float4 col[32];    // r, g, b, cull threshold (log2 units)
+  float4 conic[32];  // raw a, b, c, alpha (backward)
+  int32_t id[32];
+};
+
+struct SplatRegs {
+  float4 a, b;
+  float c;
+  int32_t g;
+};
+
+__device__ __forceinline__ void fetch_splat(SplatRegs &r, const float4 *__restrict__ splats,
+                                            const int32_t *__restrict__ ids, int pos, bool ok) {
+  if (ok) {
+    r.g = __ldg(ids + pos);
+    r.a = __ldg(splats + 3 * r.g);
+    r.b = __ldg(splats + 3 * r.g + 1);
+    r.c = __ldg(reinterpret_cast<const float *>(splats + 3 * r.g + 2));
+  }
+}
+
+__global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
     const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
     float *__restrict__ transmit, float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
-  __shared__ Stage S;
+  __shared__ WStage SW[kT16Threads / 32];
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  WStage &S = SW[warp];
   int px, pyA, pyB;
   pixel_pair16(t, tx, ty, px, pyA, pyB);
   const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
   const float4 wb = warp_bounds2(inA, inB, px, pyA, pyB);
-  const int start = offsets[tile], stop = offsets[tile + 1];
+  const int start = __ldg(offsets + tile), stop = __ldg(offsets + tile + 1);
   const float fpx = (float)px, fyA = (float)pyA, fyB = (float)pyB;
   Fwd16Pixel A, B;
   A.done = !inA;
   B.done = !inB;
-  for (int base = start; base < stop; base += kBatch) {
-    if (__syncthreads_count(A.done && B.done) == kT16Threads) break;
-    for (int k = t; k < kBatch && base + k < stop; k += kT16Threads) stage_splat(S, k, splats, ids[base + k]);
-    __syncthreads();
-    const int cnt = min(kBatch, stop - base);
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-      if (__all_sync(0xffffffffu, A.done && B.done)) break;
-      const int j = j0 + lane;
-      uint32_t mask = __ballot_sync(0xffffffffu, j < cnt && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
-      while (mask) {
-        const int k = j0 + __ffs(mask) - 1;
-        mask &= mask - 1;
-        const float2 m = S.xy[k];
-        const float4 q = S.q[k], col = S.col[k];
-        const int pos = base - start + k + 1;
-        fwd_entry(A, fpx, fyA, m, q, col, pos, hits, S.id[k]);
-        fwd_entry(B, fpx, fyB, m, q, col, pos, hits, S.id[k]);
-      }
+  SplatRegs nx;
+  fetch_splat(nx, splats, ids, start + lane, start + lane < stop);
+  for (int c = start; c < stop; c += 32) {
+    if (__all_sync(0xffffffffu, A.done && B.done)) break;
+    const bool ok = c + lane < stop;
+    bool keep = false;
+    if (ok) {
+      const float4 q = prescaled_conic(nx.a, nx.b);
+      const float thr = splat_thr2(nx.b.y);
+      const float2 m = make_float2(nx.a.x, nx.a.y);
+      S.xy[lane] = m;
+      S.q[lane] = q;
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      S.id[lane] = nx.g;
+      keep = !quad_misses(m, q, thr, wb);
+    }
+    uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    fetch_splat(nx, splats, ids, c + 32 + lane, c + 32 + lane < stop);
+    while (mask) {
+      const int k = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const float2 m = S.xy[k];
+      const float4 q = S.q[k], col = S.col[k];
+      const int pos = c - start + k + 1;
+      fwd_entry(A, fpx, fyA, m, q, col, pos, hits, S.id[k]);
+      fwd_entry(B, fpx, fyB, m, q, col, pos, hits, S.id[k]);
     }
     if (A.T < kTTerm) A.done = true;
     if (B.T < kTTerm) B.done = true;
+    __syncwarp();
   }
   if (inA) {
     const int p = pyA * W + px;
@@ -489,70 +580,18 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16(
   }
 }
 
-struct Bwd16Pixel {
-  int lastp = 0;
-  float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 0.f;
-  float GS = 0.f;  // sum_c g_c * S_c, S = suffix colour seeded with bg * T_final
-};
-
-// one list entry of the back-to-front walk for one pixel (_kernels.py:136-181),
-// with dL/dalpha_hat = (g . c) T_before - (g . S) / (1 - a)
-__device__ __forceinline__ bool bwd_entry(Bwd16Pixel &P, int pos, float fpx, float fpy, float2 m, float4 q,
-                                          float4 cn, float4 col, float v[9]) {
-  if (pos >= P.lastp) return false;
-  const float dx = fpx - m.x, dy = fpy - m.y;
-  const float e2 = exponent2(q, dx, dy);
-  if (e2 < kE2Min || e2 > 0.0f) return false;
-  const float gauss = ex2_approx(e2);
-  const float a_raw = __fmul_rn(cn.w, gauss);
-  const float al = fminf(a_raw, kAlphaMax);
-  if (al < kAlphaSkip) return false;
-  const float inv_om = __fdividef(1.0f, 1.0f - al);
-  const float t_before = P.T * inv_om;
-  const float gc = P.g0 * col.x + P.g1 * col.y + P.g2 * col.z;
-  const float ga = gc * t_before - P.GS * inv_om;
-  const float w = al * t_before;
-  v[6] += P.g0 * w;
-  v[7] += P.g1 * w;
-  v[8] += P.g2 * w;
-  if (a_raw <= kAlphaMax) {
-    v[5] += ga * gauss;
-    const float gG = ga * cn.w * gauss;
-    const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
-    v[0] += gG * v0;
-    v[1] += gG * v1;
-    v[2] += gG * 0.5f * v0 * v0;
-    v[3] += gG * v0 * v1;
-    v[4] += gG * 0.5f * v1 * v1;
-  }
-  P.GS += gc * w;
-  P.T = t_before;
-  return true;
-}
-
-struct Bwd16Shared {
-  float2 xy[kT16Threads];
-  float4 q[kT16Threads];
-  float4 conic[kT16Threads];
-  float4 col[kT16Threads];
-  int32_t id[kT16Threads];
-  float acc[kT16Threads / 32][9][kT16Threads];
-};
-
-__global__ void __launch_bounds__(kT16Threads) k_blend_bwd16(
+__global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, const float *__restrict__ transmit,
     const int32_t *__restrict__ last_pos, const float *__restrict__ dimage, float *__restrict__ dsplats) {
-  constexpr int kBB = kT16Threads;
-  constexpr int kW = kT16Threads / 32;
-  __shared__ Bwd16Shared S;
-  __shared__ int wmax[kW];
+  __shared__ WStage SW[kT16Threads / 32];
   const int tile = blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  WStage &S = SW[warp];
   int px, pyA, pyB;
   pixel_pair16(t, tx, ty, px, pyA, pyB);
-  const int start = offsets[tile];
+  const int start = __ldg(offsets + tile);
   const float fpx = (float)px, fyA = (float)pyA, fyB = (float)pyB;
   Bwd16Pixel A, B;
   auto load_pixel = [&](Bwd16Pixel &P, int py) {
@@ -570,62 +609,49 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16(
   load_pixel(B, pyB);
   const float4 wb = warp_bounds2(A.lastp > 0, B.lastp > 0, px, pyA, pyB);
   const int wlast = __reduce_max_sync(0xffffffffu, max(A.lastp, B.lastp));
-  if (lane == 0) wmax[warp] = wlast;
-  __syncthreads();
-  int max_last = 0;
-#pragma unroll
-  for (int w = 0; w < kW; ++w) max_last = max(max_last, wmax[w]);
-  for (int hi = max_last; hi > 0; hi -= kBB) {
-    const int lo = hi > kBB ? hi - kBB : 0;
-    const int cnt = hi - lo;
-    __syncthreads();
-    if (t < cnt) {
-      const int g = ids[start + lo + t];
-      const float4 a = splats[3 * g], b = splats[3 * g + 1];
-      S.xy[t] = make_float2(a.x, a.y);
-      S.q[t] = prescaled_conic(a, b);
-      S.conic[t] = make_float4(a.z, a.w, b.x, b.y);
-      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, splat_thr2(b.y));
-      S.id[t] = g;
+  SplatRegs nx;
+  // back to front over chunks [lo, hi) of 32 list positions below this warp's last blend
+  int hi = wlast;
+  fetch_splat(nx, splats, ids, start + hi - 32 + lane, hi - 32 + lane >= 0);
+  for (; hi > 0; hi -= 32) {
+    const int lo = hi - 32;  // may be negative: lanes below position 0 are idle
+    const bool ok = lo + lane >= 0;
+    bool keep = false;
+    if (ok) {
+      const float4 q = prescaled_conic(nx.a, nx.b);
+      const float thr = splat_thr2(nx.b.y);
+      const float2 m = make_float2(nx.a.x, nx.a.y);
+      S.xy[lane] = m;
+      S.q[lane] = q;
+      S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      S.id[lane] = nx.g;
+      keep = !quad_misses(m, q, thr, wb);
     }
-    for (int e = t; e < kW * 9 * kBB; e += kT16Threads) (&S.acc[0][0][0])[e] = 0.0f;
-    __syncthreads();
-    for (int j0 = (cnt - 1) & ~31; j0 >= 0; j0 -= 32) {
-      const int j = j0 + lane;
-      uint32_t mask =
-          __ballot_sync(0xffffffffu, j < cnt && lo + j < wlast && !quad_misses(S.xy[j], S.q[j], S.col[j].w, wb));
-      while (mask) {
-        const int bit = 31 - __clz(mask);
-        mask &= ~(1u << bit);
-        const int qi = j0 + bit;
-        const float2 m = S.xy[qi];
-        const float4 q = S.q[qi], cn = S.conic[qi], col = S.col[qi];
-        float v[9];
+    uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    fetch_splat(nx, splats, ids, start + lo - 32 + lane, lo - 32 + lane >= 0);
+    while (mask) {
+      const int bit = 31 - __clz(mask);
+      mask &= ~(1u << bit);
+      const float2 m = S.xy[bit];
+      const float4 q = S.q[bit], cn = S.conic[bit], col = S.col[bit];
+      float v[9];
 #pragma unroll
-        for (int f = 0; f < 9; ++f) v[f] = 0.0f;
-        const bool hA = bwd_entry(A, lo + qi, fpx, fyA, m, q, cn, col, v);
-        const bool hB = bwd_entry(B, lo + qi, fpx, fyB, m, q, cn, col, v);
-        if (__any_sync(0xffffffffu, hA || hB)) {
-          const float r8 = warp_reduce8_transpose(v, lane);
-          float r9 = v[8];
+      for (int f = 0; f < 9; ++f) v[f] = 0.0f;
+      const bool hA = bwd_entry(A, lo + bit, fpx, fyA, m, q, cn, col, v);
+      const bool hB = bwd_entry(B, lo + bit, fpx, fyB, m, q, cn, col, v);
+      if (__any_sync(0xffffffffu, hA || hB)) {
+        const float r8 = warp_reduce8_transpose(v, lane);
+        float r9 = v[8];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
-          if ((lane & 3) == 0) S.acc[warp][lane >> 2][qi] = r8;
-          if (lane == 0) S.acc[warp][8][qi] = r9;
-        }
+        for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
+        float *d = dsplats + 9 * (int64_t)S.id[bit];
+        if ((lane & 3) == 0 && r8 != 0.0f) atomicAdd(d + (lane >> 2), r8);
+        if (lane == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
       }
     }
-    __syncthreads();
-    if (t < cnt) {
-      float *d = dsplats + 9 * (int64_t)S.id[t];
-#pragma unroll
-      for (int f = 0; f < 9; ++f) {
-        float x = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kW; ++w) x += S.acc[w][f][t];
-        if (x != 0.0f) atomicAdd(d + f, x);
-      }
-    }
+    __syncwarp();
   }
 }
 
@@ -684,7 +710,7 @@ extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offset
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   if (s->tile_size == 16) {
-    k_blend_fwd16<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+    k_blend_fwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
         last_pos, hits);
@@ -722,7 +748,7 @@ extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offse
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   if (s->tile_size == 16) {
-    k_blend_bwd16<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+    k_blend_bwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats);
     return launch_status();
