@@ -6,24 +6,30 @@
 // channels, and the analytic gradient whose adjoint folds the padded border
 // back onto its source pixels (metrics.py:126-135).
 //
-// One fused kernel: each CTA owns a 32x32 output tile and, per channel, keeps
-// everything in shared memory —
-//   inputs a, b on the tile + 10 px halo (52 x 52, symmetric reflection),
-//   horizontal window sums of {a, b, a^2, b^2, ab} on 52 x 42,
-//   vertical window -> SSIM partials dSSIM/d{mu_a, s_aa, s_ab} on 42 x 42
-//     (tile + 5 px, image pixels only), SSIM and L1 sums on the 32 x 32 tile,
-//   vertical adjoint on 32 x 42 and horizontal adjoint on 32 x 32, both with the
-//     reflection fold, combined with sign(a - b) into dimage.
-// HBM traffic is the algorithmic 36 B/pixel (read image + target, write dimage).
+// Two kernels, one CTA per (32 x 32 tile, channel):
+//   k_ssim_fwd  inputs a, b on the tile + 5 px halo (42 x 42, symmetric
+//               reflection) -> horizontal window sums of {a, b, a^2, b^2, ab}
+//               (42 x 32) -> vertical window -> per-pixel SSIM and the partials
+//               d0 = dS/dmu_a, d1 = dS/ds_aa, d2 = dS/ds_ab, written to the
+//               workspace; per-CTA L1 and SSIM partial sums.
+//   k_ssim_adj  partials on the tile + 5 px halo (zero outside the image) ->
+//               vertical adjoint (32 x 42) -> horizontal adjoint (32 x 32), both
+//               with the reflection fold on border tiles, combined with
+//               sign(a - b) into dimage:
+//               dL/da = (1-lam) sign(a-b)/N - lam/2 (G'd0 + 2a G'd1 + b G'd2)/N.
+// Splitting at the partials removes the fused kernel's second 10 px halo (the
+// forward maps no longer have to cover the adjoint's footprint) and keeps each
+// CTA's shared memory under 42 KB, so five CTAs share an SM.
 #include "tgs_common.cuh"
 
 namespace tgs {
 
-constexpr int kR = 5;          // window radius (11 taps)
-constexpr int kT = 32;         // output tile edge
-constexpr int kIn = kT + 4 * kR;   // 52: tile + forward + adjoint halo
-constexpr int kMid = kT + 2 * kR;  // 42: positions whose SSIM partials the tile's adjoint reads
+constexpr int kR = 5;              // window radius (11 taps)
+constexpr int kT = 32;             // output tile edge
+constexpr int kH = kT + 2 * kR;    // 42: tile + halo
 constexpr int kLossThreads = 256;
+constexpr int kHOut = 4;           // horizontal outputs per work item
+constexpr int kVOut = 4;           // vertical outputs per work item
 
 struct Taps {
   float w[2 * kR + 1];
@@ -36,7 +42,7 @@ __device__ __forceinline__ int reflect_clamp(int k, int n) {  // numpy 'symmetri
 }
 
 // Reflection-fold terms of the adjoint at image index y (only near the borders):
-// sum_i w_i (u[R-1-y-i+R] for y < R) + (u[2n-1-y-i+R] for y >= n-R), valid indices.
+// sum_i w_i (u[-1-y-i+R] for y < R) + (u[2n-1-y-i+R] for y >= n-R), valid indices.
 template <typename F>
 __device__ __forceinline__ float adjoint_fold(int y, int n, const Taps &tp, F get) {
   float s = 0.0f;
@@ -53,179 +59,19 @@ __device__ __forceinline__ float adjoint_fold(int y, int n, const Taps &tp, F ge
   return s;
 }
 
-// Work items per phase are sized so each phase fills the 256 threads between
-// barriers: H 52x14 = 728 items (3 outputs), V 42x6 = 252 (7 outputs),
-// vertical adjoint 42x6 = 252 (6 row segments of 5-6 outputs), horizontal
-// adjoint 32x8 = 256 (4 outputs).
-constexpr int kHSeg = 3;
-constexpr int kVSeg = 7;
-constexpr int kAVSeg = 6;   // max rows per vertical-adjoint item
-constexpr int kAVItems = 6; // row segments per column: 32 = 6+5+5+5+5+6
-constexpr int kAHSeg = 4;
+struct LossArgs {
+  const float *img, *tgt;
+  int W, H;
+  Taps tp;
+  float c1, c2, lam, inv_count;
+  float *part;       // [3 channels][3 partials][H][W]
+  double *sums;      // [2][nblocks]: per-CTA L1 and SSIM sums
+  float *dimage;
+};
 
-__global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__restrict__ img,
-                                                             const float *__restrict__ tgt, int W, int H, Taps tp,
-                                                             float c1, float c2, float lam, float inv_count,
-                                                             float *__restrict__ dimage, double *__restrict__ sums) {
-  extern __shared__ float4 smem4[];
-  float *sm = reinterpret_cast<float *>(smem4);
-  float *sa = sm;                         // [kIn][kIn]
-  float *sb = sa + kIn * kIn;             // [kIn][kIn]
-  float *hs = sb + kIn * kIn;             // [5][kIn][kMid] (planar)
-  float *sd = hs + 5 * kIn * kMid;        // [3][kMid][kMid] (planar, zero outside the image)
-  float *se = hs;                         // [3][kT][kMid] (reuses hs)
+__device__ __forceinline__ void block_sum2(double l1, double ss, double *dst0, double *dst1) {
   __shared__ double red[2][kLossThreads / 32];
-  const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
-  const int gx = x0 - 2 * kR, gy = y0 - 2 * kR;  // image coords of sa[0][0]
-  const int mx = x0 - kR, my = y0 - kR;          // image coords of the kMid region origin
-  const int t = threadIdx.x;
-  const bool border = x0 < kR || y0 < kR || x0 + kT > W - kR || y0 + kT > H - kR;
-  double l1 = 0.0, ss = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    for (int e = t; e < kIn * kIn; e += kLossThreads) {
-      const int r = e / kIn, q = e - r * kIn;
-      const size_t p = ((size_t)reflect_clamp(gy + r, H) * W + reflect_clamp(gx + q, W)) * 3 + c;
-      sa[e] = img[p];
-      sb[e] = tgt[p];
-    }
-    __syncthreads();
-    // ---- horizontal window sums: item = (row, 6 mid columns), sliding window in registers
-    for (int it = t; it < kIn * (kMid / kHSeg); it += kLossThreads) {
-      const int r = it / (kMid / kHSeg), q0 = (it - r * (kMid / kHSeg)) * kHSeg;
-      float av[kHSeg + 2 * kR], bv[kHSeg + 2 * kR];
-#pragma unroll
-      for (int j = 0; j < kHSeg + 2 * kR; ++j) {
-        av[j] = sa[r * kIn + q0 + j];
-        bv[j] = sb[r * kIn + q0 + j];
-      }
-#pragma unroll
-      for (int o = 0; o < kHSeg; ++o) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
-#pragma unroll
-        for (int j = 0; j < 2 * kR + 1; ++j) {
-          const float w = tp.w[j], x = av[o + j], y = bv[o + j];
-          const float wx = w * x, wy = w * y;
-          s0 += wx;
-          s1 += wy;
-          s2 = fmaf(wx, x, s2);
-          s3 = fmaf(wy, y, s3);
-          s4 = fmaf(wx, y, s4);
-        }
-        const int off = r * kMid + q0 + o;
-        hs[off] = s0;
-        hs[kIn * kMid + off] = s1;
-        hs[2 * kIn * kMid + off] = s2;
-        hs[3 * kIn * kMid + off] = s3;
-        hs[4 * kIn * kMid + off] = s4;
-      }
-    }
-    __syncthreads();
-    // ---- vertical window -> SSIM partials: item = (mid column, 6 mid rows)
-    for (int it = t; it < kMid * (kMid / kVSeg); it += kLossThreads) {
-      const int q = it % kMid, r0 = (it / kMid) * kVSeg;
-      float m[5][kVSeg];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        float col[kVSeg + 2 * kR];
-#pragma unroll
-        for (int j = 0; j < kVSeg + 2 * kR; ++j) col[j] = hs[k * kIn * kMid + (r0 + j) * kMid + q];
-#pragma unroll
-        for (int o = 0; o < kVSeg; ++o) {
-          float acc = 0.f;
-#pragma unroll
-          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
-          m[k][o] = acc;
-        }
-      }
-#pragma unroll
-      for (int o = 0; o < kVSeg; ++o) {
-        const int r = r0 + o;
-        const int yy = my + r, xx = mx + q;
-        const int off = r * kMid + q;
-        if (yy < 0 || yy >= H || xx < 0 || xx >= W) {
-          sd[off] = 0.f;
-          sd[kMid * kMid + off] = 0.f;
-          sd[2 * kMid * kMid + off] = 0.f;
-          continue;
-        }
-        const float m0 = m[0][o], m1 = m[1][o];
-        const float var_a = m[2][o] - m0 * m0, var_b = m[3][o] - m1 * m1, cov = m[4][o] - m0 * m1;
-        const float A1 = 2.0f * m0 * m1 + c1, A2 = 2.0f * cov + c2;
-        const float B1 = m0 * m0 + m1 * m1 + c1, B2 = var_a + var_b + c2;
-        const float den = B1 * B2;
-        const float smap = A1 * A2 / den;
-        sd[off] = 2.0f * m1 * (A2 - A1) / den - 2.0f * m0 * smap * (1.0f / B1 - 1.0f / B2);
-        sd[kMid * kMid + off] = -smap / B2;
-        sd[2 * kMid * kMid + off] = 2.0f * A1 / den;
-        if (r >= kR && r < kR + kT && q >= kR && q < kR + kT) {  // this tile's own pixels
-          ss += smap;
-          l1 += fabsf(sa[(r + kR) * kIn + q + kR] - sb[(r + kR) * kIn + q + kR]);
-        }
-      }
-    }
-    __syncthreads();
-    // ---- vertical adjoint: item = (mid column, row segment of 5-6); symmetric taps -> correlation
-    for (int it = t; it < kMid * kAVItems; it += kLossThreads) {
-      const int q = it % kMid, sgi = it / kMid;
-      const int r0 = sgi == 0 ? 0 : 1 + 5 * sgi;       // 0, 6, 11, 16, 21, 26
-      const int len = (sgi == 0 || sgi == kAVItems - 1) ? 6 : 5;
-      const int xx = mx + q;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float col[kAVSeg + 2 * kR];
-#pragma unroll
-        for (int j = 0; j < kAVSeg + 2 * kR; ++j) col[j] = (j < len + 2 * kR) ? sd[k * kMid * kMid + (r0 + j) * kMid + q] : 0.0f;
-#pragma unroll
-        for (int o = 0; o < kAVSeg; ++o) {
-          if (o >= len) break;
-          float acc = 0.f;
-#pragma unroll
-          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
-          const int yy = y0 + r0 + o;
-          if (border && (yy < kR || yy >= H - kR) && xx >= 0 && xx < W)
-            acc += adjoint_fold(yy, H, tp, [&](int j) { return sd[k * kMid * kMid + (j - my) * kMid + q]; });
-          se[k * kT * kMid + (r0 + o) * kMid + q] = (yy < H && xx >= 0 && xx < W) ? acc : 0.0f;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- horizontal adjoint: item = (tile row, 4 columns); combine with the L1 sign
-    for (int it = t; it < kT * (kT / kAHSeg); it += kLossThreads) {
-      const int r = it / (kT / kAHSeg), c0 = (it - r * (kT / kAHSeg)) * kAHSeg;
-      const int yy = y0 + r;
-      float g[3][kAHSeg];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float row[kAHSeg + 2 * kR];
-#pragma unroll
-        for (int j = 0; j < kAHSeg + 2 * kR; ++j) row[j] = se[k * kT * kMid + r * kMid + c0 + j];
-#pragma unroll
-        for (int o = 0; o < kAHSeg; ++o) {
-          float acc = 0.f;
-#pragma unroll
-          for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], row[o + i], acc);
-          const int xx = x0 + c0 + o;
-          if (border && (xx < kR || xx >= W - kR))
-            acc += adjoint_fold(xx, W, tp, [&](int j) { return se[k * kT * kMid + r * kMid + (j - mx)]; });
-          g[k][o] = acc;
-        }
-      }
-      if (yy >= H) continue;
-#pragma unroll
-      for (int o = 0; o < kAHSeg; ++o) {
-        const int xx = x0 + c0 + o;
-        if (xx >= W) continue;
-        const float av = sa[(r + 2 * kR) * kIn + c0 + o + 2 * kR], bv = sb[(r + 2 * kR) * kIn + c0 + o + 2 * kR];
-        const float grad = (g[0][o] + 2.0f * av * g[1][o] + bv * g[2][o]) * inv_count;
-        const float diff = av - bv;
-        const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
-        dimage[((size_t)yy * W + xx) * 3 + c] = (1.0f - lam) * sgn * inv_count - lam * 0.5f * grad;
-      }
-    }
-    __syncthreads();
-  }
-  // block reduction -> one double atomic pair per CTA
-  const int lane = t & 31, warp = t >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     l1 += __shfl_xor_sync(0xffffffffu, l1, o);
@@ -236,23 +82,219 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_fused(const float *__rest
     red[1][warp] = ss;
   }
   __syncthreads();
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     double a = 0.0, b = 0.0;
     for (int w = 0; w < kLossThreads / 32; ++w) {
       a += red[0][w];
       b += red[1][w];
     }
-    atomicAdd(sums, a);
-    atomicAdd(sums + 1, b);
+    *dst0 = a;
+    *dst1 = b;
   }
 }
 
-__global__ void k_loss_finalize(double *terms, double inv_count) {
-  terms[0] *= inv_count;  // mean |a - b|
-  terms[1] *= inv_count;  // mean SSIM over pixels and channels
+__global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
+  __shared__ float sa[kH * kH], sb[kH * kH];
+  __shared__ float hs[5][kH][kT];  // horizontal window sums on the tile columns, halo rows
+  const int c = blockIdx.z;
+  const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+  const int W = A.W, H = A.H;
+  const int t = threadIdx.x;
+  const Taps &tp = A.tp;
+  for (int e = t; e < kH * kH; e += kLossThreads) {
+    const int r = e / kH, q = e - r * kH;
+    const size_t p = ((size_t)reflect_clamp(y0 - kR + r, H) * W + reflect_clamp(x0 - kR + q, W)) * 3 + c;
+    sa[e] = __ldg(A.img + p);
+    sb[e] = __ldg(A.tgt + p);
+  }
+  __syncthreads();
+  // horizontal: item = (halo row, 4 tile columns)
+  for (int it = t; it < kH * (kT / kHOut); it += kLossThreads) {
+    const int r = it / (kT / kHOut), q0 = (it - r * (kT / kHOut)) * kHOut;
+    float av[kHOut + 2 * kR], bv[kHOut + 2 * kR];
+#pragma unroll
+    for (int j = 0; j < kHOut + 2 * kR; ++j) {
+      av[j] = sa[r * kH + q0 + j];
+      bv[j] = sb[r * kH + q0 + j];
+    }
+#pragma unroll
+    for (int o = 0; o < kHOut; ++o) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2 * kR + 1; ++j) {
+        const float w = tp.w[j], x = av[o + j], y = bv[o + j];
+        const float wx = w * x, wy = w * y;
+        s0 += wx;
+        s1 += wy;
+        s2 = fmaf(wx, x, s2);
+        s3 = fmaf(wy, y, s3);
+        s4 = fmaf(wx, y, s4);
+      }
+      hs[0][r][q0 + o] = s0;
+      hs[1][r][q0 + o] = s1;
+      hs[2][r][q0 + o] = s2;
+      hs[3][r][q0 + o] = s3;
+      hs[4][r][q0 + o] = s4;
+    }
+  }
+  __syncthreads();
+  // vertical: item = (tile column, 4 tile rows) -> SSIM, partials, sums
+  double l1 = 0.0, ss = 0.0;
+  {
+    const int q = t % kT, r0 = (t / kT) * kVOut;
+    float m[5][kVOut];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      float col[kVOut + 2 * kR];
+#pragma unroll
+      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = hs[k][r0 + j][q];
+#pragma unroll
+      for (int o = 0; o < kVOut; ++o) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
+        m[k][o] = acc;
+      }
+    }
+    const int xx = x0 + q;
+#pragma unroll
+    for (int o = 0; o < kVOut; ++o) {
+      const int yy = y0 + r0 + o;
+      if (yy >= H || xx >= W) continue;
+      const float m0 = m[0][o], m1 = m[1][o];
+      const float var_a = m[2][o] - m0 * m0, var_b = m[3][o] - m1 * m1, cov = m[4][o] - m0 * m1;
+      const float A1 = 2.0f * m0 * m1 + A.c1, A2 = 2.0f * cov + A.c2;
+      const float B1 = m0 * m0 + m1 * m1 + A.c1, B2 = var_a + var_b + A.c2;
+      const float den = B1 * B2;
+      const float smap = A1 * A2 / den;
+      const size_t plane = (size_t)H * W, p = (size_t)yy * W + xx;
+      float *pc = A.part + (size_t)c * 3 * plane;
+      pc[p] = 2.0f * m1 * (A2 - A1) / den - 2.0f * m0 * smap * (1.0f / B1 - 1.0f / B2);
+      pc[plane + p] = -smap / B2;
+      pc[2 * plane + p] = 2.0f * A1 / den;
+      ss += smap;
+      l1 += fabsf(sa[(r0 + o + kR) * kH + q + kR] - sb[(r0 + o + kR) * kH + q + kR]);
+    }
+  }
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  block_sum2(l1, ss, A.sums + bid, A.sums + nb + bid);
 }
 
-constexpr size_t kLossSmem = (size_t)(2 * kIn * kIn + 5 * kIn * kMid + 3 * kMid * kMid) * sizeof(float);
+__global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
+  __shared__ float sd[3][kH][kH];  // partials on the tile + halo, zero outside the image
+  __shared__ float se[3][kT][kH];  // vertical adjoint on the tile rows, halo columns
+  const int c = blockIdx.z;
+  const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+  const int mx = x0 - kR, my = y0 - kR;  // image coords of sd[.][0][0]
+  const int W = A.W, H = A.H;
+  const int t = threadIdx.x;
+  const Taps &tp = A.tp;
+  const bool border = x0 < kR || y0 < kR || x0 + kT > W - kR || y0 + kT > H - kR;
+  const size_t plane = (size_t)H * W;
+  const float *pc = A.part + (size_t)c * 3 * plane;
+  for (int e = t; e < kH * kH; e += kLossThreads) {
+    const int r = e / kH, q = e - r * kH;
+    const int yy = my + r, xx = mx + q;
+    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
+    const size_t p = in ? (size_t)yy * W + xx : 0;
+    sd[0][r][q] = in ? __ldg(pc + p) : 0.0f;
+    sd[1][r][q] = in ? __ldg(pc + plane + p) : 0.0f;
+    sd[2][r][q] = in ? __ldg(pc + 2 * plane + p) : 0.0f;
+  }
+  __syncthreads();
+  // vertical adjoint: item = (halo column, 4 tile rows), symmetric taps -> correlation
+  for (int it = t; it < kH * (kT / kVOut); it += kLossThreads) {
+    const int q = it % kH, r0 = (it / kH) * kVOut;
+    const int xx = mx + q;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float col[kVOut + 2 * kR];
+#pragma unroll
+      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = sd[k][r0 + j][q];
+#pragma unroll
+      for (int o = 0; o < kVOut; ++o) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
+        const int yy = y0 + r0 + o;
+        if (border && yy < H && (yy < kR || yy >= H - kR) && xx >= 0 && xx < W)
+          acc += adjoint_fold(yy, H, tp, [&](int j) { return sd[k][j - my][q]; });
+        se[k][r0 + o][q] = (yy < H && xx >= 0 && xx < W) ? acc : 0.0f;
+      }
+    }
+  }
+  __syncthreads();
+  // horizontal adjoint: item = (tile row, 4 tile columns); combine with the L1 sign
+  {
+    const int r = t / (kT / kHOut), c0 = (t - r * (kT / kHOut)) * kHOut;
+    const int yy = y0 + r;
+    float g[3][kHOut];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float row[kHOut + 2 * kR];
+#pragma unroll
+      for (int j = 0; j < kHOut + 2 * kR; ++j) row[j] = se[k][r][c0 + j];
+#pragma unroll
+      for (int o = 0; o < kHOut; ++o) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], row[o + i], acc);
+        const int xx = x0 + c0 + o;
+        if (border && xx < W && (xx < kR || xx >= W - kR))
+          acc += adjoint_fold(xx, W, tp, [&](int j) { return se[k][r][j - mx]; });
+        g[k][o] = acc;
+      }
+    }
+    if (yy < H) {
+#pragma unroll
+      for (int o = 0; o < kHOut; ++o) {
+        const int xx = x0 + c0 + o;
+        if (xx >= W) continue;
+        const size_t p = ((size_t)yy * W + xx) * 3 + c;
+        const float av = __ldg(A.img + p), bv = __ldg(A.tgt + p);
+        const float grad = (g[0][o] + 2.0f * av * g[1][o] + bv * g[2][o]) * A.inv_count;
+        const float diff = av - bv;
+        const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+        A.dimage[p] = (1.0f - A.lam) * sgn * A.inv_count - A.lam * 0.5f * grad;
+      }
+    }
+  }
+}
+
+// terms = {mean |a - b|, mean SSIM}: sum of the per-CTA partials (fixed order)
+__global__ void __launch_bounds__(1024) k_loss_finalize(const double *__restrict__ sums, int nb, double inv_count,
+                                                        double *__restrict__ terms) {
+  __shared__ double red[2][32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += sums[i];
+    b += sums[nb + i];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0.0;
+    b = 0.0;
+    for (int w = 0; w < 32; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    terms[0] = a * inv_count;
+    terms[1] = b * inv_count;
+  }
+}
+
+inline size_t loss_blocks(int W, int H) { return (size_t)ceil_div(W, kT) * ceil_div(H, kT) * 3; }
 
 }  // namespace tgs
 
@@ -260,37 +302,41 @@ using namespace tgs;
 
 extern "C" int tgs_loss_workspace(int32_t width, int32_t height, size_t *bytes) {
   if (width < 1 || height < 1 || !bytes) return TGS_ERR_INVALID;
-  *bytes = 0;  // the fused kernel keeps every intermediate in shared memory
+  // per-channel SSIM partials (3 x 3 planes) + per-CTA double sums
+  *bytes = align_up((size_t)9 * width * height * sizeof(float)) + 2 * loss_blocks(width, height) * sizeof(double);
   return TGS_OK;
 }
 
 extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t width, int32_t height,
                                 float lambda_ssim, float *dimage, double *terms, void *workspace,
                                 tgs_stream_t stream) {
-  (void)workspace;
   if (width < 2 * kR + 1 || height < 2 * kR + 1) return TGS_ERR_INVALID;  // metrics.py:83-84
-  if (!image || !target || !dimage || !terms) return TGS_ERR_INVALID;
+  if (!image || !target || !dimage || !terms || !workspace) return TGS_ERR_INVALID;
   cudaStream_t st = as_stream(stream);
-  static bool attr_done = false;  // idempotent function attribute, set once per process
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(k_loss_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLossSmem) !=
-        cudaSuccess)
-      return launch_status();
-    attr_done = true;
-  }
-  Taps tp;
+  LossArgs A;
   double w[2 * kR + 1], tot = 0.0;  // gaussian_taps (metrics.py:58-61), float64 then rounded
   for (int i = 0; i < 2 * kR + 1; ++i) {
     const double xx = (double)(i - kR) / 1.5;
     w[i] = exp(-0.5 * xx * xx);
     tot += w[i];
   }
-  for (int i = 0; i < 2 * kR + 1; ++i) tp.w[i] = (float)(w[i] / tot);
+  for (int i = 0; i < 2 * kR + 1; ++i) A.tp.w[i] = (float)(w[i] / tot);
   const size_t count = (size_t)width * height * 3;
-  cudaMemsetAsync(terms, 0, 2 * sizeof(double), st);
-  const dim3 grd((unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT));
-  k_loss_fused<<<grd, kLossThreads, kLossSmem, st>>>(image, target, width, height, tp, 0.01f * 0.01f, 0.03f * 0.03f,
-                                                     lambda_ssim, 1.0f / (float)count, dimage, terms);
-  k_loss_finalize<<<1, 1, 0, st>>>(terms, 1.0 / (double)count);
+  A.img = image;
+  A.tgt = target;
+  A.W = width;
+  A.H = height;
+  A.c1 = 0.01f * 0.01f;
+  A.c2 = 0.03f * 0.03f;
+  A.lam = lambda_ssim;
+  A.inv_count = 1.0f / (float)count;
+  A.part = static_cast<float *>(workspace);
+  A.sums = reinterpret_cast<double *>(static_cast<char *>(workspace) +
+                                      align_up((size_t)9 * width * height * sizeof(float)));
+  A.dimage = dimage;
+  const dim3 grd((unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT), 3);
+  k_ssim_fwd<<<grd, kLossThreads, 0, st>>>(A);
+  k_ssim_adj<<<grd, kLossThreads, 0, st>>>(A);
+  k_loss_finalize<<<1, 1024, 0, st>>>(A.sums, (int)loss_blocks(width, height), 1.0 / (double)count, terms);
   return launch_status();
 }
