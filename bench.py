@@ -318,9 +318,8 @@ def main():
     terms_host = torch.empty((VIEWS, 2), dtype=torch.float64).pin_memory()
 
     def e2e_step():
-        for v in views:
-            trainer.targets[v].copy_(host_targets[v], non_blocking=True)
-        trainer.step()
+        # targets stream in on the trainer's copy stream, overlapped with earlier views
+        trainer.step(host_targets=host_targets)
         terms_host.copy_(trainer.terms, non_blocking=True)
 
     e2e_step()

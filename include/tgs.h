@@ -228,6 +228,18 @@ TGS_API int tgs_loss_l1_ssim(const float *image, const float *target, int32_t wi
 TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, int64_t n, float lr,
                   float beta1, float beta2, float eps, float bias_c1, float bias_c2,
                   tgs_stream_t stream);
+/* All groups in one launch (optim.py:37-49 per group): groups are contiguous,
+ * 64-float aligned ranges [offsets[k], offsets[k] + sizes[k]) of the flat
+ * param/grad/moment buffers (16 B aligned), each with its own lr and bias
+ * corrections.  kinds[k] = 1 adds the Gaussian-mask penalty gradient
+ * lambda_m * sigmoid'(m) / n, kinds[k] = 2 the SH-band-mask penalty
+ * lambda_sh * sigmoid'(m_l) * band_weights[l] / n (masking.py:60-67), to that
+ * group's gradient before the update (written back to grad). */
+TGS_API int tgs_adam_step_groups(float *param, float *grad, float *m, float *v, int32_t ngroups,
+                                 const int64_t *offsets, const int64_t *sizes, const float *lrs,
+                                 const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
+                                 float beta2, float eps, float lambda_m, float lambda_sh,
+                                 const float *band_weights, int64_t n_gaussians, tgs_stream_t stream);
 
 /* ---- target-side progressive ops (images.py:58-102), (H, W, 3) float32.
  * area_resize: exact fractional box filter (downsampling only); workspace

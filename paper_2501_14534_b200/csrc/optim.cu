@@ -43,6 +43,56 @@ __global__ void k_adam(float *__restrict__ p, const float *__restrict__ g, float
   for (; i < n; i += stride) adam1(p[i], g[i], m[i], v[i], lr, b1, b2, eps, bc1, bc2);
 }
 
+// All parameter groups in one launch.  Groups are contiguous 64-float aligned
+// ranges of the flat buffers, so a float4 chunk never straddles two groups; the
+// padding between groups is skipped.  The mask penalties of total_loss
+// (masking.py:60-67: L_m = mean sigmoid(m), L_sh = mean sum_l w_l sigmoid(m_l))
+// are added to their groups' gradients in registers (and written back), i.e.
+// g += lambda * sigmoid'(logit) * weight / n before the update.
+struct AdamGroupArgs {
+  int64_t off[9];      // group starts (floats) and the end of the last group
+  int64_t size[8];
+  float lr[8], bc1[8], bc2[8];
+  int kind[8];         // 0: plain, 1: Gaussian-mask penalty, 2: SH-band-mask penalty
+  int ngroups;
+  float b1, b2, eps, lam_m, lam_sh, inv_n, wband[3];
+};
+
+__global__ void __launch_bounds__(256) k_adam_groups(float *__restrict__ p, float *__restrict__ g,
+                                                     float *__restrict__ m, float *__restrict__ v, AdamGroupArgs a) {
+  const int64_t n4 = a.off[a.ngroups] / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n4; c += stride) {
+    const int64_t e = 4 * c;
+    int k = 0;
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < a.ngroups && e >= a.off[q]) k = q;
+    const int64_t local = e - a.off[k];
+    if (local >= a.size[k]) continue;  // padding
+    float4 pp = reinterpret_cast<float4 *>(p)[c];
+    float4 gg = reinterpret_cast<const float4 *>(g)[c];
+    float4 mm = reinterpret_cast<float4 *>(m)[c];
+    float4 vv = reinterpret_cast<float4 *>(v)[c];
+    float *pq = &pp.x, *gq = &gg.x, *mq = &mm.x, *vq = &vv.x;
+    const int kind = a.kind[k];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (local + j >= a.size[k]) break;
+      if (kind) {
+        const float sg = 1.0f / (1.0f + expf(-pq[j]));
+        const float w = kind == 1 ? a.lam_m : a.lam_sh * a.wband[(local + j) % 3];
+        gq[j] += w * (sg * (1.0f - sg)) * a.inv_n;
+      }
+      adam1(pq[j], gq[j], mq[j], vq[j], a.lr[k], a.b1, a.b2, a.eps, a.bc1[k], a.bc2[k]);
+    }
+    reinterpret_cast<float4 *>(p)[c] = pp;
+    reinterpret_cast<float4 *>(m)[c] = mm;
+    reinterpret_cast<float4 *>(v)[c] = vv;
+    if (kind) reinterpret_cast<float4 *>(g)[c] = gg;
+  }
+}
+
 __global__ void k_gather_rows(const float *__restrict__ in, float *__restrict__ out,
                               const int64_t *__restrict__ keep, int64_t n_keep, int row) {
   const int64_t total = n_keep * row;
@@ -80,6 +130,45 @@ extern "C" int tgs_adam_step(float *param, const float *grad, float *m, float *v
   const int64_t work = vec ? n / 4 + 1 : n;
   const unsigned grid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(work, 256), 148 * 16);
   k_adam<<<grid, 256, 0, as_stream(stream)>>>(param, grad, m, v, n, lr, beta1, beta2, eps, bias_c1, bias_c2, vec);
+  return launch_status();
+}
+
+extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *v, int32_t ngroups,
+                                    const int64_t *offsets, const int64_t *sizes, const float *lrs,
+                                    const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
+                                    float beta2, float eps, float lambda_m, float lambda_sh,
+                                    const float *band_weights, int64_t n_gaussians, tgs_stream_t stream) {
+  if (ngroups < 1 || ngroups > 8 || !param || !grad || !m || !v || !offsets || !sizes || !lrs || !bias_c1 ||
+      !bias_c2 || !kinds || n_gaussians < 0)
+    return TGS_ERR_INVALID;
+  if (((reinterpret_cast<uintptr_t>(param) | reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(m) |
+        reinterpret_cast<uintptr_t>(v)) & 15) != 0)
+    return TGS_ERR_INVALID;
+  AdamGroupArgs a{};
+  a.ngroups = ngroups;
+  for (int k = 0; k < ngroups; ++k) {
+    if (offsets[k] % 64 != 0 || sizes[k] < 0 || (k > 0 && offsets[k] < offsets[k - 1] + sizes[k - 1]) ||
+        !(bias_c1[k] > 0.0f) || !(bias_c2[k] > 0.0f) || kinds[k] < 0 || kinds[k] > 2)
+      return TGS_ERR_INVALID;
+    a.off[k] = offsets[k];
+    a.size[k] = sizes[k];
+    a.lr[k] = lrs[k];
+    a.bc1[k] = bias_c1[k];
+    a.bc2[k] = bias_c2[k];
+    a.kind[k] = kinds[k];
+  }
+  a.off[ngroups] = (offsets[ngroups - 1] + sizes[ngroups - 1] + 63) / 64 * 64;
+  a.b1 = beta1;
+  a.b2 = beta2;
+  a.eps = eps;
+  a.lam_m = lambda_m;
+  a.lam_sh = lambda_sh;
+  a.inv_n = n_gaussians > 0 ? 1.0f / (float)n_gaussians : 0.0f;
+  for (int l = 0; l < 3; ++l) a.wband[l] = band_weights ? band_weights[l] : 0.0f;
+  const int64_t n4 = a.off[ngroups] / 4;
+  if (n4 == 0) return TGS_OK;
+  const unsigned grid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n4, 256), 148 * 8);
+  k_adam_groups<<<grid, 256, 0, as_stream(stream)>>>(param, grad, m, v, a);
   return launch_status();
 }
 

@@ -1,8 +1,11 @@
 """Adam over the flat parameter buffer (optim.py:37-73 of the reference).
 
-One `tgs_adam_step` launch per named group (the groups are contiguous ranges of
-GaussianCloud.flat), moments kept in two flat buffers with the same layout, so
-pruning compacts params and moments with the same gather (optim.py:51-55).
+The groups are contiguous ranges of GaussianCloud.flat; a full step updates all
+of them in ONE `tgs_adam_step_groups` launch (per-group lr and bias
+corrections, optional mask-penalty gradients added in registers), a partial
+step uses `tgs_adam_step` per group.  Moments are kept in two flat buffers with
+the same layout, so pruning compacts params and moments with the same gather
+(optim.py:51-55).
 """
 
 from __future__ import annotations
@@ -36,9 +39,39 @@ class Adam:
                   _lib.ptr(self.v[off:]), size, float(self.lrs[name]), self.beta1, self.beta2, self.eps,
                   1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t, _lib.stream_handle(cloud.device))
 
-    def step(self, cloud: GaussianCloud, grads, names=PARAM_FIELDS) -> None:
-        for f in names:
-            self.update(cloud, grads, f)
+    def step(self, cloud: GaussianCloud, grads, names=PARAM_FIELDS, lambda_m: float = 0.0,
+             lambda_sh: float = 0.0) -> None:
+        """Update `names`; with all groups, one fused launch.  lambda_m / lambda_sh add the
+        mask penalties of total_loss (masking.py:60-67) to the mask-logit gradients first."""
+        if tuple(names) != tuple(PARAM_FIELDS):
+            if lambda_m or lambda_sh:
+                raise ValueError("mask penalties need the fused all-group step")
+            for f in names:
+                self.update(cloud, grads, f)
+            return
+        import ctypes
+        from .loss import SH_BAND_WEIGHTS
+        k = len(PARAM_FIELDS)
+        offs, sizes, lrs, b1s, b2s, kinds = [], [], [], [], [], []
+        for f in PARAM_FIELDS:
+            off, size = cloud.field_range(f)
+            goff, _ = grads.field_range(f)
+            if goff != off:
+                raise ValueError("gradient and parameter layouts differ")
+            self.steps[f] += 1
+            t = self.steps[f]
+            offs.append(off)
+            sizes.append(size)
+            lrs.append(float(self.lrs[f]))
+            b1s.append(1.0 - self.beta1 ** t)
+            b2s.append(1.0 - self.beta2 ** t)
+            kinds.append(1 if (f == "mask_logits" and lambda_m) else (2 if (f == "sh_mask_logits" and lambda_sh) else 0))
+        arr = lambda ct, xs: (ct * k)(*xs)  # noqa: E731
+        _lib.call("tgs_adam_step_groups", _lib.ptr(cloud.flat), _lib.ptr(grads.flat), _lib.ptr(self.m),
+                  _lib.ptr(self.v), k, arr(ctypes.c_int64, offs), arr(ctypes.c_int64, sizes),
+                  arr(ctypes.c_float, lrs), arr(ctypes.c_float, b1s), arr(ctypes.c_float, b2s),
+                  arr(ctypes.c_int32, kinds), self.beta1, self.beta2, self.eps, float(lambda_m), float(lambda_sh),
+                  (ctypes.c_float * 3)(*SH_BAND_WEIGHTS), len(cloud), _lib.stream_handle(cloud.device))
 
 
 def exponential_lr(step: int, lr_init: float, lr_final: float, max_steps: int) -> float:

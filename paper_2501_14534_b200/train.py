@@ -5,9 +5,9 @@ for a BATCH of views, which is how BASELINE.json config 3 defines the step:
 
     for each view of this rank:  render_forward -> L1 + D-SSIM loss -> render_backward
                                  (gradients accumulated into one flat buffer)
-    mask-penalty gradients       (masking.py:60-67, training.py:310-311)
     NCCL all-reduce(sum) of the flat gradient buffer       (data parallel, N > 1)
-    Adam over the 8 parameter groups                        (training.py:314-331)
+    mask-penalty gradients + Adam over the 8 parameter groups, one fused launch
+                                 (masking.py:60-67, training.py:310-331)
 
 The batch gradient is the sum of per-view reference gradients (SURVEY.md
 §8(d): "define batch gradient = sum of per-view reference gradients"), so the
@@ -55,13 +55,27 @@ class Trainer:
         self.dsplats = {}
         # >= 2 streams pipeline consecutive views; 1 stream serialises them (per-kernel timing)
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
+        self.copy_stream = torch.cuda.Stream(device=cloud.device)
         self.launches_per_step = 0
 
-    def step(self) -> torch.Tensor:
-        """One optimisation step over this rank's views; returns the device loss terms."""
+    def step(self, host_targets=None) -> torch.Tensor:
+        """One optimisation step over this rank's views; returns the device loss terms.
+
+        host_targets: optional {view: pinned (H, W, 3) float32 CPU tensor}.  Each view's
+        target is copied on a dedicated copy stream and its loss waits only for that
+        copy, so the transfers of later views overlap the compute of earlier ones."""
         g = self.grads
         vis, parts = [], []
         main = torch.cuda.current_stream(self.cloud.device)
+        copied = {}
+        if host_targets is not None:
+            self.copy_stream.wait_stream(main)  # the previous step has finished reading the targets
+            with torch.cuda.stream(self.copy_stream):
+                for v in self.views:
+                    self.targets[v].copy_(host_targets[v], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy_stream)
+                    copied[v] = ev
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam
         for i, v in enumerate(self.views):
@@ -75,6 +89,8 @@ class Trainer:
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
                 if d is None:
                     d = self.dimage[(i % len(self.streams), cam.height, cam.width)] = torch.empty_like(out.image)
+                if v in copied:
+                    st.wait_event(copied[v])
                 with stage("loss"):
                     loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
                 ds = self.dsplats.get(v)
@@ -86,20 +102,17 @@ class Trainer:
                 parts.append(ds)
         for s_ in self.streams:
             main.wait_stream(s_)
+        if copied:
+            main.wait_stream(self.copy_stream)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
                                   accumulate=False)
-        if self.pg is None or self.rank == 0:
-            with stage("mask_loss"):
-                # mask penalties of total_loss (masking.py:60-67), once per optimisation
-                # step (rank 0 only, so the all-reduce does not multiply them)
-                _, _, dm, dsh = loss_mod.mask_terms(self.cloud.mask_logits, self.cloud.sh_mask_logits)
-                g.mask_logits.add_(dm, alpha=self.lambda_m)
-                g.sh_mask_logits.add_(dsh, alpha=self.lambda_sh)
         if self.pg is not None:
             import torch.distributed as dist
             with stage("allreduce"):
                 dist.all_reduce(g.flat, group=self.pg)
         with stage("adam"):
-            self.opt.step(self.cloud, g)
+            # the mask penalties of total_loss (masking.py:60-67) enter the reduced gradient
+            # inside the fused Adam launch (identically on every rank)
+            self.opt.step(self.cloud, g, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
         return self.terms

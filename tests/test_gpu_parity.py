@@ -460,3 +460,41 @@ def test_depth_sort_fallback_path_runs_only_on_bucket_overflow(tgs):
         assert np.array_equal(_np(out._tiles.offsets).astype(np.int64), off)
         assert np.array_equal(_np(out._tiles.indices).astype(np.int64), ids)
     assert ran == {"random": False, "plane": True}
+
+
+def test_fused_adam_all_groups_with_mask_penalties(tgs):
+    """tgs_adam_step_groups: every group in one launch + the mask penalties of total_loss
+    (masking.py:60-67) vs optim.py:37-49 per group in float64."""
+    from paper_2501_14534_b200 import optim
+    from paper_2501_14534_b200.loss import SH_BAND_WEIGHTS
+    rng = np.random.default_rng(1)
+    sc = golden_io.load("fd16")
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    n = len(cloud)
+    lrs = {f: 10 ** rng.uniform(-4, -1) for f in golden_io.FIELDS}
+    opt = optim.Adam(cloud, lrs, eps=1e-15)
+    lam_m, lam_sh = 0.05, 0.07
+    p = {f: _np(getattr(cloud, f)).astype(np.float64) for f in golden_io.FIELDS}
+    m = {f: np.zeros_like(p[f]) for f in golden_io.FIELDS}
+    v = {f: np.zeros_like(p[f]) for f in golden_io.FIELDS}
+    for step in range(1, 4):
+        g = tgs.CloudGrads.zeros(n)
+        grads = {}
+        for f in golden_io.FIELDS:
+            grads[f] = rng.standard_normal(p[f].shape).astype(np.float32)
+            getattr(g, f).copy_(torch.from_numpy(grads[f]))
+        opt.step(cloud, g, lambda_m=lam_m, lambda_sh=lam_sh)
+        for f in golden_io.FIELDS:
+            gr = grads[f].astype(np.float64)
+            s = 1.0 / (1.0 + np.exp(-p[f]))
+            if f == "mask_logits":
+                gr = gr + lam_m * s * (1 - s) / n
+            elif f == "sh_mask_logits":
+                gr = gr + lam_sh * s * (1 - s) * np.asarray(SH_BAND_WEIGHTS) / n
+            if f in ("mask_logits", "sh_mask_logits"):
+                np.testing.assert_allclose(_np(getattr(g, f)), gr, rtol=1e-5, atol=1e-7, err_msg=f)
+            m[f] = 0.9 * m[f] + 0.1 * gr
+            v[f] = 0.999 * v[f] + 0.001 * gr * gr
+            p[f] = p[f] - lrs[f] * (m[f] / (1 - 0.9 ** step)) / (np.sqrt(v[f] / (1 - 0.999 ** step)) + 1e-15)
+    for f in golden_io.FIELDS:
+        np.testing.assert_allclose(_np(getattr(cloud, f)), p[f], rtol=2e-5, atol=2e-6, err_msg=f)
