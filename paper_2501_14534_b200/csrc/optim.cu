@@ -52,7 +52,7 @@ __global__ void k_adam(float *__restrict__ p, const float *__restrict__ g, float
 struct AdamGroupArgs {
   int64_t off[9];      // group starts (floats) and the end of the last group
   int64_t size[8];
-  float lr[8], bc1[8], bc2[8];
+  float lr_bc1[8], inv_bc2[8];
   int kind[8];         // 0: plain, 1: Gaussian-mask penalty, 2: SH-band-mask penalty
   int ngroups;
   float b1, b2, eps, lam_m, lam_sh, inv_n, wband[3];
@@ -84,7 +84,11 @@ __global__ void __launch_bounds__(256) k_adam_groups(float *__restrict__ p, floa
         const float w = kind == 1 ? a.lam_m : a.lam_sh * a.wband[(local + j) % 3];
         gq[j] += w * (sg * (1.0f - sg)) * a.inv_n;
       }
-      adam1(pq[j], gq[j], mq[j], vq[j], a.lr[k], a.b1, a.b2, a.eps, a.bc1[k], a.bc2[k]);
+      // optim.py:41-49 with lr / bc1 and 1 / bc2 folded on the host side of the launch
+      const float gj = gq[j];
+      mq[j] = a.b1 * mq[j] + (1.0f - a.b1) * gj;
+      vq[j] = a.b2 * vq[j] + (1.0f - a.b2) * gj * gj;
+      pq[j] -= __fdividef(a.lr_bc1[k] * mq[j], sqrtf(vq[j] * a.inv_bc2[k]) + a.eps);
     }
     reinterpret_cast<float4 *>(p)[c] = pp;
     reinterpret_cast<float4 *>(m)[c] = mm;
@@ -152,9 +156,8 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
       return TGS_ERR_INVALID;
     a.off[k] = offsets[k];
     a.size[k] = sizes[k];
-    a.lr[k] = lrs[k];
-    a.bc1[k] = bias_c1[k];
-    a.bc2[k] = bias_c2[k];
+    a.lr_bc1[k] = lrs[k] / bias_c1[k];
+    a.inv_bc2[k] = 1.0f / bias_c2[k];
     a.kind[k] = kinds[k];
   }
   a.off[ngroups] = (offsets[ngroups - 1] + sizes[ngroups - 1] + 63) / 64 * 64;
