@@ -124,31 +124,48 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def stage_bytes(n, vis_n, inst, pixels, views):
-    """Algorithmic bytes per stage instance (one libtgs entry point).
+def stage_bytes(n, vis_n, inst, entries, pixels, views):
+    """Algorithmic bytes per stage launch as designed.
 
-    n Gaussians, inst instances and pixels are per view."""
+    n Gaussians, vis_n selected (on-screen) Gaussians, inst instances, entries
+    (Gaussian, 8x8-tile super-tile) pairs and pixels are per view."""
     return {
         # read 252 B of parameters, write 48 B record + 1 visible + 4 tiles + 8 depth key
         "preprocess_fwd": n * (252 + 48 + 1 + 4 + 8),
-        # select (16 B record fields + 4 tiles + 8 written) + compaction (24 B) + 8 stable passes moving
-        # (u64 key, u32 id) in and out (24 B) + counts gather/scan (16 B), per on-screen Gaussian
-        "bin_gaussians": n * 28 + vis_n * (24 + 8 * 24 + 16),
-        # per on-screen Gaussian: rect fields for the tile-count grid + ids/offsets for the
-        # duplicate (24 B); per instance: duplicate writes (key, id) 8 B, pass 1 moves (key, id)
-        # 16 B, the last pass reads (key, id) and writes the id 12 B
-        "bin_instances": vis_n * 24 + inst * (8 + 16 + 12),
+        # value-bucket depth sort: select (tiles 4 + mean/radius 20 + rect 8 written) + key 8, bucket
+        # count (rect 4, key 8), scatter (rect 4, key 8 in; key + id 12 out), in-bucket rank
+        # (key + id 12 in, id 4 + rect 8 gathered + rect 8 out); the 2^17-bucket scan
+        "bin_gaussians": n * (32 + 4 + 4) + vis_n * (8 + 8 + 8 + 12 + 12 + 20) + (1 << 17) * 12,
+        # rects read by the chunk counts and the level-1 scatter (2 x 8 B per Gaussian); per entry:
+        # level-1 write 4, level-2 count (entry 4 + rect 8), level-2 write (entry 4 + rect 8 + id 4);
+        # per instance the final id written
+        "bin_instances": vis_n * 16 + entries * (4 + 12 + 16) + inst * 4,
         # per instance: 4 B id + 48 B record staged; per pixel 28 B out (rgb, T, w, n, last)
         "blend_fwd": inst * 52 + pixels * 28,
         # per instance 52 B; per pixel 20 B in (dimage, T, last); 36 B partials RMW per Gaussian
         "blend_bwd": inst * 52 + pixels * 20 + vis_n * 72,
-        # read params 252 + partials 36 + visible 1, write grads 260 (RMW when accumulating: +260)
-        "preprocess_bwd": n * (252 + 36 + 1 + 2 * 260),
-        # read image + target 24 B, write dimage 12 B per pixel
-        "loss": pixels * 36,
-        # 63 floats x (read p, g, m, v; write p, m, v) once per step (one stage = 8 group launches)
+        # one launch per step: parameters 252 B, per view partials 36 B + visible 1 B, gradients 260 B
+        "preprocess_bwd": n * (252 + views * 37 + 260),
+        # image + target 24 B in, dimage 12 B out, SSIM partials 36 B written and read back per pixel
+        "loss": pixels * (36 + 72),
+        # 63 floats x (read p, g, m, v; write p, m, v), one fused launch per step
         "adam": n * 63 * 28,
     }
+
+
+# per-stage limiter measured with ncu (profiles/r01_ncu_blend_loss.txt): the dominant stage
+# (blend backward) is bound by instruction issue, not by HBM
+LIMITER = {"blend_bwd": "FP32/ALU instruction issue (ncu: issue slots busy 72%, barrier-free warps)",
+           "blend_fwd": "FP32/ALU instruction issue (ncu: issue slots busy 73%)"}
+
+
+def ncu_traffic(stage):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu --set full capture."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        return t.get(stage, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
 
 
 def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: str) -> tuple[dict, dict]:
@@ -164,8 +181,26 @@ def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: 
                      "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
     dom = max((k for k in stages if "achieved_gbs" in stages[k]), key=lambda k: stages[k]["ms_total"])
     d = stages[dom]
-    return {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": peak, "unit": "GB/s",
-            "frac": d["frac"], "traffic": None, "peak_source": peak_kind}, stages
+    rf = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": peak, "unit": "GB/s",
+          "frac": d["frac"], "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+          "algorithmic_bytes": sbytes[dom]}
+    if dom in LIMITER:
+        rf["limiter"] = LIMITER[dom]
+    return rf, stages
+
+
+def super_tile_entries(splats, tiles_touched, width, height, ts=16, st=8):
+    """(Gaussian, 8x8-tile super-tile) pairs of a view: the rect of bin_tiles
+    (rasterizer.py:112-128) in super-tile units, summed over on-screen Gaussians."""
+    import torch
+    on = tiles_touched > 0
+    m, r = splats[on, 0:2], splats[on, 10:11]
+    tx, ty = (width + ts - 1) // ts, (height + ts - 1) // ts
+    lo = torch.floor((m - r) / ts).clamp(min=0)
+    hi = torch.floor((m + r) / ts)
+    hi = torch.stack([hi[:, 0].clamp(max=tx - 1), hi[:, 1].clamp(max=ty - 1)], 1)
+    span = (torch.div(hi, st, rounding_mode="floor") - torch.div(lo, st, rounding_mode="floor") + 1).clamp(min=0)
+    return int((span[:, 0] * span[:, 1]).sum())
 
 
 # ------------------------------------------------------- CPU reference
@@ -338,15 +373,16 @@ def main():
         t_serial = timed(args.steps, serial.step)
     reset(serial)
     from paper_2501_14534_b200.rasterizer import render_forward
-    inst = []
-    vis_n = 0
+    inst, ents, vis = [], [], []
     for v in views:
         out = render_forward(cloud, sc.cameras[v], st)
         inst.append(int(out._tiles.indices.numel()))
-        vis_n = int((out._state.tiles_touched[: len(cloud)] > 0).sum())
-    inst_mean = sum(inst) / len(inst)
+        tt = out._state.tiles_touched[: len(cloud)]
+        vis.append(int((tt > 0).sum()))
+        ents.append(super_tile_entries(out._state.splats[: len(cloud)], tt, w, h))
+    inst_mean, ent_mean, vis_n = (sum(x) / len(x) for x in (inst, ents, vis))
     pk, pk_kind = peaks()
-    sb = stage_bytes(len(cloud), vis_n, inst_mean, h * w, VIEWS)
+    sb = stage_bytes(len(cloud), vis_n, inst_mean, ent_mean, h * w, VIEWS)
     rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
     launches = trainer_launches(prof.counts(), args.steps)
 
@@ -365,7 +401,8 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
             "ms_per_step_serial_views": round(t_serial / args.steps * 1e3, 3),
-            "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean)}
+            "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean),
+            "entries_per_view": int(ent_mean), "selected_per_view": int(vis_n)}
     if world == 1 and not args.no_cpu_baseline:
         from types import SimpleNamespace
         line["cpu_baseline"] = cpu_baseline(sc, SimpleNamespace(record_hits=False, **settings_kwargs()))

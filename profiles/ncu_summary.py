@@ -1,0 +1,84 @@
+"""Summarise ncu --set full reports into profiles/r01_ncu_summary.txt and the per-stage
+DRAM traffic JSON that bench.py reports as roofline.traffic.
+
+    python profiles/ncu_summary.py <view.ncu-rep> <step.ncu-rep>
+
+Runs here (no GPU): `ncu -i <rep> --page raw --csv`.
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import defaultdict
+
+STAGE_OF = [  # kernel-name prefix -> bench stage
+    ("k_preprocess_fwd", "preprocess_fwd"), ("k_bs_", "bin_gaussians"), ("k_depth_sort", "bin_gaussians"),
+    ("k_seg_", "bin_instances"), ("k_scatter", "bin_instances"), ("k_unit_table", "bin_instances"),
+    ("k_place_", "bin_instances"), ("k_tile_scan", "bin_instances"), ("k_blend_fwd", "blend_fwd"),
+    ("k_ssim_", "loss"), ("k_loss_finalize", "loss"), ("k_blend_bwd", "blend_bwd"),
+    ("k_preprocess_bwd", "preprocess_bwd"), ("k_adam", "adam"),
+]
+UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # -> microseconds
+        "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+METRICS = {
+    "time_us": ("gpu__time_duration.sum", 1.0),
+    "dram_read": ("dram__bytes_read.sum", 1.0),
+    "dram_write": ("dram__bytes_write.sum", 1.0),
+    "issue_busy_pct": ("sm__inst_issued.avg.pct_of_peak_sustained_active", 1.0),
+    "occupancy_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
+    "regs": ("launch__registers_per_thread", 1.0),
+    "fma_pipe_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+    "warp_insts": ("smsp__inst_executed.sum", 1.0),
+}
+
+
+def rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    hdr, units = r[0], dict(zip(r[0], r[1]))
+    for x in r[2:]:
+        d = dict(zip(hdr, x))
+        rec = {"kernel": d["Kernel Name"].split("(")[0].replace("void ", "").replace("tgs::", "")}
+        for k, (m, scale) in METRICS.items():
+            try:
+                rec[k] = float(d[m].replace(",", "")) * scale * UNIT.get(units.get(m, ""), 1.0)
+            except (KeyError, ValueError):
+                rec[k] = None
+        yield rec
+
+
+def stage(name):
+    short = name.split("<")[0]
+    for pre, st in STAGE_OF:
+        if short.startswith(pre):
+            return st
+    return None
+
+
+def main(reps):
+    recs = [r for rep in reps for r in rows(rep)]
+    lines = ["ncu --set full --clock-control none (one c3 view via profile_step.py; the per-step kernels via",
+             "profile_train.py, 8 views).  Cold-cache, serialised replays: compare shares, not absolute times.", "",
+             f"{'kernel':34s} {'us':>8s} {'DRAM MB':>9s} {'TB/s':>6s} {'issue%':>7s} {'occ%':>6s} {'fma%':>6s} {'regs':>5s}"]
+    per_stage = defaultdict(lambda: {"dram_bytes_per_launch": 0.0, "time_us": 0.0, "kernels": []})
+    for r in recs:
+        mb = ((r["dram_read"] or 0) + (r["dram_write"] or 0)) / 1e6
+        tbs = mb / 1e6 / (r["time_us"] * 1e-6) if r["time_us"] else 0
+        lines.append(f"{r['kernel'][:34]:34s} {r['time_us']:8.1f} {mb:9.2f} {tbs:6.2f} "
+                     f"{r['issue_busy_pct'] or 0:7.1f} {r['occupancy_pct'] or 0:6.1f} {r['fma_pipe_pct'] or 0:6.1f} "
+                     f"{int(r['regs'] or 0):5d}")
+        st = stage(r["kernel"])
+        if st:
+            per_stage[st]["dram_bytes_per_launch"] += mb * 1e6
+            per_stage[st]["time_us"] += r["time_us"]
+            per_stage[st]["kernels"].append(r["kernel"])
+    json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"]), "time_us": round(v["time_us"], 1),
+                   "kernels": v["kernels"]} for k, v in per_stage.items()},
+              open("profiles/r01_ncu_traffic.json", "w"), indent=1)
+    open("profiles/r01_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
