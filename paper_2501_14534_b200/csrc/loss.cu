@@ -93,11 +93,14 @@ __device__ __forceinline__ void block_sum2(double l1, double ss, double *dst0, d
   }
 }
 
+// Grid (3 channels, tiles_x, tiles_y): the channel is the fastest-varying block
+// index, so the three CTAs of a tile run together and share the interleaved
+// image lines (and halos) in L2.
 __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   __shared__ float sa[kH * kH], sb[kH * kH];
   __shared__ float hs[5][kH][kT];  // horizontal window sums on the tile columns, halo rows
-  const int c = blockIdx.z;
-  const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+  const int c = blockIdx.x;
+  const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int W = A.W, H = A.H;
   const int t = threadIdx.x;
   const Taps &tp = A.tp;
@@ -111,24 +114,26 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   // horizontal: item = (halo row, 4 tile columns)
   for (int it = t; it < kH * (kT / kHOut); it += kLossThreads) {
     const int r = it / (kT / kHOut), q0 = (it - r * (kT / kHOut)) * kHOut;
-    float av[kHOut + 2 * kR], bv[kHOut + 2 * kR];
+    float av[kHOut + 2 * kR], bv[kHOut + 2 * kR], aa[kHOut + 2 * kR], bb[kHOut + 2 * kR], ab[kHOut + 2 * kR];
 #pragma unroll
-    for (int j = 0; j < kHOut + 2 * kR; ++j) {
+    for (int j = 0; j < kHOut + 2 * kR; ++j) {  // products once per input, not once per tap
       av[j] = sa[r * kH + q0 + j];
       bv[j] = sb[r * kH + q0 + j];
+      aa[j] = av[j] * av[j];
+      bb[j] = bv[j] * bv[j];
+      ab[j] = av[j] * bv[j];
     }
 #pragma unroll
     for (int o = 0; o < kHOut; ++o) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
 #pragma unroll
       for (int j = 0; j < 2 * kR + 1; ++j) {
-        const float w = tp.w[j], x = av[o + j], y = bv[o + j];
-        const float wx = w * x, wy = w * y;
-        s0 += wx;
-        s1 += wy;
-        s2 = fmaf(wx, x, s2);
-        s3 = fmaf(wy, y, s3);
-        s4 = fmaf(wx, y, s4);
+        const float w = tp.w[j];
+        s0 = fmaf(w, av[o + j], s0);
+        s1 = fmaf(w, bv[o + j], s1);
+        s2 = fmaf(w, aa[o + j], s2);
+        s3 = fmaf(w, bb[o + j], s3);
+        s4 = fmaf(w, ab[o + j], s4);
       }
       hs[0][r][q0 + o] = s0;
       hs[1][r][q0 + o] = s1;
@@ -177,15 +182,15 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
     }
   }
   const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-  const unsigned bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const unsigned bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;  // any fixed order
   block_sum2(l1, ss, A.sums + bid, A.sums + nb + bid);
 }
 
 __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
   __shared__ float sd[3][kH][kH];  // partials on the tile + halo, zero outside the image
   __shared__ float se[3][kT][kH];  // vertical adjoint on the tile rows, halo columns
-  const int c = blockIdx.z;
-  const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+  const int c = blockIdx.x;
+  const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int mx = x0 - kR, my = y0 - kR;  // image coords of sd[.][0][0]
   const int W = A.W, H = A.H;
   const int t = threadIdx.x;
@@ -334,7 +339,7 @@ extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t
   A.sums = reinterpret_cast<double *>(static_cast<char *>(workspace) +
                                       align_up((size_t)9 * width * height * sizeof(float)));
   A.dimage = dimage;
-  const dim3 grd((unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT), 3);
+  const dim3 grd(3, (unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT));
   k_ssim_fwd<<<grd, kLossThreads, 0, st>>>(A);
   k_ssim_adj<<<grd, kLossThreads, 0, st>>>(A);
   k_loss_finalize<<<1, 1024, 0, st>>>(A.sums, (int)loss_blocks(width, height), 1.0 / (double)count, terms);
