@@ -890,24 +890,21 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_scatter(const uint2 *__res
                                                               const uint32_t *__restrict__ soff,
                                                               uint32_t *__restrict__ entries) {
   extern __shared__ unsigned long long mk[];
-  __shared__ uint32_t s_pre[kChunk];    // exclusive entry prefix over the chunk's Gaussians
-  __shared__ uint32_t s_rect[kChunk];   // x0 | y0 << 16 (super-tiles)
-  __shared__ uint32_t s_nx[kChunk];
-  __shared__ uint32_t ws[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t m = *d_m;
   const uint32_t live = ceil_div<uint32_t>(m, (uint32_t)kChunk);
   const uint32_t NS = (uint32_t)(sx * sy);
   const uint32_t c = blockIdx.x;
   if (c >= live) return;
-  const int mw = sx + sy + 2;           // column masks [0, sx], row masks after
-  for (int e = threadIdx.x; e < kChunkWarps * mw; e += blockDim.x) mk[e] = 0ull;
+  const int mw = sx + sy;               // column masks [0, sx), row masks after
   const uint32_t j0 = c * kChunk;
+  // lane l of warp w holds Gaussians 64w + l and 64w + 32 + l, so the group's
+  // 64-bit coverage mask of a column / row is ballot(h = 0) | ballot(h = 1) << 32
   uint32_t cnt[2];
   int x0[2], y0[2], x1[2], y1[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const uint32_t k = threadIdx.x * 2 + h;
+    const uint32_t k = warp * 64 + h * 32 + lane;
     const uint32_t j = j0 + k;
     cnt[h] = 0;
     x0[h] = 0; y0[h] = 0; x1[h] = -1; y1[h] = -1;
@@ -916,73 +913,43 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_scatter(const uint2 *__res
       x0[h] >>= kSTShift; x1[h] >>= kSTShift; y0[h] >>= kSTShift; y1[h] >>= kSTShift;
       cnt[h] = (uint32_t)((x1[h] - x0[h] + 1) * (y1[h] - y0[h] + 1));
     }
-    s_rect[k] = (uint32_t)x0[h] | ((uint32_t)y0[h] << 16);
-    s_nx[k] = (uint32_t)(x1[h] - x0[h] + 1);
   }
-  const uint32_t ex = block_exclusive_scan(cnt[0] + cnt[1], ws, nullptr);  // also a barrier (mk zeroed)
-  s_pre[threadIdx.x * 2] = ex;
-  s_pre[threadIdx.x * 2 + 1] = ex + cnt[0];
+  {
+    unsigned long long *cm = mk + warp * mw;
+    unsigned long long *rm = cm + sx;
+    for (int x = 0; x < sx; ++x) {
+      const uint32_t lo = __ballot_sync(0xffffffffu, x0[0] <= x && x <= x1[0]);
+      const uint32_t hi = __ballot_sync(0xffffffffu, x0[1] <= x && x <= x1[1]);
+      if (lane == (x & 31)) cm[x] = (unsigned long long)lo | ((unsigned long long)hi << 32);
+    }
+    for (int y = 0; y < sy; ++y) {
+      const uint32_t lo = __ballot_sync(0xffffffffu, y0[0] <= y && y <= y1[0]);
+      const uint32_t hi = __ballot_sync(0xffffffffu, y0[1] <= y && y <= y1[1]);
+      if (lane == (y & 31)) rm[y] = (unsigned long long)lo | ((unsigned long long)hi << 32);
+    }
+  }
+  __syncthreads();  // every group's masks are complete
+  const uint16_t *crel = rel + (size_t)c * NS;
+  const uint32_t *sb = segbase + (size_t)(c / kSeg) * NS;
+  // each thread enumerates its own two Gaussians' entries (a handful each)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (cnt[h] == 0) continue;
-    const uint32_t k = threadIdx.x * 2 + h;
-    unsigned long long *cm = mk + (k >> 6) * mw;
-    unsigned long long *rm = cm + sx + 1;
-    const unsigned long long bit = 1ull << (k & 63);
-    atomicXor(&cm[x0[h]], bit);
-    atomicXor(&cm[x1[h] + 1], bit);
-    atomicXor(&rm[y0[h]], bit);
-    atomicXor(&rm[y1[h] + 1], bit);
-  }
-  __syncthreads();
-  {  // XOR prefix over warp w's own group arrays
-    unsigned long long *cm = mk + warp * mw;
-    unsigned long long *rm = cm + sx + 1;
-    const int cper = (sx + 31) / 32, rper = (sy + 31) / 32;
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-      unsigned long long *arr = pass ? rm : cm;
-      const int len = pass ? sy : sx, per = pass ? rper : cper;
-      const int a0 = lane * per, a1 = min(a0 + per, len);
-      unsigned long long acc = 0;
-      for (int x = a0; x < a1; ++x) acc ^= arr[x];
-      unsigned long long pre = acc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre ^= y;
+    const int k = warp * 64 + h * 32 + lane;
+    const int g = warp;
+    const unsigned long long below = (1ull << (k & 63)) - 1ull;
+    for (int ty = y0[h]; ty <= y1[h]; ++ty)
+      for (int tx = x0[h]; tx <= x1[h]; ++tx) {
+        const uint32_t t = (uint32_t)ty * sx + (uint32_t)tx;
+        const unsigned long long *cg = mk + g * mw;
+        uint32_t pos = __ldg(soff + t) + __ldg(sb + t) + (uint32_t)__ldg(crel + t) +
+                       (uint32_t)__popcll(cg[tx] & cg[sx + ty] & below);
+        for (int w = 0; w < g; ++w) {
+          const unsigned long long *cw = mk + w * mw;
+          pos += (uint32_t)__popcll(cw[tx] & cw[sx + ty]);
+        }
+        entries[pos] = j0 + (uint32_t)k;
       }
-      unsigned long long r = pre ^ acc;  // exclusive
-      for (int x = a0; x < a1; ++x) {
-        r ^= arr[x];
-        arr[x] = r;
-      }
-    }
-  }
-  __syncthreads();
-  const uint32_t e_begin = 0, e_end = __ldg(chunk_ent + c);
-  const uint16_t *crel = rel + (size_t)c * NS;
-  const uint32_t *sb = segbase + (size_t)(c / kSeg) * NS;
-  for (uint32_t e = e_begin + threadIdx.x; e < e_end; e += blockDim.x) {
-    int k = 0;  // owner: last Gaussian whose exclusive prefix is <= e
-#pragma unroll
-    for (int step = kChunk / 2; step >= 1; step >>= 1)
-      if (s_pre[k + step] <= e) k += step;
-    const int local = (int)(e - s_pre[k]);
-    const uint32_t rc = s_rect[k];
-    const int knx = (int)s_nx[k];
-    const int row = local / knx;
-    const int tx = (int)(rc & 0xffffu) + local - row * knx, ty = (int)(rc >> 16) + row;
-    const uint32_t t = (uint32_t)ty * sx + (uint32_t)tx;
-    const int g = k >> 6;
-    const unsigned long long *cg = mk + g * mw;
-    uint32_t pos = __ldg(soff + t) + __ldg(sb + t) + (uint32_t)__ldg(crel + t) +
-                   (uint32_t)__popcll(cg[tx] & cg[sx + 1 + ty] & ((1ull << (k & 63)) - 1ull));
-    for (int w = 0; w < g; ++w) {
-      const unsigned long long *cw = mk + w * mw;
-      pos += (uint32_t)__popcll(cw[tx] & cw[sx + 1 + ty]);
-    }
-    entries[pos] = j0 + (uint32_t)k;
   }
 }
 
@@ -1091,10 +1058,17 @@ __global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ 
     const int ty = (int)(t / tiles_x), tx = (int)(t % tiles_x);
     const uint32_t S = (uint32_t)((ty >> kSTShift) * sx + (tx >> kSTShift));
     const uint32_t q = (uint32_t)(((ty & (kST - 1)) << kSTShift) | (tx & (kST - 1)));
-    for (uint32_t u = __ldg(ubase + S); u < __ldg(ubase + S + 1); ++u) {
-      const uint32_t v = ucnt[(size_t)u * 64 + q];
-      ucnt[(size_t)u * 64 + q] = run;
-      run += v;
+    const uint32_t u1 = __ldg(ubase + S + 1);
+    for (uint32_t u = __ldg(ubase + S); u < u1; u += 8) {  // independent loads first
+      uint32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = u + k < u1 ? ucnt[(size_t)(u + k) * 64 + q] : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (u + k < u1) {
+          ucnt[(size_t)(u + k) * 64 + q] = run;
+          run += v[k];
+        }
     }
   }
   uint32_t tot;
@@ -1378,7 +1352,7 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
     return launch_status();
   }
   if (!workspace || !sorted_ids) return TGS_ERR_INVALID;
-  const size_t sc_smem = (size_t)kChunkWarps * (g.sx + g.sy + 2) * 8;
+  const size_t sc_smem = (size_t)kChunkWarps * (g.sx + g.sy) * 8;
   const size_t cnt_smem = ((size_t)(g.sx + 1) * (g.slab_rows + 1) + (size_t)g.slab_rows * g.sx) * 4;
   if (sc_smem > 160 * 1024) return TGS_ERR_UNSUPPORTED;
   GaussWS gw = carve_gauss(gauss_workspace, n);
