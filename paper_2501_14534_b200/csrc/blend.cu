@@ -528,8 +528,11 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
   B.done = !inB;
   SplatRegs nx;
   fetch_splat(nx, splats, ids, start + lane, start + lane < stop);
+  float4 wbc = wb;
   for (int c = start; c < stop; c += 32) {
     if (__all_sync(0xffffffffu, A.done && B.done)) break;
+    // cull against the pixels that are still blending (terminated ones no longer count)
+    if (c != start) wbc = warp_bounds2(!A.done, !B.done, px, pyA, pyB);
     const bool ok = c + lane < stop;
     bool keep = false;
     if (ok) {
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
       S.q[lane] = q;
       S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
       S.id[lane] = nx.g;
-      keep = !quad_misses(m, q, thr, wb);
+      keep = !quad_misses(m, q, thr, wbc);
     }
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
@@ -617,6 +620,8 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     const int lo = hi - 32;  // may be negative: lanes below position 0 are idle
     const bool ok = lo + lane >= 0;
     bool keep = false;
+    // only pixels whose last blended position lies beyond lo can take part in this chunk
+    const float4 wbc = warp_bounds2(A.lastp > lo, B.lastp > lo, px, pyA, pyB);
     if (ok) {
       const float4 q = prescaled_conic(nx.a, nx.b);
       const float thr = splat_thr2(nx.b.y);
@@ -626,7 +631,7 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
       S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
       S.id[lane] = nx.g;
-      keep = !quad_misses(m, q, thr, wb);
+      keep = !quad_misses(m, q, thr, wbc);
     }
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
