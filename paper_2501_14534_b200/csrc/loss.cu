@@ -104,11 +104,29 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   const int W = A.W, H = A.H;
   const int t = threadIdx.x;
   const Taps &tp = A.tp;
-  for (int e = t; e < kH * kH; e += kLossThreads) {
-    const int r = e / kH, q = e - r * kH;
-    const size_t p = ((size_t)reflect_clamp(y0 - kR + r, H) * W + reflect_clamp(x0 - kR + q, W)) * 3 + c;
-    sa[e] = __ldg(A.img + p);
-    sb[e] = __ldg(A.tgt + p);
+  __shared__ uint32_t roff[kH], coff[kH];  // reflected row offsets / column offsets (floats)
+  if (t < kH) roff[t] = (uint32_t)reflect_clamp(y0 - kR + t, H) * (uint32_t)W * 3u;
+  else if (t < 2 * kH) coff[t - kH] = (uint32_t)reflect_clamp(x0 - kR + t - kH, W) * 3u + (uint32_t)c;
+  __syncthreads();
+  {  // every load of the thread first, then the shared-memory stores
+    constexpr int kIt = (kH * kH + kLossThreads - 1) / kLossThreads;
+    float va[kIt], vb[kIt];
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int e = t + i * kLossThreads;
+      const int r = e / kH, q = e - r * kH;
+      const uint32_t p = e < kH * kH ? roff[r] + coff[q] : 0u;
+      va[i] = __ldg(A.img + p);
+      vb[i] = __ldg(A.tgt + p);
+    }
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int e = t + i * kLossThreads;
+      if (e < kH * kH) {
+        sa[e] = va[i];
+        sb[e] = vb[i];
+      }
+    }
   }
   __syncthreads();
   // horizontal: item = (halo row, 4 tile columns)
@@ -198,14 +216,30 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
   const bool border = x0 < kR || y0 < kR || x0 + kT > W - kR || y0 + kT > H - kR;
   const size_t plane = (size_t)H * W;
   const float *pc = A.part + (size_t)c * 3 * plane;
-  for (int e = t; e < kH * kH; e += kLossThreads) {
-    const int r = e / kH, q = e - r * kH;
-    const int yy = my + r, xx = mx + q;
-    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
-    const size_t p = in ? (size_t)yy * W + xx : 0;
-    sd[0][r][q] = in ? __ldg(pc + p) : 0.0f;
-    sd[1][r][q] = in ? __ldg(pc + plane + p) : 0.0f;
-    sd[2][r][q] = in ? __ldg(pc + 2 * plane + p) : 0.0f;
+  {  // every load of the thread first, then the shared-memory stores
+    constexpr int kIt = (kH * kH + kLossThreads - 1) / kLossThreads;
+    float v0[kIt], v1[kIt], v2[kIt];
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int e = t + i * kLossThreads;
+      const int r = e / kH, q = e - r * kH;
+      const int yy = my + r, xx = mx + q;
+      const bool in = e < kH * kH && yy >= 0 && yy < H && xx >= 0 && xx < W;
+      const uint32_t p = in ? (uint32_t)yy * (uint32_t)W + (uint32_t)xx : 0u;
+      v0[i] = in ? __ldg(pc + p) : 0.0f;
+      v1[i] = in ? __ldg(pc + plane + p) : 0.0f;
+      v2[i] = in ? __ldg(pc + 2 * plane + p) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+      const int e = t + i * kLossThreads;
+      if (e < kH * kH) {
+        const int r = e / kH, q = e - r * kH;
+        sd[0][r][q] = v0[i];
+        sd[1][r][q] = v1[i];
+        sd[2][r][q] = v2[i];
+      }
+    }
   }
   __syncthreads();
   // vertical adjoint: item = (halo column, 4 tile rows), symmetric taps -> correlation
