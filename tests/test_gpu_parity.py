@@ -498,3 +498,28 @@ def test_fused_adam_all_groups_with_mask_penalties(tgs):
             p[f] = p[f] - lrs[f] * (m[f] / (1 - 0.9 ** step)) / (np.sqrt(v[f] / (1 - 0.999 ** step)) + 1e-15)
     for f in golden_io.FIELDS:
         np.testing.assert_allclose(_np(getattr(cloud, f)), p[f], rtol=2e-5, atol=2e-6, err_msg=f)
+
+
+def test_bin_tiles_huge_grid_multi_slab(tgs):
+    """Raw-array bin_tiles on a 16384 x 16384 image (1,048,576 tiles, 128 x 128 super-tiles):
+    the chunk x super-tile counts run in two row slabs.  Bit-exact vs the float32 oracle."""
+    rng = np.random.default_rng(7)
+    n, W, H, ts = 3000, 16384, 16384, 16
+    means = rng.uniform(-300, W + 300, (n, 2)).astype(np.float32)
+    radii = rng.uniform(2.0, 400.0, n).astype(np.float32)
+    depths = rng.uniform(1.0, 10.0, n).astype(np.float32)
+    b = tgs.bin_tiles(means, radii, depths, W, H, ts)
+    sp = np.zeros((n, 12), dtype=np.float32)
+    sp[:, 0:2], sp[:, 9], sp[:, 10] = means, depths, radii
+    f16 = np.float32(ts)
+    tx, ty = W // ts, H // ts
+    x0 = np.clip(np.floor((means[:, 0] - radii) / f16), 0, tx - 1)
+    x1 = np.clip(np.floor((means[:, 0] + radii) / f16), 0, tx - 1)
+    y0 = np.clip(np.floor((means[:, 1] - radii) / f16), 0, ty - 1)
+    y1 = np.clip(np.floor((means[:, 1] + radii) / f16), 0, ty - 1)
+    on = ((means[:, 0] + radii >= 0) & (means[:, 0] - radii <= W - 1) & (means[:, 1] + radii >= 0) &
+          (means[:, 1] - radii <= H - 1) & (radii > 0))
+    tt = np.where(on, (x1 - x0 + 1) * (y1 - y0 + 1), 0).astype(np.int32)
+    off, ids, _, _ = oracle.bin_tiles(sp, tt, W, H, ts, "f32")
+    assert np.array_equal(_np(b.offsets).astype(np.int64), off)
+    assert np.array_equal(_np(b.indices).astype(np.int64), ids)
