@@ -1083,9 +1083,9 @@ __global__ void __launch_bounds__(256) k_tile_scan(const uint32_t *__restrict__ 
 
 // Pass 2: rounds of 512 entries.  Per round and tile, the run of ids (entries of
 // all warps covering the tile, in entry order) is assembled in shared memory —
-// each entry's lane writes its id to stage[tile start + warp prefix + rank among
-// the warp's entries covering the tile] for every tile of its clipped rect — and
-// then copied out by consecutive lanes (coalesced).
+// lane l of warp w writes, for its tiles l and l + 32, the ids of w's entries
+// covering them (set bits of the coverage mask, in order) at the tile's run
+// start + w's prefix — and then copied out by consecutive lanes (coalesced).
 constexpr int kStage = 8192;
 
 __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t *__restrict__ entries,
@@ -1102,6 +1102,7 @@ __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t
   __shared__ uint32_t pre[kPlaceWarps][64];    // exclusive over warps
   __shared__ uint32_t len[64], sst[64], cur[64];
   __shared__ uint32_t s_total;
+  __shared__ uint32_t sg[kPlaceWarps][32];       // the round's cloud ids, per warp
   __shared__ uint32_t stage[kStage];
   uint32_t S, ea, eb;
   if (!place_unit(soff, ubase, utab, NS, blockIdx.x, S, ea, eb)) return;
@@ -1151,16 +1152,20 @@ __global__ void __launch_bounds__(kPlaceWarps * 32) k_place_write(const uint32_t
     __syncthreads();
     const uint32_t total = s_total;
     if (total <= (uint32_t)kStage) {
-      if (ok) {  // this entry's tiles inside the super-tile
-        int x0, y0, x1, y1;
-        unpack_rect(rc, x0, y0, x1, y1);
-        x0 = max(x0 - stx0, 0); x1 = min(x1 - stx0, kST - 1);
-        y0 = max(y0 - sty0, 0); y1 = min(y1 - sty0, kST - 1);
-        for (int y = y0; y <= y1; ++y)
-          for (int x = x0; x <= x1; ++x) {
-            const int q = y * kST + x;
-            stage[sst[q] + pre[warp][q] + __popc(mk[warp][q] & lt)] = gid;
-          }
+      // lane owns tiles `lane` and `lane + 32`: it writes the ids of the warp's entries
+      // covering them, in entry order (set bits of the coverage mask)
+      sg[warp][lane] = gid;
+      __syncwarp();
+#pragma unroll
+      for (int hq = 0; hq < 2; ++hq) {
+        const int q = lane + 32 * hq;
+        uint32_t mq = hq ? m1 : m0;
+        uint32_t slot = sst[q] + pre[warp][q];
+        while (mq) {
+          const int k = __ffs(mq) - 1;
+          mq &= mq - 1;
+          stage[slot++] = sg[warp][k];
+        }
       }
       __syncthreads();
       for (int q = warp; q < 64; q += kPlaceWarps) {
