@@ -188,13 +188,13 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
       const float var_a = m[2][o] - m0 * m0, var_b = m[3][o] - m1 * m1, cov = m[4][o] - m0 * m1;
       const float A1 = 2.0f * m0 * m1 + A.c1, A2 = 2.0f * cov + A.c2;
       const float B1 = m0 * m0 + m1 * m1 + A.c1, B2 = var_a + var_b + A.c2;
-      const float den = B1 * B2;
-      const float smap = A1 * A2 / den;
+      const float rB1 = 1.0f / B1, rB2 = 1.0f / B2, rden = rB1 * rB2;  // two reciprocals, no divisions
+      const float smap = A1 * A2 * rden;
       const size_t plane = (size_t)H * W, p = (size_t)yy * W + xx;
       float *pc = A.part + (size_t)c * 3 * plane;
-      pc[p] = 2.0f * m1 * (A2 - A1) / den - 2.0f * m0 * smap * (1.0f / B1 - 1.0f / B2);
-      pc[plane + p] = -smap / B2;
-      pc[2 * plane + p] = 2.0f * A1 / den;
+      pc[p] = 2.0f * m1 * (A2 - A1) * rden - 2.0f * m0 * smap * (rB1 - rB2);
+      pc[plane + p] = -smap * rB2;
+      pc[2 * plane + p] = 2.0f * A1 * rden;
       ss += smap;
       l1 += fabsf(sa[(r0 + o + kR) * kH + q + kR] - sb[(r0 + o + kR) * kH + q + kR]);
     }
