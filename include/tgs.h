@@ -199,6 +199,21 @@ TGS_API int tgs_blend_backward(const float *splats, const int32_t *tile_offsets,
                        const float *transmit, const int32_t *last_pos, const float *dimage,
                        float *dsplats, tgs_stream_t stream);
 
+/* Deterministic variant (a deterministic-reduction mode): the
+ * partials of every (tile, Gaussian) pair are summed over the tile's warps in a
+ * fixed order and stored per list position; each Gaussian then sums its own
+ * instances in rect order (row-major over its band-clipped tile rect) with one
+ * thread, so dsplats (+=) is bitwise reproducible run to run.  Needs the
+ * forward's tiles_touched (n), the instance count and a workspace of
+ * tgs_blend_backward_deterministic_workspace() bytes (≈ 40 B per instance). */
+TGS_API int tgs_blend_backward_deterministic_workspace(int64_t n, int64_t num_instances, size_t *bytes);
+TGS_API int tgs_blend_backward_deterministic(const float *splats, const int32_t *tiles_touched, int64_t n,
+                                             const int32_t *tile_offsets, const int32_t *sorted_ids,
+                                             int64_t num_instances, const tgs_camera *cam, const tgs_settings *s,
+                                             int32_t row_begin, int32_t row_end, const float *transmit,
+                                             const int32_t *last_pos, const float *dimage, float *dsplats,
+                                             void *workspace, tgs_stream_t stream);
+
 /* ---- (5) preprocess backward ------------------------------------------------
  * accumulate != 0 adds into grads (multi-view batches), else overwrites. */
 TGS_API int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,

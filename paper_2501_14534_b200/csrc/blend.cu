@@ -26,6 +26,7 @@
 // the forward's blend decisions bit for bit (a mismatch would corrupt the
 // T_before = T_after / (1 - a) recovery).
 #include "tgs_common.cuh"
+#include "tgs_math.cuh"
 
 namespace tgs {
 
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
                                                            float bg2, const float *__restrict__ transmit,
                                                            const int32_t *__restrict__ last_pos,
                                                            const float *__restrict__ dimage,
-                                                           float *__restrict__ dsplats) {
+                                                           float *__restrict__ dsplats,
+                                                           float *__restrict__ partial) {
   using SM = BwdShared<kMaxThreads>;
   constexpr int kBB = SM::kBB;
   __shared__ SM S;
@@ -369,15 +371,147 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
     }
     __syncthreads();
     if (t < cnt) {
-      float *d = dsplats + 9 * (int64_t)S.id[t];
+      if (partial) {  // deterministic mode: this (tile, splat) pair's partials, summed in warp order
+        float *pp = partial + (int64_t)(start + lo + t) * 9;
 #pragma unroll
-      for (int f = 0; f < 9; ++f) {
-        float x = 0.0f;
-        for (int w = 0; w < nwarps; ++w) x += S.acc[w][f][t];
-        if (x != 0.0f) atomicAdd(d + f, x);
+        for (int f = 0; f < 9; ++f) {
+          float x = 0.0f;
+          for (int w = 0; w < nwarps; ++w) x += S.acc[w][f][t];
+          pp[f] = x;
+        }
+      } else {
+        float *d = dsplats + 9 * (int64_t)S.id[t];
+#pragma unroll
+        for (int f = 0; f < 9; ++f) {
+          float x = 0.0f;
+          for (int w = 0; w < nwarps; ++w) x += S.acc[w][f][t];
+          if (x != 0.0f) atomicAdd(d + f, x);
+        }
       }
     }
   }
+  if (partial) {  // list positions no pixel reached contribute zero
+    const int stop = offsets[tile + 1];
+    for (int64_t e = (int64_t)(start + max_last) * 9 + t; e < (int64_t)stop * 9; e += B) partial[e] = 0.0f;
+  }
+}
+
+// ------------------------------------------------- deterministic reduction
+// Per Gaussian (cloud row), its instances in rect order (row-major over the
+// band-clipped tile rect of bin_tiles) map to list positions through `inv`;
+// the Gaussian's partials are summed in that fixed order by one thread, so the
+// result does not depend on scheduling.
+__global__ void k_inst_count(const float *__restrict__ splats, const int32_t *__restrict__ tiles_touched, int64_t n,
+                             int W, int H, int ts, int tiles_x, int tiles_y, int rb, int re,
+                             uint32_t *__restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t c = 0;
+  if (tiles_touched[i] > 0) {
+    int x0, y0, x1, y1;
+    const float *sp = splats + 12 * i;
+    if (tile_rect(sp[0], sp[1], sp[10], W, H, ts, tiles_x, tiles_y, x0, y0, x1, y1) > 0) {
+      y0 = max(y0, rb);
+      y1 = min(y1, re - 1);
+      if (y1 >= y0) c = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+    }
+  }
+  cnt[i] = c;
+}
+
+constexpr uint32_t kDetFlagAgg = 1u << 30, kDetFlagInc = 2u << 30, kDetMask = (1u << 30) - 1;
+
+// Exclusive scan of n u32 (in place), tiles of 4096 chained by decoupled look-back.
+__global__ void __launch_bounds__(256) k_det_scan(uint32_t *__restrict__ v, int64_t n, uint32_t *__restrict__ status,
+                                                  uint32_t *__restrict__ ticket) {
+  __shared__ uint32_t ws[8], s_tile, s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * 4096 + threadIdx.x * 16;
+  uint32_t x[16], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    x[k] = base + k < n ? v[base + k] : 0u;
+    sum += x[k];
+  }
+  // block exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  uint32_t woff = 0, tot = 0;
+  for (int w = 0; w < 8; ++w) {
+    if (w < warp) woff += ws[w];
+    tot += ws[w];
+  }
+  if (threadIdx.x == 0) {
+    uint32_t *mine = status + tile;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      atomicExch(mine, kDetFlagInc | tot);
+    } else {
+      atomicExch(mine, kDetFlagAgg | tot);
+      int j = (int)tile - 1;
+      for (;;) {
+        const uint32_t sv = atomicAdd(status + j, 0u);
+        if ((sv >> 30) == 0) continue;  // predecessor not published yet
+        excl += sv & kDetMask;
+        if (sv & kDetFlagInc) break;
+        --j;
+      }
+      atomicExch(mine, kDetFlagInc | (excl + tot));
+    }
+    s_excl = excl;
+  }
+  __syncthreads();
+  uint32_t run = s_excl + woff + inc - sum;
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (base + k < n) {
+      v[base + k] = run;
+      run += x[k];
+    }
+}
+
+// One CTA per band tile: list position -> slot of that instance in its Gaussian's rect order.
+__global__ void k_det_inverse(const float *__restrict__ splats, const int32_t *__restrict__ offsets,
+                              const int32_t *__restrict__ ids, const uint32_t *__restrict__ inst_off, int W, int H,
+                              int ts, int tiles_x, int tiles_y, int rb, int re, uint32_t *__restrict__ inv) {
+  const int tile = blockIdx.x;
+  const int ty = rb + tile / tiles_x, tx = tile % tiles_x;
+  const int start = offsets[tile], stop = offsets[tile + 1];
+  for (int pos = start + threadIdx.x; pos < stop; pos += blockDim.x) {
+    const int g = ids[pos];
+    const float *sp = splats + 12 * (int64_t)g;
+    int x0, y0, x1, y1;
+    tile_rect(sp[0], sp[1], sp[10], W, H, ts, tiles_x, tiles_y, x0, y0, x1, y1);
+    y0 = max(y0, rb);
+    inv[inst_off[g] + (uint32_t)((ty - y0) * (x1 - x0 + 1) + (tx - x0))] = (uint32_t)pos;
+  }
+}
+
+__global__ void k_det_reduce(const uint32_t *__restrict__ cnt_off, const uint32_t *__restrict__ inv,
+                             const float *__restrict__ partial, int64_t n, int64_t total,
+                             float *__restrict__ dsplats) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t o0 = cnt_off[i], o1 = i + 1 < n ? cnt_off[i + 1] : (uint32_t)total;
+  if (o1 == o0) return;
+  float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (uint32_t k = o0; k < o1; ++k) {
+    const float *pp = partial + (int64_t)inv[k] * 9;
+#pragma unroll
+    for (int f = 0; f < 9; ++f) acc[f] += pp[f];
+  }
+  float *d = dsplats + 9 * i;
+#pragma unroll
+  for (int f = 0; f < 9; ++f) d[f] += acc[f];
 }
 
 // ---------------------------------------------------------------------------
@@ -762,6 +896,62 @@ extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offse
   (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage,
-      dsplats);
+      dsplats, nullptr);
+  return launch_status();
+}
+
+static size_t det_ws(int64_t n, int64_t num_instances, size_t *parts) {
+  Carve c(nullptr);
+  const size_t N = (size_t)tmax<int64_t>(n, 1), I = (size_t)tmax<int64_t>(num_instances, 1);
+  parts[0] = c.off; c.take<float>(I * 9);                  // partials per list position
+  parts[1] = c.off; c.take<uint32_t>(I);                   // inverse map
+  parts[2] = c.off; c.take<uint32_t>(N);                   // per-Gaussian counts -> offsets
+  parts[3] = c.off; c.take<uint32_t>(ceil_div<size_t>(N, 4096) + 1);  // scan look-back + ticket
+  parts[4] = c.off;
+  return c.off;
+}
+
+extern "C" int tgs_blend_backward_deterministic_workspace(int64_t n, int64_t num_instances, size_t *bytes) {
+  if (n < 0 || num_instances < 0 || !bytes) return TGS_ERR_INVALID;
+  size_t parts[5];
+  *bytes = det_ws(n, num_instances, parts);
+  return TGS_OK;
+}
+
+extern "C" int tgs_blend_backward_deterministic(const float *splats, const int32_t *tiles_touched, int64_t n,
+                                                const int32_t *tile_offsets, const int32_t *sorted_ids,
+                                                int64_t num_instances, const tgs_camera *cam, const tgs_settings *s,
+                                                int32_t row_begin, int32_t row_end, const float *transmit,
+                                                const int32_t *last_pos, const float *dimage, float *dsplats,
+                                                void *workspace, tgs_stream_t stream) {
+  int tiles_x, ntiles;
+  if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if (n < 0 || num_instances < 0 || num_instances >= ((int64_t)1 << 30) || !workspace || !tiles_touched)
+    return TGS_ERR_INVALID;
+  if (ntiles == 0 || n == 0) return TGS_OK;
+  cudaStream_t st = as_stream(stream);
+  size_t parts[5];
+  det_ws(n, num_instances, parts);
+  char *w = static_cast<char *>(workspace);
+  float *partial = reinterpret_cast<float *>(w + parts[0]);
+  uint32_t *inv = reinterpret_cast<uint32_t *>(w + parts[1]);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(w + parts[2]);
+  uint32_t *status = reinterpret_cast<uint32_t *>(w + parts[3]);
+  const int tiles_y = (cam->height + s->tile_size - 1) / s->tile_size;
+  const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
+  (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, st>>>(
+      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
+      partial);
+  const unsigned gn = (unsigned)ceil_div<int64_t>(n, 256);
+  k_inst_count<<<gn, 256, 0, st>>>(splats, tiles_touched, n, cam->width, cam->height, s->tile_size, tiles_x, tiles_y,
+                                   row_begin, row_end, cnt);
+  const unsigned nt = (unsigned)ceil_div<int64_t>(n, 4096);
+  cudaMemsetAsync(status, 0, ((size_t)nt + 1) * 4, st);
+  k_det_scan<<<nt, 256, 0, st>>>(cnt, n, status, status + nt);
+  k_det_inverse<<<ntiles, 256, 0, st>>>(splats, tile_offsets, sorted_ids, cnt, cam->width, cam->height,
+                                        s->tile_size, tiles_x, tiles_y, row_begin, row_end, inv);
+  k_det_reduce<<<gn, 256, 0, st>>>(cnt, inv, partial, n, num_instances, dsplats);
   return launch_status();
 }

@@ -21,7 +21,8 @@ Deliberate differences:
     If `output` carries no device state (e.g. built by hand), it recomputes them.
   * extension keywords: `grads=` / `accumulate=` on render_backward let a
     multi-view step accumulate into one CloudGrads buffer; `row_band=` renders
-    a band of tile rows (tile-row sharding, parallel.py).
+    a band of tile rows (tile-row sharding, parallel.py); `deterministic=True`
+    selects the fixed-order (bitwise reproducible) gradient reduction.
 """
 
 from __future__ import annotations
@@ -253,9 +254,12 @@ def _records(out, splats, bins, cam, c_cam, c_set, dev):
 
 
 def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
-                   dsplats: torch.Tensor | None = None):
+                   dsplats: torch.Tensor | None = None, deterministic: bool = False):
     """First half of render_backward: the screen-space partials (N, 9) of one view
-    (tgs_blend_backward, _kernels.py:92-181) plus the forward state they refer to."""
+    (tgs_blend_backward, _kernels.py:92-181) plus the forward state they refer to.
+
+    deterministic=True sums every Gaussian's per-tile partials in a fixed order
+    (tgs_blend_backward_deterministic): bitwise reproducible, ~40 B/instance of scratch."""
     import ctypes
     if output is None or output.transmittance is None or output.last_pos is None:
         raise ContractViolationError("render_backward needs the forward pass auxiliaries")
@@ -283,9 +287,18 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
         dsplats = torch.zeros((n, 9), dtype=torch.float32, device=dev)
     c_cam = _lib.make_camera(cam)
     with stage("blend_bwd"):
-        _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
-                  ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
-                  _lib.ptr(d), _lib.ptr(dsplats), _lib.stream_handle(dev))
+        if deterministic:
+            ni = int(bins.indices.numel())
+            nb = ctypes_size("tgs_blend_backward_deterministic_workspace", n, ni)
+            ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
+            _lib.call("tgs_blend_backward_deterministic", _lib.ptr(st.splats), _lib.ptr(st.tiles_touched), n,
+                      _lib.ptr(bins.offsets), _lib.ptr(bins.indices), ni, ctypes.byref(c_cam), ctypes.byref(c_set),
+                      rb, re, _lib.ptr(transmit), _lib.ptr(last_pos), _lib.ptr(d), _lib.ptr(dsplats), _lib.ptr(ws),
+                      _lib.stream_handle(dev))
+        else:
+            _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+                      ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
+                      _lib.ptr(d), _lib.ptr(dsplats), _lib.stream_handle(dev))
     return dsplats, st
 
 
@@ -310,7 +323,8 @@ def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: Render
 
 
 def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output: RenderOutput,
-                    grads: CloudGrads | None = None, accumulate: bool = False) -> CloudGrads:
+                    grads: CloudGrads | None = None, accumulate: bool = False,
+                    deterministic: bool = False) -> CloudGrads:
     """Analytic gradients of sum(dimage * image) w.r.t. every cloud field (rasterizer.py:326-419)."""
     if output is None or output.transmittance is None or output.last_pos is None:
         raise ContractViolationError("render_backward needs the forward pass auxiliaries")
@@ -324,5 +338,5 @@ def render_backward(cloud, cam: Camera, settings: RenderSettings, dimage, output
         accumulate = False
     if n == 0:
         return grads
-    dsplats, st = blend_backward(cloud, cam, settings, dimage, output)
+    dsplats, st = blend_backward(cloud, cam, settings, dimage, output, deterministic=deterministic)
     return preprocess_backward_views(cloud, [cam], settings, [st.visible_u8], [dsplats], grads, accumulate)

@@ -34,7 +34,7 @@ DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opac
 class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
-                 views=None, streams: int = 2):
+                 views=None, streams: int = 2, deterministic: bool = False):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -57,6 +57,7 @@ class Trainer:
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
         self.launches_per_step = 0
+        self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
 
     def step(self, host_targets=None) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms.
@@ -97,7 +98,8 @@ class Trainer:
                 if ds is None or ds.shape[0] != len(self.cloud):
                     ds = self.dsplats[v] = torch.empty((len(self.cloud), 9), dtype=torch.float32, device=d.device)
                 ds.zero_()
-                _, st_state = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds)
+                _, st_state = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds,
+                                             deterministic=self.deterministic)
                 vis.append(st_state.visible_u8)
                 parts.append(ds)
         for s_ in self.streams:

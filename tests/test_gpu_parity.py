@@ -523,3 +523,46 @@ def test_bin_tiles_huge_grid_multi_slab(tgs):
     off, ids, _, _ = oracle.bin_tiles(sp, tt, W, H, ts, "f32")
     assert np.array_equal(_np(b.offsets).astype(np.int64), off)
     assert np.array_equal(_np(b.indices).astype(np.int64), ids)
+
+
+def test_deterministic_backward_reproducible_and_exact(tgs):
+    """deterministic=True: bitwise identical gradients run to run, within the north-star
+    tolerance of the float64 oracle, and equal (up to reassociation) to the atomic path."""
+    from paper_2501_14534_b200 import scenes
+    sc = scenes.config1()
+    st = tgs.RenderSettings(near=0.2)
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    cam = sc.cameras[0]
+    dimg = np.random.default_rng(3).standard_normal((cam.height, cam.width, 3)).astype(np.float32)
+    dt = torch.from_numpy(dimg).cuda()
+    out = tgs.render_forward(cloud, cam, st)
+    g1 = tgs.render_backward(cloud, cam, st, dt, out, deterministic=True)
+    g2 = tgs.render_backward(cloud, cam, st, dt, out, deterministic=True)
+    ga = tgs.render_backward(cloud, cam, st, dt, out)
+    assert torch.equal(g1.flat, g2.flat)
+    ref = oracle.render_forward(sc.fields, cam, st, "f64")
+    rg = oracle.render_backward(sc.fields, cam, st, dimg.astype(np.float64), ref, "f64")
+    for f in golden_io.FIELDS:
+        a, b = _np(getattr(g1, f)), rg[f]
+        assert np.linalg.norm(a - b) <= 1e-4 * max(np.linalg.norm(b), 1e-30), f
+        np.testing.assert_allclose(a, _np(getattr(ga, f)), rtol=1e-4, atol=1e-6 * max(1.0, np.abs(b).max()),
+                                   err_msg=f)
+
+
+def test_trainer_deterministic_steps_bitwise_reproducible(tgs):
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.train import Trainer
+    sc = scenes.small_scene(seed=31, n=20_000, width=160, height=120, dist=3.5)
+    rng = np.random.default_rng(4)
+    cams = [scenes.pinhole(rng.uniform(3.0, 4.5) * d / np.linalg.norm(d), 160, 120) for d in rng.normal(size=(4, 3))]
+    targets = [torch.from_numpy(rng.uniform(0, 1, (120, 160, 3)).astype(np.float32)).cuda() for _ in cams]
+    st = tgs.RenderSettings(near=0.2, mask_threshold=0.01)
+    flats = []
+    for _ in range(2):
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        tr = Trainer(cloud, cams, targets, st, deterministic=True)
+        for _ in range(3):
+            tr.step()
+        torch.cuda.synchronize()
+        flats.append(cloud.flat.clone())
+    assert torch.equal(flats[0], flats[1])
