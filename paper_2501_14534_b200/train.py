@@ -59,6 +59,20 @@ class Trainer:
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
 
+    def prune(self, eps: float) -> int:
+        """Mask-based pruning between steps (masking.py:70-81, training.py:340-346): keep
+        the rows whose hard mask survives, compact the cloud and the Adam moments with
+        tgs_gather_rows (optim.py:51-55) and resize the gradient buffers.  Returns the
+        new Gaussian count."""
+        from . import pruning
+        new, keep = pruning.prune_by_mask(self.cloud, eps)
+        if new is not self.cloud:
+            pruning.compact_adam(self.opt, self.cloud, new, keep)
+            self.cloud = new
+            self.grads = CloudGrads(len(new), new.device)
+            self.dsplats = {}
+        return len(self.cloud)
+
     def step(self, host_targets=None) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms.
 
