@@ -390,8 +390,22 @@ def main():
     rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
     launches = trainer_launches(prof.counts(), args.steps)
 
-    # ---- render FPS (forward only, initial scene) as a secondary number
-    fps_t = timed(args.steps, lambda: [render_forward(cloud, sc.cameras[v], st) for v in views])
+    # ---- render FPS (forward only, initial scene) as a secondary number: the views of a step
+    # alternate between two streams like the training step, device-timed
+    rstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+
+    def render_all():
+        main = torch.cuda.current_stream(dev)
+        for s_ in rstreams:
+            s_.wait_stream(main)
+        for i, v in enumerate(views):
+            with torch.cuda.stream(rstreams[i % 2]):
+                render_forward(cloud, sc.cameras[v], st)
+        for s_ in rstreams:
+            main.wait_stream(s_)
+
+    render_all()
+    fps_t = timed(args.steps, render_all)
     render_fps = args.steps * len(views) * world / fps_t
 
     if rank != 0:
