@@ -132,8 +132,9 @@ def stage_bytes(n, vis_n, inst, entries, pixels, views):
     n Gaussians, vis_n selected (on-screen) Gaussians, inst instances, entries
     (Gaussian, 8x8-tile super-tile) pairs and pixels are per view."""
     return {
-        # read 252 B of parameters, write 48 B record + 1 visible + 4 tiles + 8 depth key
-        "preprocess_fwd": n * (252 + 48 + 1 + 4 + 8),
+        # one multi-view launch per step: 252 B of parameters read once, per view a 48 B record
+        # + 1 visible + 4 tiles + 8 depth key written
+        "preprocess_fwd": n * (252 + views * (48 + 1 + 4 + 8)),
         # value-bucket depth sort: select (tiles 4 + mean/radius 20 + rect 8 written) + key 8, bucket
         # count (rect 4, key 8), scatter (rect 4, key 8 in; key + id 12 out), in-bucket rank
         # (key + id 12 in, id 4 + rect 8 gathered + rect 8 out); the 2^17-bucket scan

@@ -136,6 +136,14 @@ TGS_API const char *tgs_last_error_string(int status);
 TGS_API int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                            float *splats, uint8_t *visible, int32_t *tiles_touched, uint64_t *depth_keys,
                            int32_t *error_flag, tgs_stream_t stream);
+/* A batch of views in ONE pass over the parameters (the sh_rest block staged
+ * once): per view v the same outputs as tgs_preprocess_forward into splats[v],
+ * visible[v], tiles_touched[v], depth_keys[v] (may be NULL), bit-identical to a
+ * single-view call with cams[v]. */
+TGS_API int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                         int32_t nviews, float *const *splats, uint8_t *const *visible,
+                                         int32_t *const *tiles_touched, uint64_t *const *depth_keys,
+                                         int32_t *error_flag, tgs_stream_t stream);
 
 /* tiles_touched for arbitrary projected records (the bin_tiles(...) entry,
  * rasterizer.py:95-128): only splat fields means2d and radius are read. */

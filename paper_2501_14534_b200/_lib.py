@@ -51,6 +51,7 @@ class TgsGrads(ctypes.Structure):
 _SIGS = {
     "tgs_version": ([], _I32),
     "tgs_preprocess_forward": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
     "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P], _I32),

@@ -124,6 +124,18 @@ __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, co
 }
 
 template <int DEG>
+__device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                               const tgs_settings &s, const float *rest, float *__restrict__ splats,
+                                               uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
+                                               uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err);
+template <int DEG>
+__device__ __forceinline__ void emit_view(const tgs_cloud &cl, int64_t i, const tgs_camera &cam, const tgs_settings &s,
+                                          const float *rest, float *splats, uint8_t *visible, int32_t *tiles,
+                                          uint64_t *depth_keys, int32_t *err) {
+  emit_view_impl<DEG>(cl, i, cam, s, rest, splats, visible, tiles, depth_keys, err);
+}
+
+template <int DEG>
 __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd(tgs_cloud cl, tgs_camera cam, tgs_settings s,
                                                               float *__restrict__ splats,
                                                               uint8_t *__restrict__ visible,
@@ -136,9 +148,44 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd(tgs_cloud cl, tgs_
   if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
   __syncthreads();
   if ((int)threadIdx.x >= count) return;
-  const int64_t i = base + threadIdx.x;
+  emit_view<DEG>(cl, base + threadIdx.x, cam, s, rest_s + 45 * threadIdx.x, splats, visible, tiles, depth_keys, err);
+}
+
+// Multi-view forward: one pass over the parameters for a batch of views (the
+// sh_rest block staged once, the other fields re-read from L1); every view's
+// outputs are bit-identical to k_preprocess_fwd's (same per-view routine).
+constexpr int kMaxFwdViews = 8;
+struct FwdViews {
+  tgs_camera cam[kMaxFwdViews];
+  float *splats[kMaxFwdViews];
+  uint8_t *visible[kMaxFwdViews];
+  int32_t *tiles[kMaxFwdViews];
+  uint64_t *depth_keys[kMaxFwdViews];
+  int nviews;
+};
+
+template <int DEG>
+__global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl, FwdViews fv, tgs_settings s,
+                                                                    int32_t *__restrict__ err) {
+  __shared__ __align__(16) float rest_s[kPreBlock * 45];
+  const int64_t base = (int64_t)blockIdx.x * kPreBlock;
+  const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
+  if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  __syncthreads();
+  if ((int)threadIdx.x >= count) return;
+  for (int v = 0; v < fv.nviews; ++v)
+    emit_view<DEG>(cl, base + threadIdx.x, fv.cam[v], s, rest_s + 45 * threadIdx.x, fv.splats[v], fv.visible[v],
+                   fv.tiles[v], fv.depth_keys[v], err);
+}
+
+// One Gaussian, one view: the projected record, visibility, tile count and depth key.
+template <int DEG>
+__device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                               const tgs_settings &s, const float *rest, float *__restrict__ splats,
+                                               uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
+                                               uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err) {
   GaussFwd f;
-  gauss_forward<DEG>(cl, i, cam, s, rest_s + 45 * threadIdx.x, f);
+  gauss_forward<DEG>(cl, i, cam, s, rest, f);
   if (f.degenerate) atomicOr(err, 1);
   float4 *o = reinterpret_cast<float4 *>(splats + 12 * i);
   int nt = 0;
@@ -196,6 +243,40 @@ extern "C" int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *
   case D: k_preprocess_fwd<D><<<grid, kPreBlock, 0, st>>>(*cloud, *cam, *s, splats, visible, tiles_touched, depth_keys, error_flag); break;
     TGS_FWD(0) TGS_FWD(1) TGS_FWD(2) TGS_FWD(3)
 #undef TGS_FWD
+  }
+  return launch_status();
+}
+
+extern "C" int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                            int32_t nviews, float *const *splats, uint8_t *const *visible,
+                                            int32_t *const *tiles_touched, uint64_t *const *depth_keys,
+                                            int32_t *error_flag, tgs_stream_t stream) {
+  if (!cloud || !cams || !s || cloud->n < 0 || nviews < 1 || !splats || !visible || !tiles_touched)
+    return TGS_ERR_INVALID;
+  if (s->tile_size < 1 || s->tile_size > 32) return TGS_ERR_UNSUPPORTED;
+  if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
+  if (cloud->n == 0) return TGS_OK;
+  for (int v = 0; v < nviews; ++v)
+    if (!splats[v] || (reinterpret_cast<uintptr_t>(splats[v]) & 15) || !visible[v] || !tiles_touched[v])
+      return TGS_ERR_INVALID;
+  const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
+  cudaStream_t st = as_stream(stream);
+  for (int v0 = 0; v0 < nviews; v0 += kMaxFwdViews) {
+    FwdViews fv;
+    fv.nviews = nviews - v0 < kMaxFwdViews ? nviews - v0 : kMaxFwdViews;
+    for (int k = 0; k < fv.nviews; ++k) {
+      fv.cam[k] = cams[v0 + k];
+      fv.splats[k] = splats[v0 + k];
+      fv.visible[k] = visible[v0 + k];
+      fv.tiles[k] = tiles_touched[v0 + k];
+      fv.depth_keys[k] = depth_keys ? depth_keys[v0 + k] : nullptr;
+    }
+    switch (s->active_sh_degree) {
+#define TGS_FWDV(D) \
+  case D: k_preprocess_fwd_views<D><<<grid, kPreBlock, 0, st>>>(*cloud, fv, *s, error_flag); break;
+      TGS_FWDV(0) TGS_FWDV(1) TGS_FWDV(2) TGS_FWDV(3)
+#undef TGS_FWDV
+    }
   }
   return launch_status();
 }

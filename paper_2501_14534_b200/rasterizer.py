@@ -198,8 +198,36 @@ def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
     return splats, vis, tiles, keys, err
 
 
-def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple | None = None) -> RenderOutput:
-    """Render a cloud into an (H, W, 3) image plus blending auxiliaries (rasterizer.py:215-284)."""
+def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings) -> list:
+    """tgs_preprocess_forward_views: the per-view preprocess outputs of a batch of views in
+    one pass over the parameters; element v is what `preprocess(cloud, cams[v], settings)`
+    returns (bit-identical), the error flag shared."""
+    import ctypes
+    n = len(cloud)
+    dev = cloud.device
+    V = len(cams)
+    outs = []
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    for _ in range(V):
+        outs.append((torch.empty((max(n, 1), 12), dtype=torch.float32, device=dev),
+                     torch.zeros(max(n, 1), dtype=torch.uint8, device=dev),
+                     torch.zeros(max(n, 1), dtype=torch.int32, device=dev),
+                     torch.empty(max(n, 1), dtype=torch.int64, device=dev), err))
+    if n and V:
+        c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
+        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+        arr = lambda k: (ctypes.c_void_p * V)(*[o[k].data_ptr() for o in outs])  # noqa: E731
+        with stage("preprocess_fwd"):
+            _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0),
+                      arr(1), arr(2), arr(3), _lib.ptr(err), _lib.stream_handle(dev))
+    return outs
+
+
+def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple | None = None,
+                   pre: tuple | None = None) -> RenderOutput:
+    """Render a cloud into an (H, W, 3) image plus blending auxiliaries (rasterizer.py:215-284).
+
+    pre: this view's outputs of `preprocess_views` (skips the per-view preprocess)."""
     import ctypes
     cloud = _as_cloud(cloud)
     c_set = _lib.make_settings(settings)  # validates settings even for empty clouds
@@ -209,7 +237,7 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     n = len(cloud)
     dev = cloud.device
     rb, re = row_band if row_band is not None else (0, _tiles_y(cam, ts))
-    splats, vis, tiles, keys, err = preprocess(cloud, cam, settings)
+    splats, vis, tiles, keys, err = pre if pre is not None else preprocess(cloud, cam, settings)
     bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys)
     image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
     transmit = torch.empty((h, w), dtype=torch.float32, device=dev)

@@ -24,7 +24,8 @@ from . import loss as loss_mod
 from .cloud import CloudGrads, GaussianCloud
 from .optim import Adam
 from .profiler import stage
-from .rasterizer import RenderSettings, blend_backward, preprocess_backward_views, render_forward
+from .rasterizer import (RenderSettings, blend_backward, preprocess_backward_views, preprocess_views,
+                         render_forward)
 
 # reference defaults (config.py:76-92 OptimConfig; config.py:67-73 MaskConfig)
 DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opacity_logits": 0.05,
@@ -91,8 +92,10 @@ class Trainer:
                     ev = torch.cuda.Event()
                     ev.record(self.copy_stream)
                     copied[v] = ev
+        # every view's preprocess in one pass over the parameters (main stream)
+        pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings)
         for s_ in self.streams:
-            s_.wait_stream(main)  # parameters updated by the previous step's Adam
+            s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         for i, v in enumerate(self.views):
             # consecutive views alternate between two streams: the latency-bound binning of
             # view v overlaps the blend/loss kernels of view v-1 (and the host round trip
@@ -100,7 +103,7 @@ class Trainer:
             st = self.streams[i % len(self.streams)]
             with torch.cuda.stream(st):
                 cam, target = self.cameras[v], self.targets[v]
-                out = render_forward(self.cloud, cam, self.settings)
+                out = render_forward(self.cloud, cam, self.settings, pre=pres[i])
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
                 if d is None:
                     d = self.dimage[(i % len(self.streams), cam.height, cam.width)] = torch.empty_like(out.image)

@@ -566,3 +566,21 @@ def test_trainer_deterministic_steps_bitwise_reproducible(tgs):
         torch.cuda.synchronize()
         flats.append(cloud.flat.clone())
     assert torch.equal(flats[0], flats[1])
+
+
+def test_multiview_preprocess_bitwise_equals_single_view(tgs):
+    """tgs_preprocess_forward_views == tgs_preprocess_forward per view, bit for bit."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.rasterizer import preprocess, preprocess_views
+    sc = scenes.small_scene(seed=41, n=30_000, width=200, height=150, dist=3.0)
+    rng = np.random.default_rng(2)
+    cams = [scenes.pinhole(rng.uniform(2.5, 4.5) * d / np.linalg.norm(d), 200, 150) for d in rng.normal(size=(11, 3))]
+    for deg in (0, 3):
+        st = tgs.RenderSettings(near=0.2, active_sh_degree=deg, mask_threshold=0.3)
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        many = preprocess_views(cloud, cams, st)
+        for cam, got in zip(cams, many):
+            want = preprocess(cloud, cam, st)
+            for a, b in zip(got[:4], want[:4]):
+                assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a,
+                                   b.view(torch.int32) if b.dtype == torch.float32 else b)
