@@ -20,9 +20,7 @@ namespace tgs {
 
 // Forward quantities of Gaussian i in the documented float32 order.  `rest`
 // points at this Gaussian's 45 staged coefficients (may be null when degree 0).
-template <int DEG>
-__device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
-                                              const tgs_settings &s, const float *rest, GaussFwd &f) {
+__device__ __forceinline__ void gauss_static(const tgs_cloud &cl, int64_t i, const tgs_settings &s, GaussFwd &f) {
   // hard masks in logit space (masking.py:21-25; see tgs.h)
   const float m = cl.mask_logits[i], o = cl.opacity_logits[i];
   f.Mg = (m > s.mask_logit_min) ? 1.0f : 0.0f;
@@ -62,6 +60,13 @@ __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, co
 #pragma unroll
     for (int b = 0; b < 3; ++b)
       f.S[3 * a + b] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
+}
+
+// The view-dependent half: EWA projection, view direction and SH colour.  `f`
+// carries gauss_static's outputs (computed once per Gaussian for a batch of views).
+template <int DEG>
+__device__ __forceinline__ void gauss_view(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                           const tgs_settings &s, const float *rest, GaussFwd &f) {
   // EWA projection (geometry.py:153-183)
   const float px = cl.positions[3 * i], py = cl.positions[3 * i + 1], pz = cl.positions[3 * i + 2];
 #pragma unroll
@@ -124,10 +129,21 @@ __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, co
 }
 
 template <int DEG>
+__device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                              const tgs_settings &s, const float *rest, GaussFwd &f) {
+  gauss_static(cl, i, s, f);
+  gauss_view<DEG>(cl, i, cam, s, rest, f);
+}
+
+template <int DEG>
 __device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
                                                const tgs_settings &s, const float *rest, float *__restrict__ splats,
                                                uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
                                                uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err);
+__device__ __forceinline__ void emit_record(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                            const tgs_settings &s, const GaussFwd &f, float *__restrict__ splats,
+                                            uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
+                                            uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err);
 template <int DEG>
 __device__ __forceinline__ void emit_view(const tgs_cloud &cl, int64_t i, const tgs_camera &cam, const tgs_settings &s,
                                           const float *rest, float *splats, uint8_t *visible, int32_t *tiles,
@@ -173,9 +189,14 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl
   if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
   __syncthreads();
   if ((int)threadIdx.x >= count) return;
-  for (int v = 0; v < fv.nviews; ++v)
-    emit_view<DEG>(cl, base + threadIdx.x, fv.cam[v], s, rest_s + 45 * threadIdx.x, fv.splats[v], fv.visible[v],
-                   fv.tiles[v], fv.depth_keys[v], err);
+  const int64_t i = base + threadIdx.x;
+  GaussFwd f0;
+  gauss_static(cl, i, s, f0);  // view-independent half once
+  for (int v = 0; v < fv.nviews; ++v) {
+    GaussFwd f = f0;
+    gauss_view<DEG>(cl, i, fv.cam[v], s, rest_s + 45 * threadIdx.x, f);
+    emit_record(cl, i, fv.cam[v], s, f, fv.splats[v], fv.visible[v], fv.tiles[v], fv.depth_keys[v], err);
+  }
 }
 
 // One Gaussian, one view: the projected record, visibility, tile count and depth key.
@@ -186,6 +207,14 @@ __device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, c
                                                uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err) {
   GaussFwd f;
   gauss_forward<DEG>(cl, i, cam, s, rest, f);
+  emit_record(cl, i, cam, s, f, splats, visible, tiles, depth_keys, err);
+}
+
+// Writes one view's outputs of Gaussian i from its forward quantities.
+__device__ __forceinline__ void emit_record(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                            const tgs_settings &s, const GaussFwd &f, float *__restrict__ splats,
+                                            uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
+                                            uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err) {
   if (f.degenerate) atomicOr(err, 1);
   float4 *o = reinterpret_cast<float4 *>(splats + 12 * i);
   int nt = 0;
