@@ -76,10 +76,27 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     // ---- accumulators over views (dS symmetric: 6 unique entries)
     float gp[3] = {0.f, 0.f, 0.f}, dS6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float da_sum = 0.f, dc_sum[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f}, m2d[2] = {0.f, 0.f};
+    // the next view's visibility and partials are loaded while this view is processed
+    float dn9[9];
+    bool vis_n = vb.visible[0][i] != 0;
+    if (vis_n) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[0] + 9 * i + k);
+    }
     for (int v = 0; v < vb.nviews; ++v) {
-      if (!vb.visible[v][i]) continue;  // non-visible: every partial is zero (rasterizer.py:376-379)
+      const bool vis_v = vis_n;
+      float d[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) d[k] = dn9[k];
+      if (v + 1 < vb.nviews) {
+        vis_n = vb.visible[v + 1][i] != 0;
+        if (vis_n) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[v + 1] + 9 * i + k);
+        }
+      }
+      if (!vis_v) continue;  // non-visible: every partial is zero (rasterizer.py:376-379)
       const tgs_camera &cam = vb.cam[v];
-      const float *d = vb.dsplats[v] + 9 * i;
       const float dm0 = d[0], dm1 = d[1], g00 = d[2], g01 = d[3], g11 = d[4], da = d[5];
       const float dcol[3] = {d[6], d[7], d[8]};
       da_sum += da;
