@@ -35,8 +35,13 @@ struct ViewBatch {
 template <int DEG, bool kAcc>
 __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
                                                                     tgs_grads g) {
-  __shared__ __align__(16) float rest_s[kPreBlock * 45];
-  __shared__ __align__(16) float drest_s[kPreBlock * 45];
+  // dynamic shared memory: sh_rest stage, drest stage, and per view the view
+  // direction and clamped colour upstream for the SH-rest gradient
+  // sum_v basis(dir_v) (x) dcolor_v, accumulated in registers after the view loop
+  extern __shared__ __align__(16) float pb_smem[];
+  float *rest_s = pb_smem;
+  float *drest_s = pb_smem + kPreBlock * 45;
+  float(*vd_s)[6][kPreBlock] = reinterpret_cast<float(*)[6][kPreBlock]>(pb_smem + 2 * kPreBlock * 45);
   constexpr int K = (DEG + 1) * (DEG + 1) - 1;
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
@@ -95,7 +100,13 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
           for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[v + 1] + 9 * i + k);
         }
       }
-      if (!vis_v) continue;  // non-visible: every partial is zero (rasterizer.py:376-379)
+      if (!vis_v) {  // non-visible: every partial is zero (rasterizer.py:376-379)
+        if (rest_grads) {
+#pragma unroll
+          for (int k = 0; k < 6; ++k) vd_s[v][k][threadIdx.x] = k == 2 ? 1.0f : 0.0f;  // finite dir, zero colour
+        }
+        continue;
+      }
       const tgs_camera &cam = vb.cam[v];
       const float dm0 = d[0], dm1 = d[1], g00 = d[2], g01 = d[3], g11 = d[4], da = d[5];
       const float dcol[3] = {d[6], d[7], d[8]};
@@ -122,6 +133,13 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
           dcolor[c] = pre > 0.0f ? dcol[c] : 0.0f;
           dc_sum[c] += dcolor[c];
         }
+        if (rest_grads) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            vd_s[v][k][threadIdx.x] = dir[k];
+            vd_s[v][3 + k][threadIdx.x] = dcolor[k];
+          }
+        }
         if (DEG > 0) {
           float wk[15];
 #pragma unroll
@@ -129,17 +147,8 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
             wk[k] = 0.0f;
             if (k < K) {
               const float mb = band[band_of(k)];
-              float pc = 0.0f;
 #pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                wk[k] += my_rest[3 * k + c] * mb * dcolor[c];
-                if (rest_grads) {
-                  const float dmk = bsh[k] * dcolor[c];
-                  pc += dmk * my_rest[3 * k + c];
-                  my_drest[3 * k + c] += dmk * mb;
-                }
-              }
-              if (rest_grads) d_band[band_of(k)] += pc;
+              for (int c = 0; c < 3; ++c) wk[k] += my_rest[3 * k + c] * mb * dcolor[c];
             }
           }
           float d_dirs[3];
@@ -207,6 +216,33 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
         dt2 += -(dm0 * fx * t[0] + dm1 * fy * t[1]) * itz2;
 #pragma unroll
         for (int j = 0; j < 3; ++j) gp[j] += dt0 * cam.R[j] + dt1 * cam.R[3 + j] + dt2 * cam.R[6 + j];
+      }
+    }
+    // ---- SH-rest gradient: drest[k][c] = sum_v basis_k(dir_v) dcolor_v[c] (sh.py:202-214),
+    // band-mask upstream d_band[l] = sum_{k in band l, c} drest[k][c] rest[k][c]
+    if (rest_grads) {
+      float dr[45];
+#pragma unroll
+      for (int k = 0; k < 45; ++k) dr[k] = 0.0f;
+      for (int v = 0; v < vb.nviews; ++v) {
+        float bsh[15];
+        sh_basis_rest(vd_s[v][0][threadIdx.x], vd_s[v][1][threadIdx.x], vd_s[v][2][threadIdx.x], bsh);
+        const float c0 = vd_s[v][3][threadIdx.x], c1 = vd_s[v][4][threadIdx.x], c2 = vd_s[v][5][threadIdx.x];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          dr[3 * k] += bsh[k] * c0;
+          dr[3 * k + 1] += bsh[k] * c1;
+          dr[3 * k + 2] += bsh[k] * c2;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float mb = band[band_of(k)];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          d_band[band_of(k)] += dr[3 * k + c] * my_rest[3 * k + c];
+          my_drest[3 * k + c] = dr[3 * k + c] * mb;
+        }
       }
     }
     // ---- view-independent state again (recomputed rather than kept live across the loop)
@@ -337,12 +373,21 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
 
 using namespace tgs;
 
+constexpr int kPbSmem = (2 * kPreBlock * 45 + kMaxViews * 6 * kPreBlock) * (int)sizeof(float);
+
 static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const tgs_settings *s, tgs_grads *grads,
                             bool accumulate, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
   switch (s->active_sh_degree * 2 + (accumulate ? 1 : 0)) {
-#define TGS_BWD(D, A) \
-  case D * 2 + A: k_preprocess_bwd_views<D, A><<<grid, kPreBlock, 0, st>>>(*cloud, vb, *s, *grads); break;
+#define TGS_BWD(D, A)                                                                                          \
+  case D * 2 + A: {                                                                                            \
+    static bool attr = false; /* idempotent function attribute, set once per instance */                       \
+    if (!attr) {                                                                                               \
+      cudaFuncSetAttribute(k_preprocess_bwd_views<D, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPbSmem); \
+      attr = true;                                                                                             \
+    }                                                                                                          \
+    k_preprocess_bwd_views<D, A><<<grid, kPreBlock, kPbSmem, st>>>(*cloud, vb, *s, *grads);                    \
+  } break;
     TGS_BWD(0, 0) TGS_BWD(0, 1) TGS_BWD(1, 0) TGS_BWD(1, 1) TGS_BWD(2, 0) TGS_BWD(2, 1) TGS_BWD(3, 0) TGS_BWD(3, 1)
 #undef TGS_BWD
   }
