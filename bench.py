@@ -559,22 +559,37 @@ def render_c4(args):
     st = RenderSettings(near=0.2, tile_size=16)
     frames = sc.cameras
 
+    fstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+
     def frame(k):
         cam = frames[k % len(frames)]
         if world > 1:
             return parallel.render_sharded(cloud, cam, st)
-        return render_forward(cloud, cam, st).image
+        # single GPU: consecutive frames alternate between two streams (the binning of one
+        # frame overlaps the blending of the previous one)
+        with torch.cuda.stream(fstreams[k % 2]):
+            return render_forward(cloud, cam, st).image
+
+    def join():
+        main = torch.cuda.current_stream(dev)
+        for fs in fstreams:
+            main.wait_stream(fs)
 
     for k in range(args.warmup):
         frame(k)
+    join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        main = torch.cuda.current_stream(dev)
         s.record()
+        for fs in fstreams:
+            fs.wait_stream(main)
         for k in range(args.steps):
             frame(args.warmup + k)
+        join()
         e.record()
         torch.cuda.synchronize()
     if world > 1:
