@@ -162,13 +162,12 @@ LIMITER = {"blend_bwd": "FP32/ALU instruction issue (ncu: issue slots busy 72%, 
            "blend_fwd": "FP32/ALU instruction issue (ncu: issue slots busy 73%)"}
 
 
-def ncu_traffic(stage):
-    """DRAM bytes per launch of the stage's kernel from the committed ncu --set full capture."""
+def ncu_stage(stage):
+    """The stage's entry in the committed ncu --set full capture (profiles/r01_ncu_traffic.json)."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
-        return t.get(stage, {}).get("dram_bytes_per_launch")
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json"))).get(stage, {})
     except (OSError, ValueError):
-        return None
+        return {}
 
 
 def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: str) -> tuple[dict, dict]:
@@ -184,11 +183,15 @@ def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: 
                      "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
     dom = max((k for k in stages if "achieved_gbs" in stages[k]), key=lambda k: stages[k]["ms_total"])
     d = stages[dom]
+    nc = ncu_stage(dom)
     rf = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": peak, "unit": "GB/s",
-          "frac": d["frac"], "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+          "frac": d["frac"], "traffic": nc.get("dram_bytes_per_launch"), "peak_source": peak_kind,
           "algorithmic_bytes": sbytes[dom]}
     if dom in LIMITER:
+        # the stage's real roof: instruction issue (ncu issue-slot utilisation, same capture)
         rf["limiter"] = LIMITER[dom]
+        if nc.get("issue_busy_pct") is not None:
+            rf["issue_frac"] = round(nc["issue_busy_pct"] / 100.0, 3)
     return rf, stages
 
 

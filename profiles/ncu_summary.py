@@ -61,7 +61,7 @@ def main(reps):
     lines = ["ncu --set full --clock-control none (one c3 view via profile_step.py; the per-step kernels via",
              "profile_train.py, 8 views).  Cold-cache, serialised replays: compare shares, not absolute times.", "",
              f"{'kernel':34s} {'us':>8s} {'DRAM MB':>9s} {'TB/s':>6s} {'issue%':>7s} {'occ%':>6s} {'fma%':>6s} {'regs':>5s}"]
-    per_stage = defaultdict(lambda: {"dram_bytes_per_launch": 0.0, "time_us": 0.0, "kernels": []})
+    per_stage = defaultdict(lambda: {"dram_bytes_per_launch": 0.0, "time_us": 0.0, "kernels": [], "issue_w": 0.0})
     for r in recs:
         mb = ((r["dram_read"] or 0) + (r["dram_write"] or 0)) / 1e6
         tbs = mb / 1e6 / (r["time_us"] * 1e-6) if r["time_us"] else 0
@@ -73,7 +73,9 @@ def main(reps):
             per_stage[st]["dram_bytes_per_launch"] += mb * 1e6
             per_stage[st]["time_us"] += r["time_us"]
             per_stage[st]["kernels"].append(r["kernel"])
+            per_stage[st]["issue_w"] += (r["issue_busy_pct"] or 0.0) * r["time_us"]
     json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"]), "time_us": round(v["time_us"], 1),
+                   "issue_busy_pct": round(v["issue_w"] / max(v["time_us"], 1e-9), 1),
                    "kernels": v["kernels"]} for k, v in per_stage.items()},
               open("profiles/r01_ncu_traffic.json", "w"), indent=1)
     open("profiles/r01_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
