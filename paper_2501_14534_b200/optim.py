@@ -41,19 +41,17 @@ class Adam:
 
     def step(self, cloud: GaussianCloud, grads, names=PARAM_FIELDS, lambda_m: float = 0.0,
              lambda_sh: float = 0.0) -> None:
-        """Update `names`; with all groups, one fused launch.  lambda_m / lambda_sh add the
-        mask penalties of total_loss (masking.py:60-67) to the mask-logit gradients first."""
-        if tuple(names) != tuple(PARAM_FIELDS):
-            if lambda_m or lambda_sh:
-                raise ValueError("mask penalties need the fused all-group step")
-            for f in names:
-                self.update(cloud, grads, f)
-            return
+        """Update the groups `names` in ONE fused launch (tgs_adam_step_groups).  lambda_m /
+        lambda_sh add the mask penalties of total_loss (masking.py:60-67) to the
+        mask-logit gradients first (when those groups are among `names`)."""
         import ctypes
         from .loss import SH_BAND_WEIGHTS
-        k = len(PARAM_FIELDS)
+        names = sorted(set(names), key=lambda f: cloud.field_range(f)[0])  # layout order
+        k = len(names)
+        if k == 0:
+            return
         offs, sizes, lrs, b1s, b2s, kinds = [], [], [], [], [], []
-        for f in PARAM_FIELDS:
+        for f in names:
             off, size = cloud.field_range(f)
             goff, _ = grads.field_range(f)
             if goff != off:

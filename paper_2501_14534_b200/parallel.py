@@ -126,3 +126,26 @@ def render_sharded(cloud, cam, settings, group=None):
 def allreduce_grads(flat: torch.Tensor, group=None) -> None:
     """Sum the flat CloudGrads buffer over ranks (one NCCL all-reduce)."""
     dist.all_reduce(flat, group=group)
+
+
+def grad_buckets(layout: dict, rest_grads: bool = True) -> list[tuple[tuple[str, ...], int, int]]:
+    """Contiguous ranges [start, end) of the flat gradient buffer to all-reduce, with the
+    parameter groups each one completes, in the order they should be reduced.
+
+    The SH-rest bucket (45 of 63 floats per Gaussian) goes first so that its Adam
+    update overlaps the reduction of the small buckets; on steps without higher-band
+    gradients (compute_sh_rest_grads=False, 15 of 16 steps with the SH cadence) the
+    sh_rest and sh_mask_logits gradients are exactly zero on every rank and are not
+    reduced at all (15 instead of 63 floats per Gaussian).
+    mean2d_screen (densification statistics) is never reduced per step."""
+    end = lambda f: layout[f][0] + layout[f][1]  # noqa: E731
+    geo = ("positions", "log_scales", "rotations", "opacity_logits", "sh_dc")
+    out = []
+    if rest_grads:
+        out.append((("sh_rest",), layout["sh_rest"][0], end("sh_rest")))
+    out.append((geo, layout["positions"][0], end("sh_dc")))
+    # sh_mask_logits is optimised every step (its penalty gradient), but its rendering
+    # gradient is zero without higher-band gradients: only mask_logits needs reducing then
+    out.append((("mask_logits", "sh_mask_logits"), layout["mask_logits"][0],
+                end("sh_mask_logits" if rest_grads else "mask_logits")))
+    return out

@@ -21,7 +21,7 @@ from __future__ import annotations
 import torch
 
 from . import loss as loss_mod
-from .cloud import CloudGrads, GaussianCloud
+from .cloud import PARAM_FIELDS, CloudGrads, GaussianCloud
 from .optim import Adam
 from .profiler import stage
 from .rasterizer import (RenderSettings, blend_backward, preprocess_backward_views, preprocess_views,
@@ -57,6 +57,7 @@ class Trainer:
         # >= 2 streams pipeline consecutive views; 1 stream serialises them (per-kernel timing)
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
+        self.comm_stream = None  # data-parallel gradient reduction (created on first use)
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
 
@@ -126,12 +127,37 @@ class Trainer:
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
                                   accumulate=False)
-        if self.pg is not None:
-            import torch.distributed as dist
-            with stage("allreduce"):
-                dist.all_reduce(g.flat, group=self.pg)
+        # training.py:321-329: sh_rest is optimised only on steps with higher-band gradients
+        # and a non-zero active degree; every other group every step
+        upd = set(PARAM_FIELDS)
+        if not (self.settings.compute_sh_rest_grads and self.settings.active_sh_degree > 0):
+            upd.discard("sh_rest")
+        if self.pg is None:
+            with stage("adam"):
+                # the mask penalties of total_loss (masking.py:60-67) enter the gradient inside
+                # the fused Adam launch
+                self.opt.step(self.cloud, g, names=tuple(upd), lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
+            return self.terms
+        # data parallel: the gradient buckets are all-reduced on a communication stream in
+        # order, and each bucket's Adam update (identical on every rank, mask penalties
+        # included) starts as soon as its reduction is done, overlapping the next ones
+        import torch.distributed as dist
+        from .parallel import grad_buckets
+        if self.comm_stream is None:
+            self.comm_stream = torch.cuda.Stream(device=self.cloud.device)
+        buckets = grad_buckets(g._layout_map, rest_grads=bool(self.settings.compute_sh_rest_grads))
+        self.comm_stream.wait_stream(main)
+        done = []
+        with stage("allreduce"), torch.cuda.stream(self.comm_stream):
+            for _, a0, a1 in buckets:
+                dist.all_reduce(g.flat[a0:a1], group=self.pg)
+                ev = torch.cuda.Event()
+                ev.record(self.comm_stream)
+                done.append(ev)
         with stage("adam"):
-            # the mask penalties of total_loss (masking.py:60-67) enter the reduced gradient
-            # inside the fused Adam launch (identically on every rank)
-            self.opt.step(self.cloud, g, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
+            for (fields, _, _), ev in zip(buckets, done):
+                main.wait_event(ev)
+                names = tuple(f for f in fields if f in upd)
+                if names:
+                    self.opt.step(self.cloud, g, names=names, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
         return self.terms

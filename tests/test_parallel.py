@@ -98,3 +98,61 @@ def test_gloo_world2_sharded_render_and_dp_grads():
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] for r in res), res
     assert all(r[2] for r in res), res
+
+
+def test_grad_buckets_cover_the_parameter_groups():
+    from paper_2501_14534_b200.cloud import PARAM_FIELDS, _layout
+    fields = PARAM_FIELDS + ("mean2d_screen",)
+    lay, _ = _layout(fields, 1000)
+    for rest in (True, False):
+        b = parallel.grad_buckets(lay, rest_grads=rest)
+        groups = [f for fs, _, _ in b for f in fs]
+        assert sorted(groups) == sorted(f for f in PARAM_FIELDS if rest or f != "sh_rest")
+        for fs, a0, a1 in b:  # each range covers what it must reduce, nothing of mean2d_screen
+            assert a1 <= lay["mean2d_screen"][0]
+            for f in fs:
+                o, n = lay[f]
+                if f == "sh_mask_logits" and not rest:
+                    assert o >= a1  # zero on such steps: not reduced
+                else:
+                    assert a0 <= o and o + n <= a1
+        if rest:
+            assert b[0][0] == ("sh_rest",)  # the big bucket first: its Adam overlaps the rest
+
+
+def _bucket_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_14534_b200.cloud import PARAM_FIELDS, _layout
+        lay, total = _layout(PARAM_FIELDS + ("mean2d_screen",), 500)
+        ok = []
+        for rest in (True, False):
+            g = torch.from_numpy(np.random.default_rng(rank).standard_normal(total))
+            if not rest:  # zero on every rank without higher-band gradients
+                for f in ("sh_rest", "sh_mask_logits"):
+                    o, n = lay[f]
+                    g[o:o + n] = 0
+            full = g.clone()
+            dist.all_reduce(full)
+            for _, a0, a1 in parallel.grad_buckets(lay, rest_grads=rest):
+                dist.all_reduce(g[a0:a1])
+            for f in PARAM_FIELDS:  # every field (not the alignment padding between them)
+                o, n = lay[f]
+                ok.append(torch.allclose(g[o:o + n], full[o:o + n], rtol=1e-12, atol=1e-12))
+        q.put((rank, all(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_bucketed_allreduce_equals_full():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1] and all(r[1] for r in res), res
