@@ -230,6 +230,43 @@ __device__ __forceinline__ float warp_reduce8_transpose(const float v[8], int la
   return k1;
 }
 
+// Two visits at once: u[0..7] = visit 0's fields 0-7, u[8..15] = visit 1's.  Four
+// transposing levels (16 -> 1 value per lane) and one plain level leave lane l
+// holding the warp sum of value index l >> 1, i.e. visit l >> 4, field (l >> 1) & 7.
+__device__ __forceinline__ float warp_reduce16_transpose(const float u[16], int lane) {
+  float k8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool b = lane & 16;
+    k8[i] = (b ? u[8 + i] : u[i]) + __shfl_xor_sync(0xffffffffu, b ? u[i] : u[8 + i], 16);
+  }
+  float k4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool b = lane & 8;
+    k4[i] = (b ? k8[4 + i] : k8[i]) + __shfl_xor_sync(0xffffffffu, b ? k8[i] : k8[4 + i], 8);
+  }
+  float k2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool b = lane & 4;
+    k2[i] = (b ? k4[2 + i] : k4[i]) + __shfl_xor_sync(0xffffffffu, b ? k4[i] : k4[2 + i], 4);
+  }
+  const bool b = lane & 2;
+  float k1 = (b ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, b ? k2[0] : k2[1], 2);
+  k1 += __shfl_xor_sync(0xffffffffu, k1, 1);
+  return k1;
+}
+
+// The two visits' 9th fields: lane l ends with the warp sum of visit l >> 4's.
+__device__ __forceinline__ float warp_reduce2_transpose(float n0, float n1, int lane) {
+  const bool b = lane & 16;
+  float k = (b ? n1 : n0) + __shfl_xor_sync(0xffffffffu, b ? n0 : n1, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  return k;
+}
+
 // Backward batch: 128 splats at 16x16 tiles; each warp owns a private slice of
 // the per-splat accumulators (plain stores, no shared-memory float atomics,
 // which sm_100 emulates with a CAS loop), summed over warps at the flush.
@@ -770,24 +807,48 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
     fetch_splat(nx, splats, ids, start + lo - 32 + lane, lo - 32 + lane >= 0);
+    // surviving splats back to front, two per reduction (the second one, if any,
+    // follows the first in each pixel's walk, so the per-pixel order is unchanged)
     while (mask) {
-      const int bit = 31 - __clz(mask);
-      mask &= ~(1u << bit);
-      const float2 m = S.xy[bit];
-      const float4 q = S.q[bit], cn = S.conic[bit], col = S.col[bit];
-      float v[9];
+      float v0[9], v1[9];
 #pragma unroll
-      for (int f = 0; f < 9; ++f) v[f] = 0.0f;
-      const bool hA = bwd_entry(A, lo + bit, fpx, fyA, m, q, cn, col, v);
-      const bool hB = bwd_entry(B, lo + bit, fpx, fyB, m, q, cn, col, v);
-      if (__any_sync(0xffffffffu, hA || hB)) {
-        const float r8 = warp_reduce8_transpose(v, lane);
-        float r9 = v[8];
+      for (int f = 0; f < 9; ++f) v0[f] = v1[f] = 0.0f;
+      const int b0 = 31 - __clz(mask);
+      mask &= ~(1u << b0);
+      bool hit;
+      {
+        const float2 m = S.xy[b0];
+        const float4 q = S.q[b0], cn = S.conic[b0], col = S.col[b0];
+        const bool hA = bwd_entry(A, lo + b0, fpx, fyA, m, q, cn, col, v0);
+        const bool hB = bwd_entry(B, lo + b0, fpx, fyB, m, q, cn, col, v0);
+        hit = hA || hB;
+      }
+      int id1 = -1;
+      if (mask) {  // warp-uniform
+        const int b1 = 31 - __clz(mask);
+        mask &= ~(1u << b1);
+        const float2 m = S.xy[b1];
+        const float4 q = S.q[b1], cn = S.conic[b1], col = S.col[b1];
+        const bool hA = bwd_entry(A, lo + b1, fpx, fyA, m, q, cn, col, v1);
+        const bool hB = bwd_entry(B, lo + b1, fpx, fyB, m, q, cn, col, v1);
+        hit = hit || hA || hB;
+        id1 = S.id[b1];
+      }
+      if (__any_sync(0xffffffffu, hit)) {
+        float u[16];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r9 += __shfl_xor_sync(0xffffffffu, r9, o);
-        float *d = dsplats + 9 * (int64_t)S.id[bit];
-        if ((lane & 3) == 0 && r8 != 0.0f) atomicAdd(d + (lane >> 2), r8);
-        if (lane == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
+        for (int f = 0; f < 8; ++f) {
+          u[f] = v0[f];
+          u[8 + f] = v1[f];
+        }
+        const float r = warp_reduce16_transpose(u, lane);
+        const float r9 = warp_reduce2_transpose(v0[8], v1[8], lane);
+        const int id = (lane & 16) ? id1 : S.id[b0];
+        if (id >= 0) {
+          float *d = dsplats + 9 * (int64_t)id;
+          if ((lane & 1) == 0 && r != 0.0f) atomicAdd(d + ((lane >> 1) & 7), r);
+          if ((lane & 15) == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
+        }
       }
     }
     __syncwarp();

@@ -27,6 +27,8 @@ namespace tgs {
 constexpr int kR = 5;              // window radius (11 taps)
 constexpr int kT = 32;             // output tile edge
 constexpr int kH = kT + 2 * kR;    // 42: tile + halo
+constexpr int kHS = 45;            // shared row stride of halo-wide rows (== 1 mod 4: a warp's 4 rows
+                                   // x 8 column groups fall on distinct banks)
 constexpr int kLossThreads = 256;
 constexpr int kHOut = 4;           // horizontal outputs per work item
 constexpr int kVOut = 4;           // vertical outputs per work item
@@ -97,8 +99,9 @@ __device__ __forceinline__ void block_sum2(double l1, double ss, double *dst0, d
 // index, so the three CTAs of a tile run together and share the interleaved
 // image lines (and halos) in L2.
 __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
-  __shared__ float sa[kH * kH], sb[kH * kH];
-  __shared__ float hs[5][kH][kT];  // horizontal window sums on the tile columns, halo rows
+  __shared__ float sa[kH * kHS], sb[kH * kHS];
+  __shared__ float hs[5][kH][kT + 1];  // horizontal window sums on the tile columns, halo rows
+                                      // (row stride 33: the 4 rows a warp stores hit distinct banks)
   const int c = blockIdx.x;
   const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int W = A.W, H = A.H;
@@ -123,8 +126,9 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
     for (int i = 0; i < kIt; ++i) {
       const int e = t + i * kLossThreads;
       if (e < kH * kH) {
-        sa[e] = va[i];
-        sb[e] = vb[i];
+        const int r = e / kH, q = e - r * kH;
+        sa[r * kHS + q] = va[i];
+        sb[r * kHS + q] = vb[i];
       }
     }
   }
@@ -135,8 +139,8 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
     float av[kHOut + 2 * kR], bv[kHOut + 2 * kR], aa[kHOut + 2 * kR], bb[kHOut + 2 * kR], ab[kHOut + 2 * kR];
 #pragma unroll
     for (int j = 0; j < kHOut + 2 * kR; ++j) {  // products once per input, not once per tap
-      av[j] = sa[r * kH + q0 + j];
-      bv[j] = sb[r * kH + q0 + j];
+      av[j] = sa[r * kHS + q0 + j];
+      bv[j] = sb[r * kHS + q0 + j];
       aa[j] = av[j] * av[j];
       bb[j] = bv[j] * bv[j];
       ab[j] = av[j] * bv[j];
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
       pc[plane + p] = -smap * rB2;
       pc[2 * plane + p] = 2.0f * A1 * rden;
       ss += smap;
-      l1 += fabsf(sa[(r0 + o + kR) * kH + q + kR] - sb[(r0 + o + kR) * kH + q + kR]);
+      l1 += fabsf(sa[(r0 + o + kR) * kHS + q + kR] - sb[(r0 + o + kR) * kHS + q + kR]);
     }
   }
   const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
 
 __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
   __shared__ float sd[3][kH][kH];  // partials on the tile + halo, zero outside the image
-  __shared__ float se[3][kT][kH];  // vertical adjoint on the tile rows, halo columns
+  __shared__ float se[3][kT][kHS];  // vertical adjoint on the tile rows, halo columns
   const int c = blockIdx.x;
   const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int mx = x0 - kR, my = y0 - kR;  // image coords of sd[.][0][0]
