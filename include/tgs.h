@@ -25,6 +25,9 @@
  *   tgs_adam_step            optim.Adam.update (optim.py:37-49)
  *   tgs_gather_rows          cloud.take / Adam.compact row compaction
  *                            (cloud.py:86-89, optim.py:51-55)
+ *   tgs_significance_scores  significance.significance_scores (significance.py:45-78)
+ *   tgs_significance_keep    significance.prune_by_significance's row selection
+ *                            (significance.py:81-99)
  *
  * Conventions (all entry points):
  *   - every pointer is DEVICE memory owned by the caller, row-major, float32
@@ -117,6 +120,13 @@ typedef struct {
   int64_t n;
 } tgs_cloud;
 
+typedef struct { /* densification statistics (training.py:333-338; TrainState.reset_stats,
+                  * training.py:126-130); any pointer may be NULL */
+  float *grad_accum;   /* (n,) += ||mean2d_screen * (W/2, H/2)|| per view the row is visible in */
+  int32_t *grad_count; /* (n,) += 1 per view the row is visible in */
+  float *area_max;     /* (n,) = max(area_max, screen_areas) over the views */
+} tgs_densify_stats;
+
 typedef struct { /* CloudGrads (cloud.py:110-126) */
   float *positions, *log_scales, *rotations, *opacity_logits;
   float *sh_dc, *sh_rest, *mask_logits, *sh_mask_logits;
@@ -139,11 +149,13 @@ TGS_API int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam
 /* A batch of views in ONE pass over the parameters (the sh_rest block staged
  * once): per view v the same outputs as tgs_preprocess_forward into splats[v],
  * visible[v], tiles_touched[v], depth_keys[v] (may be NULL), bit-identical to a
- * single-view call with cams[v]. */
+ * single-view call with cams[v].  stats (may be NULL): area_max is updated with
+ * the views' screen areas (the other two fields are the backward's). */
 TGS_API int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                          int32_t nviews, float *const *splats, uint8_t *const *visible,
                                          int32_t *const *tiles_touched, uint64_t *const *depth_keys,
-                                         int32_t *error_flag, tgs_stream_t stream);
+                                         int32_t *error_flag, const tgs_densify_stats *stats,
+                                         tgs_stream_t stream);
 
 /* tiles_touched for arbitrary projected records (the bin_tiles(...) entry,
  * rasterizer.py:95-128): only splat fields means2d and radius are read. */
@@ -231,11 +243,13 @@ TGS_API int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *ca
 /* Multi-view form: sums the gradients of `nviews` views (cams[v], visible[v],
  * dsplats[v]; host arrays of device pointers) in one pass over the parameters —
  * the chains after the screen-space partials are linear, so view-independent
- * work (covariance/quaternion/scale/opacity/mask) runs once per Gaussian. */
+ * work (covariance/quaternion/scale/opacity/mask) runs once per Gaussian.
+ * stats (may be NULL): grad_accum / grad_count take every view's screen-space
+ * mean gradient norm (the densification statistics of each view's step). */
 TGS_API int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                           const uint8_t *const *visible, const float *const *dsplats,
                                           int32_t nviews, tgs_grads *grads, int32_t accumulate,
-                                          tgs_stream_t stream);
+                                          const tgs_densify_stats *stats, tgs_stream_t stream);
 
 /* ---- (6) loss: (1-lambda)*L1 + lambda*(1-SSIM)/2, 11x11 sigma 1.5 window,
  * symmetric padding (training.py:76-89, metrics.py:138-188).  image/target
@@ -277,6 +291,23 @@ TGS_API int tgs_gaussian_blur(const float *in, int32_t h, int32_t w, int32_t siz
  * rows of `row_floats` floats. */
 TGS_API int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,
                     int32_t row_floats, tgs_stream_t stream);
+
+/* Significance (significance.py:45-99).  Workspace: one u64 key per row + a
+ * small selection state.  tgs_significance_scores writes, for every row,
+ *   volumes = 4/3 pi prod(e^log_scales * M), M = mask_logit > mask_logit_min,
+ *   v_norm  = min(volumes / V90, 1) ** volume_power   (V90 > 0; else volumes > 0),
+ *   scores  = hits * sigmoid(opacity_logit) * M * v_norm,
+ * V90 = the rank90-th smallest volume (0-based; the caller passes the reference's
+ * nearest rank max(ceil(0.9 n) - 1, 0), significance.py:65).
+ * tgs_significance_keep sets keep[i] = 1 for every row except the k lowest by
+ * (score, row) — np.lexsort((arange(n), scores))[:k] (significance.py:97-98);
+ * 0 <= k < n.  Both run without host synchronisation; n < 2^32. */
+TGS_API int tgs_significance_workspace(int64_t n, size_t *bytes);
+TGS_API int tgs_significance_scores(const tgs_cloud *cloud, const int64_t *hits, float mask_logit_min,
+                                    float volume_power, int64_t rank90, float *volumes, float *v_norm,
+                                    float *scores, void *workspace, size_t workspace_bytes, tgs_stream_t stream);
+TGS_API int tgs_significance_keep(const float *scores, int64_t n, int64_t k, uint8_t *keep, void *workspace,
+                                  size_t workspace_bytes, tgs_stream_t stream);
 
 #ifdef __cplusplus
 }

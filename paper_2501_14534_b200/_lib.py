@@ -18,6 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libtgs.so")
 
 _P = ctypes.c_void_p
+_SZ = ctypes.c_size_t
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _F = ctypes.c_float
@@ -44,6 +45,10 @@ class TgsCloud(ctypes.Structure):
     _fields_ = [(f, _P) for f in CLOUD_FIELDS] + [("n", _I64)]
 
 
+class TgsDensifyStats(ctypes.Structure):
+    _fields_ = [("grad_accum", _P), ("grad_count", _P), ("area_max", _P)]
+
+
 class TgsGrads(ctypes.Structure):
     _fields_ = [(f, _P) for f in GRAD_FIELDS]
 
@@ -51,7 +56,7 @@ class TgsGrads(ctypes.Structure):
 _SIGS = {
     "tgs_version": ([], _I32),
     "tgs_preprocess_forward": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
-    "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
     "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P], _I32),
@@ -65,13 +70,16 @@ _SIGS = {
                                          _I32),
     "tgs_blend_backward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P], _I32),
     "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
-    "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P], _I32),
+    "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P, _P], _I32),
     "tgs_loss_workspace": ([_I32, _I32, _P], _I32),
     "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
     "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),
     "tgs_adam_step_groups": ([_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _P, _I64, _P],
                              _I32),
     "tgs_gather_rows": ([_P, _P, _P, _I64, _I32, _P], _I32),
+    "tgs_significance_workspace": ([_I64, _P], _I32),
+    "tgs_significance_scores": ([_P, _P, _F, _F, _I64, _P, _P, _P, _P, _SZ, _P], _I32),
+    "tgs_significance_keep": ([_P, _I64, _I64, _P, _P, _SZ, _P], _I32),
     "tgs_area_resize": ([_P, _I32, _I32, _P, _I32, _I32, _P, _P], _I32),
     "tgs_gaussian_blur": ([_P, _I32, _I32, _I32, _F, _P, _P, _P], _I32),
 }

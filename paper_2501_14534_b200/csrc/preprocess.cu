@@ -177,6 +177,7 @@ struct FwdViews {
   uint8_t *visible[kMaxFwdViews];
   int32_t *tiles[kMaxFwdViews];
   uint64_t *depth_keys[kMaxFwdViews];
+  float *area_max;  // densification statistic (may be NULL)
   int nviews;
 };
 
@@ -192,11 +193,15 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl
   const int64_t i = base + threadIdx.x;
   GaussFwd f0;
   gauss_static(cl, i, s, f0);  // view-independent half once
+  float amax = -1.0f;
   for (int v = 0; v < fv.nviews; ++v) {
     GaussFwd f = f0;
     gauss_view<DEG>(cl, i, fv.cam[v], s, rest_s + 45 * threadIdx.x, f);
     emit_record(cl, i, fv.cam[v], s, f, fv.splats[v], fv.visible[v], fv.tiles[v], fv.depth_keys[v], err);
+    if (f.visible) amax = fmaxf(amax, f.area);
   }
+  // np.maximum(area_max, screen_areas) (training.py:338): culled rows have area 0
+  if (fv.area_max && amax > fv.area_max[i]) fv.area_max[i] = amax;
 }
 
 // One Gaussian, one view: the projected record, visibility, tile count and depth key.
@@ -279,7 +284,8 @@ extern "C" int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *
 extern "C" int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                             int32_t nviews, float *const *splats, uint8_t *const *visible,
                                             int32_t *const *tiles_touched, uint64_t *const *depth_keys,
-                                            int32_t *error_flag, tgs_stream_t stream) {
+                                            int32_t *error_flag, const tgs_densify_stats *stats,
+                                            tgs_stream_t stream) {
   if (!cloud || !cams || !s || cloud->n < 0 || nviews < 1 || !splats || !visible || !tiles_touched)
     return TGS_ERR_INVALID;
   if (s->tile_size < 1 || s->tile_size > 32) return TGS_ERR_UNSUPPORTED;
@@ -300,6 +306,7 @@ extern "C" int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_ca
       fv.tiles[k] = tiles_touched[v0 + k];
       fv.depth_keys[k] = depth_keys ? depth_keys[v0 + k] : nullptr;
     }
+    fv.area_max = stats ? stats->area_max : nullptr;
     switch (s->active_sh_degree) {
 #define TGS_FWDV(D) \
   case D: k_preprocess_fwd_views<D><<<grid, kPreBlock, 0, st>>>(*cloud, fv, *s, error_flag); break;

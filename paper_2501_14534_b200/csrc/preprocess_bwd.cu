@@ -29,6 +29,8 @@ struct ViewBatch {
   tgs_camera cam[kMaxViews];
   const uint8_t *visible[kMaxViews];
   const float *dsplats[kMaxViews];
+  float *grad_accum;    // densification statistics (may be NULL)
+  int32_t *grad_count;
   int nviews;
 };
 
@@ -81,6 +83,8 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     // ---- accumulators over views (dS symmetric: 6 unique entries)
     float gp[3] = {0.f, 0.f, 0.f}, dS6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float da_sum = 0.f, dc_sum[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f}, m2d[2] = {0.f, 0.f};
+    float st_norm = 0.f;  // densification statistics over this batch's views
+    int st_count = 0;
     // the next view's visibility and partials are loaded while this view is processed
     float dn9[9];
     bool vis_n = vb.visible[0][i] != 0;
@@ -113,6 +117,11 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
       da_sum += da;
       m2d[0] += dm0;
       m2d[1] += dm1;
+      if (vb.grad_accum) {  // ||mean2d_screen * (w/2, h/2)|| (training.py:334-337)
+        const float sx = dm0 * (0.5f * (float)cam.width), sy = dm1 * (0.5f * (float)cam.height);
+        st_norm += sqrtf(sx * sx + sy * sy);
+        ++st_count;
+      }
       // view direction + SH colour backward (sh.py:164-215)
       {
         const float e0 = px - cam.center[0], e1 = py - cam.center[1], e2 = pz - cam.center[2];
@@ -359,6 +368,10 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
       g.mean2d_screen[2 * i] = o_m2d[0];
       g.mean2d_screen[2 * i + 1] = o_m2d[1];
     }
+    if (st_count) {
+      vb.grad_accum[i] += st_norm;
+      vb.grad_count[i] += st_count;
+    }
   }
   // ---- sh_rest gradients: coalesced (read-modify-)write of the smem block
   if (rest_grads || !kAcc) {
@@ -397,13 +410,13 @@ static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const t
 extern "C" int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                                        const uint8_t *visible, const float *dsplats, tgs_grads *grads,
                                        int32_t accumulate, tgs_stream_t stream) {
-  return tgs_preprocess_backward_views(cloud, cam, s, &visible, &dsplats, 1, grads, accumulate, stream);
+  return tgs_preprocess_backward_views(cloud, cam, s, &visible, &dsplats, 1, grads, accumulate, nullptr, stream);
 }
 
 extern "C" int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                              const uint8_t *const *visible, const float *const *dsplats,
                                              int32_t nviews, tgs_grads *grads, int32_t accumulate,
-                                             tgs_stream_t stream) {
+                                             const tgs_densify_stats *stats, tgs_stream_t stream) {
   if (!cloud || !cams || !s || !grads || !visible || !dsplats || cloud->n < 0 || nviews < 1) return TGS_ERR_INVALID;
   if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
   if (cloud->n == 0) return TGS_OK;
@@ -416,6 +429,8 @@ extern "C" int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_c
       vb.visible[k] = visible[v0 + k];
       vb.dsplats[k] = dsplats[v0 + k];
     }
+    vb.grad_accum = stats && stats->grad_count ? stats->grad_accum : nullptr;
+    vb.grad_count = vb.grad_accum ? stats->grad_count : nullptr;
     const int rc = launch_bwd_views(cloud, vb, s, grads, accumulate || v0 > 0, st);
     if (rc != TGS_OK) return rc;
   }

@@ -198,10 +198,11 @@ def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
     return splats, vis, tiles, keys, err
 
 
-def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings) -> list:
+def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, stats=None) -> list:
     """tgs_preprocess_forward_views: the per-view preprocess outputs of a batch of views in
     one pass over the parameters; element v is what `preprocess(cloud, cams[v], settings)`
-    returns (bit-identical), the error flag shared."""
+    returns (bit-identical), the error flag shared.  stats: optional train.DensifyStats
+    (its area_max takes the views' screen areas, training.py:338)."""
     import ctypes
     n = len(cloud)
     dev = cloud.device
@@ -218,8 +219,10 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings)
         c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
         arr = lambda k: (ctypes.c_void_p * V)(*[o[k].data_ptr() for o in outs])  # noqa: E731
         with stage("preprocess_fwd"):
+            c_stats = stats.native() if stats is not None else None
             _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0),
-                      arr(1), arr(2), arr(3), _lib.ptr(err), _lib.stream_handle(dev))
+                      arr(1), arr(2), arr(3), _lib.ptr(err), ctypes.byref(c_stats) if c_stats else None,
+                      _lib.stream_handle(dev))
     return outs
 
 
@@ -331,9 +334,11 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
 
 
 def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, visibles: list,
-                              dsplats: list, grads: CloudGrads, accumulate: bool = False) -> CloudGrads:
+                              dsplats: list, grads: CloudGrads, accumulate: bool = False, stats=None) -> CloudGrads:
     """Second half of render_backward for a batch of views in ONE pass over the
-    parameters (tgs_preprocess_backward_views): grads (+)= sum over views."""
+    parameters (tgs_preprocess_backward_views): grads (+)= sum over views.  stats:
+    optional train.DensifyStats, accumulating each view's screen-space gradient norm
+    (training.py:333-337)."""
     import ctypes
     n = len(cloud)
     if n == 0 or not cams:
@@ -344,9 +349,11 @@ def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: Render
     ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() for d in dsplats])
     c_set = _lib.make_settings(settings)
     c_cloud, c_grads = cloud.native(), grads.native()
+    c_stats = stats.native() if stats is not None else None
     with stage("preprocess_bwd"):
         _lib.call("tgs_preprocess_backward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), vis_ptrs,
-                  ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)), _lib.stream_handle(cloud.device))
+                  ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)),
+                  ctypes.byref(c_stats) if c_stats else None, _lib.stream_handle(cloud.device))
     return grads
 
 

@@ -18,6 +18,8 @@ scheduled events).
 
 from __future__ import annotations
 
+import math
+
 import torch
 
 from . import loss as loss_mod
@@ -32,10 +34,49 @@ DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opac
                "sh_dc": 2.5e-3, "sh_rest": 2.5e-3 / 20.0, "mask_logits": 0.5, "sh_mask_logits": 0.05}
 
 
+class DensifyStats:
+    """Densification statistics (TrainState.grad_accum / grad_count / area_max,
+    training.py:116-135, updated per view at training.py:333-338): the sum of the
+    per-view screen-space mean-gradient norms ||mean2d_screen * (W/2, H/2)||, the number
+    of views each Gaussian was visible in, and its largest screen area.  Accumulated
+    inside the multi-view preprocess kernels; float32 / int32 device tensors."""
+
+    def __init__(self, n: int, device):
+        self.grad_accum = torch.zeros(n, dtype=torch.float32, device=device)
+        self.grad_count = torch.zeros(n, dtype=torch.int32, device=device)
+        self.area_max = torch.zeros(n, dtype=torch.float32, device=device)
+
+    def reset(self) -> None:  # TrainState.reset_stats (training.py:126-130)
+        self.grad_accum.zero_()
+        self.grad_count.zero_()
+        self.area_max.zero_()
+
+    def compact(self, keep: torch.Tensor) -> None:
+        """TrainState.compact_stats (training.py:132-135) with the gather kernel."""
+        from . import _lib
+        k = keep.to(torch.int64).contiguous()
+        st = _lib.stream_handle(self.grad_accum.device)
+        for name in ("grad_accum", "grad_count", "area_max"):
+            src = getattr(self, name)
+            dst = torch.empty(k.numel(), dtype=src.dtype, device=src.device)
+            _lib.call("tgs_gather_rows", _lib.ptr(src), _lib.ptr(dst), _lib.ptr(k), int(k.numel()), 1, st)
+            setattr(self, name, dst)
+
+    def mean_grad(self) -> torch.Tensor:
+        """training.py:199: grad_accum / max(grad_count, 1), 0 where never visible."""
+        return torch.where(self.grad_count > 0, self.grad_accum / self.grad_count.clamp_min(1).float(),
+                           torch.zeros_like(self.grad_accum))
+
+    def native(self):
+        from . import _lib
+        return _lib.TgsDensifyStats(self.grad_accum.data_ptr(), self.grad_count.data_ptr(),
+                                    self.area_max.data_ptr())
+
+
 class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
-                 views=None, streams: int = 2, deterministic: bool = False):
+                 views=None, streams: int = 2, deterministic: bool = False, densify_stats: bool = False):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -60,6 +101,8 @@ class Trainer:
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
+        # per-view densification statistics, accumulated inside the preprocess kernels
+        self.stats = DensifyStats(len(cloud), dev) if densify_stats else None
 
     def prune(self, eps: float) -> int:
         """Mask-based pruning between steps (masking.py:70-81, training.py:340-346): keep
@@ -68,12 +111,32 @@ class Trainer:
         new Gaussian count."""
         from . import pruning
         new, keep = pruning.prune_by_mask(self.cloud, eps)
-        if new is not self.cloud:
-            pruning.compact_adam(self.opt, self.cloud, new, keep)
-            self.cloud = new
-            self.grads = CloudGrads(len(new), new.device)
-            self.dsplats = {}
+        self._apply_keep(new, keep)
         return len(self.cloud)
+
+    def significance_prune(self, cameras, settings, rate: float, volume_power: float = 0.5):
+        """A significance event (training.py:369-401): hits over `cameras`, scores
+        (significance.py:45-78), drop the floor(rate N) lowest (significance.py:81-99)
+        and compact the optimizer state and statistics.  Returns the report."""
+        from . import significance as sig
+        hits = sig.count_hits(self.cloud, cameras, settings)
+        rep = sig.significance_scores(hits, self.cloud, mask_threshold=settings.mask_threshold,
+                                      volume_power=volume_power)
+        if int(math.floor(rate * len(self.cloud))) > 0:
+            new, keep = sig.prune_by_significance(self.cloud, rep.scores, rate)
+            self._apply_keep(new, keep)
+        return rep
+
+    def _apply_keep(self, new: GaussianCloud, keep: torch.Tensor) -> None:
+        from . import pruning
+        if new is self.cloud:
+            return
+        pruning.compact_adam(self.opt, self.cloud, new, keep)
+        self.cloud = new
+        self.grads = CloudGrads(len(new), new.device)
+        self.dsplats = {}
+        if self.stats is not None:
+            self.stats.compact(keep)
 
     def step(self, host_targets=None) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms.
@@ -94,7 +157,7 @@ class Trainer:
                     ev.record(self.copy_stream)
                     copied[v] = ev
         # every view's preprocess in one pass over the parameters (main stream)
-        pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings)
+        pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, stats=self.stats)
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         for i, v in enumerate(self.views):
@@ -126,7 +189,7 @@ class Trainer:
             main.wait_stream(self.copy_stream)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
-                                  accumulate=False)
+                                  accumulate=False, stats=self.stats)
         # training.py:321-329: sh_rest is optimised only on steps with higher-band gradients
         # and a non-zero active degree; every other group every step
         upd = set(PARAM_FIELDS)

@@ -280,7 +280,43 @@ def schedule_and_images():
     print("schedule: ok")
 
 
+def significance_golden():
+    """Significance scoring and pruning (significance.py:31-104): hits over several
+    views, volumes, the nearest-rank 90th-percentile normaliser, scores, the pruned
+    set for a rate, the event schedule; plus the v90 == 0 branch (most rows masked)."""
+    from slimsplat.significance import count_hits, prune_by_significance, prune_schedule, significance_scores
+    rng = np.random.default_rng(4242)
+    d = {}
+    for tag, n, mask_mean in (("a", 700, 2.0), ("z", 300, -6.0)):
+        fields = scenes.random_fields(rng, n, ls_mean=-2.6, ls_std=0.5)
+        if tag == "z":  # all but ~5% of the rows masked off -> v90 == 0
+            m = np.full(n, mask_mean)
+            m[rng.choice(n, n // 20, replace=False)] = 3.0
+            fields["mask_logits"] = m
+        cloud = cloud_from(fields)
+        cams = [scenes.pinhole(3.2 * scenes._unit(rng), 64, 48) for _ in range(3)]
+        rcams = [ref_camera(c.fx, c.fy, c.cx, c.cy, c.R, c.t, c.width, c.height) for c in cams]
+        st = RenderSettings(near=0.2, mask_threshold=0.3)
+        hits = count_hits(cloud, rcams, st)
+        rep = significance_scores(hits, cloud, mask_threshold=0.3, volume_power=0.5)
+        _, keep = prune_by_significance(cloud, rep.scores, 0.35)
+        d.update({f"{tag}_in_{f}": getattr(cloud, f).astype(np.float32) for f in FIELDS})
+        d[f"{tag}_cam_intr"] = np.array([[c.fx, c.fy, c.cx, c.cy] for c in cams])
+        d[f"{tag}_cam_R"] = np.stack([c.R for c in cams])
+        d[f"{tag}_cam_t"] = np.stack([c.t for c in cams])
+        d[f"{tag}_cam_size"] = np.array([[c.width, c.height] for c in cams])
+        d.update({f"{tag}_hits": hits, f"{tag}_volumes": rep.volumes, f"{tag}_v_norm": rep.v_norm,
+                  f"{tag}_scores": rep.scores, f"{tag}_keep": keep})
+        print(f"significance {tag}: n={n} hits>0={int((hits > 0).sum())} kept={keep.size}")
+    d["schedule"] = np.array([[k, prune_schedule(k, 0.6, 0.5)] for k in range(5)])
+    d["mask_threshold"], d["volume_power"], d["rate"] = 0.3, 0.5, 0.35
+    np.savez_compressed(os.path.join(HERE, "significance.npz"), **d)
+
+
 if __name__ == "__main__":
     if len(sys.argv) == 1:
         main()
-    schedule_and_images()
+    if len(sys.argv) == 1 or "schedule" in sys.argv:
+        schedule_and_images()
+    if len(sys.argv) == 1 or "significance" in sys.argv:
+        significance_golden()

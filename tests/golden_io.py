@@ -46,3 +46,24 @@ def load(name: str):
         sh_mask_threshold=float(z["set_shmask"]), compute_sh_rest_grads=bool(int(z["set_rest"])),
     )
     return SimpleNamespace(name=name, fields=fields, cam=cam, settings=settings, z=z)
+
+
+def load_significance():
+    """tests/golden/significance.npz: two scenes ("a": regular, "z": v90 == 0) with
+    three cameras each, the reference's hits / volumes / v_norm / scores / kept rows."""
+    z = dict(np.load(os.path.join(GOLDEN, "significance.npz")))
+    out = {}
+    for tag in ("a", "z"):
+        fields = {f: z[f"{tag}_in_{f}"] for f in FIELDS}
+        cams = []
+        for k in range(z[f"{tag}_cam_intr"].shape[0]):
+            fx, fy, cx, cy = (float(v) for v in z[f"{tag}_cam_intr"][k])
+            w, h = (int(v) for v in z[f"{tag}_cam_size"][k])
+            cams.append(Camera(fx=fx, fy=fy, cx=cx, cy=cy, R=z[f"{tag}_cam_R"][k], t=z[f"{tag}_cam_t"][k],
+                               width=w, height=h))
+        settings = SimpleNamespace(lowpass_s=0.3, active_sh_degree=3, background=(0.0, 0.0, 0.0), tile_size=16,
+                                   near=0.2, record_hits=True, mask_threshold=float(z["mask_threshold"]),
+                                   sh_mask_threshold=0.1, compute_sh_rest_grads=True)
+        out[tag] = SimpleNamespace(fields=fields, cams=cams, settings=settings,
+                                   **{k: z[f"{tag}_{k}"] for k in ("hits", "volumes", "v_norm", "scores", "keep")})
+    return out, z

@@ -584,3 +584,113 @@ def test_multiview_preprocess_bitwise_equals_single_view(tgs):
             for a, b in zip(got[:4], want[:4]):
                 assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a,
                                    b.view(torch.int32) if b.dtype == torch.float32 else b)
+
+
+def test_significance_vs_reference_golden(tgs):
+    """significance.py:31-99 on the CUDA path against the reference's own outputs
+    (tests/golden/significance.npz) and the oracle restatement."""
+    from oracle import significance_ref as sig_ref
+    from paper_2501_14534_b200 import significance as sig
+    cases, z = golden_io.load_significance()
+    for tag, c in cases.items():
+        cloud = tgs.GaussianCloud.from_fields(c.fields)
+        st = _settings(tgs, c.settings)
+        hits = sig.count_hits(cloud, c.cams, st)
+        ref32 = sig_ref.count_hits(c.fields, c.cams, c.settings)  # float64 oracle == golden (pinned on CPU)
+        assert np.array_equal(_np(hits), c.hits), tag
+        assert np.array_equal(ref32, c.hits)
+        rep = sig.significance_scores(hits, cloud, mask_threshold=float(z["mask_threshold"]),
+                                      volume_power=float(z["volume_power"]))
+        vol, vn, sc = _np(rep.volumes), _np(rep.v_norm), _np(rep.scores)
+        np.testing.assert_allclose(vol, c.volumes, rtol=2e-6, atol=0)
+        np.testing.assert_allclose(vn, c.v_norm, rtol=2e-6, atol=0)
+        np.testing.assert_allclose(sc, c.scores, rtol=4e-6, atol=0)
+        # V90 is exactly the nearest-rank order statistic of the device volumes, and
+        # v_norm follows from it in float32 (IEEE division and square root)
+        v90 = np.sort(vol)[sig_ref.rank90(vol.size)]
+        want = np.sqrt(np.minimum(vol / v90, np.float32(1))) if v90 > 0 else (vol > 0).astype(np.float32)
+        assert np.array_equal(vn, want.astype(np.float32)), tag
+        # the kept rows: exactly the reference's lexsort rule applied to these scores,
+        # and the reference's own set
+        _, keep = sig.prune_by_significance(cloud, rep.scores, float(z["rate"]))
+        assert np.array_equal(_np(keep), sig_ref.prune_keep(sc, float(z["rate"]))), tag
+        assert np.array_equal(_np(keep), c.keep), tag
+
+
+def test_significance_selection_ties_and_edges(tgs):
+    """Radix selection at 1M rows with heavy ties (lexsort tie break by index),
+    all-equal scores, k == 0, n == 1, and the reference's error conditions."""
+    from oracle import significance_ref as sig_ref
+    from paper_2501_14534_b200 import significance as sig
+    rng = np.random.default_rng(5)
+    for n, levels, rate in ((1_000_000, 37, 0.3), (100_003, 2, 0.5), (4097, 1, 0.9), (10, 1000, 0.05)):
+        s = (rng.integers(0, levels, n) * 0.25).astype(np.float32)
+        got = _np(sig.prune_keep_indices(torch.from_numpy(s).cuda(), rate))
+        assert np.array_equal(got, sig_ref.prune_keep(s, rate)), (n, levels, rate)
+    s = rng.random(1_000_000, dtype=np.float32) * 1e-3  # distinct values, tiny magnitudes
+    assert np.array_equal(_np(sig.prune_keep_indices(torch.from_numpy(s).cuda(), 0.77)), sig_ref.prune_keep(s, 0.77))
+    one = torch.ones(1, device="cuda")
+    assert _np(sig.prune_keep_indices(one, 0.5)).tolist() == [0]  # floor(0.5) == 0: nothing pruned
+    with pytest.raises(tgs.ContractViolationError):
+        sig.prune_keep_indices(one, 1.0)
+    with pytest.raises(tgs.ContractViolationError):
+        sig.prune_schedule(-1, 0.6, 0.5)
+    with pytest.raises(tgs.ContractViolationError):
+        sig.count_hits(tgs.GaussianCloud.from_fields(golden_io.load("fd16").fields), [], tgs.RenderSettings())
+    empty = tgs.GaussianCloud.from_fields({k: v[:0] for k, v in golden_io.load("fd16").fields.items()})
+    with pytest.raises(tgs.EmptySceneError):
+        sig.significance_scores(torch.zeros(0, dtype=torch.int64), empty)
+
+
+def test_trainer_densify_stats_and_significance_event(tgs):
+    """Densification statistics (training.py:333-338) accumulated inside the
+    multi-view preprocess kernels equal the per-view formula on the step's own
+    partials; pruning compacts them with the cloud; a significance event
+    (training.py:369-401) prunes floor(rate N) rows."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.rasterizer import preprocess_views
+    from paper_2501_14534_b200.train import Trainer
+    sc = scenes.small_scene(seed=31, n=3000, width=96, height=64, dist=3.5)
+    rng = np.random.default_rng(31)
+    cams = [sc.cameras[0]] + [scenes.pinhole(3.5 * scenes._unit(rng), 80 + 16 * k, 64, name=f"v{k}")
+                              for k in range(2)]
+    st = tgs.RenderSettings(near=0.2, mask_threshold=0.05, sh_mask_threshold=0.1)
+    sc.fields["mask_logits"][:200] = -6.0  # masked rows: never visible, count stays 0
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    targets = [torch.rand((c.height, c.width, 3), device="cuda") for c in cams]
+    tr = Trainer(cloud, cams, targets, st, densify_stats=True)
+    before = tgs.GaussianCloud.from_fields(sc.fields)
+    pres = preprocess_views(before, cams, st)
+    tr.step()
+    torch.cuda.synchronize()
+    acc = np.zeros(len(cloud), np.float64)
+    cnt = np.zeros(len(cloud), np.int64)
+    amax = np.zeros(len(cloud), np.float32)
+    for v, cam in enumerate(cams):
+        vis = _np(pres[v][1]).astype(bool)
+        ds = _np(tr.dsplats[v])
+        norm = np.sqrt((ds[:, 0] * (cam.width / 2.0)) ** 2 + (ds[:, 1] * (cam.height / 2.0)) ** 2)
+        acc[vis] += norm[vis]
+        cnt[vis] += 1
+        amax = np.maximum(amax, np.where(vis, _np(pres[v][0])[:, 11], 0.0).astype(np.float32))
+    assert cnt.max() == len(cams) and (cnt == 0).any()
+    assert np.array_equal(_np(tr.stats.grad_count), cnt)
+    assert np.array_equal(_np(tr.stats.area_max), amax)
+    np.testing.assert_allclose(_np(tr.stats.grad_accum), acc, rtol=1e-5, atol=1e-9)
+    mg = _np(tr.stats.mean_grad())
+    np.testing.assert_allclose(mg, np.where(cnt > 0, acc / np.maximum(cnt, 1), 0.0), rtol=1e-5, atol=1e-9)
+    # mask pruning compacts the statistics with the cloud
+    old = (_np(tr.stats.grad_accum), _np(tr.stats.grad_count), _np(tr.stats.area_max))
+    keep = np.flatnonzero(_np(tr.cloud.mask_logits) > 0.0)
+    tr.prune(0.5)  # sigmoid(m) > 0.5 <=> m > 0
+    assert len(tr.cloud) == keep.size < len(cloud)
+    for got, ref in zip((tr.stats.grad_accum, tr.stats.grad_count, tr.stats.area_max), old):
+        assert np.array_equal(_np(got), ref[keep])
+    n0 = len(tr.cloud)
+    tr.step()  # the compacted state steps
+    rep = tr.significance_prune(cams, st, rate=0.25)
+    assert rep.scores.numel() == n0 and len(tr.cloud) == n0 - int(np.floor(0.25 * n0))
+    assert tr.stats.grad_count.numel() == len(tr.cloud)
+    tr.step()
+    torch.cuda.synchronize()
+    assert np.isfinite(_np(tr.terms)).all()

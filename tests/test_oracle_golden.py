@@ -122,3 +122,24 @@ def test_loss_restatement_matches_reference():
     l1, dssim, d = loss_ref.total_loss_image(z["image"], z["target"], float(z["lambda_ssim"]))
     assert abs(l1 - float(z["l1"])) < 1e-12 and abs(dssim - float(z["d_ssim"])) < 1e-12
     np.testing.assert_allclose(d, z["dimage"], rtol=1e-9, atol=1e-15)
+
+
+def test_significance_restatement_matches_reference():
+    """oracle/significance_ref.py against significance.py's own outputs (golden)."""
+    from oracle import significance_ref as sig
+    cases, z = golden_io.load_significance()
+    for tag, c in cases.items():
+        hits = sig.count_hits(c.fields, c.cams, c.settings)
+        assert np.array_equal(hits, c.hits), tag
+        r = sig.significance_scores(hits, c.fields, float(z["mask_threshold"]), float(z["volume_power"]))
+        np.testing.assert_allclose(r["volumes"], c.volumes, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(r["v_norm"], c.v_norm, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(r["scores"], c.scores, rtol=1e-12, atol=0)
+        assert np.array_equal(sig.prune_keep(r["scores"], float(z["rate"])), c.keep), tag
+    assert cases["z"].v_norm.max() == 1.0 and set(np.unique(cases["z"].v_norm)) <= {0.0, 1.0}  # v90 == 0 branch
+    for k, rate in z["schedule"]:
+        assert sig.prune_schedule(int(k), 0.6, 0.5) == rate
+    with pytest.raises(ValueError):
+        sig.prune_keep(np.zeros(4), 1.0)
+    with pytest.raises(ValueError):
+        sig.prune_schedule(-1, 0.6, 0.5)
