@@ -394,19 +394,13 @@ def main():
     rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
     launches = trainer_launches(prof.counts(), args.steps)
 
-    # ---- render FPS (forward only, initial scene) as a secondary number: the views of a step
-    # alternate between two streams like the training step, device-timed
-    rstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    # ---- render FPS (forward only, initial scene) as a secondary number: this rank's views
+    # through render_views (one multi-view preprocess pass, binning + blending pipelined over
+    # three streams), device-timed
+    from paper_2501_14534_b200.rasterizer import render_views
 
     def render_all():
-        main = torch.cuda.current_stream(dev)
-        for s_ in rstreams:
-            s_.wait_stream(main)
-        for i, v in enumerate(views):
-            with torch.cuda.stream(rstreams[i % 2]):
-                render_forward(cloud, sc.cameras[v], st)
-        for s_ in rstreams:
-            main.wait_stream(s_)
+        render_views(cloud, [sc.cameras[v] for v in views], st)
 
     render_all()
     fps_t = timed(args.steps, render_all)
@@ -546,7 +540,7 @@ def render_c4(args):
     import torch.distributed as dist
 
     from paper_2501_14534_b200 import GaussianCloud, RenderSettings, _lib, parallel, scenes
-    from paper_2501_14534_b200.rasterizer import render_forward
+    from paper_2501_14534_b200.rasterizer import render_views
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -562,37 +556,28 @@ def render_c4(args):
     st = RenderSettings(near=0.2, tile_size=16)
     frames = sc.cameras
 
-    fstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
-
-    def frame(k):
-        cam = frames[k % len(frames)]
+    def frames_from(k0, count):
+        """Frames k0 .. k0+count-1 of the orbit.  N > 1: each frame tile-row sharded.
+        One GPU: batches of up to 8 frames through render_views (one preprocess pass
+        per batch, binning + blending pipelined over three streams)."""
+        cams = [frames[(k0 + j) % len(frames)] for j in range(count)]
         if world > 1:
-            return parallel.render_sharded(cloud, cam, st)
-        # single GPU: consecutive frames alternate between two streams (the binning of one
-        # frame overlaps the blending of the previous one)
-        with torch.cuda.stream(fstreams[k % 2]):
-            return render_forward(cloud, cam, st).image
+            return [parallel.render_sharded(cloud, cam, st) for cam in cams]
+        out = []
+        for b in range(0, count, 8):
+            out += [o.image for o in render_views(cloud, cams[b:b + 8], st)]
+        return out
 
-    def join():
-        main = torch.cuda.current_stream(dev)
-        for fs in fstreams:
-            main.wait_stream(fs)
-
-    for k in range(args.warmup):
-        frame(k)
-    join()
+    # at least one whole batch of 8 frames untimed: the batch's buffers (sized by the
+    # per-frame instance counts) are then served from the allocator cache
+    frames_from(0, args.warmup if world > 1 else max(args.warmup, 8))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        main = torch.cuda.current_stream(dev)
         s.record()
-        for fs in fstreams:
-            fs.wait_stream(main)
-        for k in range(args.steps):
-            frame(args.warmup + k)
-        join()
+        frames_from(args.warmup, args.steps)
         e.record()
         torch.cuda.synchronize()
     if world > 1:

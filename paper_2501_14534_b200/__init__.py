@@ -10,13 +10,13 @@ from .cloud import CloudGrads, GaussianCloud
 from .errors import (ContractViolationError, DegenerateRotationError, DivergenceError, EmptySceneError,
                      NativeLibraryError, SingularCovarianceError, SlimsplatError)
 from .rasterizer import (RenderOutput, RenderSettings, TileBins, bin_tiles, render_backward, render_forward,
-                         sh_rest_update_step)
+                         render_views, sh_rest_update_step)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Camera", "CloudGrads", "GaussianCloud", "RenderOutput", "RenderSettings", "TileBins", "bin_tiles",
-    "look_at", "render_backward", "render_forward", "sh_rest_update_step", "SlimsplatError",
+    "look_at", "render_backward", "render_forward", "render_views", "sh_rest_update_step", "SlimsplatError",
     "DegenerateRotationError", "SingularCovarianceError", "ContractViolationError", "EmptySceneError",
     "DivergenceError", "NativeLibraryError",
 ]

@@ -145,10 +145,24 @@ def logit_ceil_f32(p: float) -> float:
     return float(f)
 
 
+_CAM_CACHE: dict = {}
+_SET_CACHE: dict = {}
+
+
 def make_camera(cam) -> TgsCamera:
-    v = cam.native_fields() if hasattr(cam, "native_fields") else _native_fields(cam)
-    return TgsCamera(v["fx"], v["fy"], v["cx"], v["cy"], (_F * 9)(*v["R"]), (_F * 3)(*v["t"]),
-                     (_F * 3)(*v["center"]), v["width"], v["height"], (_D * 4)(*v["depth_row"]))
+    """tgs_camera for a camera; cached on the camera's VALUES (cameras are mutable, so
+    the key is the pose and intrinsics themselves).  The struct is only read by C."""
+    key = (float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy), int(cam.width), int(cam.height),
+           np.asarray(cam.R, dtype=np.float64).tobytes(), np.asarray(cam.t, dtype=np.float64).tobytes())
+    c = _CAM_CACHE.get(key)
+    if c is None:
+        v = cam.native_fields() if hasattr(cam, "native_fields") else _native_fields(cam)
+        c = TgsCamera(v["fx"], v["fy"], v["cx"], v["cy"], (_F * 9)(*v["R"]), (_F * 3)(*v["t"]),
+                      (_F * 3)(*v["center"]), v["width"], v["height"], (_D * 4)(*v["depth_row"]))
+        if len(_CAM_CACHE) > 4096:
+            _CAM_CACHE.clear()
+        _CAM_CACHE[key] = c
+    return c
 
 
 def _native_fields(cam) -> dict:
@@ -161,6 +175,19 @@ def _native_fields(cam) -> dict:
 
 
 def make_settings(s) -> TgsSettings:
+    """tgs_settings (validated like the reference); cached on the field values."""
+    key = (s.lowpass_s, s.near, s.mask_threshold, s.sh_mask_threshold, tuple(s.background), s.active_sh_degree,
+           s.tile_size, bool(s.compute_sh_rest_grads))
+    c = _SET_CACHE.get(key)
+    if c is None:
+        c = _make_settings(s)
+        if len(_SET_CACHE) > 1024:
+            _SET_CACHE.clear()
+        _SET_CACHE[key] = c
+    return c
+
+
+def _make_settings(s) -> TgsSettings:
     if not 0.0 < s.mask_threshold < 1.0 or not 0.0 < s.sh_mask_threshold < 1.0:
         raise ContractViolationError("mask threshold must lie in (0, 1)")  # masking.py:23-24
     if s.lowpass_s < 0:

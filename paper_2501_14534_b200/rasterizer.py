@@ -27,9 +27,11 @@ Deliberate differences:
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
+
 import torch
 
 from . import _lib
@@ -116,34 +118,75 @@ def _tiles_y(cam, ts):
 
 def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
          row_begin: int, row_end: int, err: torch.Tensor | None = None,
-         depth_keys: torch.Tensor | None = None) -> TileBins:
-    """tgs_bin_gaussians + one host read of the instance count + tgs_bin_instances."""
+         depth_keys: torch.Tensor | None = None, cs=None) -> TileBins:
+    """tgs_bin_gaussians + one host read of the instance count + tgs_bin_instances
+    (cs: the current torch stream, if the caller has it)."""
     dev = splats.device
-    st = _lib.stream_handle(dev)
+    cs = cs if cs is not None else torch.cuda.current_stream(dev)
+    st = cs.cuda_stream
     tiles_x = (width + ts - 1) // ts
     tiles_y = (height + ts - 1) // ts
     nb = ctypes_size("tgs_bin_gaussians_workspace", n)
-    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
-    d_count = torch.empty(2, dtype=torch.int64, device=dev)
+    ws = _scratch("bin_g", max(nb, 16), dev, st)
+    d_count = _scratch("count", 16, dev, st).view(torch.int64)
     with stage("bin_gaussians"):
         _lib.call("tgs_bin_gaussians", _lib.ptr(splats), _lib.ptr(tiles_touched), _lib.ptr(depth_keys), n, width,
                   height, ts, row_begin, row_end, _lib.ptr(ws), _lib.ptr(d_count), st)
     if err is not None:
-        d_count[1:2].copy_(err.to(torch.int64))
-        count, flag = (int(v) for v in d_count.cpu().tolist())
-        if flag:
-            raise DegenerateRotationError("quaternion with (near-)zero norm")
-    else:
-        count = int(d_count[0].item())
+        d_count[1:2].copy_(err)
+    # the only host round trip of a render: the instance count (+ error flag), read
+    # through a pinned buffer on this stream
+    h = _pinned_count()
+    h.copy_(d_count, non_blocking=True)
+    cs.synchronize()
+    count, flag = int(h[0]), int(h[1]) if err is not None else 0
+    if flag:
+        raise DegenerateRotationError("quaternion with (near-)zero norm")
     ntiles = (row_end - row_begin) * tiles_x
-    offsets = torch.empty(ntiles + 1, dtype=torch.int32, device=dev)
-    ids = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+    offsets = _alloc(ntiles + 1, torch.int32, dev)
+    ids = _alloc(_size_class(max(count, 1)), torch.int32, dev)
     ib = ctypes_size("tgs_bin_instances_workspace", n, count, width, height, ts, row_begin, row_end)
-    ws2 = torch.empty(max(ib, 16), dtype=torch.uint8, device=dev)
+    ws2 = _scratch("bin_i", max(ib, 16), dev, st)
     with stage("bin_instances"):
         _lib.call("tgs_bin_instances", _lib.ptr(splats), n, width, height, ts, row_begin, row_end, _lib.ptr(ws),
                   count, _lib.ptr(ws2), _lib.ptr(offsets), _lib.ptr(ids), st)
     return TileBins(offsets, ids[:count], tiles_x, tiles_y, row_begin, row_end)
+
+
+_PINNED = {}
+_SCRATCH = {}
+
+
+def _scratch(tag: str, nbytes: int, dev, stream_handle: int | None = None) -> torch.Tensor:
+    """Per-stream scratch workspace, grown geometrically and reused by every later call on
+    the same stream (stream order makes the reuse safe; nothing returned references it).
+    Frame-to-frame size changes (instance counts) then cost no allocator traffic."""
+    sh = stream_handle if stream_handle is not None else torch.cuda.current_stream(dev).cuda_stream
+    key = (dev.index, sh, tag)
+    t = _SCRATCH.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(_size_class(int(nbytes * 1.25) + 4096), dtype=torch.uint8, device=dev)
+        _SCRATCH[key] = t
+    return t[:nbytes]
+
+
+def _size_class(k: int) -> int:
+    """Round an element count up to one of 8 classes per binade (<= 12.5% slack) so
+    buffers whose size follows the per-frame instance count are served from the
+    allocator's cache instead of fresh cudaMalloc calls."""
+    if k <= 1024:
+        return 1024
+    step = 1 << (k.bit_length() - 4)
+    return (k + step - 1) // step * step
+
+
+def _pinned_count() -> torch.Tensor:
+    """A pinned 2-element host buffer per host thread (the read completes before reuse)."""
+    k = threading.get_ident()
+    h = _PINNED.get(k)
+    if h is None:
+        h = _PINNED[k] = torch.empty(2, dtype=torch.int64, pin_memory=True)
+    return h
 
 
 def ctypes_size(fn: str, *args) -> int:
@@ -207,13 +250,18 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
     n = len(cloud)
     dev = cloud.device
     V = len(cams)
-    outs = []
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    for _ in range(V):
-        outs.append((torch.empty((max(n, 1), 12), dtype=torch.float32, device=dev),
-                     torch.zeros(max(n, 1), dtype=torch.uint8, device=dev),
-                     torch.zeros(max(n, 1), dtype=torch.int32, device=dev),
-                     torch.empty(max(n, 1), dtype=torch.int64, device=dev), err))
+    # one allocation per output kind for the whole batch; the kernel writes every row
+    # below n, the padding row of an empty cloud is zeroed
+    m = max(n, 1)
+    sp = torch.empty((V, m, 12), dtype=torch.float32, device=dev)
+    vis = torch.empty((V, m), dtype=torch.uint8, device=dev)
+    tiles = torch.empty((V, m), dtype=torch.int32, device=dev)
+    keys = torch.empty((V, m), dtype=torch.int64, device=dev)
+    if n == 0:
+        for t in (sp, vis, tiles, keys):
+            t.zero_()
+    outs = [(sp[v], vis[v], tiles[v], keys[v], err) for v in range(V)]
     if n and V:
         c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
         c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
@@ -223,6 +271,75 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
             _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0),
                       arr(1), arr(2), arr(3), _lib.ptr(err), ctypes.byref(c_stats) if c_stats else None,
                       _lib.stream_handle(dev))
+    return outs
+
+
+_RENDER_STREAMS = {}
+_ALLOC = threading.local()  # .stream: the pool returned tensors are allocated from (None: current)
+
+
+def _alloc(shape, dtype, dev) -> torch.Tensor:
+    """torch.empty for tensors a render RETURNS.  Inside render_views they come from the
+    caller's stream pool while the kernels writing them run on side streams: the caller's
+    stream waits for the side streams before returning, so any later reuse of that memory
+    is ordered after the writes (no record_stream, no allocator churn)."""
+    s = getattr(_ALLOC, "stream", None)
+    if s is None:
+        return torch.empty(shape, dtype=dtype, device=dev)
+    with torch.cuda.stream(s):
+        return torch.empty(shape, dtype=dtype, device=dev)
+
+
+def _alloc_many(specs, dev) -> list:
+    """Several returned tensors carved from ONE allocation (256-byte aligned typed views):
+    one allocator call, and one stream switch inside render_views, per frame."""
+    offs, total = [], 0
+    for shape, dtype in specs:
+        n = 1
+        for d in shape:
+            n *= int(d)
+        offs.append(total)
+        total += (n * dtype.itemsize + 255) // 256 * 256
+    blk = _alloc(max(total, 256), torch.uint8, dev)
+    out = []
+    for (shape, dtype), o in zip(specs, offs):
+        n = 1
+        for d in shape:
+            n *= int(d)
+        out.append(blk[o:o + n * dtype.itemsize].view(dtype).view(shape))
+    return out
+
+
+def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) -> list:
+    """Render a batch of views of one cloud (an orbit, the views of a training batch):
+    every view's preprocess in ONE pass over the parameters (tgs_preprocess_forward_views),
+    then per view binning + blending pipelined over `streams` CUDA streams, so the
+    latency-bound binning of one view (and its instance-count read-back) overlaps the
+    blending of the others.  Element v equals render_forward(cloud, cams[v], settings);
+    the outputs are ordered before later work on the caller's current stream."""
+    cloud = _as_cloud(cloud)
+    cams = list(cams)
+    if not cams:
+        return []
+    dev = cloud.device
+    main = torch.cuda.current_stream(dev)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), max(1, int(streams)))
+    pool = _RENDER_STREAMS.get(key)
+    if pool is None:
+        pool = _RENDER_STREAMS[key] = [torch.cuda.Stream(device=dev) for _ in range(key[1])]
+    pres = preprocess_views(cloud, cams, settings) if len(cloud) else [None] * len(cams)
+    for s_ in pool:
+        s_.wait_stream(main)
+    outs = []
+    _ALLOC.stream = main
+    try:
+        for i, cam in enumerate(cams):
+            with torch.cuda.stream(pool[i % len(pool)]):
+                outs.append(render_forward(cloud, cam, settings, pre=pres[i]))
+    finally:
+        _ALLOC.stream = None
+        for s_ in pool:
+            main.wait_stream(s_)
     return outs
 
 
@@ -240,13 +357,15 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     n = len(cloud)
     dev = cloud.device
     rb, re = row_band if row_band is not None else (0, _tiles_y(cam, ts))
+    cs = torch.cuda.current_stream(dev)
     splats, vis, tiles, keys, err = pre if pre is not None else preprocess(cloud, cam, settings)
-    bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys)
-    image = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
-    transmit = torch.empty((h, w), dtype=torch.float32, device=dev)
-    wsum = torch.empty((h, w), dtype=torch.float32, device=dev)
-    n_contrib = torch.empty((h, w), dtype=torch.int32, device=dev)
-    last_pos = torch.empty((h, w), dtype=torch.int32, device=dev)
+    bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys, cs)
+    specs = [((h, w, 3), torch.float32), ((h, w), torch.float32), ((h, w), torch.float32), ((h, w), torch.int32),
+             ((h, w), torch.int32), ((n,), torch.bool)]
+    if settings.record_hits:
+        specs.append(((n,), torch.int64))
+    bufs = _alloc_many(specs, dev)
+    image, transmit, wsum, n_contrib, last_pos, visible = bufs[:6]
     if row_band is not None:  # pixels outside the band are not rendered here
         for t_, v in ((image, 0.0), (transmit, 1.0), (wsum, 0.0), (n_contrib, 0), (last_pos, 0)):
             t_.fill_(v)
@@ -255,11 +374,14 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     with stage("blend_fwd"):
         _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
-                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.stream_handle(dev))
-    visible = vis[:n].bool()
+                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), cs.cuda_stream)
+    visible.copy_(vis[:n])
+    hit_counts = None
+    if hits is not None:
+        hit_counts = bufs[6]
+        hit_counts.copy_(hits[:n])
     out = RenderOutput(image=image, transmittance=transmit, weight_sum=wsum, n_contrib=n_contrib,
-                       last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11],
-                       hit_counts=hits[:n].to(torch.int64) if hits is not None else None,
+                       last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11], hit_counts=hit_counts,
                        _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins))
     if settings.record_full:
         out.hit_records = _records(out, splats, bins, cam, c_cam, c_set, dev)

@@ -694,3 +694,25 @@ def test_trainer_densify_stats_and_significance_event(tgs):
     tr.step()
     torch.cuda.synchronize()
     assert np.isfinite(_np(tr.terms)).all()
+
+
+def test_render_views_equals_render_forward(tgs):
+    """render_views (one multi-view preprocess pass, three streams) returns, view for
+    view, exactly what render_forward returns."""
+    from paper_2501_14534_b200 import scenes
+    sc = scenes.small_scene(seed=41, n=20000, width=160, height=96, dist=3.0)
+    rng = np.random.default_rng(41)
+    cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * scenes._unit(rng), 96 + 32 * (k % 3), 96, name=f"v{k}")
+                              for k in range(6)]
+    st = tgs.RenderSettings(near=0.2, record_hits=True)
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    outs = tgs.render_views(cloud, cams, st)
+    outs_again = tgs.render_views(cloud, cams, st, streams=2)
+    for cam, o, o2 in zip(cams, outs, outs_again):
+        ref = tgs.render_forward(cloud, cam, st)
+        for f in ("image", "transmittance", "weight_sum", "n_contrib", "last_pos", "visible", "screen_areas",
+                  "hit_counts"):
+            assert torch.equal(getattr(o, f), getattr(ref, f)), f
+            assert torch.equal(getattr(o2, f), getattr(ref, f)), f
+        assert torch.equal(o._tiles.indices, ref._tiles.indices) and torch.equal(o._tiles.offsets, ref._tiles.offsets)
+    assert tgs.render_views(cloud, [], st) == []
