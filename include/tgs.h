@@ -202,7 +202,7 @@ TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int
 TGS_API int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                       const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                       float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
-                      int32_t *last_pos, int32_t *hits, tgs_stream_t stream);
+                      int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream);
 
 /* Per-pixel ordered (Gaussian, blend weight) records — the reference's
  * records_kernel (_kernels.py:184-241), a test/debug payload.  pixel_offsets
@@ -217,7 +217,14 @@ TGS_API int tgs_blend_records(const float *splats, const int32_t *tile_offsets, 
 TGS_API int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                        const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                        const float *transmit, const int32_t *last_pos, const float *dimage,
-                       float *dsplats, tgs_stream_t stream);
+                       float *dsplats, const int32_t *tile_order, tgs_stream_t stream);
+
+/* Heaviest-first tile order for the blend launches (tile_order above, may be
+ * NULL = row-major): tiles sorted by floor(log2(list length)) descending, so the
+ * longest tiles start first and the tail of the launch is short tiles.
+ * `order` holds ntiles + 64 int32 (the last 64 are scratch).  Scheduling only:
+ * the blend results do not depend on it (tile_size 16 kernels use it). */
+TGS_API int tgs_tile_order(const int32_t *tile_offsets, int32_t ntiles, int32_t *order, tgs_stream_t stream);
 
 /* Deterministic variant (a deterministic-reduction mode): the
  * partials of every (tile, Gaussian) pair are summed over the tile's warps in a

@@ -682,9 +682,9 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
     const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
     float *__restrict__ transmit, float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
-    int32_t *__restrict__ last_pos, int32_t *__restrict__ hits) {
+    int32_t *__restrict__ last_pos, int32_t *__restrict__ hits, const int32_t *__restrict__ order) {
   __shared__ WStage SW[kT16Threads / 32];
-  const int tile = blockIdx.x;
+  const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   WStage &S = SW[warp];
@@ -757,9 +757,10 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
 __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, const float *__restrict__ transmit,
-    const int32_t *__restrict__ last_pos, const float *__restrict__ dimage, float *__restrict__ dsplats) {
+    const int32_t *__restrict__ last_pos, const float *__restrict__ dimage, float *__restrict__ dsplats,
+    const int32_t *__restrict__ order) {
   __shared__ WStage SW[kT16Threads / 32];
-  const int tile = blockIdx.x;
+  const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   WStage &S = SW[warp];
@@ -886,6 +887,56 @@ __global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// Heaviest-first tile order for the blend kernels (longest-processing-time-first
+// scheduling): CTAs are dispatched roughly in blockIdx order, so mapping blockIdx
+// to tiles sorted by descending list length leaves the short tiles for the tail.
+// Classes are floor(log2(length)), heaviest class first; the order inside a class
+// is arbitrary (it only affects scheduling).  order[ntiles .. ntiles+63] holds the
+// class counts and cursors.
+__device__ __forceinline__ int order_class(int32_t len) {
+  return len > 0 ? __clz(len) : 31;  // 31 - floor(log2(len)): 0 = heaviest
+}
+
+__global__ void __launch_bounds__(256) k_order_hist(const int32_t *__restrict__ offsets, int ntiles,
+                                                    uint32_t *__restrict__ cnt) {
+  __shared__ uint32_t h[32];
+  if (threadIdx.x < 32) h[threadIdx.x] = 0u;
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) atomicAdd(&h[order_class(__ldg(offsets + t + 1) - __ldg(offsets + t))], 1u);
+  __syncthreads();
+  if (threadIdx.x < 32 && h[threadIdx.x]) atomicAdd(cnt + threadIdx.x, h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_order_scatter(const int32_t *__restrict__ offsets, int ntiles,
+                                                       uint32_t *__restrict__ cnt, int32_t *__restrict__ order) {
+  __shared__ uint32_t base[32], local[32], resv[32];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x < 32) {  // class bases: exclusive scan of the global counts (heaviest first)
+    const uint32_t c = cnt[threadIdx.x];
+    uint32_t v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if ((int)threadIdx.x >= o) v += y;
+    }
+    base[threadIdx.x] = v - c;
+    local[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+  int cls = 0;
+  uint32_t r = 0;
+  if (t < ntiles) {
+    cls = order_class(__ldg(offsets + t + 1) - __ldg(offsets + t));
+    r = atomicAdd(&local[cls], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && local[threadIdx.x]) resv[threadIdx.x] = atomicAdd(cnt + 32 + threadIdx.x, local[threadIdx.x]);
+  __syncthreads();
+  if (t < ntiles) order[base[cls] + resv[cls] + r] = t;
+}
+
 inline bool blend_args(const tgs_camera *cam, const tgs_settings *s, int rb, int re, int &tiles_x, int &ntiles) {
   if (!cam || !s || s->tile_size < 1 || s->tile_size > 32) return false;
   tiles_x = (cam->width + s->tile_size - 1) / s->tile_size;
@@ -904,7 +955,7 @@ using namespace tgs;
 extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                                  const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                                  float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
-                                 int32_t *last_pos, int32_t *hits, tgs_stream_t stream) {
+                                 int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
@@ -913,7 +964,7 @@ extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offset
     k_blend_fwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
-        last_pos, hits);
+        last_pos, hits, tile_order);
     return launch_status();
   }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
@@ -942,7 +993,7 @@ extern "C" int tgs_blend_records(const float *splats, const int32_t *tile_offset
 extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
                                   const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                                   const float *transmit, const int32_t *last_pos, const float *dimage,
-                                  float *dsplats, tgs_stream_t stream) {
+                                  float *dsplats, const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
@@ -950,7 +1001,8 @@ extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offse
   if (s->tile_size == 16) {
     k_blend_bwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
-        row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats);
+        row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
+        tile_order);
     return launch_status();
   }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
@@ -1014,5 +1066,17 @@ extern "C" int tgs_blend_backward_deterministic(const float *splats, const int32
   k_det_inverse<<<ntiles, 256, 0, st>>>(splats, tile_offsets, sorted_ids, cnt, cam->width, cam->height,
                                         s->tile_size, tiles_x, tiles_y, row_begin, row_end, inv);
   k_det_reduce<<<gn, 256, 0, st>>>(cnt, inv, partial, n, num_instances, dsplats);
+  return launch_status();
+}
+
+extern "C" int tgs_tile_order(const int32_t *tile_offsets, int32_t ntiles, int32_t *order, tgs_stream_t stream) {
+  if (ntiles < 0 || !tile_offsets || !order) return TGS_ERR_INVALID;
+  if (ntiles == 0) return TGS_OK;
+  cudaStream_t st = as_stream(stream);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(order + ntiles);  // 32 counts + 32 cursors
+  cudaMemsetAsync(cnt, 0, 64 * sizeof(uint32_t), st);
+  const unsigned g = (unsigned)ceil_div<int64_t>(ntiles, 256);
+  k_order_hist<<<g, 256, 0, st>>>(tile_offsets, ntiles, cnt);
+  k_order_scatter<<<g, 256, 0, st>>>(tile_offsets, ntiles, cnt, order);
   return launch_status();
 }

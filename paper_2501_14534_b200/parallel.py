@@ -116,7 +116,8 @@ def render_sharded(cloud, cam, settings, group=None):
         with stage("blend_fwd"):
             lib.call("tgs_blend_forward", lib.ptr(splats), lib.ptr(bins.offsets), lib.ptr(bins.indices),
                      ctypes.byref(c_cam), ctypes.byref(c_set), bands_r[0], bands_r[1], lib.ptr(image),
-                     lib.ptr(transmit), lib.ptr(wsum), lib.ptr(nc), lib.ptr(lp), None, lib.stream_handle(dev))
+                     lib.ptr(transmit), lib.ptr(wsum), lib.ptr(nc), lib.ptr(lp), None, lib.ptr(bins.order),
+                     lib.stream_handle(dev))
     while len(bands) < world:
         bands.append((bands[-1][1], bands[-1][1]))
     with stage("gather"):

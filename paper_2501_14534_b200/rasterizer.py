@@ -73,6 +73,7 @@ class TileBins:
     tiles_y: int
     row_begin: int = 0
     row_end: int | None = None
+    order: torch.Tensor | None = None  # heaviest-first blend launch order (tgs_tile_order), 16-px tiles
 
 
 @dataclass
@@ -150,10 +151,38 @@ def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, 
     with stage("bin_instances"):
         _lib.call("tgs_bin_instances", _lib.ptr(splats), n, width, height, ts, row_begin, row_end, _lib.ptr(ws),
                   count, _lib.ptr(ws2), _lib.ptr(offsets), _lib.ptr(ids), st)
-    return TileBins(offsets, ids[:count], tiles_x, tiles_y, row_begin, row_end)
+        order = _blend_order(offsets, ntiles, tiles_x, row_end - row_begin, ts, dev, st)
+    return TileBins(offsets, ids[:count], tiles_x, tiles_y, row_begin, row_end, order)
 
 
 _PINNED = {}
+_CENTER = {}
+
+# Launch order of the 16x16-tile blend kernels (scheduling only: results are identical):
+#   "center": tiles by distance from the band's centre, a cached permutation per tile grid —
+#             the heavy tiles of an object-centred view start first while neighbouring tiles,
+#             which share splat records in L2, are still dispatched together (measured at
+#             c3: blend fwd 288 -> 275 us, bwd 612 -> 578 us per view, no extra launch);
+#   "lpt":    heaviest list first (tgs_tile_order, two small kernels per view), for scenes
+#             whose heavy tiles are not central;
+#   "none":   row-major.
+BLEND_ORDER = "center"
+
+
+def _blend_order(offsets, ntiles: int, tiles_x: int, rows: int, ts: int, dev, st):
+    if ts != 16 or ntiles == 0 or BLEND_ORDER == "none":
+        return None
+    if BLEND_ORDER == "lpt":
+        order = _alloc(ntiles + 64, torch.int32, dev)
+        _lib.call("tgs_tile_order", _lib.ptr(offsets), ntiles, _lib.ptr(order), st)
+        return order
+    key = (dev.index, tiles_x, rows)
+    order = _CENTER.get(key)
+    if order is None:
+        ty, tx = np.meshgrid(np.arange(rows), np.arange(tiles_x), indexing="ij")
+        d = (tx + 0.5 - tiles_x / 2.0) ** 2 + (ty + 0.5 - rows / 2.0) ** 2
+        order = _CENTER[key] = torch.from_numpy(np.argsort(d.ravel(), kind="stable").astype(np.int32)).to(dev)
+    return order
 _SCRATCH = {}
 
 
@@ -374,7 +403,8 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     with stage("blend_fwd"):
         _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
-                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), cs.cuda_stream)
+                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.ptr(bins.order),
+                  cs.cuda_stream)
     visible.copy_(vis[:n])
     hit_counts = None
     if hits is not None:
@@ -451,7 +481,7 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
         else:
             _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
                       ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
-                      _lib.ptr(d), _lib.ptr(dsplats), _lib.stream_handle(dev))
+                      _lib.ptr(d), _lib.ptr(dsplats), _lib.ptr(bins.order), _lib.stream_handle(dev))
     return dsplats, st
 
 

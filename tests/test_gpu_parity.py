@@ -716,3 +716,57 @@ def test_render_views_equals_render_forward(tgs):
             assert torch.equal(getattr(o2, f), getattr(ref, f)), f
         assert torch.equal(o._tiles.indices, ref._tiles.indices) and torch.equal(o._tiles.offsets, ref._tiles.offsets)
     assert tgs.render_views(cloud, [], st) == []
+
+
+def test_tile_order_is_a_heaviest_first_permutation_and_changes_nothing(tgs):
+    """Blend launch orders (centre-out default, heaviest-first tgs_tile_order): both
+    are permutations of the tiles, the LPT one with non-increasing
+    floor(log2(list length)); the forward blend gives the same bits under any order
+    and without one (the order only schedules CTAs)."""
+    import ctypes
+    from paper_2501_14534_b200 import _lib, scenes
+    sc = scenes.small_scene(seed=51, n=30000, width=200, height=136, dist=3.0)
+    st = tgs.RenderSettings(near=0.2)
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    cam = sc.cameras[0]
+    from paper_2501_14534_b200 import rasterizer
+    out = tgs.render_forward(cloud, cam, st)  # default launch order (centre-out)
+    bins = out._tiles
+    nt = bins.offsets.numel() - 1
+    assert np.array_equal(np.sort(_np(bins.order)), np.arange(nt))
+    prev = rasterizer.BLEND_ORDER
+    rasterizer.BLEND_ORDER = "lpt"
+    try:
+        out_lpt = tgs.render_forward(cloud, cam, st)
+    finally:
+        rasterizer.BLEND_ORDER = prev
+    for f in ("image", "transmittance", "weight_sum", "n_contrib", "last_pos"):
+        assert torch.equal(getattr(out_lpt, f), getattr(out, f))
+    order = _np(out_lpt._tiles.order[:nt])
+    assert np.array_equal(np.sort(order), np.arange(nt))
+    lens = np.diff(_np(bins.offsets))[order]
+    cls = np.floor(np.log2(np.maximum(lens, 1)))
+    assert (np.diff(cls) <= 0).all() and lens[0] == lens.max()
+    # raw ABI: same image without an order
+    h, w = cam.height, cam.width
+    bufs = [torch.empty((h, w, 3), device="cuda"), torch.empty((h, w), device="cuda"),
+            torch.empty((h, w), device="cuda"), torch.empty((h, w), dtype=torch.int32, device="cuda"),
+            torch.empty((h, w), dtype=torch.int32, device="cuda")]
+    c_cam, c_set = _lib.make_camera(cam), _lib.make_settings(st)
+    _lib.call("tgs_blend_forward", _lib.ptr(out._state.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+              ctypes.byref(c_cam), ctypes.byref(c_set), 0, bins.tiles_y, *[_lib.ptr(b) for b in bufs], None, None,
+              _lib.stream_handle())
+    for got, ref in zip(bufs, (out.image, out.transmittance, out.weight_sum, out.n_contrib, out.last_pos)):
+        assert torch.equal(got, ref)
+    # random offsets with empty tiles and a single huge tile
+    rng = np.random.default_rng(3)
+    ln = rng.integers(0, 3000, 40000).astype(np.int32)
+    ln[rng.choice(40000, 5000, replace=False)] = 0
+    ln[123] = 1 << 22
+    offs = torch.from_numpy(np.concatenate([[0], np.cumsum(ln)]).astype(np.int32)).cuda()
+    o = torch.empty(40000 + 64, dtype=torch.int32, device="cuda")
+    _lib.call("tgs_tile_order", _lib.ptr(offs), 40000, _lib.ptr(o), _lib.stream_handle())
+    oo = _np(o[:40000])
+    assert np.array_equal(np.sort(oo), np.arange(40000)) and oo[0] == 123
+    c2 = np.floor(np.log2(np.maximum(ln[oo], 1)))  # lengths 0 and 1 share the lightest class
+    assert (np.diff(c2) <= 0).all()
