@@ -178,7 +178,7 @@ def _blend_order(offsets, ntiles: int, tiles_x: int, rows: int, ts: int, dev, st
         return order
     key = (dev.index, tiles_x, rows)
     order = _CENTER.get(key)
-    if order is None:
+    if order is None:  # (2x2 / 4x4 tile blocks ordered centre-out measured slower than plain rings)
         ty, tx = np.meshgrid(np.arange(rows), np.arange(tiles_x), indexing="ij")
         d = (tx + 0.5 - tiles_x / 2.0) ** 2 + (ty + 0.5 - rows / 2.0) ** 2
         order = _CENTER[key] = torch.from_numpy(np.argsort(d.ravel(), kind="stable").astype(np.int32)).to(dev)
