@@ -185,14 +185,20 @@ template <int DEG>
 __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl, FwdViews fv, tgs_settings s,
                                                                     int32_t *__restrict__ err) {
   __shared__ __align__(16) float rest_s[kPreBlock * 45];
+  __shared__ __align__(8) uint64_t rest_bar;
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
-  if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  bool bulk = false;
+  if (DEG > 0) {
+    bulk = stage_rest_issue(cl.sh_rest, base, count, rest_s, &rest_bar);  // TMA, overlaps gauss_static
+    if (!bulk) stage_rest(cl.sh_rest, base, count, rest_s);
+  }
   __syncthreads();
   if ((int)threadIdx.x >= count) return;
   const int64_t i = base + threadIdx.x;
   GaussFwd f0;
   gauss_static(cl, i, s, f0);  // view-independent half once
+  if (bulk) stage_rest_wait(&rest_bar);
   float amax = -1.0f;
   for (int v = 0; v < fv.nviews; ++v) {
     GaussFwd f = f0;

@@ -48,7 +48,12 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
   const bool rest_grads = DEG > 0 && s.compute_sh_rest_grads;
-  if (DEG > 0) stage_rest(cl.sh_rest, base, count, rest_s);
+  __shared__ __align__(8) uint64_t rest_bar;
+  bool bulk = false;
+  if (DEG > 0) {
+    bulk = stage_rest_issue(cl.sh_rest, base, count, rest_s, &rest_bar);  // TMA, overlaps the loads below
+    if (!bulk) stage_rest(cl.sh_rest, base, count, rest_s);
+  }
   for (int j = threadIdx.x; j < kPreBlock * 45; j += kPreBlock) drest_s[j] = 0.0f;
   __syncthreads();
   const int64_t i = base + threadIdx.x;
@@ -85,24 +90,23 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     float da_sum = 0.f, dc_sum[3] = {0.f, 0.f, 0.f}, d_band[3] = {0.f, 0.f, 0.f}, m2d[2] = {0.f, 0.f};
     float st_norm = 0.f;  // densification statistics over this batch's views
     int st_count = 0;
-    // the next view's visibility and partials are loaded while this view is processed
+    // every view's visibility first (independent byte loads, one latency), then the
+    // partials one view ahead, loaded unconditionally: no load waits on another load
+    // (a non-visible row's partials are never used, rasterizer.py:376-379)
+    uint32_t vmask = 0u;
+    for (int v = 0; v < vb.nviews; ++v) vmask |= (__ldg(vb.visible[v] + i) != 0 ? 1u : 0u) << v;
     float dn9[9];
-    bool vis_n = vb.visible[0][i] != 0;
-    if (vis_n) {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[0] + 9 * i + k);
-    }
+    for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[0] + 9 * i + k);
+    if (bulk) stage_rest_wait(&rest_bar);  // the sh_rest block (TMA) is needed from here on
     for (int v = 0; v < vb.nviews; ++v) {
-      const bool vis_v = vis_n;
+      const bool vis_v = (vmask >> v) & 1u;
       float d[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) d[k] = dn9[k];
       if (v + 1 < vb.nviews) {
-        vis_n = vb.visible[v + 1][i] != 0;
-        if (vis_n) {
 #pragma unroll
-          for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[v + 1] + 9 * i + k);
-        }
+        for (int k = 0; k < 9; ++k) dn9[k] = __ldg(vb.dsplats[v + 1] + 9 * i + k);
       }
       if (!vis_v) {  // non-visible: every partial is zero (rasterizer.py:376-379)
         if (rest_grads) {

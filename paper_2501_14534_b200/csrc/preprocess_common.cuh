@@ -36,6 +36,45 @@ __device__ __forceinline__ void stage_rest(const float *__restrict__ rest, int64
   }
 }
 
+// ---- one-shot TMA bulk copy of the CTA's sh_rest block (cp.async.bulk, SASS UBLKCP):
+// thread 0 issues ONE 1-D bulk copy global -> shared completing on an mbarrier, the
+// threads load their per-Gaussian parameters meanwhile and wait on the barrier only
+// when the block is needed.  Returns false (nothing issued) when the block cannot go
+// through the bulk path (misaligned or a size that is not a multiple of 16 bytes,
+// i.e. a partial last block); the caller then uses stage_rest + __syncthreads.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ bool stage_rest_issue(const float *__restrict__ rest, int64_t base, int count, float *sm,
+                                                 uint64_t *bar) {
+  const float *src = rest + base * 45;
+  const uint32_t bytes = (uint32_t)count * 45u * 4u;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (bytes & 15) || bytes == 0) return false;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sm)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  }
+  return true;
+}
+
+// every thread: wait for the bulk copy (phase 0); the barrier must have been
+// initialised before a __syncthreads that precedes this call
+__device__ __forceinline__ void stage_rest_wait(uint64_t *bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // unit quaternion -> rotation (geometry.py:19-41); returns the raw norm
 __device__ __forceinline__ float quat_rot(const tgs_cloud &cl, int64_t i, float Rg[9], float qn[4] = nullptr) {
   const float qw = cl.rotations[4 * i], qx = cl.rotations[4 * i + 1];
