@@ -98,10 +98,17 @@ __device__ __forceinline__ void block_sum2(double l1, double ss, double *dst0, d
 // Grid (3 channels, tiles_x, tiles_y): the channel is the fastest-varying block
 // index, so the three CTAs of a tile run together and share the interleaved
 // image lines (and halos) in L2.
+__device__ __forceinline__ float2 ffma2(float w, float2 x, float2 acc) {  // packed FP32 FMA (FFMA2)
+  return __ffma2_rn(make_float2(w, w), x, acc);
+}
+
 __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
-  __shared__ float sa[kH * kHS], sb[kH * kHS];
-  __shared__ float hs[5][kH][kT + 1];  // horizontal window sums on the tile columns, halo rows
-                                      // (row stride 33: the 4 rows a warp stores hit distinct banks)
+  // The five window sums run as two packed pairs (sum a, sum b) and (sum a^2, sum b^2)
+  // plus the scalar sum ab: FFMA2 issues two FP32 FMAs per instruction with the same
+  // per-element rounding, so the maps are bit-identical to five scalar passes.
+  __shared__ float2 sab[kH * kHS];                    // (a, b) on the tile + halo
+  __shared__ float2 hab[kH][kT + 1], hsq[kH][kT + 1];  // horizontal sums: (a, b), (a^2, b^2)
+  __shared__ float hp[kH][kT + 1];                    // horizontal sums of a*b
   const int c = blockIdx.x;
   const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int W = A.W, H = A.H;
@@ -127,41 +134,37 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
       const int e = t + i * kLossThreads;
       if (e < kH * kH) {
         const int r = e / kH, q = e - r * kH;
-        sa[r * kHS + q] = va[i];
-        sb[r * kHS + q] = vb[i];
+        sab[r * kHS + q] = make_float2(va[i], vb[i]);
       }
     }
   }
   __syncthreads();
-  // horizontal: item = (halo row, 4 tile columns)
+  // horizontal: item = (halo row, 4 tile columns); consecutive lanes take consecutive
+  // rows (odd float2 row stride: conflict-free 64-bit shared accesses)
   for (int it = t; it < kH * (kT / kHOut); it += kLossThreads) {
-    const int r = it / (kT / kHOut), q0 = (it - r * (kT / kHOut)) * kHOut;
-    float av[kHOut + 2 * kR], bv[kHOut + 2 * kR], aa[kHOut + 2 * kR], bb[kHOut + 2 * kR], ab[kHOut + 2 * kR];
+    const int g = it / kH, r = it - g * kH, q0 = g * kHOut;
+    float2 x[kHOut + 2 * kR], sq[kHOut + 2 * kR];
+    float pr[kHOut + 2 * kR];
 #pragma unroll
     for (int j = 0; j < kHOut + 2 * kR; ++j) {  // products once per input, not once per tap
-      av[j] = sa[r * kHS + q0 + j];
-      bv[j] = sb[r * kHS + q0 + j];
-      aa[j] = av[j] * av[j];
-      bb[j] = bv[j] * bv[j];
-      ab[j] = av[j] * bv[j];
+      x[j] = sab[r * kHS + q0 + j];
+      sq[j] = __fmul2_rn(x[j], x[j]);
+      pr[j] = x[j].x * x[j].y;
     }
 #pragma unroll
     for (int o = 0; o < kHOut; ++o) {
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+      float s4 = 0.f;
 #pragma unroll
-      for (int j = 0; j < 2 * kR + 1; ++j) {
-        const float w = tp.w[j];
-        s0 = fmaf(w, av[o + j], s0);
-        s1 = fmaf(w, bv[o + j], s1);
-        s2 = fmaf(w, aa[o + j], s2);
-        s3 = fmaf(w, bb[o + j], s3);
-        s4 = fmaf(w, ab[o + j], s4);
+      for (int k = 0; k < 2 * kR + 1; ++k) {
+        const float w = tp.w[k];
+        s01 = ffma2(w, x[o + k], s01);
+        s23 = ffma2(w, sq[o + k], s23);
+        s4 = fmaf(w, pr[o + k], s4);
       }
-      hs[0][r][q0 + o] = s0;
-      hs[1][r][q0 + o] = s1;
-      hs[2][r][q0 + o] = s2;
-      hs[3][r][q0 + o] = s3;
-      hs[4][r][q0 + o] = s4;
+      hab[r][q0 + o] = s01;
+      hsq[r][q0 + o] = s23;
+      hp[r][q0 + o] = s4;
     }
   }
   __syncthreads();
@@ -169,18 +172,37 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   double l1 = 0.0, ss = 0.0;
   {
     const int q = t % kT, r0 = (t / kT) * kVOut;
-    float m[5][kVOut];
+    float2 m01[kVOut], m23[kVOut];
+    float m4[kVOut];
+    {
+      float2 col[kVOut + 2 * kR];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      float col[kVOut + 2 * kR];
+      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = hab[r0 + j][q];
 #pragma unroll
-      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = hs[k][r0 + j][q];
+      for (int o = 0; o < kVOut; ++o) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 2 * kR + 1; ++k) acc = ffma2(tp.w[k], col[o + k], acc);
+        m01[o] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = hsq[r0 + j][q];
+#pragma unroll
+      for (int o = 0; o < kVOut; ++o) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 2 * kR + 1; ++k) acc = ffma2(tp.w[k], col[o + k], acc);
+        m23[o] = acc;
+      }
+      float cp[kVOut + 2 * kR];
+#pragma unroll
+      for (int j = 0; j < kVOut + 2 * kR; ++j) cp[j] = hp[r0 + j][q];
 #pragma unroll
       for (int o = 0; o < kVOut; ++o) {
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
-        m[k][o] = acc;
+        for (int k = 0; k < 2 * kR + 1; ++k) acc = fmaf(tp.w[k], cp[o + k], acc);
+        m4[o] = acc;
       }
     }
     const int xx = x0 + q;
@@ -188,8 +210,8 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
     for (int o = 0; o < kVOut; ++o) {
       const int yy = y0 + r0 + o;
       if (yy >= H || xx >= W) continue;
-      const float m0 = m[0][o], m1 = m[1][o];
-      const float var_a = m[2][o] - m0 * m0, var_b = m[3][o] - m1 * m1, cov = m[4][o] - m0 * m1;
+      const float m0 = m01[o].x, m1 = m01[o].y;
+      const float var_a = m23[o].x - m0 * m0, var_b = m23[o].y - m1 * m1, cov = m4[o] - m0 * m1;
       const float A1 = 2.0f * m0 * m1 + A.c1, A2 = 2.0f * cov + A.c2;
       const float B1 = m0 * m0 + m1 * m1 + A.c1, B2 = var_a + var_b + A.c2;
       const float rB1 = 1.0f / B1, rB2 = 1.0f / B2, rden = rB1 * rB2;  // two reciprocals, no divisions
@@ -200,7 +222,8 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
       pc[plane + p] = -smap * rB2;
       pc[2 * plane + p] = 2.0f * A1 * rden;
       ss += smap;
-      l1 += fabsf(sa[(r0 + o + kR) * kHS + q + kR] - sb[(r0 + o + kR) * kHS + q + kR]);
+      const float2 ab = sab[(r0 + o + kR) * kHS + q + kR];
+      l1 += fabsf(ab.x - ab.y);
     }
   }
   const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
@@ -209,8 +232,12 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
 }
 
 __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
-  __shared__ float sd[3][kH][kH];  // partials on the tile + halo, zero outside the image
-  __shared__ float se[3][kT][kHS];  // vertical adjoint on the tile rows, halo columns
+  // partials (p0, p1) as a packed pair + p2 scalar: two FFMA2 + one FFMA per tap
+  // instead of three FFMA, bit-identical per component
+  __shared__ float2 sd01[kH][kHS];  // (p0, p1) on the tile + halo, zero outside the image
+  __shared__ float sd2[kH][kH];     // p2
+  __shared__ float2 se01[kT][kHS];  // vertical adjoint on the tile rows, halo columns
+  __shared__ float se2[kT][kHS];
   const int c = blockIdx.x;
   const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int mx = x0 - kR, my = y0 - kR;  // image coords of sd[.][0][0]
@@ -239,32 +266,44 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
       const int e = t + i * kLossThreads;
       if (e < kH * kH) {
         const int r = e / kH, q = e - r * kH;
-        sd[0][r][q] = v0[i];
-        sd[1][r][q] = v1[i];
-        sd[2][r][q] = v2[i];
+        sd01[r][q] = make_float2(v0[i], v1[i]);
+        sd2[r][q] = v2[i];
       }
     }
   }
   __syncthreads();
   // vertical adjoint: item = (halo column, 4 tile rows), symmetric taps -> correlation
+  // (the pair and the scalar in one loop: measured faster than one input window at a
+  // time despite the registers; so was the inlined lambda fold vs a strided-pointer one)
   for (int it = t; it < kH * (kT / kVOut); it += kLossThreads) {
     const int q = it % kH, r0 = (it / kH) * kVOut;
     const int xx = mx + q;
+    const bool colok = xx >= 0 && xx < W;
+    float2 col01[kVOut + 2 * kR];
+    float col2[kVOut + 2 * kR];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float col[kVOut + 2 * kR];
+    for (int j = 0; j < kVOut + 2 * kR; ++j) {
+      col01[j] = sd01[r0 + j][q];
+      col2[j] = sd2[r0 + j][q];
+    }
 #pragma unroll
-      for (int j = 0; j < kVOut + 2 * kR; ++j) col[j] = sd[k][r0 + j][q];
+    for (int o = 0; o < kVOut; ++o) {
+      float2 a01 = make_float2(0.f, 0.f);
+      float a2 = 0.f;
 #pragma unroll
-      for (int o = 0; o < kVOut; ++o) {
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], col[o + i], acc);
-        const int yy = y0 + r0 + o;
-        if (border && yy < H && (yy < kR || yy >= H - kR) && xx >= 0 && xx < W)
-          acc += adjoint_fold(yy, H, tp, [&](int j) { return sd[k][j - my][q]; });
-        se[k][r0 + o][q] = (yy < H && xx >= 0 && xx < W) ? acc : 0.0f;
+      for (int k = 0; k < 2 * kR + 1; ++k) {
+        a01 = ffma2(tp.w[k], col01[o + k], a01);
+        a2 = fmaf(tp.w[k], col2[o + k], a2);
       }
+      const int yy = y0 + r0 + o;
+      if (border && yy < H && (yy < kR || yy >= H - kR) && colok) {
+        a01.x += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q].x; });
+        a01.y += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q].y; });
+        a2 += adjoint_fold(yy, H, tp, [&](int j) { return sd2[j - my][q]; });
+      }
+      const bool ok = yy < H && colok;
+      se01[r0 + o][q] = ok ? a01 : make_float2(0.f, 0.f);
+      se2[r0 + o][q] = ok ? a2 : 0.0f;
     }
   }
   __syncthreads();
@@ -272,21 +311,33 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
   {
     const int r = t / (kT / kHOut), c0 = (t - r * (kT / kHOut)) * kHOut;
     const int yy = y0 + r;
-    float g[3][kHOut];
+    float g0[kHOut], g1[kHOut], g2[kHOut];
+    {
+      float2 row01[kHOut + 2 * kR];
+      float row2[kHOut + 2 * kR];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float row[kHOut + 2 * kR];
-#pragma unroll
-      for (int j = 0; j < kHOut + 2 * kR; ++j) row[j] = se[k][r][c0 + j];
+      for (int j = 0; j < kHOut + 2 * kR; ++j) {
+        row01[j] = se01[r][c0 + j];
+        row2[j] = se2[r][c0 + j];
+      }
 #pragma unroll
       for (int o = 0; o < kHOut; ++o) {
-        float acc = 0.f;
+        float2 a01 = make_float2(0.f, 0.f);
+        float a2 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 2 * kR + 1; ++i) acc = fmaf(tp.w[i], row[o + i], acc);
+        for (int k = 0; k < 2 * kR + 1; ++k) {
+          a01 = ffma2(tp.w[k], row01[o + k], a01);
+          a2 = fmaf(tp.w[k], row2[o + k], a2);
+        }
         const int xx = x0 + c0 + o;
-        if (border && xx < W && (xx < kR || xx >= W - kR))
-          acc += adjoint_fold(xx, W, tp, [&](int j) { return se[k][r][j - mx]; });
-        g[k][o] = acc;
+        if (border && xx < W && (xx < kR || xx >= W - kR)) {
+          a01.x += adjoint_fold(xx, W, tp, [&](int j) { return se01[r][j - mx].x; });
+          a01.y += adjoint_fold(xx, W, tp, [&](int j) { return se01[r][j - mx].y; });
+          a2 += adjoint_fold(xx, W, tp, [&](int j) { return se2[r][j - mx]; });
+        }
+        g0[o] = a01.x;
+        g1[o] = a01.y;
+        g2[o] = a2;
       }
     }
     if (yy < H) {
@@ -296,7 +347,7 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
         if (xx >= W) continue;
         const size_t p = ((size_t)yy * W + xx) * 3 + c;
         const float av = __ldg(A.img + p), bv = __ldg(A.tgt + p);
-        const float grad = (g[0][o] + 2.0f * av * g[1][o] + bv * g[2][o]) * A.inv_count;
+        const float grad = (g0[o] + 2.0f * av * g1[o] + bv * g2[o]) * A.inv_count;
         const float diff = av - bv;
         const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
         A.dimage[p] = (1.0f - A.lam) * sgn * A.inv_count - A.lam * 0.5f * grad;
