@@ -575,34 +575,51 @@ __device__ __forceinline__ float4 warp_bounds2(bool liveA, bool liveB, int px, i
   return make_float4((float)x0, (float)x1, (float)y0, (float)y1);
 }
 
-struct Fwd16Pixel {
-  float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, ws = 0.0f;
-  int contrib = 0, lastp = 0;
-  bool done;
+// The two pixels of a lane, packed: (A, B) in the .x / .y halves.  Every float
+// operation is the scalar fwd_entry's (same expression, same rounding), issued as
+// FFMA2 / FMUL2 / FADD2; a pixel that skips an entry (done, exponent out of range,
+// alpha below 1/255) gets alpha 0, which leaves T, the colour and the weight sum
+// bit-identical (all finite, colour and weights >= 0).
+struct Fwd16Pair {
+  float2 T = make_float2(1.0f, 1.0f), c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f),
+         c2 = make_float2(0.f, 0.f), ws = make_float2(0.f, 0.f);
+  int cA = 0, cB = 0, lA = 0, lB = 0;
+  bool dA, dB;
 };
 
-// one list entry for one pixel (_kernels.py:57-81)
-__device__ __forceinline__ void fwd_entry(Fwd16Pixel &P, float fpx, float fpy, float2 m, float4 q, float4 col, int pos,
-                                          int32_t *hits, int32_t gid) {
-  if (P.done) return;
-  if (P.T < kTTerm) {  // checked before each entry (_kernels.py:57-58)
-    P.done = true;
-    return;
+__device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col, int pos,
+                                           int32_t *hits, int32_t gid) {
+  // checked before each entry (_kernels.py:57-58)
+  P.dA = P.dA || P.T.x < kTTerm;
+  P.dB = P.dB || P.T.y < kTTerm;
+  const float dx = fpx - m.x;
+  const float2 dy = __fadd2_rn(fy, make_float2(-m.y, -m.y));
+  const float t1 = __fmul_rn(__fmul_rn(q.x, dx), dx);
+  const float2 s = __ffma2_rn(__fmul2_rn(make_float2(q.z, q.z), dy), dy, make_float2(t1, t1));
+  const float b = __fmul_rn(q.y, dx);
+  const float2 e2 = __ffma2_rn(make_float2(b, b), dy, s);  // exponent2() for both pixels
+  float2 al = __fmul2_rn(make_float2(q.w, q.w), make_float2(ex2_approx(e2.x), ex2_approx(e2.y)));
+  const bool okA = !P.dA && !(e2.x < kE2Min || e2.x > 0.0f) && !(al.x < kAlphaSkip);
+  const bool okB = !P.dB && !(e2.y < kE2Min || e2.y > 0.0f) && !(al.y < kAlphaSkip);
+  al = make_float2(okA ? fminf(al.x, kAlphaMax) : 0.0f, okB ? fminf(al.y, kAlphaMax) : 0.0f);
+  const float2 w = __fmul2_rn(al, P.T);
+  P.c0 = __ffma2_rn(make_float2(col.x, col.x), w, P.c0);
+  P.c1 = __ffma2_rn(make_float2(col.y, col.y), w, P.c1);
+  P.c2 = __ffma2_rn(make_float2(col.z, col.z), w, P.c2);
+  P.ws = __fadd2_rn(P.ws, w);
+  P.T = __fmul2_rn(P.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
+  if (okA) {
+    ++P.cA;
+    P.lA = pos;
   }
-  const float e2 = exponent2(q, fpx - m.x, fpy - m.y);
-  if (e2 < kE2Min || e2 > 0.0f) return;
-  float al = __fmul_rn(q.w, ex2_approx(e2));
-  if (al < kAlphaSkip) return;
-  al = fminf(al, kAlphaMax);
-  const float w = al * P.T;
-  P.c0 += col.x * w;
-  P.c1 += col.y * w;
-  P.c2 += col.z * w;
-  P.ws += w;
-  P.T = __fmul_rn(P.T, __fsub_rn(1.0f, al));
-  ++P.contrib;
-  P.lastp = pos;
-  if (hits) atomicAdd(hits + gid, 1);
+  if (okB) {
+    ++P.cB;
+    P.lB = pos;
+  }
+  if (hits) {
+    if (okA) atomicAdd(hits + gid, 1);
+    if (okB) atomicAdd(hits + gid, 1);
+  }
 }
 
 struct Bwd16Pixel {
@@ -694,16 +711,17 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
   const float4 wb = warp_bounds2(inA, inB, px, pyA, pyB);
   const int start = __ldg(offsets + tile), stop = __ldg(offsets + tile + 1);
   const float fpx = (float)px, fyA = (float)pyA, fyB = (float)pyB;
-  Fwd16Pixel A, B;
-  A.done = !inA;
-  B.done = !inB;
+  Fwd16Pair P;
+  P.dA = !inA;
+  P.dB = !inB;
+  const float2 fy = make_float2(fyA, fyB);
   SplatRegs nx;
   fetch_splat(nx, splats, ids, start + lane, start + lane < stop);
   float4 wbc = wb;
   for (int c = start; c < stop; c += 32) {
-    if (__all_sync(0xffffffffu, A.done && B.done)) break;
+    if (__all_sync(0xffffffffu, P.dA && P.dB)) break;
     // cull against the pixels that are still blending (terminated ones no longer count)
-    if (c != start) wbc = warp_bounds2(!A.done, !B.done, px, pyA, pyB);
+    if (c != start) wbc = warp_bounds2(!P.dA, !P.dB, px, pyA, pyB);
     const bool ok = c + lane < stop;
     bool keep = false;
     if (ok) {
@@ -725,32 +743,31 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
       const float2 m = S.xy[k];
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
-      fwd_entry(A, fpx, fyA, m, q, col, pos, hits, S.id[k]);
-      fwd_entry(B, fpx, fyB, m, q, col, pos, hits, S.id[k]);
+      fwd_visit2(P, fpx, fy, m, q, col, pos, hits, S.id[k]);
     }
-    if (A.T < kTTerm) A.done = true;
-    if (B.T < kTTerm) B.done = true;
+    if (P.T.x < kTTerm) P.dA = true;
+    if (P.T.y < kTTerm) P.dB = true;
     __syncwarp();
   }
   if (inA) {
     const int p = pyA * W + px;
-    image[3 * p] = A.c0 + bg0 * A.T;
-    image[3 * p + 1] = A.c1 + bg1 * A.T;
-    image[3 * p + 2] = A.c2 + bg2 * A.T;
-    transmit[p] = A.T;
-    wsum_out[p] = A.ws;
-    n_contrib[p] = A.contrib;
-    last_pos[p] = A.lastp;
+    image[3 * p] = P.c0.x + bg0 * P.T.x;
+    image[3 * p + 1] = P.c1.x + bg1 * P.T.x;
+    image[3 * p + 2] = P.c2.x + bg2 * P.T.x;
+    transmit[p] = P.T.x;
+    wsum_out[p] = P.ws.x;
+    n_contrib[p] = P.cA;
+    last_pos[p] = P.lA;
   }
   if (inB) {
     const int p = pyB * W + px;
-    image[3 * p] = B.c0 + bg0 * B.T;
-    image[3 * p + 1] = B.c1 + bg1 * B.T;
-    image[3 * p + 2] = B.c2 + bg2 * B.T;
-    transmit[p] = B.T;
-    wsum_out[p] = B.ws;
-    n_contrib[p] = B.contrib;
-    last_pos[p] = B.lastp;
+    image[3 * p] = P.c0.y + bg0 * P.T.y;
+    image[3 * p + 1] = P.c1.y + bg1 * P.T.y;
+    image[3 * p + 2] = P.c2.y + bg2 * P.T.y;
+    transmit[p] = P.T.y;
+    wsum_out[p] = P.ws.y;
+    n_contrib[p] = P.cB;
+    last_pos[p] = P.lB;
   }
 }
 
