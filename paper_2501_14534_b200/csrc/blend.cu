@@ -628,39 +628,64 @@ struct Bwd16Pixel {
   float GS = 0.f;  // sum_c g_c * S_c, S = suffix colour seeded with bg * T_final
 };
 
-// one list entry of the back-to-front walk for one pixel (_kernels.py:136-181),
-// with dL/dalpha_hat = (g . c) T_before - (g . S) / (1 - a)
-__device__ __forceinline__ bool bwd_entry(Bwd16Pixel &P, int pos, float fpx, float fpy, float2 m, float4 q,
-                                          float4 cn, float4 col, float v[9]) {
-  if (pos >= P.lastp) return false;
-  const float dx = fpx - m.x, dy = fpy - m.y;
-  const float e2 = exponent2(q, dx, dy);
-  if (e2 < kE2Min || e2 > 0.0f) return false;
-  const float gauss = ex2_approx(e2);
-  const float a_raw = __fmul_rn(cn.w, gauss);
-  const float al = fminf(a_raw, kAlphaMax);
-  if (al < kAlphaSkip) return false;
-  const float inv_om = rcp_approx(1.0f - al);  // 1 - al >= 0.01: no denormal path needed
-  const float t_before = P.T * inv_om;
-  const float gc = P.g0 * col.x + P.g1 * col.y + P.g2 * col.z;
-  const float ga = gc * t_before - P.GS * inv_om;
-  const float w = al * t_before;
-  v[6] += P.g0 * w;
-  v[7] += P.g1 * w;
-  v[8] += P.g2 * w;
-  if (a_raw <= kAlphaMax) {
-    v[5] += ga * gauss;
-    const float gG = ga * cn.w * gauss;
-    const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
-    v[0] += gG * v0;
-    v[1] += gG * v1;
-    v[2] += gG * 0.5f * v0 * v0;
-    v[3] += gG * v0 * v1;
-    v[4] += gG * 0.5f * v1 * v1;
-  }
-  P.GS += gc * w;
-  P.T = t_before;
-  return true;
+// Backward state of a lane's two pixels, packed (A, B) -> (.x, .y).
+struct Bwd16Pair {
+  int lA = 0, lB = 0;
+  float2 g0 = make_float2(0.f, 0.f), g1 = make_float2(0.f, 0.f), g2 = make_float2(0.f, 0.f);
+  float2 T = make_float2(0.f, 0.f), GS = make_float2(0.f, 0.f);
+};
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+// One list entry of the back-to-front walk (_kernels.py:136-181) for both pixels at once,
+// with dL/dalpha_hat = (g . c) T_before - (g . S) / (1 - a) (FFMA2/FMUL2/FADD2): writes the visit's 9 partials
+// v[k] = A's + B's and returns whether either pixel blended the splat.  A pixel that
+// skips the entry gets 1/(1-alpha) = 1, alpha = 0 and a zero Gaussian factor, so its
+// T and G.S are unchanged and it contributes exact zeros (the Gaussian factor is
+// masked BEFORE the products: an out-of-range exponent may give ex2 = inf).
+__device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, float2 fy, float2 m, float4 q,
+                                           float4 cn, float4 col, float v[9]) {
+  const float dx = fpx - m.x;
+  const float2 dy = __fadd2_rn(fy, f2(-m.y));
+  const float t1 = __fmul_rn(__fmul_rn(q.x, dx), dx);
+  const float2 s = __ffma2_rn(__fmul2_rn(f2(q.z), dy), dy, f2(t1));
+  const float b = __fmul_rn(q.y, dx);
+  const float2 e2 = __ffma2_rn(f2(b), dy, s);  // exponent2() for both pixels
+  const float2 gauss = make_float2(ex2_approx(e2.x), ex2_approx(e2.y));
+  const float2 a_raw = __fmul2_rn(f2(cn.w), gauss);
+  const float2 al = make_float2(fminf(a_raw.x, kAlphaMax), fminf(a_raw.y, kAlphaMax));
+  const bool okA = pos < P.lA && !(e2.x < kE2Min || e2.x > 0.0f) && !(al.x < kAlphaSkip);
+  const bool okB = pos < P.lB && !(e2.y < kE2Min || e2.y > 0.0f) && !(al.y < kAlphaSkip);
+  const float2 om = __fadd2_rn(f2(1.0f), make_float2(-al.x, -al.y));  // 1 - al >= 0.01
+  const float2 inv = make_float2(okA ? rcp_approx(om.x) : 1.0f, okB ? rcp_approx(om.y) : 1.0f);
+  const float2 tb = __fmul2_rn(P.T, inv);  // T before this entry
+  const float2 gc = __ffma2_rn(P.g2, f2(col.z), __ffma2_rn(P.g1, f2(col.y), __fmul2_rn(P.g0, f2(col.x))));
+  const float2 ga = __ffma2_rn(gc, tb, __fmul2_rn(P.GS, make_float2(-inv.x, -inv.y)));
+  const float2 w = __fmul2_rn(make_float2(okA ? al.x : 0.0f, okB ? al.y : 0.0f), tb);
+  const float2 w6 = __fmul2_rn(P.g0, w), w7 = __fmul2_rn(P.g1, w), w8 = __fmul2_rn(P.g2, w);
+  // partials through the unclamped alpha only (a_raw <= ALPHA_MAX)
+  const bool uA = okA && a_raw.x <= kAlphaMax, uB = okB && a_raw.y <= kAlphaMax;
+  const float2 gm = make_float2(uA ? gauss.x : 0.0f, uB ? gauss.y : 0.0f);
+  const float2 gam = make_float2(uA ? ga.x : 0.0f, uB ? ga.y : 0.0f);
+  const float2 v5 = __fmul2_rn(gam, gm);
+  const float2 gG = __fmul2_rn(__fmul2_rn(gam, f2(cn.w)), gm);
+  const float2 v0 = __ffma2_rn(f2(cn.y), dy, f2(cn.x * dx)), v1 = __ffma2_rn(f2(cn.z), dy, f2(cn.y * dx));
+  const float2 hG = __fmul2_rn(gG, f2(0.5f));
+  const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
+  const float2 p2 = __fmul2_rn(__fmul2_rn(hG, v0), v0), p3 = __fmul2_rn(p0, v1);
+  const float2 p4 = __fmul2_rn(__fmul2_rn(hG, v1), v1);
+  v[0] = p0.x + p0.y;
+  v[1] = p1.x + p1.y;
+  v[2] = p2.x + p2.y;
+  v[3] = p3.x + p3.y;
+  v[4] = p4.x + p4.y;
+  v[5] = v5.x + v5.y;
+  v[6] = w6.x + w6.y;
+  v[7] = w7.x + w7.y;
+  v[8] = w8.x + w8.y;
+  P.GS = __ffma2_rn(gc, w, P.GS);
+  P.T = tb;
+  return okA || okB;
 }
 
 // ---------------------------------------------------------------------------
@@ -801,6 +826,15 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
   load_pixel(B, pyB);
   const float4 wb = warp_bounds2(A.lastp > 0, B.lastp > 0, px, pyA, pyB);
   const int wlast = __reduce_max_sync(0xffffffffu, max(A.lastp, B.lastp));
+  Bwd16Pair PB;  // the two pixels packed for the per-visit arithmetic
+  PB.lA = A.lastp;
+  PB.lB = B.lastp;
+  PB.g0 = make_float2(A.g0, B.g0);
+  PB.g1 = make_float2(A.g1, B.g1);
+  PB.g2 = make_float2(A.g2, B.g2);
+  PB.T = make_float2(A.T, B.T);
+  PB.GS = make_float2(A.GS, B.GS);
+  const float2 fy = make_float2(fyA, fyB);
   SplatRegs nx;
   // back to front over chunks [lo, hi) of 32 list positions below this warp's last blend
   int hi = wlast;
@@ -810,7 +844,7 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     const bool ok = lo + lane >= 0;
     bool keep = false;
     // only pixels whose last blended position lies beyond lo can take part in this chunk
-    const float4 wbc = warp_bounds2(A.lastp > lo, B.lastp > lo, px, pyA, pyB);
+    const float4 wbc = warp_bounds2(PB.lA > lo, PB.lB > lo, px, pyA, pyB);
     if (ok) {
       const float4 q = prescaled_conic(nx.a, nx.b);
       const float thr = splat_thr2(nx.b.y);
@@ -829,28 +863,18 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     // follows the first in each pixel's walk, so the per-pixel order is unchanged)
     while (mask) {
       float v0[9], v1[9];
-#pragma unroll
-      for (int f = 0; f < 9; ++f) v0[f] = v1[f] = 0.0f;
       const int b0 = 31 - __clz(mask);
       mask &= ~(1u << b0);
-      bool hit;
-      {
-        const float2 m = S.xy[b0];
-        const float4 q = S.q[b0], cn = S.conic[b0], col = S.col[b0];
-        const bool hA = bwd_entry(A, lo + b0, fpx, fyA, m, q, cn, col, v0);
-        const bool hB = bwd_entry(B, lo + b0, fpx, fyB, m, q, cn, col, v0);
-        hit = hA || hB;
-      }
+      bool hit = bwd_visit2(PB, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], v0);
       int id1 = -1;
       if (mask) {  // warp-uniform
         const int b1 = 31 - __clz(mask);
         mask &= ~(1u << b1);
-        const float2 m = S.xy[b1];
-        const float4 q = S.q[b1], cn = S.conic[b1], col = S.col[b1];
-        const bool hA = bwd_entry(A, lo + b1, fpx, fyA, m, q, cn, col, v1);
-        const bool hB = bwd_entry(B, lo + b1, fpx, fyB, m, q, cn, col, v1);
-        hit = hit || hA || hB;
+        hit = bwd_visit2(PB, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], v1) || hit;
         id1 = S.id[b1];
+      } else {
+#pragma unroll
+        for (int f = 0; f < 9; ++f) v1[f] = 0.0f;
       }
       if (__any_sync(0xffffffffu, hit)) {
         float u[16];
