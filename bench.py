@@ -156,10 +156,11 @@ def stage_bytes(n, vis_n, inst, entries, pixels, views):
     }
 
 
-# per-stage limiter measured with ncu (profiles/r01_ncu_blend_loss.txt): the dominant stage
-# (blend backward) is bound by instruction issue, not by HBM
-LIMITER = {"blend_bwd": "FP32/ALU instruction issue (ncu: issue slots busy 72%, barrier-free warps)",
-           "blend_fwd": "FP32/ALU instruction issue (ncu: issue slots busy 73%)"}
+# per-stage limiter measured with ncu (profiles/r01_ncu_summary.txt): the blend stages are
+# bound by instruction issue (packed-FP32 arithmetic, barrier-free warps), not by HBM; the
+# issue-slot utilisation comes from the same capture (profiles/r01_ncu_traffic.json)
+LIMITER = {"blend_bwd": "instruction issue (packed FP32, barrier-free warps; ncu issue slots busy {pct}%)",
+           "blend_fwd": "instruction issue (packed FP32; ncu issue slots busy {pct}%)"}
 
 
 def ncu_stage(stage):
@@ -189,9 +190,10 @@ def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: 
           "algorithmic_bytes": sbytes[dom]}
     if dom in LIMITER:
         # the stage's real roof: instruction issue (ncu issue-slot utilisation, same capture)
-        rf["limiter"] = LIMITER[dom]
-        if nc.get("issue_busy_pct") is not None:
-            rf["issue_frac"] = round(nc["issue_busy_pct"] / 100.0, 3)
+        pct = nc.get("issue_busy_pct")
+        rf["limiter"] = LIMITER[dom].format(pct=pct if pct is not None else "?")
+        if pct is not None:
+            rf["issue_frac"] = round(pct / 100.0, 3)
     return rf, stages
 
 

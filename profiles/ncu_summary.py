@@ -56,8 +56,20 @@ def stage(name):
     return None
 
 
+PER_STEP = {"preprocess_fwd", "preprocess_bwd", "adam"}  # one launch per 8-view step (step report)
+
+
 def main(reps):
-    recs = [r for rep in reps for r in rows(rep)]
+    # reps[0]: one view (profile_step.py), reps[1]: one 8-view step (profile_train.py).
+    # The per-view stages come from the view report, the per-step ones from the step
+    # report only (the view report's single-view preprocess launches are not the step's).
+    recs, stage_recs = [], []
+    for ri, rep in enumerate(reps):
+        for r in rows(rep):
+            recs.append(r)
+            st = stage(r["kernel"])
+            if st and (st in PER_STEP) == (ri == len(reps) - 1 and len(reps) > 1):
+                stage_recs.append((st, r))
     lines = ["ncu --set full --clock-control none (one c3 view via profile_step.py; the per-step kernels via",
              "profile_train.py, 8 views).  Cold-cache, serialised replays: compare shares, not absolute times.", "",
              f"{'kernel':34s} {'us':>8s} {'DRAM MB':>9s} {'TB/s':>6s} {'issue%':>7s} {'occ%':>6s} {'fma%':>6s} {'regs':>5s}"]
@@ -68,12 +80,12 @@ def main(reps):
         lines.append(f"{r['kernel'][:34]:34s} {r['time_us']:8.1f} {mb:9.2f} {tbs:6.2f} "
                      f"{r['issue_busy_pct'] or 0:7.1f} {r['occupancy_pct'] or 0:6.1f} {r['fma_pipe_pct'] or 0:6.1f} "
                      f"{int(r['regs'] or 0):5d}")
-        st = stage(r["kernel"])
-        if st:
-            per_stage[st]["dram_bytes_per_launch"] += mb * 1e6
-            per_stage[st]["time_us"] += r["time_us"]
-            per_stage[st]["kernels"].append(r["kernel"])
-            per_stage[st]["issue_w"] += (r["issue_busy_pct"] or 0.0) * r["time_us"]
+    for st, r in stage_recs:
+        mb = ((r["dram_read"] or 0) + (r["dram_write"] or 0)) / 1e6
+        per_stage[st]["dram_bytes_per_launch"] += mb * 1e6
+        per_stage[st]["time_us"] += r["time_us"]
+        per_stage[st]["kernels"].append(r["kernel"])
+        per_stage[st]["issue_w"] += (r["issue_busy_pct"] or 0.0) * r["time_us"]
     json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"]), "time_us": round(v["time_us"], 1),
                    "issue_busy_pct": round(v["issue_w"] / max(v["time_us"], 1e-9), 1),
                    "kernels": v["kernels"]} for k, v in per_stage.items()},
