@@ -117,16 +117,34 @@ def _tiles_y(cam, ts):
     return (cam.height + ts - 1) // ts
 
 
-def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
-         row_begin: int, row_end: int, err: torch.Tensor | None = None,
-         depth_keys: torch.Tensor | None = None, cs=None) -> TileBins:
-    """tgs_bin_gaussians + one host read of the instance count + tgs_bin_instances
-    (cs: the current torch stream, if the caller has it)."""
+@dataclass
+class _BinPending:
+    """First half of a binning (tgs_bin_gaussians issued, its instance count on its way to
+    a pinned host buffer); _bin_end finishes it."""
+    splats: torch.Tensor
+    n: int
+    width: int
+    height: int
+    ts: int
+    row_begin: int
+    row_end: int
+    has_err: bool
+    cs: object          # the stream it runs on
+    ws: torch.Tensor    # tgs_bin_gaussians workspace (per-stream scratch; read by tgs_bin_instances)
+    h: torch.Tensor     # pinned (count, error flag)
+    ev: object          # recorded after the copy
+
+
+def _bin_begin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
+               row_begin: int, row_end: int, err: torch.Tensor | None = None,
+               depth_keys: torch.Tensor | None = None, cs=None) -> _BinPending:
+    """tgs_bin_gaussians and an asynchronous read of the instance count.  Callers may
+    begin the next view's binning on ANOTHER stream before ending this one, so the GPU
+    has work queued while the host waits for this count (not on the same stream: the
+    workspace is that stream's scratch)."""
     dev = splats.device
     cs = cs if cs is not None else torch.cuda.current_stream(dev)
     st = cs.cuda_stream
-    tiles_x = (width + ts - 1) // ts
-    tiles_y = (height + ts - 1) // ts
     nb = ctypes_size("tgs_bin_gaussians_workspace", n)
     ws = _scratch("bin_g", max(nb, 16), dev, st)
     d_count = _scratch("count", 16, dev, st).view(torch.int64)
@@ -135,24 +153,42 @@ def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, 
                   height, ts, row_begin, row_end, _lib.ptr(ws), _lib.ptr(d_count), st)
     if err is not None:
         d_count[1:2].copy_(err)
-    # the only host round trip of a render: the instance count (+ error flag), read
-    # through a pinned buffer on this stream
-    h = _pinned_count()
+    h = _pinned_count(st)
     h.copy_(d_count, non_blocking=True)
-    cs.synchronize()
-    count, flag = int(h[0]), int(h[1]) if err is not None else 0
+    ev = torch.cuda.Event()
+    ev.record(cs)
+    return _BinPending(splats, n, width, height, ts, row_begin, row_end, err is not None, cs, ws, h, ev)
+
+
+def _bin_end(p: _BinPending) -> TileBins:
+    """Waits for the instance count (the render's only host round trip) and issues
+    tgs_bin_instances on the pending binning's stream."""
+    dev = p.splats.device
+    st = p.cs.cuda_stream
+    p.ev.synchronize()
+    count, flag = int(p.h[0]), int(p.h[1]) if p.has_err else 0
     if flag:
         raise DegenerateRotationError("quaternion with (near-)zero norm")
-    ntiles = (row_end - row_begin) * tiles_x
+    ts, width, height, rb, re = p.ts, p.width, p.height, p.row_begin, p.row_end
+    tiles_x = (width + ts - 1) // ts
+    tiles_y = (height + ts - 1) // ts
+    ntiles = (re - rb) * tiles_x
     offsets = _alloc(ntiles + 1, torch.int32, dev)
     ids = _alloc(_size_class(max(count, 1)), torch.int32, dev)
-    ib = ctypes_size("tgs_bin_instances_workspace", n, count, width, height, ts, row_begin, row_end)
+    ib = ctypes_size("tgs_bin_instances_workspace", p.n, count, width, height, ts, rb, re)
     ws2 = _scratch("bin_i", max(ib, 16), dev, st)
-    with stage("bin_instances"):
-        _lib.call("tgs_bin_instances", _lib.ptr(splats), n, width, height, ts, row_begin, row_end, _lib.ptr(ws),
+    with torch.cuda.stream(p.cs), stage("bin_instances"):
+        _lib.call("tgs_bin_instances", _lib.ptr(p.splats), p.n, width, height, ts, rb, re, _lib.ptr(p.ws),
                   count, _lib.ptr(ws2), _lib.ptr(offsets), _lib.ptr(ids), st)
-        order = _blend_order(offsets, ntiles, tiles_x, row_end - row_begin, ts, dev, st)
-    return TileBins(offsets, ids[:count], tiles_x, tiles_y, row_begin, row_end, order)
+        order = _blend_order(offsets, ntiles, tiles_x, re - rb, ts, dev, st)
+    return TileBins(offsets, ids[:count], tiles_x, tiles_y, rb, re, order)
+
+
+def _bin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
+         row_begin: int, row_end: int, err: torch.Tensor | None = None,
+         depth_keys: torch.Tensor | None = None, cs=None) -> TileBins:
+    """tgs_bin_gaussians + one host read of the instance count + tgs_bin_instances."""
+    return _bin_end(_bin_begin(splats, tiles_touched, n, width, height, ts, row_begin, row_end, err, depth_keys, cs))
 
 
 _PINNED = {}
@@ -209,9 +245,10 @@ def _size_class(k: int) -> int:
     return (k + step - 1) // step * step
 
 
-def _pinned_count() -> torch.Tensor:
-    """A pinned 2-element host buffer per host thread (the read completes before reuse)."""
-    k = threading.get_ident()
+def _pinned_count(stream_handle: int = 0) -> torch.Tensor:
+    """A pinned 2-element host buffer per (host thread, stream): a stream's read completes
+    before its next binning reuses the buffer."""
+    k = (threading.get_ident(), stream_handle)
     h = _PINNED.get(k)
     if h is None:
         h = _PINNED[k] = torch.empty(2, dtype=torch.int64, pin_memory=True)
@@ -361,10 +398,26 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
         s_.wait_stream(main)
     outs = []
     _ALLOC.stream = main
+    n = len(cloud)
+
+    def begin(i):  # view i's depth sort and count read-back on its own stream
+        if not n or len(pool) < 2:
+            return None
+        cam, (sp, _, tiles, keys, err) = cams[i], pres[i]
+        ts = int(settings.tile_size)
+        with torch.cuda.stream(pool[i % len(pool)]):
+            return _bin_begin(sp, tiles, n, int(cam.width), int(cam.height), ts, 0, _tiles_y(cam, ts), err, keys)
+
     try:
+        pend = begin(0)
         for i, cam in enumerate(cams):
+            # the next view's binning is queued (on the next stream) before this view's
+            # count is awaited, so the GPU never idles on the host round trip
+            nxt = begin(i + 1) if i + 1 < len(cams) else None
             with torch.cuda.stream(pool[i % len(pool)]):
-                outs.append(render_forward(cloud, cam, settings, pre=pres[i]))
+                bins = _bin_end(pend) if pend is not None else None
+                outs.append(render_forward(cloud, cam, settings, pre=pres[i], bins=bins))
+            pend = nxt
     finally:
         _ALLOC.stream = None
         for s_ in pool:
@@ -373,10 +426,11 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
 
 
 def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple | None = None,
-                   pre: tuple | None = None) -> RenderOutput:
+                   pre: tuple | None = None, bins: TileBins | None = None) -> RenderOutput:
     """Render a cloud into an (H, W, 3) image plus blending auxiliaries (rasterizer.py:215-284).
 
-    pre: this view's outputs of `preprocess_views` (skips the per-view preprocess)."""
+    pre: this view's outputs of `preprocess_views` (skips the per-view preprocess);
+    bins: its tile lists from _bin_begin/_bin_end (pipelined callers, with `pre`)."""
     import ctypes
     cloud = _as_cloud(cloud)
     c_set = _lib.make_settings(settings)  # validates settings even for empty clouds
@@ -388,7 +442,8 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     rb, re = row_band if row_band is not None else (0, _tiles_y(cam, ts))
     cs = torch.cuda.current_stream(dev)
     splats, vis, tiles, keys, err = pre if pre is not None else preprocess(cloud, cam, settings)
-    bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys, cs)
+    if bins is None:
+        bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys, cs)
     specs = [((h, w, 3), torch.float32), ((h, w), torch.float32), ((h, w), torch.float32), ((h, w), torch.int32),
              ((h, w), torch.int32), ((n,), torch.bool)]
     if settings.record_hits:

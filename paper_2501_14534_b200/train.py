@@ -26,8 +26,8 @@ from . import loss as loss_mod
 from .cloud import PARAM_FIELDS, CloudGrads, GaussianCloud
 from .optim import Adam
 from .profiler import stage
-from .rasterizer import (RenderSettings, blend_backward, preprocess_backward_views, preprocess_views,
-                         render_forward)
+from .rasterizer import (RenderSettings, _bin_begin, _bin_end, _tiles_y, blend_backward, preprocess_backward_views,
+                         preprocess_views, render_forward)
 
 # reference defaults (config.py:76-92 OptimConfig; config.py:67-73 MaskConfig)
 DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opacity_logits": 0.05,
@@ -160,14 +160,31 @@ class Trainer:
         pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, stats=self.stats)
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
+        n = len(self.cloud)
+        ts = int(self.settings.tile_size)
+
+        def begin(i):  # view i's depth sort + instance-count read-back, on view i's stream
+            if not n or len(self.streams) < 2:
+                return None
+            cam_, (sp, _, tiles, keys, err) = self.cameras[self.views[i]], pres[i]
+            with torch.cuda.stream(self.streams[i % len(self.streams)]):
+                return _bin_begin(sp, tiles, n, int(cam_.width), int(cam_.height), ts, 0, _tiles_y(cam_, ts), err,
+                                  keys)
+
+        pend = begin(0) if self.views else None
         for i, v in enumerate(self.views):
             # consecutive views alternate between two streams: the latency-bound binning of
-            # view v overlaps the blend/loss kernels of view v-1 (and the host round trip
-            # for the instance count blocks only this view's stream)
+            # view v overlaps the blend/loss kernels of view v-1, and view v+1's depth sort is
+            # queued before view v's instance count is awaited (the host round trip never
+            # leaves the GPU without work)
             st = self.streams[i % len(self.streams)]
+            nxt = begin(i + 1) if i + 1 < len(self.views) else None
             with torch.cuda.stream(st):
                 cam, target = self.cameras[v], self.targets[v]
-                out = render_forward(self.cloud, cam, self.settings, pre=pres[i])
+                bins = _bin_end(pend) if pend is not None else None
+                out = render_forward(self.cloud, cam, self.settings, pre=pres[i], bins=bins)
+            pend = nxt
+            with torch.cuda.stream(st):
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
                 if d is None:
                     d = self.dimage[(i % len(self.streams), cam.height, cam.width)] = torch.empty_like(out.image)
