@@ -409,15 +409,17 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
             return _bin_begin(sp, tiles, n, int(cam.width), int(cam.height), ts, 0, _tiles_y(cam, ts), err, keys)
 
     try:
-        pend = begin(0)
+        # the next len(pool) - 1 views' binnings are queued (each on its own stream) before
+        # this view's count is awaited, so the GPU never idles on the host round trip
+        ahead = max(len(pool) - 1, 1)
+        pend = [begin(i) for i in range(min(ahead, len(cams)))]
         for i, cam in enumerate(cams):
-            # the next view's binning is queued (on the next stream) before this view's
-            # count is awaited, so the GPU never idles on the host round trip
-            nxt = begin(i + 1) if i + 1 < len(cams) else None
+            if i + ahead < len(cams):
+                pend.append(begin(i + ahead))
+            p_i = pend.pop(0)
             with torch.cuda.stream(pool[i % len(pool)]):
-                bins = _bin_end(pend) if pend is not None else None
+                bins = _bin_end(p_i) if p_i is not None else None
                 outs.append(render_forward(cloud, cam, settings, pre=pres[i], bins=bins))
-            pend = nxt
     finally:
         _ALLOC.stream = None
         for s_ in pool:
