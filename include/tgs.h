@@ -177,14 +177,20 @@ TGS_API int tgs_count_tiles(const float *splats, int64_t n, int32_t width, int32
  *
  * Step A: tgs_bin_gaussians() needs a workspace of tgs_bin_gaussians_workspace()
  * bytes, which must stay alive until step B returns.  It writes the instance count
- * to *d_num_instances (device int64).
+ * to d_num_instances[0] (device int64) and, when error_flag (device int32, e.g.
+ * tgs_preprocess_forward's) is not NULL, its value to d_num_instances[1] — so one
+ * 16-byte device-to-host read returns both.
  * Step B: tgs_bin_instances() with num_instances read back by the caller and a
  * workspace of tgs_bin_instances_workspace() bytes (same band arguments). */
 TGS_API int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes);
+/* Asynchronous device -> host copy on `stream` (the count read-back between step A
+ * and step B; dst should be pinned host memory). */
+TGS_API int tgs_memcpy_d2h_async(void *dst_host, const void *src_device, size_t bytes, tgs_stream_t stream);
 TGS_API int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, const uint64_t *depth_keys,
                       int64_t n, int32_t width,
                       int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
-                      void *workspace, int64_t *d_num_instances, tgs_stream_t stream);
+                      void *workspace, int64_t *d_num_instances, const int32_t *error_flag,
+                      tgs_stream_t stream);
 /* Instances per tile row (row_counts: tiles_y int64, accumulated): the replicated
  * histogram from which every rank derives the same balanced tile-row bands. */
 TGS_API int tgs_row_histogram(const float *splats, const int32_t *tiles_touched, int64_t n, int32_t width,
@@ -315,6 +321,35 @@ TGS_API int tgs_significance_scores(const tgs_cloud *cloud, const int64_t *hits,
                                     float *scores, void *workspace, size_t workspace_bytes, tgs_stream_t stream);
 TGS_API int tgs_significance_keep(const float *scores, int64_t n, int64_t k, uint8_t *keep, void *workspace,
                                   size_t workspace_bytes, tgs_stream_t stream);
+
+/* ---- native render pipeline for a batch of views (rasterizer.render_views) ----
+ * The per-view sequence of render_forward — one multi-view preprocess, then per view
+ * tgs_bin_gaussians -> count read-back -> tgs_bin_instances -> tgs_blend_forward —
+ * issued from C++ over `nstreams` caller streams (view v on streams[v % nstreams]),
+ * with the next nstreams-1 views' depth sorts queued before a view's count is
+ * awaited.  Outputs are the caller's (preprocess buffers as for
+ * tgs_preprocess_forward_views, per-view targets below); workspaces[k] holds
+ * workspace_bytes >= tgs_render_views_workspace(n, max instances of a view, ...)
+ * for stream k; pinned_counts is 2 * nstreams pinned host int64.  Views whose count
+ * exceeds ids_capacity or the workspace stop the batch with TGS_ERR_CAPACITY after
+ * every view's count is reported in num_instances (the caller grows and retries). */
+typedef struct {
+  int32_t *tile_offsets;     /* (tiles + 1,) */
+  int32_t *sorted_ids;       /* (ids_capacity,) */
+  int64_t ids_capacity;
+  const int32_t *tile_order; /* blend launch order (may be NULL) */
+  float *image, *transmit, *weight_sum;
+  int32_t *n_contrib, *last_pos, *hits; /* hits may be NULL (zeroed by the caller otherwise) */
+  int64_t num_instances;     /* out */
+} tgs_view_target;
+
+TGS_API int tgs_render_views_workspace(int64_t n, int64_t max_instances, int32_t width, int32_t height,
+                                       int32_t tile_size, size_t *bytes);
+TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s, int32_t nviews,
+                             float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
+                             uint64_t *const *depth_keys, int32_t *error_flag, tgs_view_target *targets,
+                             void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
+                             const tgs_stream_t *streams, int32_t nstreams);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,12 @@ class TgsDensifyStats(ctypes.Structure):
     _fields_ = [("grad_accum", _P), ("grad_count", _P), ("area_max", _P)]
 
 
+class TgsViewTarget(ctypes.Structure):
+    _fields_ = [("tile_offsets", _P), ("sorted_ids", _P), ("ids_capacity", _I64), ("tile_order", _P),
+                ("image", _P), ("transmit", _P), ("weight_sum", _P), ("n_contrib", _P), ("last_pos", _P),
+                ("hits", _P), ("num_instances", _I64)]
+
+
 class TgsGrads(ctypes.Structure):
     _fields_ = [(f, _P) for f in GRAD_FIELDS]
 
@@ -59,7 +65,10 @@ _SIGS = {
     "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
-    "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P], _I32),
+    "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P], _I32),
+    "tgs_memcpy_d2h_async": ([_P, _P, _SZ, _P], _I32),
+    "tgs_render_views_workspace": ([_I64, _I64, _I32, _I32, _I32, _P], _I32),
+    "tgs_render_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _I32], _I32),
     "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),

@@ -477,6 +477,16 @@ struct BsCtl {                 // zeroed before every call
   uint32_t m, overflow, ticket, pad;
 };
 
+// One launch instead of two memsets and a copy: zero the control block and the
+// count, and forward the preprocess error flag into counts[1] (one D2H read).
+__global__ void k_bs_init(BsCtl *ctl, unsigned long long *counts, const int32_t *error_flag) {
+  if (threadIdx.x == 0) {
+    *ctl = BsCtl{0ull, 0ull, 0u, 0u, 0u, 0u};
+    counts[0] = 0ull;
+    if (error_flag) counts[1] = (unsigned long long)(long long)*error_flag;
+  }
+}
+
 struct BsArgs {
   const float *splats;
   const int32_t *tiles_touched;
@@ -1271,15 +1281,15 @@ extern "C" int tgs_bin_gaussians_workspace(int64_t n, size_t *bytes) {
 extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touched, const uint64_t *depth_keys,
                                  int64_t n, int32_t width,
                                  int32_t height, int32_t tile_size, int32_t row_begin, int32_t row_end,
-                                 void *workspace, int64_t *d_num_instances, tgs_stream_t stream) {
+                                 void *workspace, int64_t *d_num_instances, const int32_t *error_flag,
+                                 tgs_stream_t stream) {
   Band b;
   if (n < 0 || n >= (int64_t)1 << 30 || !workspace || !d_num_instances ||
       !band_ok(width, height, tile_size, row_begin, row_end, b))
     return TGS_ERR_INVALID;
   cudaStream_t st = as_stream(stream);
   GaussWS w = carve_gauss(workspace, n);
-  cudaMemsetAsync(w.bctl, 0, sizeof(BsCtl), st);
-  cudaMemsetAsync(d_num_instances, 0, 8, st);
+  k_bs_init<<<1, 32, 0, st>>>(w.bctl, reinterpret_cast<unsigned long long *>(d_num_instances), error_flag);
   if (n == 0) return launch_status();
   BsArgs ba;
   ba.splats = splats;
@@ -1397,4 +1407,12 @@ extern "C" int tgs_row_histogram(const float *splats, const int32_t *tiles_touch
   k_row_hist<<<(unsigned)ceil_div<int64_t>(n, 256), 256, sh, as_stream(stream)>>>(
       splats, tiles_touched, n, b, reinterpret_cast<unsigned long long *>(row_counts));
   return launch_status();
+}
+
+// The binning round trip's device -> host read (the caller's pinned buffer) on an
+// explicit stream: lets a host pipeline read a view's counts without switching its
+// framework's current stream.
+extern "C" int tgs_memcpy_d2h_async(void *dst_host, const void *src_device, size_t bytes, tgs_stream_t stream) {
+  if (!dst_host || !src_device) return TGS_ERR_INVALID;
+  return cuda_status(cudaMemcpyAsync(dst_host, src_device, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
 }

@@ -135,26 +135,46 @@ class _BinPending:
     ev: object          # recorded after the copy
 
 
+_WS_G: dict = {}   # n -> tgs_bin_gaussians_workspace bytes
+_WS_I: dict = {}   # (n, band geometry) -> (largest count queried, its workspace bytes)
+
+
+def _ws_gauss(n: int) -> int:
+    b = _WS_G.get(n)
+    if b is None:
+        b = _WS_G[n] = ctypes_size("tgs_bin_gaussians_workspace", n)
+    return b
+
+
+def _ws_inst(n: int, count: int, width: int, height: int, ts: int, rb: int, re: int) -> int:
+    """tgs_bin_instances_workspace, queried only when the count exceeds the largest one
+    seen for this geometry (the size is non-decreasing in the count, so that size is
+    an upper bound for every smaller count)."""
+    key = (n, width, height, ts, rb, re)
+    hi = _WS_I.get(key)
+    if hi is None or count > hi[0]:
+        hi = _WS_I[key] = (count, ctypes_size("tgs_bin_instances_workspace", n, count, width, height, ts, rb, re))
+    return hi[1]
+
+
 def _bin_begin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width: int, height: int, ts: int,
                row_begin: int, row_end: int, err: torch.Tensor | None = None,
                depth_keys: torch.Tensor | None = None, cs=None) -> _BinPending:
-    """tgs_bin_gaussians and an asynchronous read of the instance count.  Callers may
-    begin the next view's binning on ANOTHER stream before ending this one, so the GPU
-    has work queued while the host waits for this count (not on the same stream: the
-    workspace is that stream's scratch)."""
+    """tgs_bin_gaussians and an asynchronous read of the instance count (+ the preprocess
+    error flag, forwarded by the kernel).  Callers may begin the next view's binning on
+    ANOTHER stream before ending this one, so the GPU has work queued while the host
+    waits for this count (not on the same stream: the workspace is that stream's
+    scratch).  Only explicit-stream calls: no framework stream switch."""
     dev = splats.device
     cs = cs if cs is not None else torch.cuda.current_stream(dev)
     st = cs.cuda_stream
-    nb = ctypes_size("tgs_bin_gaussians_workspace", n)
-    ws = _scratch("bin_g", max(nb, 16), dev, st)
-    d_count = _scratch("count", 16, dev, st).view(torch.int64)
+    ws = _scratch("bin_g", max(_ws_gauss(n), 16), dev, st)
+    d_count = _scratch("count", 16, dev, st)
     with stage("bin_gaussians"):
         _lib.call("tgs_bin_gaussians", _lib.ptr(splats), _lib.ptr(tiles_touched), _lib.ptr(depth_keys), n, width,
-                  height, ts, row_begin, row_end, _lib.ptr(ws), _lib.ptr(d_count), st)
-    if err is not None:
-        d_count[1:2].copy_(err)
+                  height, ts, row_begin, row_end, _lib.ptr(ws), _lib.ptr(d_count), _lib.ptr(err), st)
     h = _pinned_count(st)
-    h.copy_(d_count, non_blocking=True)
+    _lib.call("tgs_memcpy_d2h_async", h.data_ptr(), _lib.ptr(d_count), 16, st)
     ev = torch.cuda.Event()
     ev.record(cs)
     return _BinPending(splats, n, width, height, ts, row_begin, row_end, err is not None, cs, ws, h, ev)
@@ -162,7 +182,8 @@ def _bin_begin(splats: torch.Tensor, tiles_touched: torch.Tensor, n: int, width:
 
 def _bin_end(p: _BinPending) -> TileBins:
     """Waits for the instance count (the render's only host round trip) and issues
-    tgs_bin_instances on the pending binning's stream."""
+    tgs_bin_instances on the pending binning's stream (the caller's current stream, or
+    render_views' allocation stream, owns the returned buffers)."""
     dev = p.splats.device
     st = p.cs.cuda_stream
     p.ev.synchronize()
@@ -173,11 +194,9 @@ def _bin_end(p: _BinPending) -> TileBins:
     tiles_x = (width + ts - 1) // ts
     tiles_y = (height + ts - 1) // ts
     ntiles = (re - rb) * tiles_x
-    offsets = _alloc(ntiles + 1, torch.int32, dev)
-    ids = _alloc(_size_class(max(count, 1)), torch.int32, dev)
-    ib = ctypes_size("tgs_bin_instances_workspace", p.n, count, width, height, ts, rb, re)
-    ws2 = _scratch("bin_i", max(ib, 16), dev, st)
-    with torch.cuda.stream(p.cs), stage("bin_instances"):
+    offsets, ids = _alloc_many([((ntiles + 1,), torch.int32), ((_size_class(max(count, 1)),), torch.int32)], dev)
+    ws2 = _scratch("bin_i", max(_ws_inst(p.n, count, width, height, ts, rb, re), 16), dev, st)
+    with stage("bin_instances"):
         _lib.call("tgs_bin_instances", _lib.ptr(p.splats), p.n, width, height, ts, rb, re, _lib.ptr(p.ws),
                   count, _lib.ptr(ws2), _lib.ptr(offsets), _lib.ptr(ids), st)
         order = _blend_order(offsets, ntiles, tiles_x, re - rb, ts, dev, st)
@@ -222,15 +241,22 @@ def _blend_order(offsets, ntiles: int, tiles_x: int, rows: int, ts: int, dev, st
 _SCRATCH = {}
 
 
-def _scratch(tag: str, nbytes: int, dev, stream_handle: int | None = None) -> torch.Tensor:
+def _scratch(tag: str, nbytes: int, dev, stream_handle: int | None = None, owner=None) -> torch.Tensor:
     """Per-stream scratch workspace, grown geometrically and reused by every later call on
     the same stream (stream order makes the reuse safe; nothing returned references it).
-    Frame-to-frame size changes (instance counts) then cost no allocator traffic."""
+    Frame-to-frame size changes (instance counts) then cost no allocator traffic.
+    owner: the torch stream using it, when that is not the current stream (the block is
+    then allocated from that stream's pool)."""
     sh = stream_handle if stream_handle is not None else torch.cuda.current_stream(dev).cuda_stream
     key = (dev.index, sh, tag)
     t = _SCRATCH.get(key)
     if t is None or t.numel() < nbytes:
-        t = torch.empty(_size_class(int(nbytes * 1.25) + 4096), dtype=torch.uint8, device=dev)
+        size = _size_class(int(nbytes * 1.25) + 4096)
+        if owner is not None:
+            with torch.cuda.stream(owner):
+                t = torch.empty(size, dtype=torch.uint8, device=dev)
+        else:
+            t = torch.empty(size, dtype=torch.uint8, device=dev)
         _SCRATCH[key] = t
     return t[:nbytes]
 
@@ -376,6 +402,81 @@ def _alloc_many(specs, dev) -> list:
     return out
 
 
+_RV_CAP: dict = {}  # (device, n, tile, resolutions) -> per-view instance-id capacity of the native path
+
+
+def _render_views_native(cloud, cams, settings, pool, main, cap: int):
+    """tgs_render_views: the whole batch issued from C++ (see include/tgs.h).  Returns the
+    outputs, or the largest instance count of the batch when a buffer was too small."""
+    import ctypes
+    from .errors import TGS_ERR_CAPACITY, raise_for_status
+    n, dev, V, ts = len(cloud), cloud.device, len(cams), int(settings.tile_size)
+    c_set = _lib.make_settings(settings)
+    # preprocess outputs and every view's render outputs: allocated from the caller's
+    # stream pool (the side streams wait for it first and it waits for them at the end)
+    sp = torch.empty((V, n, 12), dtype=torch.float32, device=dev)
+    vis = torch.empty((V, n), dtype=torch.uint8, device=dev)
+    tiles = torch.empty((V, n), dtype=torch.int32, device=dev)
+    keys = torch.empty((V, n), dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    geo = []
+    specs = []
+    for cam in cams:
+        h, w = int(cam.height), int(cam.width)
+        tx, ty = (w + ts - 1) // ts, (h + ts - 1) // ts
+        geo.append((h, w, tx, ty))
+        specs += [((h, w, 3), torch.float32), ((h, w), torch.float32), ((h, w), torch.float32), ((h, w), torch.int32),
+                  ((h, w), torch.int32), ((tx * ty + 1,), torch.int32), ((cap,), torch.int32)]
+        if settings.record_hits:
+            specs.append(((n,), torch.int32))
+    bufs = _alloc_many(specs, dev)
+    per = 8 if settings.record_hits else 7
+    targets = (_lib.TgsViewTarget * V)()
+    orders = []
+    for v, (h, w, tx, ty) in enumerate(geo):
+        b = bufs[per * v: per * (v + 1)]
+        if settings.record_hits:
+            b[7].zero_()
+        order = _blend_order(None, tx * ty, tx, ty, ts, dev, None) if BLEND_ORDER == "center" else None
+        orders.append(order)
+        targets[v] = _lib.TgsViewTarget(b[5].data_ptr(), b[6].data_ptr(), cap, _lib.ptr(order), b[0].data_ptr(),
+                                        b[1].data_ptr(), b[2].data_ptr(), b[3].data_ptr(), b[4].data_ptr(),
+                                        b[7].data_ptr() if settings.record_hits else None, -1)
+    ns = len(pool)
+    wsb = max(ctypes_size("tgs_render_views_workspace", n, cap, w, h, ts) for h, w, _, _ in geo)
+    wss = [_scratch("render_views", wsb, dev, s_.cuda_stream, owner=s_) for s_ in pool]
+    pinned = _PINNED.get(("rv", ns))
+    if pinned is None:
+        pinned = _PINNED[("rv", ns)] = torch.empty(2 * ns, dtype=torch.int64, pin_memory=True)
+    c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+    arr = lambda t: (ctypes.c_void_p * V)(*[t[v].data_ptr() for v in range(V)])  # noqa: E731
+    c_cloud = cloud.native()
+    for s_ in pool:
+        s_.wait_stream(main)
+    rc = int(_lib.load().tgs_render_views(
+        ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(sp), arr(vis), arr(tiles), arr(keys),
+        err.data_ptr(), targets, (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), wsb, pinned.data_ptr(),
+        (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in pool]), ns))
+    if rc == TGS_ERR_CAPACITY:
+        for s_ in pool:  # the partial batch still writes these buffers: drain before they are freed
+            s_.synchronize()
+        return max(int(targets[v].num_instances) for v in range(V))
+    for s_ in pool:
+        main.wait_stream(s_)
+    raise_for_status(rc, "tgs_render_views")
+    outs = []
+    for v, (h, w, tx, ty) in enumerate(geo):
+        b = bufs[per * v: per * (v + 1)]
+        count = int(targets[v].num_instances)
+        bins = TileBins(b[5], b[6][:count], tx, ty, 0, ty, orders[v])
+        hit_counts = b[7].to(torch.int64) if settings.record_hits else None
+        outs.append(RenderOutput(image=b[0], transmittance=b[1], weight_sum=b[2], n_contrib=b[3], last_pos=b[4],
+                                 visible=vis[v].view(torch.bool), screen_areas=sp[v][:, 11], hit_counts=hit_counts,
+                                 _tiles=bins,
+                                 _state=_DeviceState(cloud.flat.data_ptr(), n, sp[v], vis[v], tiles[v], keys[v], bins)))
+    return outs
+
+
 def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) -> list:
     """Render a batch of views of one cloud (an orbit, the views of a training batch):
     every view's preprocess in ONE pass over the parameters (tgs_preprocess_forward_views),
@@ -393,6 +494,26 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
     pool = _RENDER_STREAMS.get(key)
     if pool is None:
         pool = _RENDER_STREAMS[key] = [torch.cuda.Stream(device=dev) for _ in range(key[1])]
+    # native path (tgs_render_views) once the batch's instance counts are known: the
+    # per-view sequence is issued from C++, the Python cost is one call per batch
+    _lib.make_settings(settings)
+    geom = (key[0], len(cloud), int(settings.tile_size), tuple((int(c.width), int(c.height)) for c in cams))
+    native = len(cloud) > 0 and not settings.record_full and len(cams) <= 64
+    if native and geom in _RV_CAP:
+        for _ in range(3):
+            res = _render_views_native(cloud, cams, settings, pool, main, _RV_CAP[geom])
+            if isinstance(res, list):
+                return res
+            _RV_CAP[geom] = _size_class(int(res * 1.25) + 1024)
+    outs = _render_views_py(cloud, cams, settings, pool, main)
+    if native:
+        _RV_CAP[geom] = _size_class(int(max(o._tiles.indices.numel() for o in outs) * 1.25) + 1024)
+    return outs
+
+
+def _render_views_py(cloud, cams, settings, pool, main) -> list:
+    """render_views driven from Python (first batch of a geometry, record_full)."""
+    dev = cloud.device
     pres = preprocess_views(cloud, cams, settings) if len(cloud) else [None] * len(cams)
     for s_ in pool:
         s_.wait_stream(main)
@@ -447,11 +568,12 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     if bins is None:
         bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys, cs)
     specs = [((h, w, 3), torch.float32), ((h, w), torch.float32), ((h, w), torch.float32), ((h, w), torch.int32),
-             ((h, w), torch.int32), ((n,), torch.bool)]
+             ((h, w), torch.int32)]
     if settings.record_hits:
         specs.append(((n,), torch.int64))
     bufs = _alloc_many(specs, dev)
-    image, transmit, wsum, n_contrib, last_pos, visible = bufs[:6]
+    image, transmit, wsum, n_contrib, last_pos = bufs[:5]
+    visible = vis[:n].view(torch.bool)  # the preprocess's 0/1 bytes, reinterpreted (no copy)
     if row_band is not None:  # pixels outside the band are not rendered here
         for t_, v in ((image, 0.0), (transmit, 1.0), (wsum, 0.0), (n_contrib, 0), (last_pos, 0)):
             t_.fill_(v)
@@ -462,10 +584,9 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
                   _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.ptr(bins.order),
                   cs.cuda_stream)
-    visible.copy_(vis[:n])
     hit_counts = None
     if hits is not None:
-        hit_counts = bufs[6]
+        hit_counts = bufs[5]
         hit_counts.copy_(hits[:n])
     out = RenderOutput(image=image, transmittance=transmit, weight_sum=wsum, n_contrib=n_contrib,
                        last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11], hit_counts=hit_counts,

@@ -20,16 +20,10 @@ dev = cloud.device
 streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
 
 if mode == "render":
-    def work():
-        main = torch.cuda.current_stream(dev)
-        pres = preprocess_views(cloud, sc.cameras, st)
-        for s_ in streams:
-            s_.wait_stream(main)
-        for i, cam in enumerate(sc.cameras):
-            with torch.cuda.stream(streams[i % 2]):
-                render_forward(cloud, cam, st, pre=pres[i])
-        for s_ in streams:
-            main.wait_stream(s_)
+    from paper_2501_14534_b200.rasterizer import render_views
+
+    def work():  # the batch API (native tgs_render_views once the counts are known)
+        render_views(cloud, sc.cameras, st)
 else:
     targets = [torch.from_numpy(t).to(dev) for t in sc.targets]
     tr = Trainer(cloud, sc.cameras, targets, st)

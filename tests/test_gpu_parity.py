@@ -716,6 +716,17 @@ def test_render_views_equals_render_forward(tgs):
             assert torch.equal(getattr(o2, f), getattr(ref, f)), f
         assert torch.equal(o._tiles.indices, ref._tiles.indices) and torch.equal(o._tiles.offsets, ref._tiles.offsets)
     assert tgs.render_views(cloud, [], st) == []
+    # the native batch path (tgs_render_views, used once a geometry's counts are known)
+    # recovers from a too-small id capacity: grow, retry, same results
+    from paper_2501_14534_b200 import rasterizer
+    geom = next(k for k in rasterizer._RV_CAP if k[1] == len(cloud))
+    rasterizer._RV_CAP[geom] = 1024
+    outs3 = tgs.render_views(cloud, cams, st)
+    assert rasterizer._RV_CAP[geom] >= max(o._tiles.indices.numel() for o in outs3)
+    for cam, o in zip(cams, outs3):
+        ref = tgs.render_forward(cloud, cam, st)
+        for f in ("image", "transmittance", "n_contrib", "last_pos", "visible", "hit_counts"):
+            assert torch.equal(getattr(o, f), getattr(ref, f)), f
 
 
 def test_tile_order_is_a_heaviest_first_permutation_and_changes_nothing(tgs):
