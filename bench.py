@@ -404,7 +404,8 @@ def main():
     def render_all():
         render_views(cloud, [sc.cameras[v] for v in views], st)
 
-    render_all()
+    render_all()  # learns the batch's instance counts (Python pipeline)
+    render_all()  # first native batch: its workspaces and arenas are allocated here, untimed
     fps_t = timed(args.steps, render_all)
     render_fps = args.steps * len(views) * world / fps_t
 
@@ -570,9 +571,9 @@ def render_c4(args):
             out += [o.image for o in render_views(cloud, cams[b:b + 8], st)]
         return out
 
-    # at least one whole batch of 8 frames untimed: the batch's buffers (sized by the
-    # per-frame instance counts) are then served from the allocator cache
-    frames_from(0, args.warmup if world > 1 else max(args.warmup, 8))
+    # at least two whole batches of 8 frames untimed: the first learns the instance counts
+    # (Python pipeline), the second allocates the native batch path's buffers
+    frames_from(0, args.warmup if world > 1 else max(args.warmup, 16))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
