@@ -781,3 +781,44 @@ def test_tile_order_is_a_heaviest_first_permutation_and_changes_nothing(tgs):
     assert np.array_equal(np.sort(oo), np.arange(40000)) and oo[0] == 123
     c2 = np.floor(np.log2(np.maximum(ln[oo], 1)))  # lengths 0 and 1 share the lightest class
     assert (np.diff(c2) <= 0).all()
+
+
+def test_render_views_native_mixed_batches_and_errors(tgs):
+    """tgs_render_views (native batch driver) on batches mixing resolutions, 8-px tiles,
+    a cloud that grows after its capacities were learned (retry on TGS_ERR_CAPACITY),
+    degenerate rotations (DegenerateRotationError through the driver) and an empty cloud."""
+    from paper_2501_14534_b200 import rasterizer, scenes
+    sc = scenes.small_scene(seed=71, n=15000, width=160, height=96, dist=3.0)
+    rng = np.random.default_rng(71)
+    cams = [scenes.pinhole(3.0 * scenes._unit(rng), (96, 160, 200)[k % 3], (64, 96, 80)[k % 3], name=f"m{k}")
+            for k in range(7)]
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    for ts in (16, 8):
+        st = tgs.RenderSettings(near=0.2, tile_size=ts)
+        for _ in range(2):  # first call learns the capacities (Python pipeline), second is native
+            outs = tgs.render_views(cloud, cams, st)
+        geom = (0, len(cloud), ts, tuple((c.width, c.height) for c in cams))
+        assert geom in rasterizer._RV_CAP
+        for cam, o in zip(cams, outs):
+            ref = tgs.render_forward(cloud, cam, st)
+            assert torch.equal(o.image, ref.image) and torch.equal(o.last_pos, ref.last_pos)
+            assert torch.equal(o._tiles.indices, ref._tiles.indices)
+    # grow the splats after the capacity was learned: more instances than the capacity
+    st = tgs.RenderSettings(near=0.2)
+    tgs.render_views(cloud, cams, st)
+    big = dict(sc.fields)
+    big["log_scales"] = sc.fields["log_scales"] + 1.2
+    cloud_big = tgs.GaussianCloud.from_fields(big)
+    outs = tgs.render_views(cloud_big, cams, st)  # same geometry key (n, sizes): retries natively
+    for cam, o in zip(cams, outs):
+        ref = tgs.render_forward(cloud_big, cam, st)
+        assert torch.equal(o.image, ref.image) and o._tiles.indices.numel() == ref._tiles.indices.numel()
+    # a degenerate rotation raises through the driver
+    bad = dict(sc.fields)
+    bad["rotations"] = sc.fields["rotations"].copy()
+    bad["rotations"][5] = 0.0
+    with pytest.raises(tgs.DegenerateRotationError):
+        tgs.render_views(tgs.GaussianCloud.from_fields(bad), cams, st)
+    empty = tgs.GaussianCloud.from_fields({k: v[:0] for k, v in sc.fields.items()})
+    outs = tgs.render_views(empty, cams[:2], st)
+    assert all(float(o.transmittance.min()) == 1.0 for o in outs)
