@@ -445,9 +445,10 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     ns = len(pool)
     wsb = max(ctypes_size("tgs_render_views_workspace", n, cap, w, h, ts) for h, w, _, _ in geo)
     wss = [_scratch("render_views", wsb, dev, s_.cuda_stream, owner=s_) for s_ in pool]
-    pinned = _PINNED.get(("rv", ns))
+    pkey = (threading.get_ident(), "render_views", ns)  # per host thread: the driver reads it synchronously
+    pinned = _PINNED.get(pkey)
     if pinned is None:
-        pinned = _PINNED[("rv", ns)] = torch.empty(2 * ns, dtype=torch.int64, pin_memory=True)
+        pinned = _PINNED[pkey] = torch.empty(2 * ns, dtype=torch.int64, pin_memory=True)
     c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
     arr = lambda t: (ctypes.c_void_p * V)(*[t[v].data_ptr() for v in range(V)])  # noqa: E731
     c_cloud = cloud.native()
