@@ -20,6 +20,9 @@
 // Splitting at the partials removes the fused kernel's second 10 px halo (the
 // forward maps no longer have to cover the adjoint's footprint) and keeps each
 // CTA's shared memory under 42 KB, so five CTAs share an SM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "tgs_common.cuh"
 
 namespace tgs {
@@ -63,13 +66,21 @@ __device__ __forceinline__ float adjoint_fold(int y, int n, const Taps &tp, F ge
 
 struct LossArgs {
   const float *img, *tgt;
-  int W, H;
+  int W, H, P;       // P: partials row pitch (W rounded up to 4 floats, TMA stride rule)
   Taps tp;
   float c1, c2, lam, inv_count;
-  float *part;       // [3 channels][3 partials][H][W]
+  float2 *part01;    // [3 channels][H][P] (dS/dmu_a, dS/dsigma_aa)
+  float *part2;      // [3 channels][H][P] dS/dsigma_ab
   double *sums;      // [2][nblocks]: per-CTA L1 and SSIM sums
   float *dimage;
 };
+
+// TMA boxes: the innermost start coordinate times the element size must be a multiple
+// of 16 bytes, so the (p0, p1) box (8 B elements) starts one column left of the halo
+// (x0 - 6) and the p2 box (4 B) three columns left (x0 - 8); widths cover the 42-wide
+// halo and keep the row a multiple of 16 bytes.
+constexpr int kBoxW01 = 44, kOff01 = 1;
+constexpr int kBoxW2 = 48, kOff2 = 3;
 
 __device__ __forceinline__ void block_sum2(double l1, double ss, double *dst0, double *dst1) {
   __shared__ double red[2][kLossThreads / 32];
@@ -216,11 +227,9 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
       const float B1 = m0 * m0 + m1 * m1 + A.c1, B2 = var_a + var_b + A.c2;
       const float rB1 = 1.0f / B1, rB2 = 1.0f / B2, rden = rB1 * rB2;  // two reciprocals, no divisions
       const float smap = A1 * A2 * rden;
-      const size_t plane = (size_t)H * W, p = (size_t)yy * W + xx;
-      float *pc = A.part + (size_t)c * 3 * plane;
-      pc[p] = 2.0f * m1 * (A2 - A1) * rden - 2.0f * m0 * smap * (rB1 - rB2);
-      pc[plane + p] = -smap * rB2;
-      pc[2 * plane + p] = 2.0f * A1 * rden;
+      const size_t p = ((size_t)c * H + yy) * A.P + xx;
+      A.part01[p] = make_float2(2.0f * m1 * (A2 - A1) * rden - 2.0f * m0 * smap * (rB1 - rB2), -smap * rB2);
+      A.part2[p] = 2.0f * A1 * rden;
       ss += smap;
       const float2 ab = sab[(r0 + o + kR) * kHS + q + kR];
       l1 += fabsf(ab.x - ab.y);
@@ -231,13 +240,18 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   block_sum2(l1, ss, A.sums + bid, A.sums + nb + bid);
 }
 
-__global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
+__global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A, const __grid_constant__ CUtensorMap tm01,
+                                                         const __grid_constant__ CUtensorMap tm2) {
   // partials (p0, p1) as a packed pair + p2 scalar: two FFMA2 + one FFMA per tap
-  // instead of three FFMA, bit-identical per component
-  __shared__ float2 sd01[kH][kHS];  // (p0, p1) on the tile + halo, zero outside the image
-  __shared__ float sd2[kH][kH];     // p2
+  // instead of three FFMA, bit-identical per component.  The tile + 5 px halo of the
+  // partials arrives by two 2-D TMA tile loads (one thread, one mbarrier); the TMA
+  // zero-fills rows / columns outside the image, which is exactly the adjoint's
+  // boundary condition (no per-element bounds checks, no register staging).
+  __shared__ __align__(128) float2 sd01[kH][kBoxW01];  // (p0, p1): halo column q at [q + kOff01]
+  __shared__ __align__(128) float sd2[kH][kBoxW2];      // p2: halo column q at [q + kOff2]
   __shared__ float2 se01[kT][kHS];  // vertical adjoint on the tile rows, halo columns
   __shared__ float se2[kT][kHS];
+  __shared__ __align__(8) uint64_t bar;
   const int c = blockIdx.x;
   const int x0 = blockIdx.y * kT, y0 = blockIdx.z * kT;
   const int mx = x0 - kR, my = y0 - kR;  // image coords of sd[.][0][0]
@@ -245,33 +259,30 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
   const int t = threadIdx.x;
   const Taps &tp = A.tp;
   const bool border = x0 < kR || y0 < kR || x0 + kT > W - kR || y0 + kT > H - kR;
-  const size_t plane = (size_t)H * W;
-  const float *pc = A.part + (size_t)c * 3 * plane;
-  {  // every load of the thread first, then the shared-memory stores
-    constexpr int kIt = (kH * kH + kLossThreads - 1) / kLossThreads;
-    float v0[kIt], v1[kIt], v2[kIt];
-#pragma unroll
-    for (int i = 0; i < kIt; ++i) {
-      const int e = t + i * kLossThreads;
-      const int r = e / kH, q = e - r * kH;
-      const int yy = my + r, xx = mx + q;
-      const bool in = e < kH * kH && yy >= 0 && yy < H && xx >= 0 && xx < W;
-      const uint32_t p = in ? (uint32_t)yy * (uint32_t)W + (uint32_t)xx : 0u;
-      v0[i] = in ? __ldg(pc + p) : 0.0f;
-      v1[i] = in ? __ldg(pc + plane + p) : 0.0f;
-      v2[i] = in ? __ldg(pc + 2 * plane + p) : 0.0f;
-    }
-#pragma unroll
-    for (int i = 0; i < kIt; ++i) {
-      const int e = t + i * kLossThreads;
-      if (e < kH * kH) {
-        const int r = e / kH, q = e - r * kH;
-        sd01[r][q] = make_float2(v0[i], v1[i]);
-        sd2[r][q] = v2[i];
-      }
-    }
+  const uint32_t bar_s = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s),
+                 "r"((uint32_t)(sizeof(sd01) + sizeof(sd2)))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&sd01[0][0]))),
+        "l"(reinterpret_cast<uint64_t>(&tm01)), "r"(mx - kOff01), "r"(my), "r"(c), "r"(bar_s)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&sd2[0][0]))),
+        "l"(reinterpret_cast<uint64_t>(&tm2)), "r"(mx - kOff2), "r"(my), "r"(c), "r"(bar_s)
+        : "memory");
   }
-  __syncthreads();
+  __syncthreads();  // the barrier's initialisation is visible before anyone waits on it
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(bar_s)
+      : "memory");
   // vertical adjoint: item = (halo column, 4 tile rows), symmetric taps -> correlation
   // (the pair and the scalar in one loop: measured faster than one input window at a
   // time despite the registers; so was the inlined lambda fold vs a strided-pointer one)
@@ -283,8 +294,8 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
     float col2[kVOut + 2 * kR];
 #pragma unroll
     for (int j = 0; j < kVOut + 2 * kR; ++j) {
-      col01[j] = sd01[r0 + j][q];
-      col2[j] = sd2[r0 + j][q];
+      col01[j] = sd01[r0 + j][q + kOff01];
+      col2[j] = sd2[r0 + j][q + kOff2];
     }
 #pragma unroll
     for (int o = 0; o < kVOut; ++o) {
@@ -297,9 +308,9 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A) {
       }
       const int yy = y0 + r0 + o;
       if (border && yy < H && (yy < kR || yy >= H - kR) && colok) {
-        a01.x += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q].x; });
-        a01.y += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q].y; });
-        a2 += adjoint_fold(yy, H, tp, [&](int j) { return sd2[j - my][q]; });
+        a01.x += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q + kOff01].x; });
+        a01.y += adjoint_fold(yy, H, tp, [&](int j) { return sd01[j - my][q + kOff01].y; });
+        a2 += adjoint_fold(yy, H, tp, [&](int j) { return sd2[j - my][q + kOff2]; });
       }
       const bool ok = yy < H && colok;
       se01[r0 + o][q] = ok ? a01 : make_float2(0.f, 0.f);
@@ -394,11 +405,35 @@ inline size_t loss_blocks(int W, int H) { return (size_t)ceil_div(W, kT) * ceil_
 
 using namespace tgs;
 
+static inline size_t loss_pitch(int32_t width) { return ((size_t)width + 3) / 4 * 4; }
+
 extern "C" int tgs_loss_workspace(int32_t width, int32_t height, size_t *bytes) {
   if (width < 1 || height < 1 || !bytes) return TGS_ERR_INVALID;
-  // per-channel SSIM partials (3 x 3 planes) + per-CTA double sums
-  *bytes = align_up((size_t)9 * width * height * sizeof(float)) + 2 * loss_blocks(width, height) * sizeof(double);
+  // per-channel SSIM partials ((p0, p1) pairs + p2, row pitch P) + per-CTA double sums
+  *bytes = align_up((size_t)9 * loss_pitch(width) * height * sizeof(float)) +
+           2 * loss_blocks(width, height) * sizeof(double);
   return TGS_OK;
+}
+
+// 3-D tiled tensor map over [3 channels][H][P] elements of `esize` bytes (box box_w x 42 x 1)
+static int partial_map(CUtensorMap *m, void *base, CUtensorMapDataType type, size_t esize, int W, int H, size_t P,
+                       int box_w) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return TGS_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, 3};
+  const cuuint64_t strides[2] = {(cuuint64_t)(P * esize), (cuuint64_t)(P * esize * H)};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)kH, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(m, type, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);  // out of bounds -> zeros
+  return r == CUDA_SUCCESS ? TGS_OK : TGS_ERR_CUDA;
 }
 
 extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t width, int32_t height,
@@ -406,6 +441,7 @@ extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t
                                 tgs_stream_t stream) {
   if (width < 2 * kR + 1 || height < 2 * kR + 1) return TGS_ERR_INVALID;  // metrics.py:83-84
   if (!image || !target || !dimage || !terms || !workspace) return TGS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(workspace) & 15) return TGS_ERR_INVALID;
   cudaStream_t st = as_stream(stream);
   LossArgs A;
   double w[2 * kR + 1], tot = 0.0;  // gaussian_taps (metrics.py:58-61), float64 then rounded
@@ -416,21 +452,36 @@ extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t
   }
   for (int i = 0; i < 2 * kR + 1; ++i) A.tp.w[i] = (float)(w[i] / tot);
   const size_t count = (size_t)width * height * 3;
+  const size_t P = loss_pitch(width);
   A.img = image;
   A.tgt = target;
   A.W = width;
   A.H = height;
+  A.P = (int)P;
   A.c1 = 0.01f * 0.01f;
   A.c2 = 0.03f * 0.03f;
   A.lam = lambda_ssim;
   A.inv_count = 1.0f / (float)count;
-  A.part = static_cast<float *>(workspace);
+  A.part01 = static_cast<float2 *>(workspace);
+  A.part2 = reinterpret_cast<float *>(A.part01 + 3 * P * height);
   A.sums = reinterpret_cast<double *>(static_cast<char *>(workspace) +
-                                      align_up((size_t)9 * width * height * sizeof(float)));
+                                      align_up((size_t)9 * P * height * sizeof(float)));
   A.dimage = dimage;
+  CUtensorMap tm01, tm2;
+  int rc = partial_map(&tm01, A.part01, CU_TENSOR_MAP_DATA_TYPE_UINT64, 8, width, height, P, kBoxW01);
+  if (rc == TGS_OK) rc = partial_map(&tm2, A.part2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, width, height, P, kBoxW2);
+  if (rc != TGS_OK) return rc;
   const dim3 grd(3, (unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT));
+  static bool carve = false;  // idempotent function attribute, set once
+  if (!carve) {
+    // four 44 KB CTAs per SM and the rest of the unified L1 as cache for the reflected
+    // image / target loads the three channel CTAs of a tile share (a fifth CTA would
+    // shrink that cache and costs more than its occupancy gains)
+    cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributePreferredSharedMemoryCarveout, 80);
+    carve = true;
+  }
   k_ssim_fwd<<<grd, kLossThreads, 0, st>>>(A);
-  k_ssim_adj<<<grd, kLossThreads, 0, st>>>(A);
+  k_ssim_adj<<<grd, kLossThreads, 0, st>>>(A, tm01, tm2);
   k_loss_finalize<<<1, 1024, 0, st>>>(A.sums, (int)loss_blocks(width, height), 1.0 / (double)count, terms);
   return launch_status();
 }
