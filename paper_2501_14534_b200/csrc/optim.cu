@@ -60,16 +60,18 @@ struct AdamGroupArgs {
 
 __global__ void __launch_bounds__(256) k_adam_groups(float *__restrict__ p, float *__restrict__ g,
                                                      float *__restrict__ m, float *__restrict__ v, AdamGroupArgs a) {
-  const int64_t n4 = a.off[a.ngroups] / 4;
+  // float4 chunks from the first group's start to the padded end of the last one
+  // (groups need not start at 0: a data-parallel bucket steps a subset of the groups)
+  const int64_t c0 = a.off[0] / 4, n4 = a.off[a.ngroups] / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n4; c += stride) {
+  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n4; c += stride) {
     const int64_t e = 4 * c;
     int k = 0;
 #pragma unroll
     for (int q = 1; q < 8; ++q)
       if (q < a.ngroups && e >= a.off[q]) k = q;
     const int64_t local = e - a.off[k];
-    if (local >= a.size[k]) continue;  // padding
+    if (local < 0 || local >= a.size[k]) continue;  // padding / gaps between groups
     float4 pp = reinterpret_cast<float4 *>(p)[c];
     float4 gg = reinterpret_cast<const float4 *>(g)[c];
     float4 mm = reinterpret_cast<float4 *>(m)[c];
@@ -168,8 +170,8 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
   a.lam_sh = lambda_sh;
   a.inv_n = n_gaussians > 0 ? 1.0f / (float)n_gaussians : 0.0f;
   for (int l = 0; l < 3; ++l) a.wband[l] = band_weights ? band_weights[l] : 0.0f;
-  const int64_t n4 = a.off[ngroups] / 4;
-  if (n4 == 0) return TGS_OK;
+  const int64_t n4 = a.off[ngroups] / 4 - a.off[0] / 4;
+  if (n4 <= 0) return TGS_OK;
   const unsigned grid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n4, 256), 148 * 8);
   k_adam_groups<<<grid, 256, 0, as_stream(stream)>>>(param, grad, m, v, a);
   return launch_status();

@@ -426,6 +426,23 @@ def test_render_sharded_single_rank_nccl(tgs):
         out = tgs.render_forward(cloud, sc.cameras[0], st)
         per_tile = np.diff(_np(out._tiles.offsets)).reshape(-1, out._tiles.tiles_x).sum(axis=1)
         assert np.array_equal(_np(counts), per_tile)
+        # the data-parallel training step (bucketed NCCL all-reduce on a communication
+        # stream, per-bucket Adam) equals the single-process step (one fused Adam)
+        from paper_2501_14534_b200.train import Trainer
+        rng = np.random.default_rng(8)
+        cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * scenes._unit(rng), 160, 96, name=f"d{k}") for k in range(2)]
+        tg = [torch.rand((c.height, c.width, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(k))
+              for k, c in enumerate(cams)]
+        res = []
+        for pg in (dist.group.WORLD, None):
+            c2 = tgs.GaussianCloud.from_fields(sc.fields)
+            tr = Trainer(c2, cams, [t.clone() for t in tg], st, process_group=pg, deterministic=True)
+            tr.step()
+            tr.step()
+            torch.cuda.synchronize()
+            res.append((tr.cloud.flat.clone(), tr.terms.clone(), dict(tr.opt.steps)))
+        assert torch.equal(res[0][1], res[1][1]) and res[0][2] == res[1][2]
+        np.testing.assert_allclose(_np(res[0][0]), _np(res[1][0]), rtol=1e-6, atol=1e-10)
     finally:
         dist.destroy_process_group()
 
@@ -822,3 +839,26 @@ def test_render_views_native_mixed_batches_and_errors(tgs):
     empty = tgs.GaussianCloud.from_fields({k: v[:0] for k, v in sc.fields.items()})
     outs = tgs.render_views(empty, cams[:2], st)
     assert all(float(o.transmittance.min()) == 1.0 for o in outs)
+
+
+def test_adam_subset_of_groups_leaves_other_fields_untouched(tgs):
+    """tgs_adam_step_groups on groups that do not start at offset 0 (the data-parallel
+    buckets: sh_rest alone, the two mask groups): only those groups move."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.cloud import PARAM_FIELDS, CloudGrads
+    from paper_2501_14534_b200.optim import Adam
+    sc = scenes.small_scene(seed=91, n=3000, width=64, height=64)
+    for names in (("sh_rest",), ("mask_logits", "sh_mask_logits"), ("rotations", "sh_dc")):
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        before = cloud.flat.clone()
+        g = CloudGrads(len(cloud), cloud.device)
+        g.flat.normal_()
+        opt = Adam(cloud, {f: 0.01 for f in PARAM_FIELDS})
+        opt.step(cloud, g, names=names, lambda_m=0.05, lambda_sh=0.05)
+        torch.cuda.synchronize()
+        for f in PARAM_FIELDS:
+            o, n = cloud.field_range(f)
+            moved = not torch.equal(cloud.flat[o:o + n], before[o:o + n])
+            assert moved == (f in names), (names, f)
+            if f not in names:
+                assert float(opt.m[o:o + n].abs().max()) == 0.0, (names, f)
