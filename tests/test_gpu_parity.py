@@ -862,3 +862,29 @@ def test_adam_subset_of_groups_leaves_other_fields_untouched(tgs):
             assert moved == (f in names), (names, f)
             if f not in names:
                 assert float(opt.m[o:o + n].abs().max()) == 0.0, (names, f)
+
+
+def test_trainer_host_targets_equal_device_targets(tgs):
+    """Trainer.step(host_targets=...) (per-view copies from pinned host memory on a copy
+    stream, each view's loss waiting only for its own copy: the bench's e2e path) gives
+    the same step as device-resident targets, bit for bit (deterministic reduction)."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.train import Trainer
+    sc = scenes.small_scene(seed=93, n=8000, width=128, height=96, dist=3.0)
+    rng = np.random.default_rng(93)
+    cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * scenes._unit(rng), 128, 96, name=f"h{k}") for k in range(3)]
+    host = {v: torch.rand((c.height, c.width, 3), generator=torch.Generator().manual_seed(v)).pin_memory()
+            for v, c in enumerate(cams)}
+    st = tgs.RenderSettings(near=0.2)
+    out = []
+    for use_host in (True, False):
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        dev_t = [torch.zeros((c.height, c.width, 3), device="cuda") if use_host else host[v].cuda()
+                 for v, c in enumerate(cams)]
+        tr = Trainer(cloud, cams, dev_t, st, deterministic=True)
+        for _ in range(2):
+            tr.step(host_targets=host if use_host else None)
+        torch.cuda.synchronize()
+        out.append((tr.cloud.flat.clone(), tr.terms.clone()))
+    assert torch.equal(out[0][1], out[1][1])
+    assert torch.equal(out[0][0], out[1][0])
