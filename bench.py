@@ -604,14 +604,20 @@ def render_c4(args):
 
 
 def trainer_launches(counts: dict, steps: int) -> int:
-    """Kernels of libtgs.so launched in the timed region (the per-entry-point counts are fixed by the
-    host code in csrc/: see DESIGN.md "Kernel inventory")."""
-    per_call = {"preprocess_fwd": 1,
-                # select, scan(3), compact, depth-sort hist + scan + 8 passes, count gather, scan(3)
-                "bin_gaussians": 1 + 3 + 1 + 2 + 8 + 1 + 3,
-                # tile difference grid, finalize (CSR + digit histograms), duplicate, 2 passes
-                "bin_instances": 1 + 1 + 1 + 2,
-                "blend_fwd": 1, "loss": 2, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 8}
+    """Kernels of libtgs.so launched in the timed region: per stage call, the kernel count
+    fixed by the host code in csrc/ (checked against the ncu launch list,
+    profiles/r01_launches_bench_c3.summary.txt).  Memsets and torch's own kernels are
+    not counted."""
+    per_call = {"preprocess_fwd": 1,                # k_preprocess_fwd_views (all views)
+                # k_bs_init, select, hist, scan, scatter, rank, the idle LSD fallback
+                "bin_gaussians": 7,
+                # k_seg_count, seg_base, scatter, unit_table, place_count, tile_scan, place_write
+                "bin_instances": 7,
+                "blend_fwd": 1,                      # k_blend_fwd16w
+                "loss": 3,                           # k_ssim_fwd, k_ssim_adj, k_loss_finalize
+                "blend_bwd": 1,                      # k_blend_bwd16w
+                "preprocess_bwd": 1,                 # k_preprocess_bwd_views (all views)
+                "adam": 1}                           # k_adam_groups (all groups)
     return int(sum(per_call[k] * c for k, c in counts.items() if k in per_call))
 
 
