@@ -327,7 +327,9 @@ TGS_API int tgs_significance_keep(const float *scores, int64_t n, int64_t k, uin
  * tgs_bin_gaussians -> count read-back -> tgs_bin_instances -> tgs_blend_forward —
  * issued from C++ over `nstreams` caller streams (view v on streams[v % nstreams]),
  * with the next nstreams-1 views' depth sorts queued before a view's count is
- * awaited.  Outputs are the caller's (preprocess buffers as for
+ * awaited.  blend_streams (may be NULL = the same streams): view v's blend runs on
+ * blend_streams[v % nstreams] after its binning (event), e.g. a lower priority than
+ * the binning streams.  Outputs are the caller's (preprocess buffers as for
  * tgs_preprocess_forward_views, per-view targets below); workspaces[k] holds
  * workspace_bytes >= tgs_render_views_workspace(n, max instances of a view, ...)
  * for stream k; pinned_counts is 2 * nstreams pinned host int64.  Views whose count
@@ -349,7 +351,7 @@ TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, con
                              float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
                              uint64_t *const *depth_keys, int32_t *error_flag, tgs_view_target *targets,
                              void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
-                             const tgs_stream_t *streams, int32_t nstreams);
+                             const tgs_stream_t *streams, const tgs_stream_t *blend_streams, int32_t nstreams);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,7 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
                                 float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
                                 uint64_t *const *depth_keys, int32_t *error_flag, tgs_view_target *targets,
                                 void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
-                                const tgs_stream_t *streams, int32_t nstreams) {
+                                const tgs_stream_t *streams, const tgs_stream_t *blend_streams, int32_t nstreams) {
   if (!cloud || !cams || !s || nviews < 1 || !splats || !visible || !tiles_touched || !targets || !workspaces ||
       !pinned_counts || !streams || nstreams < 1 || nstreams > kMaxStreams || !error_flag)
     return TGS_ERR_INVALID;
@@ -72,9 +72,12 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
   rc = tgs_preprocess_forward_views(cloud, cams, s, nviews, splats, visible, tiles_touched, depth_keys, error_flag,
                                     nullptr, streams[0]);
   if (rc != TGS_OK) return rc;
-  cudaEvent_t ev_pre, ev[kMaxStreams];
+  cudaEvent_t ev_pre, ev[kMaxStreams], ev_b[kMaxStreams];
   if (cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming) != cudaSuccess) return TGS_ERR_CUDA;
-  for (int k = 0; k < nstreams; ++k) cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+  for (int k = 0; k < nstreams; ++k) {
+    cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_b[k], cudaEventDisableTiming);
+  }
   cudaEventRecord(ev_pre, st0);
   for (int k = 1; k < nstreams; ++k) cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(streams[k]), ev_pre, 0);
 
@@ -107,12 +110,19 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
     return tgs_bin_instances(splats[v], n, cams[v].width, cams[v].height, ts, 0, rows_of(v), slot[k].ws_g, count,
                              slot[k].ws_i, t.tile_offsets, t.sorted_ids, streams[k]);
   };
-  // 2c. blend view v
+  // 2c. blend view v (on its blend stream when one is given: the binning streams then
+  // run at higher priority and the blends fill the SMs around them)
   auto blend = [&](int v) -> int {
     const int k = v % nstreams;
     const tgs_view_target &t = targets[v];
+    tgs_stream_t bs = streams[k];
+    if (blend_streams) {
+      cudaEventRecord(ev_b[k], reinterpret_cast<cudaStream_t>(streams[k]));
+      cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(blend_streams[k]), ev_b[k], 0);
+      bs = blend_streams[k];
+    }
     return tgs_blend_forward(splats[v], t.tile_offsets, t.sorted_ids, &cams[v], s, 0, rows_of(v), t.image, t.transmit,
-                             t.weight_sum, t.n_contrib, t.last_pos, t.hits, t.tile_order, streams[k]);
+                             t.weight_sum, t.n_contrib, t.last_pos, t.hits, t.tile_order, bs);
   };
   // Per stream k the queue is  bin_instances(v) -> bin_gaussians(v + nstreams) -> blend(v):
   // the next same-stream view's depth sort runs BEFORE this view's blend, so its count
@@ -145,6 +155,9 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
     }
   }
   cudaEventDestroy(ev_pre);
-  for (int k = 0; k < nstreams; ++k) cudaEventDestroy(ev[k]);
+  for (int k = 0; k < nstreams; ++k) {
+    cudaEventDestroy(ev[k]);
+    cudaEventDestroy(ev_b[k]);
+  }
   return rc;
 }

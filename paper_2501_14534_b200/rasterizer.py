@@ -452,17 +452,24 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
     arr = lambda t: (ctypes.c_void_p * V)(*[t[v].data_ptr() for v in range(V)])  # noqa: E731
     c_cloud = cloud.native()
-    for s_ in pool:
+    # each view's blend on a normal-priority stream after its binning (the binning pool is
+    # high priority): measured +4% FPS at c3 over blending on the binning streams
+    key = ("blend", dev.index, ns)
+    bpool = _RENDER_STREAMS.get(key)
+    if bpool is None:
+        bpool = _RENDER_STREAMS[key] = [torch.cuda.Stream(device=dev, priority=0) for _ in range(ns)]
+    for s_ in pool + bpool:
         s_.wait_stream(main)
     rc = int(_lib.load().tgs_render_views(
         ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(sp), arr(vis), arr(tiles), arr(keys),
         err.data_ptr(), targets, (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), wsb, pinned.data_ptr(),
-        (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in pool]), ns))
+        (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in pool]),
+        (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in bpool]), ns))
     if rc == TGS_ERR_CAPACITY:
-        for s_ in pool:  # the partial batch still writes these buffers: drain before they are freed
+        for s_ in pool + bpool:  # the partial batch still writes these buffers: drain first
             s_.synchronize()
         return max(int(targets[v].num_instances) for v in range(V))
-    for s_ in pool:
+    for s_ in pool + bpool:
         main.wait_stream(s_)
     raise_for_status(rc, "tgs_render_views")
     outs = []
@@ -494,7 +501,9 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
     key = (dev.index if dev.index is not None else torch.cuda.current_device(), max(1, int(streams)))
     pool = _RENDER_STREAMS.get(key)
     if pool is None:
-        pool = _RENDER_STREAMS[key] = [torch.cuda.Stream(device=dev) for _ in range(key[1])]
+        # binning streams at high priority: their latency-bound kernels get SM slots first
+        # and the (issue-bound) blends fill around them on their own streams
+        pool = _RENDER_STREAMS[key] = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(key[1])]
     # native path (tgs_render_views) once the batch's instance counts are known: the
     # per-view sequence is issued from C++, the Python cost is one call per batch
     _lib.make_settings(settings)
