@@ -76,7 +76,7 @@ class DensifyStats:
 class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
-                 views=None, streams: int = 2, deterministic: bool = False, densify_stats: bool = False):
+                 views=None, streams: int = 4, deterministic: bool = False, densify_stats: bool = False):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -95,7 +95,8 @@ class Trainer:
         self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
         self.dimage = {}
         self.dsplats = {}
-        # >= 2 streams pipeline consecutive views; 1 stream serialises them (per-kernel timing)
+        # >= 2 streams pipeline consecutive views (4 by default: measured 118 / 121 / 123 step/s
+        # with 2 / 3 / 4 at c3); 1 stream serialises them (per-kernel timing)
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
