@@ -7,7 +7,7 @@ sc = scenes.config3(views=8)
 st = RenderSettings(near=0.2, mask_threshold=0.01, sh_mask_threshold=0.1)
 base = GaussianCloud.from_fields(sc.fields)
 targets = [torch.from_numpy(t).cuda() for t in sc.targets]
-for ns in (1, 2, 3, 4):
+for ns in (1, 2, 3, 4, 6, 8):
     cloud = GaussianCloud.from_fields(sc.fields)
     tr = Trainer(cloud, sc.cameras, targets, st, streams=ns)
     for _ in range(3): tr.step()
