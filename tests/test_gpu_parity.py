@@ -888,3 +888,19 @@ def test_trainer_host_targets_equal_device_targets(tgs):
         out.append((tr.cloud.flat.clone(), tr.terms.clone()))
     assert torch.equal(out[0][1], out[1][1])
     assert torch.equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("hw", [(11, 11), (13, 17), (33, 40), (31, 64), (45, 19)])
+def test_loss_small_and_odd_images(tgs, hw):
+    """The loss on images smaller than one 32x32 tile or one TMA halo box (42 x 44/48),
+    odd widths (padded partial row pitch): vs oracle/loss_ref.py."""
+    from oracle import loss_ref
+    from paper_2501_14534_b200 import loss
+    h, w = hw
+    rng = np.random.default_rng(h * 100 + w)
+    img = rng.uniform(0, 1, (h, w, 3)).astype(np.float32)
+    tgt = np.clip(img + rng.normal(0, 0.2, img.shape), 0, 1).astype(np.float32)
+    terms, d = loss.l1_ssim(torch.from_numpy(img).cuda(), torch.from_numpy(tgt).cuda(), 0.2)
+    l1, dssim, dref = loss_ref.total_loss_image(img, tgt, 0.2)
+    assert abs(terms["l1"] - l1) < 1e-6 and abs(terms["d_ssim"] - dssim) < 1e-5
+    np.testing.assert_allclose(_np(d), dref, rtol=1e-3, atol=1e-4 * np.abs(dref).max())
