@@ -62,8 +62,21 @@ __device__ __forceinline__ void gauss_static(const tgs_cloud &cl, int64_t i, con
       f.S[3 * a + b] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
 }
 
+// The SH-rest coefficients times their band masks (sh.py:152-160), once per Gaussian
+// (in place in its staged shared-memory row): the per-view colour sums then skip the
+// 45 mask products — the same float32 products, so the same bits.
+template <int DEG>
+__device__ __forceinline__ void premask_rest(float *rest, const GaussFwd &f) {
+  constexpr int K = (DEG + 1) * (DEG + 1) - 1;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rest[3 * k + c] = rest[3 * k + c] * f.band[band_of(k)];
+}
+
 // The view-dependent half: EWA projection, view direction and SH colour.  `f`
-// carries gauss_static's outputs (computed once per Gaussian for a batch of views).
+// carries gauss_static's outputs (computed once per Gaussian for a batch of views);
+// `rest` is the band-masked row (premask_rest).
 template <int DEG>
 __device__ __forceinline__ void gauss_view(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
                                            const tgs_settings &s, const float *rest, GaussFwd &f) {
@@ -116,13 +129,18 @@ __device__ __forceinline__ void gauss_view(const tgs_cloud &cl, int64_t i, const
   constexpr int K = (DEG + 1) * (DEG + 1) - 1;
   float b[15];
   sh_basis_rest(f.dir[0], f.dir[1], f.dir[2], b);
+  // (scalar on purpose: packed f32x2 multiply + add, even as explicit-rounding PTX,
+  // is fused into FFMA2 by ptxas under -fmad=false and would break the bit-exact
+  // forward — measured)
+  float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = acc[c] + b[k] * rest[3 * k + c];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc = acc + b[k] * (rest[3 * k + c] * f.band[band_of(k)]);
     float col = SH_C0 * cl.sh_dc[3 * i + c] + 0.5f;
-    if (DEG > 0) col = col + acc;
+    if (DEG > 0) col = col + acc[c];
     f.pre[c] = col;
     f.col[c] = max0(col);
   }
@@ -130,14 +148,15 @@ __device__ __forceinline__ void gauss_view(const tgs_cloud &cl, int64_t i, const
 
 template <int DEG>
 __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
-                                              const tgs_settings &s, const float *rest, GaussFwd &f) {
+                                              const tgs_settings &s, float *rest, GaussFwd &f) {
   gauss_static(cl, i, s, f);
+  if (DEG > 0) premask_rest<DEG>(rest, f);
   gauss_view<DEG>(cl, i, cam, s, rest, f);
 }
 
 template <int DEG>
 __device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
-                                               const tgs_settings &s, const float *rest, float *__restrict__ splats,
+                                               const tgs_settings &s, float *rest, float *__restrict__ splats,
                                                uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
                                                uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err);
 __device__ __forceinline__ void emit_record(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
@@ -146,7 +165,7 @@ __device__ __forceinline__ void emit_record(const tgs_cloud &cl, int64_t i, cons
                                             uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err);
 template <int DEG>
 __device__ __forceinline__ void emit_view(const tgs_cloud &cl, int64_t i, const tgs_camera &cam, const tgs_settings &s,
-                                          const float *rest, float *splats, uint8_t *visible, int32_t *tiles,
+                                          float *rest, float *splats, uint8_t *visible, int32_t *tiles,
                                           uint64_t *depth_keys, int32_t *err) {
   emit_view_impl<DEG>(cl, i, cam, s, rest, splats, visible, tiles, depth_keys, err);
 }
@@ -199,6 +218,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl
   GaussFwd f0;
   gauss_static(cl, i, s, f0);  // view-independent half once
   if (bulk) stage_rest_wait(&rest_bar);
+  if (DEG > 0) premask_rest<DEG>(rest_s + 45 * threadIdx.x, f0);  // this thread's row, once
   float amax = -1.0f;
   for (int v = 0; v < fv.nviews; ++v) {
     GaussFwd f = f0;
@@ -213,7 +233,7 @@ __global__ void __launch_bounds__(kPreBlock) k_preprocess_fwd_views(tgs_cloud cl
 // One Gaussian, one view: the projected record, visibility, tile count and depth key.
 template <int DEG>
 __device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
-                                               const tgs_settings &s, const float *rest, float *__restrict__ splats,
+                                               const tgs_settings &s, float *rest, float *__restrict__ splats,
                                                uint8_t *__restrict__ visible, int32_t *__restrict__ tiles,
                                                uint64_t *__restrict__ depth_keys, int32_t *__restrict__ err) {
   GaussFwd f;
