@@ -149,6 +149,7 @@ class Trainer:
         vis, parts = [], []
         main = torch.cuda.current_stream(self.cloud.device)
         copied = {}
+        n = len(self.cloud)
         if host_targets is not None:
             self.copy_stream.wait_stream(main)  # the previous step has finished reading the targets
             with torch.cuda.stream(self.copy_stream):
@@ -161,7 +162,6 @@ class Trainer:
         pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, stats=self.stats)
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
-        n = len(self.cloud)
         ts = int(self.settings.tile_size)
 
         def begin(i):  # view i's depth sort + instance-count read-back, on view i's stream
@@ -172,19 +172,21 @@ class Trainer:
                 return _bin_begin(sp, tiles, n, int(cam_.width), int(cam_.height), ts, 0, _tiles_y(cam_, ts), err,
                                   keys)
 
-        pend = begin(0) if self.views else None
+        # consecutive views rotate over the streams: the latency-bound binning of a view
+        # overlaps the blend / loss kernels of the others, and the next streams-1 views'
+        # depth sorts are queued before a view's instance count is awaited (the host round
+        # trip never leaves the GPU without work, also at the start of a step)
+        ahead = max(len(self.streams) - 1, 1)
+        pend = [begin(i) for i in range(min(ahead, len(self.views)))]
         for i, v in enumerate(self.views):
-            # consecutive views alternate between two streams: the latency-bound binning of
-            # view v overlaps the blend/loss kernels of view v-1, and view v+1's depth sort is
-            # queued before view v's instance count is awaited (the host round trip never
-            # leaves the GPU without work)
             st = self.streams[i % len(self.streams)]
-            nxt = begin(i + 1) if i + 1 < len(self.views) else None
+            if i + ahead < len(self.views):
+                pend.append(begin(i + ahead))
+            p_i = pend.pop(0)
             with torch.cuda.stream(st):
                 cam, target = self.cameras[v], self.targets[v]
-                bins = _bin_end(pend) if pend is not None else None
+                bins = _bin_end(p_i) if p_i is not None else None
                 out = render_forward(self.cloud, cam, self.settings, pre=pres[i], bins=bins)
-            pend = nxt
             with torch.cuda.stream(st):
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
                 if d is None:
