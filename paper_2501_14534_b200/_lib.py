@@ -15,7 +15,8 @@ import numpy as np
 from .errors import ContractViolationError, NativeLibraryError, raise_for_status
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtgs.so")
+# TGS_LIB: load another build of the library (A/B timing of kernel variants, profiles/)
+LIB_PATH = os.environ.get("TGS_LIB") or os.path.join(PKG, "libtgs.so")
 
 _P = ctypes.c_void_p
 _SZ = ctypes.c_size_t

@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(LossArgs A) {
   block_sum2(l1, ss, A.sums + bid, A.sums + nb + bid);
 }
 
-__global__ void __launch_bounds__(kLossThreads) k_ssim_adj(LossArgs A, const __grid_constant__ CUtensorMap tm01,
+// Four CTAs per SM (64 registers, 40 B of spills): 175 -> 159 us per c3 loss call and
+// +2.4% training step/s against the unconstrained 79-register build (3 CTAs per SM)
+__global__ void __launch_bounds__(kLossThreads, 4) k_ssim_adj(LossArgs A, const __grid_constant__ CUtensorMap tm01,
                                                          const __grid_constant__ CUtensorMap tm2) {
   // partials (p0, p1) as a packed pair + p2 scalar: two FFMA2 + one FFMA per tap
   // instead of three FFMA, bit-identical per component.  The tile + 5 px halo of the
