@@ -13,8 +13,12 @@ st = RenderSettings(near=0.2, mask_threshold=0.01, sh_mask_threshold=0.1)
 cloud = GaussianCloud.from_fields(sc.fields)
 target = torch.from_numpy(sc.targets[0]).cuda()
 for it in range(3):
+    if it == 2:  # ncu --profile-from-start off captures the last (warm) iteration only
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     out = render_forward(cloud, sc.cameras[0], st)
     terms, d = loss.l1_ssim(out.image, target)
     g = render_backward(cloud, sc.cameras[0], st, d, out)
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
 print("ok", terms)
