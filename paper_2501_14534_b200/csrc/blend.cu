@@ -665,10 +665,11 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   const float2 w6 = __fmul2_rn(P.g0, w), w7 = __fmul2_rn(P.g1, w), w8 = __fmul2_rn(P.g2, w);
   // partials through the unclamped alpha only (a_raw <= ALPHA_MAX)
   const bool uA = okA && a_raw.x <= kAlphaMax, uB = okB && a_raw.y <= kAlphaMax;
-  const float2 gm = make_float2(uA ? gauss.x : 0.0f, uB ? gauss.y : 0.0f);
-  const float2 gam = make_float2(uA ? ga.x : 0.0f, uB ? ga.y : 0.0f);
-  const float2 v5 = __fmul2_rn(gam, gm);
-  const float2 gG = __fmul2_rn(__fmul2_rn(gam, f2(cn.w)), gm);
+  // dL/dalpha_raw-side product ga * G, masked once (a select discards the NaN / Inf an
+  // out-of-range Gaussian factor can give)
+  const float2 gx = __fmul2_rn(ga, gauss);
+  const float2 v5 = make_float2(uA ? gx.x : 0.0f, uB ? gx.y : 0.0f);
+  const float2 gG = __fmul2_rn(v5, f2(cn.w));
   const float2 v0 = __ffma2_rn(f2(cn.y), dy, f2(cn.x * dx)), v1 = __ffma2_rn(f2(cn.z), dy, f2(cn.y * dx));
   const float2 hG = __fmul2_rn(gG, f2(0.5f));
   const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
