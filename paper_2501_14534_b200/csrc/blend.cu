@@ -656,12 +656,15 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   const float2 al = make_float2(fminf(a_raw.x, kAlphaMax), fminf(a_raw.y, kAlphaMax));
   const bool okA = pos < P.lA && !(e2.x < kE2Min || e2.x > 0.0f) && !(al.x < kAlphaSkip);
   const bool okB = pos < P.lB && !(e2.y < kE2Min || e2.y > 0.0f) && !(al.y < kAlphaSkip);
-  const float2 om = __fadd2_rn(f2(1.0f), make_float2(-al.x, -al.y));  // 1 - al >= 0.01
-  const float2 inv = make_float2(okA ? rcp_approx(om.x) : 1.0f, okB ? rcp_approx(om.y) : 1.0f);
+  // a pixel that skips the entry blends alpha 0: 1 / (1 - 0) is exactly 1 (rcp.approx of
+  // 1.0f is exact, profiles/tma_dbg/rcp_one.cu), so T and the weights need no more selects
+  const float2 alm = make_float2(okA ? al.x : 0.0f, okB ? al.y : 0.0f);
+  const float2 om = __fadd2_rn(f2(1.0f), make_float2(-alm.x, -alm.y));  // 1 - al >= 0.01
+  const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
   const float2 tb = __fmul2_rn(P.T, inv);  // T before this entry
   const float2 gc = __ffma2_rn(P.g2, f2(col.z), __ffma2_rn(P.g1, f2(col.y), __fmul2_rn(P.g0, f2(col.x))));
   const float2 ga = __ffma2_rn(gc, tb, __fmul2_rn(P.GS, make_float2(-inv.x, -inv.y)));
-  const float2 w = __fmul2_rn(make_float2(okA ? al.x : 0.0f, okB ? al.y : 0.0f), tb);
+  const float2 w = __fmul2_rn(alm, tb);
   const float2 w6 = __fmul2_rn(P.g0, w), w7 = __fmul2_rn(P.g1, w), w8 = __fmul2_rn(P.g2, w);
   // partials through the unclamped alpha only (a_raw <= ALPHA_MAX)
   const bool uA = okA && a_raw.x <= kAlphaMax, uB = okB && a_raw.y <= kAlphaMax;
