@@ -19,7 +19,8 @@
 //               dL/da = (1-lam) sign(a-b)/N - lam/2 (G'd0 + 2a G'd1 + b G'd2)/N.
 // Splitting at the partials removes the fused kernel's second 10 px halo (the
 // forward maps no longer have to cover the adjoint's footprint) and keeps each
-// CTA's shared memory under 42 KB, so five CTAs share an SM.
+// CTA's shared memory under 44 KB: the forward runs four CTAs per SM (shared-memory
+// carveout 80%, the rest L1), the adjoint four (launch bound: 64 registers).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
