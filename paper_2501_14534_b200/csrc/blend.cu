@@ -673,7 +673,8 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   const float2 gx = __fmul2_rn(ga, gauss);
   const float2 v5 = make_float2(uA ? gx.x : 0.0f, uB ? gx.y : 0.0f);
   const float2 gG = __fmul2_rn(v5, f2(cn.w));
-  const float2 v0 = __ffma2_rn(f2(cn.y), dy, f2(cn.x * dx)), v1 = __ffma2_rn(f2(cn.z), dy, f2(cn.y * dx));
+  const float2 cx = __fmul2_rn(make_float2(cn.x, cn.y), f2(dx));  // (a dx, b dx) in one FMUL2
+  const float2 v0 = __ffma2_rn(f2(cn.y), dy, f2(cx.x)), v1 = __ffma2_rn(f2(cn.z), dy, f2(cx.y));
   const float2 hG = __fmul2_rn(gG, f2(0.5f));
   const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
   const float2 p2 = __fmul2_rn(__fmul2_rn(hG, v0), v0), p3 = __fmul2_rn(p0, v1);
