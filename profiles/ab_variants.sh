@@ -1,6 +1,6 @@
 # A/B of kernel-variant builds (profiles/variants/*.so, built with -D overrides of the
 # launch bounds) on the c3 bench: step/s, render FPS and the per-launch stage times.
-# Usage: bash profiles/ab_variants.sh variants/a.so variants/b.so ...  (default build first and last)
+# Usage (repo root): bash profiles/ab_variants.sh profiles/variants/a.so profiles/variants/b.so ...  (default build first and last)
 # Building a variant (here: loss.cu with -DNAME=VALUE; the kernel reads the macro):
 #   cd paper_2501_14534_b200/csrc && make
 #   F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
