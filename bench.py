@@ -67,7 +67,9 @@ def config_dict(n, world):
             "views_per_step": VIEWS, "resolution": "1920x1080", "tile": 16, "loss": "0.8*L1 + 0.2*D-SSIM (11x11)",
             "mask_threshold": 0.01, "sh_mask_threshold": 0.1, "optimizer": "Adam, 8 groups",
             "parallelism": f"dp{world} (views sharded, NCCL all-reduce of the flat gradient buffer)",
-            "l2": "inputs larger than L2: params+grads+Adam moments = 1.0 GB touched per step"}
+            "l2": "inputs larger than L2: params+grads+Adam moments = 1.0 GB touched per step",
+            "timing": "fixed workload: each timed step starts from the initial parameters and Adam state "
+                      "(restored outside the step's CUDA events); per-step device times summed, max over ranks"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -156,22 +158,34 @@ def stage_bytes(n, vis_n, inst, entries, pixels, views):
     }
 
 
-# per-stage limiter measured with ncu (profiles/r01_ncu_summary.txt): the blend stages are
-# bound by instruction issue (packed-FP32 arithmetic, barrier-free warps), not by HBM; the
-# issue-slot utilisation comes from the same capture (profiles/r01_ncu_traffic.json)
-LIMITER = {"blend_bwd": "instruction issue (packed FP32, barrier-free warps; ncu issue slots busy {pct}%)",
-           "blend_fwd": "instruction issue (packed FP32; ncu issue slots busy {pct}%)"}
+# Stages whose roof is instruction issue, not HBM (ncu: issue slots ~75% busy, DRAM ~3% of
+# peak; the splat records they stage are L2-served): packed-FP32 per-pixel arithmetic with
+# barrier-free warps.  Their roofline is the SM issue rate, 148 SMs x 4 schedulers x one
+# warp instruction per clock at the measured SM clock.
+ISSUE_BOUND = {"blend_fwd", "blend_bwd"}
+SMS, SCHEDULERS = 148, 4
 
 
 def ncu_stage(stage):
-    """The stage's entry in the committed ncu --set full capture (profiles/r01_ncu_traffic.json)."""
-    try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json"))).get(stage, {})
-    except (OSError, ValueError):
-        return {}
+    """The stage's entry in the newest committed ncu --set full capture
+    (profiles/r0N_ncu_traffic.json, written by profiles/ncu_summary.py)."""
+    for rnd in ("r02", "r01"):
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_traffic.json")))
+        except (OSError, ValueError):
+            continue
+        if stage in d:
+            return dict(d[stage], capture=f"profiles/{rnd}_ncu_traffic.json")
+    return {}
 
 
-def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: str) -> tuple[dict, dict]:
+def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: str, pairs: float,
+             sm_mhz) -> tuple[dict, dict]:
+    """Per-stage achieved bytes/s (algorithmic bytes over the live CUDA-event time) and the
+    roofline object of the dominant stage by device time.  For an issue-bound stage the
+    roofline is the SM issue rate (achieved = the stage's executed warp instructions per
+    launch from the committed ncu capture / the live launch time), with the HBM view
+    (algorithmic and DRAM bytes) and the evaluated (pixel, splat) pairs per second beside it."""
     stages = {}
     for k, ms in prof_ms.items():
         c = counts.get(k, 0)
@@ -181,19 +195,37 @@ def roofline(prof_ms: dict, counts: dict, sbytes: dict, peak: float, peak_kind: 
         per = ms / c
         gbs = sbytes[k] / (per * 1e-3) / 1e9
         stages[k] = {"ms_per_launch": round(per, 4), "launches": c, "ms_total": round(ms, 4),
-                     "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
-    dom = max((k for k in stages if "achieved_gbs" in stages[k]), key=lambda k: stages[k]["ms_total"])
+                     "algorithmic_gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                     "bound": "issue" if k in ISSUE_BOUND else "hbm"}
+        nc = ncu_stage(k)
+        if nc.get("dram_bytes_per_launch"):
+            stages[k]["dram_gbs"] = round(nc["dram_bytes_per_launch"] / (per * 1e-3) / 1e9, 1)
+            stages[k]["dram_frac"] = round(stages[k]["dram_gbs"] / peak, 4)
+        for key in ("issue_busy_pct", "fma_pipe_pct"):
+            if nc.get(key) is not None:
+                stages[k][key] = nc[key]
+    dom = max((k for k in stages if "algorithmic_gbs" in stages[k]), key=lambda k: stages[k]["ms_total"])
     d = stages[dom]
     nc = ncu_stage(dom)
-    rf = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbs"], "peak": peak, "unit": "GB/s",
-          "frac": d["frac"], "traffic": nc.get("dram_bytes_per_launch"), "peak_source": peak_kind,
-          "algorithmic_bytes": sbytes[dom]}
-    if dom in LIMITER:
-        # the stage's real roof: instruction issue (ncu issue-slot utilisation, same capture)
-        pct = nc.get("issue_busy_pct")
-        rf["limiter"] = LIMITER[dom].format(pct=pct if pct is not None else "?")
-        if pct is not None:
-            rf["issue_frac"] = round(pct / 100.0, 3)
+    per_s = d["ms_per_launch"] * 1e-3
+    hbm = {"algorithmic_bytes": int(sbytes[dom]), "algorithmic_gbs": d["algorithmic_gbs"],
+           "frac_algorithmic": d["frac"], "dram_bytes_per_launch": nc.get("dram_bytes_per_launch"),
+           "dram_gbs": d.get("dram_gbs"), "frac_dram": d.get("dram_frac"), "peak_gbs": peak, "peak_source": peak_kind}
+    if dom in ISSUE_BOUND and nc.get("warp_insts") and sm_mhz:
+        achieved = nc["warp_insts"] / per_s / 1e9
+        ipk = SMS * SCHEDULERS * float(sm_mhz) * 1e6 / 1e9
+        rf = {"kernel": dom, "bound": "issue", "achieved": round(achieved, 1), "peak": round(ipk, 1),
+              "unit": "Gwarp-inst/s", "frac": round(achieved / ipk, 4),
+              "traffic": nc.get("dram_bytes_per_launch"),
+              "peak_source": f"{SMS} SMs x {SCHEDULERS} schedulers x 1 warp-inst/clk at the measured "
+                             f"median SM clock {sm_mhz} MHz",
+              "warp_insts_per_launch": nc["warp_insts"], "ncu_issue_busy_pct": nc.get("issue_busy_pct"),
+              "ncu_fma_pipe_pct": nc.get("fma_pipe_pct"), "ncu_capture": nc.get("capture"),
+              "pairs_per_launch": int(pairs), "pairs_per_s": round(pairs / per_s / 1e9, 2),
+              "pairs_unit": "G (pixel, list entry) pairs/s: sum over pixels of last_pos", "hbm": hbm}
+    else:
+        rf = {"kernel": dom, "bound": "hbm", "achieved": d["algorithmic_gbs"], "peak": peak, "unit": "GB/s",
+              "frac": d["frac"], "traffic": nc.get("dram_bytes_per_launch"), "peak_source": peak_kind, "hbm": hbm}
     return rf, stages
 
 
@@ -232,6 +264,27 @@ def cpu_adam_seconds(n_floats):
     return time.perf_counter() - t
 
 
+def host_info() -> dict:
+    """The CPU the baseline ran on (lscpu model, cores) and the BLAS/OpenMP thread environment."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    if model is None:
+        try:
+            model = next(line.split(":", 1)[1].strip() for line in open("/proc/cpuinfo") if line.startswith("model name"))
+        except (OSError, StopIteration):
+            model = "unknown"
+    env = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                          "NUMBA_NUM_THREADS")}
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "thread_env": env, "numpy": np.__version__}
+
+
 def cpu_baseline(sc, st, views_to_time=1):
     """Bounded sample: `views_to_time` view-steps on 1 core, scaled to the 8-view step."""
     t0 = time.perf_counter()
@@ -240,7 +293,7 @@ def cpu_baseline(sc, st, views_to_time=1):
     t_view = (time.perf_counter() - t0) / views_to_time
     t_adam = cpu_adam_seconds(sc.n * 63)
     t_step = VIEWS * t_view + t_adam
-    return {"value": round(1.0 / t_step, 6), "unit": "train step/s", "cores": 1, "kind": "port",
+    return {"value": round(1.0 / t_step, 6), "unit": "train step/s", "cores": 1, "kind": "port", "host": host_info(),
             "sample": f"{views_to_time} of 8 views (fwd+loss+bwd, float64 oracle/oracle.cpp) timed "
                       f"({t_view:.1f} s/view) + numpy Adam over {sc.n * 63} floats ({t_adam:.1f} s); "
                       f"step = 8 x view + Adam = {t_step:.1f} s"}
@@ -276,6 +329,7 @@ def reference_arm(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE.json config 3 generator)", "config": config_dict(args.n, 1),
             "cpu_baseline": {"value": round(v, 6), "unit": "train step/s", "cores": workers, "kind": "port",
+                             "host": host_info(),
                              "sample": f"full 8-view step: views in {workers} threads of the float64 oracle "
                                        f"(oracle/oracle.cpp + oracle/loss_ref.py), numpy Adam; "
                                        f"{steps} timed step(s) after 1 warm-up"},
@@ -325,6 +379,7 @@ def main():
             dist.barrier()
 
     def timed(k, body):
+        """K consecutive steps bracketed by one event pair (the scene evolves under training)."""
         torch.cuda.synchronize()
         barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -339,9 +394,10 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
-    # Every timed region starts from the same initial parameters and Adam state: training
-    # changes the scene (e.g. the reference's mask lr 0.5 prunes Gaussians within a few
-    # steps), so regions timed after other steps would measure a lighter workload.
+    # A FIXED workload: training changes the scene (the reference's mask lr of 0.5 prunes
+    # occluded Gaussians within ~13 steps), so every timed step starts from the same initial
+    # parameters and Adam state, restored before the step and outside its events; the
+    # per-step device times are summed (max over ranks of the sum).
     init = (cloud.flat.clone(), trainer.opt.m.clone(), trainer.opt.v.clone(), dict(trainer.opt.steps))
 
     def reset(tr):
@@ -351,14 +407,39 @@ def main():
         tr.opt.steps = dict(init[3])
         torch.cuda.synchronize()
 
+    def timed_fixed(k, body, tr):
+        total, inst = 0.0, []
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(k):
+            reset(tr)
+            barrier()
+            s.record()
+            body()
+            e.record()
+            e.synchronize()
+            total += s.elapsed_time(e) / 1e3
+            inst.append(sum(tr.instances))
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([total], device=dev)
+        if pg is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t), inst
+
     for _ in range(args.warmup):
         trainer.step()
-    reset(trainer)
-    # ---- device-resident timed region (inputs already in HBM), views pipelined on 2 streams
+    trainer.check_divergence()
+    # ---- device-resident timed region (inputs already in HBM), views pipelined on 4 streams
     with ClockSampler(local) as clk:
-        t_dev = timed(args.steps, trainer.step)
+        t_dev, inst_steps = timed_fixed(args.steps, trainer.step, trainer)
     clocks = clk.summary()
+    trainer.check_divergence()
     value = args.steps / t_dev
+    # the same K steps back to back without the per-step restore (the scene prunes itself
+    # as it trains): reported for comparison only
+    reset(trainer)
+    t_cont = timed(args.steps, trainer.step)
+    trainer.check_divergence()
     # ---- end-to-end through the public API: targets H2D from pinned host memory, loss D2H
     terms_host = torch.empty((VIEWS, 2), dtype=torch.float64).pin_memory()
 
@@ -368,32 +449,34 @@ def main():
         terms_host.copy_(trainer.terms, non_blocking=True)
 
     e2e_step()
-    reset(trainer)
-    t_e2e = timed(args.steps, e2e_step)
+    t_e2e, _ = timed_fixed(args.steps, e2e_step, trainer)
+    trainer.check_divergence()
     h2d = sum(host_targets[v].numel() * 4 for v in views)
     d2h = terms_host.numel() * 8
 
-    # ---- per-kernel roofline: the same step with views serialised on one stream, so the
-    # CUDA-event duration of each stage is its own (no overlap with the other view)
+    # ---- per-kernel roofline: the same fixed-workload steps with views serialised on one
+    # stream, so the CUDA-event duration of each stage is its own (no overlap with the other
+    # views)
     serial = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, process_group=pg, views=views, streams=1)
     serial.opt = trainer.opt
     serial.step()
-    reset(serial)
     with profiler.StageTimer() as prof:
-        t_serial = timed(args.steps, serial.step)
+        t_serial, _ = timed_fixed(args.steps, serial.step, serial)
     reset(serial)
     from paper_2501_14534_b200.rasterizer import render_forward
-    inst, ents, vis = [], [], []
+    inst, ents, vis, pairs = [], [], [], []
     for v in views:
         out = render_forward(cloud, sc.cameras[v], st)
         inst.append(int(out._tiles.indices.numel()))
         tt = out._state.tiles_touched[: len(cloud)]
         vis.append(int((tt > 0).sum()))
         ents.append(super_tile_entries(out._state.splats[: len(cloud)], tt, w, h))
-    inst_mean, ent_mean, vis_n = (sum(x) / len(x) for x in (inst, ents, vis))
+        pairs.append(int(out.last_pos.to(torch.int64).sum()))  # per-pixel list entries walked
+    inst_mean, ent_mean, vis_n, pairs_mean = (sum(x) / len(x) for x in (inst, ents, vis, pairs))
     pk, pk_kind = peaks()
     sb = stage_bytes(len(cloud), vis_n, inst_mean, ent_mean, h * w, VIEWS)
-    rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind)
+    rf, stages = roofline(prof.durations_ms(), prof.counts(), sb, float(pk["hbm_gbs"]), pk_kind, pairs_mean,
+                          clocks.get("sm_mhz"))
     launches = trainer_launches(prof.counts(), args.steps)
 
     # ---- render FPS (forward only, initial scene) as a secondary number: this rank's views
@@ -420,8 +503,11 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
             "ms_per_step_serial_views": round(t_serial / args.steps * 1e3, 3),
+            "ms_per_step_continuous": round(t_cont / args.steps * 1e3, 3),
             "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean),
-            "entries_per_view": int(ent_mean), "selected_per_view": int(vis_n)}
+            "instances_per_step_first_last": [inst_steps[0], inst_steps[-1]] if inst_steps else None,
+            "entries_per_view": int(ent_mean), "selected_per_view": int(vis_n),
+            "pairs_per_view": int(pairs_mean)}
     if world == 1 and not args.no_cpu_baseline:
         from types import SimpleNamespace
         line["cpu_baseline"] = cpu_baseline(sc, SimpleNamespace(record_hits=False, **settings_kwargs()))

@@ -25,6 +25,8 @@
  *   tgs_adam_step            optim.Adam.update (optim.py:37-49)
  *   tgs_gather_rows          cloud.take / Adam.compact row compaction
  *                            (cloud.py:86-89, optim.py:51-55)
+ *   tgs_select_rows          the np.nonzero row selection of the prunings
+ *                            (masking.py:70-81, significance.py:81-99)
  *   tgs_significance_scores  significance.significance_scores (significance.py:45-78)
  *   tgs_significance_keep    significance.prune_by_significance's row selection
  *                            (significance.py:81-99)
@@ -258,11 +260,15 @@ TGS_API int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *ca
  * the chains after the screen-space partials are linear, so view-independent
  * work (covariance/quaternion/scale/opacity/mask) runs once per Gaussian.
  * stats (may be NULL): grad_accum / grad_count take every view's screen-space
- * mean gradient norm (the densification statistics of each view's step). */
+ * mean gradient norm (the densification statistics of each view's step).
+ * clear_partials != 0: every dsplats[v] (then writable, 16 B aligned) is zeroed
+ * after it has been read, so a training loop's next blend backward accumulates
+ * into it without a separate fill. */
 TGS_API int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                           const uint8_t *const *visible, const float *const *dsplats,
                                           int32_t nviews, tgs_grads *grads, int32_t accumulate,
-                                          const tgs_densify_stats *stats, tgs_stream_t stream);
+                                          const tgs_densify_stats *stats, int32_t clear_partials,
+                                          tgs_stream_t stream);
 
 /* ---- (6) loss: (1-lambda)*L1 + lambda*(1-SSIM)/2, 11x11 sigma 1.5 window,
  * symmetric padding (training.py:76-89, metrics.py:138-188).  image/target
@@ -284,12 +290,17 @@ TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, i
  * corrections.  kinds[k] = 1 adds the Gaussian-mask penalty gradient
  * lambda_m * sigmoid'(m) / n, kinds[k] = 2 the SH-band-mask penalty
  * lambda_sh * sigmoid'(m_l) * band_weights[l] / n (masking.py:60-67), to that
- * group's gradient before the update (written back to grad). */
+ * group's gradient before the update (written back to grad).
+ * Divergence guard (training.py:298-308): with n_terms > 0, if any of the
+ * n_terms doubles at loss_terms (device) is not finite, NOTHING is updated and
+ * *nonfinite_flag (device int32, may be NULL) is set to 1; the host raises
+ * DivergenceError from it. */
 TGS_API int tgs_adam_step_groups(float *param, float *grad, float *m, float *v, int32_t ngroups,
                                  const int64_t *offsets, const int64_t *sizes, const float *lrs,
                                  const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
                                  float beta2, float eps, float lambda_m, float lambda_sh,
-                                 const float *band_weights, int64_t n_gaussians, tgs_stream_t stream);
+                                 const float *band_weights, int64_t n_gaussians, const double *loss_terms,
+                                 int32_t n_terms, int32_t *nonfinite_flag, tgs_stream_t stream);
 
 /* ---- target-side progressive ops (images.py:58-102), (H, W, 3) float32.
  * area_resize: exact fractional box filter (downsampling only); workspace
@@ -304,6 +315,15 @@ TGS_API int tgs_gaussian_blur(const float *in, int32_t h, int32_t w, int32_t siz
  * rows of `row_floats` floats. */
 TGS_API int tgs_gather_rows(const float *in, float *out, const int64_t *keep, int64_t n_keep,
                     int32_t row_floats, tgs_stream_t stream);
+
+/* Row selection for the compactions (np.nonzero of masking.prune_by_mask,
+ * masking.py:70-81, and of significance.prune_by_significance, significance.py:
+ * 81-99): writes the rows i with flags[i] != 0 — or, with flags == NULL, with
+ * x[i] > threshold — in ascending order to indices (capacity n) and their number
+ * to *count (device int64).  n < 2^30.  Workspace: tgs_select_rows_workspace. */
+TGS_API int tgs_select_rows_workspace(int64_t n, size_t *bytes);
+TGS_API int tgs_select_rows(const uint8_t *flags, const float *x, float threshold, int64_t n, int64_t *indices,
+                            int64_t *count, void *workspace, size_t workspace_bytes, tgs_stream_t stream);
 
 /* Significance (significance.py:45-99).  Workspace: one u64 key per row + a
  * small selection state.  tgs_significance_scores writes, for every row,

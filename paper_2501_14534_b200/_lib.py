@@ -81,13 +81,15 @@ _SIGS = {
                                          _I32),
     "tgs_blend_backward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
-    "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P, _P], _I32),
+    "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P, _I32, _P], _I32),
     "tgs_loss_workspace": ([_I32, _I32, _P], _I32),
     "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
     "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),
-    "tgs_adam_step_groups": ([_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _P, _I64, _P],
-                             _I32),
+    "tgs_adam_step_groups": ([_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _P, _I64, _P, _I32,
+                              _P, _P], _I32),
     "tgs_gather_rows": ([_P, _P, _P, _I64, _I32, _P], _I32),
+    "tgs_select_rows_workspace": ([_I64, _P], _I32),
+    "tgs_select_rows": ([_P, _P, _F, _I64, _P, _P, _P, _SZ, _P], _I32),
     "tgs_significance_workspace": ([_I64, _P], _I32),
     "tgs_significance_scores": ([_P, _P, _F, _F, _I64, _P, _P, _P, _P, _SZ, _P], _I32),
     "tgs_significance_keep": ([_P, _I64, _I64, _P, _P, _SZ, _P], _I32),

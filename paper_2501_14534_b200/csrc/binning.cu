@@ -1332,11 +1332,11 @@ extern "C" int tgs_bin_gaussians(const float *splats, const int32_t *tiles_touch
   a.T0 = w.T0;
   a.TP = w.TP;
   a.num_instances = nullptr;
-  static bool attr_done = false;  // idempotent function attribute, set once per process
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsSmem));
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  const int arc = attr_once_per_device(attr_done, [] {
+    return cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsSmem));
+  });
+  if (arc != TGS_OK) return arc;
   const unsigned fg = (unsigned)tmin<uint64_t>((uint64_t)w.T0 + kDsPasses * w.TP, 148 * 3);
   k_depth_sort<<<fg, kDsThreads, sizeof(DsSmem), st>>>(a, &w.bctl->overflow);
   return launch_status();
@@ -1373,12 +1373,14 @@ extern "C" int tgs_bin_instances(const float *splats, int64_t n, int32_t width, 
   GaussWS gw = carve_gauss(gauss_workspace, n);
   InstWS w = carve_inst(workspace, g);
   const uint32_t *d_m = &gw.bctl->m;
-  static bool attr_done = false;  // idempotent function attributes, set once per process
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(k_seg_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDiffCells * 4);
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  const int arc = attr_once_per_device(attr_done, [] {
+    const cudaError_t e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    return e != cudaSuccess ? e
+                            : cudaFuncSetAttribute(k_seg_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   2 * kDiffCells * 4);
+  });
+  if (arc != TGS_OK) return arc;
   cudaMemsetAsync(static_cast<char *>(workspace) + w.zero_off, 0, w.zero_bytes, st);
   k_seg_count<<<dim3(g.nseg, g.slabs), 256, cnt_smem, st>>>(gw.rects_sorted, d_m, g.sx, g.slab_rows, g.sy, w.rel,
                                                            w.segsum, w.chunk_ent);

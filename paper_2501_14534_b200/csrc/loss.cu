@@ -475,14 +475,14 @@ extern "C" int tgs_loss_l1_ssim(const float *image, const float *target, int32_t
   if (rc == TGS_OK) rc = partial_map(&tm2, A.part2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, width, height, P, kBoxW2);
   if (rc != TGS_OK) return rc;
   const dim3 grd(3, (unsigned)ceil_div(width, kT), (unsigned)ceil_div(height, kT));
-  static bool carve = false;  // idempotent function attribute, set once
-  if (!carve) {
-    // four 44 KB CTAs per SM and the rest of the unified L1 as cache for the reflected
-    // image / target loads the three channel CTAs of a tile share (a fifth CTA would
-    // shrink that cache and costs more than its occupancy gains)
-    cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributePreferredSharedMemoryCarveout, 80);
-    carve = true;
-  }
+  // four 44 KB CTAs per SM and the rest of the unified L1 as cache for the reflected
+  // image / target loads the three channel CTAs of a tile share (a fifth CTA would
+  // shrink that cache and costs more than its occupancy gains)
+  static std::atomic<uint64_t> carve{0};
+  rc = attr_once_per_device(carve, [] {
+    return cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributePreferredSharedMemoryCarveout, 80);
+  });
+  if (rc != TGS_OK) return rc;
   k_ssim_fwd<<<grd, kLossThreads, 0, st>>>(A);
   k_ssim_adj<<<grd, kLossThreads, 0, st>>>(A, tm01, tm2);
   k_loss_finalize<<<1, 1024, 0, st>>>(A.sums, (int)loss_blocks(width, height), 1.0 / (double)count, terms);

@@ -56,10 +56,31 @@ struct AdamGroupArgs {
   int kind[8];         // 0: plain, 1: Gaussian-mask penalty, 2: SH-band-mask penalty
   int ngroups;
   float b1, b2, eps, lam_m, lam_sh, inv_n, wband[3];
+  const double *terms;  // optional divergence guard: loss terms of this step (nterms doubles)
+  int nterms;
+  int32_t *nonfinite;   // set to 1 (and no parameter touched) when a term is not finite
 };
+
+// training.py:298-308 raises DivergenceError BEFORE the backward's results reach the
+// optimizer when the loss is not finite; on the device the same guard skips the whole
+// update (parameters and moments stay as they were) and raises a flag the host reads.
+__device__ __forceinline__ bool loss_nonfinite(const AdamGroupArgs &a) {
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) {
+    int bad = 0;
+    for (int i = 0; i < a.nterms; ++i) bad |= !isfinite(a.terms[i]);
+    s_bad = bad;
+  }
+  __syncthreads();
+  return s_bad != 0;
+}
 
 __global__ void __launch_bounds__(256) k_adam_groups(float *__restrict__ p, float *__restrict__ g,
                                                      float *__restrict__ m, float *__restrict__ v, AdamGroupArgs a) {
+  if (a.terms && loss_nonfinite(a)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.nonfinite) *a.nonfinite = 1;
+    return;
+  }
   // float4 chunks from the first group's start to the padded end of the last one
   // (groups need not start at 0: a data-parallel bucket steps a subset of the groups)
   const int64_t c0 = a.off[0] / 4, n4 = a.off[a.ngroups] / 4;
@@ -109,6 +130,75 @@ __global__ void k_gather_rows(const float *__restrict__ in, float *__restrict__ 
   }
 }
 
+// Stream compaction of the kept rows (masking.prune_by_mask's np.nonzero, masking.py:70-81;
+// significance.prune_by_significance's, significance.py:81-99): row i is kept when
+// flags[i] != 0, or (flags == NULL) when x[i] > thr.  One launch: tiles of 4096 rows
+// take tickets in launch order, scan their keep counts in the block and chain the tile
+// prefixes by decoupled look-back (30-bit payloads), then write the kept row numbers in
+// ascending order; the total lands in *count.
+constexpr uint32_t kSelAgg = 1u << 30, kSelInc = 2u << 30, kSelMask = (1u << 30) - 1;
+constexpr int kSelItems = 16, kSelThreads = 256, kSelTile = kSelItems * kSelThreads;
+
+__global__ void __launch_bounds__(kSelThreads) k_select_rows(const uint8_t *__restrict__ flags,
+                                                             const float *__restrict__ x, float thr, int64_t n,
+                                                             int64_t *__restrict__ idx, int64_t *__restrict__ count,
+                                                             uint32_t *__restrict__ status,
+                                                             uint32_t *__restrict__ ticket) {
+  __shared__ uint32_t ws[kSelThreads / 32], s_tile, s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kSelTile + (int64_t)threadIdx.x * kSelItems;
+  uint32_t keep = 0u;  // bit k: row base + k is kept
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    const int64_t r = base + k;
+    const bool on = r < n && (flags ? flags[r] != 0 : x[r] > thr);
+    keep |= (on ? 1u : 0u) << k;
+  }
+  const uint32_t mine = __popc(keep);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  uint32_t woff = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSelThreads / 32; ++w) {
+    if (w < warp) woff += ws[w];
+    tot += ws[w];
+  }
+  if (threadIdx.x == 0) {
+    uint32_t excl = 0;
+    if (tile == 0) {
+      atomicExch(status, kSelInc | tot);
+    } else {
+      atomicExch(status + tile, kSelAgg | tot);
+      for (int j = (int)tile - 1;; ) {
+        const uint32_t sv = atomicAdd(status + j, 0u);
+        if ((sv >> 30) == 0) continue;  // predecessor not published yet (it holds an earlier ticket)
+        excl += sv & kSelMask;
+        if (sv & kSelInc) break;
+        --j;
+      }
+      atomicExch(status + tile, kSelInc | (excl + tot));
+    }
+    s_excl = excl;
+    if ((int64_t)(tile + 1) * kSelTile >= n) *count = (int64_t)(excl + tot);  // the last tile
+  }
+  __syncthreads();
+  int64_t out = (int64_t)s_excl + woff + inc - mine;
+  while (keep) {
+    const int k = __ffs(keep) - 1;
+    keep &= keep - 1;
+    idx[out++] = base + k;
+  }
+}
+
 }  // namespace tgs
 
 using namespace tgs;
@@ -143,9 +233,10 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
                                     const int64_t *offsets, const int64_t *sizes, const float *lrs,
                                     const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
                                     float beta2, float eps, float lambda_m, float lambda_sh,
-                                    const float *band_weights, int64_t n_gaussians, tgs_stream_t stream) {
+                                    const float *band_weights, int64_t n_gaussians, const double *loss_terms,
+                                    int32_t n_terms, int32_t *nonfinite_flag, tgs_stream_t stream) {
   if (ngroups < 1 || ngroups > 8 || !param || !grad || !m || !v || !offsets || !sizes || !lrs || !bias_c1 ||
-      !bias_c2 || !kinds || n_gaussians < 0)
+      !bias_c2 || !kinds || n_gaussians < 0 || n_terms < 0 || (n_terms > 0 && !loss_terms))
     return TGS_ERR_INVALID;
   if (((reinterpret_cast<uintptr_t>(param) | reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(m) |
         reinterpret_cast<uintptr_t>(v)) & 15) != 0)
@@ -170,6 +261,9 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
   a.lam_sh = lambda_sh;
   a.inv_n = n_gaussians > 0 ? 1.0f / (float)n_gaussians : 0.0f;
   for (int l = 0; l < 3; ++l) a.wband[l] = band_weights ? band_weights[l] : 0.0f;
+  a.terms = n_terms > 0 ? loss_terms : nullptr;
+  a.nterms = n_terms;
+  a.nonfinite = nonfinite_flag;
   const int64_t n4 = a.off[ngroups] / 4 - a.off[0] / 4;
   if (n4 <= 0) return TGS_OK;
   const unsigned grid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n4, 256), 148 * 8);
@@ -183,5 +277,28 @@ extern "C" int tgs_gather_rows(const float *in, float *out, const int64_t *keep,
   if (n_keep == 0) return TGS_OK;
   const unsigned grid = (unsigned)tmin<int64_t>(ceil_div<int64_t>(n_keep * row_floats, 256), 148 * 16);
   k_gather_rows<<<grid, 256, 0, as_stream(stream)>>>(in, out, keep, n_keep, row_floats);
+  return launch_status();
+}
+
+extern "C" int tgs_select_rows_workspace(int64_t n, size_t *bytes) {
+  if (n < 0 || !bytes) return TGS_ERR_INVALID;
+  *bytes = align_up(((size_t)ceil_div<int64_t>(n, kSelTile) + 1) * sizeof(uint32_t));
+  return TGS_OK;
+}
+
+extern "C" int tgs_select_rows(const uint8_t *flags, const float *x, float threshold, int64_t n, int64_t *indices,
+                               int64_t *count, void *workspace, size_t workspace_bytes, tgs_stream_t stream) {
+  if (n < 0 || !count || (n > 0 && (!indices || (!flags && !x) || !workspace))) return TGS_ERR_INVALID;
+  if (n >= (int64_t)1 << 30) return TGS_ERR_UNSUPPORTED;  // 30-bit look-back payloads
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) return cuda_status(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+  size_t need = 0;
+  tgs_select_rows_workspace(n, &need);
+  if (workspace_bytes < need) return TGS_ERR_INVALID;
+  const int64_t tiles = ceil_div<int64_t>(n, kSelTile);
+  uint32_t *status = static_cast<uint32_t *>(workspace), *ticket = status + tiles;
+  const int rc = cuda_status(cudaMemsetAsync(workspace, 0, (size_t)(tiles + 1) * sizeof(uint32_t), st));
+  if (rc != TGS_OK) return rc;
+  k_select_rows<<<(unsigned)tiles, kSelThreads, 0, st>>>(flags, x, threshold, n, indices, count, status, ticket);
   return launch_status();
 }

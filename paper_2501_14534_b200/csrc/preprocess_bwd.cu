@@ -32,6 +32,7 @@ struct ViewBatch {
   float *grad_accum;    // densification statistics (may be NULL)
   int32_t *grad_count;
   int nviews;
+  int clear;            // zero every view's partials after reading them (ready for the next step)
 };
 
 template <int DEG, bool kAcc>
@@ -384,6 +385,23 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     const int total = count * 45;
     for (int j = threadIdx.x; j < total; j += blockDim.x) put<kAcc>(dst + j, drest_s[j]);
   }
+  // ---- the consumer clears: every view's partial rows of this CTA back to zero, so the
+  // next step's blend backward can accumulate into them without a separate fill launch
+  // (coalesced float4 stores over the CTA's contiguous 36 B rows)
+  if (vb.clear) {
+    __syncthreads();  // every thread has read its rows of every view
+    const int total = count * 9;
+    for (int v = 0; v < vb.nviews; ++v) {
+      float *dst = const_cast<float *>(vb.dsplats[v]) + base * 9;  // base * 36 B: 16 B aligned
+      for (int j = 4 * (int)threadIdx.x; j < total; j += 4 * kPreBlock) {
+        if (j + 4 <= total) {
+          *reinterpret_cast<float4 *>(dst + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          for (int k = j; k < total; ++k) dst[k] = 0.0f;
+        }
+      }
+    }
+  }
 }
 
 }  // namespace tgs
@@ -398,11 +416,12 @@ static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const t
   switch (s->active_sh_degree * 2 + (accumulate ? 1 : 0)) {
 #define TGS_BWD(D, A)                                                                                          \
   case D * 2 + A: {                                                                                            \
-    static bool attr = false; /* idempotent function attribute, set once per instance */                       \
-    if (!attr) {                                                                                               \
-      cudaFuncSetAttribute(k_preprocess_bwd_views<D, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPbSmem); \
-      attr = true;                                                                                             \
-    }                                                                                                          \
+    static std::atomic<uint64_t> attr{0}; /* per device: function attributes are per device */               \
+    const int arc = attr_once_per_device(attr, [] {                                                            \
+      return cudaFuncSetAttribute(k_preprocess_bwd_views<D, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                  kPbSmem);                                                                    \
+    });                                                                                                        \
+    if (arc != TGS_OK) return arc;                                                                             \
     k_preprocess_bwd_views<D, A><<<grid, kPreBlock, kPbSmem, st>>>(*cloud, vb, *s, *grads);                    \
   } break;
     TGS_BWD(0, 0) TGS_BWD(0, 1) TGS_BWD(1, 0) TGS_BWD(1, 1) TGS_BWD(2, 0) TGS_BWD(2, 1) TGS_BWD(3, 0) TGS_BWD(3, 1)
@@ -414,14 +433,18 @@ static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const t
 extern "C" int tgs_preprocess_backward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                                        const uint8_t *visible, const float *dsplats, tgs_grads *grads,
                                        int32_t accumulate, tgs_stream_t stream) {
-  return tgs_preprocess_backward_views(cloud, cam, s, &visible, &dsplats, 1, grads, accumulate, nullptr, stream);
+  return tgs_preprocess_backward_views(cloud, cam, s, &visible, &dsplats, 1, grads, accumulate, nullptr, 0, stream);
 }
 
 extern "C" int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                              const uint8_t *const *visible, const float *const *dsplats,
                                              int32_t nviews, tgs_grads *grads, int32_t accumulate,
-                                             const tgs_densify_stats *stats, tgs_stream_t stream) {
+                                             const tgs_densify_stats *stats, int32_t clear_partials,
+                                             tgs_stream_t stream) {
   if (!cloud || !cams || !s || !grads || !visible || !dsplats || cloud->n < 0 || nviews < 1) return TGS_ERR_INVALID;
+  if (clear_partials)
+    for (int v = 0; v < nviews; ++v)
+      if (reinterpret_cast<uintptr_t>(dsplats[v]) & 15) return TGS_ERR_INVALID;  // float4 clears
   if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
   if (cloud->n == 0) return TGS_OK;
   cudaStream_t st = as_stream(stream);
@@ -435,6 +458,7 @@ extern "C" int tgs_preprocess_backward_views(const tgs_cloud *cloud, const tgs_c
     }
     vb.grad_accum = stats && stats->grad_count ? stats->grad_accum : nullptr;
     vb.grad_count = vb.grad_accum ? stats->grad_count : nullptr;
+    vb.clear = clear_partials != 0;
     const int rc = launch_bwd_views(cloud, vb, s, grads, accumulate || v0 > 0, st);
     if (rc != TGS_OK) return rc;
   }

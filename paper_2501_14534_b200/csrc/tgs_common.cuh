@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 
@@ -39,6 +40,20 @@ __host__ __device__ inline T tmin(T a, T b) {
 template <typename T>
 __host__ __device__ inline T tmax(T a, T b) {
   return a < b ? b : a;
+}
+
+// Function attributes (dynamic shared memory, carve-out) are per DEVICE: set them once
+// per (kernel, device).  `done` is the kernel's bitmask of devices already configured;
+// two threads racing here both set the (idempotent) attribute, which is harmless.
+template <typename F>
+inline int attr_once_per_device(std::atomic<uint64_t> &done, F &&set) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TGS_ERR_CUDA;
+  const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;  // devices >= 64: set on every call
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return TGS_OK;
+  if (set() != cudaSuccess) return cuda_status(cudaGetLastError());
+  if (bit) done.fetch_or(bit, std::memory_order_release);
+  return TGS_OK;
 }
 
 inline size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }

@@ -40,10 +40,15 @@ class Adam:
                   1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t, _lib.stream_handle(cloud.device))
 
     def step(self, cloud: GaussianCloud, grads, names=PARAM_FIELDS, lambda_m: float = 0.0,
-             lambda_sh: float = 0.0) -> None:
+             lambda_sh: float = 0.0, guard=None) -> None:
         """Update the groups `names` in ONE fused launch (tgs_adam_step_groups).  lambda_m /
         lambda_sh add the mask penalties of total_loss (masking.py:60-67) to the
-        mask-logit gradients first (when those groups are among `names`)."""
+        mask-logit gradients first (when those groups are among `names`).
+
+        guard: optional (terms, flag) device tensors — float64 loss terms and an int32
+        flag: if any term is not finite the launch updates nothing and sets the flag
+        (the reference raises DivergenceError before its update, training.py:298-308).
+        The host-side step counters are still advanced; the caller rolls them back."""
         import ctypes
         from .loss import SH_BAND_WEIGHTS
         names = sorted(set(names), key=lambda f: cloud.field_range(f)[0])  # layout order
@@ -69,7 +74,10 @@ class Adam:
                   _lib.ptr(self.v), k, arr(ctypes.c_int64, offs), arr(ctypes.c_int64, sizes),
                   arr(ctypes.c_float, lrs), arr(ctypes.c_float, b1s), arr(ctypes.c_float, b2s),
                   arr(ctypes.c_int32, kinds), self.beta1, self.beta2, self.eps, float(lambda_m), float(lambda_sh),
-                  (ctypes.c_float * 3)(*SH_BAND_WEIGHTS), len(cloud), _lib.stream_handle(cloud.device))
+                  (ctypes.c_float * 3)(*SH_BAND_WEIGHTS), len(cloud),
+                  _lib.ptr(guard[0]) if guard is not None else None,
+                  int(guard[0].numel()) if guard is not None else 0,
+                  _lib.ptr(guard[1]) if guard is not None else None, _lib.stream_handle(cloud.device))
 
 
 def exponential_lr(step: int, lr_init: float, lr_final: float, max_steps: int) -> float:

@@ -16,11 +16,29 @@ from .cloud import PARAM_FIELDS, GaussianCloud, _ROW
 from .errors import ContractViolationError, EmptySceneError
 
 
+def select_rows(n: int, device, flags: torch.Tensor | None = None, x: torch.Tensor | None = None,
+                threshold: float = 0.0) -> torch.Tensor:
+    """Ascending int64 row numbers with flags != 0 (or x > threshold): the np.nonzero of
+    the prunings, by the tgs_select_rows compaction kernel.  One host read of the count
+    (the returned tensor's length)."""
+    import ctypes
+    nb = ctypes.c_size_t(0)
+    _lib.call("tgs_select_rows_workspace", int(n), ctypes.byref(nb))
+    ws = torch.empty(max(int(nb.value), 16), dtype=torch.uint8, device=device)
+    idx = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=device)
+    _lib.call("tgs_select_rows", _lib.ptr(flags), _lib.ptr(x), float(threshold), int(n), _lib.ptr(idx), _lib.ptr(cnt),
+              _lib.ptr(ws), ws.numel(), _lib.stream_handle(device))
+    return idx[: int(cnt.item())]
+
+
 def keep_indices(cloud: GaussianCloud, eps: float) -> torch.Tensor:
+    """Rows whose hard mask survives: sigmoid(m) > eps <=> m > logit_floor(eps) (masking.py:21-25,
+    evaluated in logit space like the kernels)."""
     if not 0.0 < eps < 1.0:
         raise ContractViolationError("mask threshold must lie in (0, 1)")
     thr = _lib.logit_floor_f32(eps)
-    return torch.nonzero(cloud.mask_logits > thr, as_tuple=False).flatten()
+    return select_rows(len(cloud), cloud.device, x=cloud.mask_logits, threshold=thr)
 
 
 def prune_by_mask(cloud: GaussianCloud, eps: float):

@@ -674,11 +674,13 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
 
 
 def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, visibles: list,
-                              dsplats: list, grads: CloudGrads, accumulate: bool = False, stats=None) -> CloudGrads:
+                              dsplats: list, grads: CloudGrads, accumulate: bool = False, stats=None,
+                              clear: bool = False) -> CloudGrads:
     """Second half of render_backward for a batch of views in ONE pass over the
     parameters (tgs_preprocess_backward_views): grads (+)= sum over views.  stats:
     optional train.DensifyStats, accumulating each view's screen-space gradient norm
-    (training.py:333-337)."""
+    (training.py:333-337).  clear=True zeroes every dsplats[v] after reading it (the
+    training loop's buffers are then ready for the next step's blend backward)."""
     import ctypes
     n = len(cloud)
     if n == 0 or not cams:
@@ -693,7 +695,7 @@ def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: Render
     with stage("preprocess_bwd"):
         _lib.call("tgs_preprocess_backward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), vis_ptrs,
                   ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)),
-                  ctypes.byref(c_stats) if c_stats else None, _lib.stream_handle(cloud.device))
+                  ctypes.byref(c_stats) if c_stats else None, int(bool(clear)), _lib.stream_handle(cloud.device))
     return grads
 
 

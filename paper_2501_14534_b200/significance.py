@@ -100,7 +100,8 @@ def prune_keep_indices(scores: torch.Tensor, rate: float) -> torch.Tensor:
     ws = _workspace(n, scores.device)
     _lib.call("tgs_significance_keep", _lib.ptr(scores), n, k, _lib.ptr(keep), _lib.ptr(ws), ws.numel(),
               _lib.stream_handle(scores.device))
-    return torch.nonzero(keep, as_tuple=False).flatten()
+    from .pruning import select_rows
+    return select_rows(n, scores.device, flags=keep)
 
 
 def prune_by_significance(cloud: GaussianCloud, scores: torch.Tensor, rate: float):

@@ -20,10 +20,12 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 from . import loss as loss_mod
 from .cloud import PARAM_FIELDS, CloudGrads, GaussianCloud
+from .errors import DivergenceError
 from .optim import Adam
 from .profiler import stage
 from .rasterizer import (RenderSettings, _bin_begin, _bin_end, _tiles_y, blend_backward, preprocess_backward_views,
@@ -104,6 +106,15 @@ class Trainer:
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
         # per-view densification statistics, accumulated inside the preprocess kernels
         self.stats = DensifyStats(len(cloud), dev) if densify_stats else None
+        self.iteration = 0
+        self.instances = []  # tile-list instances per view of the last step (host-known counts)
+        # divergence guard (training.py:298-308): the fused Adam skips the whole update when a
+        # loss term is not finite and raises this flag; the host learns it from a pinned copy
+        # made at the end of the step, without a synchronisation of its own
+        self._nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._nf_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._terms_host = torch.zeros((len(cameras), 2), dtype=torch.float64, pin_memory=True)
+        self._pending = None  # (iteration, event, Adam step counters before it, n, resolution)
 
     def prune(self, eps: float) -> int:
         """Mask-based pruning between steps (masking.py:70-81, training.py:340-346): keep
@@ -139,12 +150,47 @@ class Trainer:
         if self.stats is not None:
             self.stats.compact(keep)
 
+    def check_divergence(self, block: bool = True) -> None:
+        """Raise DivergenceError (with the reference's snapshot keys, training.py:298-308)
+        if a finished step saw a non-finite loss term.  That step updated nothing on the
+        device (the guarded Adam launch) and its optimizer step counters are rolled back.
+        block=False only looks at a step whose flag has already reached the host."""
+        p = self._pending
+        if p is None or (not block and not p[1].query()):
+            return
+        self._pending = None
+        p[1].synchronize()
+        if not int(self._nf_host[0]):
+            return
+        it, _, steps_before, n, res = p
+        self.opt.steps = dict(steps_before)
+        self.iteration = it
+        terms = self._terms_host.numpy()
+        bad = [v for v in self.views if not np.isfinite(terms[v]).all()] or list(self.views)
+        v = bad[0]
+        l1, ssim = float(terms[v, 0]), float(terms[v, 1])
+        raise DivergenceError(f"non-finite loss at iteration {it}",
+                              snapshot={"iteration": it, "n_gaussians": n, "l1": l1, "d_ssim": (1.0 - ssim) / 2.0,
+                                        "resolution": res, "view": v})
+
     def step(self, host_targets=None) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the device loss terms.
 
         host_targets: optional {view: pinned (H, W, 3) float32 CPU tensor}.  Each view's
         target is copied on a dedicated copy stream and its loss waits only for that
-        copy, so the transfers of later views overlap the compute of earlier ones."""
+        copy, so the transfers of later views overlap the compute of earlier ones.
+
+        A non-finite loss (training.py:298-308) leaves the parameters and Adam state
+        untouched; DivergenceError is raised by the next step() (as soon as that step's
+        first host read shows the flag) or by check_divergence()."""
+        self.check_divergence(block=False)
+        try:
+            return self._step(host_targets)
+        except BaseException:
+            self.dsplats = {}  # partial buffers may be left non-zero: start the next step afresh
+            raise
+
+    def _step(self, host_targets):
         g = self.grads
         vis, parts = [], []
         main = torch.cuda.current_stream(self.cloud.device)
@@ -158,6 +204,8 @@ class Trainer:
                     ev = torch.cuda.Event()
                     ev.record(self.copy_stream)
                     copied[v] = ev
+        if self.pg is not None:
+            self.terms.zero_()  # other ranks' rows are summed in by the step's terms all-reduce
         # every view's preprocess in one pass over the parameters (main stream)
         pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, stats=self.stats)
         for s_ in self.streams:
@@ -186,6 +234,11 @@ class Trainer:
             with torch.cuda.stream(st):
                 cam, target = self.cameras[v], self.targets[v]
                 bins = _bin_end(p_i) if p_i is not None else None
+                if i == 0:  # the previous step's flag is on the host once this view's count is
+                    self.check_divergence(block=False)
+                    self.instances = []
+                if bins is not None:
+                    self.instances.append(int(bins.indices.numel()))
                 out = render_forward(self.cloud, cam, self.settings, pre=pres[i], bins=bins)
             with torch.cuda.stream(st):
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
@@ -197,8 +250,9 @@ class Trainer:
                     loss_mod.l1_ssim_async(out.image, target, self.lambda_ssim, d, self.terms[v])
                 ds = self.dsplats.get(v)
                 if ds is None or ds.shape[0] != len(self.cloud):
-                    ds = self.dsplats[v] = torch.empty((len(self.cloud), 9), dtype=torch.float32, device=d.device)
-                ds.zero_()
+                    # zeroed once; afterwards the multi-view preprocess backward clears each
+                    # buffer after reading it (no fill launch per view)
+                    ds = self.dsplats[v] = torch.zeros((len(self.cloud), 9), dtype=torch.float32, device=d.device)
                 _, st_state = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds,
                                              deterministic=self.deterministic)
                 vis.append(st_state.visible_u8)
@@ -209,7 +263,11 @@ class Trainer:
             main.wait_stream(self.copy_stream)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
-                                  accumulate=False, stats=self.stats)
+                                  accumulate=False, stats=self.stats, clear=True)
+        steps_before = dict(self.opt.steps)
+        cam0 = self.cameras[self.views[0]] if self.views else None
+        res = (int(cam0.height), int(cam0.width)) if cam0 is not None else (0, 0)
+        guard = (self.terms, self._nonfinite)
         # training.py:321-329: sh_rest is optimised only on steps with higher-band gradients
         # and a non-zero active degree; every other group every step
         upd = set(PARAM_FIELDS)
@@ -219,8 +277,9 @@ class Trainer:
             with stage("adam"):
                 # the mask penalties of total_loss (masking.py:60-67) enter the gradient inside
                 # the fused Adam launch
-                self.opt.step(self.cloud, g, names=tuple(upd), lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
-            return self.terms
+                self.opt.step(self.cloud, g, names=tuple(upd), lambda_m=self.lambda_m, lambda_sh=self.lambda_sh,
+                              guard=guard)
+            return self._finish(main, steps_before, n, res)
         # data parallel: the gradient buckets are all-reduced on a communication stream in
         # order, and each bucket's Adam update (identical on every rank, mask penalties
         # included) starts as soon as its reduction is done, overlapping the next ones
@@ -232,6 +291,9 @@ class Trainer:
         self.comm_stream.wait_stream(main)
         done = []
         with stage("allreduce"), torch.cuda.stream(self.comm_stream):
+            # every view's loss terms on every rank (each rank wrote only its own rows, the
+            # others are zero): the divergence guard then decides identically everywhere
+            dist.all_reduce(self.terms, group=self.pg)
             for _, a0, a1 in buckets:
                 dist.all_reduce(g.flat[a0:a1], group=self.pg)
                 ev = torch.cuda.Event()
@@ -242,5 +304,17 @@ class Trainer:
                 main.wait_event(ev)
                 names = tuple(f for f in fields if f in upd)
                 if names:
-                    self.opt.step(self.cloud, g, names=names, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh)
+                    self.opt.step(self.cloud, g, names=names, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh,
+                                  guard=guard)
+        return self._finish(main, steps_before, n, res)
+
+    def _finish(self, main, steps_before, n, res) -> torch.Tensor:
+        """Queue the pinned copy of the divergence flag and the loss terms; the next step
+        (or check_divergence) reads it."""
+        self._nf_host.copy_(self._nonfinite, non_blocking=True)
+        self._terms_host.copy_(self.terms, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self._pending = (self.iteration, ev, steps_before, n, res)
+        self.iteration += 1
         return self.terms

@@ -1,4 +1,4 @@
-"""Summarise ncu --set full reports into profiles/r01_ncu_summary.txt and the per-stage
+"""Summarise ncu --set full reports into profiles/<prefix>_ncu_summary.txt and the per-stage
 DRAM traffic JSON that bench.py reports as roofline.traffic.
 
     python profiles/ncu_summary.py <view.ncu-rep> <step.ncu-rep>
@@ -73,7 +73,8 @@ def main(reps):
     lines = ["ncu --set full --clock-control none (one c3 view via profile_step.py; the per-step kernels via",
              "profile_train.py, 8 views).  Cold-cache, serialised replays: compare shares, not absolute times.", "",
              f"{'kernel':34s} {'us':>8s} {'DRAM MB':>9s} {'TB/s':>6s} {'issue%':>7s} {'occ%':>6s} {'fma%':>6s} {'regs':>5s}"]
-    per_stage = defaultdict(lambda: {"dram_bytes_per_launch": 0.0, "time_us": 0.0, "kernels": [], "issue_w": 0.0})
+    per_stage = defaultdict(lambda: {"dram_bytes_per_launch": 0.0, "time_us": 0.0, "kernels": [], "issue_w": 0.0,
+                                     "fma_w": 0.0, "insts": 0.0})
     for r in recs:
         mb = ((r["dram_read"] or 0) + (r["dram_write"] or 0)) / 1e6
         tbs = mb / 1e6 / (r["time_us"] * 1e-6) if r["time_us"] else 0
@@ -86,13 +87,21 @@ def main(reps):
         per_stage[st]["time_us"] += r["time_us"]
         per_stage[st]["kernels"].append(r["kernel"])
         per_stage[st]["issue_w"] += (r["issue_busy_pct"] or 0.0) * r["time_us"]
+        per_stage[st]["fma_w"] += (r["fma_pipe_pct"] or 0.0) * r["time_us"]
+        per_stage[st]["insts"] += r["warp_insts"] or 0.0
     json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"]), "time_us": round(v["time_us"], 1),
                    "issue_busy_pct": round(v["issue_w"] / max(v["time_us"], 1e-9), 1),
-                   "kernels": v["kernels"]} for k, v in per_stage.items()},
-              open("profiles/r01_ncu_traffic.json", "w"), indent=1)
-    open("profiles/r01_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
+                   "fma_pipe_pct": round(v["fma_w"] / max(v["time_us"], 1e-9), 1),
+                   "warp_insts": int(v["insts"]), "kernels": v["kernels"]} for k, v in per_stage.items()},
+              open(f"profiles/{PREFIX}_ncu_traffic.json", "w"), indent=1)
+    open(f"profiles/{PREFIX}_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:])
+    # python profiles/ncu_summary.py [--prefix r02] <view.ncu-rep> <step.ncu-rep>
+    args = sys.argv[1:]
+    PREFIX = "r01"
+    if args[:1] == ["--prefix"]:
+        PREFIX, args = args[1], args[2:]
+    main(args)

@@ -1,5 +1,11 @@
 """A few c4 frames (3M Gaussians, 4K) through render_forward — the command profiled by
 `ncu -k regex:k_blend_fwd16w` for the 4K forward blend."""
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
 import torch
 
 from paper_2501_14534_b200 import GaussianCloud, RenderSettings, render_forward, scenes

@@ -1,7 +1,10 @@
 """One c3 view forward + loss + backward after warm-up — the command profiled by
 `ncu --set full -k regex:<kernel>` (profiles/README.md)."""
 
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 

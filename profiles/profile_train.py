@@ -1,7 +1,10 @@
 """Two c3 training steps (8 views) through train.Trainer — the command profiled by
 `ncu -k regex:<kernel>` for the per-step kernels (preprocess backward, Adam)."""
 
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 
