@@ -202,14 +202,20 @@ def blend_forward(splats, offsets, ids, width, height, tile_size, background, re
 def blend_backward(splats, offsets, ids, width, height, tile_size, background, transmit, last_pos, dimage,
                    dtype="f64"):
     npt, sfx = _rt(dtype)
+    # every buffer handed to C is bound to a local first: a temporary passed straight into
+    # _ptr() would be freed before the call (only its address survives), and under
+    # concurrent callers its memory is reused at once
     splats = np.ascontiguousarray(splats, dtype=npt)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    bg = np.asarray(background, dtype=np.float64)
+    transmit = np.ascontiguousarray(transmit, dtype=npt)
+    last_pos = np.ascontiguousarray(last_pos, dtype=np.int32)
+    dimage = np.ascontiguousarray(dimage, dtype=npt)
     dsp = np.zeros((splats.shape[0], 9), dtype=npt)
     getattr(lib(), f"oracle_blend_bwd_{sfx}")(
-        _ptr(splats), _ptr(np.ascontiguousarray(offsets, dtype=np.int64)),
-        _ptr(np.ascontiguousarray(ids, dtype=np.int64)), int(width), int(height), int(tile_size),
-        _ptr(np.asarray(background, dtype=np.float64)), _ptr(np.ascontiguousarray(transmit, dtype=npt)),
-        _ptr(np.ascontiguousarray(last_pos, dtype=np.int32)), _ptr(np.ascontiguousarray(dimage, dtype=npt)),
-        _ptr(dsp))
+        _ptr(splats), _ptr(offsets), _ptr(ids), int(width), int(height), int(tile_size), _ptr(bg), _ptr(transmit),
+        _ptr(last_pos), _ptr(dimage), _ptr(dsp))
     return dsp
 
 
@@ -221,8 +227,9 @@ def preprocess_backward(cloud, cam, settings, dsplats, dtype="f64"):
                   sh_rest=(n, 15, 3), mask_logits=(n,), sh_mask_logits=(n, 3), mean2d_screen=(n, 2))
     g = {k: np.zeros(v, dtype=npt) for k, v in shapes.items()}
     cc, ss = _camera(cam), _settings(settings)
+    dsp = np.ascontiguousarray(dsplats, dtype=npt)  # bound to a local: see blend_backward
     getattr(lib(), f"oracle_preprocess_bwd_{sfx}")(
-        ctypes.byref(hold.c), ctypes.byref(cc), ctypes.byref(ss), _ptr(np.ascontiguousarray(dsplats, dtype=npt)),
+        ctypes.byref(hold.c), ctypes.byref(cc), ctypes.byref(ss), _ptr(dsp),
         _ptr(g["positions"]), _ptr(g["log_scales"]), _ptr(g["rotations"]), _ptr(g["opacity_logits"]),
         _ptr(g["sh_dc"]), _ptr(g["sh_rest"]), _ptr(g["mask_logits"]), _ptr(g["sh_mask_logits"]),
         _ptr(g["mean2d_screen"]))

@@ -108,6 +108,9 @@ class Trainer:
         self.stats = DensifyStats(len(cloud), dev) if densify_stats else None
         self.iteration = 0
         self.instances = []  # tile-list instances per view of the last step (host-known counts)
+        # the multi-view preprocess backward zeroes each view's partial buffer after reading it
+        # (False keeps the last step's partials readable, e.g. for inspection in tests)
+        self.clear_partials = True
         # divergence guard (training.py:298-308): the fused Adam skips the whole update when a
         # loss term is not finite and raises this flag; the host learns it from a pinned copy
         # made at the end of the step, without a synchronisation of its own
@@ -253,6 +256,8 @@ class Trainer:
                     # zeroed once; afterwards the multi-view preprocess backward clears each
                     # buffer after reading it (no fill launch per view)
                     ds = self.dsplats[v] = torch.zeros((len(self.cloud), 9), dtype=torch.float32, device=d.device)
+                elif not self.clear_partials:
+                    ds.zero_()
                 _, st_state = blend_backward(self.cloud, cam, self.settings, d, out, dsplats=ds,
                                              deterministic=self.deterministic)
                 vis.append(st_state.visible_u8)
@@ -263,7 +268,7 @@ class Trainer:
             main.wait_stream(self.copy_stream)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
-                                  accumulate=False, stats=self.stats, clear=True)
+                                  accumulate=False, stats=self.stats, clear=self.clear_partials)
         steps_before = dict(self.opt.steps)
         cam0 = self.cameras[self.views[0]] if self.views else None
         res = (int(cam0.height), int(cam0.width)) if cam0 is not None else (0, 0)

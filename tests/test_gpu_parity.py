@@ -676,6 +676,7 @@ def test_trainer_densify_stats_and_significance_event(tgs):
     cloud = tgs.GaussianCloud.from_fields(sc.fields)
     targets = [torch.rand((c.height, c.width, 3), device="cuda") for c in cams]
     tr = Trainer(cloud, cams, targets, st, densify_stats=True)
+    tr.clear_partials = False  # keep the step's partials readable below
     before = tgs.GaussianCloud.from_fields(sc.fields)
     pres = preprocess_views(before, cams, st)
     tr.step()
