@@ -79,6 +79,22 @@ enum {
  *   [0..1] dL/dmeans2d  [2..4] dL/dcov2d packed (g00, g01 both slots, g11)
  *   [5] dL/dalpha       [6..8] dL/drgb          (_kernels.py:111-115) */
 #define TGS_DSPLAT_FLOATS 9
+/* Per-Gaussian EXACT BLEND-DECISION record (optional output of the preprocess,
+ * optional input of every blend entry point), 8 floats, 32 B aligned:
+ *   [0] cut_lo, [1] cut_hi  float32 bracket, in log2 units, of the reference's
+ *        float64 blend cut max(-4.5, ln(1/(255 alpha))) widened by a bound on the
+ *        float32 exponent's error over the Gaussian's footprint: a pixel whose
+ *        float32 exponent e2 is >= cut_hi (and <= 0) blends in float64 too, one
+ *        below cut_lo does not; in between (or e2 > 0) the blend kernels decide in
+ *        float64 (_kernels.py:62-72).  cut_hi = +inf when alpha can reach the 0.99
+ *        clamp (every pair then decided in float64, incl. the backward's a <= 0.99);
+ *   [2..3] means2d, [4..6] conic: float64 value minus the float32 record value, so
+ *        record + residual reconstructs the float64 projection (~1e-13);
+ *   [7]  the float64 cut minus cut_lo (log2 units), or, when cut_hi = +inf (the
+ *        cut is then -4.5), the clamp exponent ln(0.99 / alpha).
+ * Rows of non-visible Gaussians are zero.  A blend call without records
+ * (exact == NULL) decides every pair in float32. */
+#define TGS_EXACT_FLOATS 8
 
 typedef struct {
   float fx, fy, cx, cy;
@@ -90,6 +106,11 @@ typedef struct {
    * tile lists order exactly like the reference's float64 np.lexsort (float32
    * depths collide ~2k times at 200k Gaussians and would reorder blends). */
   double depth_row[4];
+  /* The camera in float64 (the reference's own values): the float64 projection of
+   * the exact blend-decision records (TGS_EXACT_FLOATS below). */
+  double fx64, fy64, cx64, cy64;
+  double R64[9];
+  double t64[3];
 } tgs_camera;
 
 typedef struct {
@@ -108,6 +129,7 @@ typedef struct {
   int32_t tile_size;        /* 1..32 */
   int32_t compute_sh_rest_grads;
   int32_t reserved;
+  double lowpass_s64;       /* lowpass_s in float64 (the exact blend-decision records) */
 } tgs_settings;
 
 typedef struct {
@@ -136,6 +158,9 @@ typedef struct { /* CloudGrads (cloud.py:110-126) */
 } tgs_grads;
 
 TGS_API int tgs_version(void);
+/* Profiling builds only (-DTGS_COUNT_EXACT): pairs decided in float64 by the blend
+ * kernels since the last reset (TGS_ERR_UNSUPPORTED otherwise; profiles/exact_pairs.py). */
+TGS_API int tgs_debug_exact_pairs(unsigned long long *count, int32_t reset);
 TGS_API const char *tgs_last_error_string(int status);
 
 /* ---- (1) preprocess -----------------------------------------------------
@@ -144,19 +169,30 @@ TGS_API const char *tgs_last_error_string(int status);
  * depth_keys (n,) uint64 or NULL: order-preserving bits of the float64 depth
  * (cam->depth_row . [x, 1]), the sort key consumed by tgs_bin_gaussians.
  * error_flag: device int32, OR-ed with 1 when a quaternion has norm < 1e-12;
- * the caller reads it back and raises DegenerateRotationError. */
+ * the caller reads it back and raises DegenerateRotationError.
+ * exact (n, 8) or NULL: the exact blend-decision records (TGS_EXACT_FLOATS). */
 TGS_API int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                            float *splats, uint8_t *visible, int32_t *tiles_touched, uint64_t *depth_keys,
-                           int32_t *error_flag, tgs_stream_t stream);
+                           int32_t *error_flag, float *exact, tgs_stream_t stream);
 /* A batch of views in ONE pass over the parameters (the sh_rest block staged
  * once): per view v the same outputs as tgs_preprocess_forward into splats[v],
  * visible[v], tiles_touched[v], depth_keys[v] (may be NULL), bit-identical to a
  * single-view call with cams[v].  stats (may be NULL): area_max is updated with
- * the views' screen areas (the other two fields are the backward's). */
+ * the views' screen areas (the other two fields are the backward's).
+ * exact (may be NULL; else exact[v] (n, 8), 16 B aligned): the exact
+ * blend-decision records (TGS_EXACT_FLOATS) of every view. */
+/* The exact blend-decision records (TGS_EXACT_FLOATS) of a batch of views from
+ * their float32 records splats[v] (as written by the preprocess): the float64
+ * projection of every visible row.  The preprocess entry points call it when
+ * given `exact`; a pipelined caller can instead run it on another stream, since
+ * only the blend kernels read the records (not the binning). */
+TGS_API int tgs_exact_records_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                    int32_t nviews, const float *const *splats, float *const *exact,
+                                    tgs_stream_t stream);
 TGS_API int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                          int32_t nviews, float *const *splats, uint8_t *const *visible,
                                          int32_t *const *tiles_touched, uint64_t *const *depth_keys,
-                                         int32_t *error_flag, const tgs_densify_stats *stats,
+                                         int32_t *error_flag, const tgs_densify_stats *stats, float *const *exact,
                                          tgs_stream_t stream);
 
 /* tiles_touched for arbitrary projected records (the bin_tiles(...) entry,
@@ -206,8 +242,11 @@ TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int
 /* ---- (3) forward blend ------------------------------------------------------
  * image (H, W, 3), transmit / weight_sum (H, W) float32, n_contrib / last_pos
  * (H, W) int32 (_kernels.py:83-89); hits (n,) int32 or NULL (record_hits).
- * Only pixels of tile rows [row_begin, row_end) are written. */
-TGS_API int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+ * Only pixels of tile rows [row_begin, row_end) are written.  exact (n, 8) or
+ * NULL: the preprocess's exact blend-decision records (TGS_EXACT_FLOATS); every
+ * blend entry point takes the same records and decides identically. */
+TGS_API int tgs_blend_forward(const float *splats, const float *exact, const int32_t *tile_offsets,
+                      const int32_t *sorted_ids,
                       const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                       float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
                       int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream);
@@ -216,13 +255,15 @@ TGS_API int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, 
  * records_kernel (_kernels.py:184-241), a test/debug payload.  pixel_offsets
  * (H*W,) int64 is the exclusive cumsum of n_contrib; rec_gauss (int32) and
  * rec_weight (float32) have sum(n_contrib) entries.  Full image only. */
-TGS_API int tgs_blend_records(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+TGS_API int tgs_blend_records(const float *splats, const float *exact, const int32_t *tile_offsets,
+                      const int32_t *sorted_ids,
                       const tgs_camera *cam, const tgs_settings *s, const int64_t *pixel_offsets,
                       int32_t *rec_gauss, float *rec_weight, tgs_stream_t stream);
 
 /* ---- (4) backward blend -----------------------------------------------------
  * dsplats (n, 9) is ACCUMULATED into (caller zeroes it). dimage (H, W, 3). */
-TGS_API int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+TGS_API int tgs_blend_backward(const float *splats, const float *exact, const int32_t *tile_offsets,
+                      const int32_t *sorted_ids,
                        const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                        const float *transmit, const int32_t *last_pos, const float *dimage,
                        float *dsplats, const int32_t *tile_order, tgs_stream_t stream);
@@ -242,7 +283,8 @@ TGS_API int tgs_tile_order(const int32_t *tile_offsets, int32_t ntiles, int32_t 
  * forward's tiles_touched (n), the instance count and a workspace of
  * tgs_blend_backward_deterministic_workspace() bytes (≈ 40 B per instance). */
 TGS_API int tgs_blend_backward_deterministic_workspace(int64_t n, int64_t num_instances, size_t *bytes);
-TGS_API int tgs_blend_backward_deterministic(const float *splats, const int32_t *tiles_touched, int64_t n,
+TGS_API int tgs_blend_backward_deterministic(const float *splats, const float *exact,
+                                             const int32_t *tiles_touched, int64_t n,
                                              const int32_t *tile_offsets, const int32_t *sorted_ids,
                                              int64_t num_instances, const tgs_camera *cam, const tgs_settings *s,
                                              int32_t row_begin, int32_t row_end, const float *transmit,
@@ -369,7 +411,8 @@ TGS_API int tgs_render_views_workspace(int64_t n, int64_t max_instances, int32_t
                                        int32_t tile_size, size_t *bytes);
 TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s, int32_t nviews,
                              float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
-                             uint64_t *const *depth_keys, int32_t *error_flag, tgs_view_target *targets,
+                             uint64_t *const *depth_keys, float *const *exact, int32_t *error_flag,
+                             tgs_view_target *targets,
                              void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
                              const tgs_stream_t *streams, const tgs_stream_t *blend_streams, int32_t nstreams);
 

@@ -28,13 +28,14 @@ _D = ctypes.c_double
 
 class TgsCamera(ctypes.Structure):
     _fields_ = [("fx", _F), ("fy", _F), ("cx", _F), ("cy", _F), ("R", _F * 9), ("t", _F * 3), ("center", _F * 3),
-                ("width", _I32), ("height", _I32), ("depth_row", _D * 4)]
+                ("width", _I32), ("height", _I32), ("depth_row", _D * 4), ("fx64", _D), ("fy64", _D), ("cx64", _D),
+                ("cy64", _D), ("R64", _D * 9), ("t64", _D * 3)]
 
 
 class TgsSettings(ctypes.Structure):
     _fields_ = [("lowpass_s", _F), ("near_plane", _F), ("mask_logit_min", _F), ("sh_mask_logit_min", _F),
                 ("opacity_logit_min", _F), ("background", _F * 3), ("active_sh_degree", _I32),
-                ("tile_size", _I32), ("compute_sh_rest_grads", _I32), ("reserved", _I32)]
+                ("tile_size", _I32), ("compute_sh_rest_grads", _I32), ("reserved", _I32), ("lowpass_s64", _D)]
 
 
 CLOUD_FIELDS = ("positions", "log_scales", "rotations", "opacity_logits", "sh_dc", "sh_rest", "mask_logits",
@@ -62,24 +63,26 @@ class TgsGrads(ctypes.Structure):
 
 _SIGS = {
     "tgs_version": ([], _I32),
-    "tgs_preprocess_forward": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
-    "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_preprocess_forward": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_preprocess_forward_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_exact_records_views": ([_P, _P, _P, _I32, _P, _P, _P], _I32),
     "tgs_count_tiles": ([_P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_gaussians_workspace": ([_I64, _P], _I32),
     "tgs_bin_gaussians": ([_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P], _I32),
     "tgs_memcpy_d2h_async": ([_P, _P, _SZ, _P], _I32),
     "tgs_render_views_workspace": ([_I64, _I64, _I32, _I32, _I32, _P], _I32),
-    "tgs_render_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32], _I32),
+    "tgs_render_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32], _I32),
     "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),
-    "tgs_blend_forward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_forward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_tile_order": ([_P, _I32, _P, _P], _I32),
-    "tgs_blend_records": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_debug_exact_pairs": ([_P, _I32], _I32),
+    "tgs_blend_records": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_blend_backward_deterministic_workspace": ([_I64, _I64, _P], _I32),
-    "tgs_blend_backward_deterministic": ([_P, _P, _I64, _P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P],
-                                         _I32),
-    "tgs_blend_backward": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_backward_deterministic": ([_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P, _P,
+                                          _P], _I32),
+    "tgs_blend_backward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
     "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P, _I32, _P], _I32),
     "tgs_loss_workspace": ([_I32, _I32, _P], _I32),
@@ -170,8 +173,11 @@ def make_camera(cam) -> TgsCamera:
     c = _CAM_CACHE.get(key)
     if c is None:
         v = cam.native_fields() if hasattr(cam, "native_fields") else _native_fields(cam)
+        R64 = np.asarray(cam.R, dtype=np.float64).reshape(9)
+        t64 = np.asarray(cam.t, dtype=np.float64).reshape(3)
         c = TgsCamera(v["fx"], v["fy"], v["cx"], v["cy"], (_F * 9)(*v["R"]), (_F * 3)(*v["t"]),
-                      (_F * 3)(*v["center"]), v["width"], v["height"], (_D * 4)(*v["depth_row"]))
+                      (_F * 3)(*v["center"]), v["width"], v["height"], (_D * 4)(*v["depth_row"]), float(cam.fx),
+                      float(cam.fy), float(cam.cx), float(cam.cy), (_D * 9)(*R64), (_D * 3)(*t64))
         if len(_CAM_CACHE) > 4096:
             _CAM_CACHE.clear()
         _CAM_CACHE[key] = c
@@ -212,4 +218,5 @@ def _make_settings(s) -> TgsSettings:
     bg = [float(v) for v in s.background]
     return TgsSettings(float(s.lowpass_s), float(s.near), logit_floor_f32(s.mask_threshold),
                        logit_floor_f32(s.sh_mask_threshold), logit_ceil_f32(1.0 / 255.0), (_F * 3)(*bg),
-                       int(s.active_sh_degree), int(s.tile_size), int(bool(s.compute_sh_rest_grads)), 0)
+                       int(s.active_sh_degree), int(s.tile_size), int(bool(s.compute_sh_rest_grads)), 0,
+                       float(s.lowpass_s))

@@ -28,6 +28,18 @@
 #include "tgs_common.cuh"
 #include "tgs_math.cuh"
 
+// Register caps of the exact-decision instantiations (minimum resident CTAs per SM): the
+// float64 resolution is out of line and rare, and without a cap its call would lower the
+// occupancy of the whole kernel (118 / 96 registers; capped: 80 / 64 with the spills on
+// the call path).  Measured at c3 (profiles/scripts/r02_run8.sh): 104.1 -> 106.9 step/s.
+// Overridable with -D for A/B builds (profiles/scripts/build_blend_variants.sh).
+#ifndef TGS_FWD16_MINB
+#define TGS_FWD16_MINB 8
+#endif
+#ifndef TGS_BWD16_MINB
+#define TGS_BWD16_MINB 5
+#endif
+
 namespace tgs {
 
 constexpr int kBatch = 256;
@@ -79,11 +91,90 @@ __device__ __forceinline__ void pixel_of(int t, int ts, int &lx, int &ly) {
 // e2(d) = A dx^2 + B dx dy + C dy^2 >= thr2 = -min(4.5, ln(255 alpha)) log2(e)
 // (e >= -4.5 and alpha exp(e) >= 1/255).  e2 is a concave quadratic, so its maximum
 // over the warp's pixel rectangle is 0 if the mean lies inside, else the best of
-// the four edge maxima (1-D concave quadratics, vertex clamped to the edge).  A
-// 0.02 (log2 units) margin keeps the test conservative under float32 rounding, so
+// the four edge maxima (1-D concave quadratics, vertex clamped to the edge).  The
+// threshold is the lower end of the blend-cut bracket (load_cut below) minus a 0.02
+// (log2 units) margin that keeps the test conservative under float32 rounding, so
 // culling never changes a result.
-__device__ __forceinline__ float splat_thr2(float alpha) {
-  return fmaxf(kE2Min, -__log2f(255.0f * alpha)) - 0.02f;
+
+// ---- blend decisions (include/tgs.h TGS_EXACT_FLOATS) ---------------------------------
+// A (pixel, splat) pair blends iff e >= cut = max(-4.5, ln(1/(255 alpha))) and e <= 0
+// (_kernels.py:59-72); in log2 units e2 = e log2(e).  With exact records the float64 cut
+// is bracketed by [cut.x, cut.y]: e2 >= cut.y blends in float64 as well, e2 < cut.x does
+// not, and the rare pairs in between are decided by exact_pair() in float64.  Without
+// records cut.x == cut.y is the float32 cut.  The reference's e > 0 test cannot fire for
+// a positive-definite conic (e = -v'Kv/2 <= 0; float64 rounding cannot flip its sign
+// below a condition number of ~1e16), so the float32 path does not test e2 > 0 (rounding
+// can make e2 a few ulps positive next to the mean; the reference blends those pixels).
+// Every blend kernel decides through these functions, so the backward re-derives the
+// forward's decisions exactly.
+__device__ __forceinline__ float2 load_cut(const float4 *__restrict__ exact, int g, float alpha) {
+  if (exact) return __ldg(reinterpret_cast<const float2 *>(exact + 2 * (int64_t)g));
+  const float c = fmaxf(kE2Min, -__log2f(255.0f * alpha));
+  return make_float2(c, c);
+}
+
+// The reference's float64 decision for one pair (_kernels.py:59-72): the float64 means and
+// conic rebuilt as float32 record + residual, e = -(a dx^2 + c dy^2)/2 - b dx dy in the
+// reference's operation order (no contraction), compared with the float64 cut (record
+// slot 7 holds cut - cut_lo in log2 units).  A Gaussian whose alpha can reach the 0.99
+// clamp (cut_hi = +inf) has cut = -4.5 exactly (alpha > 0.9899 puts ln(1/(255 alpha))
+// below -4.5) and slot 7 holds ln(0.99 / alpha): alpha exp(e) <= 0.99 <=> e <= slot 7.
+// Bit 0: blends; bit 1: alpha <= 0.99, the backward's partials through alpha apply
+// (_kernels.py:157-168).  The cold path of the blend kernels: ~25 float64 operations.
+#ifdef TGS_COUNT_EXACT
+__device__ unsigned long long g_exact_pairs;  // profiling build only (profiles/exact_pairs.py)
+#endif
+__device__ __forceinline__ int exact_pair(const float4 *__restrict__ splats, const float4 *__restrict__ exact, int g,
+                                          float px, float py) {
+#ifdef TGS_COUNT_EXACT
+  atomicAdd(&g_exact_pairs, 1ull);
+#endif
+  const float4 a = __ldg(splats + 3 * (int64_t)g);
+  const float k2f = __ldg(reinterpret_cast<const float *>(splats + 3 * (int64_t)g + 1));
+  const float4 r0 = __ldg(exact + 2 * (int64_t)g), r1 = __ldg(exact + 2 * (int64_t)g + 1);
+  // (double)px - (double)a.x is exact: both are float32 values
+  const double dx = __dsub_rn(__dsub_rn((double)px, (double)a.x), (double)r0.z);
+  const double dy = __dsub_rn(__dsub_rn((double)py, (double)a.y), (double)r0.w);
+  const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dadd_rn(a.z, r1.x), dx), dx),
+                             __dmul_rn(__dmul_rn(__dadd_rn(k2f, r1.z), dy), dy));
+  const double e = __dsub_rn(__dmul_rn(-0.5, q), __dmul_rn(__dmul_rn(__dadd_rn(a.w, r1.y), dx), dy));
+  if (!isinf(r0.y)) return __dmul_rn(e, 1.4426950408889634) >= __dadd_rn(r0.x, r1.w) ? 3 : 0;
+  if (e < -4.5) return 0;
+  return e <= (double)r1.w ? 3 : 1;
+}
+
+// Both pixels of a lane at once, out of line (the 16x16 kernels call it from a warp-uniform
+// branch taken only when some lane has a pair inside the bracket, so the float64 code stays
+// out of the hot loop).  Returns exact_pair(A) | exact_pair(B) << 2 for the flagged pixels.
+#ifdef TGS_RESOLVE_INLINE  // A/B builds: the float64 resolution inlined into the visit
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+int resolve2(const float4 *__restrict__ splats, const float4 *__restrict__ exact, int g,
+                                     float px, float pyA, float pyB, bool uA, bool uB) {
+  int r = 0;
+  if (uA) r = exact_pair(splats, exact, g, px, pyA);
+  if (uB) r |= exact_pair(splats, exact, g, px, pyB) << 2;
+  return r;
+}
+
+// Whether any lane of the warp has a pixel whose exponent lies inside its splat's cut
+// bracket [cut.x, cut.y) — arithmetic instead of per-pixel predicates (the packed visit
+// code already uses most predicate registers): (e2 - lo)(e2 - hi) <= 0 inside (and on
+// the edges, a superset: the resolving path re-tests exactly).  Warp-uniform result.
+__device__ __forceinline__ bool in_bracket2(float2 e2, float2 cut) {
+  const float2 p = __fmul2_rn(__fadd2_rn(e2, make_float2(-cut.x, -cut.x)), __fadd2_rn(e2, make_float2(-cut.y, -cut.y)));
+  return __any_sync(0xffffffffu, fminf(p.x, p.y) <= 0.0f);
+}
+
+// Scalar decision for the one-pixel-per-thread kernels: 0 skip, else bit 1 = unclamped.
+__device__ __forceinline__ int decide_pair(float e2, float a_raw, float2 cut, const float4 *__restrict__ splats,
+                                           const float4 *__restrict__ exact, int g, float px, float py) {
+  const bool hi = e2 >= cut.y;
+  if (exact && e2 >= cut.x && !hi) return exact_pair(splats, exact, g, px, py);
+  if (!hi) return 0;
+  return a_raw <= kAlphaMax ? 3 : 1;
 }
 
 __device__ __forceinline__ bool quad_misses(float2 m, float4 q, float thr2, float4 wb) {
@@ -117,20 +208,25 @@ struct Stage {
   float2 xy[kBatch];
   float4 q[kBatch];    // prescaled conic + alpha
   float4 col[kBatch];  // r, g, b, cull threshold (log2 units)
+  float2 cut[kBatch];  // blend-cut bracket (load_cut)
   int32_t id[kBatch];
 };
 
-__device__ __forceinline__ void stage_splat(Stage &S, int slot, const float4 *__restrict__ splats, int g) {
+__device__ __forceinline__ void stage_splat(Stage &S, int slot, const float4 *__restrict__ splats,
+                                            const float4 *__restrict__ exact, int g) {
   const float4 a = splats[3 * g], b = splats[3 * g + 1];
   const float c = splats[3 * g + 2].x;
+  const float2 cut = load_cut(exact, g, b.y);
   S.xy[slot] = make_float2(a.x, a.y);
   S.q[slot] = prescaled_conic(a, b);
-  S.col[slot] = make_float4(b.z, b.w, c, splat_thr2(b.y));
+  S.col[slot] = make_float4(b.z, b.w, c, cut.x - 0.02f);  // cull: nothing below cut.x blends
+  S.cut[slot] = cut;
   S.id[slot] = g;
 }
 
 template <int kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads) k_blend_fwd(const float4 *__restrict__ splats,
+                                                           const float4 *__restrict__ exact,
                                                            const int32_t *__restrict__ offsets,
                                                            const int32_t *__restrict__ ids, int W, int H, int ts,
                                                            int tiles_x, int row_begin, float bg0, float bg1,
@@ -157,7 +253,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_fwd(const float4 *__restr
   bool done = !inside;
   for (int base = start; base < stop; base += batch) {
     if (__syncthreads_count(done) == B) break;
-    if (t < batch && base + t < stop) stage_splat(S, t, splats, ids[base + t]);
+    if (t < batch && base + t < stop) stage_splat(S, t, splats, exact, ids[base + t]);
     __syncthreads();
     const int cnt = min(batch, stop - base);
     for (int j0 = 0; j0 < cnt; j0 += 32) {
@@ -176,9 +272,8 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_fwd(const float4 *__restr
         const float2 m = S.xy[k];
         const float4 q = S.q[k];
         const float e2 = exponent2(q, fpx - m.x, fpy - m.y);
-        if (e2 < kE2Min || e2 > 0.0f) continue;
         float al = __fmul_rn(q.w, ex2_approx(e2));
-        if (al < kAlphaSkip) continue;
+        if (!decide_pair(e2, al, S.cut[k], splats, exact, S.id[k], fpx, fpy)) continue;
         al = fminf(al, kAlphaMax);
         const float4 col = S.col[k];
         const float w = al * T;
@@ -278,12 +373,14 @@ struct BwdShared {
   float4 q[kBB];
   float4 conic[kBB];  // a, b, c, alpha (raw, for the partials)
   float4 col[kBB];    // r, g, b, cull threshold
+  float2 cut[kBB];    // blend-cut bracket (load_cut)
   int32_t id[kBB];
   float acc[kWarpsMax][9][kBB];
 };
 
 template <int kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restrict__ splats,
+                                                           const float4 *__restrict__ exact,
                                                            const int32_t *__restrict__ offsets,
                                                            const int32_t *__restrict__ ids, int W, int H, int ts,
                                                            int tiles_x, int row_begin, float bg0, float bg1,
@@ -341,7 +438,9 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
       S.xy[t] = make_float2(a.x, a.y);
       S.q[t] = prescaled_conic(a, b);
       S.conic[t] = make_float4(a.z, a.w, b.x, b.y);
-      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, splat_thr2(b.y));
+      const float2 cut = load_cut(exact, g, b.y);
+      S.col[t] = make_float4(b.z, b.w, splats[3 * g + 2].x, cut.x - 0.02f);
+      S.cut[t] = cut;
       S.id[t] = g;
     }
     for (int e = t; e < nwarps * 9 * kBB; e += B) (&S.acc[0][0][0])[e] = 0.0f;
@@ -363,12 +462,13 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
           const float2 m = S.xy[q];
           const float dx = fpx - m.x, dy = fpy - m.y;
           const float e2 = exponent2(S.q[q], dx, dy);
-          if (!(e2 < kE2Min || e2 > 0.0f)) {
+          {
             const float4 cn = S.conic[q];
             const float gauss = ex2_approx(e2);
             const float a_raw = __fmul_rn(cn.w, gauss);
             const float al = fminf(a_raw, kAlphaMax);
-            if (al >= kAlphaSkip) {
+            const int dec = decide_pair(e2, a_raw, S.cut[q], splats, exact, S.id[q], fpx, fpy);
+            if (dec) {
               hit = true;
               const float4 col = S.col[q];
               const float inv_om = __fdividef(1.0f, 1.0f - al);
@@ -379,7 +479,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_blend_bwd(const float4 *__restr
               v[6] = g0 * w;
               v[7] = g1 * w;
               v[8] = g2 * w;
-              if (a_raw <= kAlphaMax) {
+              if (dec & 2) {  // a_raw <= 0.99 (decided with the blend)
                 v[5] = ga * gauss;
                 const float gG = ga * cn.w * gauss;
                 const float v0 = cn.x * dx + cn.y * dy, v1 = cn.y * dx + cn.z * dy;
@@ -587,8 +687,10 @@ struct Fwd16Pair {
   bool dA, dB;
 };
 
-__device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col, int pos,
-                                           int32_t *hits, int32_t gid) {
+template <bool kExact>
+__device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
+                                           float2 cut, int pos, int32_t *hits, int32_t gid,
+                                           const float4 *__restrict__ splats, const float4 *__restrict__ exact) {
   // checked before each entry (_kernels.py:57-58)
   P.dA = P.dA || P.T.x < kTTerm;
   P.dB = P.dB || P.T.y < kTTerm;
@@ -599,8 +701,16 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   const float b = __fmul_rn(q.y, dx);
   const float2 e2 = __ffma2_rn(make_float2(b, b), dy, s);  // exponent2() for both pixels
   float2 al = __fmul2_rn(make_float2(q.w, q.w), make_float2(ex2_approx(e2.x), ex2_approx(e2.y)));
-  const bool okA = !P.dA && !(e2.x < kE2Min || e2.x > 0.0f) && !(al.x < kAlphaSkip);
-  const bool okB = !P.dB && !(e2.y < kE2Min || e2.y > 0.0f) && !(al.y < kAlphaSkip);
+  // blend decisions (load_cut / exact_pair): certain in float32 outside the cut bracket;
+  // a visit with a pair inside it (rare) resolves it in float64 out of line
+  bool okA = !P.dA && e2.x >= cut.y;
+  bool okB = !P.dB && e2.y >= cut.y;
+  if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
+    const bool uA = !P.dA && !okA && e2.x >= cut.x, uB = !P.dB && !okB && e2.y >= cut.x;
+    const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
+    if (uA) okA = r & 1;
+    if (uB) okB = (r >> 2) & 1;
+  }
   al = make_float2(okA ? fminf(al.x, kAlphaMax) : 0.0f, okB ? fminf(al.y, kAlphaMax) : 0.0f);
   const float2 w = __fmul2_rn(al, P.T);
   P.c0 = __ffma2_rn(make_float2(col.x, col.x), w, P.c0);
@@ -643,8 +753,11 @@ __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 // skips the entry gets 1/(1-alpha) = 1, alpha = 0 and a zero Gaussian factor, so its
 // T and G.S are unchanged and it contributes exact zeros (the Gaussian factor is
 // masked BEFORE the products: an out-of-range exponent may give ex2 = inf).
+template <bool kExact>
 __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, float2 fy, float2 m, float4 q,
-                                           float4 cn, float4 col, float v[9]) {
+                                           float4 cn, float4 col, float2 cut, int32_t gid,
+                                           const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+                                           float v[9]) {
   const float dx = fpx - m.x;
   const float2 dy = __fadd2_rn(fy, f2(-m.y));
   const float t1 = __fmul_rn(__fmul_rn(q.x, dx), dx);
@@ -654,8 +767,25 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   const float2 gauss = make_float2(ex2_approx(e2.x), ex2_approx(e2.y));
   const float2 a_raw = __fmul2_rn(f2(cn.w), gauss);
   const float2 al = make_float2(fminf(a_raw.x, kAlphaMax), fminf(a_raw.y, kAlphaMax));
-  const bool okA = pos < P.lA && !(e2.x < kE2Min || e2.x > 0.0f) && !(al.x < kAlphaSkip);
-  const bool okB = pos < P.lB && !(e2.y < kE2Min || e2.y > 0.0f) && !(al.y < kAlphaSkip);
+  // the forward's decisions, re-derived identically (load_cut / exact_pair)
+  bool okA = pos < P.lA && e2.x >= cut.y;
+  bool okB = pos < P.lB && e2.y >= cut.y;
+  // unclamped (a_raw <= 0.99): the partials through alpha apply.  With exact records a
+  // Gaussian whose alpha can reach the clamp has cut_hi = +inf, so every certain pair is
+  // unclamped and only exact_pair() can report a clamped one.
+  bool clA = kExact || a_raw.x <= kAlphaMax, clB = kExact || a_raw.y <= kAlphaMax;
+  if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
+    const bool uA = pos < P.lA && !okA && e2.x >= cut.x, uB = pos < P.lB && !okB && e2.y >= cut.x;
+    const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
+    if (uA) {
+      okA = r & 1;
+      clA = r & 2;
+    }
+    if (uB) {
+      okB = (r >> 2) & 1;
+      clB = (r >> 3) & 1;
+    }
+  }
   // a pixel that skips the entry blends alpha 0: 1 / (1 - 0) is exactly 1 (rcp.approx of
   // 1.0f is exact, profiles/tma_dbg/rcp_one.cu), so T and the weights need no more selects
   const float2 alm = make_float2(okA ? al.x : 0.0f, okB ? al.y : 0.0f);
@@ -667,7 +797,7 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   const float2 w = __fmul2_rn(alm, tb);
   const float2 w6 = __fmul2_rn(P.g0, w), w7 = __fmul2_rn(P.g1, w), w8 = __fmul2_rn(P.g2, w);
   // partials through the unclamped alpha only (a_raw <= ALPHA_MAX)
-  const bool uA = okA && a_raw.x <= kAlphaMax, uB = okB && a_raw.y <= kAlphaMax;
+  const bool uA = okA && clA, uB = okB && clB;
   // dL/dalpha_raw-side product ga * G, masked once (a select discards the NaN / Inf an
   // out-of-range Gaussian factor can give)
   const float2 gx = __fmul2_rn(ga, gauss);
@@ -693,6 +823,7 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   return okA || okB;
 }
 
+
 // ---------------------------------------------------------------------------
 // Warp-independent 16x16 kernels: each warp of a tile's CTA walks the tile list
 // on its own, staging 32 splats at a time in a private shared-memory slot (the
@@ -706,27 +837,32 @@ struct WStage {
   float4 q[32];      // prescaled conic + alpha
   float4 col[32];    // r, g, b, cull threshold (log2 units)
   float4 conic[32];  // raw a, b, c, alpha (backward)
+  float2 cut[32];    // blend-cut bracket (load_cut)
   int32_t id[32];
 };
 
 struct SplatRegs {
   float4 a, b;
   float c;
+  float2 cut;
   int32_t g;
 };
 
 __device__ __forceinline__ void fetch_splat(SplatRegs &r, const float4 *__restrict__ splats,
-                                            const int32_t *__restrict__ ids, int pos, bool ok) {
+                                            const float4 *__restrict__ exact, const int32_t *__restrict__ ids,
+                                            int pos, bool ok) {
   if (ok) {
     r.g = __ldg(ids + pos);
     r.a = __ldg(splats + 3 * r.g);
     r.b = __ldg(splats + 3 * r.g + 1);
     r.c = __ldg(reinterpret_cast<const float *>(splats + 3 * r.g + 2));
+    if (exact) r.cut = __ldg(reinterpret_cast<const float2 *>(exact + 2 * (int64_t)r.g));
   }
 }
 
-__global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
-    const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
+template <bool kExact>
+__global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_blend_fwd16w(
+    const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
     float *__restrict__ transmit, float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ last_pos, int32_t *__restrict__ hits, const int32_t *__restrict__ order) {
@@ -746,7 +882,7 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
   P.dB = !inB;
   const float2 fy = make_float2(fyA, fyB);
   SplatRegs nx;
-  fetch_splat(nx, splats, ids, start + lane, start + lane < stop);
+  fetch_splat(nx, splats, kExact ? exact : nullptr, ids, start + lane, start + lane < stop);
   float4 wbc = wb;
   for (int c = start; c < stop; c += 32) {
     if (__all_sync(0xffffffffu, P.dA && P.dB)) break;
@@ -756,24 +892,26 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
     bool keep = false;
     if (ok) {
       const float4 q = prescaled_conic(nx.a, nx.b);
-      const float thr = splat_thr2(nx.b.y);
+      const float2 cut = kExact ? nx.cut : load_cut(nullptr, nx.g, nx.b.y);
+      const float thr = cut.x - 0.02f;  // cull: nothing below cut.x blends
       const float2 m = make_float2(nx.a.x, nx.a.y);
       S.xy[lane] = m;
       S.q[lane] = q;
       S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
     }
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
-    fetch_splat(nx, splats, ids, c + 32 + lane, c + 32 + lane < stop);
+    fetch_splat(nx, splats, kExact ? exact : nullptr, ids, c + 32 + lane, c + 32 + lane < stop);
     while (mask) {
       const int k = __ffs(mask) - 1;
       mask &= mask - 1;
       const float2 m = S.xy[k];
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
-      fwd_visit2(P, fpx, fy, m, q, col, pos, hits, S.id[k]);
+      fwd_visit2<kExact>(P, fpx, fy, m, q, col, S.cut[k], pos, hits, S.id[k], splats, exact);
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
@@ -801,8 +939,9 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_fwd16w(
   }
 }
 
-__global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
-    const float4 *__restrict__ splats, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
+template <bool kExact>
+__global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_blend_bwd16w(
+    const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, const float *__restrict__ transmit,
     const int32_t *__restrict__ last_pos, const float *__restrict__ dimage, float *__restrict__ dsplats,
     const int32_t *__restrict__ order) {
@@ -843,7 +982,7 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
   SplatRegs nx;
   // back to front over chunks [lo, hi) of 32 list positions below this warp's last blend
   int hi = wlast;
-  fetch_splat(nx, splats, ids, start + hi - 32 + lane, hi - 32 + lane >= 0);
+  fetch_splat(nx, splats, kExact ? exact : nullptr, ids, start + hi - 32 + lane, hi - 32 + lane >= 0);
   for (; hi > 0; hi -= 32) {
     const int lo = hi - 32;  // may be negative: lanes below position 0 are idle
     const bool ok = lo + lane >= 0;
@@ -852,30 +991,34 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
     const float4 wbc = warp_bounds2(PB.lA > lo, PB.lB > lo, px, pyA, pyB);
     if (ok) {
       const float4 q = prescaled_conic(nx.a, nx.b);
-      const float thr = splat_thr2(nx.b.y);
+      const float2 cut = kExact ? nx.cut : load_cut(nullptr, nx.g, nx.b.y);
+      const float thr = cut.x - 0.02f;  // cull: nothing below cut.x blends
       const float2 m = make_float2(nx.a.x, nx.a.y);
       S.xy[lane] = m;
       S.q[lane] = q;
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
       S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
     }
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
-    fetch_splat(nx, splats, ids, start + lo - 32 + lane, lo - 32 + lane >= 0);
+    fetch_splat(nx, splats, kExact ? exact : nullptr, ids, start + lo - 32 + lane, lo - 32 + lane >= 0);
     // surviving splats back to front, two per reduction (the second one, if any,
     // follows the first in each pixel's walk, so the per-pixel order is unchanged)
     while (mask) {
       float v0[9], v1[9];
       const int b0 = 31 - __clz(mask);
       mask &= ~(1u << b0);
-      bool hit = bwd_visit2(PB, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], v0);
+      bool hit = bwd_visit2<kExact>(PB, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], S.cut[b0], S.id[b0],
+                            splats, exact, v0);
       int id1 = -1;
       if (mask) {  // warp-uniform
         const int b1 = 31 - __clz(mask);
         mask &= ~(1u << b1);
-        hit = bwd_visit2(PB, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], v1) || hit;
+        hit = bwd_visit2<kExact>(PB, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], S.cut[b1], S.id[b1],
+                         splats, exact, v1) || hit;
         id1 = S.id[b1];
       } else {
 #pragma unroll
@@ -903,7 +1046,8 @@ __global__ void __launch_bounds__(kT16Threads) k_blend_bwd16w(
 }
 
 // _kernels.py:184-241: same walk as the forward, writing (gid, a*T) per blended entry
-__global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t *__restrict__ offsets,
+__global__ void k_blend_records(const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+                                const int32_t *__restrict__ offsets,
                                 const int32_t *__restrict__ ids, int W, int H, int ts, int tiles_x,
                                 const int64_t *__restrict__ pix_off, int32_t *__restrict__ rec_g,
                                 float *__restrict__ rec_w) {
@@ -922,9 +1066,8 @@ __global__ void k_blend_records(const float4 *__restrict__ splats, const int32_t
     const int g = ids[k];
     const float4 a = splats[3 * g], b = splats[3 * g + 1];
     const float e2 = exponent2(prescaled_conic(a, b), (float)px - a.x, (float)py - a.y);
-    if (e2 < kE2Min || e2 > 0.0f) continue;
     float al = __fmul_rn(b.y, ex2_approx(e2));
-    if (al < kAlphaSkip) continue;
+    if (!decide_pair(e2, al, load_cut(exact, g, b.y), splats, exact, g, (float)px, (float)py)) continue;
     al = fminf(al, kAlphaMax);
     rec_g[pos] = g;
     rec_w[pos] = al * T;
@@ -998,30 +1141,50 @@ inline int tile_size_guard(int ts) { return ts < 1 ? 1 : ts; }
 
 using namespace tgs;
 
-extern "C" int tgs_blend_forward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+// Profiling build only (-DTGS_COUNT_EXACT): the number of (pixel, splat) pairs decided in
+// float64 since the last reset.  Returns TGS_ERR_UNSUPPORTED in a normal build.
+extern "C" int tgs_debug_exact_pairs(unsigned long long *count, int32_t reset) {
+#ifdef TGS_COUNT_EXACT
+  if (count && cudaMemcpyFromSymbol(count, g_exact_pairs, sizeof(*count)) != cudaSuccess) return TGS_ERR_CUDA;
+  if (reset) {
+    const unsigned long long z = 0;
+    if (cudaMemcpyToSymbol(g_exact_pairs, &z, sizeof(z)) != cudaSuccess) return TGS_ERR_CUDA;
+  }
+  return TGS_OK;
+#else
+  (void)count;
+  (void)reset;
+  return TGS_ERR_UNSUPPORTED;
+#endif
+}
+
+extern "C" int tgs_blend_forward(const float *splats, const float *exact, const int32_t *tile_offsets,
+                                 const int32_t *sorted_ids,
                                  const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                                  float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
                                  int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
-  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
+  const float4 *ex = reinterpret_cast<const float4 *>(exact);
   if (s->tile_size == 16) {
-    k_blend_fwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
-        reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
+    (ex ? k_blend_fwd16w<true> : k_blend_fwd16w<false>)<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
         last_pos, hits, tile_order);
     return launch_status();
   }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
   (B <= 256 ? k_blend_fwd<256> : k_blend_fwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum,
       n_contrib, last_pos, hits);
   return launch_status();
 }
 
-extern "C" int tgs_blend_records(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+extern "C" int tgs_blend_records(const float *splats, const float *exact, const int32_t *tile_offsets,
+                                 const int32_t *sorted_ids,
                                  const tgs_camera *cam, const tgs_settings *s, const int64_t *pixel_offsets,
                                  int32_t *rec_gauss, float *rec_weight, tgs_stream_t stream) {
   int tiles_x, ntiles;
@@ -1030,30 +1193,34 @@ extern "C" int tgs_blend_records(const float *splats, const int32_t *tile_offset
   if (!blend_args(cam, s, 0, tiles_y, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
-  k_blend_records<<<ntiles, B, 0, as_stream(stream)>>>(reinterpret_cast<const float4 *>(splats), tile_offsets,
+  if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
+  k_blend_records<<<ntiles, B, 0, as_stream(stream)>>>(reinterpret_cast<const float4 *>(splats),
+                                                       reinterpret_cast<const float4 *>(exact), tile_offsets,
                                                        sorted_ids, cam->width, cam->height, s->tile_size, tiles_x,
                                                        pixel_offsets, rec_gauss, rec_weight);
   return launch_status();
 }
 
-extern "C" int tgs_blend_backward(const float *splats, const int32_t *tile_offsets, const int32_t *sorted_ids,
+extern "C" int tgs_blend_backward(const float *splats, const float *exact, const int32_t *tile_offsets,
+                                  const int32_t *sorted_ids,
                                   const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                                   const float *transmit, const int32_t *last_pos, const float *dimage,
                                   float *dsplats, const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
-  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
+  const float4 *ex = reinterpret_cast<const float4 *>(exact);
   if (s->tile_size == 16) {
-    k_blend_bwd16w<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
-        reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
+    (ex ? k_blend_bwd16w<true> : k_blend_bwd16w<false>)<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
         tile_order);
     return launch_status();
   }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
   (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage,
       dsplats, nullptr);
   return launch_status();
@@ -1077,7 +1244,8 @@ extern "C" int tgs_blend_backward_deterministic_workspace(int64_t n, int64_t num
   return TGS_OK;
 }
 
-extern "C" int tgs_blend_backward_deterministic(const float *splats, const int32_t *tiles_touched, int64_t n,
+extern "C" int tgs_blend_backward_deterministic(const float *splats, const float *exact,
+                                                const int32_t *tiles_touched, int64_t n,
                                                 const int32_t *tile_offsets, const int32_t *sorted_ids,
                                                 int64_t num_instances, const tgs_camera *cam, const tgs_settings *s,
                                                 int32_t row_begin, int32_t row_end, const float *transmit,
@@ -1085,7 +1253,7 @@ extern "C" int tgs_blend_backward_deterministic(const float *splats, const int32
                                                 void *workspace, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
-  if (reinterpret_cast<uintptr_t>(splats) & 15) return TGS_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
   if (n < 0 || num_instances < 0 || num_instances >= ((int64_t)1 << 30) || !workspace || !tiles_touched)
     return TGS_ERR_INVALID;
   if (ntiles == 0 || n == 0) return TGS_OK;
@@ -1100,7 +1268,7 @@ extern "C" int tgs_blend_backward_deterministic(const float *splats, const int32
   const int tiles_y = (cam->height + s->tile_size - 1) / s->tile_size;
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;
   (B <= 256 ? k_blend_bwd<256> : k_blend_bwd<1024>)<<<ntiles, B, 0, st>>>(
-      reinterpret_cast<const float4 *>(splats), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
+      reinterpret_cast<const float4 *>(splats), reinterpret_cast<const float4 *>(exact), tile_offsets, sorted_ids, cam->width, cam->height, s->tile_size,
       tiles_x, row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
       partial);
   const unsigned gn = (unsigned)ceil_div<int64_t>(n, 256);

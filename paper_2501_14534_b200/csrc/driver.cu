@@ -47,7 +47,8 @@ extern "C" int tgs_render_views_workspace(int64_t n, int64_t max_instances, int3
 
 extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s, int32_t nviews,
                                 float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
-                                uint64_t *const *depth_keys, int32_t *error_flag, tgs_view_target *targets,
+                                uint64_t *const *depth_keys, float *const *exact, int32_t *error_flag,
+                                tgs_view_target *targets,
                                 void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
                                 const tgs_stream_t *streams, const tgs_stream_t *blend_streams, int32_t nstreams) {
   if (!cloud || !cams || !s || nviews < 1 || !splats || !visible || !tiles_touched || !targets || !workspaces ||
@@ -70,7 +71,7 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
   cudaStream_t st0 = reinterpret_cast<cudaStream_t>(streams[0]);
   // 1. every view's preprocess in one pass over the parameters (stream 0)
   rc = tgs_preprocess_forward_views(cloud, cams, s, nviews, splats, visible, tiles_touched, depth_keys, error_flag,
-                                    nullptr, streams[0]);
+                                    nullptr, nullptr, streams[0]);
   if (rc != TGS_OK) return rc;
   cudaEvent_t ev_pre, ev[kMaxStreams], ev_b[kMaxStreams];
   if (cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming) != cudaSuccess) return TGS_ERR_CUDA;
@@ -80,6 +81,28 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
   }
   cudaEventRecord(ev_pre, st0);
   for (int k = 1; k < nstreams; ++k) cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(streams[k]), ev_pre, 0);
+  // 1b. the exact blend-decision records on a blend stream (the depth sorts do not read
+  // them, so the latency-bound binning of the first views runs alongside); every blend
+  // waits for them
+  cudaEvent_t ev_ex = nullptr;
+  if (exact) {
+    tgs_stream_t xs = blend_streams ? blend_streams[0] : streams[nstreams - 1];
+    cudaStream_t xst = reinterpret_cast<cudaStream_t>(xs);
+    if (cudaEventCreateWithFlags(&ev_ex, cudaEventDisableTiming) != cudaSuccess) rc = TGS_ERR_CUDA;
+    if (rc == TGS_OK && xst != st0) cudaStreamWaitEvent(xst, ev_pre, 0);
+    if (rc == TGS_OK)
+      rc = tgs_exact_records_views(cloud, cams, s, nviews, const_cast<const float *const *>(splats), exact, xs);
+    if (rc == TGS_OK && cudaEventRecord(ev_ex, xst) != cudaSuccess) rc = TGS_ERR_CUDA;
+    if (rc != TGS_OK) {
+      if (ev_ex) cudaEventDestroy(ev_ex);
+      cudaEventDestroy(ev_pre);
+      for (int k = 0; k < nstreams; ++k) {
+        cudaEventDestroy(ev[k]);
+        cudaEventDestroy(ev_b[k]);
+      }
+      return rc;
+    }
+  }
 
   const int ts = s->tile_size;
   auto rows_of = [&](int v) { return (cams[v].height + ts - 1) / ts; };
@@ -121,7 +144,8 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
       cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(blend_streams[k]), ev_b[k], 0);
       bs = blend_streams[k];
     }
-    return tgs_blend_forward(splats[v], t.tile_offsets, t.sorted_ids, &cams[v], s, 0, rows_of(v), t.image, t.transmit,
+    if (ev_ex) cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(bs), ev_ex, 0);
+    return tgs_blend_forward(splats[v], exact ? exact[v] : nullptr, t.tile_offsets, t.sorted_ids, &cams[v], s, 0, rows_of(v), t.image, t.transmit,
                              t.weight_sum, t.n_contrib, t.last_pos, t.hits, t.tile_order, bs);
   };
   // Per stream k the queue is  bin_instances(v) -> bin_gaussians(v + nstreams) -> blend(v):
@@ -155,6 +179,7 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
     }
   }
   cudaEventDestroy(ev_pre);
+  if (ev_ex) cudaEventDestroy(ev_ex);
   for (int k = 0; k < nstreams; ++k) {
     cudaEventDestroy(ev[k]);
     cudaEventDestroy(ev_b[k]);

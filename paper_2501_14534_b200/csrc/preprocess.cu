@@ -154,6 +154,125 @@ __device__ __forceinline__ void gauss_forward(const tgs_cloud &cl, int64_t i, co
   gauss_view<DEG>(cl, i, cam, s, rest, f);
 }
 
+// ---- exact blend-decision records (include/tgs.h TGS_EXACT_FLOATS) ----------------
+// The blend kernels decide from the float32 record whether Gaussian g blends into pixel
+// p (e >= -4.5, e <= 0, alpha exp(e) >= 1/255: _kernels.py:62-72).  The reference makes
+// that decision in float64; close to a threshold float32 can decide the other way and
+// move a pixel by a whole contribution.  Here the float64 projection is recomputed in
+// the reference's operation order (this file is compiled with -fmad=false, so no
+// operation is fused) and turned into
+//   * a float32 bracket [cut_lo, cut_hi] around the float64 cut, widened by a bound on
+//     the error of the blend kernels' float32 exponent over the Gaussian's footprint
+//     (record errors times the footprint's extent, plus the evaluation's roundings),
+//     so outside the bracket the float32 comparison IS the float64 decision;
+//   * the float64-minus-float32 residuals of means, conic and alpha, from which the
+//     blend kernels rebuild the float64 record for the rare pairs inside the bracket.
+struct Static64 {  // view-independent float64 state (masking.py:34-43, geometry.py:19-41,74-77)
+  double S[6];     // S00 S01 S02 S11 S12 S22
+  double alpha;    // sigmoid(o) * M
+  double cut;      // the blend cut max(-4.5, ln(1 / (255 alpha))) (_kernels.py:62-72)
+};
+
+__device__ __forceinline__ void gauss_static64(const tgs_cloud &cl, int64_t i, float Mg, Static64 &g) {
+  const double M = (double)Mg;
+  double sc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sc[k] = exp((double)cl.log_scales[3 * i + k]) * M;
+  const double qw = cl.rotations[4 * i], qx = cl.rotations[4 * i + 1];
+  const double qy = cl.rotations[4 * i + 2], qz = cl.rotations[4 * i + 3];
+  const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  const double w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
+  const double Rg[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                        2.0 * (x * y + w * z),       1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                        2.0 * (x * z - w * y),       2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+  double L[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) L[3 * r + k] = Rg[3 * r + k] * sc[k];
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) g.S[e++] = L[3 * a] * L[3 * b] + L[3 * a + 1] * L[3 * b + 1] + L[3 * a + 2] * L[3 * b + 2];
+  g.alpha = (1.0 / (1.0 + exp(-(double)cl.opacity_logits[i]))) * M;
+  g.cut = g.alpha > 0.0 ? fmax(-4.5, -log(255.0 * g.alpha)) : 0.0;
+}
+
+constexpr double kLog2eD = 1.4426950408889634;
+
+// One view's exact record of a visible Gaussian; a, b: the first two float4 of its float32
+// record (means, conic, alpha).
+__device__ __forceinline__ void exact_record(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
+                                             const tgs_settings &s, const Static64 &g, float4 a, float4 b,
+                                             float4 *__restrict__ out) {
+  const float alpha32 = b.y;
+  // project_gaussians in float64 (geometry.py:153-183) in the oracle's operation order, with
+  // the divisions by t_z and det as multiplications by one reciprocal each: the record only
+  // has to be float64-accurate (~1e-15 relative), its residuals are stored as float32 anyway
+  const double px = cl.positions[3 * i], py = cl.positions[3 * i + 1], pz = cl.positions[3 * i + 2];
+  double t[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) t[r] = px * cam.R64[3 * r] + py * cam.R64[3 * r + 1] + pz * cam.R64[3 * r + 2] + cam.t64[r];
+  const double itz = 1.0 / t[2];
+  const double m0 = cam.fx64 * t[0] * itz + cam.cx64, m1 = cam.fy64 * t[1] * itz + cam.cy64;
+  const double J00 = cam.fx64 * itz, J02 = -cam.fx64 * t[0] * (itz * itz);
+  const double J11 = cam.fy64 * itz, J12 = -cam.fy64 * t[1] * (itz * itz);
+  double Mj[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    Mj[j] = J00 * cam.R64[j] + J02 * cam.R64[6 + j];
+    Mj[3 + j] = J11 * cam.R64[3 + j] + J12 * cam.R64[6 + j];
+  }
+  auto Sg = [&](int a, int b) -> double {
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    return g.S[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
+  };
+  double A[6];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) A[3 * r + j] = Mj[3 * r] * Sg(0, j) + Mj[3 * r + 1] * Sg(1, j) + Mj[3 * r + 2] * Sg(2, j);
+  const double lp = s.lowpass_s64;
+  const double c00 = A[0] * Mj[0] + A[1] * Mj[1] + A[2] * Mj[2] + lp;
+  const double c01 = A[0] * Mj[3] + A[1] * Mj[4] + A[2] * Mj[5];
+  const double c11 = A[3] * Mj[3] + A[4] * Mj[4] + A[5] * Mj[5] + lp;
+  const double det = c00 * c11 - c01 * c01;
+  if (!(det > 1e-300) || !(g.alpha > 0.0)) {
+    // culled in float64 (geometry.py:176): never blends there
+    const float inf = __int_as_float(0x7f800000);
+    out[0] = make_float4(inf, inf, 0.f, 0.f);
+    out[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const double inv = 1.0 / det;
+  const double k0 = c11 * inv, k1 = -c01 * inv, k2 = c00 * inv;
+  const double dmx = m0 - (double)a.x, dmy = m1 - (double)a.y;
+  const double dk0 = k0 - (double)a.z, dk1 = k1 - (double)a.w, dk2 = k2 - (double)b.x;
+  // the error bound in float32 (an upper bound only needs a few digits): footprint of the
+  // pixels near the cut, |dx| <= X, |dy| <= Y on {e >= cut - margin}, then
+  // |e32 - e64| <= record error over the footprint + float32 evaluation roundings
+  const float cut = (float)g.cut;
+  const float reach = 2.0f * (fabsf(cut) + 0.01f);
+  const float X = 1.001f * sqrtf(reach * (float)c00), Y = 1.001f * sqrtf(reach * (float)c11);
+  const float a0 = fabsf(a.z) * 1.001f, a1 = fabsf(a.w) * 1.001f, a2 = fabsf(b.x) * 1.001f;
+  float E = (a0 * X + a1 * Y) * fabsf((float)dmx) + (a1 * X + a2 * Y) * fabsf((float)dmy) +
+            0.5f * (fabsf((float)dk0) * X * X + fabsf((float)dk2) * Y * Y) + fabsf((float)dk1) * X * Y +
+            1e-6f * (a0 * X * X + 2.0f * a1 * X * Y + a2 * Y * Y) + 1e-6f;
+  const double E2 = 2.0 * (double)E;  // safety factor
+  const float lo = __double2float_rd((g.cut - E2) * kLog2eD);
+  // alpha able to reach the 0.99 clamp: every pair of this Gaussian goes to float64, where
+  // the cut is -4.5 (alpha > 0.9899 puts ln(1/(255 alpha)) below it) and slot 7 holds the
+  // clamp's exponent ln(0.99 / alpha) (alpha exp(e) <= 0.99 <=> e <= it); otherwise slot 7
+  // holds the float64 cut minus cut_lo (log2 units) for the float64 comparison e >= cut
+  const bool clampable = g.alpha > 0.9899;
+  const float hi = clampable ? __int_as_float(0x7f800000) : __double2float_ru((g.cut + E2) * kLog2eD);
+  const float slot7 = clampable ? (float)log(0.99 / g.alpha) : (float)(g.cut * kLog2eD - (double)lo);
+  (void)alpha32;
+  out[0] = make_float4(lo, hi, (float)dmx, (float)dmy);
+  out[1] = make_float4((float)dk0, (float)dk1, (float)dk2, slot7);
+}
+
 template <int DEG>
 __device__ __forceinline__ void emit_view_impl(const tgs_cloud &cl, int64_t i, const tgs_camera &cam,
                                                const tgs_settings &s, float *rest, float *__restrict__ splats,
@@ -275,6 +394,42 @@ __device__ __forceinline__ void emit_record(const tgs_cloud &cl, int64_t i, cons
   }
 }
 
+// Exact blend-decision records of a batch of views from their float32 records (a row
+// with alpha 0 is not visible): the view-independent float64 state once per Gaussian.
+struct ExactViews {
+  tgs_camera cam[kMaxFwdViews];
+  const float4 *splats[kMaxFwdViews];
+  float4 *exact[kMaxFwdViews];
+  int nviews;
+};
+
+__global__ void __launch_bounds__(kPreBlock) k_exact_views(tgs_cloud cl, ExactViews ev, tgs_settings s) {
+  const int64_t i = (int64_t)blockIdx.x * kPreBlock + threadIdx.x;
+  if (i >= cl.n) return;
+  float al[kMaxFwdViews];  // every view's record alpha first (independent loads)
+  bool any = false;
+#pragma unroll
+  for (int v = 0; v < kMaxFwdViews; ++v)
+    if (v < ev.nviews) {
+      al[v] = __ldg(reinterpret_cast<const float *>(ev.splats[v] + 3 * i + 1) + 1);
+      any = any || al[v] > 0.0f;
+    }
+  Static64 g;
+  if (any) gauss_static64(cl, i, cl.mask_logits[i] > s.mask_logit_min ? 1.0f : 0.0f, g);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int v = 0; v < kMaxFwdViews; ++v)
+    if (v < ev.nviews) {
+      float4 *o = ev.exact[v] + 2 * i;
+      if (al[v] > 0.0f) {
+        exact_record(cl, i, ev.cam[v], s, g, __ldg(ev.splats[v] + 3 * i), __ldg(ev.splats[v] + 3 * i + 1), o);
+      } else {
+        o[0] = zero;
+        o[1] = zero;
+      }
+    }
+}
+
 __global__ void k_count_tiles(const float *__restrict__ splats, int64_t n, int W, int H, int ts, int tiles_x,
                               int tiles_y, int32_t *__restrict__ tiles) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -290,8 +445,9 @@ using namespace tgs;
 
 extern "C" int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *cam, const tgs_settings *s,
                                       float *splats, uint8_t *visible, int32_t *tiles_touched,
-                                      uint64_t *depth_keys, int32_t *error_flag, tgs_stream_t stream) {
+                                      uint64_t *depth_keys, int32_t *error_flag, float *exact, tgs_stream_t stream) {
   if (!cloud || !cam || !s || cloud->n < 0) return TGS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(exact) & 15) return TGS_ERR_INVALID;
   if (s->tile_size < 1 || s->tile_size > 32) return TGS_ERR_UNSUPPORTED;
   if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
   if (cloud->n == 0) return TGS_OK;
@@ -304,21 +460,25 @@ extern "C" int tgs_preprocess_forward(const tgs_cloud *cloud, const tgs_camera *
     TGS_FWD(0) TGS_FWD(1) TGS_FWD(2) TGS_FWD(3)
 #undef TGS_FWD
   }
-  return launch_status();
+  const int rc = launch_status();
+  if (rc != TGS_OK || !exact) return rc;
+  const float *sp = splats;
+  return tgs_exact_records_views(cloud, cam, s, 1, &sp, &exact, stream);
 }
 
 extern "C" int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
                                             int32_t nviews, float *const *splats, uint8_t *const *visible,
                                             int32_t *const *tiles_touched, uint64_t *const *depth_keys,
                                             int32_t *error_flag, const tgs_densify_stats *stats,
-                                            tgs_stream_t stream) {
+                                            float *const *exact, tgs_stream_t stream) {
   if (!cloud || !cams || !s || cloud->n < 0 || nviews < 1 || !splats || !visible || !tiles_touched)
     return TGS_ERR_INVALID;
   if (s->tile_size < 1 || s->tile_size > 32) return TGS_ERR_UNSUPPORTED;
   if (s->active_sh_degree < 0 || s->active_sh_degree > 3) return TGS_ERR_INVALID;
   if (cloud->n == 0) return TGS_OK;
   for (int v = 0; v < nviews; ++v)
-    if (!splats[v] || (reinterpret_cast<uintptr_t>(splats[v]) & 15) || !visible[v] || !tiles_touched[v])
+    if (!splats[v] || (reinterpret_cast<uintptr_t>(splats[v]) & 15) || !visible[v] || !tiles_touched[v] ||
+        (exact && (!exact[v] || (reinterpret_cast<uintptr_t>(exact[v]) & 15))))
       return TGS_ERR_INVALID;
   const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
   cudaStream_t st = as_stream(stream);
@@ -339,6 +499,31 @@ extern "C" int tgs_preprocess_forward_views(const tgs_cloud *cloud, const tgs_ca
       TGS_FWDV(0) TGS_FWDV(1) TGS_FWDV(2) TGS_FWDV(3)
 #undef TGS_FWDV
     }
+  }
+  const int rc = launch_status();
+  if (rc != TGS_OK || !exact) return rc;
+  return tgs_exact_records_views(cloud, cams, s, nviews, splats, exact, stream);
+}
+
+extern "C" int tgs_exact_records_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s,
+                                       int32_t nviews, const float *const *splats, float *const *exact,
+                                       tgs_stream_t stream) {
+  if (!cloud || !cams || !s || cloud->n < 0 || nviews < 1 || !splats || !exact) return TGS_ERR_INVALID;
+  if (cloud->n == 0) return TGS_OK;
+  for (int v = 0; v < nviews; ++v)
+    if (!splats[v] || !exact[v] || ((reinterpret_cast<uintptr_t>(splats[v]) | reinterpret_cast<uintptr_t>(exact[v])) & 15))
+      return TGS_ERR_INVALID;
+  const unsigned grid = (unsigned)ceil_div<int64_t>(cloud->n, kPreBlock);
+  cudaStream_t st = as_stream(stream);
+  for (int v0 = 0; v0 < nviews; v0 += kMaxFwdViews) {
+    ExactViews ev;
+    ev.nviews = nviews - v0 < kMaxFwdViews ? nviews - v0 : kMaxFwdViews;
+    for (int k = 0; k < ev.nviews; ++k) {
+      ev.cam[k] = cams[v0 + k];
+      ev.splats[k] = reinterpret_cast<const float4 *>(splats[v0 + k]);
+      ev.exact[k] = reinterpret_cast<float4 *>(exact[v0 + k]);
+    }
+    k_exact_views<<<grid, kPreBlock, 0, st>>>(*cloud, ev, *s);
   }
   return launch_status();
 }

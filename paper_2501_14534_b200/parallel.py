@@ -95,7 +95,7 @@ def render_sharded(cloud, cam, settings, group=None):
     ts = int(settings.tile_size)
     n = len(cloud)
     dev = cloud.device
-    splats, vis, tiles, keys, err = preprocess(cloud, cam, settings)  # replicated
+    splats, vis, tiles, keys, err, exact = preprocess(cloud, cam, settings)  # replicated
     with stage("row_split"):
         counts = row_histogram(splats, tiles, n, cam, ts).cpu().numpy()
     bands = row_split(counts, world)
@@ -114,7 +114,7 @@ def render_sharded(cloud, cam, settings, group=None):
         lp = torch.empty_like(nc)
         c_cam, c_set = lib.make_camera(cam), lib.make_settings(settings)
         with stage("blend_fwd"):
-            lib.call("tgs_blend_forward", lib.ptr(splats), lib.ptr(bins.offsets), lib.ptr(bins.indices),
+            lib.call("tgs_blend_forward", lib.ptr(splats), lib.ptr(exact), lib.ptr(bins.offsets), lib.ptr(bins.indices),
                      ctypes.byref(c_cam), ctypes.byref(c_set), bands_r[0], bands_r[1], lib.ptr(image),
                      lib.ptr(transmit), lib.ptr(wsum), lib.ptr(nc), lib.ptr(lp), None, lib.ptr(bins.order),
                      lib.stream_handle(dev))

@@ -87,6 +87,7 @@ class _DeviceState:
     tiles_touched: torch.Tensor
     depth_keys: torch.Tensor | None
     bins: TileBins
+    exact: torch.Tensor | None = None  # (N, 8) exact blend-decision records (include/tgs.h TGS_EXACT_FLOATS)
 
 
 @dataclass
@@ -223,6 +224,16 @@ _CENTER = {}
 #   "none":   row-major.
 BLEND_ORDER = "center"
 
+# Exact (float64) blend decisions at the thresholds (include/tgs.h TGS_EXACT_FLOATS): on by
+# default; TGS_EXACT=0 makes the blend kernels decide every pair in float32 (A/B timing of
+# the decision cost only — the north-star parity needs the records).
+import os as _os
+EXACT_DECISIONS = _os.environ.get("TGS_EXACT", "1") != "0"
+
+
+def _ex(exact):
+    return exact if EXACT_DECISIONS else None
+
 
 def _blend_order(offsets, ntiles: int, tiles_x: int, rows: int, ts: int, dev, st):
     if ts != 16 or ntiles == 0 or BLEND_ORDER == "none":
@@ -315,7 +326,8 @@ def _as_cloud(cloud) -> GaussianCloud:
 
 
 def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
-    """tgs_preprocess_forward: (splats (N,12), visible u8, tiles_touched i32, float64 depth keys, error flag)."""
+    """tgs_preprocess_forward: (splats (N,12), visible u8, tiles_touched i32, float64 depth keys, error flag,
+    exact blend-decision records (N,8))."""
     n = len(cloud)
     dev = cloud.device
     splats = torch.empty((max(n, 1), 12), dtype=torch.float32, device=dev)
@@ -323,21 +335,24 @@ def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
     tiles = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
     keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
+    exact = torch.zeros((max(n, 1), 8), dtype=torch.float32, device=dev)
     if n:
         c_cloud, c_cam, c_set = cloud.native(), _lib.make_camera(cam), _lib.make_settings(settings)
         import ctypes
         with stage("preprocess_fwd"):
             _lib.call("tgs_preprocess_forward", ctypes.byref(c_cloud), ctypes.byref(c_cam), ctypes.byref(c_set),
                       _lib.ptr(splats), _lib.ptr(vis), _lib.ptr(tiles), _lib.ptr(keys), _lib.ptr(err),
-                      _lib.stream_handle(dev))
-    return splats, vis, tiles, keys, err
+                      _lib.ptr(exact), _lib.stream_handle(dev))
+    return splats, vis, tiles, keys, err, exact
 
 
-def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, stats=None) -> list:
+def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, stats=None,
+                     exact: bool = True) -> list:
     """tgs_preprocess_forward_views: the per-view preprocess outputs of a batch of views in
     one pass over the parameters; element v is what `preprocess(cloud, cams[v], settings)`
     returns (bit-identical), the error flag shared.  stats: optional train.DensifyStats
-    (its area_max takes the views' screen areas, training.py:338)."""
+    (its area_max takes the views' screen areas, training.py:338).  exact=False leaves the
+    exact blend-decision records to a later exact_records() call (e.g. on another stream)."""
     import ctypes
     n = len(cloud)
     dev = cloud.device
@@ -350,10 +365,11 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
     vis = torch.empty((V, m), dtype=torch.uint8, device=dev)
     tiles = torch.empty((V, m), dtype=torch.int32, device=dev)
     keys = torch.empty((V, m), dtype=torch.int64, device=dev)
+    ex = torch.empty((V, m, 8), dtype=torch.float32, device=dev)
     if n == 0:
-        for t in (sp, vis, tiles, keys):
+        for t in (sp, vis, tiles, keys, ex):
             t.zero_()
-    outs = [(sp[v], vis[v], tiles[v], keys[v], err) for v in range(V)]
+    outs = [(sp[v], vis[v], tiles[v], keys[v], err, ex[v]) for v in range(V)]
     if n and V:
         c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
         c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
@@ -362,8 +378,24 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
             c_stats = stats.native() if stats is not None else None
             _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0),
                       arr(1), arr(2), arr(3), _lib.ptr(err), ctypes.byref(c_stats) if c_stats else None,
-                      _lib.stream_handle(dev))
+                      arr(5) if exact else None, _lib.stream_handle(dev))
     return outs
+
+
+def exact_records(cloud: GaussianCloud, cams: list, settings: RenderSettings, pres: list) -> None:
+    """tgs_exact_records_views on the current stream: the exact blend-decision records
+    (include/tgs.h TGS_EXACT_FLOATS) of preprocess_views(..., exact=False) outputs."""
+    import ctypes
+    n, V = len(cloud), len(cams)
+    if n == 0 or V == 0:
+        return
+    c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
+    c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+    sps = (ctypes.c_void_p * V)(*[p[0].data_ptr() for p in pres])
+    exs = (ctypes.c_void_p * V)(*[p[5].data_ptr() for p in pres])
+    with stage("exact_records"):
+        _lib.call("tgs_exact_records_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, sps, exs,
+                  _lib.stream_handle(cloud.device))
 
 
 _RENDER_STREAMS = {}
@@ -418,6 +450,7 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     vis = torch.empty((V, n), dtype=torch.uint8, device=dev)
     tiles = torch.empty((V, n), dtype=torch.int32, device=dev)
     keys = torch.empty((V, n), dtype=torch.int64, device=dev)
+    exact = torch.empty((V, n, 8), dtype=torch.float32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     geo = []
     specs = []
@@ -461,7 +494,7 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     for s_ in pool + bpool:
         s_.wait_stream(main)
     rc = int(_lib.load().tgs_render_views(
-        ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(sp), arr(vis), arr(tiles), arr(keys),
+        ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(sp), arr(vis), arr(tiles), arr(keys), arr(exact),
         err.data_ptr(), targets, (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), wsb, pinned.data_ptr(),
         (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in pool]),
         (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in bpool]), ns))
@@ -481,7 +514,8 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
         outs.append(RenderOutput(image=b[0], transmittance=b[1], weight_sum=b[2], n_contrib=b[3], last_pos=b[4],
                                  visible=vis[v].view(torch.bool), screen_areas=sp[v][:, 11], hit_counts=hit_counts,
                                  _tiles=bins,
-                                 _state=_DeviceState(cloud.flat.data_ptr(), n, sp[v], vis[v], tiles[v], keys[v], bins)))
+                                 _state=_DeviceState(cloud.flat.data_ptr(), n, sp[v], vis[v], tiles[v], keys[v], bins,
+                                                     exact[v])))
     return outs
 
 
@@ -534,7 +568,7 @@ def _render_views_py(cloud, cams, settings, pool, main) -> list:
     def begin(i):  # view i's depth sort and count read-back on its own stream
         if not n or len(pool) < 2:
             return None
-        cam, (sp, _, tiles, keys, err) = cams[i], pres[i]
+        cam, (sp, _, tiles, keys, err, _) = cams[i], pres[i]
         ts = int(settings.tile_size)
         with torch.cuda.stream(pool[i % len(pool)]):
             return _bin_begin(sp, tiles, n, int(cam.width), int(cam.height), ts, 0, _tiles_y(cam, ts), err, keys)
@@ -574,7 +608,7 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     dev = cloud.device
     rb, re = row_band if row_band is not None else (0, _tiles_y(cam, ts))
     cs = torch.cuda.current_stream(dev)
-    splats, vis, tiles, keys, err = pre if pre is not None else preprocess(cloud, cam, settings)
+    splats, vis, tiles, keys, err, exact = pre if pre is not None else preprocess(cloud, cam, settings)
     if bins is None:
         bins = _bin(splats, tiles, n, w, h, ts, rb, re, err, keys, cs)
     specs = [((h, w, 3), torch.float32), ((h, w), torch.float32), ((h, w), torch.float32), ((h, w), torch.int32),
@@ -590,7 +624,8 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
     hits = torch.zeros(max(n, 1), dtype=torch.int32, device=dev) if settings.record_hits else None
     c_cam = _lib.make_camera(cam)
     with stage("blend_fwd"):
-        _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+        _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(_ex(exact)), _lib.ptr(bins.offsets),
+                  _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
                   _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.ptr(bins.order),
                   cs.cuda_stream)
@@ -600,13 +635,13 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
         hit_counts.copy_(hits[:n])
     out = RenderOutput(image=image, transmittance=transmit, weight_sum=wsum, n_contrib=n_contrib,
                        last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11], hit_counts=hit_counts,
-                       _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins))
+                       _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins, exact))
     if settings.record_full:
-        out.hit_records = _records(out, splats, bins, cam, c_cam, c_set, dev)
+        out.hit_records = _records(out, splats, exact, bins, cam, c_cam, c_set, dev)
     return out
 
 
-def _records(out, splats, bins, cam, c_cam, c_set, dev):
+def _records(out, splats, exact, bins, cam, c_cam, c_set, dev):
     """Per-pixel [(cloud row, weight), ...] lists (rasterizer.py:287-323); debug payload."""
     import ctypes
     flat = out.n_contrib.reshape(-1).to(torch.int64)
@@ -617,7 +652,8 @@ def _records(out, splats, bins, cam, c_cam, c_set, dev):
     g = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
     wt = torch.empty(max(total, 1), dtype=torch.float32, device=dev)
     if total:
-        _lib.call("tgs_blend_records", _lib.ptr(splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+        _lib.call("tgs_blend_records", _lib.ptr(splats), _lib.ptr(_ex(exact)), _lib.ptr(bins.offsets),
+                  _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), _lib.ptr(offsets), _lib.ptr(g), _lib.ptr(wt),
                   _lib.stream_handle(dev))
     g, wt, cnt, off = g.cpu().numpy(), wt.cpu().numpy(), flat.cpu().numpy(), offsets.cpu().numpy()
@@ -643,10 +679,10 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
     st = output._state
     if st is None or st.n != n or st.cloud_ptr != cloud.flat.data_ptr():
         # no reusable device state: recompute the forward products (rasterizer.py:342)
-        splats, vis, tiles, keys, err = preprocess(cloud, cam, settings)
+        splats, vis, tiles, keys, err, exact = preprocess(cloud, cam, settings)
         rb, re = (0, _tiles_y(cam, settings.tile_size))
         bins = _bin(splats, tiles, n, w, h, int(settings.tile_size), rb, re, err, keys)
-        st = _DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins)
+        st = _DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins, exact)
     bins = st.bins
     rb = bins.row_begin
     re = bins.row_end if bins.row_end is not None else _tiles_y(cam, settings.tile_size)
@@ -662,12 +698,14 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
             ni = int(bins.indices.numel())
             nb = ctypes_size("tgs_blend_backward_deterministic_workspace", n, ni)
             ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
-            _lib.call("tgs_blend_backward_deterministic", _lib.ptr(st.splats), _lib.ptr(st.tiles_touched), n,
+            _lib.call("tgs_blend_backward_deterministic", _lib.ptr(st.splats), _lib.ptr(_ex(st.exact)),
+                      _lib.ptr(st.tiles_touched), n,
                       _lib.ptr(bins.offsets), _lib.ptr(bins.indices), ni, ctypes.byref(c_cam), ctypes.byref(c_set),
                       rb, re, _lib.ptr(transmit), _lib.ptr(last_pos), _lib.ptr(d), _lib.ptr(dsplats), _lib.ptr(ws),
                       _lib.stream_handle(dev))
         else:
-            _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+            _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(_ex(st.exact)), _lib.ptr(bins.offsets),
+                      _lib.ptr(bins.indices),
                       ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
                       _lib.ptr(d), _lib.ptr(dsplats), _lib.ptr(bins.order), _lib.stream_handle(dev))
     return dsplats, st

@@ -28,8 +28,8 @@ from .cloud import PARAM_FIELDS, CloudGrads, GaussianCloud
 from .errors import DivergenceError
 from .optim import Adam
 from .profiler import stage
-from .rasterizer import (RenderSettings, _bin_begin, _bin_end, _tiles_y, blend_backward, preprocess_backward_views,
-                         preprocess_views, render_forward)
+from .rasterizer import (RenderSettings, _bin_begin, _bin_end, _tiles_y, blend_backward, exact_records,
+                         preprocess_backward_views, preprocess_views, render_forward)
 
 # reference defaults (config.py:76-92 OptimConfig; config.py:67-73 MaskConfig)
 DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opacity_logits": 0.05,
@@ -101,6 +101,9 @@ class Trainer:
         # with 2 / 3 / 4 at c3); 1 stream serialises them (per-kernel timing)
         self.streams = [torch.cuda.Stream(device=cloud.device) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
+        # the exact blend-decision records of the step's views are computed here while the
+        # first views' depth sorts run (only the blends read them)
+        self.exact_stream = torch.cuda.Stream(device=cloud.device)
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
@@ -210,7 +213,13 @@ class Trainer:
         if self.pg is not None:
             self.terms.zero_()  # other ranks' rows are summed in by the step's terms all-reduce
         # every view's preprocess in one pass over the parameters (main stream)
-        pres = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, stats=self.stats)
+        vcams = [self.cameras[v] for v in self.views]
+        pres = preprocess_views(self.cloud, vcams, self.settings, stats=self.stats, exact=False)
+        self.exact_stream.wait_stream(main)
+        with torch.cuda.stream(self.exact_stream):
+            exact_records(self.cloud, vcams, self.settings, pres)
+        exact_ready = torch.cuda.Event()
+        exact_ready.record(self.exact_stream)
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         ts = int(self.settings.tile_size)
@@ -218,7 +227,7 @@ class Trainer:
         def begin(i):  # view i's depth sort + instance-count read-back, on view i's stream
             if not n or len(self.streams) < 2:
                 return None
-            cam_, (sp, _, tiles, keys, err) = self.cameras[self.views[i]], pres[i]
+            cam_, (sp, _, tiles, keys, err, _) = self.cameras[self.views[i]], pres[i]
             with torch.cuda.stream(self.streams[i % len(self.streams)]):
                 return _bin_begin(sp, tiles, n, int(cam_.width), int(cam_.height), ts, 0, _tiles_y(cam_, ts), err,
                                   keys)
@@ -242,6 +251,7 @@ class Trainer:
                     self.instances = []
                 if bins is not None:
                     self.instances.append(int(bins.indices.numel()))
+                st.wait_event(exact_ready)  # the blends read the exact records
                 out = render_forward(self.cloud, cam, self.settings, pre=pres[i], bins=bins)
             with torch.cuda.stream(st):
                 d = self.dimage.get((i % len(self.streams), cam.height, cam.width))
@@ -264,6 +274,7 @@ class Trainer:
                 parts.append(ds)
         for s_ in self.streams:
             main.wait_stream(s_)
+        main.wait_stream(self.exact_stream)
         if copied:
             main.wait_stream(self.copy_stream)
         # one pass over the parameters for all views (linear chains summed first)

@@ -81,6 +81,23 @@ def grad_stats(got, ref):
             "entries_outside_1e-3rel_1e-5abs": int(bad.sum()), "entries": int(d.size)}
 
 
+def flip_rows(out, ref, cam, ts):
+    """Cloud rows blended by a pixel whose float32 transmittance crosses T = 1e-4 at another
+    entry than the float64 reference's (last_pos differs).  The extra or missing entry
+    changes the pixel's suffix colour S, and dL/dalpha of every earlier entry carries
+    S / (1 - alpha) (_kernels.py:157-168), so every row of the pixel's walk is affected:
+    the image moves by < 1e-4, the partials under an O(1) upstream gradient do not."""
+    lp, rl = _np(out.last_pos), ref["last_pos"]
+    ys, xs = np.nonzero(lp != rl)
+    off, ids = ref["offsets"], ref["ids"]
+    tx = -(-cam.width // ts)
+    rows = set()
+    for y, x in zip(ys, xs):
+        t = (y // ts) * tx + x // ts
+        rows.update(int(g) for g in ids[off[t]: off[t] + max(int(lp[y, x]), int(rl[y, x]))])
+    return np.array(sorted(rows), dtype=np.int64), int(ys.size)
+
+
 @pytest.mark.parametrize("view", [0, 5])
 def test_c3_preprocess_and_sort_bit_exact_vs_fp32_oracle(tgs, c3, view):
     sc, st, cloud = c3
@@ -142,15 +159,24 @@ def test_c3_gradients_vs_fp64_oracle(tgs, c3, upstream):
     for f in FIELDS:
         got, r = _np(getattr(g, f)).astype(np.float64), ref[f]
         stats[f] = grad_stats(got, r)
+    # T = 1e-4 termination is decided in float32: a pixel whose transmittance crosses 1e-4
+    # one entry earlier or later than in float64 (a handful per view, out.last_pos) blends
+    # one entry more or less.  Its image moves by < 1e-4, but under an O(1) upstream
+    # gradient the Gaussians between the two stopping positions see a different partial.
+    flipped = flip_rows(out, fwd64(sc, st, 0), cam, st.tile_size)
+    stats["T_flip_pixels"], stats["T_flip_rows"] = flipped[1], int(flipped[0].size)
     report(f"c3_view0_grads_{upstream}", stats)
+    keep = np.ones(len(cloud), dtype=bool)
+    keep[flipped[0]] = False
     for f in FIELDS:
         got, r = _np(getattr(g, f)).astype(np.float64), ref[f]
-        if upstream == "l1_ssim":
+        assert stats[f]["rel_l2"] < (1e-3 if upstream == "l1_ssim" else 1e-4), (f, stats[f])
+        if upstream == "l1_ssim":  # every entry, the plain north-star bar
             np.testing.assert_allclose(got, r, rtol=1e-3, atol=1e-5, err_msg=f)
-            assert stats[f]["rel_l2"] < 1e-3, (f, stats[f])
-        else:
-            assert stats[f]["rel_l2"] < 1e-4, (f, stats[f])
-            np.testing.assert_allclose(got, r, rtol=1e-3, atol=1e-5 * max(1.0, stats[f]["max_abs_ref"]), err_msg=f)
+        else:  # O(1) upstream: every row outside the T-flip rows, a scaled floor (float32 sums)
+            np.testing.assert_allclose(got[keep], r[keep], rtol=1e-3, atol=1e-5 * max(1.0, stats[f]["max_abs_ref"]),
+                                       err_msg=f)
+    assert flipped[1] < 1e-4 * out.last_pos.numel()  # T-flip pixels (measured: 129 of 2,073,600)
 
 
 def test_c3_trainer_batch_gradient_vs_sum_of_fp64_views(tgs, c3):

@@ -42,6 +42,13 @@ def _np(t):
 
 
 def _grad_close(got, ref, name):
+    """Gradients under an O(1) upstream gradient (the golden fixtures and c1 use N(0, 1), as
+    the reference's own tests do): 1e-3 relative, and an absolute floor of 1e-5 times the
+    field's largest entry.  Such a gradient is a float32 sum of O(1)..O(10) per-pixel terms
+    that can cancel to ~1e-3, where float32 reassociation alone moves it by ~1e-5 (measured:
+    1 entry in 1,200 at masked72x40 and deg1_norest, |err| 1.2e-5 / 2.5e-5).  The plain
+    1e-3 / 1e-5 bar holds for every entry under the training loss's own upstream gradient
+    at c3 (tests/test_gpu_c3_parity.py::test_c3_gradients_vs_fp64_oracle[l1_ssim])."""
     atol = 1e-5 * max(1.0, float(np.abs(ref).max()) if ref.size else 1.0)
     np.testing.assert_allclose(got, ref, rtol=1e-3, atol=atol, err_msg=name)
 
@@ -124,13 +131,13 @@ def test_c2_image_vs_fp64_oracle(tgs):
     out = tgs.render_forward(tgs.GaussianCloud.from_fields(sc.fields), sc.cameras[0], st)
     ref = oracle.render_forward(sc.fields, sc.cameras[0], st, "f64")
     assert np.array_equal(_np(out.visible), ref["visible"])
-    err = np.abs(_np(out.image) - ref["image"])
-    # float32 vs float64 can flip a blend decision exactly at a threshold (alpha 1/255,
-    # e = -4.5, T = 1e-4); such pixels must be rare and bounded by one contribution
-    bad = err.max(axis=2) > 1e-4
-    # measured with the fp32 oracle: 57 of 921,600 pixels, max 5.1e-3 (one flipped decision)
-    assert bad.mean() < 2e-4, f"{bad.sum()} pixels above 1e-4 (max {err.max():.3e})"
-    assert err.max() < 2e-2
+    # the blend decisions at alpha = 1/255 and e = -4.5 are the float64 ones (exact
+    # blend-decision records), so every pixel is within the north-star 1e-4 (a float32
+    # decision flips 57 of 921,600 pixels here by up to 5.1e-3)
+    for got, want in ((out.image, ref["image"]), (out.transmittance, ref["transmittance"]),
+                      (out.weight_sum, ref["weight_sum"])):
+        err = np.abs(_np(got) - want)
+        assert err.max() <= 1e-4, f"max err {err.max():.3e}, {(err > 1e-4).sum()} entries above 1e-4"
     np.testing.assert_allclose(_np(out.weight_sum) + _np(out.transmittance), 1.0, atol=1e-5)
 
 
@@ -146,11 +153,18 @@ def test_c1_gradients_vs_fp64_oracle_full(tgs):
     g = tgs.render_backward(cloud, cam, st, torch.from_numpy(dimg).cuda(), out)
     ref_f = oracle.render_forward(sc.fields, cam, st, "f64")
     ref_g = oracle.render_backward(sc.fields, cam, st, dimg.astype(np.float64), ref_f, "f64")
+    # rows between the two stopping positions of a pixel whose transmittance crosses
+    # T = 1e-4 one entry apart in float32 and float64 (see test_gpu_c3_parity.flip_rows)
+    from test_gpu_c3_parity import flip_rows
+    flipped, npix = flip_rows(out, ref_f, cam, st.tile_size)
+    keep = np.ones(len(cloud), dtype=bool)
+    keep[flipped] = False
+    assert npix <= 1e-4 * out.last_pos.numel() + 5, (npix, flipped.size)
     for f in GRAD_FIELDS:
         got, ref = _np(getattr(g, f)), ref_g[f]
         rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
         assert rel < 1e-4, (f, rel)
-        _grad_close(got, ref, f)
+        _grad_close(got[keep], ref[keep], f)
 
 
 def test_hits_and_records_vs_reference(tgs):
@@ -421,7 +435,7 @@ def test_render_sharded_single_rank_nccl(tgs):
         ref = tgs.render_forward(cloud, sc.cameras[0], st).image
         assert torch.equal(img, ref)
         from paper_2501_14534_b200 import rasterizer
-        splats, _, tiles, _, _ = rasterizer.preprocess(cloud, sc.cameras[0], st)
+        splats, _, tiles, _, _, _ = rasterizer.preprocess(cloud, sc.cameras[0], st)
         counts = parallel.row_histogram(splats, tiles, len(cloud), sc.cameras[0], 16)
         out = tgs.render_forward(cloud, sc.cameras[0], st)
         per_tile = np.diff(_np(out._tiles.offsets)).reshape(-1, out._tiles.tiles_x).sum(axis=1)
@@ -598,7 +612,7 @@ def test_multiview_preprocess_bitwise_equals_single_view(tgs):
         many = preprocess_views(cloud, cams, st)
         for cam, got in zip(cams, many):
             want = preprocess(cloud, cam, st)
-            for a, b in zip(got[:4], want[:4]):
+            for a, b in zip(got[:4] + got[5:], want[:4] + want[5:]):
                 assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a,
                                    b.view(torch.int32) if b.dtype == torch.float32 else b)
 
@@ -782,7 +796,8 @@ def test_tile_order_is_a_heaviest_first_permutation_and_changes_nothing(tgs):
             torch.empty((h, w), device="cuda"), torch.empty((h, w), dtype=torch.int32, device="cuda"),
             torch.empty((h, w), dtype=torch.int32, device="cuda")]
     c_cam, c_set = _lib.make_camera(cam), _lib.make_settings(st)
-    _lib.call("tgs_blend_forward", _lib.ptr(out._state.splats), _lib.ptr(bins.offsets), _lib.ptr(bins.indices),
+    _lib.call("tgs_blend_forward", _lib.ptr(out._state.splats), _lib.ptr(out._state.exact), _lib.ptr(bins.offsets),
+              _lib.ptr(bins.indices),
               ctypes.byref(c_cam), ctypes.byref(c_set), 0, bins.tiles_y, *[_lib.ptr(b) for b in bufs], None, None,
               _lib.stream_handle())
     for got, ref in zip(bufs, (out.image, out.transmittance, out.weight_sum, out.n_contrib, out.last_pos)):
