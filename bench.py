@@ -52,6 +52,11 @@ def parse():
                    help="c3: training step (default, the metric's config); c4: 3M-Gaussian 4K render orbit; "
                         "c5: progressive-schedule sweep (2000 steps with pruning)")
     p.add_argument("--c5-steps", type=int, default=2000, help="c5: schedule length")
+    p.add_argument("--rank-share", type=int, default=0,
+                   help="N > 1: time rank 0's share of an N-GPU ZeRO-1 step on this one GPU and print a projected "
+                        "N-GPU step (measured share + an NCCL reduce-scatter/all-gather bandwidth model)")
+    p.add_argument("--nvlink-gbs", type=float, default=720.0,
+                   help="--rank-share model: NCCL reduce-scatter / all-gather bus bandwidth per GPU, GB/s")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -346,6 +351,8 @@ def main():
         return schedule_c5(args)
     if args.impl == "reference":
         return reference_arm(args)
+    if args.rank_share > 1:
+        return rank_share(args)
     import torch
     import torch.distributed as dist
 
@@ -516,6 +523,69 @@ def main():
         dist.destroy_process_group()
 
 
+def rank_share(args):
+    """Projection of the N-GPU c3 step from ONE GPU (only one GPU is available to this
+    build): rank 0's share of an N-rank ZeRO-1 step — its views (0, N, 2N, ...), the
+    multi-view preprocess forward / backward of those views and the fused Adam on its 1/N
+    parameter shard (train.Trainer(zero_sim=(0, N))) — timed exactly like the bench's
+    fixed-workload step, plus the reduce-scatter and all-gather of the 252 B/Gaussian
+    parameter buffer at an assumed NCCL bus bandwidth (--nvlink-gbs), NOT overlapped with
+    compute (the real step overlaps chunk k's all-gather with chunk k+1's Adam)."""
+    import torch
+
+    from paper_2501_14534_b200 import GaussianCloud, RenderSettings, _lib, scenes
+    from paper_2501_14534_b200.train import Trainer
+    N = args.rank_share
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    _lib.load()
+    sc = scenes.config3(n=args.n)
+    st = RenderSettings(**settings_kwargs())
+    cloud = GaussianCloud.from_fields(sc.fields, device=dev)
+    views = list(range(0, VIEWS, N))
+    targets = [None] * VIEWS
+    for v in views:
+        targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
+    out = {}
+    for label, kw in (("share", dict(views=views, zero_sim=(0, N))), ("full", dict(views=list(range(VIEWS))))):
+        if label == "full":
+            for v in range(VIEWS):
+                targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
+        tr = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, **kw)
+        init = (cloud.flat.clone(), tr.opt.m.clone(), tr.opt.v.clone(), dict(tr.opt.steps))
+        for _ in range(args.warmup):
+            tr.step()
+        total = 0.0
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(args.steps):
+            cloud.flat.copy_(init[0])
+            tr.opt.m.copy_(init[1])
+            tr.opt.v.copy_(init[2])
+            tr.opt.steps = dict(init[3])
+            torch.cuda.synchronize()
+            s.record()
+            tr.step()
+            e.record()
+            e.synchronize()
+            total += s.elapsed_time(e)
+        tr.check_divergence()
+        cloud.flat.copy_(init[0])
+        out[label] = total / args.steps
+    from paper_2501_14534_b200.cloud import params_end
+    pbytes = params_end(cloud._layout_map) * 4
+    comm_ms = 2 * (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
+    proj = out["share"] + comm_ms
+    print(json.dumps({"metric": f"projected c3 train step/s at {N} GPUs (1-GPU rank-share measurement + NCCL model)",
+                      "value": round(1e3 / proj, 3), "unit": "train step/s", "n_gpus": 1, "projected_n_gpus": N,
+                      "ms_per_step_projected": round(proj, 3), "ms_rank_share_measured": round(out["share"], 3),
+                      "ms_comm_model": round(comm_ms, 3), "ms_per_step_1gpu_measured": round(out["full"], 3),
+                      "projected_speedup": round(out["full"] / proj, 3), "views_on_rank0": views,
+                      "comm_model": f"reduce-scatter + all-gather of {pbytes} B (parameter floats) at "
+                                    f"{args.nvlink_gbs} GB/s NCCL bus bandwidth, not overlapped",
+                      "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded BASELINE.json config 3)",
+                      "config": config_dict(len(cloud), N)}), flush=True)
+
+
 def schedule_c5(args):
     """BASELINE.json configs[4]: the progressive-training schedule on 1M Gaussians — render
     resolution stepped 1/8 -> 1/4 -> 1/2 -> 1 of 1920x1080 (targets area-resized on the GPU),
@@ -623,8 +693,11 @@ def schedule_c5(args):
 
 def render_c4(args):
     """BASELINE.json configs[3]: 3M Gaussians in 64 anisotropic clusters (radius 10), 3840x2160,
-    render-only over the 200-frame orbit; tile rows sharded across ranks (parallel.render_sharded:
-    replicated preprocess, balanced bands from the replicated row histogram, one all-gather)."""
+    render-only: the WHOLE 200-frame orbit is timed (after two untimed passes over its
+    first 16 frames).  One GPU: batches of 8 frames through render_views (one preprocess pass
+    per batch, binning + blending pipelined over three streams).  N ranks: tile rows sharded
+    (parallel.ShardedRenderer: replicated preprocess, bands from the previous batch's
+    replicated row histogram, the band rows of a batch gathered to rank 0 in one call)."""
     import torch
     import torch.distributed as dist
 
@@ -644,29 +717,27 @@ def render_c4(args):
     cloud = GaussianCloud.from_fields(sc.fields, device=dev)
     st = RenderSettings(near=0.2, tile_size=16)
     frames = sc.cameras
+    renderer = parallel.ShardedRenderer(cloud, st) if world > 1 else None
 
-    def frames_from(k0, count):
-        """Frames k0 .. k0+count-1 of the orbit.  N > 1: each frame tile-row sharded.
-        One GPU: batches of up to 8 frames through render_views (one preprocess pass
-        per batch, binning + blending pipelined over three streams)."""
+    def orbit(k0, count):
         cams = [frames[(k0 + j) % len(frames)] for j in range(count)]
-        if world > 1:
-            return [parallel.render_sharded(cloud, cam, st) for cam in cams]
-        out = []
         for b in range(0, count, 8):
-            out += [o.image for o in render_views(cloud, cams[b:b + 8], st)]
-        return out
+            if renderer is not None:
+                renderer.render(cams[b:b + 8])
+            else:
+                render_views(cloud, cams[b:b + 8], st)
 
-    # at least two whole batches of 8 frames untimed: the first learns the instance counts
-    # (Python pipeline), the second allocates the native batch path's buffers
-    frames_from(0, args.warmup if world > 1 else max(args.warmup, 16))
+    # untimed: the first batch learns the instance counts (Python pipeline), the second
+    # allocates the native batch path's buffers
+    orbit(0, 16)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    count = len(frames)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         s.record()
-        frames_from(args.warmup, args.steps)
+        orbit(0, count)
         e.record()
         torch.cuda.synchronize()
     if world > 1:
@@ -674,15 +745,15 @@ def render_c4(args):
     t = torch.tensor([s.elapsed_time(e) / 1e3], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    fps = args.steps / float(t)
+    fps = count / float(t)
     if rank == 0:
         print(json.dumps({"metric": "render FPS at 3M Gaussians 3840x2160 (c4 orbit)", "value": round(fps, 3),
-                          "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                          "ms_per_step": round(float(t) / args.steps * 1e3, 3), "higher_is_better": True,
+                          "unit": "frames/s", "n_gpus": world, "steps": count, "warmup": 16,
+                          "ms_per_step": round(float(t) / count * 1e3, 3), "higher_is_better": True,
                           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                           "data": "synthetic (seeded BASELINE.json config 4 generator)",
-                          "config": {"workload": "c4: BASELINE.json configs[3] render-only", "gaussians": n,
-                                     "resolution": "3840x2160", "frames": len(frames),
+                          "config": {"workload": "c4: BASELINE.json configs[3] render-only, the full orbit timed",
+                                     "gaussians": n, "resolution": "3840x2160", "frames": len(frames),
                                      "parallelism": f"tile-row sharding x{world}" if world > 1 else "single GPU"},
                           "clocks": clk.summary()}), flush=True)
     if world > 1:

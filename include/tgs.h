@@ -335,14 +335,17 @@ TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, i
  * group's gradient before the update (written back to grad).
  * Divergence guard (training.py:298-308): with n_terms > 0, if any of the
  * n_terms doubles at loss_terms (device) is not finite, NOTHING is updated and
- * *nonfinite_flag (device int32, may be NULL) is set to 1; the host raises
- * DivergenceError from it. */
+ * *nonfinite_flag (device int32, may be NULL) is written 1 (else 0); the host
+ * raises DivergenceError from it.  Only the floats in [range_begin, range_end)
+ * (multiples of 4) are updated — a rank's shard under ZeRO-1 data parallelism;
+ * [0, INT64_MAX) for all. */
 TGS_API int tgs_adam_step_groups(float *param, float *grad, float *m, float *v, int32_t ngroups,
                                  const int64_t *offsets, const int64_t *sizes, const float *lrs,
                                  const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
                                  float beta2, float eps, float lambda_m, float lambda_sh,
                                  const float *band_weights, int64_t n_gaussians, const double *loss_terms,
-                                 int32_t n_terms, int32_t *nonfinite_flag, tgs_stream_t stream);
+                                 int32_t n_terms, int32_t *nonfinite_flag, int64_t range_begin,
+                                 int64_t range_end, tgs_stream_t stream);
 
 /* ---- target-side progressive ops (images.py:58-102), (H, W, 3) float32.
  * area_resize: exact fractional box filter (downsampling only); workspace
@@ -405,6 +408,10 @@ typedef struct {
   float *image, *transmit, *weight_sum;
   int32_t *n_contrib, *last_pos, *hits; /* hits may be NULL (zeroed by the caller otherwise) */
   int64_t num_instances;     /* out */
+  /* tile rows [row_begin, row_end) of the view (tile-row sharding: only these rows are
+   * binned and blended, tile_offsets then has (row_end - row_begin) * tiles_x + 1
+   * entries); row_end <= 0 = the whole view */
+  int32_t row_begin, row_end;
 } tgs_view_target;
 
 TGS_API int tgs_render_views_workspace(int64_t n, int64_t max_instances, int32_t width, int32_t height,

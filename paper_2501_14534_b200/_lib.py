@@ -54,7 +54,7 @@ class TgsDensifyStats(ctypes.Structure):
 class TgsViewTarget(ctypes.Structure):
     _fields_ = [("tile_offsets", _P), ("sorted_ids", _P), ("ids_capacity", _I64), ("tile_order", _P),
                 ("image", _P), ("transmit", _P), ("weight_sum", _P), ("n_contrib", _P), ("last_pos", _P),
-                ("hits", _P), ("num_instances", _I64)]
+                ("hits", _P), ("num_instances", _I64), ("row_begin", _I32), ("row_end", _I32)]
 
 
 class TgsGrads(ctypes.Structure):
@@ -89,7 +89,7 @@ _SIGS = {
     "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
     "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),
     "tgs_adam_step_groups": ([_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _P, _I64, _P, _I32,
-                              _P, _P], _I32),
+                              _P, _I64, _I64, _P], _I32),
     "tgs_gather_rows": ([_P, _P, _P, _I64, _I32, _P], _I32),
     "tgs_select_rows_workspace": ([_I64, _P], _I32),
     "tgs_select_rows": ([_P, _P, _F, _I64, _P, _P, _P, _SZ, _P], _I32),

@@ -23,14 +23,32 @@ _ROW = {"positions": (3,), "log_scales": (3,), "rotations": (4,), "opacity_logit
 PARAM_FLOATS = sum(int(np.prod(_ROW[f])) for f in PARAM_FIELDS)  # 63
 
 
+# Floats of headroom after the parameter fields (in both the parameter and the gradient
+# layouts): a ZeRO-1 chunk is padded to a multiple of world x 64 floats, and its padded
+# tail may run past the last parameter field (parallel.zero_plan, world <= 64).
+ZERO_PAD = 4096
+
+
 def _layout(fields, n):
-    """Offsets (in floats) of each field inside the flat buffer, 64-float aligned."""
-    off, out = 0, {}
+    """Offsets (in floats) of each field inside the flat buffer, 64-float aligned, with
+    ZERO_PAD floats between the parameter fields and anything after them."""
+    off, out, padded = 0, {}, False
     for f in fields:
+        if f not in PARAM_FIELDS and not padded:
+            off += ZERO_PAD
+            padded = True
         size = n * int(np.prod(_ROW[f]))
         out[f] = (off, size)
         off += (size + 63) // 64 * 64
+    if not padded:
+        off += ZERO_PAD
     return out, max(off, 64)
+
+
+def params_end(layout: dict) -> int:
+    """First float after the parameter fields (64-aligned)."""
+    o, n = layout["sh_mask_logits"]
+    return o + (n + 63) // 64 * 64
 
 
 class _FlatFields:

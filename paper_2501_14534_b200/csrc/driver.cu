@@ -105,13 +105,17 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
   }
 
   const int ts = s->tile_size;
-  auto rows_of = [&](int v) { return (cams[v].height + ts - 1) / ts; };
+  // the view's tile-row band (tile-row sharding), the whole view by default
+  auto rb_of = [&](int v) { return targets[v].row_end > 0 ? targets[v].row_begin : 0; };
+  auto rows_of = [&](int v) {
+    return targets[v].row_end > 0 ? targets[v].row_end : (cams[v].height + ts - 1) / ts;
+  };
   // 2a. depth sort of view v + asynchronous read of its instance count
   auto begin = [&](int v) -> int {
     const int k = v % nstreams;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(streams[k]);
     int r = tgs_bin_gaussians(splats[v], tiles_touched[v], depth_keys ? depth_keys[v] : nullptr, n, cams[v].width,
-                              cams[v].height, ts, 0, rows_of(v), slot[k].ws_g, slot[k].counts, error_flag,
+                              cams[v].height, ts, rb_of(v), rows_of(v), slot[k].ws_g, slot[k].counts, error_flag,
                               streams[k]);
     if (r != TGS_OK) return r;
     if (cudaMemcpyAsync(pinned_counts + 2 * k, slot[k].counts, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -127,10 +131,10 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
     tgs_view_target &t = targets[v];
     t.num_instances = count;
     size_t need = 0;
-    int r = tgs_bin_instances_workspace(n, count, cams[v].width, cams[v].height, ts, 0, rows_of(v), &need);
+    int r = tgs_bin_instances_workspace(n, count, cams[v].width, cams[v].height, ts, rb_of(v), rows_of(v), &need);
     if (r != TGS_OK) return r;
     if (count > t.ids_capacity || need > slot[k].ws_i_bytes) return TGS_ERR_CAPACITY;
-    return tgs_bin_instances(splats[v], n, cams[v].width, cams[v].height, ts, 0, rows_of(v), slot[k].ws_g, count,
+    return tgs_bin_instances(splats[v], n, cams[v].width, cams[v].height, ts, rb_of(v), rows_of(v), slot[k].ws_g, count,
                              slot[k].ws_i, t.tile_offsets, t.sorted_ids, streams[k]);
   };
   // 2c. blend view v (on its blend stream when one is given: the binning streams then
@@ -145,7 +149,7 @@ extern "C" int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, 
       bs = blend_streams[k];
     }
     if (ev_ex) cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(bs), ev_ex, 0);
-    return tgs_blend_forward(splats[v], exact ? exact[v] : nullptr, t.tile_offsets, t.sorted_ids, &cams[v], s, 0, rows_of(v), t.image, t.transmit,
+    return tgs_blend_forward(splats[v], exact ? exact[v] : nullptr, t.tile_offsets, t.sorted_ids, &cams[v], s, rb_of(v), rows_of(v), t.image, t.transmit,
                              t.weight_sum, t.n_contrib, t.last_pos, t.hits, t.tile_order, bs);
   };
   // Per stream k the queue is  bin_instances(v) -> bin_gaussians(v + nstreams) -> blend(v):

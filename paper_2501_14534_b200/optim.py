@@ -40,7 +40,7 @@ class Adam:
                   1.0 - self.beta1 ** t, 1.0 - self.beta2 ** t, _lib.stream_handle(cloud.device))
 
     def step(self, cloud: GaussianCloud, grads, names=PARAM_FIELDS, lambda_m: float = 0.0,
-             lambda_sh: float = 0.0, guard=None) -> None:
+             lambda_sh: float = 0.0, guard=None, ranges=None, count: bool = True) -> None:
         """Update the groups `names` in ONE fused launch (tgs_adam_step_groups).  lambda_m /
         lambda_sh add the mask penalties of total_loss (masking.py:60-67) to the
         mask-logit gradients first (when those groups are among `names`).
@@ -48,7 +48,11 @@ class Adam:
         guard: optional (terms, flag) device tensors — float64 loss terms and an int32
         flag: if any term is not finite the launch updates nothing and sets the flag
         (the reference raises DivergenceError before its update, training.py:298-308).
-        The host-side step counters are still advanced; the caller rolls them back."""
+        The host-side step counters are still advanced; the caller rolls them back.
+
+        ranges: optional [(begin, end), ...] flat-buffer float ranges to update (a rank's
+        ZeRO-1 shard; one launch per range); count=False leaves the step counters as they
+        are (the further launches of one logical step)."""
         import ctypes
         from .loss import SH_BAND_WEIGHTS
         names = sorted(set(names), key=lambda f: cloud.field_range(f)[0])  # layout order
@@ -61,7 +65,8 @@ class Adam:
             goff, _ = grads.field_range(f)
             if goff != off:
                 raise ValueError("gradient and parameter layouts differ")
-            self.steps[f] += 1
+            if count:
+                self.steps[f] += 1
             t = self.steps[f]
             offs.append(off)
             sizes.append(size)
@@ -70,14 +75,16 @@ class Adam:
             b2s.append(1.0 - self.beta2 ** t)
             kinds.append(1 if (f == "mask_logits" and lambda_m) else (2 if (f == "sh_mask_logits" and lambda_sh) else 0))
         arr = lambda ct, xs: (ct * k)(*xs)  # noqa: E731
-        _lib.call("tgs_adam_step_groups", _lib.ptr(cloud.flat), _lib.ptr(grads.flat), _lib.ptr(self.m),
-                  _lib.ptr(self.v), k, arr(ctypes.c_int64, offs), arr(ctypes.c_int64, sizes),
-                  arr(ctypes.c_float, lrs), arr(ctypes.c_float, b1s), arr(ctypes.c_float, b2s),
-                  arr(ctypes.c_int32, kinds), self.beta1, self.beta2, self.eps, float(lambda_m), float(lambda_sh),
-                  (ctypes.c_float * 3)(*SH_BAND_WEIGHTS), len(cloud),
-                  _lib.ptr(guard[0]) if guard is not None else None,
-                  int(guard[0].numel()) if guard is not None else 0,
-                  _lib.ptr(guard[1]) if guard is not None else None, _lib.stream_handle(cloud.device))
+        args = (k, arr(ctypes.c_int64, offs), arr(ctypes.c_int64, sizes), arr(ctypes.c_float, lrs),
+                arr(ctypes.c_float, b1s), arr(ctypes.c_float, b2s), arr(ctypes.c_int32, kinds), self.beta1,
+                self.beta2, self.eps, float(lambda_m), float(lambda_sh), (ctypes.c_float * 3)(*SH_BAND_WEIGHTS),
+                len(cloud), _lib.ptr(guard[0]) if guard is not None else None,
+                int(guard[0].numel()) if guard is not None else 0, _lib.ptr(guard[1]) if guard is not None else None)
+        for r0, r1 in (ranges if ranges is not None else [(0, (1 << 62))]):
+            if r1 <= r0:
+                continue
+            _lib.call("tgs_adam_step_groups", _lib.ptr(cloud.flat), _lib.ptr(grads.flat), _lib.ptr(self.m),
+                      _lib.ptr(self.v), *args, int(r0), int(r1), _lib.stream_handle(cloud.device))
 
 
 def exponential_lr(step: int, lr_init: float, lr_final: float, max_steps: int) -> float:

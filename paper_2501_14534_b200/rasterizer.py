@@ -437,7 +437,7 @@ def _alloc_many(specs, dev) -> list:
 _RV_CAP: dict = {}  # (device, n, tile, resolutions) -> per-view instance-id capacity of the native path
 
 
-def _render_views_native(cloud, cams, settings, pool, main, cap: int):
+def _render_views_native(cloud, cams, settings, pool, main, cap: int, bands=None):
     """tgs_render_views: the whole batch issued from C++ (see include/tgs.h).  Returns the
     outputs, or the largest instance count of the batch when a buffer was too small."""
     import ctypes
@@ -470,11 +470,12 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
         b = bufs[per * v: per * (v + 1)]
         if settings.record_hits:
             b[7].zero_()
-        order = _blend_order(None, tx * ty, tx, ty, ts, dev, None) if BLEND_ORDER == "center" else None
+        rb, re = bands[v] if bands is not None else (0, ty)
+        order = _blend_order(None, (re - rb) * tx, tx, re - rb, ts, dev, None) if BLEND_ORDER == "center" else None
         orders.append(order)
         targets[v] = _lib.TgsViewTarget(b[5].data_ptr(), b[6].data_ptr(), cap, _lib.ptr(order), b[0].data_ptr(),
                                         b[1].data_ptr(), b[2].data_ptr(), b[3].data_ptr(), b[4].data_ptr(),
-                                        b[7].data_ptr() if settings.record_hits else None, -1)
+                                        b[7].data_ptr() if settings.record_hits else None, -1, rb, re)
     ns = len(pool)
     wsb = max(ctypes_size("tgs_render_views_workspace", n, cap, w, h, ts) for h, w, _, _ in geo)
     wss = [_scratch("render_views", wsb, dev, s_.cuda_stream, owner=s_) for s_ in pool]
@@ -509,7 +510,8 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     for v, (h, w, tx, ty) in enumerate(geo):
         b = bufs[per * v: per * (v + 1)]
         count = int(targets[v].num_instances)
-        bins = TileBins(b[5], b[6][:count], tx, ty, 0, ty, orders[v])
+        rb, re = bands[v] if bands is not None else (0, ty)
+        bins = TileBins(b[5][: (re - rb) * tx + 1], b[6][:count], tx, ty, rb, re, orders[v])
         hit_counts = b[7].to(torch.int64) if settings.record_hits else None
         outs.append(RenderOutput(image=b[0], transmittance=b[1], weight_sum=b[2], n_contrib=b[3], last_pos=b[4],
                                  visible=vis[v].view(torch.bool), screen_areas=sp[v][:, 11], hit_counts=hit_counts,
@@ -519,13 +521,15 @@ def _render_views_native(cloud, cams, settings, pool, main, cap: int):
     return outs
 
 
-def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) -> list:
+def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3, row_bands: list | None = None) -> list:
     """Render a batch of views of one cloud (an orbit, the views of a training batch):
     every view's preprocess in ONE pass over the parameters (tgs_preprocess_forward_views),
     then per view binning + blending pipelined over `streams` CUDA streams, so the
     latency-bound binning of one view (and its instance-count read-back) overlaps the
     blending of the others.  Element v equals render_forward(cloud, cams[v], settings);
-    the outputs are ordered before later work on the caller's current stream."""
+    the outputs are ordered before later work on the caller's current stream.
+    row_bands: optional [(row_begin, row_end), ...] tile-row band per view (tile-row
+    sharding): only those rows are binned and blended (the other pixels are unspecified)."""
     cloud = _as_cloud(cloud)
     cams = list(cams)
     if not cams:
@@ -545,17 +549,17 @@ def render_views(cloud, cams: list, settings: RenderSettings, streams: int = 3) 
     native = len(cloud) > 0 and not settings.record_full and len(cams) <= 64
     if native and geom in _RV_CAP:
         for _ in range(3):
-            res = _render_views_native(cloud, cams, settings, pool, main, _RV_CAP[geom])
+            res = _render_views_native(cloud, cams, settings, pool, main, _RV_CAP[geom], row_bands)
             if isinstance(res, list):
                 return res
             _RV_CAP[geom] = _size_class(int(res * 1.25) + 1024)
-    outs = _render_views_py(cloud, cams, settings, pool, main)
+    outs = _render_views_py(cloud, cams, settings, pool, main, row_bands)
     if native:
         _RV_CAP[geom] = _size_class(int(max(o._tiles.indices.numel() for o in outs) * 1.25) + 1024)
     return outs
 
 
-def _render_views_py(cloud, cams, settings, pool, main) -> list:
+def _render_views_py(cloud, cams, settings, pool, main, row_bands=None) -> list:
     """render_views driven from Python (first batch of a geometry, record_full)."""
     dev = cloud.device
     pres = preprocess_views(cloud, cams, settings) if len(cloud) else [None] * len(cams)
@@ -570,8 +574,9 @@ def _render_views_py(cloud, cams, settings, pool, main) -> list:
             return None
         cam, (sp, _, tiles, keys, err, _) = cams[i], pres[i]
         ts = int(settings.tile_size)
+        rb, re = row_bands[i] if row_bands is not None else (0, _tiles_y(cam, ts))
         with torch.cuda.stream(pool[i % len(pool)]):
-            return _bin_begin(sp, tiles, n, int(cam.width), int(cam.height), ts, 0, _tiles_y(cam, ts), err, keys)
+            return _bin_begin(sp, tiles, n, int(cam.width), int(cam.height), ts, rb, re, err, keys)
 
     try:
         # the next len(pool) - 1 views' binnings are queued (each on its own stream) before
@@ -584,7 +589,8 @@ def _render_views_py(cloud, cams, settings, pool, main) -> list:
             p_i = pend.pop(0)
             with torch.cuda.stream(pool[i % len(pool)]):
                 bins = _bin_end(p_i) if p_i is not None else None
-                outs.append(render_forward(cloud, cam, settings, pre=pres[i], bins=bins))
+                outs.append(render_forward(cloud, cam, settings, pre=pres[i], bins=bins,
+                                           row_band=row_bands[i] if row_bands is not None else None))
     finally:
         _ALLOC.stream = None
         for s_ in pool:

@@ -78,7 +78,8 @@ class DensifyStats:
 class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
-                 views=None, streams: int = 4, deterministic: bool = False, densify_stats: bool = False):
+                 views=None, streams: int = 4, deterministic: bool = False, densify_stats: bool = False,
+                 dp_mode: str = "zero", zero_chunks: int = 4, zero_sim: tuple | None = None):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -87,6 +88,13 @@ class Trainer:
         self.lambda_ssim = lambda_ssim
         self.lambda_m, self.lambda_sh = lambda_m, lambda_sh
         self.pg = process_group
+        # data parallelism (process_group given): "zero" = ZeRO-1 (reduce-scatter, Adam on this
+        # rank's shard, all-gather; parallel.zero_plan), "allreduce" = bucketed all-reduce +
+        # replicated Adam.  zero_sim=(rank, world): one GPU runs rank `rank`'s share of a
+        # world-rank step without communication (bench.py --rank-share projections).
+        if dp_mode not in ("zero", "allreduce"):
+            raise ValueError("dp_mode must be 'zero' or 'allreduce'")
+        self.dp_mode, self.zero_chunks, self.zero_sim = dp_mode, int(zero_chunks), zero_sim
         self.rank = 0
         if process_group is not None:
             import torch.distributed as dist
@@ -149,6 +157,7 @@ class Trainer:
         from . import pruning
         if new is self.cloud:
             return
+        self._zero_sync_moments()
         pruning.compact_adam(self.opt, self.cloud, new, keep)
         self.cloud = new
         self.grads = CloudGrads(len(new), new.device)
@@ -289,6 +298,8 @@ class Trainer:
         upd = set(PARAM_FIELDS)
         if not (self.settings.compute_sh_rest_grads and self.settings.active_sh_degree > 0):
             upd.discard("sh_rest")
+        if self.zero_sim is not None or (self.pg is not None and self.dp_mode == "zero"):
+            return self._zero_update(main, g, upd, guard, steps_before, n, res)
         if self.pg is None:
             with stage("adam"):
                 # the mask penalties of total_loss (masking.py:60-67) enter the gradient inside
@@ -323,6 +334,65 @@ class Trainer:
                     self.opt.step(self.cloud, g, names=names, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh,
                                   guard=guard)
         return self._finish(main, steps_before, n, res)
+
+    def _zero_world(self):
+        if self.pg is not None:
+            import torch.distributed as dist
+            return self.rank, dist.get_world_size(self.pg)
+        return self.zero_sim
+
+    def _zero_update(self, main, g, upd, guard, steps_before, n, res) -> torch.Tensor:
+        """ZeRO-1 (parallel.zero_plan): per chunk, an in-place reduce-scatter of the gradient
+        on the communication stream, the fused Adam (mask penalties and divergence guard
+        included) on this rank's shard, and an in-place all-gather of the parameters — chunk
+        k's all-gather overlaps chunk k+1's Adam.  Without a process group (zero_sim) the
+        same Adam launches run with no communication."""
+        from .parallel import all_gather_inplace, reduce_scatter_inplace, zero_plan
+        rank, world = self._zero_world()
+        plan = zero_plan(g._layout_map, world, rest_grads=bool(self.settings.compute_sh_rest_grads),
+                         chunks=self.zero_chunks)
+        if self.comm_stream is None:
+            self.comm_stream = torch.cuda.Stream(device=self.cloud.device)
+        comm = self.comm_stream
+        comm.wait_stream(main)
+        reduced = []
+        with stage("reduce_scatter"), torch.cuda.stream(comm):
+            if self.pg is not None:
+                import torch.distributed as dist
+                # every view's loss terms on every rank (each rank wrote only its own rows,
+                # the others are zero): the divergence guard then decides identically everywhere
+                dist.all_reduce(self.terms, group=self.pg)
+            for ch in plan:
+                if self.pg is not None:
+                    reduce_scatter_inplace(g.flat, ch, rank, world, self.pg)
+                ev = torch.cuda.Event()
+                ev.record(comm)
+                reduced.append(ev)
+        names = tuple(upd)
+        for k, (ch, ev) in enumerate(zip(plan, reduced)):
+            main.wait_event(ev)
+            with stage("adam"):
+                self.opt.step(self.cloud, g, names=names, lambda_m=self.lambda_m, lambda_sh=self.lambda_sh, guard=guard,
+                              ranges=[ch.rank_range(rank)], count=k == 0)
+            if self.pg is not None:
+                done = torch.cuda.Event()
+                done.record(main)
+                comm.wait_event(done)
+                with stage("all_gather"), torch.cuda.stream(comm):
+                    all_gather_inplace(self.cloud.flat, ch, rank, world, self.pg)
+        main.wait_stream(comm)
+        return self._finish(main, steps_before, n, res)
+
+    def _zero_sync_moments(self) -> None:
+        """ZeRO-1 keeps each rank's Adam moments current on its own shard only; before the
+        rows are compacted (pruning) every rank gathers the full moments."""
+        if self.pg is None or self.dp_mode != "zero":
+            return
+        from .parallel import all_gather_inplace, zero_plan
+        rank, world = self._zero_world()
+        for ch in zero_plan(self.grads._layout_map, world, rest_grads=True, chunks=self.zero_chunks):
+            all_gather_inplace(self.opt.m, ch, rank, world, self.pg)
+            all_gather_inplace(self.opt.v, ch, rank, world, self.pg)
 
     def _finish(self, main, steps_before, n, res) -> torch.Tensor:
         """Queue the pinned copy of the divergence flag and the loss terms; the next step

@@ -17,7 +17,7 @@ STAGE_OF = [  # kernel-name prefix -> bench stage
     ("k_seg_", "bin_instances"), ("k_scatter", "bin_instances"), ("k_unit_table", "bin_instances"),
     ("k_place_", "bin_instances"), ("k_tile_scan", "bin_instances"), ("k_blend_fwd", "blend_fwd"),
     ("k_ssim_", "loss"), ("k_loss_finalize", "loss"), ("k_blend_bwd", "blend_bwd"),
-    ("k_preprocess_bwd", "preprocess_bwd"), ("k_adam", "adam"),
+    ("k_preprocess_bwd", "preprocess_bwd"), ("k_adam", "adam"), ("k_exact", "exact_records"),
 ]
 UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # -> microseconds
         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
@@ -56,7 +56,7 @@ def stage(name):
     return None
 
 
-PER_STEP = {"preprocess_fwd", "preprocess_bwd", "adam"}  # one launch per 8-view step (step report)
+PER_STEP = {"preprocess_fwd", "preprocess_bwd", "adam", "exact_records"}  # one launch per 8-view step (step report)
 
 
 def main(reps):
@@ -89,10 +89,17 @@ def main(reps):
         per_stage[st]["issue_w"] += (r["issue_busy_pct"] or 0.0) * r["time_us"]
         per_stage[st]["fma_w"] += (r["fma_pipe_pct"] or 0.0) * r["time_us"]
         per_stage[st]["insts"] += r["warp_insts"] or 0.0
-    json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"]), "time_us": round(v["time_us"], 1),
+    # a stage's kernels can repeat (the step report profiles two steps): per launch of the
+    # stage = the sums over its kernel list divided by the repeat count
+    def reps(v):
+        names = v["kernels"]
+        return max(names.count(k) for k in set(names)) if names else 1
+    json.dump({k: {"dram_bytes_per_launch": int(v["dram_bytes_per_launch"] / reps(v)),
+                   "time_us": round(v["time_us"] / reps(v), 1),
                    "issue_busy_pct": round(v["issue_w"] / max(v["time_us"], 1e-9), 1),
                    "fma_pipe_pct": round(v["fma_w"] / max(v["time_us"], 1e-9), 1),
-                   "warp_insts": int(v["insts"]), "kernels": v["kernels"]} for k, v in per_stage.items()},
+                   "warp_insts": int(v["insts"] / reps(v)), "kernels": sorted(set(v["kernels"]), key=v["kernels"].index)}
+               for k, v in per_stage.items()},
               open(f"profiles/{PREFIX}_ncu_traffic.json", "w"), indent=1)
     open(f"profiles/{PREFIX}_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))

@@ -434,6 +434,13 @@ def test_render_sharded_single_rank_nccl(tgs):
         img = parallel.render_sharded(cloud, sc.cameras[0], st)
         ref = tgs.render_forward(cloud, sc.cameras[0], st).image
         assert torch.equal(img, ref)
+        # a sequence through one renderer (bands from the previous batch's histogram)
+        rng = np.random.default_rng(9)
+        orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, 170, name=f"o{k}") for k in range(5)]
+        r = parallel.ShardedRenderer(cloud, st)
+        got = r.render(orbit[:3]) + r.render(orbit[3:])
+        for cam, im in zip(orbit, got):
+            assert torch.equal(im, tgs.render_forward(cloud, cam, st).image)
         from paper_2501_14534_b200 import rasterizer
         splats, _, tiles, _, _, _ = rasterizer.preprocess(cloud, sc.cameras[0], st)
         counts = parallel.row_histogram(splats, tiles, len(cloud), sc.cameras[0], 16)
@@ -751,7 +758,8 @@ def test_render_views_equals_render_forward(tgs):
     # the native batch path (tgs_render_views, used once a geometry's counts are known)
     # recovers from a too-small id capacity: grow, retry, same results
     from paper_2501_14534_b200 import rasterizer
-    geom = next(k for k in rasterizer._RV_CAP if k[1] == len(cloud))
+    sizes = tuple((int(c.width), int(c.height)) for c in cams)
+    geom = next(k for k in rasterizer._RV_CAP if k[1] == len(cloud) and k[3] == sizes)
     rasterizer._RV_CAP[geom] = 1024
     outs3 = tgs.render_views(cloud, cams, st)
     assert rasterizer._RV_CAP[geom] >= max(o._tiles.indices.numel() for o in outs3)

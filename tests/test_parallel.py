@@ -156,3 +156,139 @@ def test_gloo_world2_bucketed_allreduce_equals_full():
     for p in procs:
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == [0, 1] and all(r[1] for r in res), res
+
+
+def test_zero_plan_tiles_the_parameters():
+    """ZeRO-1 chunks: shard sizes are multiples of 64 floats, the padded extents of a
+    segment's chunks tile it without overlap, every parameter field is covered by exactly
+    one rank's range, and padded tails stay inside sh_rest (steps without higher-band
+    gradients) or the ZERO_PAD headroom."""
+    from paper_2501_14534_b200.cloud import PARAM_FIELDS, ZERO_PAD, _layout, params_end
+    for n in (1, 37, 1000, 123457):
+        lay, total = _layout(PARAM_FIELDS + ("mean2d_screen",), n)
+        end = params_end(lay)
+        for world in (1, 2, 3, 8):
+            for rest in (True, False):
+                plan = parallel.zero_plan(lay, world, rest_grads=rest, chunks=4)
+                owned = np.zeros(end, dtype=np.int32)
+                for i, ch in enumerate(plan):
+                    assert ch.shard % 64 == 0 and ch.begin % 64 == 0
+                    pe = ch.padded_end(world)
+                    nxt = plan[i + 1].begin if i + 1 < len(plan) else None
+                    if nxt is not None and nxt < pe:
+                        raise AssertionError("padded chunk overlaps the next one")
+                    if pe > ch.end:  # a padded tail: sh_rest on no-rest steps, else the headroom
+                        if not rest and ch.end == lay["sh_rest"][0]:
+                            assert pe <= lay["mask_logits"][0]
+                        else:
+                            assert ch.end == end and pe <= end + ZERO_PAD and pe <= lay["mean2d_screen"][0]
+                    for r in range(world):
+                        a, b = ch.rank_range(r)
+                        owned[a:b] += 1
+                single = len({c.end for c in plan if c.end == lay["sh_rest"][0]}) == 0
+                for f in PARAM_FIELDS:
+                    if f == "sh_rest" and not rest and not single:
+                        continue
+                    o, m = lay[f]
+                    assert (owned[o:o + m] == 1).all(), (n, world, rest, f)
+
+
+def _zero_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_14534_b200.cloud import PARAM_FIELDS, _layout
+        lay, total = _layout(PARAM_FIELDS + ("mean2d_screen",), 777)
+        ok = []
+        for rest in (True, False):
+            rng = np.random.default_rng(100 + rank)
+            g = torch.from_numpy(rng.standard_normal(total))
+            p0 = torch.from_numpy(np.random.default_rng(7).standard_normal(total))  # replicated
+            if not rest:
+                o, m = lay["sh_rest"]
+                g[o:o + m] = 0  # zero on every rank without higher-band gradients
+            # reference: all-reduce + the update on every field
+            gs = g.clone()
+            dist.all_reduce(gs)
+            ref = p0.clone()
+            for f in PARAM_FIELDS:
+                if f == "sh_rest" and not rest:
+                    continue
+                o, m = lay[f]
+                ref[o:o + m] -= 0.1 * gs[o:o + m]
+            # ZeRO-1: in-place reduce-scatter, update of this rank's shard, in-place all-gather
+            p = p0.clone()
+            plan = parallel.zero_plan(lay, world, rest_grads=rest, chunks=3)
+            for ch in plan:
+                parallel.reduce_scatter_inplace(g, ch, rank, world)
+            for ch in plan:
+                a, b = ch.rank_range(rank)
+                for f in PARAM_FIELDS:  # the kernel updates field floats only, never padding
+                    if f == "sh_rest" and not rest:
+                        continue
+                    o, m = lay[f]
+                    lo, hi = max(a, o), min(b, o + m)
+                    if hi > lo:
+                        p[lo:hi] -= 0.1 * g[lo:hi]
+                parallel.all_gather_inplace(p, ch, rank, world)
+            for f in PARAM_FIELDS:
+                o, m = lay[f]
+                ok.append(torch.allclose(p[o:o + m], ref[o:o + m], rtol=1e-12, atol=1e-12))
+        q.put((rank, all(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_zero1_update_equals_allreduce_update(world):
+    """ZeRO-1 over gloo (world 2 and 3): reduce-scatter + shard update + all-gather gives
+    every rank the parameters of all-reduce + full update."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_zero_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == list(range(world)) and all(r[1] for r in res), res
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        h, w, ts, nf = 70, 9, 16, 3
+        frames = [torch.from_numpy(np.random.default_rng(f).standard_normal((h, w, 3))) for f in range(nf)]
+        rows = (h + ts - 1) // ts
+        bands = parallel.row_split(np.random.default_rng(5).uniform(1, 9, rows), world)
+        maxr = max(min(e * ts, h) - b * ts for b, e in bands)
+        b, e = bands[rank]
+        buf = torch.zeros((nf, maxr, w, 3), dtype=torch.float64)
+        for f in range(nf):
+            buf[f, : min(e * ts, h) - b * ts] = frames[f][b * ts: min(e * ts, h)]
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, parts, dst=0)
+        ok = True
+        if rank == 0:
+            got = parallel.assemble_bands(parts, bands, ts, h)
+            ok = all(torch.equal(a, b_) for a, b_ in zip(got, frames))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_band_gather_to_rank0_assembles_frames():
+    """The sharded render's batch gather: every rank's band rows of every frame to rank 0
+    in one gather, assembled into the full frames (parallel.assemble_bands)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1, 2] and all(r[1] for r in res), res
