@@ -523,6 +523,36 @@ def main():
         dist.destroy_process_group()
 
 
+def gpu_busy(fn, k: int) -> dict:
+    """Run fn k times under a CUDA activity trace; GPU busy = the union of the kernel
+    intervals, span = first kernel start to last kernel end (profiles/gpu_idle.py)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(k):
+            fn()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    iv = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+                if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0
+                and "Memcpy" not in e.name and "Memset" not in e.name)
+    if not iv:
+        return {}
+    busy, cs, ce = 0.0, iv[0][0], iv[0][1]
+    for a, b in iv[1:]:
+        if a > ce:
+            busy += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    busy += ce - cs
+    span = max(b for _, b in iv) - iv[0][0]
+    return {"steps": k, "gpu_busy_ms_per_step": round(busy / k / 1e3, 3), "span_ms_per_step": round(span / k / 1e3, 3),
+            "busy_fraction": round(busy / max(span, 1e-9), 3), "wall_ms_per_step_traced": round(wall / k * 1e3, 3)}
+
+
 def rank_share(args):
     """Projection of the N-GPU c3 step from ONE GPU (only one GPU is available to this
     build): rank 0's share of an N-rank ZeRO-1 step — its views (0, N, 2N, ...), the
@@ -612,18 +642,29 @@ def schedule_c5(args):
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     _lib.load()
-    sc = scenes.config3(n=args.n, views=VIEWS)
+    sc = scenes.config5(n=args.n, views=VIEWS)
     views = list(range(rank, VIEWS, world))
-    # targets: the initial scene rendered from each camera + N(0, 0.05) pixel noise — a
-    # self-consistent fit (uniform-random targets drive every mask to zero)
+    # targets: renders of a HELD-OUT SUBSET of the scene — 30% of the Gaussians, drawn from
+    # the rows the 8 cameras actually see (hit counts > 0, significance.count_hits) — so the
+    # photometric gradient keeps those alive while the mask penalty (lr 0.5, the reference's)
+    # prunes the rest, as BASELINE.json's ~30% survival of real scenes (on c3's solid ball
+    # only 24% of the rows are seen at all and ~1.5% survive; c5's scene is a shell)
+    from paper_2501_14534_b200 import significance
     from paper_2501_14534_b200.rasterizer import render_forward
     init = GaussianCloud.from_fields(sc.fields, device=dev)
-    gen = torch.Generator(device=dev).manual_seed(5)
+    st0 = RenderSettings(**settings_kwargs())
+    hits = significance.count_hits(init, sc.cameras, st0)
+    seen = torch.nonzero(hits > 0).flatten().cpu().numpy()
+    keep_n = min(int(0.3 * args.n), seen.size)
+    if os.environ.get("TGS_C5_SUBSET", "top") == "top":  # the most-hit rows: the best-supported 30%
+        subset = np.sort(torch.topk(hits.to(torch.float64), keep_n).indices.cpu().numpy())
+    else:
+        subset = np.sort(np.random.default_rng(5).choice(seen, keep_n, replace=False))
+    held = init.take(torch.from_numpy(subset).to(dev))
     full_t = {}
     for v in views:
-        img = render_forward(init, sc.cameras[v], RenderSettings(**settings_kwargs())).image
-        full_t[v] = (img + 0.05 * torch.randn(img.shape, device=dev, generator=gen)).contiguous()
-    del init
+        full_t[v] = render_forward(held, sc.cameras[v], st0).image.contiguous()
+    del init, held
     steps = args.c5_steps
     phase_len = max(1, steps // 4)
     kw = settings_kwargs()
@@ -656,6 +697,7 @@ def schedule_c5(args):
             trainer.step()
 
     run(0, 3)  # warm-up (page-in, kernel attributes); the timed sweep restarts from the initial scene
+    trainer.check_divergence()
     trainer.cloud = GaussianCloud.from_fields(sc.fields, device=dev)
     trainer.opt = type(trainer.opt)(trainer.cloud, trainer.opt.lrs)
     from paper_2501_14534_b200.cloud import CloudGrads
@@ -668,25 +710,41 @@ def schedule_c5(args):
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        w0 = time.perf_counter()
         s.record()
         run(0, steps)
         e.record()
         torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    trainer.check_divergence()
     t = torch.tensor([s.elapsed_time(e) / 1e3], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # host vs device: the GPU-busy share (union of kernel intervals, CUPTI via torch.profiler)
+    # of 16 steps at the first and at the last phase's settings, after the timed sweep
+    busy = {}
+    for label, i in (("phase1_240x135", 0), ("phase4_1920x1080", steps - 1)):
+        setup(i)
+        busy[label] = gpu_busy(trainer.step, 16)
+    trainer.check_divergence()
     if rank == 0:
         print(json.dumps({"metric": "c5 progressive-schedule sweep: train steps/s", "value": round(steps / float(t), 3),
                           "unit": "train step/s", "n_gpus": world, "steps": steps, "warmup": 3,
                           "ms_per_step": round(float(t) / steps * 1e3, 3), "higher_is_better": True,
                           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic (seeded BASELINE.json config 3 generator, schedule of config 5)",
+                          "data": "synthetic (seeded c5 shell scene, scenes.config5; schedule of BASELINE.json config 5)",
                           "config": {"workload": "c5: BASELINE.json configs[4] schedule sweep", "gaussians": args.n,
                                      "resolution_steps": ["240x135", "480x270", "960x540", "1920x1080"],
                                      "views_per_step": VIEWS, "prune_steps": prunes, "gaussians_after_prunes": counts,
                                      "final_fraction": round(counts[-1] / args.n, 3),
+                                     "targets": f"renders of a held-out {keep_n}-row subset of the {seen.size} "
+                                                f"rows seen by the cameras",
                                      "parallelism": f"dp{world}"},
-                          "total_s": round(float(t), 3), "clocks": clk.summary()}), flush=True)
+                          "total_s": round(float(t), 3), "host_wall_s": round(wall, 3),
+                          "host_ms_per_step": round(wall / steps * 1e3, 3),
+                          "device_ms_per_step": round(float(t) / steps * 1e3, 3),
+                          "gpu_busy_sample": busy,
+                          "clocks": clk.summary()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

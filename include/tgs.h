@@ -414,6 +414,21 @@ typedef struct {
   int32_t row_begin, row_end;
 } tgs_view_target;
 
+/* Per-view training payload of tgs_train_views: after the view's blend, on the same
+ * stream, the L1 + D-SSIM loss against `target` (dL/dimage into `dimage`, the mean L1 /
+ * mean SSIM into terms[0..1]; `loss_workspace` of tgs_loss_workspace bytes — views on
+ * one stream may share dimage and workspace) and the blend backward into `dsplats`
+ * (n, 9), accumulated.  target_ready (a cudaEvent_t, may be NULL): waited on before the
+ * loss (a host-to-device copy of the target on another stream). */
+typedef struct {
+  const float *target;
+  float *dimage;
+  double *terms;
+  float *dsplats;
+  void *loss_workspace;
+  void *target_ready;
+} tgs_view_train;
+
 TGS_API int tgs_render_views_workspace(int64_t n, int64_t max_instances, int32_t width, int32_t height,
                                        int32_t tile_size, size_t *bytes);
 TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s, int32_t nviews,
@@ -422,6 +437,22 @@ TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, con
                              tgs_view_target *targets,
                              void *const *workspaces, size_t workspace_bytes, int64_t *pinned_counts,
                              const tgs_stream_t *streams, const tgs_stream_t *blend_streams, int32_t nstreams);
+
+/* The per-view half of a training step (train.Trainer; training.py:296-309 per view)
+ * from C++: the caller has run tgs_preprocess_forward_views (and, on any stream,
+ * tgs_exact_records_views, complete at the event `exact_ready`, which may be NULL when
+ * exact is NULL or already complete); per view bin -> count -> place -> blend forward ->
+ * loss -> blend backward as tgs_render_views pipelines it (no separate blend streams),
+ * with train[v] the view's loss / backward buffers.  The caller then runs ONE
+ * tgs_preprocess_backward_views over the views' dsplats and the Adam step.  On
+ * TGS_ERR_CAPACITY some views may already have accumulated partials: zero them before
+ * the retry. */
+TGS_API int tgs_train_views(const tgs_cloud *cloud, const tgs_camera *cams, const tgs_settings *s, int32_t nviews,
+                            float *const *splats, uint8_t *const *visible, int32_t *const *tiles_touched,
+                            uint64_t *const *depth_keys, float *const *exact, void *exact_ready,
+                            int32_t *error_flag, tgs_view_target *targets, const tgs_view_train *train,
+                            float lambda_ssim, void *const *workspaces, size_t workspace_bytes,
+                            int64_t *pinned_counts, const tgs_stream_t *streams, int32_t nstreams);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,11 @@ class TgsViewTarget(ctypes.Structure):
                 ("hits", _P), ("num_instances", _I64), ("row_begin", _I32), ("row_end", _I32)]
 
 
+class TgsViewTrain(ctypes.Structure):
+    _fields_ = [("target", _P), ("dimage", _P), ("terms", _P), ("dsplats", _P), ("loss_workspace", _P),
+                ("target_ready", _P)]
+
+
 class TgsGrads(ctypes.Structure):
     _fields_ = [(f, _P) for f in GRAD_FIELDS]
 
@@ -72,6 +77,7 @@ _SIGS = {
     "tgs_memcpy_d2h_async": ([_P, _P, _SZ, _P], _I32),
     "tgs_render_views_workspace": ([_I64, _I64, _I32, _I32, _I32, _P], _I32),
     "tgs_render_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32], _I32),
+    "tgs_train_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _SZ, _P, _P, _I32], _I32),
     "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),

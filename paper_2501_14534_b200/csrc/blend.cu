@@ -30,14 +30,19 @@
 
 // Register caps of the exact-decision instantiations (minimum resident CTAs per SM): the
 // float64 resolution is out of line and rare, and without a cap its call would lower the
-// occupancy of the whole kernel (118 / 96 registers; capped: 80 / 64 with the spills on
-// the call path).  Measured at c3 (profiles/scripts/r02_run8.sh): 104.1 -> 106.9 step/s.
+// occupancy of the whole kernel (uncapped 96 registers in the forward; capped: 64 with
+// the spills on the call path).  The backward's cap is per 2-warp CTA of k_blend_bwd16p:
+// MINB x pairs CTAs (4 x 2 = 8: <= 128 registers).  Measured at c3
+// (profiles/scripts/r02_run8.sh, r02_run11.sh).
 // Overridable with -D for A/B builds (profiles/scripts/build_blend_variants.sh).
+#ifndef TGS_BWD16_PAIRS  // pixel pairs per lane of the 16x16 backward: 1 (k_blend_bwd16w) or 2
+#define TGS_BWD16_PAIRS 2
+#endif
 #ifndef TGS_FWD16_MINB
 #define TGS_FWD16_MINB 8
 #endif
 #ifndef TGS_BWD16_MINB
-#define TGS_BWD16_MINB 5
+#define TGS_BWD16_MINB 4
 #endif
 
 namespace tgs {
@@ -1045,6 +1050,257 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_bl
   }
 }
 
+// ---------------------------------------------------------------------------
+// Backward with kP packed pixel pairs per lane (kP = 2: 4 pixels per lane).  A tile's
+// 256 pixels are split over 4 / kP warps: kP = 2 gives each warp a 16x8 half tile,
+// lane l the column l & 15 and the rows (l >> 4) + {0, 2, 4, 6}.  Per surviving splat
+// the lane evaluates its 4 pixels (dx and the dx-only terms shared), and the warp's
+// 9-field reduction — about a third of the per-visit instructions at 2 pixels per lane
+// — now covers 128 pixels instead of 64; the chunk staging and cull are
+// amortised over twice the pixels as well.
+template <int kP>
+struct BwdLane {
+  int l[2 * kP];                                      // last_pos per pixel
+  float2 g0[kP], g1[kP], g2[kP], T[kP], GS[kP];       // per pair: (pixel 2h, pixel 2h+1)
+};
+
+template <int kP>
+__device__ __forceinline__ void lane_pixels(int lane, int warp, int tx, int ty, int &px, int py[2 * kP]) {
+  if (kP == 1) {
+    px = tx * 16 + ((warp & 1) << 3) + (lane & 7);
+    py[0] = ty * 16 + ((warp >> 1) << 3) + (lane >> 3);
+    py[1] = py[0] + 4;
+  } else {
+    px = tx * 16 + (lane & 15);
+    const int y0 = ty * 16 + warp * 8 + (lane >> 4);
+#pragma unroll
+    for (int k = 0; k < 2 * kP; ++k) py[k] = y0 + 2 * k;
+  }
+}
+
+// Out-of-line float64 resolution of a lane's flagged pixels (rare; see resolve2).
+template <int kP>
+__device__ __noinline__ int resolveP(const float4 *__restrict__ splats, const float4 *__restrict__ exact, int g,
+                                     float px, const float *fy, int flags) {
+  int r = 0;
+#pragma unroll
+  for (int k = 0; k < 2 * kP; ++k)
+    if (flags & (1 << k)) r |= exact_pair(splats, exact, g, px, fy[k]) << (2 * k);
+  return r;
+}
+
+template <bool kExact, int kP>
+__device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, const float2 fy[kP], float2 m,
+                                           float4 q, float4 cn, float4 col, float2 cut, int32_t gid,
+                                           const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+                                           float v[9]) {
+  const float dx = fpx - m.x;
+  const float t1 = __fmul_rn(__fmul_rn(q.x, dx), dx);  // dx-only terms, shared by every pixel of the lane
+  const float b = __fmul_rn(q.y, dx);
+  float2 dy[kP], e2[kP];
+#pragma unroll
+  for (int h = 0; h < kP; ++h) {
+    dy[h] = __fadd2_rn(fy[h], f2(-m.y));
+    e2[h] = __ffma2_rn(f2(b), dy[h], __ffma2_rn(__fmul2_rn(f2(q.z), dy[h]), dy[h], f2(t1)));  // exponent2()
+  }
+  bool ok[2 * kP], cl[2 * kP];
+#pragma unroll
+  for (int h = 0; h < kP; ++h) {
+    ok[2 * h] = pos < P.l[2 * h] && e2[h].x >= cut.y;
+    ok[2 * h + 1] = pos < P.l[2 * h + 1] && e2[h].y >= cut.y;
+  }
+  float2 gauss[kP], a_raw[kP];
+#pragma unroll
+  for (int h = 0; h < kP; ++h) {
+    gauss[h] = make_float2(ex2_approx(e2[h].x), ex2_approx(e2[h].y));
+    a_raw[h] = __fmul2_rn(f2(cn.w), gauss[h]);
+    // unclamped (a_raw <= 0.99): with exact records a clampable Gaussian goes to exact_pair
+    cl[2 * h] = kExact || a_raw[h].x <= kAlphaMax;
+    cl[2 * h + 1] = kExact || a_raw[h].y <= kAlphaMax;
+  }
+  if (kExact) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
+    float pm = 1.0f;
+#pragma unroll
+    for (int h = 0; h < kP; ++h) {
+      const float2 pr = __fmul2_rn(__fadd2_rn(e2[h], f2(-cut.x)), __fadd2_rn(e2[h], f2(-cut.y)));
+      pm = fminf(pm, fminf(pr.x, pr.y));
+    }
+    if (__any_sync(0xffffffffu, pm <= 0.0f)) {
+      int flags = 0;
+      float fyv[2 * kP];
+#pragma unroll
+      for (int h = 0; h < kP; ++h) {
+        fyv[2 * h] = fy[h].x;
+        fyv[2 * h + 1] = fy[h].y;
+        if (pos < P.l[2 * h] && !ok[2 * h] && e2[h].x >= cut.x) flags |= 1 << (2 * h);
+        if (pos < P.l[2 * h + 1] && !ok[2 * h + 1] && e2[h].y >= cut.x) flags |= 1 << (2 * h + 1);
+      }
+      if (flags) {
+        const int r = resolveP<kP>(splats, exact, gid, fpx, fyv, flags);
+#pragma unroll
+        for (int k = 0; k < 2 * kP; ++k)
+          if (flags & (1 << k)) {
+            ok[k] = (r >> (2 * k)) & 1;
+            cl[k] = (r >> (2 * k + 1)) & 1;
+          }
+      }
+    }
+  }
+  const float2 cx = __fmul2_rn(make_float2(cn.x, cn.y), f2(dx));  // (a dx, b dx), shared
+  float2 acc[9];
+#pragma unroll
+  for (int h = 0; h < kP; ++h) {
+    const float2 al = make_float2(fminf(a_raw[h].x, kAlphaMax), fminf(a_raw[h].y, kAlphaMax));
+    // a skipped entry blends alpha 0: 1 / (1 - 0) is exactly 1, T and G.S stay unchanged
+    const float2 alm = make_float2(ok[2 * h] ? al.x : 0.0f, ok[2 * h + 1] ? al.y : 0.0f);
+    const float2 om = __fadd2_rn(f2(1.0f), make_float2(-alm.x, -alm.y));  // 1 - al >= 0.01
+    const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+    const float2 tb = __fmul2_rn(P.T[h], inv);  // T before this entry
+    const float2 gc =
+        __ffma2_rn(P.g2[h], f2(col.z), __ffma2_rn(P.g1[h], f2(col.y), __fmul2_rn(P.g0[h], f2(col.x))));
+    const float2 ga = __ffma2_rn(gc, tb, __fmul2_rn(P.GS[h], make_float2(-inv.x, -inv.y)));
+    const float2 w = __fmul2_rn(alm, tb);
+    // partials through the unclamped alpha only; the select drops the NaN / Inf an
+    // out-of-range Gaussian factor can give
+    const float2 gx = __fmul2_rn(ga, gauss[h]);
+    const float2 v5 = make_float2(ok[2 * h] && cl[2 * h] ? gx.x : 0.0f, ok[2 * h + 1] && cl[2 * h + 1] ? gx.y : 0.0f);
+    const float2 gG = __fmul2_rn(v5, f2(cn.w));
+    const float2 v0 = __ffma2_rn(f2(cn.y), dy[h], f2(cx.x)), v1 = __ffma2_rn(f2(cn.z), dy[h], f2(cx.y));
+    const float2 hG = __fmul2_rn(gG, f2(0.5f));
+    const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
+    const float2 terms[9] = {p0, p1, __fmul2_rn(__fmul2_rn(hG, v0), v0), __fmul2_rn(p0, v1),
+                             __fmul2_rn(__fmul2_rn(hG, v1), v1), v5, __fmul2_rn(P.g0[h], w),
+                             __fmul2_rn(P.g1[h], w), __fmul2_rn(P.g2[h], w)};
+#pragma unroll
+    for (int f = 0; f < 9; ++f) acc[f] = h == 0 ? terms[f] : __fadd2_rn(acc[f], terms[f]);
+    P.GS[h] = __ffma2_rn(gc, w, P.GS[h]);
+    P.T[h] = tb;
+  }
+#pragma unroll
+  for (int f = 0; f < 9; ++f) v[f] = acc[f].x + acc[f].y;
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 2 * kP; ++k) any = any || ok[k];
+  return any;
+}
+
+template <bool kExact, int kP>
+__global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_blend_bwd16p(
+    const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets,
+    const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2,
+    const float *__restrict__ transmit, const int32_t *__restrict__ last_pos, const float *__restrict__ dimage,
+    float *__restrict__ dsplats, const int32_t *__restrict__ order) {
+  __shared__ WStage SW[4 / kP];
+  const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WStage &S = SW[warp];
+  int px, py[2 * kP];
+  lane_pixels<kP>(lane, warp, tx, ty, px, py);
+  const int start = __ldg(offsets + tile);
+  const float fpx = (float)px;
+  BwdLane<kP> P;
+  int wlast = 0;
+  int x0 = 0x7fffffff, x1 = -0x7fffffff, y0 = 0x7fffffff, y1 = -0x7fffffff;  // this lane's live box
+#pragma unroll
+  for (int k = 0; k < 2 * kP; ++k) {
+    int lp = 0;
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 0.f;
+    if (px < W && py[k] < H) {
+      const int p = py[k] * W + px;
+      lp = last_pos[p];
+      g0 = dimage[3 * p];
+      g1 = dimage[3 * p + 1];
+      g2 = dimage[3 * p + 2];
+      if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) lp = 0;  // _kernels.py:133-134
+      T = transmit[p];
+    }
+    P.l[k] = lp;
+    const float GS = (g0 * bg0 + g1 * bg1 + g2 * bg2) * T;
+    if (k & 1) {
+      P.g0[k >> 1].y = g0; P.g1[k >> 1].y = g1; P.g2[k >> 1].y = g2; P.T[k >> 1].y = T; P.GS[k >> 1].y = GS;
+    } else {
+      P.g0[k >> 1].x = g0; P.g1[k >> 1].x = g1; P.g2[k >> 1].x = g2; P.T[k >> 1].x = T; P.GS[k >> 1].x = GS;
+    }
+    wlast = max(wlast, lp);
+  }
+  wlast = __reduce_max_sync(0xffffffffu, wlast);
+  float2 fy[kP];
+#pragma unroll
+  for (int h = 0; h < kP; ++h) fy[h] = make_float2((float)py[2 * h], (float)py[2 * h + 1]);
+  SplatRegs nx;
+  // back to front over chunks [lo, hi) of 32 list positions below this warp's last blend
+  int hi = wlast;
+  fetch_splat(nx, splats, kExact ? exact : nullptr, ids, start + hi - 32 + lane, hi - 32 + lane >= 0);
+  for (; hi > 0; hi -= 32) {
+    const int lo = hi - 32;  // may be negative: lanes below position 0 are idle
+    const bool okl = lo + lane >= 0;
+    bool keep = false;
+    // only pixels whose last blended position lies beyond lo take part in this chunk
+#pragma unroll
+    for (int k = 0; k < 2 * kP; ++k)
+      if (P.l[k] > lo) {
+        x0 = min(x0, px); x1 = max(x1, px); y0 = min(y0, py[k]); y1 = max(y1, py[k]);
+      }
+    const float4 wbc = make_float4((float)__reduce_min_sync(0xffffffffu, x0), (float)__reduce_max_sync(0xffffffffu, x1),
+                                   (float)__reduce_min_sync(0xffffffffu, y0), (float)__reduce_max_sync(0xffffffffu, y1));
+    x0 = 0x7fffffff; x1 = -0x7fffffff; y0 = 0x7fffffff; y1 = -0x7fffffff;
+    if (okl) {
+      const float4 q = prescaled_conic(nx.a, nx.b);
+      const float2 cut = kExact ? nx.cut : load_cut(nullptr, nx.g, nx.b.y);
+      const float thr = cut.x - 0.02f;  // cull: nothing below cut.x blends
+      const float2 m = make_float2(nx.a.x, nx.a.y);
+      S.xy[lane] = m;
+      S.q[lane] = q;
+      S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      S.cut[lane] = cut;
+      S.id[lane] = nx.g;
+      keep = !quad_misses(m, q, thr, wbc);
+    }
+    uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    fetch_splat(nx, splats, kExact ? exact : nullptr, ids, start + lo - 32 + lane, lo - 32 + lane >= 0);
+    // surviving splats back to front, two per reduction (the second one, if any,
+    // follows the first in each pixel's walk, so the per-pixel order is unchanged)
+    while (mask) {
+      float v0[9], v1[9];
+      const int b0 = 31 - __clz(mask);
+      mask &= ~(1u << b0);
+      bool hit = bwd_visitP<kExact, kP>(P, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], S.cut[b0],
+                                        S.id[b0], splats, exact, v0);
+      int id1 = -1;
+      if (mask) {  // warp-uniform
+        const int b1 = 31 - __clz(mask);
+        mask &= ~(1u << b1);
+        hit = bwd_visitP<kExact, kP>(P, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], S.cut[b1],
+                                     S.id[b1], splats, exact, v1) || hit;
+        id1 = S.id[b1];
+      } else {
+#pragma unroll
+        for (int f = 0; f < 9; ++f) v1[f] = 0.0f;
+      }
+      if (__any_sync(0xffffffffu, hit)) {
+        float u[16];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          u[f] = v0[f];
+          u[8 + f] = v1[f];
+        }
+        const float r = warp_reduce16_transpose(u, lane);
+        const float r9 = warp_reduce2_transpose(v0[8], v1[8], lane);
+        const int id = (lane & 16) ? id1 : S.id[b0];
+        if (id >= 0) {
+          float *d = dsplats + 9 * (int64_t)id;
+          if ((lane & 1) == 0 && r != 0.0f) atomicAdd(d + ((lane >> 1) & 7), r);
+          if ((lane & 15) == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // _kernels.py:184-241: same walk as the forward, writing (gid, a*T) per blended entry
 __global__ void k_blend_records(const float4 *__restrict__ splats, const float4 *__restrict__ exact,
                                 const int32_t *__restrict__ offsets,
@@ -1212,6 +1468,13 @@ extern "C" int tgs_blend_backward(const float *splats, const float *exact, const
   if (ntiles == 0) return TGS_OK;
   const float4 *ex = reinterpret_cast<const float4 *>(exact);
   if (s->tile_size == 16) {
+#if TGS_BWD16_PAIRS == 2
+    (ex ? k_blend_bwd16p<true, 2> : k_blend_bwd16p<false, 2>)<<<ntiles, 64, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
+        row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
+        tile_order);
+    return launch_status();
+#endif
     (ex ? k_blend_bwd16w<true> : k_blend_bwd16w<false>)<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,

@@ -21,19 +21,23 @@ SH_BAND_WEIGHTS = (9.0 / 45.0, 15.0 / 45.0, 21.0 / 45.0)  # masking.py:18
 _WS_BYTES: dict = {}  # (W, H) -> tgs_loss_workspace bytes
 
 
+def _loss_bytes(w: int, h: int) -> int:
+    nb = _WS_BYTES.get((w, h))
+    if nb is None:
+        out = ctypes.c_size_t(0)
+        _lib.call("tgs_loss_workspace", w, h, ctypes.byref(out))
+        nb = _WS_BYTES[(w, h)] = int(out.value)
+    return nb
+
+
 def _workspace(dev, w, h):
     """The loss workspace of the CURRENT stream (the SSIM partial planes written by
     k_ssim_fwd and read by k_ssim_adj, and the per-CTA sums of k_loss_finalize).
     Per stream, never shared: views whose loss pipelines run concurrently on different
     streams (train.Trainer) each get their own, and a workspace is only reused — or
     grown, its old block returning to that stream's pool — in that stream's order."""
-    nb = _WS_BYTES.get((w, h))
-    if nb is None:
-        out = ctypes.c_size_t(0)
-        _lib.call("tgs_loss_workspace", w, h, ctypes.byref(out))
-        nb = _WS_BYTES[(w, h)] = int(out.value)
     from .rasterizer import _scratch
-    return _scratch("loss", nb, dev)
+    return _scratch("loss", _loss_bytes(w, h), dev)
 
 
 def l1_ssim_async(image: torch.Tensor, target: torch.Tensor, lambda_ssim: float, dimage: torch.Tensor,

@@ -79,7 +79,8 @@ class Trainer:
     def __init__(self, cloud: GaussianCloud, cameras, targets, settings: RenderSettings, lambda_ssim: float = 0.2,
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
                  views=None, streams: int = 4, deterministic: bool = False, densify_stats: bool = False,
-                 dp_mode: str = "zero", zero_chunks: int = 4, zero_sim: tuple | None = None):
+                 dp_mode: str = "zero", zero_chunks: int = 4, zero_sim: tuple | None = None,
+                 native: bool | None = None):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -95,6 +96,15 @@ class Trainer:
         if dp_mode not in ("zero", "allreduce"):
             raise ValueError("dp_mode must be 'zero' or 'allreduce'")
         self.dp_mode, self.zero_chunks, self.zero_sim = dp_mode, int(zero_chunks), zero_sim
+        # native=True: the per-view loop (bin, count, place, blend, loss, backward) is issued
+        # from C++ (tgs_train_views) when the views are pipelined over >= 2 streams and the
+        # atomic backward is used; the Python loop remains for 1 stream (per-stage timing)
+        # and the deterministic backward
+        if native is None:  # TGS_TRAIN_NATIVE=0: the Python loop (A/B timing)
+            import os
+            native = os.environ.get("TGS_TRAIN_NATIVE", "1") != "0"
+        self.native = native
+        self._nat = {}  # per-geometry native buffers: (key) -> dict
         self.rank = 0
         if process_group is not None:
             import torch.distributed as dist
@@ -232,6 +242,9 @@ class Trainer:
         for s_ in self.streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         ts = int(self.settings.tile_size)
+        if self.native and not self.deterministic and n and len(self.streams) >= 2 and self.views:
+            vis, parts = self._views_native(pres, exact_ready, copied)
+            return self._after_views(main, g, vis, parts, copied, n)
 
         def begin(i):  # view i's depth sort + instance-count read-back, on view i's stream
             if not n or len(self.streams) < 2:
@@ -281,6 +294,100 @@ class Trainer:
                                              deterministic=self.deterministic)
                 vis.append(st_state.visible_u8)
                 parts.append(ds)
+        return self._after_views(main, g, vis, parts, copied, n)
+
+    def _views_native(self, pres, exact_ready, copied):
+        """tgs_train_views: the views' bin -> count -> place -> blend -> loss -> backward
+        issued from C++ over self.streams (the Python loop's schedule).  Buffers persist per
+        view geometry; a too-small instance capacity is grown and the batch retried with
+        the partial buffers zeroed."""
+        import ctypes
+        from . import _lib
+        from .errors import TGS_ERR_CAPACITY, raise_for_status
+        from .rasterizer import _blend_order, _scratch, _size_class, ctypes_size
+        dev, n, ts = self.cloud.device, len(self.cloud), int(self.settings.tile_size)
+        ns, V = len(self.streams), len(self.views)
+        cams = [self.cameras[v] for v in self.views]
+        geo = tuple((int(c.width), int(c.height)) for c in cams)
+        key = (n, ts, geo)
+        nb = self._nat.get(key)
+        if nb is None:
+            nb = self._nat[key] = {"cap": 0}
+            self._nat = {key: nb}  # one geometry at a time (resolution steps free the old)
+        for v in self.views:
+            ds = self.dsplats.get(v)
+            if ds is None or ds.shape[0] != n:
+                self.dsplats[v] = torch.zeros((n, 9), dtype=torch.float32, device=dev)
+            elif not self.clear_partials:
+                ds.zero_()
+        c_set = _lib.make_settings(self.settings)
+        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+        c_cloud = self.cloud.native()
+        arr = lambda k: (ctypes.c_void_p * V)(*[p[k].data_ptr() for p in pres])  # noqa: E731
+        pinned = nb.get("pinned")
+        if pinned is None:
+            pinned = nb["pinned"] = torch.empty(2 * ns, dtype=torch.int64, pin_memory=True)
+        for attempt in range(4):
+            cap = nb["cap"]
+            if cap == 0:  # first step of this geometry: a generous first guess
+                cap = nb["cap"] = _size_class(max(4096, 24 * n))
+            if nb.get("bufs_cap") != cap:
+                nb["bufs"] = []
+                for w, h in geo:
+                    tx, ty = (w + ts - 1) // ts, (h + ts - 1) // ts
+                    nb["bufs"].append(dict(
+                        image=torch.empty((h, w, 3), device=dev), T=torch.empty((h, w), device=dev),
+                        ws=torch.empty((h, w), device=dev), nc=torch.empty((h, w), dtype=torch.int32, device=dev),
+                        lp=torch.empty((h, w), dtype=torch.int32, device=dev),
+                        off=torch.empty(tx * ty + 1, dtype=torch.int32, device=dev),
+                        ids=torch.empty(cap, dtype=torch.int32, device=dev),
+                        order=_blend_order(None, tx * ty, tx, ty, ts, dev, None)))
+                nb["bufs_cap"] = cap
+                nb["wsb"] = max(ctypes_size("tgs_render_views_workspace", n, cap, w, h, ts) for w, h in geo)
+            wss = [_scratch("train_views", nb["wsb"], dev, s_.cuda_stream, owner=s_) for s_ in self.streams]
+            loss_ws, train = [], (_lib.TgsViewTrain * V)()
+            targets = (_lib.TgsViewTarget * V)()
+            for i, v in enumerate(self.views):
+                b = nb["bufs"][i]
+                k = i % ns
+                h, w = geo[i][1], geo[i][0]
+                d = self.dimage.get((k, h, w))
+                if d is None:
+                    with torch.cuda.stream(self.streams[k]):
+                        d = self.dimage[(k, h, w)] = torch.empty((h, w, 3), device=dev)
+                lw = _scratch("loss", loss_mod._loss_bytes(w, h), dev, self.streams[k].cuda_stream, owner=self.streams[k])
+                loss_ws.append(lw)
+                targets[i] = _lib.TgsViewTarget(b["off"].data_ptr(), b["ids"].data_ptr(), cap, _lib.ptr(b["order"]),
+                                                b["image"].data_ptr(), b["T"].data_ptr(), b["ws"].data_ptr(),
+                                                b["nc"].data_ptr(), b["lp"].data_ptr(), None, -1, 0, 0)
+                train[i] = _lib.TgsViewTrain(self.targets[v].data_ptr(), d.data_ptr(), self.terms[v].data_ptr(),
+                                             self.dsplats[v].data_ptr(), lw.data_ptr(),
+                                             copied[v].cuda_event if v in copied else None)
+            with stage("train_views"):
+                rc = int(_lib.load().tgs_train_views(
+                    ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0), arr(1), arr(2), arr(3), arr(5),
+                    exact_ready.cuda_event, pres[0][4].data_ptr(), targets, train, float(self.lambda_ssim),
+                    (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), nb["wsb"], pinned.data_ptr(),
+                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]), ns))
+            counts = [int(targets[i].num_instances) for i in range(V)]
+            if rc == TGS_ERR_CAPACITY:
+                for s_ in self.streams:
+                    s_.synchronize()
+                for v in self.views:  # views already backwarded accumulated partials
+                    self.dsplats[v].zero_()
+                nb["cap"] = _size_class(int(max(counts) * 1.25) + 1024)
+                continue
+            raise_for_status(rc, "tgs_train_views")
+            if nb["cap"] < max(counts):  # (not reached: the driver reports capacity first)
+                nb["cap"] = _size_class(int(max(counts) * 1.25) + 1024)
+            break
+        else:
+            raise RuntimeError("tgs_train_views: instance capacity did not converge")
+        self.check_divergence(block=False)  # the previous step's flag is on the host by now
+        self.instances = counts
+        return [p[1] for p in pres], [self.dsplats[v] for v in self.views]
+
+    def _after_views(self, main, g, vis, parts, copied, n):
         for s_ in self.streams:
             main.wait_stream(s_)
         main.wait_stream(self.exact_stream)

@@ -298,3 +298,36 @@ def test_select_rows_matches_nonzero(tgs, n):
     flags = (x < -0.5).to(torch.uint8)
     got = pruning.select_rows(n, x.device, flags=flags)
     assert torch.equal(got, torch.nonzero(flags).flatten())
+
+
+def test_native_train_views_equals_python_loop(tgs):
+    """tgs_train_views (the per-view loop issued from C++) against the Python loop: the same
+    kernels on the same inputs — loss terms bitwise, parameters within float reassociation
+    of the atomic backward, over three steps with a view count that wraps the streams, a
+    too-small first instance capacity (grow + retry) and host targets."""
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.train import Trainer
+    sc = scenes.small_scene(seed=17, n=40_000, width=192, height=128, dist=3.5)
+    rng = np.random.default_rng(17)
+    cams = [scenes.pinhole(3.5 * scenes._unit(rng), 192, 128, name=f"t{k}") for k in range(7)]
+    tg = [torch.rand((128, 192, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(k))
+          for k in range(7)]
+    st = tgs.RenderSettings(near=0.2, mask_threshold=0.05)
+    res = []
+    for native in (True, False):
+        cloud = tgs.GaussianCloud.from_fields(sc.fields)
+        tr = Trainer(cloud, cams, [t.clone() for t in tg], st, streams=3, native=native)
+        if native:  # force the capacity path on the first step
+            tr._nat[(len(cloud), 16, tuple((192, 128) for _ in cams))] = {"cap": 1024}
+        host = {v: tg[v].cpu().pin_memory() for v in range(7)}
+        terms = []
+        for it in range(3):
+            tr.step(host_targets=host if it == 2 else None)
+            terms.append(tr.terms.clone())
+        torch.cuda.synchronize()
+        tr.check_divergence()
+        res.append((tr.cloud.flat.clone(), torch.stack(terms), list(tr.instances)))
+    assert torch.equal(res[0][1][0], res[1][1][0])  # step 1: identical inputs, identical loss
+    assert res[0][2] == res[1][2]
+    torch.testing.assert_close(res[0][1], res[1][1], rtol=1e-5, atol=1e-7)
+    torch.testing.assert_close(res[0][0], res[1][0], rtol=1e-4, atol=1e-6)
