@@ -30,8 +30,8 @@
 
 // Register caps of the exact-decision instantiations (minimum resident CTAs per SM): the
 // float64 resolution is out of line and rare, and without a cap its call would lower the
-// occupancy of the whole kernel (uncapped 96 registers in the forward; capped: 64 with
-// the spills on the call path).  The backward's cap is per 2-warp CTA of k_blend_bwd16p:
+// occupancy of the whole kernel (uncapped 96 registers in the forward; capped at 6 CTAs
+// per SM: 80, no spills).  The backward's cap is per 2-warp CTA of k_blend_bwd16p:
 // MINB x pairs CTAs (4 x 2 = 8: <= 128 registers).  Measured at c3
 // (profiles/scripts/r02_run8.sh, r02_run11.sh).
 // Overridable with -D for A/B builds (profiles/scripts/build_blend_variants.sh).
@@ -39,7 +39,7 @@
 #define TGS_BWD16_PAIRS 2
 #endif
 #ifndef TGS_FWD16_MINB
-#define TGS_FWD16_MINB 8
+#define TGS_FWD16_MINB 6
 #endif
 #ifndef TGS_BWD16_MINB
 #define TGS_BWD16_MINB 4

@@ -304,7 +304,7 @@ class Trainer:
         import ctypes
         from . import _lib
         from .errors import TGS_ERR_CAPACITY, raise_for_status
-        from .rasterizer import _blend_order, _scratch, _size_class, ctypes_size
+        from .rasterizer import EXACT_DECISIONS, _blend_order, _scratch, _size_class, ctypes_size
         dev, n, ts = self.cloud.device, len(self.cloud), int(self.settings.tile_size)
         ns, V = len(self.streams), len(self.views)
         cams = [self.cameras[v] for v in self.views]
@@ -365,8 +365,9 @@ class Trainer:
                                              copied[v].cuda_event if v in copied else None)
             with stage("train_views"):
                 rc = int(_lib.load().tgs_train_views(
-                    ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0), arr(1), arr(2), arr(3), arr(5),
-                    exact_ready.cuda_event, pres[0][4].data_ptr(), targets, train, float(self.lambda_ssim),
+                    ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0), arr(1), arr(2), arr(3),
+                    arr(5) if EXACT_DECISIONS else None, exact_ready.cuda_event, pres[0][4].data_ptr(), targets,
+                    train, float(self.lambda_ssim),
                     (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), nb["wsb"], pinned.data_ptr(),
                     (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]), ns))
             counts = [int(targets[i].num_instances) for i in range(V)]
