@@ -688,11 +688,12 @@ __device__ __forceinline__ float4 warp_bounds2(bool liveA, bool liveB, int px, i
 struct Fwd16Pair {
   float2 T = make_float2(1.0f, 1.0f), c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f),
          c2 = make_float2(0.f, 0.f), ws = make_float2(0.f, 0.f);
-  int cA = 0, cB = 0, lA = 0, lB = 0;
+  float2 cnt = make_float2(0.f, 0.f);  // n_contrib of both pixels, counted in one FADD2 (exact < 2^24)
+  int lA = 0, lB = 0;
   bool dA, dB;
 };
 
-template <bool kExact>
+template <bool kExact, bool kHits>
 __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
                                            float2 cut, int pos, int32_t *hits, int32_t gid,
                                            const float4 *__restrict__ splats, const float4 *__restrict__ exact) {
@@ -705,33 +706,30 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   const float2 s = __ffma2_rn(__fmul2_rn(make_float2(q.z, q.z), dy), dy, make_float2(t1, t1));
   const float b = __fmul_rn(q.y, dx);
   const float2 e2 = __ffma2_rn(make_float2(b, b), dy, s);  // exponent2() for both pixels
-  float2 al = __fmul2_rn(make_float2(q.w, q.w), make_float2(ex2_approx(e2.x), ex2_approx(e2.y)));
+  const float2 a_raw = __fmul2_rn(make_float2(q.w, q.w), make_float2(ex2_approx(e2.x), ex2_approx(e2.y)));
   // blend decisions (load_cut / exact_pair): certain in float32 outside the cut bracket;
-  // a visit with a pair inside it (rare) resolves it in float64 out of line
-  bool okA = !P.dA && e2.x >= cut.y;
-  bool okB = !P.dB && e2.y >= cut.y;
+  // a visit with a pair inside it (rare) resolves it in float64 out of line.  The
+  // decision is carried as the blended alpha itself (0 = skipped; a blended alpha is
+  // >= ~1/255 > 0), so no boolean has to live across the rare branch.
+  float2 al = make_float2(!P.dA && e2.x >= cut.y ? fminf(a_raw.x, kAlphaMax) : 0.0f,
+                          !P.dB && e2.y >= cut.y ? fminf(a_raw.y, kAlphaMax) : 0.0f);
   if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
-    const bool uA = !P.dA && !okA && e2.x >= cut.x, uB = !P.dB && !okB && e2.y >= cut.x;
+    const bool uA = !P.dA && !(e2.x >= cut.y) && e2.x >= cut.x, uB = !P.dB && !(e2.y >= cut.y) && e2.y >= cut.x;
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
-    if (uA) okA = r & 1;
-    if (uB) okB = (r >> 2) & 1;
+    if (uA && (r & 1)) al.x = fminf(a_raw.x, kAlphaMax);
+    if (uB && (r & 4)) al.y = fminf(a_raw.y, kAlphaMax);
   }
-  al = make_float2(okA ? fminf(al.x, kAlphaMax) : 0.0f, okB ? fminf(al.y, kAlphaMax) : 0.0f);
+  const bool okA = al.x > 0.0f, okB = al.y > 0.0f;
   const float2 w = __fmul2_rn(al, P.T);
   P.c0 = __ffma2_rn(make_float2(col.x, col.x), w, P.c0);
   P.c1 = __ffma2_rn(make_float2(col.y, col.y), w, P.c1);
   P.c2 = __ffma2_rn(make_float2(col.z, col.z), w, P.c2);
   P.ws = __fadd2_rn(P.ws, w);
   P.T = __fmul2_rn(P.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
-  if (okA) {
-    ++P.cA;
-    P.lA = pos;
-  }
-  if (okB) {
-    ++P.cB;
-    P.lB = pos;
-  }
-  if (hits) {
+  P.cnt = __fadd2_rn(P.cnt, make_float2(okA ? 1.0f : 0.0f, okB ? 1.0f : 0.0f));
+  if (okA) P.lA = pos;
+  if (okB) P.lB = pos;
+  if (kHits) {
     if (okA) atomicAdd(hits + gid, 1);
     if (okB) atomicAdd(hits + gid, 1);
   }
@@ -865,7 +863,7 @@ __device__ __forceinline__ void fetch_splat(SplatRegs &r, const float4 *__restri
   }
 }
 
-template <bool kExact>
+template <bool kExact, bool kHits>
 __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_blend_fwd16w(
     const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
@@ -916,7 +914,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       const float2 m = S.xy[k];
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
-      fwd_visit2<kExact>(P, fpx, fy, m, q, col, S.cut[k], pos, hits, S.id[k], splats, exact);
+      fwd_visit2<kExact, kHits>(P, fpx, fy, m, q, col, S.cut[k], pos, hits, kHits || kExact ? S.id[k] : 0, splats,
+                                exact);
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
@@ -929,7 +928,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     image[3 * p + 2] = P.c2.x + bg2 * P.T.x;
     transmit[p] = P.T.x;
     wsum_out[p] = P.ws.x;
-    n_contrib[p] = P.cA;
+    n_contrib[p] = (int32_t)P.cnt.x;
     last_pos[p] = P.lA;
   }
   if (inB) {
@@ -939,7 +938,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     image[3 * p + 2] = P.c2.y + bg2 * P.T.y;
     transmit[p] = P.T.y;
     wsum_out[p] = P.ws.y;
-    n_contrib[p] = P.cB;
+    n_contrib[p] = (int32_t)P.cnt.y;
     last_pos[p] = P.lB;
   }
 }
@@ -1097,26 +1096,22 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
   const float dx = fpx - m.x;
   const float t1 = __fmul_rn(__fmul_rn(q.x, dx), dx);  // dx-only terms, shared by every pixel of the lane
   const float b = __fmul_rn(q.y, dx);
-  float2 dy[kP], e2[kP];
+  float2 dy[kP], e2[kP], gauss[kP], a_raw[kP], alm[kP], gm[kP];
 #pragma unroll
   for (int h = 0; h < kP; ++h) {
     dy[h] = __fadd2_rn(fy[h], f2(-m.y));
     e2[h] = __ffma2_rn(f2(b), dy[h], __ffma2_rn(__fmul2_rn(f2(q.z), dy[h]), dy[h], f2(t1)));  // exponent2()
-  }
-  bool ok[2 * kP], cl[2 * kP];
-#pragma unroll
-  for (int h = 0; h < kP; ++h) {
-    ok[2 * h] = pos < P.l[2 * h] && e2[h].x >= cut.y;
-    ok[2 * h + 1] = pos < P.l[2 * h + 1] && e2[h].y >= cut.y;
-  }
-  float2 gauss[kP], a_raw[kP];
-#pragma unroll
-  for (int h = 0; h < kP; ++h) {
     gauss[h] = make_float2(ex2_approx(e2[h].x), ex2_approx(e2[h].y));
     a_raw[h] = __fmul2_rn(f2(cn.w), gauss[h]);
-    // unclamped (a_raw <= 0.99): with exact records a clampable Gaussian goes to exact_pair
-    cl[2 * h] = kExact || a_raw[h].x <= kAlphaMax;
-    cl[2 * h + 1] = kExact || a_raw[h].y <= kAlphaMax;
+    // the forward's decisions, re-derived identically (load_cut / exact_pair) and carried as
+    // floats — alm: the blended alpha or 0 (a skipped entry blends alpha 0: 1 / (1 - 0) is
+    // exactly 1, T and G.S stay unchanged); gm: 1 where the partials through alpha apply
+    // (unclamped a_raw <= 0.99; with exact records a clampable Gaussian goes to exact_pair,
+    // so every certain pair is unclamped) — no boolean has to live across the rare branch
+    alm[h] = make_float2(pos < P.l[2 * h] && e2[h].x >= cut.y ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
+                         pos < P.l[2 * h + 1] && e2[h].y >= cut.y ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
+    gm[h] = make_float2(alm[h].x > 0.0f && (kExact || a_raw[h].x <= kAlphaMax) ? 1.0f : 0.0f,
+                        alm[h].y > 0.0f && (kExact || a_raw[h].y <= kAlphaMax) ? 1.0f : 0.0f);
   }
   if (kExact) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
     float pm = 1.0f;
@@ -1132,38 +1127,43 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
       for (int h = 0; h < kP; ++h) {
         fyv[2 * h] = fy[h].x;
         fyv[2 * h + 1] = fy[h].y;
-        if (pos < P.l[2 * h] && !ok[2 * h] && e2[h].x >= cut.x) flags |= 1 << (2 * h);
-        if (pos < P.l[2 * h + 1] && !ok[2 * h + 1] && e2[h].y >= cut.x) flags |= 1 << (2 * h + 1);
+        if (pos < P.l[2 * h] && !(e2[h].x >= cut.y) && e2[h].x >= cut.x) flags |= 1 << (2 * h);
+        if (pos < P.l[2 * h + 1] && !(e2[h].y >= cut.y) && e2[h].y >= cut.x) flags |= 1 << (2 * h + 1);
       }
       if (flags) {
         const int r = resolveP<kP>(splats, exact, gid, fpx, fyv, flags);
 #pragma unroll
-        for (int k = 0; k < 2 * kP; ++k)
-          if (flags & (1 << k)) {
-            ok[k] = (r >> (2 * k)) & 1;
-            cl[k] = (r >> (2 * k + 1)) & 1;
+        for (int h = 0; h < kP; ++h) {
+          if ((flags >> (2 * h)) & 1) {
+            const int rk = r >> (4 * h);
+            alm[h].x = (rk & 1) ? fminf(a_raw[h].x, kAlphaMax) : 0.0f;
+            gm[h].x = (rk & 3) == 3 ? 1.0f : 0.0f;
           }
+          if ((flags >> (2 * h + 1)) & 1) {
+            const int rk = r >> (4 * h + 2);
+            alm[h].y = (rk & 1) ? fminf(a_raw[h].y, kAlphaMax) : 0.0f;
+            gm[h].y = (rk & 3) == 3 ? 1.0f : 0.0f;
+          }
+        }
       }
     }
   }
   const float2 cx = __fmul2_rn(make_float2(cn.x, cn.y), f2(dx));  // (a dx, b dx), shared
   float2 acc[9];
+  float hitm = 0.0f;
 #pragma unroll
   for (int h = 0; h < kP; ++h) {
-    const float2 al = make_float2(fminf(a_raw[h].x, kAlphaMax), fminf(a_raw[h].y, kAlphaMax));
-    // a skipped entry blends alpha 0: 1 / (1 - 0) is exactly 1, T and G.S stay unchanged
-    const float2 alm = make_float2(ok[2 * h] ? al.x : 0.0f, ok[2 * h + 1] ? al.y : 0.0f);
-    const float2 om = __fadd2_rn(f2(1.0f), make_float2(-alm.x, -alm.y));  // 1 - al >= 0.01
+    const float2 om = __fadd2_rn(f2(1.0f), make_float2(-alm[h].x, -alm[h].y));  // 1 - al >= 0.01
     const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
     const float2 tb = __fmul2_rn(P.T[h], inv);  // T before this entry
     const float2 gc =
         __ffma2_rn(P.g2[h], f2(col.z), __ffma2_rn(P.g1[h], f2(col.y), __fmul2_rn(P.g0[h], f2(col.x))));
     const float2 ga = __ffma2_rn(gc, tb, __fmul2_rn(P.GS[h], make_float2(-inv.x, -inv.y)));
-    const float2 w = __fmul2_rn(alm, tb);
+    const float2 w = __fmul2_rn(alm[h], tb);
     // partials through the unclamped alpha only; the select drops the NaN / Inf an
-    // out-of-range Gaussian factor can give
+    // out-of-range Gaussian factor could give
     const float2 gx = __fmul2_rn(ga, gauss[h]);
-    const float2 v5 = make_float2(ok[2 * h] && cl[2 * h] ? gx.x : 0.0f, ok[2 * h + 1] && cl[2 * h + 1] ? gx.y : 0.0f);
+    const float2 v5 = make_float2(gm[h].x > 0.0f ? gx.x : 0.0f, gm[h].y > 0.0f ? gx.y : 0.0f);
     const float2 gG = __fmul2_rn(v5, f2(cn.w));
     const float2 v0 = __ffma2_rn(f2(cn.y), dy[h], f2(cx.x)), v1 = __ffma2_rn(f2(cn.z), dy[h], f2(cx.y));
     const float2 hG = __fmul2_rn(gG, f2(0.5f));
@@ -1175,13 +1175,11 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     for (int f = 0; f < 9; ++f) acc[f] = h == 0 ? terms[f] : __fadd2_rn(acc[f], terms[f]);
     P.GS[h] = __ffma2_rn(gc, w, P.GS[h]);
     P.T[h] = tb;
+    hitm = fmaxf(hitm, fmaxf(alm[h].x, alm[h].y));
   }
 #pragma unroll
   for (int f = 0; f < 9; ++f) v[f] = acc[f].x + acc[f].y;
-  bool any = false;
-#pragma unroll
-  for (int k = 0; k < 2 * kP; ++k) any = any || ok[k];
-  return any;
+  return hitm > 0.0f;
 }
 
 template <bool kExact, int kP>
@@ -1425,7 +1423,9 @@ extern "C" int tgs_blend_forward(const float *splats, const float *exact, const 
   if (ntiles == 0) return TGS_OK;
   const float4 *ex = reinterpret_cast<const float4 *>(exact);
   if (s->tile_size == 16) {
-    (ex ? k_blend_fwd16w<true> : k_blend_fwd16w<false>)<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
+    auto kern = ex ? (hits ? k_blend_fwd16w<true, true> : k_blend_fwd16w<true, false>)
+                   : (hits ? k_blend_fwd16w<false, true> : k_blend_fwd16w<false, false>);
+    kern<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
         last_pos, hits, tile_order);
