@@ -336,16 +336,17 @@ TGS_API int tgs_adam_step(float *param, const float *grad, float *m, float *v, i
  * Divergence guard (training.py:298-308): with n_terms > 0, if any of the
  * n_terms doubles at loss_terms (device) is not finite, NOTHING is updated and
  * *nonfinite_flag (device int32, may be NULL) is written 1 (else 0); the host
- * raises DivergenceError from it.  Only the floats in [range_begin, range_end)
- * (multiples of 4) are updated — a rank's shard under ZeRO-1 data parallelism;
- * [0, INT64_MAX) for all. */
+ * raises DivergenceError from it.  nranges > 0 (<= 8): only the floats in the
+ * ranges [range_begin[r], range_end[r]) (multiples of 4) are updated — a rank's
+ * shard under ZeRO-1 data parallelism, the rows of one preprocess-backward
+ * chunk; nranges = 0: all. */
 TGS_API int tgs_adam_step_groups(float *param, float *grad, float *m, float *v, int32_t ngroups,
                                  const int64_t *offsets, const int64_t *sizes, const float *lrs,
                                  const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
                                  float beta2, float eps, float lambda_m, float lambda_sh,
                                  const float *band_weights, int64_t n_gaussians, const double *loss_terms,
-                                 int32_t n_terms, int32_t *nonfinite_flag, int64_t range_begin,
-                                 int64_t range_end, tgs_stream_t stream);
+                                 int32_t n_terms, int32_t *nonfinite_flag, const int64_t *range_begin,
+                                 const int64_t *range_end, int32_t nranges, tgs_stream_t stream);
 
 /* ---- target-side progressive ops (images.py:58-102), (H, W, 3) float32.
  * area_resize: exact fractional box filter (downsampling only); workspace

@@ -95,7 +95,7 @@ _SIGS = {
     "tgs_loss_l1_ssim": ([_P, _P, _I32, _I32, _F, _P, _P, _P, _P], _I32),
     "tgs_adam_step": ([_P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _F, _P], _I32),
     "tgs_adam_step_groups": ([_P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _P, _I64, _P, _I32,
-                              _P, _I64, _I64, _P], _I32),
+                              _P, _P, _P, _I32, _P], _I32),
     "tgs_gather_rows": ([_P, _P, _P, _I64, _I32, _P], _I32),
     "tgs_select_rows_workspace": ([_I64, _P], _I32),
     "tgs_select_rows": ([_P, _P, _F, _I64, _P, _P, _P, _SZ, _P], _I32),

@@ -56,7 +56,10 @@ struct AdamGroupArgs {
   int kind[8];         // 0: plain, 1: Gaussian-mask penalty, 2: SH-band-mask penalty
   int ngroups;
   float b1, b2, eps, lam_m, lam_sh, inv_n, wband[3];
-  int64_t range_begin, range_end;  // only floats in [range_begin, range_end) (a ZeRO shard)
+  // the float4 chunks to update: up to 8 ranges [rb[r], rb[r] + 4 (r4[r+1] - r4[r])) (a ZeRO
+  // shard, the rows of a preprocess-backward chunk), r4 = prefix sums of their float4 counts
+  int nranges;
+  int64_t rb[8], r4[9];
   const double *terms;  // optional divergence guard: loss terms of this step (nterms doubles)
   int nterms;
   int32_t *nonfinite;   // set to 1 (and no parameter touched) when a term is not finite
@@ -82,14 +85,18 @@ __global__ void __launch_bounds__(256) k_adam_groups(float *__restrict__ p, floa
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.nonfinite) *a.nonfinite = 1;
     return;
   }
-  // float4 chunks from the first group's start to the padded end of the last one
-  // (groups need not start at 0: a data-parallel bucket steps a subset of the groups),
-  // clipped to the range (a rank's shard under ZeRO-1: its groups' indices stay global,
-  // so the per-group lr, bias corrections and SH-band weights are unchanged)
-  const int64_t c0 = (a.off[0] > a.range_begin ? a.off[0] : a.range_begin) / 4;
-  const int64_t n4 = (a.off[a.ngroups] < a.range_end ? a.off[a.ngroups] : a.range_end) / 4;
+  // float4 chunks of the ranges (each clipped to [first group start, padded end of the last
+  // group] on the host; groups need not start at 0: a data-parallel bucket steps a subset
+  // of the groups).  The groups keep their global indices inside a range, so the per-group
+  // lr, bias corrections and SH-band weights are unchanged.
+  const int64_t n4 = a.r4[a.nranges];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n4; c += stride) {
+  for (int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < n4; ci += stride) {
+    int r = 0;
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < a.nranges && ci >= a.r4[q]) r = q;
+    const int64_t c = a.rb[r] / 4 + (ci - a.r4[r]);
     const int64_t e = 4 * c;
     int k = 0;
 #pragma unroll
@@ -238,11 +245,11 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
                                     const float *bias_c1, const float *bias_c2, const int32_t *kinds, float beta1,
                                     float beta2, float eps, float lambda_m, float lambda_sh,
                                     const float *band_weights, int64_t n_gaussians, const double *loss_terms,
-                                    int32_t n_terms, int32_t *nonfinite_flag, int64_t range_begin,
-                                    int64_t range_end, tgs_stream_t stream) {
+                                    int32_t n_terms, int32_t *nonfinite_flag, const int64_t *range_begin,
+                                    const int64_t *range_end, int32_t nranges, tgs_stream_t stream) {
   if (ngroups < 1 || ngroups > 8 || !param || !grad || !m || !v || !offsets || !sizes || !lrs || !bias_c1 ||
-      !bias_c2 || !kinds || n_gaussians < 0 || n_terms < 0 || (n_terms > 0 && !loss_terms) || range_begin < 0 ||
-      (range_begin & 3) || (range_end & 3))
+      !bias_c2 || !kinds || n_gaussians < 0 || n_terms < 0 || (n_terms > 0 && !loss_terms) || nranges < 0 ||
+      nranges > 8 || (nranges > 0 && (!range_begin || !range_end)))
     return TGS_ERR_INVALID;
   if (((reinterpret_cast<uintptr_t>(param) | reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(m) |
         reinterpret_cast<uintptr_t>(v)) & 15) != 0)
@@ -267,14 +274,25 @@ extern "C" int tgs_adam_step_groups(float *param, float *grad, float *m, float *
   a.lam_sh = lambda_sh;
   a.inv_n = n_gaussians > 0 ? 1.0f / (float)n_gaussians : 0.0f;
   for (int l = 0; l < 3; ++l) a.wband[l] = band_weights ? band_weights[l] : 0.0f;
-  a.range_begin = range_begin;
-  a.range_end = range_end;
   a.terms = n_terms > 0 ? loss_terms : nullptr;
   a.nterms = n_terms;
   a.nonfinite = nonfinite_flag;
-  const int64_t lo = a.off[0] > range_begin ? a.off[0] : range_begin;
-  const int64_t hi = a.off[ngroups] < range_end ? a.off[ngroups] : range_end;
-  const int64_t n4 = hi / 4 - lo / 4;
+  // the ranges clipped to the groups' span; none given = the whole span
+  a.nranges = 0;
+  a.r4[0] = 0;
+  for (int r = 0; r < (nranges > 0 ? nranges : 1); ++r) {
+    int64_t lo = a.off[0], hi = a.off[ngroups];
+    if (nranges > 0) {
+      if ((range_begin[r] & 3) || (range_end[r] & 3)) return TGS_ERR_INVALID;
+      lo = range_begin[r] > lo ? range_begin[r] : lo;
+      hi = range_end[r] < hi ? range_end[r] : hi;
+    }
+    if (hi <= lo) continue;
+    a.rb[a.nranges] = lo;
+    a.r4[a.nranges + 1] = a.r4[a.nranges] + (hi - lo) / 4;
+    ++a.nranges;
+  }
+  const int64_t n4 = a.r4[a.nranges];
   if (n4 <= 0 && !a.terms) return TGS_OK;  // (with a guard, one block still writes the flag)
   const unsigned grid = (unsigned)tmax<int64_t>(1, tmin<int64_t>(ceil_div<int64_t>(n4, 256), 148 * 8));
   k_adam_groups<<<grid, 256, 0, as_stream(stream)>>>(param, grad, m, v, a);

@@ -80,11 +80,17 @@ class Adam:
                 self.beta2, self.eps, float(lambda_m), float(lambda_sh), (ctypes.c_float * 3)(*SH_BAND_WEIGHTS),
                 len(cloud), _lib.ptr(guard[0]) if guard is not None else None,
                 int(guard[0].numel()) if guard is not None else 0, _lib.ptr(guard[1]) if guard is not None else None)
-        for r0, r1 in (ranges if ranges is not None else [(0, (1 << 62))]):
-            if r1 <= r0:
-                continue
+        rs = [(int(a), int(b)) for a, b in ranges if b > a] if ranges is not None else []
+        if ranges is not None and not rs:
+            if guard is None:
+                return
+            rs = [(0, 0)]  # nothing to update, but the guard still writes its flag
+        for i in range(0, max(len(rs), 1), 8):  # one launch per 8 ranges (nranges = 0: all)
+            part = rs[i:i + 8]
             _lib.call("tgs_adam_step_groups", _lib.ptr(cloud.flat), _lib.ptr(grads.flat), _lib.ptr(self.m),
-                      _lib.ptr(self.v), *args, int(r0), int(r1), _lib.stream_handle(cloud.device))
+                      _lib.ptr(self.v), *args, (ctypes.c_int64 * max(len(part), 1))(*[a for a, _ in part] or [0]),
+                      (ctypes.c_int64 * max(len(part), 1))(*[b for _, b in part] or [0]),
+                      len(part) if ranges is not None else 0, _lib.stream_handle(cloud.device))
 
 
 def exponential_lr(step: int, lr_init: float, lr_final: float, max_steps: int) -> float:

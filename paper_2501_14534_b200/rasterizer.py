@@ -719,23 +719,42 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
 
 def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, visibles: list,
                               dsplats: list, grads: CloudGrads, accumulate: bool = False, stats=None,
-                              clear: bool = False) -> CloudGrads:
+                              clear: bool = False, rows: tuple | None = None) -> CloudGrads:
     """Second half of render_backward for a batch of views in ONE pass over the
     parameters (tgs_preprocess_backward_views): grads (+)= sum over views.  stats:
     optional train.DensifyStats, accumulating each view's screen-space gradient norm
     (training.py:333-337).  clear=True zeroes every dsplats[v] after reading it (the
-    training loop's buffers are then ready for the next step's blend backward)."""
+    training loop's buffers are then ready for the next step's blend backward).
+    rows=(r0, r1): only cloud rows [r0, r1) (r0 a multiple of 64) — a chunk of a pipelined
+    step whose Adam updates the finished rows while the next chunk runs."""
     import ctypes
     n = len(cloud)
     if n == 0 or not cams:
         return grads
     V = len(cams)
+    r0, r1 = rows if rows is not None else (0, n)
+    if r1 <= r0:
+        return grads
     c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
-    vis_ptrs = (ctypes.c_void_p * V)(*[v.data_ptr() for v in visibles])
-    ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() for d in dsplats])
+    vis_ptrs = (ctypes.c_void_p * V)(*[v.data_ptr() + r0 for v in visibles])
+    ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() + 36 * r0 for d in dsplats])
     c_set = _lib.make_settings(settings)
     c_cloud, c_grads = cloud.native(), grads.native()
     c_stats = stats.native() if stats is not None else None
+    if rows is not None:  # the same structs over the row sub-range (pointer offsets)
+        from .cloud import _ROW
+        f4 = 4
+        for f in ("positions", "log_scales", "rotations", "opacity_logits", "sh_dc", "sh_rest", "mask_logits",
+                  "sh_mask_logits"):
+            w = int(np.prod(_ROW[f]))
+            setattr(c_cloud, f, getattr(c_cloud, f) + f4 * w * r0)
+            setattr(c_grads, f, getattr(c_grads, f) + f4 * w * r0)
+        c_grads.mean2d_screen = c_grads.mean2d_screen + f4 * 2 * r0 if c_grads.mean2d_screen else None
+        c_cloud.n = r1 - r0
+        if c_stats is not None:
+            c_stats.grad_accum = c_stats.grad_accum + 4 * r0 if c_stats.grad_accum else None
+            c_stats.grad_count = c_stats.grad_count + 4 * r0 if c_stats.grad_count else None
+            c_stats.area_max = c_stats.area_max + 4 * r0 if c_stats.area_max else None
     with stage("preprocess_bwd"):
         _lib.call("tgs_preprocess_backward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), vis_ptrs,
                   ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)),

@@ -36,6 +36,19 @@ DEFAULT_LRS = {"positions": 1.6e-4, "log_scales": 5e-3, "rotations": 1e-3, "opac
                "sh_dc": 2.5e-3, "sh_rest": 2.5e-3 / 20.0, "mask_logits": 0.5, "sh_mask_logits": 0.05}
 
 
+def _row_ranges(layout: dict, names, n: int, r0: int, r1: int) -> list:
+    """Flat-buffer float ranges of cloud rows [r0, r1) of the fields `names` (r0 a multiple
+    of 64; the last chunk runs to the field's 64-float padded end)."""
+    from .cloud import _ROW
+    out = []
+    for f in sorted(names, key=lambda f: layout[f][0]):
+        off, size = layout[f]
+        w = int(np.prod(_ROW[f]))
+        end = off + (size + 63) // 64 * 64 if r1 >= n else off + r1 * w
+        out.append((off + r0 * w, end))
+    return out
+
+
 class DensifyStats:
     """Densification statistics (TrainState.grad_accum / grad_count / area_max,
     training.py:116-135, updated per view at training.py:333-338): the sum of the
@@ -122,6 +135,13 @@ class Trainer:
         # the exact blend-decision records of the step's views are computed here while the
         # first views' depth sorts run (only the blends read them)
         self.exact_stream = torch.cuda.Stream(device=cloud.device)
+        # one GPU: the preprocess backward may run in row chunks, each chunk's Adam on
+        # adam_stream beside the next chunk (TGS_BWD_CHUNKS).  Default 1: measured no gain at
+        # c3 (113.3 step/s for 1, 2, 4 and 8 chunks) — the backward's 3 CTAs x 128 threads x
+        # 160 registers fill the register file, so no Adam block co-resides
+        import os
+        self.bwd_chunks = int(os.environ.get("TGS_BWD_CHUNKS", "1"))
+        self.adam_stream = torch.cuda.Stream(device=cloud.device)
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
@@ -394,9 +414,6 @@ class Trainer:
         main.wait_stream(self.exact_stream)
         if copied:
             main.wait_stream(self.copy_stream)
-        # one pass over the parameters for all views (linear chains summed first)
-        preprocess_backward_views(self.cloud, [self.cameras[v] for v in self.views], self.settings, vis, parts, g,
-                                  accumulate=False, stats=self.stats, clear=self.clear_partials)
         steps_before = dict(self.opt.steps)
         cam0 = self.cameras[self.views[0]] if self.views else None
         res = (int(cam0.height), int(cam0.width)) if cam0 is not None else (0, 0)
@@ -406,6 +423,29 @@ class Trainer:
         upd = set(PARAM_FIELDS)
         if not (self.settings.compute_sh_rest_grads and self.settings.active_sh_degree > 0):
             upd.discard("sh_rest")
+        vcams = [self.cameras[v] for v in self.views]
+        if self.pg is None and self.zero_sim is None and self.bwd_chunks > 1 and n >= 64 * self.bwd_chunks:
+            # one GPU: the multi-view preprocess backward in row chunks on the main stream, and
+            # each chunk's Adam (all groups, the chunk's rows) on a side stream as soon as
+            # the chunk is done — the HBM-bound Adam overlaps the latency-bound backward
+            self.adam_stream.wait_stream(main)
+            per = -(-n // self.bwd_chunks)
+            per = -(-per // 64) * 64
+            for k, r0 in enumerate(range(0, n, per)):
+                r1 = min(n, r0 + per)
+                preprocess_backward_views(self.cloud, vcams, self.settings, vis, parts, g, accumulate=False,
+                                          stats=self.stats, clear=self.clear_partials, rows=(r0, r1))
+                done = torch.cuda.Event()
+                done.record(main)
+                self.adam_stream.wait_event(done)
+                with stage("adam"), torch.cuda.stream(self.adam_stream):
+                    self.opt.step(self.cloud, g, names=tuple(upd), lambda_m=self.lambda_m, lambda_sh=self.lambda_sh,
+                                  guard=guard, ranges=_row_ranges(g._layout_map, upd, n, r0, r1), count=k == 0)
+            main.wait_stream(self.adam_stream)
+            return self._finish(main, steps_before, n, res)
+        # one pass over the parameters for all views (linear chains summed first)
+        preprocess_backward_views(self.cloud, vcams, self.settings, vis, parts, g,
+                                  accumulate=False, stats=self.stats, clear=self.clear_partials)
         if self.zero_sim is not None or (self.pg is not None and self.dp_mode == "zero"):
             return self._zero_update(main, g, upd, guard, steps_before, n, res)
         if self.pg is None:
