@@ -244,12 +244,21 @@ TGS_API int tgs_bin_instances(const float *splats, int64_t n, int32_t width, int
  * (H, W) int32 (_kernels.py:83-89); hits (n,) int32 or NULL (record_hits).
  * Only pixels of tile rows [row_begin, row_end) are written.  exact (n, 8) or
  * NULL: the preprocess's exact blend-decision records (TGS_EXACT_FLOATS); every
- * blend entry point takes the same records and decides identically. */
+ * blend entry point takes the same records and decides identically.
+ * exceptions / exc_overflow (tile_size 16 with exact records; both NULL or both
+ * set): the forward's blend exceptions, handed to tgs_blend_backward so it
+ * decides the rare bracket pairs without float64 — exceptions (H, W) int32
+ * (the 1-based list position a pixel's float64 resolution blended, 0 = none),
+ * exc_overflow TGS_EXC_OVERFLOW_WORDS(ntiles) uint32 (zeroed here: [count, flag per
+ * tile] of the tiles whose pixels need more, which the backward re-resolves in float64),
+ * ntiles = tiles in rows [row_begin, row_end). */
+#define TGS_EXC_OVERFLOW_WORDS(ntiles) (1 + (size_t)(ntiles))
 TGS_API int tgs_blend_forward(const float *splats, const float *exact, const int32_t *tile_offsets,
                       const int32_t *sorted_ids,
                       const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                       float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
-                      int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream);
+                      int32_t *last_pos, int32_t *hits, int32_t *exceptions, uint32_t *exc_overflow,
+                      const int32_t *tile_order, tgs_stream_t stream);
 
 /* Per-pixel ordered (Gaussian, blend weight) records — the reference's
  * records_kernel (_kernels.py:184-241), a test/debug payload.  pixel_offsets
@@ -261,11 +270,13 @@ TGS_API int tgs_blend_records(const float *splats, const float *exact, const int
                       int32_t *rec_gauss, float *rec_weight, tgs_stream_t stream);
 
 /* ---- (4) backward blend -----------------------------------------------------
- * dsplats (n, 9) is ACCUMULATED into (caller zeroes it). dimage (H, W, 3). */
+ * dsplats (n, 9) is ACCUMULATED into (caller zeroes it). dimage (H, W, 3).
+ * exceptions / exc_overflow: the forward's (same rows and records), or NULL. */
 TGS_API int tgs_blend_backward(const float *splats, const float *exact, const int32_t *tile_offsets,
                       const int32_t *sorted_ids,
                        const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
-                       const float *transmit, const int32_t *last_pos, const float *dimage,
+                       const float *transmit, const int32_t *last_pos, const int32_t *exceptions,
+                       const uint32_t *exc_overflow, const float *dimage,
                        float *dsplats, const int32_t *tile_order, tgs_stream_t stream);
 
 /* Heaviest-first tile order for the blend launches (tile_order above, may be
@@ -420,7 +431,9 @@ typedef struct {
  * mean SSIM into terms[0..1]; `loss_workspace` of tgs_loss_workspace bytes — views on
  * one stream may share dimage and workspace) and the blend backward into `dsplats`
  * (n, 9), accumulated.  target_ready (a cudaEvent_t, may be NULL): waited on before the
- * loss (a host-to-device copy of the target on another stream). */
+ * loss (a host-to-device copy of the target on another stream).  exceptions /
+ * exc_overflow (may be NULL; views on one stream may share them): the blend exception
+ * buffers tgs_blend_forward hands its backward (with exact records). */
 typedef struct {
   const float *target;
   float *dimage;
@@ -428,6 +441,8 @@ typedef struct {
   float *dsplats;
   void *loss_workspace;
   void *target_ready;
+  int32_t *exceptions;
+  uint32_t *exc_overflow;
 } tgs_view_train;
 
 TGS_API int tgs_render_views_workspace(int64_t n, int64_t max_instances, int32_t width, int32_t height,

@@ -59,7 +59,7 @@ class TgsViewTarget(ctypes.Structure):
 
 class TgsViewTrain(ctypes.Structure):
     _fields_ = [("target", _P), ("dimage", _P), ("terms", _P), ("dsplats", _P), ("loss_workspace", _P),
-                ("target_ready", _P)]
+                ("target_ready", _P), ("exceptions", _P), ("exc_overflow", _P)]
 
 
 class TgsGrads(ctypes.Structure):
@@ -81,14 +81,14 @@ _SIGS = {
     "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),
-    "tgs_blend_forward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_forward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_tile_order": ([_P, _I32, _P, _P], _I32),
     "tgs_debug_exact_pairs": ([_P, _I32], _I32),
     "tgs_blend_records": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_blend_backward_deterministic_workspace": ([_I64, _I64, _P], _I32),
     "tgs_blend_backward_deterministic": ([_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P, _P,
                                           _P], _I32),
-    "tgs_blend_backward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "tgs_blend_backward": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "tgs_preprocess_backward": ([_P, _P, _P, _P, _P, _P, _I32, _P], _I32),
     "tgs_preprocess_backward_views": ([_P, _P, _P, _P, _P, _I32, _P, _I32, _P, _I32, _P], _I32),
     "tgs_loss_workspace": ([_I32, _I32, _P], _I32),

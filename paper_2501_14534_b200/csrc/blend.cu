@@ -690,13 +690,23 @@ struct Fwd16Pair {
          c2 = make_float2(0.f, 0.f), ws = make_float2(0.f, 0.f);
   float2 cnt = make_float2(0.f, 0.f);  // n_contrib of both pixels, counted in one FADD2 (exact < 2^24)
   int lA = 0, lB = 0;
+  // blend exception (exact decisions): the 1-based list position pos where the float64
+  // resolution blended a pair the certain rule (e2 >= cut_hi) skips, one per lane, as
+  // 2 pos + (pixel B); -1: a second one, or a clamped one (the tile's backward then
+  // re-resolves its bracket pairs in float64 instead).  One register for both pixels.
+  int ex = 0;
   bool dA, dB;
 };
+
+__device__ __forceinline__ void note_exception(int &ex, int pos, int pixel_b, bool unclamped) {
+  ex = !unclamped || ex ? -1 : 2 * pos + pixel_b;
+}
 
 template <bool kExact, bool kHits>
 __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
                                            float2 cut, int pos, int32_t *hits, int32_t gid,
-                                           const float4 *__restrict__ splats, const float4 *__restrict__ exact) {
+                                           const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+                                           const int32_t *exc) {
   // checked before each entry (_kernels.py:57-58)
   P.dA = P.dA || P.T.x < kTTerm;
   P.dB = P.dB || P.T.y < kTTerm;
@@ -716,8 +726,14 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
     const bool uA = !P.dA && !(e2.x >= cut.y) && e2.x >= cut.x, uB = !P.dB && !(e2.y >= cut.y) && e2.y >= cut.x;
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
-    if (uA && (r & 1)) al.x = fminf(a_raw.x, kAlphaMax);
-    if (uB && (r & 4)) al.y = fminf(a_raw.y, kAlphaMax);
+    if (uA && (r & 1)) {
+      al.x = fminf(a_raw.x, kAlphaMax);
+      if (exc) note_exception(P.ex, pos, 0, (r & 2) != 0);
+    }
+    if (uB && (r & 4)) {
+      al.y = fminf(a_raw.y, kAlphaMax);
+      if (exc) note_exception(P.ex, pos, 1, (r & 8) != 0);
+    }
   }
   const bool okA = al.x > 0.0f, okB = al.y > 0.0f;
   const float2 w = __fmul2_rn(al, P.T);
@@ -868,7 +884,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
     float *__restrict__ transmit, float *__restrict__ wsum_out, int32_t *__restrict__ n_contrib,
-    int32_t *__restrict__ last_pos, int32_t *__restrict__ hits, const int32_t *__restrict__ order) {
+    int32_t *__restrict__ last_pos, int32_t *__restrict__ hits, const int32_t *__restrict__ order,
+    int32_t *__restrict__ exc, uint32_t *__restrict__ ovf) {
   __shared__ WStage SW[kT16Threads / 32];
   const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
@@ -915,7 +932,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
       fwd_visit2<kExact, kHits>(P, fpx, fy, m, q, col, S.cut[k], pos, hits, kHits || kExact ? S.id[k] : 0, splats,
-                                exact);
+                                exact, exc);
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
@@ -930,6 +947,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.x;
     n_contrib[p] = (int32_t)P.cnt.x;
     last_pos[p] = P.lA;
+    if (kExact && exc) exc[p] = P.ex > 0 && !(P.ex & 1) ? P.ex >> 1 : 0;
   }
   if (inB) {
     const int p = pyB * W + px;
@@ -940,7 +958,12 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.y;
     n_contrib[p] = (int32_t)P.cnt.y;
     last_pos[p] = P.lB;
+    if (kExact && exc) exc[p] = P.ex > 0 && (P.ex & 1) ? P.ex >> 1 : 0;
   }
+  // a tile with an exception the lists cannot carry: flagged (and counted) once, for the
+  // backward to re-resolve its bracket pairs in float64 (ovf = [count, flags[ntiles]])
+  if (kExact && exc && __any_sync(0xffffffffu, P.ex < 0) && lane == 0)
+    if (atomicCAS(ovf + 1 + tile, 0u, 1u) == 0u) atomicAdd(ovf, 1u);
 }
 
 template <bool kExact>
@@ -1060,6 +1083,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_bl
 template <int kP>
 struct BwdLane {
   int l[2 * kP];                                      // last_pos per pixel
+  int e[2 * kP];                                      // blend exception (kExc), 1-based position
   float2 g0[kP], g1[kP], g2[kP], T[kP], GS[kP];       // per pair: (pixel 2h, pixel 2h+1)
 };
 
@@ -1088,7 +1112,7 @@ __device__ __noinline__ int resolveP(const float4 *__restrict__ splats, const fl
   return r;
 }
 
-template <bool kExact, int kP>
+template <bool kExact, int kP, bool kExc>
 __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, const float2 fy[kP], float2 m,
                                            float4 q, float4 cn, float4 col, float2 cut, int32_t gid,
                                            const float4 *__restrict__ splats, const float4 *__restrict__ exact,
@@ -1108,12 +1132,16 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     // exactly 1, T and G.S stay unchanged); gm: 1 where the partials through alpha apply
     // (unclamped a_raw <= 0.99; with exact records a clampable Gaussian goes to exact_pair,
     // so every certain pair is unclamped) — no boolean has to live across the rare branch
-    alm[h] = make_float2(pos < P.l[2 * h] && e2[h].x >= cut.y ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
-                         pos < P.l[2 * h + 1] && e2[h].y >= cut.y ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
+    // With the forward's exception lists (kExc) a bracket pair blends iff the forward
+    // resolved it to blend, i.e. it is the pixel's recorded exception: no float64 here.
+    const bool bx = e2[h].x >= cut.y || (kExc && pos + 1 == P.e[2 * h]);
+    const bool by = e2[h].y >= cut.y || (kExc && pos + 1 == P.e[2 * h + 1]);
+    alm[h] = make_float2(pos < P.l[2 * h] && bx ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
+                         pos < P.l[2 * h + 1] && by ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
     gm[h] = make_float2(alm[h].x > 0.0f && (kExact || a_raw[h].x <= kAlphaMax) ? 1.0f : 0.0f,
                         alm[h].y > 0.0f && (kExact || a_raw[h].y <= kAlphaMax) ? 1.0f : 0.0f);
   }
-  if (kExact) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
+  if (kExact && !kExc) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
     float pm = 1.0f;
 #pragma unroll
     for (int h = 0; h < kP; ++h) {
@@ -1182,14 +1210,15 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
   return hitm > 0.0f;
 }
 
-template <bool kExact, int kP>
-__global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_blend_bwd16p(
-    const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets,
-    const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2,
-    const float *__restrict__ transmit, const int32_t *__restrict__ last_pos, const float *__restrict__ dimage,
-    float *__restrict__ dsplats, const int32_t *__restrict__ order) {
-  __shared__ WStage SW[4 / kP];
-  const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+// One tile of the backward.  Exact decisions come in two modes: kExc, the forward's
+// exception lists decide the bracket pairs (pos + 1 == exc[pixel], no float64); !kExc,
+// the bracket pairs are re-resolved in float64 (resolveP).
+template <bool kExact, int kP, bool kExc>
+__device__ __forceinline__ void bwd16p_tile(
+    WStage *SW, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+    const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin,
+    float bg0, float bg1, float bg2, const float *__restrict__ transmit, const int32_t *__restrict__ last_pos,
+    const float *__restrict__ dimage, float *__restrict__ dsplats, const int32_t *__restrict__ exc) {
   const int ty = row_begin + tile / tiles_x, tx = tile % tiles_x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WStage &S = SW[warp];
@@ -1202,11 +1231,12 @@ __global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_
   int x0 = 0x7fffffff, x1 = -0x7fffffff, y0 = 0x7fffffff, y1 = -0x7fffffff;  // this lane's live box
 #pragma unroll
   for (int k = 0; k < 2 * kP; ++k) {
-    int lp = 0;
+    int lp = 0, ex = 0;
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, T = 0.f;
     if (px < W && py[k] < H) {
       const int p = py[k] * W + px;
       lp = last_pos[p];
+      if (kExc) ex = exc[p];
       g0 = dimage[3 * p];
       g1 = dimage[3 * p + 1];
       g2 = dimage[3 * p + 2];
@@ -1214,6 +1244,7 @@ __global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_
       T = transmit[p];
     }
     P.l[k] = lp;
+    P.e[k] = ex;
     const float GS = (g0 * bg0 + g1 * bg1 + g2 * bg2) * T;
     if (k & 1) {
       P.g0[k >> 1].y = g0; P.g1[k >> 1].y = g1; P.g2[k >> 1].y = g2; P.T[k >> 1].y = T; P.GS[k >> 1].y = GS;
@@ -1265,13 +1296,13 @@ __global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_
       float v0[9], v1[9];
       const int b0 = 31 - __clz(mask);
       mask &= ~(1u << b0);
-      bool hit = bwd_visitP<kExact, kP>(P, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], S.cut[b0],
+      bool hit = bwd_visitP<kExact, kP, kExc>(P, lo + b0, fpx, fy, S.xy[b0], S.q[b0], S.conic[b0], S.col[b0], S.cut[b0],
                                         S.id[b0], splats, exact, v0);
       int id1 = -1;
       if (mask) {  // warp-uniform
         const int b1 = 31 - __clz(mask);
         mask &= ~(1u << b1);
-        hit = bwd_visitP<kExact, kP>(P, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], S.cut[b1],
+        hit = bwd_visitP<kExact, kP, kExc>(P, lo + b1, fpx, fy, S.xy[b1], S.q[b1], S.conic[b1], S.col[b1], S.cut[b1],
                                      S.id[b1], splats, exact, v1) || hit;
         id1 = S.id[b1];
       } else {
@@ -1297,6 +1328,43 @@ __global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_
     }
     __syncwarp();
   }
+}
+
+#ifdef TGS_BWD_CHK_NOINLINE  // A/B builds: the float64-resolving tile body out of line
+template <bool kExact, int kP>
+__device__ __noinline__ void bwd16p_tile_chk(
+    WStage *SW, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+    const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin,
+    float bg0, float bg1, float bg2, const float *__restrict__ transmit, const int32_t *__restrict__ last_pos,
+    const float *__restrict__ dimage, float *__restrict__ dsplats) {
+  bwd16p_tile<kExact, kP, false>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+                                 transmit, last_pos, dimage, dsplats, nullptr);
+}
+#endif
+
+// With exception lists (exc != NULL) a tile the forward flagged in ovf (a pixel with two
+// exceptions, or a clamped one) takes the float64-resolving body instead — in the same
+// launch, so the few flagged tiles (4-16 of 8,160 per c3 view) add no serial tail.
+template <bool kExact, int kP>
+__global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_blend_bwd16p(
+    const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets,
+    const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2,
+    const float *__restrict__ transmit, const int32_t *__restrict__ last_pos, const float *__restrict__ dimage,
+    float *__restrict__ dsplats, const int32_t *__restrict__ order, const int32_t *__restrict__ exc,
+    const uint32_t *__restrict__ ovf) {
+  __shared__ WStage SW[4 / kP];
+  const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  if (kExact && exc && !__ldg(ovf + 1 + tile))
+    bwd16p_tile<kExact, kP, true>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+                                  transmit, last_pos, dimage, dsplats, exc);
+  else
+#ifdef TGS_BWD_CHK_NOINLINE
+    bwd16p_tile_chk<kExact, kP>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+                                transmit, last_pos, dimage, dsplats);
+#else
+    bwd16p_tile<kExact, kP, false>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+                                   transmit, last_pos, dimage, dsplats, nullptr);
+#endif
 }
 
 // _kernels.py:184-241: same walk as the forward, writing (gid, a*T) per blended entry
@@ -1416,19 +1484,25 @@ extern "C" int tgs_blend_forward(const float *splats, const float *exact, const 
                                  const int32_t *sorted_ids,
                                  const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
                                  float *image, float *transmit, float *weight_sum, int32_t *n_contrib,
-                                 int32_t *last_pos, int32_t *hits, const int32_t *tile_order, tgs_stream_t stream) {
+                                 int32_t *last_pos, int32_t *hits, int32_t *exceptions, uint32_t *exc_overflow,
+                                 const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
+  if (!exceptions != !exc_overflow || (exceptions && (!exact || s->tile_size != 16))) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   const float4 *ex = reinterpret_cast<const float4 *>(exact);
+  if (exc_overflow) {
+    const cudaError_t e = cudaMemsetAsync(exc_overflow, 0, (1 + (size_t)ntiles) * sizeof(uint32_t), as_stream(stream));
+    if (e != cudaSuccess) return cuda_status(e);
+  }
   if (s->tile_size == 16) {
     auto kern = ex ? (hits ? k_blend_fwd16w<true, true> : k_blend_fwd16w<true, false>)
                    : (hits ? k_blend_fwd16w<false, true> : k_blend_fwd16w<false, false>);
     kern<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
-        last_pos, hits, tile_order);
+        last_pos, hits, tile_order, exceptions, exc_overflow);
     return launch_status();
   }
   const int B = (s->tile_size * s->tile_size + 31) / 32 * 32;  // whole warps; extra lanes are idle pixels
@@ -1460,19 +1534,23 @@ extern "C" int tgs_blend_records(const float *splats, const float *exact, const 
 extern "C" int tgs_blend_backward(const float *splats, const float *exact, const int32_t *tile_offsets,
                                   const int32_t *sorted_ids,
                                   const tgs_camera *cam, const tgs_settings *s, int32_t row_begin, int32_t row_end,
-                                  const float *transmit, const int32_t *last_pos, const float *dimage,
+                                  const float *transmit, const int32_t *last_pos, const int32_t *exceptions,
+                                  const uint32_t *exc_overflow, const float *dimage,
                                   float *dsplats, const int32_t *tile_order, tgs_stream_t stream) {
   int tiles_x, ntiles;
   if (!blend_args(cam, s, row_begin, row_end, tiles_x, ntiles)) return TGS_ERR_INVALID;
   if ((reinterpret_cast<uintptr_t>(splats) | reinterpret_cast<uintptr_t>(exact)) & 15) return TGS_ERR_INVALID;
+  if (!exceptions != !exc_overflow || (exceptions && (!exact || s->tile_size != 16))) return TGS_ERR_INVALID;
   if (ntiles == 0) return TGS_OK;
   const float4 *ex = reinterpret_cast<const float4 *>(exact);
   if (s->tile_size == 16) {
 #if TGS_BWD16_PAIRS == 2
-    (ex ? k_blend_bwd16p<true, 2> : k_blend_bwd16p<false, 2>)<<<ntiles, 64, 0, as_stream(stream)>>>(
-        reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
-        row_begin, s->background[0], s->background[1], s->background[2], transmit, last_pos, dimage, dsplats,
-        tile_order);
+    cudaStream_t st = as_stream(stream);
+    const float4 *sp = reinterpret_cast<const float4 *>(splats);
+    (ex ? k_blend_bwd16p<true, 2> : k_blend_bwd16p<false, 2>)<<<ntiles, 64, 0, st>>>(
+        sp, ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x, row_begin, s->background[0],
+        s->background[1], s->background[2], transmit, last_pos, dimage, dsplats, tile_order, exceptions,
+        exc_overflow);
     return launch_status();
 #endif
     (ex ? k_blend_bwd16w<true> : k_blend_bwd16w<false>)<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(

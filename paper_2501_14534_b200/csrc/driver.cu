@@ -180,16 +180,21 @@ int run_views(const Batch &B) {
     }
     if (ex_ready) cudaStreamWaitEvent(stream(bs), ex_ready, 0);
     const float *ex = B.exact ? B.exact[v] : nullptr;
+    const tgs_view_train *tr_ = B.train ? &B.train[v] : nullptr;
+    int32_t *exc = tr_ && ex ? tr_->exceptions : nullptr;
+    uint32_t *ovf = exc ? tr_->exc_overflow : nullptr;
+    if (!ovf) exc = nullptr;
     int r = tgs_blend_forward(B.splats[v], ex, t.tile_offsets, t.sorted_ids, &cams[v], B.s, rb_of(v), rows_of(v),
-                              t.image, t.transmit, t.weight_sum, t.n_contrib, t.last_pos, t.hits, t.tile_order, bs);
+                              t.image, t.transmit, t.weight_sum, t.n_contrib, t.last_pos, t.hits, exc, ovf,
+                              t.tile_order, bs);
     if (r != TGS_OK || !B.train) return r;
-    const tgs_view_train &tr = B.train[v];
+    const tgs_view_train &tr = *tr_;
     if (tr.target_ready) cudaStreamWaitEvent(stream(bs), static_cast<cudaEvent_t>(tr.target_ready), 0);
     r = tgs_loss_l1_ssim(t.image, tr.target, cams[v].width, cams[v].height, B.lambda_ssim, tr.dimage, tr.terms,
                          tr.loss_workspace, bs);
     if (r != TGS_OK) return r;
     return tgs_blend_backward(B.splats[v], ex, t.tile_offsets, t.sorted_ids, &cams[v], B.s, rb_of(v), rows_of(v),
-                              t.transmit, t.last_pos, tr.dimage, tr.dsplats, t.tile_order, bs);
+                              t.transmit, t.last_pos, exc, ovf, tr.dimage, tr.dsplats, t.tile_order, bs);
   };
   // Per stream k the queue is  bin_instances(v) -> bin_gaussians(v + nstreams) -> blend(v):
   // the next same-stream view's depth sort runs BEFORE this view's blend, so its count

@@ -88,6 +88,8 @@ class _DeviceState:
     depth_keys: torch.Tensor | None
     bins: TileBins
     exact: torch.Tensor | None = None  # (N, 8) exact blend-decision records (include/tgs.h TGS_EXACT_FLOATS)
+    exceptions: torch.Tensor | None = None    # (H, W) int32 blend exceptions of the forward (tgs_blend_forward)
+    exc_overflow: torch.Tensor | None = None  # TGS_EXC_OVERFLOW_WORDS(ntiles) int32 (uint32 words)
 
 
 @dataclass
@@ -116,6 +118,10 @@ def sh_rest_update_step(iteration: int, cadence: int) -> bool:
 
 def _tiles_y(cam, ts):
     return (cam.height + ts - 1) // ts
+
+
+def _tiles_x(cam, ts):
+    return (cam.width + ts - 1) // ts
 
 
 @dataclass
@@ -229,6 +235,10 @@ BLEND_ORDER = "center"
 # the decision cost only — the north-star parity needs the records).
 import os as _os
 EXACT_DECISIONS = _os.environ.get("TGS_EXACT", "1") != "0"
+# The blend forward's exception lists (tgs_blend_forward `exceptions`): the backward then
+# decides the bracket pairs without float64.  TGS_EXC=0: the backward re-resolves them
+# (A/B timing; same results).
+EXCEPTION_LISTS = EXACT_DECISIONS and _os.environ.get("TGS_EXC", "1") != "0"
 
 
 def _ex(exact):
@@ -628,20 +638,24 @@ def render_forward(cloud, cam: Camera, settings: RenderSettings, row_band: tuple
         for t_, v in ((image, 0.0), (transmit, 1.0), (wsum, 0.0), (n_contrib, 0), (last_pos, 0)):
             t_.fill_(v)
     hits = torch.zeros(max(n, 1), dtype=torch.int32, device=dev) if settings.record_hits else None
+    exc = ovf = None
+    if EXCEPTION_LISTS and exact is not None and ts == 16:  # the backward's exception lists (include/tgs.h)
+        exc, ovf = _alloc_many([((h, w), torch.int32), ((1 + (re - rb) * _tiles_x(cam, ts),), torch.int32)], dev)
     c_cam = _lib.make_camera(cam)
     with stage("blend_fwd"):
         _lib.call("tgs_blend_forward", _lib.ptr(splats), _lib.ptr(_ex(exact)), _lib.ptr(bins.offsets),
                   _lib.ptr(bins.indices),
                   ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(image), _lib.ptr(transmit),
-                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.ptr(bins.order),
-                  cs.cuda_stream)
+                  _lib.ptr(wsum), _lib.ptr(n_contrib), _lib.ptr(last_pos), _lib.ptr(hits), _lib.ptr(exc),
+                  _lib.ptr(ovf), _lib.ptr(bins.order), cs.cuda_stream)
     hit_counts = None
     if hits is not None:
         hit_counts = bufs[5]
         hit_counts.copy_(hits[:n])
     out = RenderOutput(image=image, transmittance=transmit, weight_sum=wsum, n_contrib=n_contrib,
                        last_pos=last_pos, visible=visible, screen_areas=splats[:n, 11], hit_counts=hit_counts,
-                       _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins, exact))
+                       _tiles=bins, _state=_DeviceState(cloud.flat.data_ptr(), n, splats, vis, tiles, keys, bins, exact,
+                                                        exc, ovf))
     if settings.record_full:
         out.hit_records = _records(out, splats, exact, bins, cam, c_cam, c_set, dev)
     return out
@@ -713,7 +727,8 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
             _lib.call("tgs_blend_backward", _lib.ptr(st.splats), _lib.ptr(_ex(st.exact)), _lib.ptr(bins.offsets),
                       _lib.ptr(bins.indices),
                       ctypes.byref(c_cam), ctypes.byref(c_set), rb, re, _lib.ptr(transmit), _lib.ptr(last_pos),
-                      _lib.ptr(d), _lib.ptr(dsplats), _lib.ptr(bins.order), _lib.stream_handle(dev))
+                      _lib.ptr(st.exceptions), _lib.ptr(st.exc_overflow), _lib.ptr(d), _lib.ptr(dsplats),
+                      _lib.ptr(bins.order), _lib.stream_handle(dev))
     return dsplats, st
 
 

@@ -127,6 +127,7 @@ class Trainer:
         dev = cloud.device
         self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
         self.dimage = {}
+        self._exc_bufs = {}  # (stream, H, W) -> blend exception lists (native path)
         self.dsplats = {}
         # >= 2 streams pipeline consecutive views (4 by default: measured 118 / 121 / 123 step/s
         # with 2 / 3 / 4 at c3); 1 stream serialises them (per-kernel timing)
@@ -324,7 +325,7 @@ class Trainer:
         import ctypes
         from . import _lib
         from .errors import TGS_ERR_CAPACITY, raise_for_status
-        from .rasterizer import EXACT_DECISIONS, _blend_order, _scratch, _size_class, ctypes_size
+        from .rasterizer import EXACT_DECISIONS, EXCEPTION_LISTS, _blend_order, _scratch, _size_class, ctypes_size
         dev, n, ts = self.cloud.device, len(self.cloud), int(self.settings.tile_size)
         ns, V = len(self.streams), len(self.views)
         cams = [self.cameras[v] for v in self.views]
@@ -377,12 +378,19 @@ class Trainer:
                         d = self.dimage[(k, h, w)] = torch.empty((h, w, 3), device=dev)
                 lw = _scratch("loss", loss_mod._loss_bytes(w, h), dev, self.streams[k].cuda_stream, owner=self.streams[k])
                 loss_ws.append(lw)
+                xb = self._exc_bufs.get((k, h, w))  # the blend exception lists, shared per stream
+                if xb is None and EXCEPTION_LISTS and ts == 16:
+                    ntl = ((w + ts - 1) // ts) * ((h + ts - 1) // ts)
+                    with torch.cuda.stream(self.streams[k]):
+                        xb = self._exc_bufs[(k, h, w)] = (torch.empty((h, w), dtype=torch.int32, device=dev),
+                                                          torch.empty(1 + ntl, dtype=torch.int32, device=dev))
                 targets[i] = _lib.TgsViewTarget(b["off"].data_ptr(), b["ids"].data_ptr(), cap, _lib.ptr(b["order"]),
                                                 b["image"].data_ptr(), b["T"].data_ptr(), b["ws"].data_ptr(),
                                                 b["nc"].data_ptr(), b["lp"].data_ptr(), None, -1, 0, 0)
                 train[i] = _lib.TgsViewTrain(self.targets[v].data_ptr(), d.data_ptr(), self.terms[v].data_ptr(),
                                              self.dsplats[v].data_ptr(), lw.data_ptr(),
-                                             copied[v].cuda_event if v in copied else None)
+                                             copied[v].cuda_event if v in copied else None,
+                                             _lib.ptr(xb[0]) if xb else None, _lib.ptr(xb[1]) if xb else None)
             with stage("train_views"):
                 rc = int(_lib.load().tgs_train_views(
                     ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0), arr(1), arr(2), arr(3),

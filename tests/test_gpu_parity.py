@@ -141,6 +141,45 @@ def test_c2_image_vs_fp64_oracle(tgs):
     np.testing.assert_allclose(_np(out.weight_sum) + _np(out.transmittance), 1.0, atol=1e-5)
 
 
+def test_blend_exception_lists_equal_float64_resolution(tgs):
+    """The backward deciding bracket pairs from the forward's exception lists gives the
+    same partials as re-resolving them in float64: at c2 with 2% clampable Gaussians
+    (alpha > 0.9899: every blended pair of theirs is resolved in float64), so both the
+    per-pixel exceptions and the overflow tiles (float64 body) are exercised; and with
+    every tile flagged."""
+    import dataclasses
+    from paper_2501_14534_b200 import scenes
+    sc = scenes.config2()
+    fields = dict(sc.fields)
+    rng = np.random.default_rng(11)
+    ol = fields["opacity_logits"].copy()
+    ol[rng.choice(ol.size, ol.size // 50, replace=False)] = 6.0
+    fields["opacity_logits"] = ol
+    st = tgs.RenderSettings(near=0.2)
+    cam = sc.cameras[0]
+    cloud = tgs.GaussianCloud.from_fields(fields)
+    out = tgs.render_forward(cloud, cam, st)
+    state = out._state
+    assert state.exceptions is not None and state.exc_overflow is not None
+    nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    ovf = _np(state.exc_overflow).view(np.uint32)
+    cnt, flags = int(ovf[0]), ovf[1:1 + nt]
+    assert 0 < cnt < nt and int(flags.sum()) == cnt and set(np.unique(flags)) <= {0, 1}
+    exc, lp = _np(state.exceptions), _np(out.last_pos)
+    assert (exc >= 0).all() and (exc <= lp).all()
+    assert (exc > 0).sum() > 0
+    dimg = torch.from_numpy(rng.standard_normal((cam.height, cam.width, 3)).astype(np.float32)).cuda()
+    ds_exc, _ = tgs.rasterizer.blend_backward(cloud, cam, st, dimg, out)
+    plain = dataclasses.replace(out, _state=dataclasses.replace(state, exceptions=None, exc_overflow=None))
+    ds_chk, _ = tgs.rasterizer.blend_backward(cloud, cam, st, dimg, plain)
+    a, b = _np(ds_exc), _np(ds_chk)
+    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    every = torch.from_numpy(np.concatenate([[nt], np.ones(nt)]).astype(np.int32)).cuda()
+    forced = dataclasses.replace(out, _state=dataclasses.replace(state, exc_overflow=every))
+    ds_all, _ = tgs.rasterizer.blend_backward(cloud, cam, st, dimg, forced)
+    np.testing.assert_allclose(_np(ds_all), b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+
+
 def test_c1_gradients_vs_fp64_oracle_full(tgs):
     """All N rows at c1 with an O(1) upstream gradient (dimage ~ N(0,1))."""
     from paper_2501_14534_b200 import scenes
@@ -807,7 +846,7 @@ def test_tile_order_is_a_heaviest_first_permutation_and_changes_nothing(tgs):
     _lib.call("tgs_blend_forward", _lib.ptr(out._state.splats), _lib.ptr(out._state.exact), _lib.ptr(bins.offsets),
               _lib.ptr(bins.indices),
               ctypes.byref(c_cam), ctypes.byref(c_set), 0, bins.tiles_y, *[_lib.ptr(b) for b in bufs], None, None,
-              _lib.stream_handle())
+              None, None, _lib.stream_handle())
     for got, ref in zip(bufs, (out.image, out.transmittance, out.weight_sum, out.n_contrib, out.last_pos)):
         assert torch.equal(got, ref)
     # random offsets with empty tiles and a single huge tile
