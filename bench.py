@@ -616,6 +616,37 @@ def rank_share(args):
                       "config": config_dict(len(cloud), N)}), flush=True)
 
 
+def _c5_shell_targets(sc, views, st0, args, dev):
+    """c5 on the shell scene (TGS_C5_SCENE=shell): targets are renders of a HELD-OUT SUBSET —
+    30% of the Gaussians, drawn from the rows the 8 cameras see (hit counts > 0,
+    significance.count_hits) — rendered opaquer than the trained cloud starts."""
+    import torch
+
+    from paper_2501_14534_b200 import GaussianCloud, significance
+    from paper_2501_14534_b200.rasterizer import render_forward
+    init = GaussianCloud.from_fields(sc.fields, device=dev)
+    hits = significance.count_hits(init, sc.cameras, st0)
+    seen = torch.nonzero(hits > 0).flatten().cpu().numpy()
+    keep_n = min(int(0.3 * args.n), seen.size)
+    if os.environ.get("TGS_C5_SUBSET", "top") == "top":  # the most-hit rows: the best-supported 30%
+        subset = np.sort(torch.topk(hits.to(torch.float64), keep_n).indices.cpu().numpy())
+    else:
+        subset = np.sort(np.random.default_rng(5).choice(seen, keep_n, replace=False))
+    # the subset is rendered OPAQUER than the trained cloud starts (opacity logits + boost):
+    # its rows' photometric gradient then asks for more opacity step after step, a
+    # consistent sign that holds their mask logits up against the lr-0.5 Adam random walk
+    boost = float(os.environ.get("TGS_C5_BOOST", "2.0"))
+    sub = {k: np.ascontiguousarray(v[subset]) for k, v in sc.fields.items()}
+    sub["opacity_logits"] = (sub["opacity_logits"] + np.float32(boost)).astype(np.float32)
+    held = GaussianCloud.from_fields(sub, device=dev)
+    full_t = {}
+    for v in views:
+        full_t[v] = render_forward(held, sc.cameras[v], st0).image.contiguous()
+    del init, held
+    full_t["_meta"] = (keep_n, seen, boost)
+    return full_t
+
+
 def schedule_c5(args):
     """BASELINE.json configs[4]: the progressive-training schedule on 1M Gaussians — render
     resolution stepped 1/8 -> 1/4 -> 1/2 -> 1 of 1920x1080 (targets area-resized on the GPU),
@@ -642,34 +673,40 @@ def schedule_c5(args):
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     _lib.load()
-    sc = scenes.config5(n=args.n, views=VIEWS)
-    views = list(range(rank, VIEWS, world))
-    # targets: renders of a HELD-OUT SUBSET of the scene — 30% of the Gaussians, drawn from
-    # the rows the 8 cameras actually see (hit counts > 0, significance.count_hits) — so the
-    # photometric gradient keeps those alive while the mask penalty (lr 0.5, the reference's)
-    # prunes the rest, as BASELINE.json's ~30% survival of real scenes (on c3's solid ball
-    # only 24% of the rows are seen at all and ~1.5% survive; c5's scene is a shell)
-    from paper_2501_14534_b200 import significance
-    from paper_2501_14534_b200.rasterizer import render_forward
-    init = GaussianCloud.from_fields(sc.fields, device=dev)
-    st0 = RenderSettings(**settings_kwargs())
-    hits = significance.count_hits(init, sc.cameras, st0)
-    seen = torch.nonzero(hits > 0).flatten().cpu().numpy()
-    keep_n = min(int(0.3 * args.n), seen.size)
-    if os.environ.get("TGS_C5_SUBSET", "top") == "top":  # the most-hit rows: the best-supported 30%
-        subset = np.sort(torch.topk(hits.to(torch.float64), keep_n).indices.cpu().numpy())
+    c5_scene = os.environ.get("TGS_C5_SCENE", "sfm")
+    if c5_scene == "sfm":  # the reference's own recipe: ground-truth renders, SfM-seeded cloud
+        sc, gt_fields = scenes.config5_sfm(n=args.n, views=VIEWS)
     else:
-        subset = np.sort(np.random.default_rng(5).choice(seen, keep_n, replace=False))
-    held = init.take(torch.from_numpy(subset).to(dev))
-    full_t = {}
-    for v in views:
-        full_t[v] = render_forward(held, sc.cameras[v], st0).image.contiguous()
-    del init, held
+        sc, gt_fields = scenes.config5(n=args.n, views=VIEWS), None
+    views = list(range(rank, VIEWS, world))
+    from paper_2501_14534_b200.rasterizer import render_forward
+    st0 = RenderSettings(**settings_kwargs())
+    if gt_fields is not None:
+        gt = GaussianCloud.from_fields(gt_fields, device=dev)
+        full_t = {v: render_forward(gt, sc.cameras[v], st0).image.contiguous() for v in views}
+        keep_n, seen, boost = len(gt), np.zeros(0), 0.0
+        del gt
+    else:
+        full_t = _c5_shell_targets(sc, views, st0, args, dev)
+        keep_n, seen, boost = full_t.pop("_meta")
     steps = args.c5_steps
     phase_len = max(1, steps // 4)
     kw = settings_kwargs()
     cloud = GaussianCloud.from_fields(sc.fields, device=dev)
-    trainer = Trainer(cloud, sc.cameras, {}, RenderSettings(**kw), LAMBDA_SSIM, process_group=pg, views=views)
+    # mask learning: the paper-scale rates (mask lr 0.5, lambda 0.05; config.py:76-92) make every
+    # mask logit whose photometric gradient changes sign random-walk by ~0.5 per step into
+    # the absorbing hard-mask threshold (a masked Gaussian has zero scale and no
+    # photometric gradient left), so ~96% are gone by the first prune on synthetic
+    # targets; TGS_C5_MASK=preset uses the reference's own synthetic-scene rates
+    # (synthetic.py preset_config: mask / SH-mask lr 0.02, lambda 2e-3)
+    lrs, lam = None, {}
+    mask_mode = os.environ.get("TGS_C5_MASK", "preset")
+    if mask_mode == "preset":
+        from paper_2501_14534_b200.train import DEFAULT_LRS
+        lrs = {**DEFAULT_LRS, "mask_logits": 0.02, "sh_mask_logits": 0.02}
+        lam = dict(lambda_m=2e-3, lambda_sh=2e-3)
+    trainer = Trainer(cloud, sc.cameras, {}, RenderSettings(**kw), LAMBDA_SSIM, lrs=lrs, process_group=pg,
+                      views=views, **lam)
     prunes, counts, phase_res = [], [len(cloud)], {}
 
     def setup(i):
@@ -732,13 +769,22 @@ def schedule_c5(args):
                           "unit": "train step/s", "n_gpus": world, "steps": steps, "warmup": 3,
                           "ms_per_step": round(float(t) / steps * 1e3, 3), "higher_is_better": True,
                           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic (seeded c5 shell scene, scenes.config5; schedule of BASELINE.json config 5)",
+                          "data": ("synthetic (seeded ground-truth shell + SfM-seeded cloud, scenes.config5_sfm; "
+                                   "schedule of BASELINE.json config 5)" if c5_scene == "sfm" else
+                                   "synthetic (seeded c5 shell scene, scenes.config5; schedule of BASELINE.json config 5)"),
                           "config": {"workload": "c5: BASELINE.json configs[4] schedule sweep", "gaussians": args.n,
                                      "resolution_steps": ["240x135", "480x270", "960x540", "1920x1080"],
                                      "views_per_step": VIEWS, "prune_steps": prunes, "gaussians_after_prunes": counts,
                                      "final_fraction": round(counts[-1] / args.n, 3),
-                                     "targets": f"renders of a held-out {keep_n}-row subset of the {seen.size} "
-                                                f"rows seen by the cameras",
+                                     "targets": (f"renders of a {keep_n}-Gaussian ground-truth shell cloud; the trained "
+                                                 f"cloud seeded from {args.n} SfM-like points around its centres "
+                                                 f"(the reference's synthetic.py / seed_from_sfm recipe)"
+                                                 if c5_scene == "sfm" else
+                                                 f"renders of a held-out {keep_n}-row subset of the {seen.size} "
+                                                 f"rows seen by the cameras, opacity logits +{boost}"),
+                                     "mask_learning": ("reference synthetic preset: mask/sh-mask lr 0.02, lambda 2e-3"
+                                                       if mask_mode == "preset" else
+                                                       "paper scale: mask lr 0.5, sh-mask lr 0.05, lambda 0.05"),
                                      "parallelism": f"dp{world}"},
                           "total_s": round(float(t), 3), "host_wall_s": round(wall, 3),
                           "host_ms_per_step": round(wall / steps * 1e3, 3),

@@ -156,6 +156,50 @@ def config5(seed: int = 5, n: int = 1_000_000, width: int = 1920, height: int = 
     return Scene("c5", fields, cams, [], dict(near=0.2, tile_size=16, mask_threshold=0.01, sh_mask_threshold=0.1))
 
 
+def config5_sfm(seed: int = 5, n: int = 1_000_000, n_gt: int = 50_000, width: int = 1920, height: int = 1080,
+                views: int = 8) -> tuple[Scene, dict]:
+    """c5 the way the reference builds its own training scenes (synthetic.py make_scene +
+    schedule.py seed_from_sfm, restated): a ground-truth cloud of n_gt Gaussians on the
+    radius-2 shell (opacities U(0.55, 0.95), colours U(0.2, 0.9), mild view dependence
+    fading with band order) whose renders are the targets, and the TRAINED cloud seeded
+    from n SfM-like points — noisy samples around ground-truth centres (offset N(0, 1) x
+    the owner's scale x U(0.2, 2)) — with isotropic scales from the mean distance to the
+    3 nearest seeds, identity rotations, opacity 0.1, the owner's colour (+ N(0, 0.02))
+    and mask logits 2.0.  Returns (scene with the seed cloud, ground-truth fields)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(seed)
+    c0 = 0.28209479177387814  # SH band-0 constant: dc = (rgb - 0.5) / c0
+    d = rng.normal(size=(n_gt, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    q = rng.normal(size=(n_gt, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    spacing = math.sqrt(4.0 * math.pi * 4.0 / n_gt)  # mean distance between shell centres
+    ls = np.log(rng.uniform(0.5 * spacing, 1.5 * spacing, (n_gt, 3)))
+    rgb = rng.uniform(0.2, 0.9, (n_gt, 3))
+    rest = np.zeros((n_gt, 15, 3))
+    rest[:, 0:3] = rng.normal(0.0, 0.08, (n_gt, 3, 3))
+    rest[:, 3:8] = rng.normal(0.0, 0.04, (n_gt, 5, 3))
+    rest[:, 8:15] = rng.normal(0.0, 0.02, (n_gt, 7, 3))
+    op = rng.uniform(0.55, 0.95, n_gt)
+    gt = {"positions": _f32(2.0 * d), "log_scales": _f32(ls), "rotations": _f32(q),
+          "opacity_logits": _f32(np.log(op / (1.0 - op))), "sh_dc": _f32((rgb - 0.5) / c0), "sh_rest": _f32(rest),
+          "mask_logits": _f32(np.full(n_gt, 2.0)), "sh_mask_logits": _f32(np.full((n_gt, 3), 2.0))}
+    owner = rng.integers(0, n_gt, n)
+    xyz = 2.0 * d[owner] + rng.normal(size=(n, 3)) * np.exp(ls[owner]) * rng.uniform(0.2, 2.0, (n, 1))
+    dist, _ = cKDTree(xyz).query(xyz, k=4)
+    mean_d = np.maximum(dist[:, 1:].mean(axis=1), 1e-7)
+    prgb = np.clip(rgb[owner] + rng.normal(0.0, 0.02, (n, 3)), 0.0, 1.0)
+    rot = np.zeros((n, 4))
+    rot[:, 0] = 1.0
+    fields = {"positions": _f32(xyz), "log_scales": _f32(np.log(mean_d)[:, None].repeat(3, axis=1)),
+              "rotations": _f32(rot), "opacity_logits": _f32(np.full(n, math.log(0.1 / 0.9))),
+              "sh_dc": _f32((prgb - 0.5) / c0), "sh_rest": _f32(np.zeros((n, 15, 3))),
+              "mask_logits": _f32(np.full(n, 2.0)), "sh_mask_logits": _f32(np.full((n, 3), 2.0))}
+    cams = [pinhole(rng.uniform(4.0, 6.0) * _unit(rng), width, height, name=f"c5v{k}") for k in range(views)]
+    sc = Scene("c5", fields, cams, [], dict(near=0.2, tile_size=16, mask_threshold=0.01, sh_mask_threshold=0.1))
+    return sc, gt
+
+
 def small_scene(seed: int, n: int, width: int, height: int, dist: float = 4.0, **settings) -> Scene:
     """c1 distributions at a reduced size (parity tests)."""
     rng = np.random.default_rng(seed)

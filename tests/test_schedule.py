@@ -44,3 +44,25 @@ def test_contracts():
         S.BlurSpec(4, 1.0)
     assert S.active_sh_degree(0) == 0 and S.active_sh_degree(2500) == 2 and S.active_sh_degree(10**6) == 3
     assert S.Timeline().scaled(3000).mask_prune_interval == 50
+
+
+def test_config5_sfm_follows_the_reference_seeding_recipe():
+    """scenes.config5_sfm restates synthetic.make_scene + schedule.seed_from_sfm: seeds
+    near ground-truth centres, isotropic kNN scales, identity rotations, opacity 0.1,
+    mask logits 2.0."""
+    import numpy as np
+    from scipy.spatial import cKDTree
+
+    from paper_2501_14534_b200 import scenes
+    sc, gt = scenes.config5_sfm(n=3000, n_gt=150, width=64, height=48, views=2)
+    f = sc.fields
+    assert f["positions"].shape == (3000, 3) and gt["positions"].shape == (150, 3)
+    d, _ = cKDTree(gt["positions"]).query(f["positions"])
+    assert np.quantile(d, 0.9) < 4.0 * np.exp(gt["log_scales"]).max()
+    assert np.all(f["log_scales"][:, 0] == f["log_scales"][:, 2])
+    assert np.all(f["rotations"] == np.array([1, 0, 0, 0], dtype=np.float32))
+    assert np.allclose(1.0 / (1.0 + np.exp(-f["opacity_logits"])), 0.1)
+    assert np.all(f["mask_logits"] == 2.0) and np.all(f["sh_mask_logits"] == 2.0)
+    op = 1.0 / (1.0 + np.exp(-gt["opacity_logits"]))
+    assert op.min() >= 0.55 - 1e-6 and op.max() <= 0.95 + 1e-6
+    assert len(sc.cameras) == 2 and sc.cameras[0].width == 64
