@@ -368,6 +368,45 @@ __device__ __forceinline__ float warp_reduce2_transpose(float n0, float n1, int 
   return k;
 }
 
+// The 16-value reduction of k_blend_bwd16p through the warp's shared-memory slot instead
+// of the butterfly (whose per value cost is one SHFL, two lane-dependent FSELs and one
+// FADD): each lane stores its 16 values as one row (4 x STS.128), lane l then sums
+// column l & 15 over its half warp's 16 rows (16 LDS, a 4-deep FADD tree) and one
+// SHFL adds the halves.  Rows are 20 floats apart and the upper 16 rows shifted by 16
+// more, so both the row stores (per 8-lane phase) and the column loads are
+// bank-conflict free.  Lane l ends with the warp sum of u[l & 15].
+#ifndef TGS_BWD_SMEM_RED
+#define TGS_BWD_SMEM_RED 1
+#endif
+constexpr int kRedStride = 20;
+constexpr int kRedFloats = 32 * kRedStride + 16;
+__device__ __forceinline__ int red_row(int r) { return r * kRedStride + (r & 16); }
+
+__device__ __forceinline__ float warp_reduce16_smem(float *buf, const float u[16], int lane) {
+  float4 *w = reinterpret_cast<float4 *>(buf + red_row(lane));
+#pragma unroll
+  for (int c = 0; c < 4; ++c) w[c] = make_float4(u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+  __syncwarp();
+  const float *col = buf + red_row(lane & 16) + (lane & 15);
+#ifndef TGS_RED_CHUNK
+#define TGS_RED_CHUNK 16
+#endif
+  float acc = 0.0f;
+#pragma unroll
+  for (int c0 = 0; c0 < 16; c0 += TGS_RED_CHUNK) {  // loads in flight per batch (registers)
+    float t[TGS_RED_CHUNK];
+#pragma unroll
+    for (int i = 0; i < TGS_RED_CHUNK; ++i) t[i] = col[(c0 + i) * kRedStride];
+#pragma unroll
+    for (int h = TGS_RED_CHUNK / 2; h > 0; h >>= 1)
+#pragma unroll
+      for (int i = 0; i < h; ++i) t[i] += t[i + h];
+    acc = c0 ? acc + t[0] : t[0];
+  }
+  __syncwarp();
+  return acc + __shfl_xor_sync(0xffffffffu, acc, 16);
+}
+
 // Backward batch: 128 splats at 16x16 tiles; each warp owns a private slice of
 // the per-splat accumulators (plain stores, no shared-memory float atomics,
 // which sm_100 emulates with a CAS loop), summed over warps at the flush.
@@ -1225,7 +1264,7 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
 // the bracket pairs are re-resolved in float64 (resolveP).
 template <bool kExact, int kP, bool kExc>
 __device__ __forceinline__ void bwd16p_tile(
-    WStage *SW, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+    WStage *SW, float *RB, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin,
     float bg0, float bg1, float bg2, const float *__restrict__ transmit, const int32_t *__restrict__ last_pos,
     const float *__restrict__ dimage, float *__restrict__ dsplats, const int32_t *__restrict__ exc) {
@@ -1326,6 +1365,13 @@ __device__ __forceinline__ void bwd16p_tile(
           u[f] = v0[f];
           u[8 + f] = v1[f];
         }
+#if TGS_BWD_SMEM_RED
+        const float r = warp_reduce16_smem(RB + warp * kRedFloats, u, lane);  // lane l: u[l & 15]
+        const float r9 = warp_reduce2_transpose(v0[8], v1[8], lane);
+        const int idA = (lane & 8) ? id1 : S.id[b0], idB = (lane & 16) ? id1 : S.id[b0];
+        if (lane < 16 && idA >= 0 && r != 0.0f) atomicAdd(dsplats + 9 * (int64_t)idA + (lane & 7), r);
+        if ((lane & 15) == 1 && idB >= 0 && r9 != 0.0f) atomicAdd(dsplats + 9 * (int64_t)idB + 8, r9);
+#else
         const float r = warp_reduce16_transpose(u, lane);
         const float r9 = warp_reduce2_transpose(v0[8], v1[8], lane);
         const int id = (lane & 16) ? id1 : S.id[b0];
@@ -1334,6 +1380,7 @@ __device__ __forceinline__ void bwd16p_tile(
           if ((lane & 1) == 0 && r != 0.0f) atomicAdd(d + ((lane >> 1) & 7), r);
           if ((lane & 15) == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
         }
+#endif
       }
     }
     __syncwarp();
@@ -1343,11 +1390,11 @@ __device__ __forceinline__ void bwd16p_tile(
 #ifdef TGS_BWD_CHK_NOINLINE  // A/B builds: the float64-resolving tile body out of line
 template <bool kExact, int kP>
 __device__ __noinline__ void bwd16p_tile_chk(
-    WStage *SW, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
+    WStage *SW, float *RB, int tile, const float4 *__restrict__ splats, const float4 *__restrict__ exact,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W, int H, int tiles_x, int row_begin,
     float bg0, float bg1, float bg2, const float *__restrict__ transmit, const int32_t *__restrict__ last_pos,
     const float *__restrict__ dimage, float *__restrict__ dsplats) {
-  bwd16p_tile<kExact, kP, false>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+  bwd16p_tile<kExact, kP, false>(SW, RB, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
                                  transmit, last_pos, dimage, dsplats, nullptr);
 }
 #endif
@@ -1363,16 +1410,17 @@ __global__ void __launch_bounds__(128 / kP, kExact ? TGS_BWD16_MINB * kP : 1) k_
     float *__restrict__ dsplats, const int32_t *__restrict__ order, const int32_t *__restrict__ exc,
     const uint32_t *__restrict__ ovf) {
   __shared__ WStage SW[4 / kP];
+  __shared__ __align__(16) float RB[TGS_BWD_SMEM_RED ? (4 / kP) * kRedFloats : 4];  // warp_reduce16_smem slots
   const int tile = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
   if (kExact && exc && !__ldg(ovf + 1 + tile))
-    bwd16p_tile<kExact, kP, true>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+    bwd16p_tile<kExact, kP, true>(SW, RB, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
                                   transmit, last_pos, dimage, dsplats, exc);
   else
 #ifdef TGS_BWD_CHK_NOINLINE
-    bwd16p_tile_chk<kExact, kP>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+    bwd16p_tile_chk<kExact, kP>(SW, RB, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
                                 transmit, last_pos, dimage, dsplats);
 #else
-    bwd16p_tile<kExact, kP, false>(SW, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
+    bwd16p_tile<kExact, kP, false>(SW, RB, tile, splats, exact, offsets, ids, W, H, tiles_x, row_begin, bg0, bg1, bg2,
                                    transmit, last_pos, dimage, dsplats, nullptr);
 #endif
 }
