@@ -1161,6 +1161,10 @@ __device__ __noinline__ int resolveP(const float4 *__restrict__ splats, const fl
   return r;
 }
 
+// bwd_visitP accumulates fields 2 and 4 (the conic partials' squared terms) at twice their
+// value; the factor 1/2 (exact) is applied to the warp sums.
+__device__ __forceinline__ float bwd_field_scale(int f) { return (f == 2 || f == 4) ? 0.5f : 1.0f; }
+
 template <bool kExact, int kP, bool kExc>
 __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, const float2 fy[kP], float2 m,
                                            float4 q, float4 cn, float4 col, float2 cut, int32_t gid,
@@ -1243,13 +1247,23 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     const float2 v5 = make_float2(gm[h].x > 0.0f ? gx.x : 0.0f, gm[h].y > 0.0f ? gx.y : 0.0f);
     const float2 gG = __fmul2_rn(v5, f2(cn.w));
     const float2 v0 = __ffma2_rn(f2(cn.y), dy[h], f2(cx.x)), v1 = __ffma2_rn(f2(cn.z), dy[h], f2(cx.y));
-    const float2 hG = __fmul2_rn(gG, f2(0.5f));
     const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
-    const float2 terms[9] = {p0, p1, __fmul2_rn(__fmul2_rn(hG, v0), v0), __fmul2_rn(p0, v1),
-                             __fmul2_rn(__fmul2_rn(hG, v1), v1), v5, __fmul2_rn(P.g0[h], w),
-                             __fmul2_rn(P.g1[h], w), __fmul2_rn(P.g2[h], w)};
-#pragma unroll
-    for (int f = 0; f < 9; ++f) acc[f] = h == 0 ? terms[f] : __fadd2_rn(acc[f], terms[f]);
+    // fields 2 and 4 accumulate gG v0^2 and gG v1^2, twice the partials (the 1/2 is applied
+    // once per splat after the warp reduction, bwd_field_scale); products of the second
+    // pair fold into the sum as FFMA2 (the partials need the gradient tolerance, not the
+    // forward's bit-exactness)
+    if (h == 0) {
+      acc[0] = p0; acc[1] = p1;
+      acc[2] = __fmul2_rn(p0, v0); acc[3] = __fmul2_rn(p0, v1); acc[4] = __fmul2_rn(p1, v1);
+      acc[5] = v5;
+      acc[6] = __fmul2_rn(P.g0[h], w); acc[7] = __fmul2_rn(P.g1[h], w); acc[8] = __fmul2_rn(P.g2[h], w);
+    } else {
+      acc[0] = __fadd2_rn(acc[0], p0); acc[1] = __fadd2_rn(acc[1], p1);
+      acc[2] = __ffma2_rn(p0, v0, acc[2]); acc[3] = __ffma2_rn(p0, v1, acc[3]); acc[4] = __ffma2_rn(p1, v1, acc[4]);
+      acc[5] = __fadd2_rn(acc[5], v5);
+      acc[6] = __ffma2_rn(P.g0[h], w, acc[6]); acc[7] = __ffma2_rn(P.g1[h], w, acc[7]);
+      acc[8] = __ffma2_rn(P.g2[h], w, acc[8]);
+    }
     P.GS[h] = __ffma2_rn(gc, w, P.GS[h]);
     P.T[h] = tb;
     hitm = fmaxf(hitm, fmaxf(alm[h].x, alm[h].y));
@@ -1369,7 +1383,8 @@ __device__ __forceinline__ void bwd16p_tile(
         const float r = warp_reduce16_smem(RB + warp * kRedFloats, u, lane);  // lane l: u[l & 15]
         const float r9 = warp_reduce2_transpose(v0[8], v1[8], lane);
         const int idA = (lane & 8) ? id1 : S.id[b0], idB = (lane & 16) ? id1 : S.id[b0];
-        if (lane < 16 && idA >= 0 && r != 0.0f) atomicAdd(dsplats + 9 * (int64_t)idA + (lane & 7), r);
+        if (lane < 16 && idA >= 0 && r != 0.0f)
+          atomicAdd(dsplats + 9 * (int64_t)idA + (lane & 7), r * bwd_field_scale(lane & 7));
         if ((lane & 15) == 1 && idB >= 0 && r9 != 0.0f) atomicAdd(dsplats + 9 * (int64_t)idB + 8, r9);
 #else
         const float r = warp_reduce16_transpose(u, lane);
@@ -1377,7 +1392,7 @@ __device__ __forceinline__ void bwd16p_tile(
         const int id = (lane & 16) ? id1 : S.id[b0];
         if (id >= 0) {
           float *d = dsplats + 9 * (int64_t)id;
-          if ((lane & 1) == 0 && r != 0.0f) atomicAdd(d + ((lane >> 1) & 7), r);
+          if ((lane & 1) == 0 && r != 0.0f) atomicAdd(d + ((lane >> 1) & 7), r * bwd_field_scale((lane >> 1) & 7));
           if ((lane & 15) == 1 && r9 != 0.0f) atomicAdd(d + 8, r9);
         }
 #endif
