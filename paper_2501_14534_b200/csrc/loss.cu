@@ -355,14 +355,24 @@ __global__ void __launch_bounds__(kLossThreads, 4) k_ssim_adj(LossArgs A, const 
       }
     }
     if (yy < H) {
+      // all eight image / target loads in flight before the first store (the stores to
+      // dimage could alias them, so the compiler would otherwise serialise load -> store
+      // per pixel: a quarter of the kernel's stall samples)
+      float av[kHOut], bv[kHOut];
+#pragma unroll
+      for (int o = 0; o < kHOut; ++o) {
+        const int xx = min(x0 + c0 + o, W - 1);
+        const size_t p = ((size_t)yy * W + xx) * 3 + c;
+        av[o] = __ldg(A.img + p);
+        bv[o] = __ldg(A.tgt + p);
+      }
 #pragma unroll
       for (int o = 0; o < kHOut; ++o) {
         const int xx = x0 + c0 + o;
         if (xx >= W) continue;
         const size_t p = ((size_t)yy * W + xx) * 3 + c;
-        const float av = __ldg(A.img + p), bv = __ldg(A.tgt + p);
-        const float grad = (g0[o] + 2.0f * av * g1[o] + bv * g2[o]) * A.inv_count;
-        const float diff = av - bv;
+        const float grad = (g0[o] + 2.0f * av[o] * g1[o] + bv[o] * g2[o]) * A.inv_count;
+        const float diff = av[o] - bv[o];
         const float sgn = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
         A.dimage[p] = (1.0f - A.lam) * sgn * A.inv_count - A.lam * 0.5f * grad;
       }
