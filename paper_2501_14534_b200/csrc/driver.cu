@@ -140,8 +140,15 @@ int run_views(const Batch &B) {
     return B.targets[v].row_end > 0 ? B.targets[v].row_end : (cams[v].height + ts - 1) / ts;
   };
   // 2a. depth sort of view v + asynchronous read of its instance count
+#ifdef TGS_EXP_SKIP_BIN  // experiment builds only (profiles/binning_cost_exp.py): after 3 batches, reuse
+  static int calls = 0;   // the views' tile lists of the previous batch (a static scene) and skip binning
+  const bool skip_bin = ++calls > 3;
+#else
+  constexpr bool skip_bin = false;
+#endif
   auto begin = [&](int v) -> int {
     const int k = v % B.nstreams;
+    if (skip_bin) return cudaEventRecord(E.count[k], stream(B.streams[k])) == cudaSuccess ? TGS_OK : TGS_ERR_CUDA;
     int r = tgs_bin_gaussians(B.splats[v], B.tiles_touched[v], B.depth_keys ? B.depth_keys[v] : nullptr, n,
                               cams[v].width, cams[v].height, ts, rb_of(v), rows_of(v), slot[k].ws_g, slot[k].counts,
                               B.error_flag, B.streams[k]);
@@ -155,6 +162,10 @@ int run_views(const Batch &B) {
   auto place = [&](int v) -> int {
     const int k = v % B.nstreams;
     if (cudaEventSynchronize(E.count[k]) != cudaSuccess) return TGS_ERR_CUDA;
+    if (skip_bin) {
+      B.targets[v].num_instances = 0;
+      return TGS_OK;
+    }
     const int64_t count = B.pinned_counts[2 * k], flag = B.pinned_counts[2 * k + 1];
     if (flag) return TGS_ERR_DEGENERATE_ROTATION;
     tgs_view_target &t = B.targets[v];
