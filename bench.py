@@ -20,6 +20,7 @@ the GPU box) on the host's cores for the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -414,18 +415,27 @@ def main():
         tr.opt.steps = dict(init[3])
         torch.cuda.synchronize()
 
-    def timed_fixed(k, body, tr):
-        total, inst = 0.0, []
+    each = {}
+
+    def timed_fixed(k, body, tr, label="device"):
+        total, inst, ms = 0.0, [], []
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for _ in range(k):
-            reset(tr)
-            barrier()
-            s.record()
-            body()
-            e.record()
-            e.synchronize()
-            total += s.elapsed_time(e) / 1e3
-            inst.append(sum(tr.instances))
+        gc.collect()
+        gc.disable()  # no collector pause inside a timed step (the host enqueues the step)
+        try:
+            for _ in range(k):
+                reset(tr)
+                barrier()
+                s.record()
+                body()
+                e.record()
+                e.synchronize()
+                ms.append(s.elapsed_time(e))
+                total += ms[-1] / 1e3
+                inst.append(sum(tr.instances))
+        finally:
+            gc.enable()
+        each[label] = [round(x, 3) for x in ms]
         torch.cuda.synchronize()
         barrier()
         t = torch.tensor([total], device=dev)
@@ -456,7 +466,7 @@ def main():
         terms_host.copy_(trainer.terms, non_blocking=True)
 
     e2e_step()
-    t_e2e, _ = timed_fixed(args.steps, e2e_step, trainer)
+    t_e2e, _ = timed_fixed(args.steps, e2e_step, trainer, "e2e")
     trainer.check_divergence()
     h2d = sum(host_targets[v].numel() * 4 for v in views)
     d2h = terms_host.numel() * 8
@@ -468,7 +478,7 @@ def main():
     serial.opt = trainer.opt
     serial.step()
     with profiler.StageTimer() as prof:
-        t_serial, _ = timed_fixed(args.steps, serial.step, serial)
+        t_serial, _ = timed_fixed(args.steps, serial.step, serial, "serial_views")
     reset(serial)
     from paper_2501_14534_b200.rasterizer import render_forward
     inst, ents, vis, pairs = [], [], [], []
@@ -509,6 +519,7 @@ def main():
             "e2e": {"value": round(args.steps / t_e2e, 4), "unit": "train step/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
+            "ms_each_step": each,
             "ms_per_step_serial_views": round(t_serial / args.steps * 1e3, 3),
             "ms_per_step_continuous": round(t_cont / args.steps * 1e3, 3),
             "render_fps": round(render_fps, 2), "instances_per_view": int(inst_mean),
