@@ -1243,8 +1243,13 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     const float2 w = __fmul2_rn(alm[h], tb);
     // partials through the unclamped alpha only; the select drops the NaN / Inf an
     // out-of-range Gaussian factor could give
-    const float2 gx = __fmul2_rn(ga, gauss[h]);
-    const float2 v5 = make_float2(gm[h].x > 0.0f ? gx.x : 0.0f, gm[h].y > 0.0f ? gx.y : 0.0f);
+    float2 v5;
+    if (kExc) {  // every blended pair is unclamped (gm == alm > 0): mask the Gaussian factor
+      v5 = __fmul2_rn(ga, make_float2(alm[h].x > 0.0f ? gauss[h].x : 0.0f, alm[h].y > 0.0f ? gauss[h].y : 0.0f));
+    } else {
+      const float2 gx = __fmul2_rn(ga, gauss[h]);
+      v5 = make_float2(gm[h].x > 0.0f ? gx.x : 0.0f, gm[h].y > 0.0f ? gx.y : 0.0f);
+    }
     const float2 gG = __fmul2_rn(v5, f2(cn.w));
     const float2 v0 = __ffma2_rn(f2(cn.y), dy[h], f2(cx.x)), v1 = __ffma2_rn(f2(cn.z), dy[h], f2(cx.y));
     const float2 p0 = __fmul2_rn(gG, v0), p1 = __fmul2_rn(gG, v1);
