@@ -569,60 +569,86 @@ def rank_share(args):
     build): rank 0's share of an N-rank ZeRO-1 step — its views (0, N, 2N, ...), the
     multi-view preprocess forward / backward of those views and the fused Adam on its 1/N
     parameter shard (train.Trainer(zero_sim=(0, N))) — timed exactly like the bench's
-    fixed-workload step, plus the reduce-scatter and all-gather of the 252 B/Gaussian
-    parameter buffer at an assumed NCCL bus bandwidth (--nvlink-gbs), NOT overlapped with
-    compute (the real step overlaps chunk k's all-gather with chunk k+1's Adam)."""
+    fixed-workload step, plus the reduce-scatter and all-gather of the step's parameter
+    range at an assumed NCCL bus bandwidth (--nvlink-gbs), NOT overlapped with compute
+    (the real step overlaps chunk k's all-gather with chunk k+1's Adam).  Measured for the
+    bench's step (every gradient, SH-rest included: 252 B/Gaussian exchanged) and for the
+    SH-cadence steps in between (compute_sh_rest_grads off, rasterizer.py:88-92: sh_rest
+    neither differentiated nor updated nor exchanged), and as the schedule average of one
+    cadence step per 16."""
+    import dataclasses
+
     import torch
 
     from paper_2501_14534_b200 import GaussianCloud, RenderSettings, _lib, scenes
+    from paper_2501_14534_b200.parallel import zero_plan
     from paper_2501_14534_b200.train import Trainer
     N = args.rank_share
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     _lib.load()
     sc = scenes.config3(n=args.n)
-    st = RenderSettings(**settings_kwargs())
+    st_full = RenderSettings(**settings_kwargs())
     cloud = GaussianCloud.from_fields(sc.fields, device=dev)
     views = list(range(0, VIEWS, N))
     targets = [None] * VIEWS
     for v in views:
         targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
     out = {}
-    for label, kw in (("share", dict(views=views, zero_sim=(0, N))), ("full", dict(views=list(range(VIEWS))))):
-        if label == "full":
-            for v in range(VIEWS):
-                targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
-        tr = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, **kw)
-        init = (cloud.flat.clone(), tr.opt.m.clone(), tr.opt.v.clone(), dict(tr.opt.steps))
-        for _ in range(args.warmup):
-            tr.step()
-        total = 0.0
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for _ in range(args.steps):
+    for rest in (True, False):
+        st = dataclasses.replace(st_full, compute_sh_rest_grads=rest)
+        for label, kw in (("share", dict(views=views, zero_sim=(0, N))), ("full", dict(views=list(range(VIEWS))))):
+            if label == "full":
+                for v in range(VIEWS):
+                    targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
+            tr = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, **kw)
+            init = (cloud.flat.clone(), tr.opt.m.clone(), tr.opt.v.clone(), dict(tr.opt.steps))
+            for _ in range(args.warmup):
+                tr.step()
+            total = 0.0
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(args.steps):
+                cloud.flat.copy_(init[0])
+                tr.opt.m.copy_(init[1])
+                tr.opt.v.copy_(init[2])
+                tr.opt.steps = dict(init[3])
+                torch.cuda.synchronize()
+                s.record()
+                tr.step()
+                e.record()
+                e.synchronize()
+                total += s.elapsed_time(e)
+            tr.check_divergence()
             cloud.flat.copy_(init[0])
-            tr.opt.m.copy_(init[1])
-            tr.opt.v.copy_(init[2])
-            tr.opt.steps = dict(init[3])
-            torch.cuda.synchronize()
-            s.record()
-            tr.step()
-            e.record()
-            e.synchronize()
-            total += s.elapsed_time(e)
-        tr.check_divergence()
-        cloud.flat.copy_(init[0])
-        out[label] = total / args.steps
-    from paper_2501_14534_b200.cloud import params_end
-    pbytes = params_end(cloud._layout_map) * 4
-    comm_ms = 2 * (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
-    proj = out["share"] + comm_ms
+            out[(rest, label)] = total / args.steps
+        for v in range(VIEWS):
+            targets[v] = torch.from_numpy(sc.targets[v]).to(dev) if v in views else None
+    res = {}
+    for rest in (True, False):
+        pbytes = sum(ch.end - ch.begin for ch in zero_plan(cloud._layout_map, N, rest_grads=rest)) * 4
+        comm_ms = 2 * (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
+        res[rest] = dict(share=out[(rest, "share")], full=out[(rest, "full")], comm=comm_ms, bytes=pbytes,
+                         proj=out[(rest, "share")] + comm_ms)
+    avg = lambda k: (res[True][k] + 15 * res[False][k]) / 16  # noqa: E731
+    proj, full = res[True]["proj"], res[True]["full"]
     print(json.dumps({"metric": f"projected c3 train step/s at {N} GPUs (1-GPU rank-share measurement + NCCL model)",
                       "value": round(1e3 / proj, 3), "unit": "train step/s", "n_gpus": 1, "projected_n_gpus": N,
-                      "ms_per_step_projected": round(proj, 3), "ms_rank_share_measured": round(out["share"], 3),
-                      "ms_comm_model": round(comm_ms, 3), "ms_per_step_1gpu_measured": round(out["full"], 3),
-                      "projected_speedup": round(out["full"] / proj, 3), "views_on_rank0": views,
-                      "comm_model": f"reduce-scatter + all-gather of {pbytes} B (parameter floats) at "
-                                    f"{args.nvlink_gbs} GB/s NCCL bus bandwidth, not overlapped",
+                      "ms_per_step_projected": round(proj, 3), "ms_rank_share_measured": round(res[True]["share"], 3),
+                      "ms_comm_model": round(res[True]["comm"], 3), "ms_per_step_1gpu_measured": round(full, 3),
+                      "projected_speedup": round(full / proj, 3),
+                      "sh_cadence_step": {"ms_rank_share_measured": round(res[False]["share"], 3),
+                                          "ms_comm_model": round(res[False]["comm"], 3),
+                                          "exchanged_bytes": res[False]["bytes"],
+                                          "ms_per_step_projected": round(res[False]["proj"], 3),
+                                          "ms_per_step_1gpu_measured": round(res[False]["full"], 3),
+                                          "projected_speedup": round(res[False]["full"] / res[False]["proj"], 3)},
+                      "schedule_average_1_in_16": {"ms_per_step_projected": round(avg("proj"), 3),
+                                                   "ms_per_step_1gpu_measured": round(avg("full"), 3),
+                                                   "projected_speedup": round(avg("full") / avg("proj"), 3)},
+                      "views_on_rank0": views,
+                      "comm_model": f"reduce-scatter + all-gather of the step's parameter range ({res[True]['bytes']} B; "
+                                    f"{res[False]['bytes']} B on SH-cadence steps) at {args.nvlink_gbs} GB/s NCCL bus "
+                                    f"bandwidth, not overlapped",
                       "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded BASELINE.json config 3)",
                       "config": config_dict(len(cloud), N)}), flush=True)
 
