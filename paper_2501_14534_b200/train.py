@@ -128,6 +128,7 @@ class Trainer:
         self.terms = torch.zeros((len(cameras), 2), dtype=torch.float64, device=dev)
         self.dimage = {}
         self._exc_bufs = {}  # (stream, H, W) -> blend exception lists (native path)
+        self._pre_cache = {}  # preprocess_views' reused outputs (rasterizer.preprocess_views)
         self.dsplats = {}
         # >= 2 streams pipeline consecutive views (4 by default: measured 118 / 121 / 123 step/s
         # with 2 / 3 / 4 at c3); 1 stream serialises them (per-kernel timing)
@@ -254,10 +255,10 @@ class Trainer:
             self.terms.zero_()  # other ranks' rows are summed in by the step's terms all-reduce
         # every view's preprocess in one pass over the parameters (main stream)
         vcams = [self.cameras[v] for v in self.views]
-        pres = preprocess_views(self.cloud, vcams, self.settings, stats=self.stats, exact=False)
+        pres = preprocess_views(self.cloud, vcams, self.settings, stats=self.stats, exact=False, cache=self._pre_cache)
         self.exact_stream.wait_stream(main)
         with torch.cuda.stream(self.exact_stream):
-            exact_records(self.cloud, vcams, self.settings, pres)
+            exact_records(self.cloud, vcams, self.settings, pres, cache=self._pre_cache)
         exact_ready = torch.cuda.Event()
         exact_ready.record(self.exact_stream)
         for s_ in self.streams:
