@@ -458,8 +458,9 @@ TGS_API int tgs_render_views(const tgs_cloud *cloud, const tgs_camera *cams, con
  * from C++: the caller has run tgs_preprocess_forward_views (and, on any stream,
  * tgs_exact_records_views, complete at the event `exact_ready`, which may be NULL when
  * exact is NULL or already complete); per view bin -> count -> place -> blend forward ->
- * loss -> blend backward as tgs_render_views pipelines it (no separate blend streams),
- * with train[v] the view's loss / backward buffers.  The caller then runs ONE
+ * loss -> blend backward as tgs_render_views pipelines it, with train[v] the view's
+ * loss / backward buffers; blend_streams (may be NULL) take each view's blend, loss and
+ * backward (after an event on its binning stream), as in tgs_render_views.  The caller then runs ONE
  * tgs_preprocess_backward_views over the views' dsplats and the Adam step.  On
  * TGS_ERR_CAPACITY some views may already have accumulated partials: zero them before
  * the retry. */
@@ -468,7 +469,8 @@ TGS_API int tgs_train_views(const tgs_cloud *cloud, const tgs_camera *cams, cons
                             uint64_t *const *depth_keys, float *const *exact, void *exact_ready,
                             int32_t *error_flag, tgs_view_target *targets, const tgs_view_train *train,
                             float lambda_ssim, void *const *workspaces, size_t workspace_bytes,
-                            int64_t *pinned_counts, const tgs_stream_t *streams, int32_t nstreams);
+                            int64_t *pinned_counts, const tgs_stream_t *streams,
+                            const tgs_stream_t *blend_streams, int32_t nstreams);
 
 #ifdef __cplusplus
 }

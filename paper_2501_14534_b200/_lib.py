@@ -77,7 +77,7 @@ _SIGS = {
     "tgs_memcpy_d2h_async": ([_P, _P, _SZ, _P], _I32),
     "tgs_render_views_workspace": ([_I64, _I64, _I32, _I32, _I32, _P], _I32),
     "tgs_render_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32], _I32),
-    "tgs_train_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _SZ, _P, _P, _I32], _I32),
+    "tgs_train_views": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _P, _SZ, _P, _P, _P, _I32], _I32),
     "tgs_bin_instances_workspace": ([_I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "tgs_row_histogram": ([_P, _P, _I64, _I32, _I32, _I32, _P, _P], _I32),
     "tgs_bin_instances": ([_P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _I64, _P, _P, _P, _P], _I32),

@@ -270,12 +270,13 @@ extern "C" int tgs_train_views(const tgs_cloud *cloud, const tgs_camera *cams, c
                                uint64_t *const *depth_keys, float *const *exact, void *exact_ready,
                                int32_t *error_flag, tgs_view_target *targets, const tgs_view_train *train,
                                float lambda_ssim, void *const *workspaces, size_t workspace_bytes,
-                               int64_t *pinned_counts, const tgs_stream_t *streams, int32_t nstreams) {
+                               int64_t *pinned_counts, const tgs_stream_t *streams,
+                               const tgs_stream_t *blend_streams, int32_t nstreams) {
   if (!train || nviews < 1) return TGS_ERR_INVALID;
   for (int v = 0; v < nviews; ++v)
     if (!train[v].target || !train[v].dimage || !train[v].terms || !train[v].dsplats || !train[v].loss_workspace)
       return TGS_ERR_INVALID;
   return run_views(Batch{cloud, cams, s, nviews, splats, visible, tiles_touched, depth_keys, exact, error_flag,
-                         targets, workspaces, workspace_bytes, pinned_counts, streams, nullptr, nstreams,
+                         targets, workspaces, workspace_bytes, pinned_counts, streams, blend_streams, nstreams,
                          /*preprocess=*/false, exact_ready, train, lambda_ssim});
 }

@@ -115,7 +115,6 @@ class Trainer:
         # atomic backward is used; the Python loop remains for 1 stream (per-stage timing)
         # and the deterministic backward
         if native is None:  # TGS_TRAIN_NATIVE=0: the Python loop (A/B timing)
-            import os
             native = os.environ.get("TGS_TRAIN_NATIVE", "1") != "0"
         self.native = native
         self._nat = {}  # per-geometry native buffers: (key) -> dict
@@ -133,20 +132,28 @@ class Trainer:
         self.dsplats = {}
         # >= 2 streams pipeline consecutive views (4 by default: measured 118 / 121 / 123 step/s
         # with 2 / 3 / 4 at c3); 1 stream serialises them (per-kernel timing)
-        # the view streams (binning, blends) at high priority, so the views' binning CTAs are
-        # scheduled ahead of the exact records' side kernel, which only the blends need
-        # (same-box A/B: 122.7-123.1 vs 120.0-121.0 step/s; TGS_VIEW_PRIO=0 for the default)
-        vp = int(os.environ.get("TGS_VIEW_PRIO", "-1"))
+        # stream priorities (CUDA range 0 .. -3, lower = scheduled first): the view streams
+        # (each view's binning) highest, the blend streams (each view's blend / loss /
+        # backward) next, the exact records' side kernel and the per-step kernels (main)
+        # last — the latency-bound binning CTAs go ahead of the issue-bound blends, and
+        # both ahead of the exact records only the blends need.  Same-box A/Bs
+        # (profiles/r02_ab_view_stream_priority.log, r02_ab_blend_streams.log): high-priority
+        # view streams 122.7-123.1 vs 120.0-121.0 step/s; separate blend streams e2e
+        # 119.0-120.6 vs 117.7-118.9.  TGS_VIEW_PRIO / TGS_BLEND_PRIO / TGS_TRAIN_BLEND_STREAMS
+        # override (A/B).
+        vp = int(os.environ.get("TGS_VIEW_PRIO", "-2"))
         self.streams = [torch.cuda.Stream(device=cloud.device, priority=vp) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
         # the exact blend-decision records of the step's views are computed here while the
         # first views' depth sorts run (only the blends read them)
         self.exact_stream = torch.cuda.Stream(device=cloud.device)
+        bp = int(os.environ.get("TGS_BLEND_PRIO", "-1"))
+        self.blend_streams = ([torch.cuda.Stream(device=cloud.device, priority=bp) for _ in self.streams]
+                              if os.environ.get("TGS_TRAIN_BLEND_STREAMS", "1") == "1" else [])
         # one GPU: the preprocess backward may run in row chunks, each chunk's Adam on
         # adam_stream beside the next chunk (TGS_BWD_CHUNKS).  Default 1: measured no gain at
         # c3 (113.3 step/s for 1, 2, 4 and 8 chunks) — the backward's 3 CTAs x 128 threads x
         # 160 registers fill the register file, so no Adam block co-resides
-        import os
         self.bwd_chunks = int(os.environ.get("TGS_BWD_CHUNKS", "1"))
         self.adam_stream = torch.cuda.Stream(device=cloud.device)
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
@@ -266,7 +273,7 @@ class Trainer:
             exact_records(self.cloud, vcams, self.settings, pres, cache=self._pre_cache)
         exact_ready = torch.cuda.Event()
         exact_ready.record(self.exact_stream)
-        for s_ in self.streams:
+        for s_ in self.streams + self.blend_streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         ts = int(self.settings.tile_size)
         if self.native and not self.deterministic and n and len(self.streams) >= 2 and self.views:
@@ -403,10 +410,12 @@ class Trainer:
                     arr(5) if EXACT_DECISIONS else None, exact_ready.cuda_event, pres[0][4].data_ptr(), targets,
                     train, float(self.lambda_ssim),
                     (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), nb["wsb"], pinned.data_ptr(),
-                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]), ns))
+                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]),
+                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.blend_streams])
+                    if self.blend_streams else None, ns))
             counts = [int(targets[i].num_instances) for i in range(V)]
             if rc == TGS_ERR_CAPACITY:
-                for s_ in self.streams:
+                for s_ in self.streams + self.blend_streams:
                     s_.synchronize()
                 for v in self.views:  # views already backwarded accumulated partials
                     self.dsplats[v].zero_()
@@ -423,7 +432,7 @@ class Trainer:
         return [p[1] for p in pres], [self.dsplats[v] for v in self.views]
 
     def _after_views(self, main, g, vis, parts, copied, n):
-        for s_ in self.streams:
+        for s_ in self.streams + self.blend_streams:
             main.wait_stream(s_)
         main.wait_stream(self.exact_stream)
         if copied:
