@@ -142,6 +142,8 @@ class Trainer:
         # 119.0-120.6 vs 117.7-118.9.  TGS_VIEW_PRIO / TGS_BLEND_PRIO / TGS_TRAIN_BLEND_STREAMS
         # override (A/B).
         vp = int(os.environ.get("TGS_VIEW_PRIO", "-2"))
+        if streams > 1:  # TGS_TRAIN_STREAMS: A/B of the pipelined stream count
+            streams = int(os.environ.get("TGS_TRAIN_STREAMS", streams))
         self.streams = [torch.cuda.Stream(device=cloud.device, priority=vp) for _ in range(max(1, streams))]
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
         # the exact blend-decision records of the step's views are computed here while the
