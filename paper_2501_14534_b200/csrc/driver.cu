@@ -21,6 +21,9 @@
 // are the caller's.  A view whose instance count exceeds its id capacity (or the
 // workspace) stops the batch with TGS_ERR_CAPACITY after writing every view's count to
 // targets[].num_instances (-1 = not reached); the caller grows its buffers and calls again.
+#include <memory>
+#include <vector>
+
 #include "tgs_common.cuh"
 
 namespace {
@@ -39,28 +42,42 @@ struct Slot {  // one stream's share of the caller's workspace
   size_t ws_i_bytes;
 };
 
-// The events of one batch: created up front (a failure leaves nothing uninitialised)
-// and destroyed on every exit.
+// The events of a batch.  Creating and destroying them per call (up to 2 + 2 x 8) cost
+// host time before the batch's first launch, so each thread keeps one set per device and
+// re-records it every batch (a wait issued by an earlier batch captured that batch's
+// record; reuse is safe).  Destroyed with the thread.
 struct Events {
   cudaEvent_t pre = nullptr, ex = nullptr, count[kMaxStreams] = {}, blend[kMaxStreams] = {};
-  int n = 0;
+  bool ready = false;
   ~Events() {
     if (pre) cudaEventDestroy(pre);
     if (ex) cudaEventDestroy(ex);
-    for (int k = 0; k < n; ++k) {
+    for (int k = 0; k < kMaxStreams; ++k) {
       if (count[k]) cudaEventDestroy(count[k]);
       if (blend[k]) cudaEventDestroy(blend[k]);
     }
   }
   static bool make(cudaEvent_t &e) { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess; }
-  int create(int nstreams, bool with_ex) {
-    n = nstreams;
-    if (!make(pre) || (with_ex && !make(ex))) return cuda_status(cudaGetLastError());
-    for (int k = 0; k < nstreams; ++k)
+  int create() {
+    if (ready) return TGS_OK;
+    if (!make(pre) || !make(ex)) return cuda_status(cudaGetLastError());
+    for (int k = 0; k < kMaxStreams; ++k)
       if (!make(count[k]) || !make(blend[k])) return cuda_status(cudaGetLastError());
+    ready = true;
     return TGS_OK;
   }
 };
+
+// this thread's event set for the current device
+int batch_events(Events *&E) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return TGS_ERR_CUDA;
+  thread_local std::vector<std::unique_ptr<Events>> sets;
+  if ((size_t)dev >= sets.size()) sets.resize((size_t)dev + 1);
+  if (!sets[dev]) sets[dev] = std::make_unique<Events>();
+  E = sets[dev].get();
+  return E->create();  // a partial failure keeps what was made (destroyed with the thread)
+}
 
 struct Batch {
   const tgs_cloud *cloud;
@@ -105,9 +122,10 @@ int run_views(const Batch &B) {
     char *b = static_cast<char *>(B.workspaces[k]);
     slot[k] = Slot{b, b, reinterpret_cast<int64_t *>(b + off_counts), b + off_i, B.workspace_bytes - off_i};
   }
-  Events E;
-  rc = E.create(B.nstreams, B.preprocess && B.exact);
+  Events *Ep = nullptr;
+  rc = batch_events(Ep);
   if (rc != TGS_OK) return rc;
+  Events &E = *Ep;
   auto stream = [](tgs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); };
   cudaStream_t st0 = stream(B.streams[0]);
   // 1. every view's preprocess in one pass over the parameters (stream 0), or the caller's

@@ -380,6 +380,30 @@ class Trainer:
                         order=_blend_order(None, tx * ty, tx, ty, ts, dev, None)))
                 nb["bufs_cap"] = cap
                 nb["wsb"] = max(ctypes_size("tgs_render_views_workspace", n, cap, w, h, ts) for w, h in geo)
+            # the driver's argument structs are rebuilt only when a buffer behind them can have
+            # changed (capacity, partial / target buffers, the preprocess outputs); otherwise
+            # only the per-step events are patched in (~0.1 ms of host work per step saved,
+            # which sits before the step's first binning launch)
+            sig = (cap, tuple(self.dsplats[v].data_ptr() for v in self.views),
+                   tuple(self.targets[v].data_ptr() for v in self.views),
+                   tuple(pres[0][k].data_ptr() for k in (0, 1, 2, 3, 5)), EXACT_DECISIONS)
+            ct = nb.get("ct")
+            if ct is not None and ct["sig"] == sig:
+                targets, train = ct["targets"], ct["train"]
+                for i, v in enumerate(self.views):
+                    train[i].target_ready = copied[v].cuda_event if v in copied else None
+                rc = self._train_views_call(ct, c_cloud, c_cams, c_set, V, exact_ready, pres, targets, train, nb,
+                                            pinned, ns)
+                counts = [int(targets[i].num_instances) for i in range(V)]
+                if rc == TGS_ERR_CAPACITY:
+                    for s_ in self.streams + self.blend_streams:
+                        s_.synchronize()
+                    for v in self.views:
+                        self.dsplats[v].zero_()
+                    nb["cap"] = _size_class(int(max(counts) * 1.25) + 1024)
+                    continue
+                raise_for_status(rc, "tgs_train_views")
+                break
             wss = [_scratch("train_views", nb["wsb"], dev, s_.cuda_stream, owner=s_) for s_ in self.streams]
             loss_ws, train = [], (_lib.TgsViewTrain * V)()
             targets = (_lib.TgsViewTarget * V)()
@@ -406,15 +430,15 @@ class Trainer:
                                              self.dsplats[v].data_ptr(), lw.data_ptr(),
                                              copied[v].cuda_event if v in copied else None,
                                              _lib.ptr(xb[0]) if xb else None, _lib.ptr(xb[1]) if xb else None)
-            with stage("train_views"):
-                rc = int(_lib.load().tgs_train_views(
-                    ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, arr(0), arr(1), arr(2), arr(3),
-                    arr(5) if EXACT_DECISIONS else None, exact_ready.cuda_event, pres[0][4].data_ptr(), targets,
-                    train, float(self.lambda_ssim),
-                    (ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]), nb["wsb"], pinned.data_ptr(),
-                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]),
-                    (ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.blend_streams])
-                    if self.blend_streams else None, ns))
+            ct = nb["ct"] = dict(
+                sig=sig, targets=targets, train=train, loss_ws=loss_ws,
+                ptrs=[arr(0), arr(1), arr(2), arr(3), arr(5) if EXACT_DECISIONS else None],
+                wss=(ctypes.c_void_p * ns)(*[t.data_ptr() for t in wss]),
+                streams=(ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.streams]),
+                blend_streams=(ctypes.c_void_p * ns)(*[s_.cuda_stream for s_ in self.blend_streams])
+                if self.blend_streams else None)
+            rc = self._train_views_call(ct, c_cloud, c_cams, c_set, V, exact_ready, pres, targets, train, nb, pinned,
+                                        ns)
             counts = [int(targets[i].num_instances) for i in range(V)]
             if rc == TGS_ERR_CAPACITY:
                 for s_ in self.streams + self.blend_streams:
@@ -432,6 +456,16 @@ class Trainer:
         self.check_divergence(block=False)  # the previous step's flag is on the host by now
         self.instances = counts
         return [p[1] for p in pres], [self.dsplats[v] for v in self.views]
+
+    def _train_views_call(self, ct, c_cloud, c_cams, c_set, V, exact_ready, pres, targets, train, nb, pinned, ns):
+        import ctypes
+        from . import _lib
+        p = ct["ptrs"]
+        with stage("train_views"):
+            return int(_lib.load().tgs_train_views(
+                ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, p[0], p[1], p[2], p[3], p[4],
+                exact_ready.cuda_event, pres[0][4].data_ptr(), targets, train, float(self.lambda_ssim), ct["wss"],
+                nb["wsb"], pinned.data_ptr(), ct["streams"], ct["blend_streams"], ns))
 
     def _after_views(self, main, g, vis, parts, copied, n):
         for s_ in self.streams + self.blend_streams:
