@@ -148,7 +148,8 @@ class Trainer:
         self.copy_stream = torch.cuda.Stream(device=cloud.device)
         # the exact blend-decision records of the step's views are computed here while the
         # first views' depth sorts run (only the blends read them)
-        self.exact_stream = torch.cuda.Stream(device=cloud.device)
+        self.exact_stream = torch.cuda.Stream(device=cloud.device,
+                                              priority=int(os.environ.get("TGS_EXACT_PRIO", "0")))
         bp = int(os.environ.get("TGS_BLEND_PRIO", "-1"))
         self.blend_streams = ([torch.cuda.Stream(device=cloud.device, priority=bp) for _ in self.streams]
                               if os.environ.get("TGS_TRAIN_BLEND_STREAMS", "1") == "1" else [])
