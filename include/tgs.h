@@ -86,12 +86,15 @@ enum {
  *        float32 exponent's error over the Gaussian's footprint: a pixel whose
  *        float32 exponent e2 is >= cut_hi (and <= 0) blends in float64 too, one
  *        below cut_lo does not; in between (or e2 > 0) the blend kernels decide in
- *        float64 (_kernels.py:62-72).  cut_hi = +inf when alpha can reach the 0.99
- *        clamp (every pair then decided in float64, incl. the backward's a <= 0.99);
+ *        float64 (_kernels.py:62-72);
  *   [2..3] means2d, [4..6] conic: float64 value minus the float32 record value, so
  *        record + residual reconstructs the float64 projection (~1e-13);
- *   [7]  the float64 cut minus cut_lo (log2 units), or, when cut_hi = +inf (the
- *        cut is then -4.5), the clamp exponent ln(0.99 / alpha).
+ *   [7]  the float64 cut minus cut_lo (log2 units), or, when the float32 alpha
+ *        exceeds 0.9899 so that alpha exp(e) can reach the 0.99 clamp (the cut is
+ *        then -4.5), the clamp exponent ln(0.99 / alpha): the blend kernels bracket
+ *        it with the cut's error bound ((cut_hi - cut_lo) / 2) and decide the
+ *        backward's a <= 0.99 (_kernels.py:157-168) in float64 for the blended pairs
+ *        above the bracket's lower end (rare: near the Gaussian's centre).
  * Rows of non-visible Gaussians are zero.  A blend call without records
  * (exact == NULL) decides every pair in float32. */
 #define TGS_EXACT_FLOATS 8

@@ -63,6 +63,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 constexpr float kLog2e = 1.44269504088896341f;
 constexpr float kE2Min = (float)(-4.5 * 1.44269504088896341);  // the e >= -4.5 cut in log2 units
+constexpr float kClampAlpha = 0.9899f;  // float32 alpha above which alpha exp(e) can reach 0.99
 
 // Pre-scaled conic (A, B, C, alpha) with A = -a log2(e) / 2, B = -b log2(e),
 // C = -c log2(e) / 2, so e2 = A dx^2 + B dx dy + C dy^2 = e log2(e) and
@@ -143,9 +144,25 @@ __device__ __forceinline__ int exact_pair(const float4 *__restrict__ splats, con
   const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dadd_rn(a.z, r1.x), dx), dx),
                              __dmul_rn(__dmul_rn(__dadd_rn(k2f, r1.z), dy), dy));
   const double e = __dsub_rn(__dmul_rn(-0.5, q), __dmul_rn(__dmul_rn(__dadd_rn(a.w, r1.y), dx), dy));
-  if (!isinf(r0.y)) return __dmul_rn(e, 1.4426950408889634) >= __dadd_rn(r0.x, r1.w) ? 3 : 0;
+  const float alpha = __ldg(reinterpret_cast<const float *>(splats + 3 * (int64_t)g + 1) + 1);
+  if (!(alpha > kClampAlpha)) return __dmul_rn(e, 1.4426950408889634) >= __dadd_rn(r0.x, r1.w) ? 3 : 0;
   if (e < -4.5) return 0;
   return e <= (double)r1.w ? 3 : 1;
+}
+
+// The clamp bracket's lower end (log2 units) of a Gaussian whose alpha can reach the 0.99
+// clamp (float32 alpha > kClampAlpha): a blended pair whose float32 exponent e2 lies below
+// it is certainly unclamped (alpha exp(e) <= 0.99: the partials through alpha apply,
+// _kernels.py:157-168); at or above it the float64 decision (exact_pair, record slot 7 =
+// ln(0.99 / alpha)) is taken — only the backward needs it (the forward blends min(a, 0.99)
+// either way).  Computed from registers the staging already holds: log2(0.99 / alpha)
+// from the float32 alpha is within ~1e-6 of the float64 exponent (alpha's rounding
+// ~4e-7 relative, lg2.approx ~2.4e-7 absolute), and the float32 exponent's own error is at
+// most (cut_hi - cut_lo) / 2 (the record's bracket half-width bounds it over the
+// footprint, preprocess.cu exact_record).  +inf for the other Gaussians.
+__device__ __forceinline__ float clamp_lo_of(float2 cut, float alpha) {
+  const float v = __log2f(__fdividef(0.99f, alpha)) - 0.5f * (cut.y - cut.x) - 4e-6f;
+  return alpha > kClampAlpha ? v : __int_as_float(0x7f800000);
 }
 
 // Both pixels of a lane at once, out of line (the 16x16 kernels call it from a warp-uniform
@@ -173,6 +190,13 @@ __device__ __forceinline__ bool in_bracket2(float2 e2, float2 cut) {
   const bool a = e2.x >= cut.x && !(e2.x >= cut.y), b = e2.y >= cut.x && !(e2.y >= cut.y);
   return __any_sync(0xffffffffu, a || b);
 }
+// ... or at / above the clamp bracket's lower end clo (the forward's clamp candidates):
+// e2 >= cut_lo && !(cut_hi <= e2 < clo), one more compare per pixel in the same chain
+__device__ __forceinline__ bool in_bracket_or_clamp2(float2 e2, float2 cut, float clo) {
+  const bool a = e2.x >= cut.x && !(e2.x >= cut.y && e2.x < clo);
+  const bool b = e2.y >= cut.x && !(e2.y >= cut.y && e2.y < clo);
+  return __any_sync(0xffffffffu, a || b);
+}
 
 // Scalar decision for the one-pixel-per-thread kernels: 0 skip, else bit 1 = unclamped.
 __device__ __forceinline__ int decide_pair(float e2, float a_raw, float2 cut, const float4 *__restrict__ splats,
@@ -180,7 +204,10 @@ __device__ __forceinline__ int decide_pair(float e2, float a_raw, float2 cut, co
   const bool hi = e2 >= cut.y;
   if (exact && e2 >= cut.x && !hi) return exact_pair(splats, exact, g, px, py);
   if (!hi) return 0;
-  return a_raw <= kAlphaMax ? 3 : 1;
+  if (!exact) return a_raw <= kAlphaMax ? 3 : 1;
+  const float alpha = __ldg(reinterpret_cast<const float *>(splats + 3 * (int64_t)g + 1) + 1);
+  if (e2 < clamp_lo_of(cut, alpha)) return 3;  // certainly unclamped (or cannot clamp)
+  return exact_pair(splats, exact, g, px, py);
 }
 
 __device__ __forceinline__ bool quad_misses(float2 m, float4 q, float thr2, float4 wb) {
@@ -730,21 +757,26 @@ struct Fwd16Pair {
          c2 = make_float2(0.f, 0.f), ws = make_float2(0.f, 0.f);
   float2 cnt = make_float2(0.f, 0.f);  // n_contrib of both pixels, counted in one FADD2 (exact < 2^24)
   int lA = 0, lB = 0;
-  // blend exception (exact decisions): the 1-based list position pos where the float64
-  // resolution blended a pair the certain rule (e2 >= cut_hi) skips, one per lane, as
-  // 2 pos + (pixel B); -1: a second one, or a clamped one (the tile's backward then
-  // re-resolves its bracket pairs in float64 instead).  One register for both pixels.
+  // blend exception (exact decisions): a blended pair the float64 resolution decided — in
+  // the cut bracket, or at / above a clampable Gaussian's clamp bracket (whose a <= 0.99
+  // only the backward needs) — one per lane, as 4 pos + 2 clamped + (pixel B), pos the
+  // 1-based list position; -1: a second one on the lane (the tile's backward then
+  // re-resolves its pairs in float64 instead).  One register for both pixels.
   int ex = 0;
   bool dA, dB;
 };
 
 __device__ __forceinline__ void note_exception(int &ex, int pos, int pixel_b, bool unclamped) {
-  ex = !unclamped || ex ? -1 : 2 * pos + pixel_b;
+  ex = ex ? -1 : 4 * pos + (unclamped ? 0 : 2) + pixel_b;
+}
+// the exceptions array's word for a pixel: pos | clamped << 31 (0: none)
+__device__ __forceinline__ int32_t exception_word(int ex, int pixel_b) {
+  return ex > 0 && (ex & 1) == pixel_b ? (int32_t)((uint32_t)(ex >> 2) | ((ex & 2) ? 0x80000000u : 0u)) : 0;
 }
 
 template <bool kExact, bool kHits>
 __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
-                                           float2 cut, int pos, int32_t *hits, int32_t gid,
+                                           float2 cut, float clo, int pos, int32_t *hits, int32_t gid,
                                            const float4 *__restrict__ splats, const float4 *__restrict__ exact,
                                            const int32_t *exc) {
   // checked before each entry (_kernels.py:57-58)
@@ -763,14 +795,18 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   // >= ~1/255 > 0), so no boolean has to live across the rare branch.
   float2 al = make_float2(!P.dA && e2.x >= cut.y ? fminf(a_raw.x, kAlphaMax) : 0.0f,
                           !P.dB && e2.y >= cut.y ? fminf(a_raw.y, kAlphaMax) : 0.0f);
-  if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
-    const bool uA = !P.dA && !(e2.x >= cut.y) && e2.x >= cut.x, uB = !P.dB && !(e2.y >= cut.y) && e2.y >= cut.x;
+  // float64 for pairs inside the cut bracket and — for a Gaussian that can reach the 0.99
+  // clamp, when the backward will need it (clo finite: clamp_lo_of) — blended pairs at /
+  // above its clamp bracket's lower end, recorded with their clamp bit
+  if (kExact && in_bracket_or_clamp2(e2, cut, clo)) {  // warp-uniform, rare
+    const bool uA = !P.dA && e2.x >= cut.x && !(e2.x >= cut.y && e2.x < clo);
+    const bool uB = !P.dB && e2.y >= cut.x && !(e2.y >= cut.y && e2.y < clo);
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
-    if (uA && (r & 1)) {
+    if (uA && (al.x > 0.0f || (r & 1))) {  // a certain pair stays blended (float64 agrees)
       al.x = fminf(a_raw.x, kAlphaMax);
       if (exc) note_exception(P.ex, pos, 0, (r & 2) != 0);
     }
-    if (uB && (r & 4)) {
+    if (uB && (al.y > 0.0f || (r & 4))) {
       al.y = fminf(a_raw.y, kAlphaMax);
       if (exc) note_exception(P.ex, pos, 1, (r & 8) != 0);
     }
@@ -830,18 +866,21 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   bool okA = pos < P.lA && e2.x >= cut.y;
   bool okB = pos < P.lB && e2.y >= cut.y;
   // unclamped (a_raw <= 0.99): the partials through alpha apply.  With exact records a
-  // Gaussian whose alpha can reach the clamp has cut_hi = +inf, so every certain pair is
-  // unclamped and only exact_pair() can report a clamped one.
+  // certain pair below its Gaussian's clamp bracket (col.w: clamp_lo_of, +inf when alpha
+  // cannot reach 0.99) is unclamped; pairs in the cut bracket and blended pairs at / above
+  // the clamp bracket are decided by exact_pair().
   bool clA = kExact || a_raw.x <= kAlphaMax, clB = kExact || a_raw.y <= kAlphaMax;
-  if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
-    const bool uA = pos < P.lA && !okA && e2.x >= cut.x, uB = pos < P.lB && !okB && e2.y >= cut.x;
+  if (kExact && (in_bracket2(e2, cut) ||
+                 __any_sync(0xffffffffu, (okA && e2.x >= col.w) || (okB && e2.y >= col.w)))) {  // warp-uniform, rare
+    const bool uA = pos < P.lA && e2.x >= cut.x && (!okA || e2.x >= col.w);
+    const bool uB = pos < P.lB && e2.y >= cut.x && (!okB || e2.y >= col.w);
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
     if (uA) {
-      okA = r & 1;
+      okA = okA || (r & 1);
       clA = r & 2;
     }
     if (uB) {
-      okB = (r >> 2) & 1;
+      okB = okB || ((r >> 2) & 1);
       clB = (r >> 3) & 1;
     }
   }
@@ -963,7 +1002,10 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       const float2 m = make_float2(nx.a.x, nx.a.y);
       S.xy[lane] = m;
       S.q[lane] = q;
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      // col.w: the clamp bracket's lower end when the backward will need the clamp
+      // decision (exception lists requested); +inf otherwise and for most Gaussians
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c,
+                                kExact && exc ? clamp_lo_of(cut, nx.b.y) : __int_as_float(0x7f800000));
       S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
@@ -977,8 +1019,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       const float2 m = S.xy[k];
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
-      fwd_visit2<kExact, kHits>(P, fpx, fy, m, q, col, S.cut[k], pos, hits, kHits || kExact ? S.id[k] : 0, splats,
-                                exact, exc);
+      fwd_visit2<kExact, kHits>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits, kHits || kExact ? S.id[k] : 0,
+                                splats, exact, exc);
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
@@ -993,7 +1035,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.x;
     n_contrib[p] = (int32_t)P.cnt.x;
     last_pos[p] = P.lA;
-    if (kExact && exc) exc[p] = P.ex > 0 && !(P.ex & 1) ? P.ex >> 1 : 0;
+    if (kExact && exc) exc[p] = exception_word(P.ex, 0);
   }
   if (PIX_X < W && PIX_YB < H) {
     const int p = PIX_YB * W + PIX_X;
@@ -1004,7 +1046,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.y;
     n_contrib[p] = (int32_t)P.cnt.y;
     last_pos[p] = P.lB;
-    if (kExact && exc) exc[p] = P.ex > 0 && (P.ex & 1) ? P.ex >> 1 : 0;
+    if (kExact && exc) exc[p] = exception_word(P.ex, 1);
   }
   // a tile with an exception the lists cannot carry: flagged (and counted) once, for the
   // backward to re-resolve its bracket pairs in float64 (ovf = [count, flags[ntiles]])
@@ -1073,7 +1115,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_bl
       S.xy[lane] = m;
       S.q[lane] = q;
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      // col.w: the clamp bracket's lower end (exact decisions; +inf for most Gaussians)
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, kExact ? clamp_lo_of(cut, nx.b.y) : thr);
       S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
@@ -1132,7 +1175,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_bl
 template <int kP>
 struct BwdLane {
   int l[2 * kP];                                      // last_pos per pixel
-  int e[2 * kP];                                      // blend exception (kExc), 1-based position
+  int e[2 * kP];                                      // exception word (kExc): pos | clamped << 31
+  int emax;                                           // the lane's highest pending exception position
   float2 g0[kP], g1[kP], g2[kP], T[kP], GS[kP];       // per pair: (pixel 2h, pixel 2h+1)
 };
 
@@ -1185,45 +1229,80 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     // exactly 1, T and G.S stay unchanged); gm: 1 where the partials through alpha apply
     // (unclamped a_raw <= 0.99; with exact records a clampable Gaussian goes to exact_pair,
     // so every certain pair is unclamped) — no boolean has to live across the rare branch
-    // With the forward's exception lists (kExc) a bracket pair blends iff the forward
-    // resolved it to blend, i.e. it is the pixel's recorded exception: no float64 here.
-    const bool bx = e2[h].x >= cut.y || (kExc && pos + 1 == P.e[2 * h]);
-    const bool by = e2[h].y >= cut.y || (kExc && pos + 1 == P.e[2 * h + 1]);
-    alm[h] = make_float2(pos < P.l[2 * h] && bx ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
-                         pos < P.l[2 * h + 1] && by ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
-    gm[h] = make_float2(alm[h].x > 0.0f && (kExact || a_raw[h].x <= kAlphaMax) ? 1.0f : 0.0f,
-                        alm[h].y > 0.0f && (kExact || a_raw[h].y <= kAlphaMax) ? 1.0f : 0.0f);
+    // With the forward's exception lists (kExc) the certain pairs are decided here and
+    // every pair the forward decided in float64 — a bracket pair it blended, a blended pair
+    // at / above a clampable Gaussian's clamp bracket — is the pixel's recorded exception,
+    // applied below when the walk reaches its position: no float64 in this body.
+    alm[h] = make_float2(pos < P.l[2 * h] && e2[h].x >= cut.y ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
+                         pos < P.l[2 * h + 1] && e2[h].y >= cut.y ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
+    // exact: a certain pair below its Gaussian's clamp bracket (col.w: clamp_lo_of, +inf
+    // when alpha cannot reach 0.99) is unclamped; with exception lists the others are
+    // recorded, without them decided below
+    gm[h] = make_float2(
+        alm[h].x > 0.0f && (kExc || (kExact ? e2[h].x < col.w : a_raw[h].x <= kAlphaMax)) ? 1.0f : 0.0f,
+        alm[h].y > 0.0f && (kExc || (kExact ? e2[h].y < col.w : a_raw[h].y <= kAlphaMax)) ? 1.0f : 0.0f);
   }
-  if (kExact && !kExc) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
+  if (kExc) {  // a recorded exception at this list position (one compare per lane; rare)
+    if (__any_sync(0xffffffffu, pos + 1 == P.emax)) {
+      int nmax = 0;
+#pragma unroll
+      for (int h = 0; h < kP; ++h) {
+        const int wx = P.e[2 * h], wy = P.e[2 * h + 1];
+        // blended; a clamped one gets no partials through alpha: its Gaussian factor,
+        // used only by them, is zeroed (the common path then needs no clamp mask)
+        if (pos + 1 == (wx & 0x7fffffff)) {
+          alm[h].x = fminf(a_raw[h].x, kAlphaMax);
+          if (wx < 0) gauss[h].x = 0.0f;
+          P.e[2 * h] = 0;
+        }
+        if (pos + 1 == (wy & 0x7fffffff)) {
+          alm[h].y = fminf(a_raw[h].y, kAlphaMax);
+          if (wy < 0) gauss[h].y = 0.0f;
+          P.e[2 * h + 1] = 0;
+        }
+        nmax = max(nmax, max(P.e[2 * h] & 0x7fffffff, P.e[2 * h + 1] & 0x7fffffff));
+      }
+      P.emax = nmax;
+    }
+  } else if (kExact) {  // the float64 decisions (rare, warp-uniform branch): pairs inside the cut
+    // bracket and blended pairs at / above the clamp bracket
     float pm = 1.0f;
+    bool cl = false;
 #pragma unroll
     for (int h = 0; h < kP; ++h) {
       const float2 pr = __fmul2_rn(__fadd2_rn(e2[h], f2(-cut.x)), __fadd2_rn(e2[h], f2(-cut.y)));
       pm = fminf(pm, fminf(pr.x, pr.y));
+      cl = cl || (alm[h].x > 0.0f && !(gm[h].x > 0.0f)) || (alm[h].y > 0.0f && !(gm[h].y > 0.0f));
     }
-    if (__any_sync(0xffffffffu, pm <= 0.0f)) {
+    if (__any_sync(0xffffffffu, pm <= 0.0f || cl)) {
       int flags = 0;
       float fyv[2 * kP];
 #pragma unroll
       for (int h = 0; h < kP; ++h) {
         fyv[2 * h] = fy[h].x;
         fyv[2 * h + 1] = fy[h].y;
-        if (pos < P.l[2 * h] && !(e2[h].x >= cut.y) && e2[h].x >= cut.x) flags |= 1 << (2 * h);
-        if (pos < P.l[2 * h + 1] && !(e2[h].y >= cut.y) && e2[h].y >= cut.x) flags |= 1 << (2 * h + 1);
+        if ((alm[h].x > 0.0f && !(gm[h].x > 0.0f)) ||
+            (pos < P.l[2 * h] && !(e2[h].x >= cut.y) && e2[h].x >= cut.x))
+          flags |= 1 << (2 * h);
+        if ((alm[h].y > 0.0f && !(gm[h].y > 0.0f)) ||
+            (pos < P.l[2 * h + 1] && !(e2[h].y >= cut.y) && e2[h].y >= cut.x))
+          flags |= 1 << (2 * h + 1);
       }
       if (flags) {
         const int r = resolveP<kP>(splats, exact, gid, fpx, fyv, flags);
 #pragma unroll
-        for (int h = 0; h < kP; ++h) {
+        for (int h = 0; h < kP; ++h) {  // a blended pair stays blended (float64 agrees)
           if ((flags >> (2 * h)) & 1) {
             const int rk = r >> (4 * h);
-            alm[h].x = (rk & 1) ? fminf(a_raw[h].x, kAlphaMax) : 0.0f;
-            gm[h].x = (rk & 3) == 3 ? 1.0f : 0.0f;
+            const bool bl = alm[h].x > 0.0f || (rk & 1);
+            alm[h].x = bl ? fminf(a_raw[h].x, kAlphaMax) : 0.0f;
+            gm[h].x = bl && (rk & 2) ? 1.0f : 0.0f;
           }
           if ((flags >> (2 * h + 1)) & 1) {
             const int rk = r >> (4 * h + 2);
-            alm[h].y = (rk & 1) ? fminf(a_raw[h].y, kAlphaMax) : 0.0f;
-            gm[h].y = (rk & 3) == 3 ? 1.0f : 0.0f;
+            const bool bl = alm[h].y > 0.0f || (rk & 1);
+            alm[h].y = bl ? fminf(a_raw[h].y, kAlphaMax) : 0.0f;
+            gm[h].y = bl && (rk & 2) ? 1.0f : 0.0f;
           }
         }
       }
@@ -1244,7 +1323,8 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     // partials through the unclamped alpha only; the select drops the NaN / Inf an
     // out-of-range Gaussian factor could give
     float2 v5;
-    if (kExc) {  // every blended pair is unclamped (gm == alm > 0): mask the Gaussian factor
+    if (kExc) {  // every blended pair passes its partials through alpha (a clamped exception's
+      // Gaussian factor was zeroed above): mask the factor (finite where alm > 0), not the product
       v5 = __fmul2_rn(ga, make_float2(alm[h].x > 0.0f ? gauss[h].x : 0.0f, alm[h].y > 0.0f ? gauss[h].y : 0.0f));
     } else {
       const float2 gx = __fmul2_rn(ga, gauss[h]);
@@ -1312,7 +1392,7 @@ __device__ __forceinline__ void bwd16p_tile(
       T = transmit[p];
     }
     P.l[k] = lp;
-    P.e[k] = ex;
+    P.e[k] = lp > 0 ? ex : 0;  // (a pixel the walk skips needs none)
     const float GS = (g0 * bg0 + g1 * bg1 + g2 * bg2) * T;
     if (k & 1) {
       P.g0[k >> 1].y = g0; P.g1[k >> 1].y = g1; P.g2[k >> 1].y = g2; P.T[k >> 1].y = T; P.GS[k >> 1].y = GS;
@@ -1322,6 +1402,9 @@ __device__ __forceinline__ void bwd16p_tile(
     wlast = max(wlast, lp);
   }
   wlast = __reduce_max_sync(0xffffffffu, wlast);
+  P.emax = 0;
+#pragma unroll
+  for (int k = 0; k < 2 * kP; ++k) P.emax = max(P.emax, P.e[k] & 0x7fffffff);
   float2 fy[kP];
 #pragma unroll
   for (int h = 0; h < kP; ++h) fy[h] = make_float2((float)py[2 * h], (float)py[2 * h + 1]);
@@ -1350,7 +1433,8 @@ __device__ __forceinline__ void bwd16p_tile(
       S.xy[lane] = m;
       S.q[lane] = q;
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      // col.w: the clamp bracket's lower end (exact decisions; +inf for most Gaussians)
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, kExact ? clamp_lo_of(cut, nx.b.y) : thr);
       S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);

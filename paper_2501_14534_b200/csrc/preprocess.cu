@@ -261,14 +261,16 @@ __device__ __forceinline__ void exact_record(const tgs_cloud &cl, int64_t i, con
             1e-6f * (a0 * X * X + 2.0f * a1 * X * Y + a2 * Y * Y) + 1e-6f;
   const double E2 = 2.0 * (double)E;  // safety factor
   const float lo = __double2float_rd((g.cut - E2) * kLog2eD);
-  // alpha able to reach the 0.99 clamp: every pair of this Gaussian goes to float64, where
-  // the cut is -4.5 (alpha > 0.9899 puts ln(1/(255 alpha)) below it) and slot 7 holds the
-  // clamp's exponent ln(0.99 / alpha) (alpha exp(e) <= 0.99 <=> e <= it); otherwise slot 7
-  // holds the float64 cut minus cut_lo (log2 units) for the float64 comparison e >= cut
-  const bool clampable = g.alpha > 0.9899;
-  const float hi = clampable ? __int_as_float(0x7f800000) : __double2float_ru((g.cut + E2) * kLog2eD);
+  // a Gaussian whose alpha can reach the 0.99 clamp (float32 alpha > 0.9899, the same test
+  // the blend kernels make on the same float): its cut is -4.5 exactly (alpha > 0.353 puts
+  // ln(1/(255 alpha)) below it) and slot 7 holds the clamp's exponent ln(0.99 / alpha)
+  // (alpha exp(e) <= 0.99 <=> e <= it): the kernels bracket it with the same error bound
+  // as the cut (clamp_lo_of in blend.cu) and decide the pairs above the bracket's lower end
+  // in float64; otherwise slot 7 holds the float64 cut minus cut_lo (log2 units) for the
+  // float64 comparison e >= cut
+  const bool clampable = alpha32 > 0.9899f;
+  const float hi = __double2float_ru((g.cut + E2) * kLog2eD);
   const float slot7 = clampable ? (float)log(0.99 / g.alpha) : (float)(g.cut * kLog2eD - (double)lo);
-  (void)alpha32;
   out[0] = make_float4(lo, hi, (float)dmx, (float)dmy);
   out[1] = make_float4((float)dk0, (float)dk1, (float)dk2, slot7);
 }
