@@ -161,8 +161,9 @@ __device__ __forceinline__ int exact_pair(const float4 *__restrict__ splats, con
 // most (cut_hi - cut_lo) / 2 (the record's bracket half-width bounds it over the
 // footprint, preprocess.cu exact_record).  +inf for the other Gaussians.
 __device__ __forceinline__ float clamp_lo_of(float2 cut, float alpha) {
-  const float v = __log2f(__fdividef(0.99f, alpha)) - 0.5f * (cut.y - cut.x) - 4e-6f;
-  return alpha > kClampAlpha ? v : __int_as_float(0x7f800000);
+  float v = __int_as_float(0x7f800000);
+  if (alpha > kClampAlpha) v = __log2f(__fdividef(0.99f, alpha)) - 0.5f * (cut.y - cut.x) - 4e-6f;
+  return v;
 }
 
 // Both pixels of a lane at once, out of line (the 16x16 kernels call it from a warp-uniform
@@ -866,21 +867,18 @@ __device__ __forceinline__ bool bwd_visit2(Bwd16Pair &P, int pos, float fpx, flo
   bool okA = pos < P.lA && e2.x >= cut.y;
   bool okB = pos < P.lB && e2.y >= cut.y;
   // unclamped (a_raw <= 0.99): the partials through alpha apply.  With exact records a
-  // certain pair below its Gaussian's clamp bracket (col.w: clamp_lo_of, +inf when alpha
-  // cannot reach 0.99) is unclamped; pairs in the cut bracket and blended pairs at / above
-  // the clamp bracket are decided by exact_pair().
+  // Gaussian that can reach the clamp is staged with cut_hi = +inf, so every certain pair
+  // is unclamped and only exact_pair() can report a clamped one.
   bool clA = kExact || a_raw.x <= kAlphaMax, clB = kExact || a_raw.y <= kAlphaMax;
-  if (kExact && (in_bracket2(e2, cut) ||
-                 __any_sync(0xffffffffu, (okA && e2.x >= col.w) || (okB && e2.y >= col.w)))) {  // warp-uniform, rare
-    const bool uA = pos < P.lA && e2.x >= cut.x && (!okA || e2.x >= col.w);
-    const bool uB = pos < P.lB && e2.y >= cut.x && (!okB || e2.y >= col.w);
+  if (kExact && in_bracket2(e2, cut)) {  // warp-uniform, rare
+    const bool uA = pos < P.lA && !okA && e2.x >= cut.x, uB = pos < P.lB && !okB && e2.y >= cut.x;
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
     if (uA) {
-      okA = okA || (r & 1);
+      okA = r & 1;
       clA = r & 2;
     }
     if (uB) {
-      okB = okB || ((r >> 2) & 1);
+      okB = (r >> 2) & 1;
       clB = (r >> 3) & 1;
     }
   }
@@ -1115,9 +1113,11 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_BWD16_MINB : 1) k_bl
       S.xy[lane] = m;
       S.q[lane] = q;
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
-      // col.w: the clamp bracket's lower end (exact decisions; +inf for most Gaussians)
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, kExact ? clamp_lo_of(cut, nx.b.y) : thr);
-      S.cut[lane] = cut;
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      // exact decisions: a Gaussian that can reach the 0.99 clamp has no certain pairs here
+      // (its clamp decision is taken in float64 with its blend decision; FLT_MAX, not +inf:
+      // the bracket test stays well-defined at e2 == cut_lo)
+      S.cut[lane] = kExact && nx.b.y > kClampAlpha ? make_float2(cut.x, 3.4e38f) : cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
     }
@@ -1227,20 +1227,17 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
     // the forward's decisions, re-derived identically (load_cut / exact_pair) and carried as
     // floats — alm: the blended alpha or 0 (a skipped entry blends alpha 0: 1 / (1 - 0) is
     // exactly 1, T and G.S stay unchanged); gm: 1 where the partials through alpha apply
-    // (unclamped a_raw <= 0.99; with exact records a clampable Gaussian goes to exact_pair,
-    // so every certain pair is unclamped) — no boolean has to live across the rare branch
-    // With the forward's exception lists (kExc) the certain pairs are decided here and
-    // every pair the forward decided in float64 — a bracket pair it blended, a blended pair
-    // at / above a clampable Gaussian's clamp bracket — is the pixel's recorded exception,
-    // applied below when the walk reaches its position: no float64 in this body.
+    // (unclamped a_raw <= 0.99) — no boolean has to live across the rare branch.  Exact
+    // decisions: a certain pair (e2 >= cut_hi) of a Gaussian that cannot reach the 0.99 clamp
+    // is unclamped.  With the forward's exception lists (kExc) every pair the forward
+    // decided in float64 — a bracket pair it blended, a blended pair at / above a clampable
+    // Gaussian's clamp bracket — is the pixel's recorded exception, applied below when the
+    // walk reaches its position (no float64 in this body); without them (the float64 body)
+    // a clampable Gaussian's staged bracket is [cut_lo, +inf): its pairs all go to float64.
     alm[h] = make_float2(pos < P.l[2 * h] && e2[h].x >= cut.y ? fminf(a_raw[h].x, kAlphaMax) : 0.0f,
                          pos < P.l[2 * h + 1] && e2[h].y >= cut.y ? fminf(a_raw[h].y, kAlphaMax) : 0.0f);
-    // exact: a certain pair below its Gaussian's clamp bracket (col.w: clamp_lo_of, +inf
-    // when alpha cannot reach 0.99) is unclamped; with exception lists the others are
-    // recorded, without them decided below
-    gm[h] = make_float2(
-        alm[h].x > 0.0f && (kExc || (kExact ? e2[h].x < col.w : a_raw[h].x <= kAlphaMax)) ? 1.0f : 0.0f,
-        alm[h].y > 0.0f && (kExc || (kExact ? e2[h].y < col.w : a_raw[h].y <= kAlphaMax)) ? 1.0f : 0.0f);
+    gm[h] = make_float2(alm[h].x > 0.0f && (kExact || a_raw[h].x <= kAlphaMax) ? 1.0f : 0.0f,
+                        alm[h].y > 0.0f && (kExact || a_raw[h].y <= kAlphaMax) ? 1.0f : 0.0f);
   }
   if (kExc) {  // a recorded exception at this list position (one compare per lane; rare)
     if (__any_sync(0xffffffffu, pos + 1 == P.emax)) {
@@ -1264,45 +1261,36 @@ __device__ __forceinline__ bool bwd_visitP(BwdLane<kP> &P, int pos, float fpx, c
       }
       P.emax = nmax;
     }
-  } else if (kExact) {  // the float64 decisions (rare, warp-uniform branch): pairs inside the cut
-    // bracket and blended pairs at / above the clamp bracket
+  } else if (kExact) {  // pairs inside the cut bracket: the float64 decision (rare, warp-uniform branch)
     float pm = 1.0f;
-    bool cl = false;
 #pragma unroll
     for (int h = 0; h < kP; ++h) {
       const float2 pr = __fmul2_rn(__fadd2_rn(e2[h], f2(-cut.x)), __fadd2_rn(e2[h], f2(-cut.y)));
       pm = fminf(pm, fminf(pr.x, pr.y));
-      cl = cl || (alm[h].x > 0.0f && !(gm[h].x > 0.0f)) || (alm[h].y > 0.0f && !(gm[h].y > 0.0f));
     }
-    if (__any_sync(0xffffffffu, pm <= 0.0f || cl)) {
+    if (__any_sync(0xffffffffu, pm <= 0.0f)) {
       int flags = 0;
       float fyv[2 * kP];
 #pragma unroll
       for (int h = 0; h < kP; ++h) {
         fyv[2 * h] = fy[h].x;
         fyv[2 * h + 1] = fy[h].y;
-        if ((alm[h].x > 0.0f && !(gm[h].x > 0.0f)) ||
-            (pos < P.l[2 * h] && !(e2[h].x >= cut.y) && e2[h].x >= cut.x))
-          flags |= 1 << (2 * h);
-        if ((alm[h].y > 0.0f && !(gm[h].y > 0.0f)) ||
-            (pos < P.l[2 * h + 1] && !(e2[h].y >= cut.y) && e2[h].y >= cut.x))
-          flags |= 1 << (2 * h + 1);
+        if (pos < P.l[2 * h] && !(e2[h].x >= cut.y) && e2[h].x >= cut.x) flags |= 1 << (2 * h);
+        if (pos < P.l[2 * h + 1] && !(e2[h].y >= cut.y) && e2[h].y >= cut.x) flags |= 1 << (2 * h + 1);
       }
       if (flags) {
         const int r = resolveP<kP>(splats, exact, gid, fpx, fyv, flags);
 #pragma unroll
-        for (int h = 0; h < kP; ++h) {  // a blended pair stays blended (float64 agrees)
+        for (int h = 0; h < kP; ++h) {
           if ((flags >> (2 * h)) & 1) {
             const int rk = r >> (4 * h);
-            const bool bl = alm[h].x > 0.0f || (rk & 1);
-            alm[h].x = bl ? fminf(a_raw[h].x, kAlphaMax) : 0.0f;
-            gm[h].x = bl && (rk & 2) ? 1.0f : 0.0f;
+            alm[h].x = (rk & 1) ? fminf(a_raw[h].x, kAlphaMax) : 0.0f;
+            gm[h].x = (rk & 3) == 3 ? 1.0f : 0.0f;
           }
           if ((flags >> (2 * h + 1)) & 1) {
             const int rk = r >> (4 * h + 2);
-            const bool bl = alm[h].y > 0.0f || (rk & 1);
-            alm[h].y = bl ? fminf(a_raw[h].y, kAlphaMax) : 0.0f;
-            gm[h].y = bl && (rk & 2) ? 1.0f : 0.0f;
+            alm[h].y = (rk & 1) ? fminf(a_raw[h].y, kAlphaMax) : 0.0f;
+            gm[h].y = (rk & 3) == 3 ? 1.0f : 0.0f;
           }
         }
       }
@@ -1433,9 +1421,11 @@ __device__ __forceinline__ void bwd16p_tile(
       S.xy[lane] = m;
       S.q[lane] = q;
       S.conic[lane] = make_float4(nx.a.z, nx.a.w, nx.b.x, nx.b.y);
-      // col.w: the clamp bracket's lower end (exact decisions; +inf for most Gaussians)
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, kExact ? clamp_lo_of(cut, nx.b.y) : thr);
-      S.cut[lane] = cut;
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, thr);
+      // the float64 body (no exception lists): a Gaussian that can reach the 0.99 clamp has
+      // no certain pairs (its clamp decision is taken in float64 with its blend decision;
+      // FLT_MAX, not +inf: the bracket product stays <= 0 at e2 == cut_lo)
+      S.cut[lane] = kExact && !kExc && nx.b.y > kClampAlpha ? make_float2(cut.x, 3.4e38f) : cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
     }
