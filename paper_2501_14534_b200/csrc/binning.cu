@@ -714,7 +714,10 @@ constexpr int kSeg = 4;                 // chunks per segment (counted by one CT
 constexpr int kDiffCells = 12288;       // 2D difference cells per count CTA
 constexpr int kScanCols = 32;           // bins per segment-scan CTA
 constexpr int kScanGroups = 32;         // segment ranges per segment-scan CTA
-constexpr int kPlaceWarps = 16;
+#ifndef TGS_PLACE_WARPS
+#define TGS_PLACE_WARPS 16
+#endif
+constexpr int kPlaceWarps = TGS_PLACE_WARPS;
 constexpr int kPUnit = 2048;            // entries per L2 unit
 
 struct InstGeom {
