@@ -258,14 +258,7 @@ class Trainer:
         main = torch.cuda.current_stream(self.cloud.device)
         copied = {}
         n = len(self.cloud)
-        if host_targets is not None:
-            self.copy_stream.wait_stream(main)  # the previous step has finished reading the targets
-            with torch.cuda.stream(self.copy_stream):
-                for v in self.views:
-                    self.targets[v].copy_(host_targets[v], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(self.copy_stream)
-                    copied[v] = ev
+        prev_done = main.record_event() if host_targets is not None else None  # the previous step's reads
         if self.pg is not None:
             self.terms.zero_()  # other ranks' rows are summed in by the step's terms all-reduce
         # every view's preprocess in one pass over the parameters (main stream)
@@ -276,6 +269,14 @@ class Trainer:
             exact_records(self.cloud, vcams, self.settings, pres, cache=self._pre_cache)
         exact_ready = torch.cuda.Event()
         exact_ready.record(self.exact_stream)
+        if host_targets is not None:  # issued after the first heavy launch; each view's loss waits for its copy
+            self.copy_stream.wait_event(prev_done)  # the previous step has finished reading the targets
+            with torch.cuda.stream(self.copy_stream):
+                for v in self.views:
+                    self.targets[v].copy_(host_targets[v], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy_stream)
+                    copied[v] = ev
         for s_ in self.streams + self.blend_streams:
             s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
         ts = int(self.settings.tile_size)
