@@ -357,7 +357,7 @@ def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
 
 
 def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, stats=None,
-                     exact: bool = True, cache: dict | None = None) -> list:
+                     exact: bool = True, cache: dict | None = None, c_cams=None) -> list:
     """tgs_preprocess_forward_views: the per-view preprocess outputs of a batch of views in
     one pass over the parameters; element v is what `preprocess(cloud, cams[v], settings)`
     returns (bit-identical), the error flag shared.  stats: optional train.DensifyStats
@@ -398,7 +398,8 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
             t.zero_()
     if n and V:
         c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
-        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+        if c_cams is None:  # (a caller issuing several calls per step passes its own array)
+            c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
         with stage("preprocess_fwd"):
             c_stats = stats.native() if stats is not None else None
             _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, ptrs[0],
@@ -408,7 +409,7 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
 
 
 def exact_records(cloud: GaussianCloud, cams: list, settings: RenderSettings, pres: list,
-                  cache: dict | None = None) -> None:
+                  cache: dict | None = None, c_cams=None) -> None:
     """tgs_exact_records_views on the current stream: the exact blend-decision records
     (include/tgs.h TGS_EXACT_FLOATS) of preprocess_views(..., exact=False) outputs.
     cache: preprocess_views' cache of the same call (its pointer arrays are reused)."""
@@ -417,7 +418,8 @@ def exact_records(cloud: GaussianCloud, cams: list, settings: RenderSettings, pr
     if n == 0 or V == 0:
         return
     c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
-    c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+    if c_cams is None:
+        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
     ent = cache.get((V, max(n, 1), cloud.device)) if cache is not None else None
     if ent is not None and ent[0] is pres:
         sps, exs = ent[1][0], ent[1][5]

@@ -263,10 +263,13 @@ class Trainer:
             self.terms.zero_()  # other ranks' rows are summed in by the step's terms all-reduce
         # every view's preprocess in one pass over the parameters (main stream)
         vcams = [self.cameras[v] for v in self.views]
-        pres = preprocess_views(self.cloud, vcams, self.settings, stats=self.stats, exact=False, cache=self._pre_cache)
+        from . import _lib
+        self._c_cams = (_lib.TgsCamera * len(vcams))(*[_lib.make_camera(c) for c in vcams])  # once per step
+        pres = preprocess_views(self.cloud, vcams, self.settings, stats=self.stats, exact=False, cache=self._pre_cache,
+                                c_cams=self._c_cams)
         self.exact_stream.wait_stream(main)
         with torch.cuda.stream(self.exact_stream):
-            exact_records(self.cloud, vcams, self.settings, pres, cache=self._pre_cache)
+            exact_records(self.cloud, vcams, self.settings, pres, cache=self._pre_cache, c_cams=self._c_cams)
         exact_ready = torch.cuda.Event()
         exact_ready.record(self.exact_stream)
         if host_targets is not None:  # issued after the first heavy launch; each view's loss waits for its copy
@@ -359,7 +362,7 @@ class Trainer:
             elif not self.clear_partials:
                 ds.zero_()
         c_set = _lib.make_settings(self.settings)
-        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+        c_cams = self._c_cams  # this step's (the same views, built in _step)
         c_cloud = self.cloud.native()
         arr = lambda k: (ctypes.c_void_p * V)(*[p[k].data_ptr() for p in pres])  # noqa: E731
         pinned = nb.get("pinned")
