@@ -775,7 +775,7 @@ __device__ __forceinline__ int32_t exception_word(int ex, int pixel_b) {
   return ex > 0 && (ex & 1) == pixel_b ? (int32_t)((uint32_t)(ex >> 2) | ((ex & 2) ? 0x80000000u : 0u)) : 0;
 }
 
-template <bool kExact, bool kHits>
+template <bool kExact, bool kHits, bool kRec>
 __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
                                            float2 cut, float clo, int pos, int32_t *hits, int32_t gid,
                                            const float4 *__restrict__ splats, const float4 *__restrict__ exact,
@@ -799,17 +799,18 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   // float64 for pairs inside the cut bracket and — for a Gaussian that can reach the 0.99
   // clamp, when the backward will need it (clo finite: clamp_lo_of) — blended pairs at /
   // above its clamp bracket's lower end, recorded with their clamp bit
-  if (kExact && in_bracket_or_clamp2(e2, cut, clo)) {  // warp-uniform, rare
-    const bool uA = !P.dA && e2.x >= cut.x && !(e2.x >= cut.y && e2.x < clo);
-    const bool uB = !P.dB && e2.y >= cut.x && !(e2.y >= cut.y && e2.y < clo);
+  // (kRec false — no exception lists recorded, e.g. a render — needs no clamp candidates)
+  if (kExact && (kRec ? in_bracket_or_clamp2(e2, cut, clo) : in_bracket2(e2, cut))) {  // warp-uniform, rare
+    const bool uA = !P.dA && e2.x >= cut.x && !(e2.x >= cut.y && (!kRec || e2.x < clo));
+    const bool uB = !P.dB && e2.y >= cut.x && !(e2.y >= cut.y && (!kRec || e2.y < clo));
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
     if (uA && (al.x > 0.0f || (r & 1))) {  // a certain pair stays blended (float64 agrees)
       al.x = fminf(a_raw.x, kAlphaMax);
-      if (exc) note_exception(P.ex, pos, 0, (r & 2) != 0);
+      if (kRec) note_exception(P.ex, pos, 0, (r & 2) != 0);
     }
     if (uB && (al.y > 0.0f || (r & 4))) {
       al.y = fminf(a_raw.y, kAlphaMax);
-      if (exc) note_exception(P.ex, pos, 1, (r & 8) != 0);
+      if (kRec) note_exception(P.ex, pos, 1, (r & 8) != 0);
     }
   }
   const bool okA = al.x > 0.0f, okB = al.y > 0.0f;
@@ -962,7 +963,7 @@ __device__ __forceinline__ void fetch_splat(SplatRegs &r, const float4 *__restri
 #define PIX_X ((int)fpx)
 #define PIX_YA ((int)fy.x)
 #define PIX_YB ((int)fy.y)
-template <bool kExact, bool kHits>
+template <bool kExact, bool kHits, bool kRec>
 __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_blend_fwd16w(
     const float4 *__restrict__ splats, const float4 *__restrict__ exact, const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids, int W,
     int H, int tiles_x, int row_begin, float bg0, float bg1, float bg2, float *__restrict__ image,
@@ -1003,7 +1004,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       // col.w: the clamp bracket's lower end when the backward will need the clamp
       // decision (exception lists requested); +inf otherwise and for most Gaussians
       S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c,
-                                kExact && exc ? clamp_lo_of(cut, nx.b.y) : __int_as_float(0x7f800000));
+                                kExact && kRec ? clamp_lo_of(cut, nx.b.y) : __int_as_float(0x7f800000));
       S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
@@ -1017,8 +1018,8 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       const float2 m = S.xy[k];
       const float4 q = S.q[k], col = S.col[k];
       const int pos = c - start + k + 1;
-      fwd_visit2<kExact, kHits>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits, kHits || kExact ? S.id[k] : 0,
-                                splats, exact, exc);
+      fwd_visit2<kExact, kHits, kRec>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits,
+                                      kHits || kExact ? S.id[k] : 0, splats, exact, exc);
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
@@ -1033,7 +1034,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.x;
     n_contrib[p] = (int32_t)P.cnt.x;
     last_pos[p] = P.lA;
-    if (kExact && exc) exc[p] = exception_word(P.ex, 0);
+    if (kRec) exc[p] = exception_word(P.ex, 0);
   }
   if (PIX_X < W && PIX_YB < H) {
     const int p = PIX_YB * W + PIX_X;
@@ -1044,11 +1045,11 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     wsum_out[p] = P.ws.y;
     n_contrib[p] = (int32_t)P.cnt.y;
     last_pos[p] = P.lB;
-    if (kExact && exc) exc[p] = exception_word(P.ex, 1);
+    if (kRec) exc[p] = exception_word(P.ex, 1);
   }
   // a tile with an exception the lists cannot carry: flagged (and counted) once, for the
   // backward to re-resolve its bracket pairs in float64 (ovf = [count, flags[ntiles]])
-  if (kExact && exc && __any_sync(0xffffffffu, P.ex < 0) && lane == 0)
+  if (kRec && __any_sync(0xffffffffu, P.ex < 0) && lane == 0)
     if (atomicCAS(ovf + 1 + tile, 0u, 1u) == 0u) atomicAdd(ovf, 1u);
 }
 #undef PIX_X
@@ -1649,8 +1650,9 @@ extern "C" int tgs_blend_forward(const float *splats, const float *exact, const 
     if (e != cudaSuccess) return cuda_status(e);
   }
   if (s->tile_size == 16) {
-    auto kern = ex ? (hits ? k_blend_fwd16w<true, true> : k_blend_fwd16w<true, false>)
-                   : (hits ? k_blend_fwd16w<false, true> : k_blend_fwd16w<false, false>);
+    auto kern = ex ? (exceptions ? (hits ? k_blend_fwd16w<true, true, true> : k_blend_fwd16w<true, false, true>)
+                                 : (hits ? k_blend_fwd16w<true, true, false> : k_blend_fwd16w<true, false, false>))
+                   : (hits ? k_blend_fwd16w<false, true, false> : k_blend_fwd16w<false, false, false>);
     kern<<<ntiles, kT16Threads, 0, as_stream(stream)>>>(
         reinterpret_cast<const float4 *>(splats), ex, tile_offsets, sorted_ids, cam->width, cam->height, tiles_x,
         row_begin, s->background[0], s->background[1], s->background[2], image, transmit, weight_sum, n_contrib,
