@@ -775,7 +775,7 @@ __device__ __forceinline__ int32_t exception_word(int ex, int pixel_b) {
   return ex > 0 && (ex & 1) == pixel_b ? (int32_t)((uint32_t)(ex >> 2) | ((ex & 2) ? 0x80000000u : 0u)) : 0;
 }
 
-template <bool kExact, bool kHits, bool kRec>
+template <bool kExact, bool kHits, bool kRec, bool kClamp>
 __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, float2 m, float4 q, float4 col,
                                            float2 cut, float clo, int pos, int32_t *hits, int32_t gid,
                                            const float4 *__restrict__ splats, const float4 *__restrict__ exact,
@@ -799,10 +799,11 @@ __device__ __forceinline__ void fwd_visit2(Fwd16Pair &P, float fpx, float2 fy, f
   // float64 for pairs inside the cut bracket and — for a Gaussian that can reach the 0.99
   // clamp, when the backward will need it (clo finite: clamp_lo_of) — blended pairs at /
   // above its clamp bracket's lower end, recorded with their clamp bit
-  // (kRec false — no exception lists recorded, e.g. a render — needs no clamp candidates)
-  if (kExact && (kRec ? in_bracket_or_clamp2(e2, cut, clo) : in_bracket2(e2, cut))) {  // warp-uniform, rare
-    const bool uA = !P.dA && e2.x >= cut.x && !(e2.x >= cut.y && (!kRec || e2.x < clo));
-    const bool uB = !P.dB && e2.y >= cut.x && !(e2.y >= cut.y && (!kRec || e2.y < clo));
+  // (kClamp false: no clamp candidates — no exception lists recorded, e.g. a render, or
+  // no staged clamp disk reaches this warp's pixels in this chunk)
+  if (kExact && (kClamp ? in_bracket_or_clamp2(e2, cut, clo) : in_bracket2(e2, cut))) {  // warp-uniform, rare
+    const bool uA = !P.dA && e2.x >= cut.x && !(e2.x >= cut.y && (!kClamp || e2.x < clo));
+    const bool uB = !P.dB && e2.y >= cut.x && !(e2.y >= cut.y && (!kClamp || e2.y < clo));
     const int r = resolve2(splats, exact, gid, fpx, fy.x, fy.y, uA, uB);
     if (uA && (al.x > 0.0f || (r & 1))) {  // a certain pair stays blended (float64 agrees)
       al.x = fminf(a_raw.x, kAlphaMax);
@@ -993,7 +994,7 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
     // cull against the pixels that are still blending (terminated ones no longer count)
     if (c != start) wbc = warp_bounds2(!P.dA, !P.dB, PIX_X, PIX_YA, PIX_YB);
     const bool ok = c + lane < stop;
-    bool keep = false;
+    bool keep = false, reach = false;
     if (ok) {
       const float4 q = prescaled_conic(nx.a, nx.b);
       const float2 cut = kExact ? nx.cut : load_cut(nullptr, nx.g, nx.b.y);
@@ -1003,23 +1004,40 @@ __global__ void __launch_bounds__(kT16Threads, kExact ? TGS_FWD16_MINB : 1) k_bl
       S.q[lane] = q;
       // col.w: the clamp bracket's lower end when the backward will need the clamp
       // decision (exception lists requested); +inf otherwise and for most Gaussians
-      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c,
-                                kExact && kRec ? clamp_lo_of(cut, nx.b.y) : __int_as_float(0x7f800000));
+      const float clo = kExact && kRec ? clamp_lo_of(cut, nx.b.y) : __int_as_float(0x7f800000);
+      S.col[lane] = make_float4(nx.b.z, nx.b.w, nx.c, clo);
       S.cut[lane] = cut;
       S.id[lane] = nx.g;
       keep = !quad_misses(m, q, thr, wbc);
+      // a clamp bracket this warp's pixels can reach (the same exact box test as the cull)
+      reach = keep && clo < __int_as_float(0x7f800000) && !quad_misses(m, q, clo, wbc);
     }
     uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    // the chunk's visits test the clamp candidates only when a staged splat's clamp disk can
+    // reach the warp's box (chunk-uniform: two copies of the visit loop)
+    const bool clamp_chunk = kRec && __any_sync(0xffffffffu, reach);
     __syncwarp();
     fetch_splat(nx, splats, kExact ? exact : nullptr, ids, c + 32 + lane, c + 32 + lane < stop);
-    while (mask) {
-      const int k = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const float2 m = S.xy[k];
-      const float4 q = S.q[k], col = S.col[k];
-      const int pos = c - start + k + 1;
-      fwd_visit2<kExact, kHits, kRec>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits,
-                                      kHits || kExact ? S.id[k] : 0, splats, exact, exc);
+    if (clamp_chunk) {
+      while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float2 m = S.xy[k];
+        const float4 q = S.q[k], col = S.col[k];
+        const int pos = c - start + k + 1;
+        fwd_visit2<kExact, kHits, kRec, kRec>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits,
+                                              kHits || kExact ? S.id[k] : 0, splats, exact, exc);
+      }
+    } else {
+      while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float2 m = S.xy[k];
+        const float4 q = S.q[k], col = S.col[k];
+        const int pos = c - start + k + 1;
+        fwd_visit2<kExact, kHits, kRec, false>(P, fpx, fy, m, q, col, S.cut[k], col.w, pos, hits,
+                                               kHits || kExact ? S.id[k] : 0, splats, exact, exc);
+      }
     }
     if (P.T.x < kTTerm) P.dA = true;
     if (P.T.y < kTTerm) P.dB = true;
