@@ -508,6 +508,7 @@ def main():
     render_all()  # first native batch: its workspaces and arenas are allocated here, untimed
     fps_t = timed(args.steps, render_all)
     render_fps = args.steps * len(views) * world / fps_t
+    compat = compat_cost(sc, st, dev) if world == 1 else None
 
     if rank != 0:
         return
@@ -526,12 +527,45 @@ def main():
             "instances_per_step_first_last": [inst_steps[0], inst_steps[-1]] if inst_steps else None,
             "entries_per_view": int(ent_mean), "selected_per_view": int(vis_n),
             "pairs_per_view": int(pairs_mean)}
+    if compat is not None:
+        line["compat_drop_in"] = compat
     if world == 1 and not args.no_cpu_baseline:
         from types import SimpleNamespace
         line["cpu_baseline"] = cpu_baseline(sc, SimpleNamespace(record_hits=False, **settings_kwargs()))
     print(json.dumps(line), flush=True)
     if pg is not None:
         dist.destroy_process_group()
+
+
+def compat_cost(sc, st, dev) -> dict:
+    """The literal drop-in (compat.py: the reference's own float64 numpy objects in and out,
+    what its training.py:296-309 iteration calls): one c3 view's render_forward +
+    render_backward per iteration, wall time per iteration (the cloud's upload and the
+    outputs' / gradients' download included), against the same view's device time."""
+    import types
+
+    import torch
+
+    from paper_2501_14534_b200 import compat
+    cloud64 = types.SimpleNamespace(**{k: np.asarray(v, dtype=np.float64) for k, v in sc.fields.items()})
+    cam = sc.cameras[0]
+    dimg = np.random.default_rng(0).standard_normal((cam.height, cam.width, 3))
+    for _ in range(2):
+        compat.render_backward(cloud64, cam, st, dimg, compat.render_forward(cloud64, cam, st))
+    torch.cuda.synchronize()
+    k = 3
+    t0 = time.perf_counter()
+    for _ in range(k):
+        out = compat.render_forward(cloud64, cam, st)
+        compat.render_backward(cloud64, cam, st, dimg, out)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / k
+    return {"ms_per_view_iteration": round(wall * 1e3, 2),
+            "what": "compat.render_forward + compat.render_backward of one c3 view with float64 numpy "
+                    "inputs / outputs: the cloud (63 float64 per Gaussian) converted and uploaded, the "
+                    "image, auxiliaries and 9 gradient fields downloaded and widened to float64 — the "
+                    "reference's per-iteration call pattern; a training loop keeping the cloud on the "
+                    "GPU (train.Trainer) does not pay it"}
 
 
 def gpu_busy(fn, k: int) -> dict:

@@ -15,8 +15,10 @@ GaussianCloud / Camera / RenderSettings attribute names); outputs are float64
 numpy arrays with the reference's shapes, and `RenderOutput._tiles.indices`
 index the compacted visible subset exactly like `bin_tiles` does in
 `_prepare` (rasterizer.py:177-200).  Each call uploads the cloud and downloads
-the results — the host<->device cost of a literal drop-in; a training loop
-that keeps the cloud on the GPU should use the tensor API (rasterizer.py).
+the results — the host<->device cost of a literal drop-in (bench.py
+`compat_drop_in`); a training loop that keeps the cloud on the GPU should use the
+tensor API (rasterizer.py, train.Trainer).  The float64 <-> float32 conversions run
+on the GPU (the copies carry float64), the tile lists are remapped only when read.
 """
 
 from __future__ import annotations
@@ -52,8 +54,20 @@ class RenderOutputNP:
     screen_areas: np.ndarray
     hit_counts: np.ndarray | None = None
     hit_records: list | None = None
-    _tiles: TileBinsNP | None = field(default=None, repr=False)
+    _tiles_np: TileBinsNP | None = field(default=None, repr=False)
     _device: object = field(default=None, repr=False)
+
+    @property
+    def _tiles(self) -> TileBinsNP | None:
+        """The reference's TileBins (rasterizer.py:177-200), made on first access: the
+        device lists' ids remapped to the compacted visible subset."""
+        if self._tiles_np is None and self._device is not None:
+            out = self._device[1]
+            remap = np.cumsum(self.visible) - 1
+            ids = out._tiles.indices.cpu().numpy()
+            self._tiles_np = TileBinsNP(out._tiles.offsets.cpu().numpy().astype(np.int64), remap[ids],
+                                        out._tiles.tiles_x, out._tiles.tiles_y)
+        return self._tiles_np
 
 
 @dataclass
@@ -77,29 +91,51 @@ def _settings(s) -> _r.RenderSettings:
     return _r.RenderSettings(**{k: getattr(s, k, getattr(d, k)) for k in _r.RenderSettings.__dataclass_fields__})
 
 
-def _np64(t):
-    return t.detach().cpu().numpy().astype(np.float64)
+def _host(tensors: dict) -> dict:
+    """Device tensors to numpy, float32 ones widened to float64 on the GPU, through pinned
+    blocks of torch's caching host allocator (a pageable .cpu() of the ~0.5 GB of gradients
+    ran at ~2 GB/s): every copy is issued, then one synchronisation.  The returned arrays
+    own their pinned blocks, which return to the allocator's cache when released."""
+    out = {}
+    for k, t in tensors.items():
+        if t is None:
+            out[k] = None
+            continue
+        src = t.detach()
+        if src.dtype == torch.float32:
+            src = src.double()
+        buf = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        buf.copy_(src, non_blocking=True)
+        out[k] = buf
+    torch.cuda.current_stream().synchronize()
+    return {k: (v.numpy() if v is not None else None) for k, v in out.items()}
 
 
 def _upload(cloud) -> GaussianCloud:
-    return GaussianCloud.from_fields({f: np.asarray(getattr(cloud, f)) for f in FIELDS})
+    """The reference cloud's float64 fields copied as they are and rounded to float32 on
+    the GPU, into the flat parameter buffer."""
+    arrs = {f: np.asarray(getattr(cloud, f)) for f in FIELDS}
+    n = int(arrs["positions"].shape[0])
+    dev = GaussianCloud(n, "cuda")
+    for f in FIELDS:
+        dst = getattr(dev, f)
+        src = torch.from_numpy(np.ascontiguousarray(arrs[f])).to(dst.device)
+        if tuple(src.shape) != tuple(dst.shape):
+            from .errors import ContractViolationError
+            raise ContractViolationError(f"field {f} has shape {tuple(src.shape)}, expected {tuple(dst.shape)}")
+        dst.copy_(src)
+    return dev
 
 
 def render_forward(cloud, cam, settings) -> RenderOutputNP:
     dev_cloud = _upload(cloud)
     out = _r.render_forward(dev_cloud, cam, _settings(settings))
-    vis = out.visible.cpu().numpy()
-    # reference TileBins index the compacted visible set (rasterizer.py:177-188)
-    remap = np.cumsum(vis) - 1
-    ids = out._tiles.indices.cpu().numpy().astype(np.int64)
-    bins = TileBinsNP(out._tiles.offsets.cpu().numpy().astype(np.int64), remap[ids], out._tiles.tiles_x,
-                      out._tiles.tiles_y)
-    return RenderOutputNP(
-        image=_np64(out.image), transmittance=_np64(out.transmittance), weight_sum=_np64(out.weight_sum),
-        n_contrib=out.n_contrib.cpu().numpy(), last_pos=out.last_pos.cpu().numpy(), visible=vis,
-        screen_areas=_np64(out.screen_areas),
-        hit_counts=out.hit_counts.cpu().numpy() if out.hit_counts is not None else None,
-        hit_records=out.hit_records, _tiles=bins, _device=(dev_cloud, out))
+    h = _host(dict(image=out.image, transmittance=out.transmittance, weight_sum=out.weight_sum,
+                   n_contrib=out.n_contrib, last_pos=out.last_pos, visible=out.visible, screen_areas=out.screen_areas,
+                   hit_counts=out.hit_counts))
+    # the reference TileBins (indexing the compacted visible set, rasterizer.py:177-188)
+    # are made from the device lists on first access (RenderOutputNP._tiles)
+    return RenderOutputNP(**h, hit_records=out.hit_records, _device=(dev_cloud, out))
 
 
 def render_backward(cloud, cam, settings, dimage, output) -> CloudGradsNP:
@@ -115,7 +151,12 @@ def render_backward(cloud, cam, settings, dimage, output) -> CloudGradsNP:
                                   last_pos=torch.from_numpy(np.asarray(output.last_pos)), visible=None,
                                   screen_areas=None)
     g = _r.render_backward(dev_cloud, cam, _settings(settings), np.asarray(dimage), dev_out)
-    return CloudGradsNP(**{f: _np64(getattr(g, f)) for f in FIELDS + ("mean2d_screen",)})
+    flat = _host({"g": g.flat})["g"]  # one transfer of every field (widened on the GPU), then views
+    out = {}
+    for f in FIELDS + ("mean2d_screen",):
+        o, size = g._layout_map[f]
+        out[f] = flat[o:o + size].reshape(tuple(getattr(g, f).shape))
+    return CloudGradsNP(**out)
 
 
 def bin_tiles(means2d, radii, depths, width, height, tile_size) -> TileBinsNP:
