@@ -24,6 +24,12 @@ __device__ __forceinline__ void put(float *p, float v) {
 // the parameters are read once per step instead of once per view.  The sum of
 // per-view reference gradients (rasterizer.py:375-419) up to float reassociation.
 constexpr int kMaxViews = 8;
+// 4 CTAs/SM: <= 128 registers (no spills) and 47.6 KB dynamic smem per CTA (the drest
+// stage aliases the sh_rest stage); 3 CTAs/SM with separate stages measured 0.414 ms/step
+// vs 0.371 on c3 (profiles/r02_ab_pb_alias.log)
+#ifndef TGS_PB_MINB
+#define TGS_PB_MINB 4
+#endif
 
 struct ViewBatch {
   tgs_camera cam[kMaxViews];
@@ -36,15 +42,17 @@ struct ViewBatch {
 };
 
 template <int DEG, bool kAcc>
-__global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
+__global__ void __launch_bounds__(kPreBlock, TGS_PB_MINB) k_preprocess_bwd_views(tgs_cloud cl, ViewBatch vb, tgs_settings s,
                                                                     tgs_grads g) {
-  // dynamic shared memory: sh_rest stage, drest stage, and per view the view
+  // dynamic shared memory: sh_rest stage (reused as the drest stage), and per view the view
   // direction and clamped colour upstream for the SH-rest gradient
   // sum_v basis(dir_v) (x) dcolor_v, accumulated in registers after the view loop
   extern __shared__ __align__(16) float pb_smem[];
   float *rest_s = pb_smem;
-  float *drest_s = pb_smem + kPreBlock * 45;
-  float(*vd_s)[6][kPreBlock] = reinterpret_cast<float(*)[6][kPreBlock]>(pb_smem + 2 * kPreBlock * 45);
+  // the drest stage overwrites the thread's own sh_rest row, entry by entry after its last
+  // read (the d_band loop below), so one 45-float row per thread serves both
+  float *drest_s = pb_smem;
+  float(*vd_s)[6][kPreBlock] = reinterpret_cast<float(*)[6][kPreBlock]>(pb_smem + kPreBlock * 45);
   constexpr int K = (DEG + 1) * (DEG + 1) - 1;
   const int64_t base = (int64_t)blockIdx.x * kPreBlock;
   const int count = (int)(cl.n - base < kPreBlock ? cl.n - base : kPreBlock);
@@ -55,7 +63,6 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     bulk = stage_rest_issue(cl.sh_rest, base, count, rest_s, &rest_bar);  // TMA, overlaps the loads below
     if (!bulk) stage_rest(cl.sh_rest, base, count, rest_s);
   }
-  for (int j = threadIdx.x; j < kPreBlock * 45; j += kPreBlock) drest_s[j] = 0.0f;
   __syncthreads();
   const int64_t i = base + threadIdx.x;
   const bool live = (int)threadIdx.x < count;
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
           my_drest[3 * k + c] = dr[3 * k + c] * mb;
         }
       }
+      for (int k = 3 * K; k < 45; ++k) my_drest[k] = 0.0f;
     }
     // ---- view-independent state again (recomputed rather than kept live across the loop)
     float s_raw[3], sc[3], Rg[9], L[9], qn[4], qnorm;
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
     __syncthreads();
     float *dst = g.sh_rest + base * 45;
     const int total = count * 45;
-    for (int j = threadIdx.x; j < total; j += blockDim.x) put<kAcc>(dst + j, drest_s[j]);
+    for (int j = threadIdx.x; j < total; j += blockDim.x) put<kAcc>(dst + j, rest_grads ? drest_s[j] : 0.0f);
   }
   // ---- the consumer clears: every view's partial rows of this CTA back to zero, so the
   // next step's blend backward can accumulate into them without a separate fill launch
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(kPreBlock, 3) k_preprocess_bwd_views(tgs_cloud
 
 using namespace tgs;
 
-constexpr int kPbSmem = (2 * kPreBlock * 45 + kMaxViews * 6 * kPreBlock) * (int)sizeof(float);
+constexpr int kPbSmem = (kPreBlock * 45 + kMaxViews * 6 * kPreBlock) * (int)sizeof(float);
 
 static int launch_bwd_views(const tgs_cloud *cloud, const ViewBatch &vb, const tgs_settings *s, tgs_grads *grads,
                             bool accumulate, cudaStream_t st) {
