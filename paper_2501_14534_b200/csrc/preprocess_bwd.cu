@@ -26,7 +26,7 @@ __device__ __forceinline__ void put(float *p, float v) {
 constexpr int kMaxViews = 8;
 // 4 CTAs/SM: <= 128 registers (no spills) and 47.6 KB dynamic smem per CTA (the drest
 // stage aliases the sh_rest stage); 3 CTAs/SM with separate stages measured 0.414 ms/step
-// vs 0.371 on c3 (profiles/r02_ab_pb_alias.log)
+// vs 0.371 on c3 (profiles/r02_ab_late.log)
 #ifndef TGS_PB_MINB
 #define TGS_PB_MINB 4
 #endif
