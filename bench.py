@@ -57,7 +57,9 @@ def parse():
                    help="N > 1: time rank 0's share of an N-GPU ZeRO-1 step on this one GPU and print a projected "
                         "N-GPU step (measured share + an NCCL reduce-scatter/all-gather bandwidth model)")
     p.add_argument("--nvlink-gbs", type=float, default=720.0,
-                   help="--rank-share model: NCCL reduce-scatter / all-gather bus bandwidth per GPU, GB/s")
+                   help="--rank-share model: NCCL reduce-scatter / all-gather / all-to-all bus bandwidth per GPU, GB/s")
+    p.add_argument("--dp", choices=("zero", "gaussians"), default="gaussians",
+                   help="data-parallel design for N > 1 and --rank-share (train.Trainer dp_mode)")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -68,11 +70,17 @@ def settings_kwargs():
                 sh_mask_threshold=0.1, compute_sh_rest_grads=True, background=(0.0, 0.0, 0.0))
 
 
-def config_dict(n, world):
+DP_DESIGNS = {"gaussians": "Gaussian-sharded: this rank's rows of every view's preprocess, NCCL all-to-all of the "
+                            "preprocess outputs and splat partials, preprocess backward + Adam on this rank's rows",
+              "zero": "ZeRO-1: NCCL reduce-scatter of the flat gradient, Adam on this rank's 1/N, all-gather of the "
+                      "parameters"}
+
+
+def config_dict(n, world, dp="gaussians"):
     return {"workload": "c3: BASELINE.json configs[2] training step", "gaussians": n, "sh_degree": 3,
             "views_per_step": VIEWS, "resolution": "1920x1080", "tile": 16, "loss": "0.8*L1 + 0.2*D-SSIM (11x11)",
             "mask_threshold": 0.01, "sh_mask_threshold": 0.1, "optimizer": "Adam, 8 groups",
-            "parallelism": f"dp{world} (views sharded, NCCL all-reduce of the flat gradient buffer)",
+            "parallelism": f"dp{world} (views sharded; {DP_DESIGNS[dp]})" if world > 1 else "dp1 (one GPU, no exchange)",
             "l2": "inputs larger than L2: params+grads+Adam moments = 1.0 GB touched per step",
             "timing": "fixed workload: each timed step starts from the initial parameters and Adam state "
                       "(restored outside the step's CUDA events); per-step device times summed, max over ranks"}
@@ -380,7 +388,7 @@ def main():
     targets = [None] * VIEWS
     for v in views:
         targets[v] = host_targets[v].to(dev)
-    trainer = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, process_group=pg, views=views)
+    trainer = Trainer(cloud, sc.cameras, targets, st, LAMBDA_SSIM, process_group=pg, views=views, dp_mode=args.dp)
 
     def barrier():
         if pg is not None:
@@ -516,7 +524,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_dev / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE.json config 3 generator; random-init Gaussians, U[0,1] targets)",
-            "config": config_dict(len(cloud), world),
+            "config": config_dict(len(cloud), world, args.dp),
             "e2e": {"value": round(args.steps / t_e2e, 4), "unit": "train step/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "roofline": rf, "stages": stages,
@@ -600,16 +608,18 @@ def gpu_busy(fn, k: int) -> dict:
 
 def rank_share(args):
     """Projection of the N-GPU c3 step from ONE GPU (only one GPU is available to this
-    build): rank 0's share of an N-rank ZeRO-1 step — its views (0, N, 2N, ...), the
-    multi-view preprocess forward / backward of those views and the fused Adam on its 1/N
-    parameter shard (train.Trainer(zero_sim=(0, N))) — timed exactly like the bench's
-    fixed-workload step, plus the reduce-scatter and all-gather of the step's parameter
-    range at an assumed NCCL bus bandwidth (--nvlink-gbs), NOT overlapped with compute
-    (the real step overlaps chunk k's all-gather with chunk k+1's Adam).  Measured for the
-    bench's step (every gradient, SH-rest included: 252 B/Gaussian exchanged) and for the
-    SH-cadence steps in between (compute_sh_rest_grads off, rasterizer.py:88-92: sh_rest
-    neither differentiated nor updated nor exchanged), and as the schedule average of one
-    cadence step per 16."""
+    build): rank 0's share of an N-rank step, timed exactly like the bench's fixed-workload
+    step, plus the step's NCCL exchange at an assumed bus bandwidth (--nvlink-gbs), NOT
+    overlapped with compute.  --dp gaussians (default, train.Trainer(gshard_sim=(0, N))):
+    its views (0, N, 2N, ...), the preprocess forward / backward of every view over its 1/N
+    rows of the cloud and Adam on those rows; exchange = the all-to-alls of its views'
+    preprocess outputs and splat partials.  --dp zero (Trainer(zero_sim=(0, N))): its views,
+    the multi-view preprocess forward / backward of those views over the whole cloud and
+    Adam on its 1/N parameter shard; exchange = reduce-scatter + all-gather of the step's
+    parameter range.  Measured for the bench's step (every gradient, SH-rest included) and
+    for the SH-cadence steps in between (compute_sh_rest_grads off, rasterizer.py:88-92:
+    sh_rest neither differentiated nor updated), as the schedule average of one cadence
+    step per 16, and with steps enqueued back to back ("continuous")."""
     import dataclasses
 
     import torch
@@ -625,13 +635,16 @@ def rank_share(args):
     st_full = RenderSettings(**settings_kwargs())
     cloud = GaussianCloud.from_fields(sc.fields, device=dev)
     views = list(range(0, VIEWS, N))
+    gs = args.dp == "gaussians"
+    share_kw = (dict(views=views, dp_mode="gaussians", gshard_sim=(0, N),
+                     all_views=[list(range(d, VIEWS, N)) for d in range(N)]) if gs else dict(views=views, zero_sim=(0, N)))
     targets = [None] * VIEWS
     for v in views:
         targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
-    out = {}
+    out, cont = {}, {}
     for rest in (True, False):
         st = dataclasses.replace(st_full, compute_sh_rest_grads=rest)
-        for label, kw in (("share", dict(views=views, zero_sim=(0, N))), ("full", dict(views=list(range(VIEWS))))):
+        for label, kw in (("share", share_kw), ("full", dict(views=list(range(VIEWS))))):
             if label == "full":
                 for v in range(VIEWS):
                     targets[v] = torch.from_numpy(sc.targets[v]).to(dev)
@@ -653,23 +666,55 @@ def rank_share(args):
                 e.synchronize()
                 total += s.elapsed_time(e)
             tr.check_divergence()
+            # the same fixed workload without the host synchronisation before every step:
+            # each step's restore is enqueued ahead of it (outside its events), so the host
+            # prepares step k+1 while the GPU runs step k, as in back-to-back training
+            evs = []
+            for _ in range(args.steps):
+                cloud.flat.copy_(init[0])
+                tr.opt.m.copy_(init[1])
+                tr.opt.v.copy_(init[2])
+                tr.opt.steps = dict(init[3])
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                tr.step()
+                e.record()
+                evs.append((s, e))
+            torch.cuda.synchronize()
+            tr.check_divergence()
+            cont[(rest, label)] = sum(a.elapsed_time(b) for a, b in evs) / args.steps
             cloud.flat.copy_(init[0])
             out[(rest, label)] = total / args.steps
         for v in range(VIEWS):
             targets[v] = torch.from_numpy(sc.targets[v]).to(dev) if v in views else None
     res = {}
+    from paper_2501_14534_b200.parallel import GSHARD_BWD_BYTES, GSHARD_FWD_BYTES
     for rest in (True, False):
-        pbytes = sum(ch.end - ch.begin for ch in zero_plan(cloud._layout_map, N, rest_grads=rest)) * 4
-        comm_ms = 2 * (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
+        if gs:  # per rank: its views' preprocess outputs in, their splat partials out (all-to-alls)
+            pbytes = len(views) * len(cloud) * (GSHARD_FWD_BYTES + GSHARD_BWD_BYTES)
+            comm_ms = (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
+        else:
+            pbytes = sum(ch.end - ch.begin for ch in zero_plan(cloud._layout_map, N, rest_grads=rest)) * 4
+            comm_ms = 2 * (N - 1) / N * pbytes / (args.nvlink_gbs * 1e9) * 1e3
         res[rest] = dict(share=out[(rest, "share")], full=out[(rest, "full")], comm=comm_ms, bytes=pbytes,
                          proj=out[(rest, "share")] + comm_ms)
     avg = lambda k: (res[True][k] + 15 * res[False][k]) / 16  # noqa: E731
     proj, full = res[True]["proj"], res[True]["full"]
-    print(json.dumps({"metric": f"projected c3 train step/s at {N} GPUs (1-GPU rank-share measurement + NCCL model)",
+    design = "Gaussian-sharded" if gs else "ZeRO-1"
+    print(json.dumps({"metric": f"projected c3 train step/s at {N} GPUs ({design}: 1-GPU rank-share measurement + "
+                                f"NCCL model)",
                       "value": round(1e3 / proj, 3), "unit": "train step/s", "n_gpus": 1, "projected_n_gpus": N,
                       "ms_per_step_projected": round(proj, 3), "ms_rank_share_measured": round(res[True]["share"], 3),
                       "ms_comm_model": round(res[True]["comm"], 3), "ms_per_step_1gpu_measured": round(full, 3),
-                      "projected_speedup": round(full / proj, 3),
+                      "projected_speedup": round(full / proj, 3), "dp": args.dp,
+                      "continuous": {"ms_rank_share_measured": round(cont[(True, "share")], 3),
+                                     "ms_per_step_1gpu_measured": round(cont[(True, "full")], 3),
+                                     "ms_per_step_projected": round(cont[(True, "share")] + res[True]["comm"], 3),
+                                     "projected_speedup": round(cont[(True, "full")] /
+                                                                (cont[(True, "share")] + res[True]["comm"]), 3),
+                                     "how": "same fixed workload, steps enqueued back to back (no host sync "
+                                            "between steps; restores enqueued outside each step's events)"},
+                      "projected_speedup_at_half_bandwidth": round(full / (proj + res[True]["comm"]), 3),
                       "sh_cadence_step": {"ms_rank_share_measured": round(res[False]["share"], 3),
                                           "ms_comm_model": round(res[False]["comm"], 3),
                                           "exchanged_bytes": res[False]["bytes"],
@@ -680,11 +725,14 @@ def rank_share(args):
                                                    "ms_per_step_1gpu_measured": round(avg("full"), 3),
                                                    "projected_speedup": round(avg("full") / avg("proj"), 3)},
                       "views_on_rank0": views,
-                      "comm_model": f"reduce-scatter + all-gather of the step's parameter range ({res[True]['bytes']} B; "
-                                    f"{res[False]['bytes']} B on SH-cadence steps) at {args.nvlink_gbs} GB/s NCCL bus "
-                                    f"bandwidth, not overlapped",
+                      "comm_model": (f"all-to-all of rank 0's views' preprocess outputs ({GSHARD_FWD_BYTES} B per "
+                                     f"Gaussian and view) and splat partials ({GSHARD_BWD_BYTES} B): {res[True]['bytes']} B "
+                                     f"x (N-1)/N at {args.nvlink_gbs} GB/s NCCL bus bandwidth, not overlapped" if gs else
+                                     f"reduce-scatter + all-gather of the step's parameter range ({res[True]['bytes']} B; "
+                                     f"{res[False]['bytes']} B on SH-cadence steps) at {args.nvlink_gbs} GB/s NCCL bus "
+                                     f"bandwidth, not overlapped"),
                       "higher_is_better": True, "dtype": "f32", "data": "synthetic (seeded BASELINE.json config 3)",
-                      "config": config_dict(len(cloud), N)}), flush=True)
+                      "config": config_dict(len(cloud), N, args.dp)}), flush=True)
 
 
 def _c5_shell_targets(sc, views, st0, args, dev):

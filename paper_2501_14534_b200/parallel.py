@@ -292,3 +292,89 @@ def grad_buckets(layout: dict, rest_grads: bool = True) -> list[tuple[tuple[str,
     out.append((("mask_logits", "sh_mask_logits"), layout["mask_logits"][0],
                 end("sh_mask_logits" if rest_grads else "mask_logits")))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Gaussian-sharded data parallelism (train.Trainer dp_mode="gaussians").  Rank r owns
+# cloud rows shard_rows(n, world)[r]: it runs the multi-view preprocess of EVERY view of
+# the step over its rows only, and one all-to-all per view slot delivers to each view's
+# owner the full per-Gaussian preprocess outputs of its view (rows arrive in rank order,
+# which is the cloud's row order, so the depth sort and the blends are the single-GPU
+# ones bit for bit).  After the view's blend backward, a second all-to-all returns each
+# shard's rows of the view's splat partials to the shard owner, which runs the multi-view
+# preprocess backward and Adam over its rows only.  Per step and rank this exchanges the
+# preprocess outputs (GSHARD_FWD_BYTES per Gaussian and view) and the splat partials
+# (36 B) instead of ZeRO-1's reduce-scatter + all-gather of the 252 B/Gaussian parameter
+# range, and the preprocess forward / backward and Adam are 1/world of the cloud.
+
+# splats (12 f32), visible (u8), tiles_touched (i32), depth keys (i64), exact records (8 f32)
+GSHARD_FWD_KINDS = ((0, 48), (1, 1), (2, 4), (3, 8), (5, 32))
+GSHARD_FWD_BYTES = sum(b for _, b in GSHARD_FWD_KINDS)
+GSHARD_BWD_BYTES = 36
+
+
+def shard_rows(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous row shards of a cloud of n rows, one per rank, in rank order; shard
+    starts are multiples of 64 (Adam's per-field row ranges, train._row_ranges)."""
+    world = max(1, int(world))
+    per = -(-max(n, 1) // world)
+    per = -(-per // 64) * 64
+    return [(min(n, r * per), min(n, (r + 1) * per)) for r in range(world)]
+
+
+def slot_order(views_of: list[list[int]]) -> list[int]:
+    """The step's global view order for the shard-local preprocess: slot-major (slot j:
+    view j of rank 0, of rank 1, ...), so that slot j's outputs for all ranks are one
+    contiguous block — the all-to-all's input.  Every rank must own the same number of
+    views."""
+    k = len(views_of[0]) if views_of else 0
+    if any(len(v) != k for v in views_of):
+        raise ValueError("dp_mode='gaussians' needs the same number of views on every rank")
+    return [views_of[d][j] for j in range(k) for d in range(len(views_of))]
+
+
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits: list[int], in_splits: list[int], group) -> None:
+    dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=group)
+
+
+def gshard_forward_exchange(sub: list, full: list, rows: list[tuple[int, int]], rank: int, group=None) -> None:
+    """Slot j of every rank's shard outputs to slot j's view owners.
+
+    sub:  per output kind, the shard-local preprocess buffer [V][n_rank][...] of this rank
+          (V = k x world views in slot_order);
+    full: per output kind, this rank's own views' full buffers [k][n][...];
+    group None: no communication, only this rank's own rows are written into `full`
+    (single-GPU simulation of one rank's share, bench.py --rank-share --dp gaussians)."""
+    world = len(rows)
+    a, b = rows[rank]
+    for s, f in zip(sub, full):
+        k = f.shape[0]
+        w = s[0, 0].numel() if s.dim() > 2 else 1
+        for j in range(k):
+            blk = s[j * world:(j + 1) * world]
+            if group is None:
+                f[j, a:b].copy_(blk[rank, :b - a])
+                continue
+            _a2a(f[j].reshape(-1), blk[:, :b - a].reshape(-1), [(e - d) * w for d, e in rows], [(b - a) * w] * world,
+                 group)
+
+
+def gshard_backward_exchange(own: list, sub: torch.Tensor, rows: list[tuple[int, int]], rank: int,
+                             group=None) -> None:
+    """Each own view's splat partials (own[j]: [n][9]) back to the shard owners: rank r
+    receives rows rows[r] of every view, as sub[j * world + d] = partials of slot j's view
+    of rank d ([V][n_rank][9], slot_order).  group None: only this rank's own rows."""
+    world = len(rows)
+    a, b = rows[rank]
+    for j, p in enumerate(own):
+        blk = sub[j * world:(j + 1) * world]
+        if group is None:
+            blk[rank, :b - a].copy_(p[a:b])
+            continue
+        out = blk[:, :b - a]
+        if out.is_contiguous():
+            _a2a(out.reshape(-1), p.reshape(-1), [(b - a) * 9] * world, [(e - d) * 9 for d, e in rows], group)
+        else:  # (an empty shard's one-row padding)
+            tmp = torch.empty_like(out)
+            _a2a(tmp.reshape(-1), p.reshape(-1), [(b - a) * 9] * world, [(e - d) * 9 for d, e in rows], group)
+            out.copy_(tmp)

@@ -356,8 +356,31 @@ def preprocess(cloud: GaussianCloud, cam: Camera, settings: RenderSettings):
     return splats, vis, tiles, keys, err, exact
 
 
+_ROW_BYTES = None  # bytes per cloud row of each parameter field (cloud._ROW)
+
+
+def _offset_rows(c_cloud, c_grads, c_stats, r0: int, r1: int) -> None:
+    """Point native cloud / gradient / statistics structs at cloud rows [r0, r1) (in place:
+    every per-row field pointer advanced by r0 rows, n = r1 - r0)."""
+    global _ROW_BYTES
+    if _ROW_BYTES is None:
+        from .cloud import PARAM_FIELDS, _ROW
+        _ROW_BYTES = tuple((f, 4 * int(np.prod(_ROW[f]))) for f in PARAM_FIELDS)
+    for f, w in _ROW_BYTES:
+        setattr(c_cloud, f, getattr(c_cloud, f) + w * r0)
+        if c_grads is not None:
+            setattr(c_grads, f, getattr(c_grads, f) + w * r0)
+    if c_grads is not None:
+        c_grads.mean2d_screen = c_grads.mean2d_screen + 4 * 2 * r0 if c_grads.mean2d_screen else None
+    c_cloud.n = r1 - r0
+    if c_stats is not None:
+        c_stats.grad_accum = c_stats.grad_accum + 4 * r0 if c_stats.grad_accum else None
+        c_stats.grad_count = c_stats.grad_count + 4 * r0 if c_stats.grad_count else None
+        c_stats.area_max = c_stats.area_max + 4 * r0 if c_stats.area_max else None
+
+
 def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, stats=None,
-                     exact: bool = True, cache: dict | None = None, c_cams=None) -> list:
+                     exact: bool = True, cache: dict | None = None, c_cams=None, rows: tuple | None = None) -> list:
     """tgs_preprocess_forward_views: the per-view preprocess outputs of a batch of views in
     one pass over the parameters; element v is what `preprocess(cloud, cams[v], settings)`
     returns (bit-identical), the error flag shared.  stats: optional train.DensifyStats
@@ -367,13 +390,16 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
     Trainer): the output buffers, their per-view views and the pointer arrays are made
     once per (views, rows) and reused — the previous call's outputs are overwritten, so
     their consumers must be ordered before this call on the stream (~0.15 ms of host
-    work per step saved, all of it GPU idle at the start of a step)."""
+    work per step saved, all of it GPU idle at the start of a step).
+    rows=(r0, r1): only cloud rows [r0, r1) — a rank's Gaussian shard (train.Trainer
+    dp_mode="gaussians"); the outputs then have r1 - r0 rows, row i being cloud row r0 + i."""
     import ctypes
-    n = len(cloud)
+    r0, r1 = rows if rows is not None else (0, len(cloud))
+    n = max(r1 - r0, 0)
     dev = cloud.device
     V = len(cams)
     m = max(n, 1)
-    key = (V, m, dev)
+    key = (V, m, dev, r0)
     ent = cache.get(key) if cache is not None else None
     if ent is None:
         err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -402,6 +428,8 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
             c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
         with stage("preprocess_fwd"):
             c_stats = stats.native() if stats is not None else None
+            if rows is not None:
+                _offset_rows(c_cloud, None, c_stats, r0, r1)
             _lib.call("tgs_preprocess_forward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), V, ptrs[0],
                       ptrs[1], ptrs[2], ptrs[3], _lib.ptr(err), ctypes.byref(c_stats) if c_stats else None,
                       ptrs[5] if exact else None, _lib.stream_handle(dev))
@@ -409,18 +437,22 @@ def preprocess_views(cloud: GaussianCloud, cams: list, settings: RenderSettings,
 
 
 def exact_records(cloud: GaussianCloud, cams: list, settings: RenderSettings, pres: list,
-                  cache: dict | None = None, c_cams=None) -> None:
+                  cache: dict | None = None, c_cams=None, rows: tuple | None = None) -> None:
     """tgs_exact_records_views on the current stream: the exact blend-decision records
     (include/tgs.h TGS_EXACT_FLOATS) of preprocess_views(..., exact=False) outputs.
-    cache: preprocess_views' cache of the same call (its pointer arrays are reused)."""
+    cache: preprocess_views' cache of the same call (its pointer arrays are reused).
+    rows: the preprocess_views call's row range."""
     import ctypes
-    n, V = len(cloud), len(cams)
+    r0, r1 = rows if rows is not None else (0, len(cloud))
+    n, V = max(r1 - r0, 0), len(cams)
     if n == 0 or V == 0:
         return
     c_cloud, c_set = cloud.native(), _lib.make_settings(settings)
+    if rows is not None:
+        _offset_rows(c_cloud, None, None, r0, r1)
     if c_cams is None:
         c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
-    ent = cache.get((V, max(n, 1), cloud.device)) if cache is not None else None
+    ent = cache.get((V, max(n, 1), cloud.device, r0)) if cache is not None else None
     if ent is not None and ent[0] is pres:
         sps, exs = ent[1][0], ent[1][5]
     else:
@@ -757,14 +789,18 @@ def blend_backward(cloud: GaussianCloud, cam: Camera, settings: RenderSettings, 
 
 def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: RenderSettings, visibles: list,
                               dsplats: list, grads: CloudGrads, accumulate: bool = False, stats=None,
-                              clear: bool = False, rows: tuple | None = None) -> CloudGrads:
+                              clear: bool = False, rows: tuple | None = None, local: bool = False,
+                              c_cams=None) -> CloudGrads:
     """Second half of render_backward for a batch of views in ONE pass over the
     parameters (tgs_preprocess_backward_views): grads (+)= sum over views.  stats:
     optional train.DensifyStats, accumulating each view's screen-space gradient norm
     (training.py:333-337).  clear=True zeroes every dsplats[v] after reading it (the
     training loop's buffers are then ready for the next step's blend backward).
     rows=(r0, r1): only cloud rows [r0, r1) (r0 a multiple of 64) — a chunk of a pipelined
-    step whose Adam updates the finished rows while the next chunk runs."""
+    step whose Adam updates the finished rows while the next chunk runs.  local=True: the
+    visibles / dsplats hold only those rows (a Gaussian shard's, train.Trainer
+    dp_mode="gaussians"), row i being cloud row r0 + i.  c_cams: a caller's prebuilt
+    camera array of `cams`."""
     import ctypes
     n = len(cloud)
     if n == 0 or not cams:
@@ -773,26 +809,16 @@ def preprocess_backward_views(cloud: GaussianCloud, cams: list, settings: Render
     r0, r1 = rows if rows is not None else (0, n)
     if r1 <= r0:
         return grads
-    c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
-    vis_ptrs = (ctypes.c_void_p * V)(*[v.data_ptr() + r0 for v in visibles])
-    ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() + 36 * r0 for d in dsplats])
+    if c_cams is None:
+        c_cams = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in cams])
+    o = 0 if local else r0
+    vis_ptrs = (ctypes.c_void_p * V)(*[v.data_ptr() + o for v in visibles])
+    ds_ptrs = (ctypes.c_void_p * V)(*[d.data_ptr() + 36 * o for d in dsplats])
     c_set = _lib.make_settings(settings)
     c_cloud, c_grads = cloud.native(), grads.native()
     c_stats = stats.native() if stats is not None else None
     if rows is not None:  # the same structs over the row sub-range (pointer offsets)
-        from .cloud import _ROW
-        f4 = 4
-        for f in ("positions", "log_scales", "rotations", "opacity_logits", "sh_dc", "sh_rest", "mask_logits",
-                  "sh_mask_logits"):
-            w = int(np.prod(_ROW[f]))
-            setattr(c_cloud, f, getattr(c_cloud, f) + f4 * w * r0)
-            setattr(c_grads, f, getattr(c_grads, f) + f4 * w * r0)
-        c_grads.mean2d_screen = c_grads.mean2d_screen + f4 * 2 * r0 if c_grads.mean2d_screen else None
-        c_cloud.n = r1 - r0
-        if c_stats is not None:
-            c_stats.grad_accum = c_stats.grad_accum + 4 * r0 if c_stats.grad_accum else None
-            c_stats.grad_count = c_stats.grad_count + 4 * r0 if c_stats.grad_count else None
-            c_stats.area_max = c_stats.area_max + 4 * r0 if c_stats.area_max else None
+        _offset_rows(c_cloud, c_grads, c_stats, r0, r1)
     with stage("preprocess_bwd"):
         _lib.call("tgs_preprocess_backward_views", ctypes.byref(c_cloud), c_cams, ctypes.byref(c_set), vis_ptrs,
                   ds_ptrs, V, ctypes.byref(c_grads), int(bool(accumulate)),

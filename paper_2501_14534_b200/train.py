@@ -44,7 +44,7 @@ def _row_ranges(layout: dict, names, n: int, r0: int, r1: int) -> list:
     out = []
     for f in sorted(names, key=lambda f: layout[f][0]):
         off, size = layout[f]
-        w = int(np.prod(_ROW[f]))
+        w = math.prod(_ROW[f])
         end = off + (size + 63) // 64 * 64 if r1 >= n else off + r1 * w
         out.append((off + r0 * w, end))
     return out
@@ -94,7 +94,7 @@ class Trainer:
                  lrs: dict | None = None, lambda_m: float = 0.05, lambda_sh: float = 0.05, process_group=None,
                  views=None, streams: int = 4, deterministic: bool = False, densify_stats: bool = False,
                  dp_mode: str = "zero", zero_chunks: int = 4, zero_sim: tuple | None = None,
-                 native: bool | None = None):
+                 native: bool | None = None, all_views: list | None = None, gshard_sim: tuple | None = None):
         self.cloud = cloud
         self.cameras = cameras
         self.targets = targets              # list of (H, W, 3) float32 device tensors (this rank's views)
@@ -105,10 +105,14 @@ class Trainer:
         self.pg = process_group
         # data parallelism (process_group given): "zero" = ZeRO-1 (reduce-scatter, Adam on this
         # rank's shard, all-gather; parallel.zero_plan), "allreduce" = bucketed all-reduce +
-        # replicated Adam.  zero_sim=(rank, world): one GPU runs rank `rank`'s share of a
-        # world-rank step without communication (bench.py --rank-share projections).
-        if dp_mode not in ("zero", "allreduce"):
-            raise ValueError("dp_mode must be 'zero' or 'allreduce'")
+        # replicated Adam, "gaussians" = Gaussian-sharded (parallel.py: this rank's rows of
+        # every view's preprocess, all-to-all exchanges of the preprocess outputs and the splat
+        # partials, preprocess backward and Adam on this rank's rows; all_views = every
+        # rank's view list, gathered when not given).  zero_sim=(rank, world) /
+        # gshard_sim=(rank, world): one GPU runs rank `rank`'s share of a world-rank ZeRO-1 /
+        # Gaussian-sharded step without communication (bench.py --rank-share projections).
+        if dp_mode not in ("zero", "allreduce", "gaussians"):
+            raise ValueError("dp_mode must be 'zero', 'allreduce' or 'gaussians'")
         self.dp_mode, self.zero_chunks, self.zero_sim = dp_mode, int(zero_chunks), zero_sim
         # native=True: the per-view loop (bin, count, place, blend, loss, backward) is issued
         # from C++ (tgs_train_views) when the views are pipelined over >= 2 streams and the
@@ -122,6 +126,25 @@ class Trainer:
         if process_group is not None:
             import torch.distributed as dist
             self.rank = dist.get_rank(process_group)
+        self._gs = None  # Gaussian-sharded state (dp_mode="gaussians")
+        if dp_mode == "gaussians" and (process_group is not None or gshard_sim is not None):
+            from .parallel import slot_order
+            if process_group is not None:
+                import torch.distributed as dist
+                rank, world = self.rank, dist.get_world_size(process_group)
+                if all_views is None:
+                    all_views = [None] * world
+                    dist.all_gather_object(all_views, self.views, group=process_group)
+            else:
+                rank, world = gshard_sim
+                if all_views is None:
+                    raise ValueError("gshard_sim needs all_views (every rank's view list)")
+            if list(all_views[rank]) != self.views:
+                raise ValueError("all_views[rank] must be this rank's views")
+            self._gs = dict(rank=int(rank), world=int(world), order=slot_order([list(v) for v in all_views]), n=None)
+        # the exact records inside the shard preprocess launch (one host call less before the
+        # views' first launch) or as their own launch on the exact stream (TGS_GS_EXACT=side)
+        self._gs_exact_inline = os.environ.get("TGS_GS_EXACT", "inline") == "inline"
         self.grads = CloudGrads(len(cloud), cloud.device)
         self.opt = Adam(cloud, lrs or DEFAULT_LRS)
         dev = cloud.device
@@ -162,6 +185,8 @@ class Trainer:
         self.comm_stream = None  # data-parallel gradient reduction (created on first use)
         self.launches_per_step = 0
         self.deterministic = deterministic  # fixed-order gradient sums (bitwise reproducible steps)
+        if self._gs is not None and (not self.native or deterministic or len(self.streams) < 2):
+            raise ValueError("dp_mode='gaussians' runs the native multi-stream views path")
         # per-view densification statistics, accumulated inside the preprocess kernels
         self.stats = DensifyStats(len(cloud), dev) if densify_stats else None
         self.iteration = 0
@@ -183,6 +208,7 @@ class Trainer:
         tgs_gather_rows (optim.py:51-55) and resize the gradient buffers.  Returns the
         new Gaussian count."""
         from . import pruning
+        self.sync_shards()
         new, keep = pruning.prune_by_mask(self.cloud, eps)
         self._apply_keep(new, keep)
         return len(self.cloud)
@@ -192,6 +218,7 @@ class Trainer:
         (significance.py:45-78), drop the floor(rate N) lowest (significance.py:81-99)
         and compact the optimizer state and statistics.  Returns the report."""
         from . import significance as sig
+        self.sync_shards()
         hits = sig.count_hits(self.cloud, cameras, settings)
         rep = sig.significance_scores(hits, self.cloud, mask_threshold=settings.mask_threshold,
                                       volume_power=volume_power)
@@ -247,6 +274,8 @@ class Trainer:
         first host read shows the flag) or by check_divergence()."""
         self.check_divergence(block=False)
         try:
+            if self._gs is not None:
+                return self._step_gshard(host_targets)
             return self._step(host_targets)
         except BaseException:
             self.dsplats = {}  # partial buffers may be left non-zero: start the next step afresh
@@ -280,8 +309,9 @@ class Trainer:
                     ev = torch.cuda.Event()
                     ev.record(self.copy_stream)
                     copied[v] = ev
+        ready = main.record_event()
         for s_ in self.streams + self.blend_streams:
-            s_.wait_stream(main)  # parameters updated by the previous step's Adam; the preprocess
+            s_.wait_event(ready)  # parameters updated by the previous step's Adam; the preprocess
         ts = int(self.settings.tile_size)
         if self.native and not self.deterministic and n and len(self.streams) >= 2 and self.views:
             vis, parts = self._views_native(pres, exact_ready, copied)
@@ -336,6 +366,146 @@ class Trainer:
                 vis.append(st_state.visible_u8)
                 parts.append(ds)
         return self._after_views(main, g, vis, parts, copied, n)
+
+    def _step_gshard(self, host_targets):
+        """Gaussian-sharded step (parallel.py, dp_mode="gaussians"): this rank's rows of
+        every view's preprocess -> all-to-all of the preprocess outputs to the view owners ->
+        this rank's views (tgs_train_views, the one-GPU schedule) -> all-to-all of the splat
+        partials back to the shard owners -> preprocess backward and Adam over this rank's
+        rows.  The parameters outside this rank's rows go stale between sync_shards() calls
+        (pruning and significance events call it); nothing in the step reads them."""
+        import torch.distributed as dist
+        from . import _lib
+        from .parallel import gshard_backward_exchange, gshard_forward_exchange, shard_rows
+        G, g = self._gs, self.grads
+        dev, n = self.cloud.device, len(self.cloud)
+        main = torch.cuda.current_stream(dev)
+        rank, world = G["rank"], G["world"]
+        if G["n"] != n:  # (re)build the shard plan and the exchange buffers for this cloud size
+            rows = shard_rows(n, world)
+            a, b = rows[rank]
+            k, V = len(self.views), len(G["order"])
+            G.update(n=n, rows=rows, err=torch.zeros(1, dtype=torch.int32, device=dev),
+                     full=[torch.empty((k, n, 12), device=dev), torch.empty((k, n), dtype=torch.uint8, device=dev),
+                           torch.empty((k, n), dtype=torch.int32, device=dev),
+                           torch.empty((k, n), dtype=torch.int64, device=dev), torch.empty((k, n, 8), device=dev)],
+                     parts=torch.zeros((V, max(b - a, 1), 9), device=dev))
+            if self.pg is None:  # simulation: every row as the exchange would deliver it for the
+                # current parameters (bench.py restores them before every step)
+                own = preprocess_views(self.cloud, [self.cameras[v] for v in self.views], self.settings)
+                for kind, f in zip((0, 1, 2, 3, 5), G["full"]):
+                    for j in range(k):
+                        f[j].copy_(own[j][kind])
+        rows = G["rows"]
+        a, b = rows[rank]
+        copied = {}
+        prev_done = main.record_event() if host_targets is not None else None
+        if self.pg is not None:
+            self.terms.zero_()
+        gcams = [self.cameras[v] for v in G["order"]]
+        V = len(gcams)
+        c_all = (_lib.TgsCamera * V)(*[_lib.make_camera(c) for c in gcams])  # once per step (~13 us)
+        self._c_cams = (_lib.TgsCamera * len(self.views))(*[_lib.make_camera(self.cameras[v]) for v in self.views])
+        # 1. this rank's rows of every view's preprocess (main stream) and their exchange to
+        # the view owners.  The exact records are computed inside the preprocess launch and
+        # travel with the other outputs (default), or (TGS_GS_EXACT=side) are their own launch
+        # and exchange on the exact stream, which only the blends wait for.
+        inline = self._gs_exact_inline
+        pres = preprocess_views(self.cloud, gcams, self.settings, stats=self.stats, exact=inline, cache=self._pre_cache,
+                                c_cams=c_all, rows=(a, b))
+        bases = self._pre_cache[(V, max(b - a, 1), dev, a)][3]  # (splats, visible, tiles, keys, exact) [V][rows]
+        full = G["full"]
+        # (simulation, no process group: nothing moves — the full buffers already hold every
+        # row, primed above, and the exchange's time is bench.py's communication model)
+        err = pres[0][4]
+        if self.pg is not None:
+            with stage("gshard_exchange"):
+                gshard_forward_exchange(list(bases) if inline else list(bases[:4]), full if inline else full[:4], rows,
+                                        rank, self.pg)
+                G["err"].copy_(err)
+                dist.all_reduce(G["err"], op=dist.ReduceOp.MAX, group=self.pg)
+                err = G["err"]
+        ready = main.record_event()  # every view stream waits for the exchanged outputs
+        if inline:
+            exact_ready = ready
+        else:
+            self.exact_stream.wait_event(ready)
+            with torch.cuda.stream(self.exact_stream):
+                exact_records(self.cloud, gcams, self.settings, pres, cache=self._pre_cache, c_cams=c_all, rows=(a, b))
+                if self.pg is not None:
+                    with stage("gshard_exchange"):
+                        gshard_forward_exchange([bases[4]], full[4:], rows, rank, self.pg)
+            exact_ready = self.exact_stream.record_event()
+        own = [(full[0][j], full[1][j], full[2][j], full[3][j], err, full[4][j]) for j in range(len(self.views))]
+        if host_targets is not None:
+            self.copy_stream.wait_event(prev_done)
+            with torch.cuda.stream(self.copy_stream):
+                for v in self.views:
+                    self.targets[v].copy_(host_targets[v], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy_stream)
+                    copied[v] = ev
+        for s_ in self.streams + self.blend_streams:
+            s_.wait_event(ready)
+        # 3. this rank's views: bin, blend, loss, blend backward (the one-GPU driver)
+        _, parts_own = self._views_native(own, exact_ready, copied)
+        for s_ in self.streams + self.blend_streams:
+            main.wait_stream(s_)
+        if not inline:
+            main.wait_stream(self.exact_stream)
+        if copied:
+            main.wait_stream(self.copy_stream)
+        steps_before = dict(self.opt.steps)
+        # 4. every view's partials of this rank's rows; the own buffers start the next step
+        # zeroed (on one GPU the preprocess backward clears them as it reads them)
+        if self.pg is not None:
+            with stage("gshard_exchange"):
+                gshard_backward_exchange(parts_own, G["parts"], rows, rank, self.pg)
+        for p in parts_own:
+            p.zero_()
+        # 5. preprocess backward and Adam over this rank's rows
+        preprocess_backward_views(self.cloud, gcams, self.settings, [p[1] for p in pres],
+                                  [G["parts"][i] for i in range(V)], g, accumulate=False, stats=self.stats,
+                                  rows=(a, b), local=True, c_cams=c_all)
+        upd = set(PARAM_FIELDS)
+        if not (self.settings.compute_sh_rest_grads and self.settings.active_sh_degree > 0):
+            upd.discard("sh_rest")
+        if self.pg is not None:
+            dist.all_reduce(self.terms, group=self.pg)
+        with stage("adam"):
+            self.opt.step(self.cloud, g, names=tuple(upd), lambda_m=self.lambda_m, lambda_sh=self.lambda_sh,
+                          guard=(self.terms, self._nonfinite),
+                          ranges=_row_ranges(g._layout_map, upd, n, a, b) if b > a else [])
+        cam0 = self.cameras[self.views[0]] if self.views else None
+        res = (int(cam0.height), int(cam0.width)) if cam0 is not None else (0, 0)
+        return self._finish(main, steps_before, n, res)
+
+    def sync_shards(self) -> None:
+        """dp_mode="gaussians": every rank's rows of the parameters, the Adam moments and the
+        densification statistics to every rank (before events that read the whole cloud:
+        pruning, significance scoring, checkpoints).  No-op otherwise."""
+        G = self._gs
+        if G is None or self.pg is None:
+            return
+        import torch.distributed as dist
+        from .parallel import shard_rows
+        n = len(self.cloud)
+        rows = shard_rows(n, G["world"])
+        bufs = []
+        for f in PARAM_FIELDS:
+            off, size = self.cloud.field_range(f)
+            w = size // max(n, 1)
+            for t in (self.cloud.flat, self.opt.m, self.opt.v):
+                bufs.append((t, off, w))
+        for d, (a, b) in enumerate(rows):
+            if b <= a:
+                continue
+            src = dist.get_global_rank(self.pg, d)
+            for t, off, w in bufs:
+                dist.broadcast(t[off + a * w: off + b * w], src=src, group=self.pg)
+            if self.stats is not None:
+                for t in (self.stats.grad_accum, self.stats.grad_count, self.stats.area_max):
+                    dist.broadcast(t[a:b], src=src, group=self.pg)
 
     def _views_native(self, pres, exact_ready, copied):
         """tgs_train_views: the views' bin -> count -> place -> blend -> loss -> backward
@@ -509,7 +679,7 @@ class Trainer:
             return self._finish(main, steps_before, n, res)
         # one pass over the parameters for all views (linear chains summed first)
         preprocess_backward_views(self.cloud, vcams, self.settings, vis, parts, g,
-                                  accumulate=False, stats=self.stats, clear=self.clear_partials)
+                                  accumulate=False, stats=self.stats, clear=self.clear_partials, c_cams=self._c_cams)
         if self.zero_sim is not None or (self.pg is not None and self.dp_mode == "zero"):
             return self._zero_update(main, g, upd, guard, steps_before, n, res)
         if self.pg is None:

@@ -1,6 +1,6 @@
 """Host side of rank 0's 1-view share of an 8-rank step (Trainer(views=[0], zero_sim=(0, 8))):
 wall vs device time per step and a cProfile of the host work.
-    python profiles/host_prof_share.py"""
+    python profiles/host_prof_share.py [zero|gaussians]"""
 import cProfile
 import os
 import pstats
@@ -19,7 +19,10 @@ sc = scenes.config3()
 st = RenderSettings(**bench.settings_kwargs())
 cloud = GaussianCloud.from_fields(sc.fields)
 targets = [torch.from_numpy(sc.targets[0]).cuda()] + [None] * 7
-tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM, views=[0], zero_sim=(0, 8))
+mode = sys.argv[1] if len(sys.argv) > 1 else "zero"
+kw = (dict(dp_mode="gaussians", gshard_sim=(0, 8), all_views=[[d] for d in range(8)]) if mode == "gaussians"
+      else dict(zero_sim=(0, 8)))
+tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM, views=[0], **kw)
 for _ in range(5):
     tr.step()
 torch.cuda.synchronize()

@@ -1,9 +1,11 @@
 """Where rank 0's share of an N-rank step goes (bench.py --rank-share N measures its total):
 a CUPTI kernel trace (torch.profiler) of 4 share steps — per-kernel time per step, the
-GPU-busy union and the idle gaps.  Usage: python profiles/rank_share_trace.py [N]"""
+GPU-busy union and the idle gaps, and the host time per step.
+Usage: python profiles/rank_share_trace.py [N] [zero|gaussians]"""
 import collections
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -20,11 +22,21 @@ st = RenderSettings(**bench.settings_kwargs())
 cloud = GaussianCloud.from_fields(sc.fields)
 views = list(range(0, 8, N))
 targets = [torch.from_numpy(t).cuda() if v in views else None for v, t in enumerate(sc.targets)]
-tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM, views=views, zero_sim=(0, N))
+mode = sys.argv[2] if len(sys.argv) > 2 else "zero"
+kw = (dict(dp_mode="gaussians", gshard_sim=(0, N), all_views=[list(range(d, 8, N)) for d in range(N)])
+      if mode == "gaussians" else dict(zero_sim=(0, N)))
+tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM, views=views, **kw)
 for _ in range(3):
     tr.step()
 torch.cuda.synchronize()
 K = 4
+host = []
+for _ in range(K):  # host time of a step (enqueue only), GPU idle at its start
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr.step()
+    host.append((time.perf_counter() - t0) * 1e6)
+torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(K):
         tr.step()
@@ -44,8 +56,8 @@ for s, e, n in iv[1:]:
         ce = max(ce, e)
 busy += ce - cs
 span = iv[-1][1] - iv[0][0]
-print(f"N={N} views {views}: span {span / K:.0f} us/step, busy {busy / K:.0f} us/step ({100 * busy / span:.1f}%), "
-      f"idle {(span - busy) / K:.0f} us/step")
+print(f"N={N} {mode} views {views}: span {span / K:.0f} us/step, busy {busy / K:.0f} us/step "
+      f"({100 * busy / span:.1f}%), idle {(span - busy) / K:.0f} us/step; host enqueue {sorted(host)[K // 2]:.0f} us/step")
 for k, v in sorted(per.items(), key=lambda x: -x[1])[:22]:
     print(f"  {v:8.1f} us/step  {k}")
 gaps.sort(reverse=True)

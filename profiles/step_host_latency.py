@@ -1,7 +1,9 @@
 """Host latency at the start of a training step (the fixed-workload bench synchronizes
 before every timed step, so the host's time to its first heavy launch is GPU idle inside
 the step): host time of each phase of Trainer._step up to the views' driver call, and the
-allocator's device-malloc count per step.    python profiles/step_host_latency.py"""
+allocator's device-malloc count per step.
+    python profiles/step_host_latency.py            (one GPU, the bench's 8-view step)
+    python profiles/step_host_latency.py gaussians  (rank 0's share of an 8-rank Gaussian-sharded step)"""
 import os
 import sys
 import time
@@ -19,7 +21,11 @@ sc = scenes.config3()
 st = RenderSettings(**bench.settings_kwargs())
 cloud = GaussianCloud.from_fields(sc.fields)
 targets = [torch.from_numpy(t).cuda() for t in sc.targets]
-tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM)
+if len(sys.argv) > 1 and sys.argv[1] == "gaussians":
+    tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM, views=[0], dp_mode="gaussians",
+                 gshard_sim=(0, 8), all_views=[[d] for d in range(8)])
+else:
+    tr = Trainer(cloud, sc.cameras, targets, st, bench.LAMBDA_SSIM)
 for _ in range(4):
     tr.step()
 torch.cuda.synchronize()

@@ -1001,3 +1001,91 @@ def test_loss_small_and_odd_images(tgs, hw):
     l1, dssim, dref = loss_ref.total_loss_image(img, tgt, 0.2)
     assert abs(terms["l1"] - l1) < 1e-6 and abs(terms["d_ssim"] - dssim) < 1e-5
     np.testing.assert_allclose(_np(d), dref, rtol=1e-3, atol=1e-4 * np.abs(dref).max())
+
+
+def test_preprocess_row_shards_equal_full_cloud(tgs):
+    """dp_mode="gaussians" runs the multi-view preprocess forward, the exact records and the
+    preprocess backward over a rank's rows only: the shards' outputs, gradients and
+    densification statistics put together equal the whole-cloud calls bit for bit
+    (4,999 rows in 3 shards, the last uneven)."""
+    from paper_2501_14534_b200 import parallel, scenes
+    from paper_2501_14534_b200.rasterizer import exact_records, preprocess_backward_views, preprocess_views
+    from paper_2501_14534_b200.train import DensifyStats
+    sc = scenes.small_scene(seed=41, n=4999, width=96, height=64, dist=3.5)
+    rng = np.random.default_rng(41)
+    cams = [sc.cameras[0]] + [scenes.pinhole(3.5 * scenes._unit(rng), 80, 64, name=f"s{k}") for k in range(2)]
+    st = tgs.RenderSettings(near=0.2, mask_threshold=0.05, sh_mask_threshold=0.1)
+    cloud = tgs.GaussianCloud.from_fields(sc.fields)
+    n = len(cloud)
+    st_full = DensifyStats(n, cloud.device)
+    full = preprocess_views(cloud, cams, st, stats=st_full, exact=False)
+    exact_records(cloud, cams, st, full)
+    g = torch.Generator("cuda").manual_seed(41)
+    ds = [torch.randn((n, 9), device="cuda", generator=g) for _ in cams]
+    gr_full = preprocess_backward_views(cloud, cams, st, [p[1] for p in full], ds, tgs.CloudGrads.zeros(n),
+                                        stats=st_full)
+    st_sh = DensifyStats(n, cloud.device)
+    gr_sh = tgs.CloudGrads.zeros(n)
+    for a, b in parallel.shard_rows(n, 3):
+        sub = preprocess_views(cloud, cams, st, stats=st_sh, exact=False, rows=(a, b))
+        exact_records(cloud, cams, st, sub, rows=(a, b))
+        for v in range(len(cams)):
+            for kind in (0, 1, 2, 3, 5):
+                assert torch.equal(sub[v][kind], full[v][kind][a:b]), (a, v, kind)
+        preprocess_backward_views(cloud, cams, st, [p[1] for p in sub], [d[a:b].contiguous() for d in ds], gr_sh,
+                                  stats=st_sh, rows=(a, b), local=True)
+    assert torch.equal(gr_sh.flat, gr_full.flat)
+    for f in ("grad_accum", "grad_count", "area_max"):
+        assert torch.equal(getattr(st_sh, f), getattr(st_full, f)), f
+
+
+def test_gaussian_sharded_trainer_single_rank_nccl(tgs):
+    """Trainer(dp_mode="gaussians") through a real NCCL group (world size 1 on this box:
+    the all-to-alls deliver every row): the step's loss terms equal the one-GPU step's
+    bit for bit and its gradient agrees to float32 atomics-order noise; with learning
+    rates the parameters after two steps agree likewise."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2501_14534_b200 import scenes
+    from paper_2501_14534_b200.train import Trainer
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        sc = scenes.small_scene(seed=43, n=20_000, width=200, height=120, dist=3.0)
+        rng = np.random.default_rng(43)
+        cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * scenes._unit(rng), 160, 96, name=f"g{k}") for k in range(3)]
+        st = tgs.RenderSettings(near=0.2, mask_threshold=0.01, sh_mask_threshold=0.1)
+        tg = [torch.rand((c.height, c.width, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(k))
+              for k, c in enumerate(cams)]
+        res = {}
+        for mode in ("gaussians", "one_gpu"):
+            c2 = tgs.GaussianCloud.from_fields(sc.fields)
+            kw = dict(process_group=dist.group.WORLD, dp_mode="gaussians") if mode == "gaussians" else {}
+            tr = Trainer(c2, cams, [t.clone() for t in tg], st, densify_stats=True, **kw)
+            lrs = dict(tr.opt.lrs)
+            for f in lrs:
+                tr.opt.set_lr(f, 0.0)
+            tr.step()
+            torch.cuda.synchronize()
+            terms, grads = tr.terms.clone(), tr.grads.flat.clone()
+            for f, lr in lrs.items():
+                tr.opt.set_lr(f, lr)
+            tr.step()
+            tr.step()
+            tr.check_divergence()
+            torch.cuda.synchronize()
+            res[mode] = (terms, grads, tr.cloud.flat.clone(), tr.stats.grad_count.clone())
+        a, b = res["gaussians"], res["one_gpu"]
+        assert torch.equal(a[0], b[0])
+        scale = float(b[1].abs().max())
+        torch.testing.assert_close(a[1], b[1], rtol=1e-3, atol=1e-5 * scale)
+        torch.testing.assert_close(a[2], b[2], rtol=1e-4, atol=1e-4)
+        assert torch.equal(a[3], b[3])
+    finally:
+        dist.destroy_process_group()

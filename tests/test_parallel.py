@@ -292,3 +292,77 @@ def test_gloo_world3_band_gather_to_rank0_assembles_frames():
     for p in procs:
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == [0, 1, 2] and all(r[1] for r in res), res
+
+
+def test_shard_rows_and_slot_order():
+    for n in (0, 1, 63, 64, 777, 1000000):
+        for world in (1, 2, 3, 8):
+            rows = parallel.shard_rows(n, world)
+            assert len(rows) == world and rows[0][0] == 0 and rows[-1][1] == n
+            assert all(b[1] == c[0] for b, c in zip(rows, rows[1:]))
+            assert all((a % 64 == 0 or a == n) and b >= a for a, b in rows)
+    assert parallel.slot_order([[0, 2], [1, 3]]) == [0, 1, 2, 3]
+    assert parallel.slot_order([[0, 3, 6], [1, 4, 7], [2, 5, 8]]) == list(range(9))
+    with pytest.raises(ValueError):
+        parallel.slot_order([[0, 1], [2]])
+
+
+def _truth_fwd(view, n):
+    """Per-Gaussian preprocess outputs of `view` with the exchange's dtypes and widths."""
+    i = torch.arange(n, dtype=torch.float64)
+    return [(view * 1000 + i[:, None] + torch.arange(12) / 100).float(),
+            ((view + torch.arange(n)) % 2).to(torch.uint8),
+            (view * 7 + torch.arange(n)).to(torch.int32),
+            (view * (1 << 40) + torch.arange(n)).to(torch.int64),
+            (-view * 1000 - i[:, None] - torch.arange(8) / 100).float()]
+
+
+def _gshard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, k = 777, 2
+        views_of = [[d + world * j for j in range(k)] for d in range(world)]
+        order = parallel.slot_order(views_of)
+        rows = parallel.shard_rows(n, world)
+        a, b = rows[rank]
+        truth = {v: _truth_fwd(v, n) for v in order}
+        # this rank's shard-local preprocess outputs of every view, slot order
+        sub = [torch.stack([truth[v][kind][a:b] for v in order]) for kind in range(5)]
+        full = [torch.zeros((k, n) + t.shape[1:], dtype=t.dtype) for t in truth[order[0]]]
+        parallel.gshard_forward_exchange(sub, full, rows, rank, dist.group.WORLD)
+        ok = all(torch.equal(full[kind][j], truth[views_of[rank][j]][kind]) for kind in range(5) for j in range(k))
+        # splat partials of the own views back to the shard owners
+        parts = {v: (v * 100 + torch.arange(n, dtype=torch.float64)[:, None] + torch.arange(9) * 1e-3).float()
+                 for v in order}
+        own = [parts[v].clone() for v in views_of[rank]]
+        recv = torch.zeros((len(order), max(b - a, 1), 9))
+        parallel.gshard_backward_exchange(own, recv, rows, rank, dist.group.WORLD)
+        ok = ok and all(torch.equal(recv[i, :b - a], parts[v][a:b]) for i, v in enumerate(order))
+        # no group (one rank's share simulated on one device): only this rank's rows move
+        full2 = [torch.zeros_like(f) for f in full]
+        parallel.gshard_forward_exchange(sub, full2, rows, rank, None)
+        ok = ok and all(torch.equal(full2[kind][j, a:b], truth[views_of[rank][j]][kind][a:b]) and
+                        not full2[kind][j, :a].any() and not full2[kind][j, b:].any()
+                        for kind in range(5) for j in range(k))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_gaussian_shard_exchanges(world):
+    """dp_mode="gaussians" exchanges over gloo (world 2 and 3, 777 rows: an uneven last
+    shard): every view owner receives its views' full per-Gaussian preprocess outputs in
+    cloud row order (all five dtypes), and every shard owner receives its rows of every
+    view's splat partials."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gshard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == list(range(world)) and all(r[1] for r in res), res
