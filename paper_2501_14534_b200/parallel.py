@@ -9,9 +9,14 @@ partitions the north star asks for, one process per GPU over NCCL:
   communication; it bins, sorts and blends only its band of tile rows, and one
   all-gather assembles the image rows.  The blend order of every pixel is the
   same as the single-GPU render, so the assembled image is bitwise identical.
-* training: CAMERA-VIEW DATA PARALLELISM.  Rank r renders views r, r+W, ...;
-  gradients accumulate locally into one flat buffer and ONE all-reduce(sum)
-  combines them (train.Trainer), followed by a replicated Adam step.
+* training: CAMERA-VIEW DATA PARALLELISM.  Rank r renders views r, r+W, ...
+  (train.Trainer).  dp_mode="gaussians" (bench.py's default) shards the Gaussians too
+  (the exchanges at the end of this module): each rank preprocesses its rows of the cloud
+  for every view, all-to-alls carry the outputs to the view owners and the splat
+  partials back, and each rank runs the preprocess backward and Adam on its rows.
+  ZeRO-1 (reduce-scatter, Adam on 1/W, all-gather; zero_plan; the Trainer's default,
+  which also serves its deterministic and one-stream paths) and one bucketed
+  all-reduce + replicated Adam (grad_buckets) are the other modes.
 
 The split / gather / shard logic below is pure host code over torch tensors
 and runs under gloo on the CPU (tests/test_parallel.py); the GPU entry points

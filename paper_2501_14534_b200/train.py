@@ -5,7 +5,8 @@ for a BATCH of views, which is how BASELINE.json config 3 defines the step:
 
     for each view of this rank:  render_forward -> L1 + D-SSIM loss -> render_backward
                                  (gradients accumulated into one flat buffer)
-    NCCL all-reduce(sum) of the flat gradient buffer       (data parallel, N > 1)
+    data parallel (N > 1): ZeRO-1 (default), Gaussian-sharded all-to-alls or one
+                                 all-reduce of the flat gradient buffer (dp_mode)
     mask-penalty gradients + Adam over the 8 parameter groups, one fused launch
                                  (masking.py:60-67, training.py:310-331)
 
