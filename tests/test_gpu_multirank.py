@@ -5,7 +5,8 @@ under test is the whole data-parallel step with real exchanges between ranks
 (parallel.py, train.Trainer): for dp_mode="gaussians" every rank's shard of the
 gradient, the loss terms, the parameters after Adam steps and the densification
 statistics equal the one-process step over all views; for ZeRO-1 the loss terms and
-every rank's (all-gathered) parameters do."""
+every rank's (all-gathered) parameters do.  The tile-row sharded renderer assembles
+frames bitwise equal to the one-GPU render."""
 
 import os
 import socket
@@ -172,3 +173,52 @@ def test_zero1_step_multirank_equals_one_process(world):
             np.testing.assert_allclose(res[r]["params"][lo:hi], ref["params"][lo:hi], rtol=1e-4, atol=_atol(f),
                                        err_msg=f"rank {r} parameters {f}")
         np.testing.assert_array_equal(res[r]["params"], res[0]["params"])  # replicated after the all-gathers
+
+
+def _render_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_14534_b200 import GaussianCloud, RenderSettings, parallel, scenes
+        sc = scenes.small_scene(seed=53, n=30_000, width=300, height=170)
+        rng = np.random.default_rng(53)
+        orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, 170, name=f"o{k}") for k in range(5)]
+        r = parallel.ShardedRenderer(GaussianCloud.from_fields(sc.fields), RenderSettings(near=0.2))
+        got = r.render(orbit[:3]) + r.render(orbit[3:]) if rank == 0 else (r.render(orbit[:3]), r.render(orbit[3:]))
+        q.put((rank, [g.cpu().numpy() for g in got] if rank == 0 else r.last_bands))
+    except BaseException as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tile_row_sharded_render_multirank_equals_one_gpu(world):
+    """parallel.ShardedRenderer with W = 2 and 3 ranks: each rank blends its band of tile
+    rows (the second batch's bands from the first batch's histogram) and rank 0 assembles
+    frames bitwise equal to the one-GPU render."""
+    import torch.multiprocessing as mp
+
+    from paper_2501_14534_b200 import GaussianCloud, RenderSettings, render_forward, scenes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_render_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    bad = {r: v for r, v in res.items() if isinstance(v, str)}
+    assert not bad, bad
+    sc = scenes.small_scene(seed=53, n=30_000, width=300, height=170)
+    rng = np.random.default_rng(53)
+    orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, 170, name=f"o{k}") for k in range(5)]
+    cloud = GaussianCloud.from_fields(sc.fields)
+    for cam, img in zip(orbit, res[0]):
+        np.testing.assert_array_equal(img, render_forward(cloud, cam, RenderSettings(near=0.2)).image.cpu().numpy())
+    bands = res[1]
+    assert len(bands) == world and bands[0][0] == 0 and bands[-1][1] == (170 + 15) // 16
