@@ -157,15 +157,20 @@ class ShardedRenderer:
             r0, r1 = rb * ts, min(re * ts, h)
             for f, o in enumerate(outs):
                 buf[f, : r1 - r0] = o.image[r0:r1]
-            # next batch's bands: the last frame's full-view row histogram (replicated preprocess)
             st = outs[-1]._state
-            with stage("row_histogram"):
-                hist = row_histogram(st.splats, st.tiles_touched, len(self.cloud), cams[-1], ts)
-            if self.hist is None or self.hist.numel() != rows:
-                self.hist = torch.empty(rows, dtype=torch.int64, pin_memory=True)
-            self.hist.copy_(hist, non_blocking=True)
-            self.hist_ready = torch.cuda.Event()
-            self.hist_ready.record()
+            splats, tiles = st.splats, st.tiles_touched
+        else:  # no rows for this rank (more ranks than tile rows): the histogram still needs
+            # the last frame's preprocess, so that every rank derives the same next bands
+            from .rasterizer import preprocess
+            splats, _, tiles, _, _, _ = preprocess(self.cloud, cams[-1], self.settings)
+        # next batch's bands: the last frame's full-view row histogram (replicated preprocess)
+        with stage("row_histogram"):
+            hist = row_histogram(splats, tiles, len(self.cloud), cams[-1], ts)
+        if self.hist is None or self.hist.numel() != rows:
+            self.hist = torch.empty(rows, dtype=torch.int64, pin_memory=True)
+        self.hist.copy_(hist, non_blocking=True)
+        self.hist_ready = torch.cuda.Event()
+        self.hist_ready.record()
         with stage("gather"):
             parts = [torch.empty_like(buf) for _ in range(self.world)] if self.rank == 0 else None
             dist.gather(buf, parts, dst=0, group=self.group)

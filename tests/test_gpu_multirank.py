@@ -175,16 +175,16 @@ def test_zero1_step_multirank_equals_one_process(world):
         np.testing.assert_array_equal(res[r]["params"], res[0]["params"])  # replicated after the all-gathers
 
 
-def _render_worker(rank, world, port, q):
+def _render_worker(rank, world, port, q, height=170):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2501_14534_b200 import GaussianCloud, RenderSettings, parallel, scenes
-        sc = scenes.small_scene(seed=53, n=30_000, width=300, height=170)
+        sc = scenes.small_scene(seed=53, n=30_000, width=300, height=height)
         rng = np.random.default_rng(53)
-        orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, 170, name=f"o{k}") for k in range(5)]
+        orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, height, name=f"o{k}") for k in range(5)]
         r = parallel.ShardedRenderer(GaussianCloud.from_fields(sc.fields), RenderSettings(near=0.2))
         got = r.render(orbit[:3]) + r.render(orbit[3:]) if rank == 0 else (r.render(orbit[:3]), r.render(orbit[3:]))
         q.put((rank, [g.cpu().numpy() for g in got] if rank == 0 else r.last_bands))
@@ -195,18 +195,19 @@ def _render_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_tile_row_sharded_render_multirank_equals_one_gpu(world):
+@pytest.mark.parametrize("world,height", [(2, 170), (3, 170), (3, 32)])
+def test_tile_row_sharded_render_multirank_equals_one_gpu(world, height):
     """parallel.ShardedRenderer with W = 2 and 3 ranks: each rank blends its band of tile
     rows (the second batch's bands from the first batch's histogram) and rank 0 assembles
-    frames bitwise equal to the one-GPU render."""
+    frames bitwise equal to the one-GPU render; with more ranks than tile rows (32 px: two
+    rows, three ranks) the idle rank still derives the same bands."""
     import torch.multiprocessing as mp
 
     from paper_2501_14534_b200 import GaussianCloud, RenderSettings, render_forward, scenes
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_render_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_render_worker, args=(r, world, port, q, height)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
@@ -214,11 +215,13 @@ def test_tile_row_sharded_render_multirank_equals_one_gpu(world):
         p.join(timeout=120)
     bad = {r: v for r, v in res.items() if isinstance(v, str)}
     assert not bad, bad
-    sc = scenes.small_scene(seed=53, n=30_000, width=300, height=170)
+    sc = scenes.small_scene(seed=53, n=30_000, width=300, height=height)
     rng = np.random.default_rng(53)
-    orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, 170, name=f"o{k}") for k in range(5)]
+    orbit = [scenes.pinhole(3.0 * scenes._unit(rng), 300, height, name=f"o{k}") for k in range(5)]
     cloud = GaussianCloud.from_fields(sc.fields)
     for cam, img in zip(orbit, res[0]):
         np.testing.assert_array_equal(img, render_forward(cloud, cam, RenderSettings(near=0.2)).image.cpu().numpy())
+    for r in range(1, world):
+        assert res[r] == res[1]  # every rank derived the same bands
     bands = res[1]
-    assert len(bands) == world and bands[0][0] == 0 and bands[-1][1] == (170 + 15) // 16
+    assert len(bands) == world and bands[0][0] == 0 and bands[-1][1] == (height + 15) // 16
