@@ -1074,6 +1074,11 @@ def test_gaussian_sharded_trainer_single_rank_nccl(tgs):
             tr.step()
             torch.cuda.synchronize()
             terms, grads = tr.terms.clone(), tr.grads.flat.clone()
+            # the same step with the targets streamed from pinned host memory (the e2e path)
+            host = {v: t.cpu().pin_memory() for v, t in enumerate(tg)}
+            tr.step(host_targets=host)
+            torch.cuda.synchronize()
+            assert torch.equal(tr.terms, terms), mode
             for f, lr in lrs.items():
                 tr.opt.set_lr(f, lr)
             tr.step()
