@@ -825,7 +825,7 @@ def schedule_c5(args):
         lrs = {**DEFAULT_LRS, "mask_logits": 0.02, "sh_mask_logits": 0.02}
         lam = dict(lambda_m=2e-3, lambda_sh=2e-3)
     trainer = Trainer(cloud, sc.cameras, {}, RenderSettings(**kw), LAMBDA_SSIM, lrs=lrs, process_group=pg,
-                      views=views, **lam)
+                      views=views, dp_mode=args.dp, **lam)
     prunes, counts, phase_res = [], [len(cloud)], {}
 
     def setup(i):
