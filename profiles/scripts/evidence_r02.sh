@@ -8,6 +8,9 @@ python bench.py --impl reference > gpurun_out/bench_ref_final.json 2>gpurun_out/
 python bench.py --config c4 > gpurun_out/c4_final.json 2>gpurun_out/c4_final.err
 python bench.py --config c5 > gpurun_out/c5_final.json 2>gpurun_out/c5_final.err
 for n in 2 4 8; do for dp in gaussians zero; do python bench.py --rank-share $n --dp $dp > gpurun_out/rank_share_${dp}_$n.json 2>gpurun_out/rank_share_${dp}_$n.err; done; done
+python profiles/rank_share_trace.py 8 gaussians > gpurun_out/r02_rank_share_trace_gaussians_8.txt 2>&1
+python profiles/rank_share_trace.py 8 zero > gpurun_out/r02_rank_share_trace_zero_8.txt 2>&1
+python profiles/step_host_latency.py gaussians > gpurun_out/r02_step_host_latency_gaussians.txt 2>&1
 python profiles/profile_step.py > gpurun_out/ps.log 2>&1 && ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"^(k_|tgs)" -f -o gpurun_out/view_final python profiles/profile_step.py > gpurun_out/ncu_view.log 2>&1
 python profiles/profile_train.py > gpurun_out/pt.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_preprocess_bwd|k_adam|k_exact|k_preprocess_fwd" -f -o gpurun_out/step_final python profiles/profile_train.py > gpurun_out/ncu_step.log 2>&1
 python profiles/ncu_summary.py --prefix r02 gpurun_out/view_final.ncu-rep gpurun_out/step_final.ncu-rep > gpurun_out/ncu_summary.log 2>&1
