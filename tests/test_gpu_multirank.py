@@ -28,13 +28,14 @@ def _port():
     return p
 
 
-def _setup():
+def _setup(rest=True):
     from paper_2501_14534_b200 import RenderSettings, scenes
     sc = scenes.small_scene(seed=47, n=20_000, width=160, height=112, dist=3.0)
     rng = np.random.default_rng(47)
     cams = [sc.cameras[0]] + [scenes.pinhole(3.0 * scenes._unit(rng), 144, 96, name=f"m{k}")
                               for k in range(VIEWS - 1)]
-    st = RenderSettings(near=0.2, mask_threshold=0.01, sh_mask_threshold=0.1)
+    st = RenderSettings(near=0.2, mask_threshold=0.01, sh_mask_threshold=0.1, compute_sh_rest_grads=rest,
+                        active_sh_degree=3 if rest else 2)
     tg = [torch.rand((c.height, c.width, 3), generator=torch.Generator().manual_seed(k)) for k, c in enumerate(cams)]
     return sc.fields, cams, st, tg
 
@@ -56,7 +57,7 @@ def _run(tr, lrs):
     return out
 
 
-def _worker(rank, world, port, q, dp="gaussians"):
+def _worker(rank, world, port, q, dp="gaussians", rest=True):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -65,7 +66,7 @@ def _worker(rank, world, port, q, dp="gaussians"):
         from paper_2501_14534_b200 import GaussianCloud
         from paper_2501_14534_b200.parallel import shard_rows
         from paper_2501_14534_b200.train import Trainer
-        fields, cams, st, tg = _setup()
+        fields, cams, st, tg = _setup(rest)
         views = list(range(rank, VIEWS, world))
         targets = [t.cuda() if v in views else None for v, t in enumerate(tg)]
         cloud = GaussianCloud.from_fields(fields)
@@ -104,8 +105,10 @@ def _field_rows(cloud, a, b):
     return out
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gaussian_sharded_step_multirank_equals_one_process(world):
+@pytest.mark.parametrize("world,rest", [(2, True), (3, True), (2, False)])
+def test_gaussian_sharded_step_multirank_equals_one_process(world, rest):
+    """(rest=False: an SH-cadence step at active degree 2 — sh_rest neither differentiated
+    nor updated)"""
     import torch.multiprocessing as mp
 
     from paper_2501_14534_b200 import GaussianCloud
@@ -113,7 +116,7 @@ def test_gaussian_sharded_step_multirank_equals_one_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, "gaussians", rest)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
@@ -122,7 +125,7 @@ def test_gaussian_sharded_step_multirank_equals_one_process(world):
     bad = {r: v for r, v in res.items() if isinstance(v, str)}
     assert not bad, bad
     # the one-process step over all views
-    fields, cams, st, tg = _setup()
+    fields, cams, st, tg = _setup(rest)
     cloud = GaussianCloud.from_fields(fields)
     tr = Trainer(cloud, cams, [t.cuda() for t in tg], st, densify_stats=True)
     ref = _run(tr, dict(tr.opt.lrs))
